@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""bench.py — BASELINE.json's headline metric on B200.
+
+Workload (BASELINE.json configs[1], "config 2"): 3D 7-point Laplacian 128^3
+(n = 2,097,152), ILU(0), SAIT tau = 5e-2, k = 3 for both factors; one STEP =
+the SAIT apply z = M_U (M_L r) on 100 seeded U[-1,1] vectors (seeds
+1000..1099), applied one after the other (one SpMV pair each).
+
+  value      algorithmic GB/s of the pair, inputs resident in HBM:
+             100 * B_pair / t_step,  B_pair = 12 (nnz_L + nnz_U) + 8 (n+1) + 32 n
+  e2e        the same metric through the public host-vector API
+             (sait_pair_apply_host: H2D r, the pair, D2H z per vector)
+  roofline   dominant kernel (the SpMV) achieved GB/s vs MEASURED_PEAKS.json
+  cpu_baseline  the reference (oracle/_ref, compiled from the reference's own
+             sources) timed on this host, all threads, bounded sample
+  build      SAIT build of both factors on device: built nnz/s
+
+`--impl reference` times the reference's own CPU path (SaitPairPreconditioner::
+apply from oracle/_ref) on the same workload and prints the same JSON line.
+Inputs larger than L2: the two factors stream 349 MB per pair (> 126 MB L2),
+so no explicit flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASE["metric"]
+GRID = 128
+TAU, STEPS_K = 5e-2, 3
+NVEC = 100
+SEED0 = 1000
+WORKLOAD = "c2: laplacian3d 128^3, ILU(0), SAIT_thr(tau=5e-2, k=3), apply pair x100 vectors"
+
+
+def b_pair(n, nnz_l, nnz_u):
+    return 12 * (nnz_l + nnz_u) + 8 * (n + 1) + 32 * n
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.out = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------- reference arm
+
+def ref_inputs(O, R):
+    A = O.laplacian_3d(GRID)
+    L, U = R.ilu_k(A, 0)
+    return A, L, U
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return  # rank 0 alone times the CPU reference
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsaitref.so not built"}))
+        return
+    import ctypes as C
+
+    R = O.get("reference")
+    A, L, U = ref_inputs(O, R)
+    ML = R.sait_thr(L, True, TAU, STEPS_K)
+    MU = R.sait_thr(U, False, TAU, STEPS_K)
+    n = A.nrows
+    B = b_pair(n, ML.nnz, MU.nnz)
+    lib = R.lib
+    lib.ref_pair_create.restype = C.c_void_p
+    lib.ref_pair_create.argtypes = [C.c_void_p, C.c_void_p]
+    lib.ref_pair_time_apply.restype = C.c_double
+    lib.ref_pair_time_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]
+    from oracle.oracle import _in
+
+    p = lib.ref_pair_create(C.byref(_in(ML)), C.byref(_in(MU)))
+    sample = int(os.environ.get("SAIT_REF_SAMPLE", "20"))  # vectors per step (bounded sample)
+    r = np.stack([O.uniform_pm1(SEED0 + i, n) for i in range(sample)])
+    z = np.empty_like(r)
+    for _ in range(args.warmup):
+        lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, sample)
+    ts = [lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, sample) for _ in range(args.steps)]
+    t = float(np.sum(ts))
+    value = sample * args.steps * B / t / 1e9
+    cores = int(lib.ref_max_threads())
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps * NVEC / sample,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": n, "nnz_L": ML.nnz, "nnz_U": MU.nnz, "bytes_per_pair": B},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample} vectors per step through SaitPairPreconditioner::apply (OpenMP {cores} threads)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    lib.ref_pair_destroy.argtypes = [C.c_void_p]
+    lib.ref_pair_destroy(p)
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------- B200 arm
+
+def cpu_baseline_sample(ML_host, MU_host, n):
+    """The reference's apply on the GPU-built factors (bitwise identical to the
+    reference's own), timed on this host's cores.  Returns dict or None."""
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return None
+    import ctypes as C
+
+    from oracle.oracle import Csr, _in
+
+    R = O.get("reference")
+    lib = R.lib
+    lib.ref_pair_create.restype = C.c_void_p
+    lib.ref_pair_create.argtypes = [C.c_void_p, C.c_void_p]
+    lib.ref_pair_time_apply.restype = C.c_double
+    lib.ref_pair_time_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]
+    ml = Csr(ML_host.nrows, ML_host.ncols, ML_host.row_ptr, ML_host.col_idx, ML_host.values)
+    mu = Csr(MU_host.nrows, MU_host.ncols, MU_host.row_ptr, MU_host.col_idx, MU_host.values)
+    p = lib.ref_pair_create(C.byref(_in(ml)), C.byref(_in(mu)))
+    sample = int(os.environ.get("SAIT_CPU_SAMPLE", "20"))
+    r = np.stack([O.uniform_pm1(SEED0 + i, n) for i in range(sample)])
+    z = np.empty_like(r)
+    lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, 2)  # warm
+    t = lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, sample)
+    lib.ref_pair_destroy.argtypes = [C.c_void_p]
+    lib.ref_pair_destroy(p)
+    B = b_pair(n, ml.nnz, mu.nnz)
+    return {"value": sample * B / t / 1e9, "unit": "GB/s", "cores": int(lib.ref_max_threads()), "kind": "reference",
+            "sample": f"{sample} of the 100 vectors through the reference SaitPairPreconditioner::apply "
+                      f"(OpenMP, {int(lib.ref_max_threads())} threads), {t:.2f} s"}
+
+
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2106_12836_b200 as S
+
+    # ---- inputs (host, then device): not timed
+    A = S.laplacian_3d(GRID)
+    n = A.nrows
+    f = S.ilu_k(A, 0)
+    Ld = S.DeviceCsr.upload(f.lower)
+    Ud = S.DeviceCsr.upload(f.upper)
+    torch.cuda.synchronize()
+    # ---- build (device): both factors, timed by the library with CUDA events
+    st = []
+    ML = S.sait_thr(Ld, S.lower_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
+    MU = S.sait_thr(Ud, S.upper_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
+    # second build (warm allocator) is the reported one
+    st = []
+    ML.free(), MU.free()
+    ML = S.sait_thr(Ld, S.lower_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
+    MU = S.sait_thr(Ud, S.upper_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
+    nnz_l, nnz_u = ML.nnz(), MU.nnz()
+    build = {
+        "built_nnz": nnz_l + nnz_u,
+        "seconds": st[0].seconds + st[1].seconds,
+        "nnz_per_s": (nnz_l + nnz_u) / (st[0].seconds + st[1].seconds),
+        "steps_run": [st[0].steps_run, st[1].steps_run],
+        "products": st[0].products + st[1].products,
+    }
+    ML_host = ML.to_host() if rank == 0 else None
+    MU_host = MU.to_host() if rank == 0 else None
+    pair = S.SaitPairPreconditioner(ML, MU)
+    B = b_pair(n, nnz_l, nnz_u)
+
+    # ---- 100 seeded vectors resident in HBM
+    R = torch.empty((NVEC, n), dtype=torch.float64, device="cuda")
+    for i in range(NVEC):
+        R[i].copy_(torch.from_numpy(S.uniform_pm1(SEED0 + i, n)))
+    Z = torch.empty_like(R)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for i in range(NVEC):
+            pair.apply(R[i], Z[i])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = S.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = S.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = NVEC * B / (ms_step * 1e-3) / 1e9 * (ws if False else 1)
+
+    # ---- dominant kernel: the SpMV, timed per launch on the launching stream
+    Lh, Uh = pair._factor(0), pair._factor(1)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    reps = 50
+    kt = {}
+    for nm, mat, src, dst in (("L", Lh, R[0], y), ("U", Uh, y, Z[0])):
+        S.spmv(mat, src, dst)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(reps):
+            S.spmv(mat, src, dst)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        kt[nm] = a0.elapsed_time(a1) / reps
+    bytes_l = 12 * nnz_l + 4 * (n + 1) + 16 * n
+    bytes_u = 12 * nnz_u + 4 * (n + 1) + 16 * n
+    peak, peak_kind = peaks()
+    achieved = (bytes_l + bytes_u) / ((kt["L"] + kt["U"]) * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get("spmv_traffic_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "spmv_rowblock",
+                "per_launch_ms": {"M_L": kt["L"], "M_U": kt["U"]},
+                "algorithmic_bytes_per_launch": {"M_L": bytes_l, "M_U": bytes_u},
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)"}
+
+    # ---- e2e: public host-vector API, H2D + pair + D2H per vector, pinned host memory
+    Rh = torch.empty((NVEC, n), dtype=torch.float64).pin_memory()
+    Rh.copy_(R.cpu())
+    Zh = torch.empty((NVEC, n), dtype=torch.float64).pin_memory()
+    Rn, Zn = Rh.numpy(), Zh.numpy()
+    z1 = Zn[0]
+    pair.apply(Rn[0], z1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(NVEC):
+        pair.apply(Rn[i], Zn[i])
+    t_e2e = time.perf_counter() - t0
+    e2e = {"value": NVEC * B / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": NVEC * 8 * n,
+           "d2h_bytes_per_step": NVEC * 8 * n, "ms_per_step": t_e2e * 1e3}
+    ok = bool(torch.equal(Zh, Z.cpu()))
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(ML_host, MU_host, n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "nnz_L": nnz_l, "nnz_U": nnz_u, "bytes_per_pair": B,
+                       "vectors_per_step": NVEC, "parallelism": f"rows{ws}" if ws > 1 else "single",
+                       "l2": "inputs larger than L2: 349 MB of factors streamed per pair (> 126 MB L2), no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "build": build, "e2e_matches_device": ok,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

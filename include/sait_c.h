@@ -1,0 +1,192 @@
+/*
+ * sait_c.h — C ABI of the B200 SAIT library (libsait_b200.so).
+ *
+ * This is the drop-in boundary for the reference's SAIT hot path: every entry
+ * point below names the reference interface it replaces (paths relative to
+ * /root/reference/proj/core/).  Plain C types only: int64 sizes, raw host or
+ * device pointers, opaque handles.  A `sait_stream_t` is a cudaStream_t
+ * (NULL = the legacy default stream); device-pointer entry points enqueue on
+ * it and return without synchronising unless stated.
+ *
+ * Status: every function returning int returns SAIT_OK (0) or an error code;
+ * the message is in sait_last_error() (thread-local).  The error kinds map to
+ * the reference's exceptions:
+ *   SAIT_ERR_INVALID_ARGUMENT  <->  std::invalid_argument
+ *   SAIT_ERR_RUNTIME           <->  std::runtime_error
+ * and the messages carry the same text as the reference's (e.g.
+ * "jacobi_split: singular matrix, zero diagonal at row 7").
+ *
+ * Device storage: CSR with int32 row_ptr / col_idx and fp64 values
+ * (nnz < 2^31 is checked at upload / build time).
+ */
+#ifndef SAIT_C_H
+#define SAIT_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAIT_ABI_VERSION 1
+
+enum sait_status {
+  SAIT_OK = 0,
+  SAIT_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  SAIT_ERR_RUNTIME = 2,          /* std::runtime_error */
+  SAIT_ERR_CUDA = 3,             /* CUDA runtime failure (no reference counterpart) */
+  SAIT_ERR_NOMEM = 4
+};
+
+typedef struct sait_dcsr_s *sait_dcsr_t; /* device CSR matrix */
+typedef struct sait_pair_s *sait_pair_t; /* SAIT pair preconditioner on one device */
+typedef void *sait_stream_t;             /* cudaStream_t */
+
+/* Host CSR in the reference layout (csr.hpp:24-43: int64 indices, fp64
+ * values).  When the library fills one, free it with sait_host_csr_free. */
+typedef struct {
+  int64_t nrows;
+  int64_t ncols;
+  int64_t *row_ptr; /* nrows + 1 */
+  int64_t *col_idx; /* nnz */
+  double *values;   /* nnz; NULL for a sparsity pattern (csr.hpp:46-60) */
+} sait_host_csr;
+
+const char *sait_last_error(void);
+int sait_abi_version(void);
+void sait_host_csr_free(sait_host_csr *m);
+
+/* ---------------------------------------------------------- device CSR ---
+ * Replaces the host-side storage of saitprec::CsrMatrix (csr.hpp:24-43). */
+
+/* Copies a host CSR (int64 indices) to the current device. */
+int sait_csr_upload(const sait_host_csr *m, sait_stream_t stream, sait_dcsr_t *out);
+/* Shape and stored-entry count. */
+int sait_csr_info(sait_dcsr_t m, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+/* Copies back into caller arrays sized from sait_csr_info (values may be NULL). Synchronous. */
+int sait_csr_download(sait_dcsr_t m, int64_t *row_ptr, int64_t *col_idx, double *values,
+                      sait_stream_t stream);
+/* Copies back into a library-allocated host CSR. Synchronous. */
+int sait_csr_to_host(sait_dcsr_t m, sait_stream_t stream, sait_host_csr *out);
+/* Raw device arrays (int32 row_ptr/col_idx, fp64 values; values NULL for a pattern). */
+int sait_csr_device_arrays(sait_dcsr_t m, const int32_t **row_ptr, const int32_t **col_idx,
+                           const double **values);
+void sait_csr_free(sait_dcsr_t m);
+
+/* ------------------------------------------------------------- kernels ---
+ * kernels.hpp:12-40 on device matrices.  Results are new device matrices with
+ * the reference's exact patterns and (bitwise) values. */
+
+/* kernels.hpp:14 / kernels.cpp:10-26: y = A x, device vectors; row-sequential
+ * accumulation in stored order (bitwise equal to the reference).  xlen/ylen are
+ * checked like the reference's span sizes. */
+int sait_spmv(sait_dcsr_t a, const double *d_x, int64_t xlen, double *d_y, int64_t ylen,
+              sait_stream_t stream);
+/* kernels.hpp:21 / kernels.cpp:34-102: C = A B (Gustavson, ascending-k accumulation). */
+int sait_spgemm(sait_dcsr_t a, sait_dcsr_t b, sait_stream_t stream, sait_dcsr_t *out);
+/* kernels.hpp:25 / kernels.cpp:104-134 */
+int sait_add_identity(sait_dcsr_t m, sait_stream_t stream, sait_dcsr_t *out);
+/* kernels.hpp:30 / kernels.cpp:136-160 */
+int sait_drop_by_threshold(sait_dcsr_t m, double tau, sait_stream_t stream, sait_dcsr_t *out);
+/* kernels.hpp:33 / kernels.cpp:162-194 (pattern: a device CSR whose values are ignored) */
+int sait_drop_by_pattern(sait_dcsr_t m, sait_dcsr_t pattern, sait_stream_t stream,
+                         sait_dcsr_t *out);
+/* kernels.hpp:40 / kernels.cpp:236-246: M * diag(d), d a device vector of length ncols. */
+int sait_scale_columns(sait_dcsr_t m, const double *d_d, int64_t dlen, sait_stream_t stream,
+                       sait_dcsr_t *out);
+/* csr.hpp:84 / csr.cpp:72-92 */
+int sait_transpose(sait_dcsr_t m, sait_stream_t stream, sait_dcsr_t *out);
+
+/* ---------------------------------------------------------------- SAIT ---
+ * sait.hpp:14-74.  `lower` selects TriangularKind::Side (1 = Lower). */
+
+enum sait_drop_kind {
+  SAIT_DROP_THRESHOLD = 1,     /* sait_thr  (sait.cpp:90-101) */
+  SAIT_DROP_PATTERN = 2,       /* sait_pat  (sait.cpp:113-136) */
+  SAIT_DROP_THRESHOLD_CAP = 3, /* BASELINE config 4 fill cap */
+  SAIT_DROP_NONE = 4           /* sait_polynomial(split, steps, {}) then M D^-1 */
+};
+
+/* SaitThrParams{threshold, steps} / SaitPatParams{pattern_steps, refine_steps}
+ * (sait.hpp:14-27) plus the fill-cap factor. */
+typedef struct {
+  int kind;            /* sait_drop_kind */
+  double tau;          /* THRESHOLD, THRESHOLD_CAP: in [0, 1) */
+  int steps;           /* THRESHOLD, THRESHOLD_CAP, NONE: >= 1 */
+  int pattern_steps;   /* PATTERN: >= 0 */
+  int refine_steps;    /* PATTERN: >= 1 */
+  double cap_factor;   /* THRESHOLD_CAP: >= 1; column j keeps <= floor(f * nnz(T[:,j])) entries */
+} sait_drop_spec;
+
+typedef struct {
+  int steps_run;       /* recursion steps executed (early stop included) */
+  int stabilized;      /* 1 if the 1e-15 early stop fired (sait.cpp:14-28) */
+  int64_t nnz_out;     /* stored entries of the result */
+  int64_t products;    /* multiply-adds executed by the SpGEMM steps (one pass) */
+  double seconds;      /* device time of the whole build (CUDA events) */
+} sait_build_stats;
+
+/* sait.hpp:40 / sait.cpp:32-73: d_inv_diag (device, length n) receives 1/T[i,i];
+ * *tt receives I - D^-1 T with no stored diagonal. */
+int sait_jacobi_split(sait_dcsr_t t, int lower, double *d_inv_diag, sait_stream_t stream,
+                      sait_dcsr_t *tt);
+/* sait_thr / sait_pat / fill-capped sait_thr in one entry (sait.cpp:75-136):
+ * returns the approximate inverse M = poly(tT) D^-1 of the triangular T. */
+int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec *spec, sait_stream_t stream,
+               sait_dcsr_t *m_out, sait_build_stats *stats);
+/* sait.hpp:64 / sait.cpp:103-111 (result: a pattern, values NULL). */
+int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_stream_t stream,
+                             sait_dcsr_t *pattern_out);
+
+/* ------------------------------------------------ pair preconditioner ---
+ * SaitPairPreconditioner (preconditioner.hpp:54-68, preconditioner.cpp:34-49). */
+
+/* Takes ownership of ml and mu when take_ownership != 0 (the reference ctor
+ * moves its matrices in); otherwise they must outlive the pair.  Shape check
+ * of preconditioner.cpp:37-39. */
+int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pair_t *out);
+/* name() == "sait" and nnz() (preconditioner.hpp:62-63) */
+int sait_pair_info(sait_pair_t p, int64_t *n, int64_t *nnz);
+/* apply(r, z): z = M_U (M_L r), device vectors (preconditioner.cpp:42-45).
+ * Enqueued on `stream`; safe to call concurrently from several threads/streams. */
+int sait_pair_apply(sait_pair_t p, const double *d_r, int64_t rlen, double *d_z, int64_t zlen,
+                    sait_stream_t stream);
+/* Same with HOST vectors (any host memory; pinned is faster).  The copies are
+ * pipelined with the two SpMVs.  Synchronous on return. */
+int sait_pair_apply_host(sait_pair_t p, const double *h_r, int64_t rlen, double *h_z,
+                         int64_t zlen, sait_stream_t stream);
+/* apply_block (preconditioner.cpp:47-49): nvec vectors.  layout 0 = column-major
+ * n x nvec (DenseMatrix, dense.hpp:12-38), 1 = row-major n x nvec. Device pointers. */
+int sait_pair_apply_block(sait_pair_t p, const double *d_r, double *d_z, int64_t n,
+                          int64_t nvec, int layout, sait_stream_t stream);
+int sait_pair_apply_block_host(sait_pair_t p, const double *h_r, double *h_z, int64_t n,
+                               int64_t nvec, int layout, sait_stream_t stream);
+/* Borrowed handles of the two factors (owned by the pair). */
+int sait_pair_factors(sait_pair_t p, sait_dcsr_t *ml, sait_dcsr_t *mu);
+void sait_pair_destroy(sait_pair_t p);
+
+/* ----------------------------------------------------- inputs (host) ---
+ * Producers of the path's inputs.  ilu_k is ilu.hpp:27 / ilu.cpp:98-173
+ * (bitwise identical factors); the generators fix BASELINE.json's synthetic
+ * problems. */
+int sait_ilu_k(const sait_host_csr *a, int level, sait_host_csr *lower, sait_host_csr *upper);
+int sait_problem_laplacian_2d(int64_t nx, sait_host_csr *out);
+int sait_problem_laplacian_3d(int64_t n, sait_host_csr *out);
+int sait_problem_convdiff_2d(int64_t nx, double bx, double by, sait_host_csr *out);
+int sait_problem_synthetic_lower(int64_t n, int64_t draws, double p, uint64_t seed,
+                                 sait_host_csr *out);
+void sait_fill_uniform_pm1(uint64_t seed, int64_t n, double *out);
+
+/* ------------------------------------------------------------ utility --- */
+int sait_device_synchronize(void);
+/* Pinned host buffers for the host-vector entry points. */
+int sait_host_alloc(size_t bytes, void **ptr);
+void sait_host_free(void *ptr);
+/* Counts kernels launched by this library on this process (all threads). */
+int64_t sait_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAIT_C_H */

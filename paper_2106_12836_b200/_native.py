@@ -1,0 +1,155 @@
+"""ctypes binding of the C ABI (include/sait_c.h) exported by libsait_b200.so.
+
+The shared library is built in-tree (``make`` / ``__graft_entry__.build()``).
+There is no fallback: if the library is missing this module raises at import.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsait_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA library first (make, or __graft_entry__.build()); "
+        "there is no CPU fallback"
+    )
+
+lib = C.CDLL(LIB_PATH)
+
+SAIT_OK = 0
+SAIT_ERR_INVALID_ARGUMENT = 1
+SAIT_ERR_RUNTIME = 2
+SAIT_ERR_CUDA = 3
+SAIT_ERR_NOMEM = 4
+
+SAIT_DROP_THRESHOLD = 1
+SAIT_DROP_PATTERN = 2
+SAIT_DROP_THRESHOLD_CAP = 3
+SAIT_DROP_NONE = 4
+
+P64 = C.POINTER(C.c_int64)
+PD = C.POINTER(C.c_double)
+VP = C.c_void_p
+
+
+class HostCsr(C.Structure):
+    _fields_ = [
+        ("nrows", C.c_int64),
+        ("ncols", C.c_int64),
+        ("row_ptr", P64),
+        ("col_idx", P64),
+        ("values", PD),
+    ]
+
+
+class DropSpec(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int),
+        ("tau", C.c_double),
+        ("steps", C.c_int),
+        ("pattern_steps", C.c_int),
+        ("refine_steps", C.c_int),
+        ("cap_factor", C.c_double),
+    ]
+
+
+class BuildStats(C.Structure):
+    _fields_ = [
+        ("steps_run", C.c_int),
+        ("stabilized", C.c_int),
+        ("nnz_out", C.c_int64),
+        ("products", C.c_int64),
+        ("seconds", C.c_double),
+    ]
+
+
+# Every symbol include/sait_c.h declares, with its prototype.
+PROTOTYPES = {
+    "sait_last_error": (C.c_char_p, []),
+    "sait_abi_version": (C.c_int, []),
+    "sait_host_csr_free": (None, [C.POINTER(HostCsr)]),
+    "sait_csr_upload": (C.c_int, [C.POINTER(HostCsr), VP, C.POINTER(VP)]),
+    "sait_csr_info": (C.c_int, [VP, P64, P64, P64]),
+    "sait_csr_download": (C.c_int, [VP, P64, P64, PD, VP]),
+    "sait_csr_to_host": (C.c_int, [VP, VP, C.POINTER(HostCsr)]),
+    "sait_csr_device_arrays": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
+    "sait_csr_free": (None, [VP]),
+    "sait_spmv": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
+    "sait_spgemm": (C.c_int, [VP, VP, VP, C.POINTER(VP)]),
+    "sait_add_identity": (C.c_int, [VP, VP, C.POINTER(VP)]),
+    "sait_drop_by_threshold": (C.c_int, [VP, C.c_double, VP, C.POINTER(VP)]),
+    "sait_drop_by_pattern": (C.c_int, [VP, VP, VP, C.POINTER(VP)]),
+    "sait_scale_columns": (C.c_int, [VP, VP, C.c_int64, VP, C.POINTER(VP)]),
+    "sait_transpose": (C.c_int, [VP, VP, C.POINTER(VP)]),
+    "sait_jacobi_split": (C.c_int, [VP, C.c_int, VP, VP, C.POINTER(VP)]),
+    "sait_build": (C.c_int, [VP, C.c_int, C.POINTER(DropSpec), VP, C.POINTER(VP), C.POINTER(BuildStats)]),
+    "sait_pat_capture_pattern": (C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
+    "sait_pair_create": (C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
+    "sait_pair_info": (C.c_int, [VP, P64, P64]),
+    "sait_pair_apply": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
+    "sait_pair_apply_host": (C.c_int, [VP, PD, C.c_int64, PD, C.c_int64, VP]),
+    "sait_pair_apply_block": (C.c_int, [VP, VP, VP, C.c_int64, C.c_int64, C.c_int, VP]),
+    "sait_pair_apply_block_host": (C.c_int, [VP, PD, PD, C.c_int64, C.c_int64, C.c_int, VP]),
+    "sait_pair_factors": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP)]),
+    "sait_pair_destroy": (None, [VP]),
+    "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),
+    "sait_problem_laplacian_2d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),
+    "sait_problem_laplacian_3d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),
+    "sait_problem_convdiff_2d": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.POINTER(HostCsr)]),
+    "sait_problem_synthetic_lower": (C.c_int, [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.POINTER(HostCsr)]),
+    "sait_fill_uniform_pm1": (None, [C.c_uint64, C.c_int64, PD]),
+    "sait_device_synchronize": (C.c_int, []),
+    "sait_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(VP)]),
+    "sait_host_free": (None, [VP]),
+    "sait_kernel_launch_count": (C.c_int64, []),
+}
+
+for _name, (_res, _args) in PROTOTYPES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class SaitError(Exception):
+    code = -1
+
+
+class SaitInvalidArgument(SaitError, ValueError):
+    """std::invalid_argument in the reference."""
+
+    code = SAIT_ERR_INVALID_ARGUMENT
+
+
+class SaitRuntimeError(SaitError, RuntimeError):
+    """std::runtime_error in the reference."""
+
+    code = SAIT_ERR_RUNTIME
+
+
+class SaitCudaError(SaitError, RuntimeError):
+    code = SAIT_ERR_CUDA
+
+
+class SaitOutOfMemory(SaitError, MemoryError):
+    code = SAIT_ERR_NOMEM
+
+
+_EXC = {
+    SAIT_ERR_INVALID_ARGUMENT: SaitInvalidArgument,
+    SAIT_ERR_RUNTIME: SaitRuntimeError,
+    SAIT_ERR_CUDA: SaitCudaError,
+    SAIT_ERR_NOMEM: SaitOutOfMemory,
+}
+
+
+def check(rc: int) -> None:
+    if rc != SAIT_OK:
+        msg = lib.sait_last_error().decode()
+        raise _EXC.get(rc, SaitError)(msg)
+
+
+def launch_count() -> int:
+    return int(lib.sait_kernel_launch_count())

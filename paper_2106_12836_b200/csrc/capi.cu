@@ -1,0 +1,740 @@
+// capi.cu — the C ABI of include/sait_c.h over the device kernels.
+// Each entry point cites the reference interface it replaces (paths relative
+// to /root/reference/proj/core/).
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct sait_dcsr_s {
+  int dev = 0;
+  sait::DevCsr m;
+};
+
+struct sait_pair_s {
+  int dev = 0;
+  sait_dcsr_s* ml = nullptr;
+  sait_dcsr_s* mu = nullptr;
+  bool owns = false;
+};
+
+namespace sait {
+int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
+void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s);
+void validate_device_csr(const DevCsr& m, cudaStream_t s);
+void narrow_indices(const int64_t* in, int32_t* out, int64_t n, cudaStream_t s);
+void widen_indices(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);
+void column_caps(const DevCsr& t, double factor, int32_t* cap, cudaStream_t s);
+void pair_apply_host_pipelined(const DevCsr& ml, const DevCsr& mu, const double* h_r, double* h_z,
+                               cudaStream_t s);
+}  // namespace sait
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SAIT_OK;
+  } catch (const sait::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return SAIT_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SAIT_ERR_RUNTIME;
+  }
+}
+
+void init_device_pool() {
+  static std::once_flag once[64];
+  int dev = 0;
+  SAIT_CUDA(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    SAIT_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) SAIT_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+sait_dcsr_s* wrap(const sait::DevCsr& m) {
+  auto* h = new sait_dcsr_s;
+  SAIT_CUDA(cudaGetDevice(&h->dev));
+  h->m = m;
+  return h;
+}
+
+void need(const void* p, const char* what) {
+  if (!p) sait::throw_invalid(std::string(what) + ": null handle or pointer");
+}
+
+std::string fmt_double(double v) {  // std::to_string(double) == "%f"
+  char b[64];
+  std::snprintf(b, sizeof b, "%f", v);
+  return b;
+}
+
+void host_csr_alloc(sait_host_csr* out, int64_t nrows, int64_t ncols, int64_t nnz, bool values) {
+  out->nrows = nrows;
+  out->ncols = ncols;
+  out->row_ptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (nrows + 1)));
+  out->col_idx = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (nnz ? nnz : 1)));
+  out->values = values ? static_cast<double*>(std::malloc(sizeof(double) * (nnz ? nnz : 1))) : nullptr;
+  if (!out->row_ptr || !out->col_idx || (values && !out->values)) throw std::bad_alloc();
+}
+
+sait::DevCsr upload(const sait_host_csr* m, cudaStream_t s) {
+  need(m, "sait_csr_upload");
+  if (m->nrows < 0 || m->ncols < 0) sait::throw_invalid("validate: negative dimension");
+  need(m->row_ptr, "sait_csr_upload(row_ptr)");
+  if (m->row_ptr[0] != 0) sait::throw_invalid("validate: bad row_ptr head");
+  const int64_t nnz = m->row_ptr[m->nrows];
+  if (nnz < 0) sait::throw_invalid("validate: bad row_ptr tail");
+  if (nnz > INT32_MAX || m->nrows >= INT32_MAX || m->ncols >= INT32_MAX)
+    sait::throw_invalid("sait_csr_upload: " + std::to_string(nnz) +
+                        " entries / dimensions exceed the int32 device index range");
+  if (nnz && !m->col_idx) sait::throw_invalid("sait_csr_upload: null col_idx");
+  sait::DevCsr d;
+  d.nrows = m->nrows;
+  d.ncols = m->ncols;
+  d.nnz = nnz;
+  d.rp = sait::dalloc<int32_t>(d.nrows + 1, s);
+  d.ci = sait::dalloc<int32_t>(nnz, s);
+  d.v = m->values ? sait::dalloc<double>(nnz, s) : nullptr;
+  int64_t* tmp = sait::dalloc<int64_t>(std::max(d.nrows + 1, nnz), s);
+  SAIT_CUDA(cudaMemcpyAsync(tmp, m->row_ptr, sizeof(int64_t) * (d.nrows + 1), cudaMemcpyHostToDevice, s));
+  sait::narrow_indices(tmp, d.rp, d.nrows + 1, s);
+  if (nnz) {
+    SAIT_CUDA(cudaMemcpyAsync(tmp, m->col_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+    sait::narrow_indices(tmp, d.ci, nnz, s);
+    if (m->values) SAIT_CUDA(cudaMemcpyAsync(d.v, m->values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+  }
+  sait::dfree(tmp, s);
+  try {
+    sait::validate_device_csr(d, s);
+  } catch (...) {
+    sait::free_csr(d, s);
+    throw;
+  }
+  return d;
+}
+
+void to_host(const sait::DevCsr& m, cudaStream_t s, int64_t* rp, int64_t* ci, double* v) {
+  int64_t* tmp = sait::dalloc<int64_t>(std::max(m.nrows + 1, m.nnz), s);
+  sait::widen_indices(m.rp, tmp, m.nrows + 1, s);
+  SAIT_CUDA(cudaMemcpyAsync(rp, tmp, sizeof(int64_t) * (m.nrows + 1), cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  if (m.nnz) {
+    sait::widen_indices(m.ci, tmp, m.nnz, s);
+    SAIT_CUDA(cudaMemcpyAsync(ci, tmp, sizeof(int64_t) * m.nnz, cudaMemcpyDeviceToHost, s));
+    if (v && m.v) SAIT_CUDA(cudaMemcpyAsync(v, m.v, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, s));
+  }
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  sait::dfree(tmp, s);
+}
+
+// Identity of order n used as the right factor for the elementwise kernels.
+sait::Epilogue no_epilogue() { return sait::Epilogue{}; }
+
+struct BuildOut {
+  sait::DevCsr mt;  // final unit-diagonal iterate, column form (M^T)
+  int steps_run = 0;
+  bool stabilized = false;
+  int64_t products = 0;
+};
+
+// The recursion of sait.cpp:75-136 in column form: row j of M_s^T is
+//   drop( sum_{k in M_{s-1}^T[j,:]} M_{s-1}^T[j,k] * tT^T[k,:] + e_j ),
+// bitwise equal to the reference's row form (same products, same
+// ascending-k order, commutative products).
+BuildOut run_recursion(const sait::DevCsr& ttT, const sait_drop_spec& spec, const int32_t* cap, cudaStream_t s) {
+  BuildOut out;
+  sait::DevCsr a = sait::make_identity(ttT.nrows, s);
+  sait::DevCsr pattern;  // pattern_steps iterate (PATTERN)
+  int steps = spec.steps;
+  sait::Epilogue epi;
+  epi.add_identity = true;
+  if (spec.kind == SAIT_DROP_PATTERN) {
+    sait::Epilogue e0;
+    e0.add_identity = true;
+    for (int k = 0; k < spec.pattern_steps; ++k) {  // sait.cpp:122-125, no early stop
+      sait::SpgemmResult r = sait::spgemm_fused(a, ttT, e0, s);
+      out.products += r.products;
+      sait::free_csr(a, s);
+      a = r.c;
+      ++out.steps_run;
+    }
+    pattern = sait::copy_csr(a, s);
+    epi.drop = 2;
+    epi.prp = pattern.rp;
+    epi.pci = pattern.ci;
+    steps = spec.refine_steps;
+  } else if (spec.kind == SAIT_DROP_THRESHOLD) {
+    epi.drop = 1;
+    epi.tau = spec.tau;
+  } else if (spec.kind == SAIT_DROP_THRESHOLD_CAP) {
+    epi.drop = 3;
+    epi.tau = spec.tau;
+    epi.cap = cap;
+  }
+  for (int k = 0; k < steps; ++k) {  // sait.cpp:80-86 / :128-134
+    epi.qrp = a.rp;
+    epi.qci = a.ci;
+    epi.qv = a.v;
+    sait::SpgemmResult r = sait::spgemm_fused(a, ttT, epi, s);
+    out.products += r.products;
+    sait::free_csr(a, s);
+    a = r.c;
+    ++out.steps_run;
+    if (!r.changed) {
+      out.stabilized = true;
+      break;
+    }
+  }
+  if (pattern.rp) sait::free_csr(pattern, s);
+  out.mt = a;
+  return out;
+}
+
+void check_spec(const sait_drop_spec* spec) {
+  need(spec, "sait_build(spec)");
+  switch (spec->kind) {
+    case SAIT_DROP_THRESHOLD:
+      if (!(spec->tau >= 0.0 && spec->tau < 1.0))
+        sait::throw_invalid("sait_thr: threshold must be in [0, 1), got " + fmt_double(spec->tau));
+      break;
+    case SAIT_DROP_THRESHOLD_CAP:
+      if (!(spec->tau >= 0.0 && spec->tau < 1.0))
+        sait::throw_invalid("sait_thr: threshold must be in [0, 1), got " + fmt_double(spec->tau));
+      if (!(spec->cap_factor >= 1.0))
+        sait::throw_invalid("sait_thr_cap: cap factor must be >= 1, got " + fmt_double(spec->cap_factor));
+      break;
+    case SAIT_DROP_PATTERN:
+      if (spec->pattern_steps < 0) sait::throw_invalid("sait_pat: pattern_steps must be >= 0");
+      if (spec->refine_steps < 1) sait::throw_invalid("sait_pat: refine_steps must be >= 1");
+      break;
+    case SAIT_DROP_NONE:
+      break;
+    default:
+      sait::throw_invalid("sait_build: unknown drop kind " + std::to_string(spec->kind));
+  }
+}
+
+}  // namespace
+
+namespace sait {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace sait
+
+extern "C" {
+
+const char* sait_last_error(void) { return g_err.c_str(); }
+int sait_abi_version(void) { return SAIT_ABI_VERSION; }
+
+void sait_host_csr_free(sait_host_csr* m) {
+  if (!m) return;
+  std::free(m->row_ptr);
+  std::free(m->col_idx);
+  std::free(m->values);
+  m->row_ptr = m->col_idx = nullptr;
+  m->values = nullptr;
+}
+
+int64_t sait_kernel_launch_count(void) { return sait::g_launches.load(); }
+
+int sait_device_synchronize(void) {
+  return guarded([] { SAIT_CUDA(cudaDeviceSynchronize()); });
+}
+
+int sait_host_alloc(size_t bytes, void** ptr) {
+  return guarded([&] { SAIT_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1)); });
+}
+void sait_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
+// ---------------------------------------------------------------- device CSR
+
+int sait_csr_upload(const sait_host_csr* m, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(out, "sait_csr_upload(out)");
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr d = upload(m, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(d);
+  });
+}
+
+int sait_csr_info(sait_dcsr_t m, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+  return guarded([&] {
+    need(m, "sait_csr_info");
+    if (nrows) *nrows = m->m.nrows;
+    if (ncols) *ncols = m->m.ncols;
+    if (nnz) *nnz = m->m.nnz;
+  });
+}
+
+int sait_csr_download(sait_dcsr_t m, int64_t* row_ptr, int64_t* col_idx, double* values, sait_stream_t stream) {
+  return guarded([&] {
+    need(m, "sait_csr_download");
+    DeviceGuard g(m->dev);
+    to_host(m->m, sait::as_stream(stream), row_ptr, col_idx, values);
+  });
+}
+
+int sait_csr_to_host(sait_dcsr_t m, sait_stream_t stream, sait_host_csr* out) {
+  return guarded([&] {
+    need(m, "sait_csr_to_host");
+    need(out, "sait_csr_to_host(out)");
+    DeviceGuard g(m->dev);
+    host_csr_alloc(out, m->m.nrows, m->m.ncols, m->m.nnz, m->m.v != nullptr);
+    to_host(m->m, sait::as_stream(stream), out->row_ptr, out->col_idx, out->values);
+  });
+}
+
+int sait_csr_device_arrays(sait_dcsr_t m, const int32_t** row_ptr, const int32_t** col_idx, const double** values) {
+  return guarded([&] {
+    need(m, "sait_csr_device_arrays");
+    if (row_ptr) *row_ptr = m->m.rp;
+    if (col_idx) *col_idx = m->m.ci;
+    if (values) *values = m->m.v;
+  });
+}
+
+void sait_csr_free(sait_dcsr_t m) {
+  if (!m) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(m->dev);
+  cudaFree(m->m.rp);
+  cudaFree(m->m.ci);
+  if (m->m.v) cudaFree(m->m.v);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete m;
+}
+
+// ------------------------------------------------------------------- kernels
+
+int sait_spmv(sait_dcsr_t a, const double* d_x, int64_t xlen, double* d_y, int64_t ylen, sait_stream_t stream) {
+  return guarded([&] {
+    need(a, "spmv");
+    if (xlen != a->m.ncols)
+      sait::throw_invalid("spmv: vector length " + std::to_string(xlen) + " does not match ncols " +
+                          std::to_string(a->m.ncols));
+    if (ylen != a->m.nrows) sait::throw_invalid("spmv: output length mismatch");
+    DeviceGuard g(a->dev);
+    sait::spmv(a->m, d_x, d_y, sait::as_stream(stream));
+  });
+}
+
+int sait_spgemm(sait_dcsr_t a, sait_dcsr_t b, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(a, "spgemm");
+    need(b, "spgemm");
+    need(out, "spgemm(out)");
+    DeviceGuard g(a->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::SpgemmResult r = sait::spgemm_fused(a->m, b->m, no_epilogue(), s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(r.c);
+  });
+}
+
+namespace {
+// elementwise row filters run as the fused SpGEMM M * I (m * 1.0 == m exactly)
+sait::DevCsr through_identity(const sait::DevCsr& m, const sait::Epilogue& epi, cudaStream_t s) {
+  sait::DevCsr eye = sait::make_identity(m.ncols, s);
+  sait::SpgemmResult r = sait::spgemm_fused(m, eye, epi, s);
+  sait::free_csr(eye, s);
+  return r.c;
+}
+}  // namespace
+
+int sait_add_identity(sait_dcsr_t m, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(m, "add_identity");
+    need(out, "add_identity(out)");
+    if (m->m.nrows != m->m.ncols) sait::throw_invalid("add_identity: matrix is not square");
+    DeviceGuard g(m->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::Epilogue e;
+    e.add_identity = true;
+    sait::DevCsr r = through_identity(m->m, e, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(r);
+  });
+}
+
+int sait_drop_by_threshold(sait_dcsr_t m, double tau, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(m, "drop_by_threshold");
+    need(out, "drop_by_threshold(out)");
+    if (!(tau >= 0.0 && tau < 1.0))
+      sait::throw_invalid("drop_by_threshold: tau must be in [0, 1), got " + fmt_double(tau));
+    DeviceGuard g(m->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr r;
+    if (tau == 0.0) {
+      r = sait::copy_csr(m->m, s);
+    } else {
+      sait::Epilogue e;
+      e.drop = 1;
+      e.tau = tau;
+      r = through_identity(m->m, e, s);
+    }
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(r);
+  });
+}
+
+int sait_drop_by_pattern(sait_dcsr_t m, sait_dcsr_t pattern, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(m, "drop_by_pattern");
+    need(pattern, "drop_by_pattern");
+    need(out, "drop_by_pattern(out)");
+    if (m->m.nrows != pattern->m.nrows || m->m.ncols != pattern->m.ncols)
+      sait::throw_invalid("drop_by_pattern: shape mismatch");
+    DeviceGuard g(m->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::Epilogue e;
+    e.drop = 2;
+    e.prp = pattern->m.rp;
+    e.pci = pattern->m.ci;
+    sait::DevCsr r = through_identity(m->m, e, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(r);
+  });
+}
+
+int sait_scale_columns(sait_dcsr_t m, const double* d_d, int64_t dlen, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(m, "scale_columns");
+    need(out, "scale_columns(out)");
+    if (dlen != m->m.ncols) sait::throw_invalid("scale_columns: scale vector length mismatch");
+    DeviceGuard g(m->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr r = sait::copy_csr(m->m, s);
+    sait::scale_columns(m->m, d_d, r, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(r);
+  });
+}
+
+int sait_transpose(sait_dcsr_t m, sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(m, "transpose");
+    need(out, "transpose(out)");
+    DeviceGuard g(m->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr r = sait::transpose(m->m, nullptr, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *out = wrap(r);
+  });
+}
+
+// ---------------------------------------------------------------------- SAIT
+
+int sait_jacobi_split(sait_dcsr_t t, int lower, double* d_inv_diag, sait_stream_t stream, sait_dcsr_t* tt) {
+  return guarded([&] {
+    need(t, "jacobi_split");
+    need(tt, "jacobi_split(out)");
+    DeviceGuard g(t->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr r = sait::jacobi_split(t->m, lower != 0, d_inv_diag, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *tt = wrap(r);
+  });
+}
+
+int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec* spec, sait_stream_t stream, sait_dcsr_t* m_out,
+               sait_build_stats* stats) {
+  return guarded([&] {
+    need(t, "sait_build");
+    need(m_out, "sait_build(out)");
+    check_spec(spec);
+    DeviceGuard g(t->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    const int64_t n = t->m.nrows;
+    cudaEvent_t e0, e1;
+    SAIT_CUDA(cudaEventCreate(&e0));
+    SAIT_CUDA(cudaEventCreate(&e1));
+    SAIT_CUDA(cudaEventRecord(e0, s));
+    double* inv = sait::dalloc<double>(n, s);
+    sait::DevCsr tt;
+    try {
+      tt = sait::jacobi_split(t->m, lower != 0, inv, s);
+    } catch (...) {
+      sait::dfree(inv, s);
+      throw;
+    }
+    if (spec->kind != SAIT_DROP_PATTERN && spec->steps < 1) {
+      sait::free_csr(tt, s);
+      sait::dfree(inv, s);
+      sait::throw_invalid("sait_polynomial: steps must be >= 1");
+    }
+    sait::DevCsr ttT = sait::transpose(tt, nullptr, s);
+    sait::free_csr(tt, s);
+    int32_t* cap = nullptr;
+    if (spec->kind == SAIT_DROP_THRESHOLD_CAP) {
+      cap = sait::dalloc<int32_t>(n, s);
+      sait::column_caps(t->m, spec->cap_factor, cap, s);
+    }
+    BuildOut bo = run_recursion(ttT, *spec, cap, s);
+    sait::free_csr(ttT, s);
+    sait::dfree(cap, s);
+    // M = (M^T)^T D^-1: column j of M scaled by inv_diag[j] (kernels.cpp:236-246)
+    sait::DevCsr m = sait::transpose(bo.mt, inv, s);
+    sait::free_csr(bo.mt, s);
+    sait::dfree(inv, s);
+    SAIT_CUDA(cudaEventRecord(e1, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    SAIT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (stats) {
+      stats->steps_run = bo.steps_run;
+      stats->stabilized = bo.stabilized ? 1 : 0;
+      stats->nnz_out = m.nnz;
+      stats->products = bo.products;
+      stats->seconds = ms * 1e-3;
+    }
+    *m_out = wrap(m);
+  });
+}
+
+int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_stream_t stream,
+                             sait_dcsr_t* pattern_out) {
+  return guarded([&] {
+    need(t, "sait_pat_capture_pattern");
+    need(pattern_out, "sait_pat_capture_pattern(out)");
+    if (pattern_steps < 0) sait::throw_invalid("sait_pat_capture_pattern: pattern_steps must be >= 0");
+    DeviceGuard g(t->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    const int64_t n = t->m.nrows;
+    double* inv = sait::dalloc<double>(n, s);
+    sait::DevCsr tt;
+    try {
+      tt = sait::jacobi_split(t->m, lower != 0, inv, s);
+    } catch (...) {
+      sait::dfree(inv, s);
+      throw;
+    }
+    sait::dfree(inv, s);
+    sait::DevCsr pat;
+    if (pattern_steps == 0) {
+      pat = sait::make_identity(n, s);
+      sait::free_csr(tt, s);
+    } else {
+      sait::DevCsr ttT = sait::transpose(tt, nullptr, s);
+      sait::free_csr(tt, s);
+      sait_drop_spec sp{SAIT_DROP_NONE, 0.0, pattern_steps, 0, 0, 0.0};
+      BuildOut bo = run_recursion(ttT, sp, nullptr, s);  // sait_polynomial(split, p, {})
+      sait::free_csr(ttT, s);
+      pat = sait::transpose(bo.mt, nullptr, s);
+      sait::free_csr(bo.mt, s);
+    }
+    sait::dfree(pat.v, s);
+    pat.v = nullptr;
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *pattern_out = wrap(pat);
+  });
+}
+
+// -------------------------------------------------------- pair preconditioner
+
+int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pair_t* out) {
+  return guarded([&] {
+    need(ml, "SaitPairPreconditioner");
+    need(mu, "SaitPairPreconditioner");
+    need(out, "SaitPairPreconditioner(out)");
+    if (ml->m.nrows != mu->m.ncols) sait::throw_invalid("SaitPairPreconditioner: factor shapes do not chain");
+    if (ml->dev != mu->dev) sait::throw_invalid("SaitPairPreconditioner: factors live on different devices");
+    if (!ml->m.v || !mu->m.v) sait::throw_invalid("SaitPairPreconditioner: factors have no values");
+    auto* p = new sait_pair_s;
+    p->dev = ml->dev;
+    p->ml = ml;
+    p->mu = mu;
+    p->owns = take_ownership != 0;
+    *out = p;
+  });
+}
+
+int sait_pair_info(sait_pair_t p, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    need(p, "sait_pair_info");
+    if (n) *n = p->ml->m.ncols;
+    if (nnz) *nnz = p->ml->m.nnz + p->mu->m.nnz;
+  });
+}
+
+int sait_pair_factors(sait_pair_t p, sait_dcsr_t* ml, sait_dcsr_t* mu) {
+  return guarded([&] {
+    need(p, "sait_pair_factors");
+    if (ml) *ml = p->ml;
+    if (mu) *mu = p->mu;
+  });
+}
+
+int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z, int64_t zlen, sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "apply");
+    const sait::DevCsr& L = p->ml->m;
+    const sait::DevCsr& U = p->mu->m;
+    if (rlen != L.ncols)
+      sait::throw_invalid("spmv: vector length " + std::to_string(rlen) + " does not match ncols " +
+                          std::to_string(L.ncols));
+    if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
+    DeviceGuard g(p->dev);
+    cudaStream_t s = sait::as_stream(stream);
+    double* y = sait::dalloc<double>(L.nrows, s);  // reference: fresh y per call
+    sait::spmv(L, d_r, y, s);
+    sait::spmv(U, y, d_z, s);
+    sait::dfree(y, s);
+  });
+}
+
+int sait_pair_apply_host(sait_pair_t p, const double* h_r, int64_t rlen, double* h_z, int64_t zlen,
+                         sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "apply");
+    const sait::DevCsr& L = p->ml->m;
+    const sait::DevCsr& U = p->mu->m;
+    if (rlen != L.ncols)
+      sait::throw_invalid("spmv: vector length " + std::to_string(rlen) + " does not match ncols " +
+                          std::to_string(L.ncols));
+    if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
+    DeviceGuard g(p->dev);
+    sait::pair_apply_host_pipelined(L, U, h_r, h_z, sait::as_stream(stream));
+  });
+}
+
+namespace {
+// Column-major slab of w (1, 2, 4 or 8) vectors: transpose to row-major, run
+// the block SpMM pair (matrix read once per slab), transpose back.
+void apply_slab(const sait::DevCsr& L, const sait::DevCsr& U, const double* r_cm, double* z_cm, int64_t n, int w,
+                double* rt, double* y, double* zt, cudaStream_t s) {
+  if (w == 1) {
+    sait::spmv(L, r_cm, y, s);
+    sait::spmv(U, y, z_cm, s);
+    return;
+  }
+  sait::transpose_block(r_cm, rt, n, w, true, s);
+  sait::spmm_rowmajor(L, rt, y, w, s);
+  sait::spmm_rowmajor(U, y, zt, w, s);
+  sait::transpose_block(zt, z_cm, n, w, false, s);
+}
+
+void apply_block_device(sait_pair_t p, const double* d_r, double* d_z, int64_t n, int64_t nvec, int layout,
+                        cudaStream_t s) {
+  const sait::DevCsr& L = p->ml->m;
+  const sait::DevCsr& U = p->mu->m;
+  if (n != L.ncols || n != U.nrows) sait::throw_invalid("spmm: dimension mismatch");
+  if (layout != 0 && layout != 1) sait::throw_invalid("apply_block: layout must be 0 or 1");
+  if (nvec <= 0 || n == 0) return;
+  if (layout == 1 && (nvec == 1 || nvec == 2 || nvec == 4 || nvec == 8)) {
+    double* y = sait::dalloc<double>(L.nrows * nvec, s);
+    sait::spmm_rowmajor(L, d_r, y, static_cast<int>(nvec), s);
+    sait::spmm_rowmajor(U, y, d_z, static_cast<int>(nvec), s);
+    sait::dfree(y, s);
+    return;
+  }
+  const double* rcm = d_r;
+  double* zcm = d_z;
+  double* tmp_r = nullptr;
+  double* tmp_z = nullptr;
+  if (layout == 1) {  // row-major in: work column-major, convert at the ends
+    tmp_r = sait::dalloc<double>(n * nvec, s);
+    tmp_z = sait::dalloc<double>(n * nvec, s);
+    sait::transpose_block(d_r, tmp_r, n, static_cast<int>(nvec), false, s);
+    rcm = tmp_r;
+    zcm = tmp_z;
+  }
+  double* y = sait::dalloc<double>(L.nrows * 8, s);
+  double* rt = sait::dalloc<double>(n * 8, s);
+  double* zt = sait::dalloc<double>(n * 8, s);
+  for (int64_t c0 = 0; c0 < nvec;) {
+    int64_t left = nvec - c0;
+    int w = left >= 8 ? 8 : (left >= 4 ? 4 : (left >= 2 ? 2 : 1));
+    apply_slab(L, U, rcm + c0 * n, zcm + c0 * n, n, w, rt, y, zt, s);
+    c0 += w;
+  }
+  sait::dfree(y, s);
+  sait::dfree(rt, s);
+  sait::dfree(zt, s);
+  if (layout == 1) {
+    sait::transpose_block(tmp_z, d_z, n, static_cast<int>(nvec), true, s);
+    sait::dfree(tmp_r, s);
+    sait::dfree(tmp_z, s);
+  }
+}
+}  // namespace
+
+int sait_pair_apply_block(sait_pair_t p, const double* d_r, double* d_z, int64_t n, int64_t nvec, int layout,
+                          sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "apply_block");
+    DeviceGuard g(p->dev);
+    apply_block_device(p, d_r, d_z, n, nvec, layout, sait::as_stream(stream));
+  });
+}
+
+int sait_pair_apply_block_host(sait_pair_t p, const double* h_r, double* h_z, int64_t n, int64_t nvec, int layout,
+                               sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "apply_block");
+    DeviceGuard g(p->dev);
+    cudaStream_t s = sait::as_stream(stream);
+    double* r = sait::dalloc<double>(n * nvec, s);
+    double* z = sait::dalloc<double>(n * nvec, s);
+    SAIT_CUDA(cudaMemcpyAsync(r, h_r, sizeof(double) * n * nvec, cudaMemcpyHostToDevice, s));
+    apply_block_device(p, r, z, n, nvec, layout, s);
+    SAIT_CUDA(cudaMemcpyAsync(h_z, z, sizeof(double) * n * nvec, cudaMemcpyDeviceToHost, s));
+    sait::dfree(r, s);
+    sait::dfree(z, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void sait_pair_destroy(sait_pair_t p) {
+  if (!p) return;
+  if (p->owns) {
+    sait_csr_free(p->ml);
+    sait_csr_free(p->mu);
+  }
+  delete p;
+}
+
+}  // extern "C"

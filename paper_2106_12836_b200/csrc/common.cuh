@@ -1,0 +1,136 @@
+// common.cuh — shared device-side types and helpers of libsait_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "sait_c.h"
+
+namespace sait {
+
+constexpr int kWarp = 32;
+
+// Error carrying a sait_status; the C ABI turns it into a status + message.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void throw_invalid(const std::string& m) { throw Error(SAIT_ERR_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void throw_runtime(const std::string& m) { throw Error(SAIT_ERR_RUNTIME, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw Error(SAIT_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e) + " in " + what + " at " +
+                                   file + ":" + std::to_string(line));
+}
+#define SAIT_CUDA(x) ::sait::cuda_check((x), #x, __FILE__, __LINE__)
+
+extern std::atomic<int64_t> g_launches;
+// Every kernel launch goes through this: counts it and checks the launch error.
+#define SAIT_LAUNCHED()                                                   \
+  do {                                                                    \
+    ::sait::g_launches.fetch_add(1, std::memory_order_relaxed);          \
+    ::sait::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+  } while (0)
+
+inline cudaStream_t as_stream(sait_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Device CSR: int32 indices, fp64 values (values may be null for a pattern).
+struct DevCsr {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  int32_t* rp = nullptr;
+  int32_t* ci = nullptr;
+  double* v = nullptr;
+};
+
+// Stream-ordered allocation from the device pool.
+template <class T>
+T* dalloc(size_t count, cudaStream_t s) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), s);
+  if (e == cudaErrorMemoryAllocation) throw Error(SAIT_ERR_NOMEM, "out of device memory");
+  SAIT_CUDA(e);
+  return static_cast<T*>(p);
+}
+inline void dfree(void* p, cudaStream_t s) {
+  if (p) SAIT_CUDA(cudaFreeAsync(p, s));
+}
+inline void free_csr(DevCsr& m, cudaStream_t s) {
+  dfree(m.rp, s);
+  dfree(m.ci, s);
+  dfree(m.v, s);
+  m.rp = m.ci = nullptr;
+  m.v = nullptr;
+}
+
+inline int num_sms() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return sms;
+}
+
+inline unsigned grid_for(int64_t work, int per_block, int64_t cap = 1 << 30) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+// ---------------------------------------------------------------- kernels API
+// (implemented in the .cu files; all enqueue on `s`)
+
+// csr_ops.cu
+// exclusive scan of per-row counts into row_ptr[0..n]; returns the total
+// (synchronises; throws if it exceeds the int32 index range)
+int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
+void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s);
+void exclusive_scan_rows(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
+int64_t read_last(const int32_t* row_ptr, int64_t n, cudaStream_t s);  // syncs
+DevCsr make_identity(int64_t n, cudaStream_t s);
+DevCsr transpose(const DevCsr& a, const double* row_scale, cudaStream_t s);
+void scale_columns(const DevCsr& a, const double* d, DevCsr& out, cudaStream_t s);
+DevCsr copy_csr(const DevCsr& a, cudaStream_t s);
+
+// split.cu
+// Validates triangularity / diagonal with the reference's precedence, then
+// fills inv_diag and tT (no stored diagonal).  Throws like jacobi_split.
+DevCsr jacobi_split(const DevCsr& t, bool lower, double* inv_diag, cudaStream_t s);
+
+// spgemm.cu
+struct Epilogue {
+  bool add_identity = false;   // insert 1.0 / add 1.0 at col == row
+  int drop = 0;                // 0 none, 1 threshold, 2 pattern, 3 threshold+cap
+  double tau = 0.0;
+  const int32_t* prp = nullptr;  // pattern row_ptr (drop == 2)
+  const int32_t* pci = nullptr;
+  const int32_t* cap = nullptr;  // per-row max entries incl. diagonal (drop == 3)
+  // stabilization check against a previous iterate with identical shape
+  const int32_t* qrp = nullptr;
+  const int32_t* qci = nullptr;
+  const double* qv = nullptr;
+};
+struct SpgemmResult {
+  DevCsr c;
+  bool changed = true;   // vs the comparison iterate (true if no comparison)
+  int64_t products = 0;
+};
+SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi, cudaStream_t s);
+
+// spmv.cu
+void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
+void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaStream_t s);
+void transpose_block(const double* in, double* out, int64_t n, int nvec, bool to_rowmajor,
+                     cudaStream_t s);
+
+}  // namespace sait

@@ -1,0 +1,332 @@
+// csr_ops.cu — device CSR plumbing: row-pointer scan, identity, transpose
+// (csr.cpp:72-92), column scaling (kernels.cpp:236-246), copies.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "sort.cuh"
+
+namespace sait {
+
+std::atomic<int64_t> g_launches{0};
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* total) {
+  __shared__ int64_t warp_sums[kScanThreads / 32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t w = lane < kScanThreads / 32 ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kScanThreads / 32) warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int64_t before = (wid > 0 ? warp_sums[wid - 1] : 0) + x - v;
+  if (total) *total = warp_sums[kScanThreads / 32 - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void scan_tile_sums(const int32_t* __restrict__ counts, int64_t n, int64_t* __restrict__ sums) {
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < n) s += counts[base + k];
+  int64_t tot;
+  block_exclusive_scan(s, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// Single block: exclusive scan of the tile sums in place; writes the grand total.
+__global__ void scan_sums(int64_t* sums, int64_t ntiles, int64_t* total) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < ntiles; base += kScanThreads) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < ntiles ? sums[i] : 0;
+    int64_t tot;
+    int64_t ex = block_exclusive_scan(v, &tot);
+    if (i < ntiles) sums[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void scan_tiles(const int32_t* __restrict__ counts, int64_t n, const int64_t* __restrict__ sums,
+                           int32_t* __restrict__ row_ptr, const int64_t* __restrict__ total) {
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
+  int32_t c[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    c[k] = base + k < n ? counts[base + k] : 0;
+    s += c[k];
+  }
+  int64_t run = sums[blockIdx.x] + block_exclusive_scan(s, nullptr);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) row_ptr[base + k] = static_cast<int32_t>(run);
+    run += c[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n] = static_cast<int32_t>(*total);
+}
+
+__global__ void identity_kernel(int64_t n, int32_t* rp, int32_t* ci, double* v) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    rp[i] = static_cast<int32_t>(i);
+    ci[i] = static_cast<int32_t>(i);
+    v[i] = 1.0;
+  }
+  if (i == 0) rp[n] = static_cast<int32_t>(n);
+}
+
+__global__ void count_cols(int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           int32_t* __restrict__ cnt) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  for (int32_t e = rp[i]; e < rp[i + 1]; ++e) atomicAdd(&cnt[ci[e]], 1);
+}
+
+// Scatter entry (i, j, v) of A to row j of A^T at an atomically claimed slot;
+// rows of the result are sorted afterwards.  Scaled value = v * scale[i]
+// (scale_columns order, kernels.cpp:243).
+__global__ void scatter_transpose(int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ v, const double* __restrict__ scale,
+                                  int32_t* __restrict__ cursor, int32_t* __restrict__ oci, double* __restrict__ ov) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  double s = scale ? scale[i] : 1.0;
+  for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+    int32_t pos = atomicAdd(&cursor[ci[e]], 1);
+    oci[pos] = static_cast<int32_t>(i);
+    if (v) ov[pos] = scale ? __dmul_rn(v[e], s) : v[e];
+  }
+}
+
+// Rows of <= 32 entries: one warp per row, rank by counting smaller keys.
+__global__ void sort_rows_warp(int64_t nrows, const int32_t* __restrict__ rp, int32_t* __restrict__ ci,
+                               double* __restrict__ v, int32_t* __restrict__ long_rows, int32_t* __restrict__ nlong) {
+  int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  int32_t b = rp[row], len = rp[row + 1] - b;
+  if (len > 32) {
+    if (lane == 0) long_rows[atomicAdd(nlong, 1)] = static_cast<int32_t>(row);
+    return;
+  }
+  if (len <= 1) return;
+  int32_t key = lane < len ? ci[b + lane] : kKeyPad;
+  double val = (lane < len && v) ? v[b + lane] : 0.0;
+  int rank = 0;
+  for (int o = 0; o < len; ++o) {
+    int32_t other = __shfl_sync(0xffffffffu, key, o);
+    rank += other < key;
+  }
+  __syncwarp();
+  if (lane < len) {
+    ci[b + rank] = key;
+    if (v) v[b + rank] = val;
+  }
+}
+
+constexpr int kSortBlock = 256;
+constexpr int kSortSmem = 2048;  // entries sorted in shared memory per block
+
+__global__ void sort_rows_block(const int32_t* __restrict__ rows, int32_t nrows_list, const int32_t* __restrict__ rp,
+                                int32_t* __restrict__ ci, double* __restrict__ v, int32_t* __restrict__ huge_rows,
+                                int32_t* __restrict__ nhuge) {
+  __shared__ int32_t sk[kSortSmem];
+  __shared__ double sv[kSortSmem];
+  for (int32_t r = blockIdx.x; r < nrows_list; r += gridDim.x) {
+    int32_t row = rows[r];
+    int32_t b = rp[row], len = rp[row + 1] - b;
+    if (len > kSortSmem) {
+      if (threadIdx.x == 0) huge_rows[atomicAdd(nhuge, 1)] = row;
+      continue;
+    }
+    int n2 = next_pow2(len);
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+      sk[i] = i < len ? ci[b + i] : kKeyPad;
+      sv[i] = (i < len && v) ? v[b + i] : 0.0;
+    }
+    __syncthreads();
+    bitonic_sort(sk, sv, n2, threadIdx.x, blockDim.x, BlockSync{});
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      ci[b + i] = sk[i];
+      if (v) v[b + i] = sv[i];
+    }
+    __syncthreads();
+  }
+}
+
+// One very long row at a time, sorted in a padded global scratch.
+__global__ void sort_row_global(int32_t row, const int32_t* __restrict__ rp, int32_t* __restrict__ ci,
+                                double* __restrict__ v, int32_t* __restrict__ sk, double* __restrict__ sv) {
+  int32_t b = rp[row], len = rp[row + 1] - b;
+  int n2 = next_pow2(len);
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    sk[i] = i < len ? ci[b + i] : kKeyPad;
+    sv[i] = (i < len && v) ? v[b + i] : 0.0;
+  }
+  __syncthreads();
+  bitonic_sort(sk, sv, n2, threadIdx.x, blockDim.x, BlockSync{});
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    ci[b + i] = sk[i];
+    if (v) v[b + i] = sv[i];
+  }
+}
+
+__global__ void scale_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                  const double* __restrict__ d, double* __restrict__ out) {
+  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < nnz) out[e] = __dmul_rn(v[e], d[ci[e]]);
+}
+
+}  // namespace
+
+int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s) {
+  int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (ntiles < 1) ntiles = 1;
+  int64_t* sums = dalloc<int64_t>(ntiles + 1, s);
+  int64_t* total = sums + ntiles;
+  scan_tile_sums<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(counts, n, sums);
+  SAIT_LAUNCHED();
+  scan_sums<<<1, kScanThreads, 0, s>>>(sums, ntiles, total);
+  SAIT_LAUNCHED();
+  scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(counts, n, sums, row_ptr, total);
+  SAIT_LAUNCHED();
+  int64_t h = 0;
+  SAIT_CUDA(cudaMemcpyAsync(&h, total, sizeof h, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(sums, s);
+  if (h > INT32_MAX)
+    throw Error(SAIT_ERR_NOMEM, "result has " + std::to_string(h) +
+                                    " stored entries; the device CSR uses int32 indices (max 2^31-1)");
+  return h;
+}
+
+void exclusive_scan_rows(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s) {
+  scan_counts(counts, row_ptr, n, s);
+}
+
+int64_t read_last(const int32_t* row_ptr, int64_t n, cudaStream_t s) {
+  int32_t h = 0;
+  SAIT_CUDA(cudaMemcpyAsync(&h, row_ptr + n, sizeof h, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+DevCsr make_identity(int64_t n, cudaStream_t s) {
+  DevCsr m;
+  m.nrows = m.ncols = m.nnz = n;
+  m.rp = dalloc<int32_t>(n + 1, s);
+  m.ci = dalloc<int32_t>(n, s);
+  m.v = dalloc<double>(n, s);
+  identity_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(n, m.rp, m.ci, m.v);
+  SAIT_LAUNCHED();
+  return m;
+}
+
+// Sort every row of (rp, ci, v) by column index.
+void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s) {
+  if (nrows == 0) return;
+  int32_t* lists = dalloc<int32_t>(2 * nrows + 2, s);
+  int32_t* long_rows = lists;
+  int32_t* huge_rows = lists + nrows;
+  int32_t* counters = lists + 2 * nrows;  // [nlong, nhuge]
+  SAIT_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
+  sort_rows_warp<<<grid_for(nrows * 32, 256), 256, 0, s>>>(nrows, rp, ci, v, long_rows, counters);
+  SAIT_LAUNCHED();
+  int32_t hc[2];
+  SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  if (hc[0] > 0) {
+    unsigned g = static_cast<unsigned>(std::min<int64_t>(hc[0], 4 * num_sms()));
+    sort_rows_block<<<g, kSortBlock, 0, s>>>(long_rows, hc[0], rp, ci, v, huge_rows, counters + 1);
+    SAIT_LAUNCHED();
+    SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    if (hc[1] > 0) {
+      std::vector<int32_t> huge(hc[1]);
+      SAIT_CUDA(cudaMemcpyAsync(huge.data(), huge_rows, hc[1] * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      std::vector<int32_t> hrp(nrows + 1);
+      SAIT_CUDA(cudaMemcpyAsync(hrp.data(), rp, (nrows + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SAIT_CUDA(cudaStreamSynchronize(s));
+      int maxlen = 0;
+      for (int32_t r : huge) maxlen = std::max(maxlen, hrp[r + 1] - hrp[r]);
+      int n2 = next_pow2(maxlen);
+      int32_t* sk = dalloc<int32_t>(n2, s);
+      double* sv = dalloc<double>(n2, s);
+      for (int32_t r : huge) {
+        sort_row_global<<<1, 1024, 0, s>>>(r, rp, ci, v, sk, sv);
+        SAIT_LAUNCHED();
+      }
+      dfree(sk, s);
+      dfree(sv, s);
+    }
+  }
+  dfree(lists, s);
+}
+
+DevCsr transpose(const DevCsr& a, const double* row_scale, cudaStream_t s) {
+  DevCsr t;
+  t.nrows = a.ncols;
+  t.ncols = a.nrows;
+  t.nnz = a.nnz;
+  t.rp = dalloc<int32_t>(t.nrows + 1, s);
+  t.ci = dalloc<int32_t>(t.nnz, s);
+  t.v = a.v ? dalloc<double>(t.nnz, s) : nullptr;
+  int32_t* cnt = dalloc<int32_t>(t.nrows + 1, s);
+  SAIT_CUDA(cudaMemsetAsync(cnt, 0, (t.nrows + 1) * sizeof(int32_t), s));
+  if (a.nrows > 0) {
+    count_cols<<<grid_for(a.nrows, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, cnt);
+    SAIT_LAUNCHED();
+  }
+  scan_counts(cnt, t.rp, t.nrows, s);
+  SAIT_CUDA(cudaMemcpyAsync(cnt, t.rp, t.nrows * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  if (a.nrows > 0) {
+    scatter_transpose<<<grid_for(a.nrows, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, row_scale, cnt, t.ci, t.v);
+    SAIT_LAUNCHED();
+  }
+  dfree(cnt, s);
+  sort_rows(t.nrows, t.rp, t.ci, t.v, s);
+  return t;
+}
+
+void scale_columns(const DevCsr& a, const double* d, DevCsr& out, cudaStream_t s) {
+  if (a.nnz == 0) return;
+  scale_cols_kernel<<<grid_for(a.nnz, 256), 256, 0, s>>>(a.nnz, a.ci, a.v, d, out.v);
+  SAIT_LAUNCHED();
+}
+
+DevCsr copy_csr(const DevCsr& a, cudaStream_t s) {
+  DevCsr c = a;
+  c.rp = dalloc<int32_t>(a.nrows + 1, s);
+  c.ci = dalloc<int32_t>(a.nnz, s);
+  c.v = a.v ? dalloc<double>(a.nnz, s) : nullptr;
+  SAIT_CUDA(cudaMemcpyAsync(c.rp, a.rp, (a.nrows + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  if (a.nnz) {
+    SAIT_CUDA(cudaMemcpyAsync(c.ci, a.ci, a.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (a.v) SAIT_CUDA(cudaMemcpyAsync(c.v, a.v, a.nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  return c;
+}
+
+}  // namespace sait

@@ -1,0 +1,518 @@
+// spgemm.cu — K2/K3: row-wise Gustavson SpGEMM C = A B with a fused epilogue
+// (+I, threshold / pattern / fill-cap drop, stabilization compare).
+//
+// Reference semantics (kernels.cpp:34-102): output (i, j) accumulates
+//   acc = a(i,k1) * b(k1,j);  acc = acc + a(i,k) * b(k,j)  for later k
+// in increasing order of k along A's row i; the product is rounded before
+// the add (no FMA); columns are emitted sorted.  add_identity
+// (kernels.cpp:104-134) then adds 1.0 to / inserts 1.0 at the diagonal, and
+// the drop rule (kernels.cpp:136-194, or the A15 cap) filters the row.
+//
+// B200 design: one warp per output row, a per-warp open-addressing hash table
+// in shared memory (global memory for very long rows).  Lanes take the row's
+// products 32 at a time in (k, b-entry) order; lanes that hit the same output
+// column in one round are grouped with __match_any_sync and their leader folds
+// the group's products into the slot in lane order, i.e. in increasing k.
+// Rounds are separated by __syncwarp, so every output entry sees its products
+// in exactly the reference order: the result is bitwise identical while all
+// 32 lanes stay busy.  The count pass computes each row's post-drop length
+// (values are needed to know what survives a threshold), a scan sizes C, and
+// the numeric pass recomputes, compacts, bitonic-sorts and writes the row.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "sort.cuh"
+
+namespace sait {
+
+int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
+
+namespace {
+
+constexpr int32_t kEmpty = -1;
+constexpr int32_t kDead = -2;
+constexpr int kFresh = 1 << 30;
+constexpr int kNumSmemBins = 7;  // tables of 64 .. 4096 slots
+constexpr int kMinLogSlots = 6;
+constexpr int kGlobalBin = kNumSmemBins;
+
+struct Args {
+  int64_t n;
+  int64_t ncols;
+  const int32_t* arp;
+  const int32_t* aci;
+  const double* av;
+  const int32_t* brp;
+  const int32_t* bci;
+  const double* bv;
+  Epilogue epi;
+  int32_t* ccount;       // count pass
+  const int32_t* crp;    // numeric pass
+  int32_t* cci;
+  double* cv;
+  int* changed;
+};
+
+// Per-warp staging for one chunk of <= 32 entries of A's row.
+struct WarpStage {
+  double aval[32];
+  double prod[32];
+  int32_t off[33];
+  int32_t bstart[32];
+};
+
+__device__ __forceinline__ int hash_slot(int32_t col, int shift) {
+  return static_cast<int>((static_cast<uint32_t>(col) * 0x9E3779B1u) >> shift);
+}
+
+// Returns the slot of `col`, inserting it if absent; bit 30 set = inserted.
+__device__ __forceinline__ int find_or_insert(int32_t* key, int mask, int shift, int32_t col) {
+  int s = hash_slot(col, shift) & mask;
+  while (true) {
+    int32_t k = *reinterpret_cast<volatile int32_t*>(&key[s]);
+    if (k == col) return s;
+    if (k == kEmpty) {
+      int32_t old = atomicCAS(&key[s], kEmpty, col);
+      if (old == kEmpty) return s | kFresh;
+      if (old == col) return s;
+    }
+    s = (s + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ bool in_pattern(const int32_t* __restrict__ pci, int32_t b, int32_t e, int32_t col) {
+  while (b < e) {
+    int32_t m = (b + e) >> 1;
+    int32_t c = pci[m];
+    if (c == col) return true;
+    if (c < col) b = m + 1;
+    else e = m;
+  }
+  return false;
+}
+
+// Accumulates row j of A*B (+I) into the table (key/val, `slots` = 2^logs).
+__device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* val, int logs,
+                               WarpStage* st, int lane) {
+  const int slots = 1 << logs, mask = slots - 1, shift = 32 - logs;
+  for (int s = lane; s < slots; s += 32) key[s] = kEmpty;
+  __syncwarp();
+  const int32_t a0 = g.arp[j], a1 = g.arp[j + 1];
+  for (int32_t ab = a0; ab < a1; ab += 32) {
+    const int nt = min(32, a1 - ab);
+    int32_t len = 0, bst = 0;
+    double aval = 0.0;
+    if (lane < nt) {
+      int32_t k = g.aci[ab + lane];
+      aval = g.av[ab + lane];
+      bst = g.brp[k];
+      len = g.brp[k + 1] - bst;
+    }
+    int32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    st->off[lane] = incl - len;
+    st->bstart[lane] = bst;
+    st->aval[lane] = aval;
+    if (lane == 0) st->off[32] = total;
+    __syncwarp();
+    for (int32_t pb = 0; pb < total; pb += 32) {
+      const int32_t p = pb + lane;
+      const bool act = p < total;
+      int32_t col = -1 - lane;  // unique dummy for idle lanes
+      double prod = 0.0;
+      if (act) {
+        // t = last index with off[t] <= p among the nt entries (entries with
+        // len == 0 share their successor's offset; upper_bound skips them)
+        int lo = 0, hi = nt;  // find first t with off[t] > p, in (lo, hi]
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (st->off[mid] > p) hi = mid;
+          else lo = mid + 1;
+        }
+        const int t = lo - 1;
+        const int32_t bi = st->bstart[t] + (p - st->off[t]);
+        col = g.bci[bi];
+        prod = __dmul_rn(st->aval[t], g.bv[bi]);
+      }
+      st->prod[lane] = prod;
+      const unsigned grp = __match_any_sync(0xffffffffu, col);
+      __syncwarp();
+      if (act && (__ffs(grp) - 1) == lane) {
+        const int hs = find_or_insert(key, mask, shift, col);
+        const int s = hs & ~kFresh;
+        double acc = (hs & kFresh) ? prod : __dadd_rn(val[s], prod);
+        unsigned rest = grp & (grp - 1);  // later lanes = later k
+        while (rest) {
+          const int m = __ffs(rest) - 1;
+          acc = __dadd_rn(acc, st->prod[m]);
+          rest &= rest - 1;
+        }
+        val[s] = acc;
+      }
+      __syncwarp();
+    }
+  }
+  if (g.epi.add_identity && lane == 0) {
+    const int hs = find_or_insert(key, mask, shift, j);
+    const int s = hs & ~kFresh;
+    val[s] = (hs & kFresh) ? 1.0 : __dadd_rn(val[s], 1.0);
+  }
+  __syncwarp();
+}
+
+// Applies the drop rule in place (dropped slots become kDead) and returns
+// the number of surviving entries (same value in all lanes).
+__device__ int drop_row(const Args& g, int32_t j, int32_t* key, double* val, int logs, int lane) {
+  const int slots = 1 << logs;
+  const int drop = g.epi.drop;
+  const bool thr = (drop == 1 || drop == 3) && g.epi.tau != 0.0;
+  int32_t pb = 0, pe = 0;
+  if (drop == 2) {
+    pb = g.epi.prp[j];
+    pe = g.epi.prp[j + 1];
+  }
+  int live = 0, offdiag = 0;
+  for (int s = lane; s < slots; s += 32) {
+    int32_t k = key[s];
+    if (k < 0) continue;
+    bool keep = true;
+    if (thr) keep = (k == j) || (fabs(val[s]) >= g.epi.tau);
+    else if (drop == 2) keep = in_pattern(g.epi.pci, pb, pe, k);
+    if (!keep) key[s] = kDead;
+    else {
+      ++live;
+      offdiag += (k != j);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    live += __shfl_xor_sync(0xffffffffu, live, o);
+    offdiag += __shfl_xor_sync(0xffffffffu, offdiag, o);
+  }
+  __syncwarp();
+  if (drop == 3) {
+    int room = g.epi.cap[j] - 1;
+    if (room < 0) room = 0;
+    if (offdiag > room) {
+      // rank of each surviving off-diagonal by (|v| desc, col asc); mark the
+      // ones ranked >= room as "to kill" (-3 - col) without disturbing ranks.
+      for (int s = lane; s < slots; s += 32) {
+        int32_t k = key[s];
+        if (k < 0 || k == j) continue;
+        const double mv = fabs(val[s]);
+        int rank = 0;
+        for (int q = 0; q < slots; ++q) {
+          int32_t kq = key[q];
+          if (kq <= -3) kq = -3 - kq;
+          else if (kq < 0) continue;
+          if (kq == j || kq == k) continue;
+          const double mq = fabs(val[q]);
+          rank += (mq > mv) || (mq == mv && kq < k);
+        }
+        if (rank >= room) key[s] = -3 - k;
+      }
+      __syncwarp();
+      for (int s = lane; s < slots; s += 32)
+        if (key[s] <= -3) key[s] = kDead;
+      __syncwarp();
+      live -= offdiag - room;
+    }
+  }
+  return live;
+}
+
+__device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val, int logs, WarpStage* st,
+                            int lane, bool numeric) {
+  accumulate_row(g, j, key, val, logs, st, lane);
+  const int live = drop_row(g, j, key, val, logs, lane);
+  if (!numeric) {
+    if (lane == 0) g.ccount[j] = live;
+    return;
+  }
+  // compact survivors to [0, live) in slot order (destinations never pass
+  // the chunk being read), pad to a power of two, sort by column.
+  const int slots = 1 << logs;
+  int base = 0;
+  for (int c = 0; c < slots; c += 32) {
+    const int32_t k = key[c + lane];
+    const double v = val[c + lane];
+    const bool keep = k >= 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {
+      const int d = base + __popc(bal & ((1u << lane) - 1));
+      key[d] = k;
+      val[d] = v;
+    }
+    base += __popc(bal);
+    __syncwarp();
+  }
+  const int n2 = next_pow2(live > 0 ? live : 1);
+  for (int s = live + lane; s < n2; s += 32) key[s] = kKeyPad;
+  __syncwarp();
+  bitonic_sort(key, val, n2, lane, 32, WarpSync{});
+  const int32_t out = g.crp[j];
+  for (int s = lane; s < live; s += 32) {
+    g.cci[out + s] = key[s];
+    g.cv[out + s] = val[s];
+  }
+  if (g.epi.qrp) {
+    const int32_t qb = g.epi.qrp[j], ql = g.epi.qrp[j + 1] - qb;
+    bool diff = ql != live;
+    if (!diff) {
+      for (int s = lane; s < live; s += 32) {
+        const double a = g.epi.qv[qb + s], b = val[s];
+        const double fa = fabs(a), fb = fabs(b);
+        const double mx = fa < fb ? fb : fa;  // std::max(fa, fb)
+        if (g.epi.qci[qb + s] != key[s] || fabs(__dsub_rn(b, a)) > __dmul_rn(1e-15, mx)) diff = true;
+      }
+    }
+    if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(g.changed, 1);
+  }
+  __syncwarp();
+}
+
+__host__ __device__ constexpr int smem_per_warp(int logs) {
+  return ((1 << logs) * 12 + static_cast<int>(sizeof(WarpStage)) + 15) / 16 * 16;
+}
+
+template <int LOGS>
+__global__ void __launch_bounds__(256) spgemm_smem(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+                                                   bool numeric) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* mine = smem + w * smem_per_warp(LOGS);
+  double* val = reinterpret_cast<double*>(mine);
+  int32_t* key = reinterpret_cast<int32_t*>(mine + (1 << LOGS) * 8);
+  WarpStage* st = reinterpret_cast<WarpStage*>(mine + (1 << LOGS) * 12);
+  const int warps = blockDim.x >> 5;
+  for (int32_t r = blockIdx.x * warps + w; r < nrows_bin; r += gridDim.x * warps)
+    process_row(g, rows[r], key, val, LOGS, st, lane, numeric);
+}
+
+// Very long rows: table in global scratch (per-row offsets), one warp per row.
+__global__ void spgemm_global(Args g, const int32_t* __restrict__ rows, const int64_t* __restrict__ offs,
+                              const int8_t* __restrict__ logs_of, int32_t nrows_bin, int32_t* gkey, double* gval,
+                              bool numeric) {
+  __shared__ WarpStage stage[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int warps = blockDim.x >> 5;
+  for (int32_t r = blockIdx.x * warps + w; r < nrows_bin; r += gridDim.x * warps)
+    process_row(g, rows[r], gkey + offs[r], gval + offs[r], logs_of[r], &stage[w], lane, numeric);
+}
+
+// products per row (P_j) -> table bin; histogram of bins; total products.
+__global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restrict__ pcap,
+                          int32_t* __restrict__ hist, unsigned long long* __restrict__ total) {
+  __shared__ int32_t h[kNumSmemBins + 1];
+  __shared__ unsigned long long tsum;
+  if (threadIdx.x <= kNumSmemBins) h[threadIdx.x] = 0;
+  if (threadIdx.x == 0) tsum = 0;
+  __syncthreads();
+  int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < g.n) {
+    int64_t p = 0;
+    for (int32_t e = g.arp[j]; e < g.arp[j + 1]; ++e) {
+      int32_t k = g.aci[e];
+      p += g.brp[k + 1] - g.brp[k];
+    }
+    atomicAdd(&tsum, static_cast<unsigned long long>(p));
+    int64_t distinct = (p < g.ncols ? p : g.ncols) + 1;  // +1: the identity entry
+    int logs = kMinLogSlots;
+    while ((int64_t{1} << logs) < 2 * distinct) ++logs;
+    int bin = logs - kMinLogSlots;
+    if (bin > kGlobalBin) bin = kGlobalBin;
+    bin_of[j] = static_cast<int8_t>(bin);
+    pcap[j] = logs;  // table log2 size (used by the global bin)
+    atomicAdd(&h[bin], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x <= kNumSmemBins && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+  if (threadIdx.x == 0 && tsum) atomicAdd(total, tsum);
+}
+
+__global__ void scatter_bins(int64_t n, const int8_t* __restrict__ bin_of, int32_t* __restrict__ cursor,
+                             int32_t* __restrict__ lists) {
+  int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int b = bin_of[j];
+  lists[atomicAdd(&cursor[b], 1)] = static_cast<int32_t>(j);
+}
+
+using SmemKernel = void (*)(Args, const int32_t*, int32_t, bool);
+
+SmemKernel smem_kernel(int bin) {
+  switch (bin) {
+    case 0: return spgemm_smem<6>;
+    case 1: return spgemm_smem<7>;
+    case 2: return spgemm_smem<8>;
+    case 3: return spgemm_smem<9>;
+    case 4: return spgemm_smem<10>;
+    case 5: return spgemm_smem<11>;
+    default: return spgemm_smem<12>;
+  }
+}
+
+int warps_for_bin(int bin) {
+  int logs = bin + kMinLogSlots;
+  int w = (200 * 1024) / smem_per_warp(logs);
+  return std::max(1, std::min(8, w));
+}
+
+struct Plan {
+  int32_t hist[kNumSmemBins + 1] = {};
+  int32_t start[kNumSmemBins + 2] = {};
+  int32_t* lists = nullptr;   // device, rows grouped by bin
+  int64_t products = 0;
+  // global bin
+  int64_t* goffs = nullptr;
+  int8_t* glogs = nullptr;
+  int32_t* gkey = nullptr;
+  double* gval = nullptr;
+};
+
+void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s) {
+  static bool attr_set[kNumSmemBins] = {};
+  for (int b = 0; b < kNumSmemBins; ++b) {
+    int32_t cnt = pl.hist[b];
+    if (!cnt) continue;
+    int warps = warps_for_bin(b);
+    int smem = warps * smem_per_warp(b + kMinLogSlots);
+    SmemKernel k = smem_kernel(b);
+    if (!attr_set[b]) {
+      SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr_set[b] = true;
+    }
+    int blocks_per_sm = std::max(1, (228 * 1024) / (smem + 1024));
+    int64_t want = (cnt + warps - 1) / warps;
+    unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, int64_t{num_sms()} * blocks_per_sm * 4));
+    k<<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, numeric);
+    SAIT_LAUNCHED();
+  }
+  int32_t gc = pl.hist[kGlobalBin];
+  if (gc) {
+    unsigned grid = static_cast<unsigned>(std::min<int64_t>((gc + 7) / 8, num_sms() * 8));
+    spgemm_global<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kGlobalBin], pl.goffs, pl.glogs, gc, pl.gkey,
+                                        pl.gval, numeric);
+    SAIT_LAUNCHED();
+  }
+}
+
+}  // namespace
+
+SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi, cudaStream_t s) {
+  if (a.ncols != b.nrows)
+    throw_invalid("spgemm: inner dimensions " + std::to_string(a.ncols) + " and " + std::to_string(b.nrows) +
+                  " do not match");
+  SpgemmResult res;
+  const int64_t n = a.nrows;
+  DevCsr& c = res.c;
+  c.nrows = n;
+  c.ncols = b.ncols;
+  c.rp = dalloc<int32_t>(n + 1, s);
+  if (n == 0) {
+    SAIT_CUDA(cudaMemsetAsync(c.rp, 0, sizeof(int32_t), s));
+    c.ci = dalloc<int32_t>(1, s);
+    c.v = dalloc<double>(1, s);
+    res.changed = epi.qrp != nullptr ? false : true;
+    return res;
+  }
+  Args g{};
+  g.n = n;
+  g.ncols = b.ncols;
+  g.arp = a.rp;
+  g.aci = a.ci;
+  g.av = a.v;
+  g.brp = b.rp;
+  g.bci = b.ci;
+  g.bv = b.v;
+  g.epi = epi;
+
+  // ---- plan: bin rows by product count
+  Plan pl;
+  int8_t* bin_of = dalloc<int8_t>(n, s);
+  int32_t* logs_of = dalloc<int32_t>(n, s);
+  int32_t* hist = dalloc<int32_t>(2 * (kNumSmemBins + 1), s);
+  unsigned long long* total = dalloc<unsigned long long>(1, s);
+  SAIT_CUDA(cudaMemsetAsync(hist, 0, 2 * (kNumSmemBins + 1) * sizeof(int32_t), s));
+  SAIT_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), s));
+  plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total);
+  SAIT_LAUNCHED();
+  unsigned long long htotal = 0;
+  SAIT_CUDA(cudaMemcpyAsync(pl.hist, hist, sizeof pl.hist, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaMemcpyAsync(&htotal, total, sizeof htotal, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  res.products = static_cast<int64_t>(htotal);
+  for (int b2 = 0; b2 <= kNumSmemBins; ++b2) pl.start[b2 + 1] = pl.start[b2] + pl.hist[b2];
+  pl.lists = dalloc<int32_t>(n, s);
+  int32_t* cursor = hist + kNumSmemBins + 1;
+  SAIT_CUDA(cudaMemcpyAsync(cursor, pl.start, (kNumSmemBins + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  scatter_bins<<<grid_for(n, 256), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
+  SAIT_LAUNCHED();
+  int32_t gc = pl.hist[kGlobalBin];
+  if (gc) {
+    // per-row global tables
+    std::vector<int32_t> rows(gc), all_logs(n);
+    SAIT_CUDA(cudaMemcpyAsync(rows.data(), pl.lists + pl.start[kGlobalBin], gc * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaMemcpyAsync(all_logs.data(), logs_of, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> offs(gc);
+    std::vector<int8_t> lg(gc);
+    int64_t tot = 0;
+    for (int32_t q = 0; q < gc; ++q) {
+      offs[q] = tot;
+      lg[q] = static_cast<int8_t>(all_logs[rows[q]]);
+      tot += int64_t{1} << lg[q];
+    }
+    pl.goffs = dalloc<int64_t>(gc, s);
+    pl.glogs = dalloc<int8_t>(gc, s);
+    pl.gkey = dalloc<int32_t>(tot, s);
+    pl.gval = dalloc<double>(tot, s);
+    SAIT_CUDA(cudaMemcpyAsync(pl.goffs, offs.data(), gc * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SAIT_CUDA(cudaMemcpyAsync(pl.glogs, lg.data(), gc * sizeof(int8_t), cudaMemcpyHostToDevice, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+  }
+
+  // ---- count pass, scan, numeric pass
+  int32_t* counts = dalloc<int32_t>(n, s);
+  g.ccount = counts;
+  launch_pass(g, pl, false, s);
+  c.nnz = scan_counts(counts, c.rp, n, s);
+  dfree(counts, s);
+  c.ci = dalloc<int32_t>(c.nnz, s);
+  c.v = dalloc<double>(c.nnz, s);
+  int* changed = dalloc<int>(1, s);
+  SAIT_CUDA(cudaMemsetAsync(changed, 0, sizeof(int), s));
+  g.ccount = nullptr;
+  g.crp = c.rp;
+  g.cci = c.ci;
+  g.cv = c.v;
+  g.changed = changed;
+  launch_pass(g, pl, true, s);
+  if (epi.qrp) {
+    int hc = 1;
+    SAIT_CUDA(cudaMemcpyAsync(&hc, changed, sizeof hc, cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    res.changed = hc != 0;
+  }
+  dfree(changed, s);
+  dfree(bin_of, s);
+  dfree(logs_of, s);
+  dfree(hist, s);
+  dfree(total, s);
+  dfree(pl.lists, s);
+  dfree(pl.goffs, s);
+  dfree(pl.glogs, s);
+  dfree(pl.gkey, s);
+  dfree(pl.gval, s);
+  return res;
+}
+
+}  // namespace sait

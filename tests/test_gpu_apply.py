@@ -1,0 +1,100 @@
+"""GPU parity of the SAIT apply z = M_U (M_L r) and the block apply against the
+reference's own outputs (golden) and the oracle port: bitwise, since each row
+is summed sequentially in stored order without FMA (kernels.cpp:18-24)."""
+import numpy as np
+import pytest
+
+from conftest import golden_csr
+from helpers import bitwise_equal, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2106_12836_b200 as S
+
+    return S
+
+
+@pytest.fixture(scope="module")
+def c1_pair(S, golden):
+    ML = to_product(golden_csr(golden, "c1/ML"))
+    MU = to_product(golden_csr(golden, "c1/MU"))
+    return S.SaitPairPreconditioner(ML, MU)
+
+
+def test_c1_apply_host(S, golden, c1_pair):
+    z = np.empty(4096)
+    c1_pair.apply(golden["c1/r"], z)
+    assert bitwise_equal(z, golden["c1/z"])
+    assert c1_pair.name() == "sait" and c1_pair.nnz() == 2 * 51215
+
+
+def test_c1_apply_device(S, golden, c1_pair):
+    import torch
+
+    r = torch.from_numpy(golden["c1/r"]).cuda()
+    z = torch.empty_like(r)
+    c1_pair.apply(r, z)
+    torch.cuda.synchronize()
+    assert bitwise_equal(z.cpu().numpy(), golden["c1/z"])
+
+
+def test_c1_apply_block(S, golden, c1_pair):
+    import torch
+
+    Z = c1_pair.apply_block(golden["c1/R8"])
+    assert bitwise_equal(np.asfortranarray(Z).ravel(order="F"), np.asfortranarray(golden["c1/Z8"]).ravel(order="F"))
+    # device, row-major layout
+    R = torch.from_numpy(np.ascontiguousarray(golden["c1/R8"])).cuda()
+    Zd = c1_pair.apply_block(R, layout="row")
+    torch.cuda.synchronize()
+    assert bitwise_equal(Zd.cpu().numpy(), golden["c1/Z8"])
+
+
+@pytest.mark.parametrize("nvec", [1, 2, 3, 5, 8, 11, 16])
+def test_block_widths(S, golden, c1_pair, nvec):
+    from oracle import oracle as O
+
+    R = np.stack([O.uniform_pm1(900 + c, 4096) for c in range(nvec)], axis=1)
+    Z = c1_pair.apply_block(R)
+    for c in range(nvec):
+        z = np.empty(4096)
+        c1_pair.apply(np.ascontiguousarray(R[:, c]), z)
+        assert bitwise_equal(Z[:, c], z)
+
+
+def test_spmv_long_and_empty_rows(S, port):
+    """rows longer than the 2048-entry staging chunk, empty rows, n % 256 != 0"""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(7)
+    n = 1000
+    dense_rows = {3: 5000, 500: 2048, 501: 2049, 999: 7000}
+    rows, cols = [], []
+    for i in range(n):
+        k = dense_rows.get(i, int(rng.integers(0, 9)))
+        c = np.sort(rng.choice(8000, size=k, replace=False))
+        rows += [i] * k
+        cols += list(c)
+    vals = rng.standard_normal(len(rows))
+    a = sp.csr_matrix((vals, (rows, cols)), shape=(n, 8000))
+    a.sort_indices()
+    A = S.CsrMatrix.from_scipy(a)
+    x = rng.standard_normal(8000)
+    y = S.spmv(A, x)
+    from helpers import to_oracle
+
+    assert bitwise_equal(y, port.spmv(to_oracle(A), x))
+
+
+def test_apply_errors(S, c1_pair):
+    with pytest.raises(S.SaitInvalidArgument, match="spmv: vector length 5 does not match ncols 4096"):
+        c1_pair.apply(np.zeros(5), np.zeros(4096))
+    with pytest.raises(S.SaitInvalidArgument, match="spmv: output length mismatch"):
+        c1_pair.apply(np.zeros(4096), np.zeros(7))
+    a = S.CsrMatrix(3, 4, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
+    b = S.CsrMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
+    with pytest.raises(S.SaitInvalidArgument, match="SaitPairPreconditioner: factor shapes do not chain"):
+        S.SaitPairPreconditioner(b, a)

@@ -1,0 +1,138 @@
+"""GPU parity of the SAIT builder against the reference (golden fixtures made
+by the compiled reference) and the C restatement (oracle port).  Bitwise:
+the device recursion performs the reference's exact operation sequence."""
+import numpy as np
+import pytest
+
+from conftest import golden_csr
+from helpers import bitwise_equal_csr, to_product
+
+pytestmark = pytest.mark.gpu
+
+THR_CASES = [(0.0, 1), (0.0, 5), (0.01, 3), (0.05, 10), (0.2, 4), (0.0, 250)]
+PAT_CASES = [(0, 1), (1, 3), (2, 2), (3, 5)]
+CAP_CASES = [(0.01, 3, 3.0), (0.0, 4, 1.5), (0.05, 6, 1.0)]
+NAMES = [("syn_lower", True), ("syn_upper", False)]
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2106_12836_b200 as S
+
+    return S
+
+
+def kind(S, lower):
+    return S.lower_triangular if lower else S.upper_triangular
+
+
+@pytest.mark.parametrize("name,lower", NAMES)
+@pytest.mark.parametrize("tau,steps", THR_CASES)
+def test_sait_thr_golden(S, golden, name, lower, tau, steps):
+    t = to_product(golden_csr(golden, f"{name}/T"))
+    m = S.sait_thr(t, kind(S, lower), S.SaitThrParams(tau, steps))
+    assert bitwise_equal_csr(m, golden_csr(golden, f"{name}/thr_{tau}_{steps}"))
+
+
+@pytest.mark.parametrize("name,lower", NAMES)
+@pytest.mark.parametrize("p,m", PAT_CASES)
+def test_sait_pat_golden(S, golden, name, lower, p, m):
+    t = to_product(golden_csr(golden, f"{name}/T"))
+    out = S.sait_pat(t, kind(S, lower), S.SaitPatParams(p, m))
+    assert bitwise_equal_csr(out, golden_csr(golden, f"{name}/pat_{p}_{m}"))
+    pat = S.sait_pat_capture_pattern(t, kind(S, lower), p)
+    assert bitwise_equal_csr(pat, golden_csr(golden, f"{name}/patcap_{p}"))
+
+
+@pytest.mark.parametrize("name,lower", NAMES)
+@pytest.mark.parametrize("tau,steps,f", CAP_CASES)
+def test_sait_cap_golden(S, golden, name, lower, tau, steps, f):
+    t = to_product(golden_csr(golden, f"{name}/T"))
+    m = S.sait_thr_cap(t, kind(S, lower), S.SaitThrParams(tau, steps), f)
+    assert bitwise_equal_csr(m, golden_csr(golden, f"{name}/cap_{tau}_{steps}_{f}"))
+
+
+def test_config1_factors(S, golden):
+    """BASELINE config 1: 64x64 Poisson, ILU(0), tau=1e-2, k=4 (51,215 nnz per factor)."""
+    L = to_product(golden_csr(golden, "c1/L"))
+    U = to_product(golden_csr(golden, "c1/U"))
+    st = []
+    ML = S.sait_thr(L, S.lower_triangular, S.SaitThrParams(1e-2, 4), stats_out=st)
+    MU = S.sait_thr(U, S.upper_triangular, S.SaitThrParams(1e-2, 4), stats_out=st)
+    assert bitwise_equal_csr(ML, golden_csr(golden, "c1/ML"))
+    assert bitwise_equal_csr(MU, golden_csr(golden, "c1/MU"))
+    assert ML.nnz() == 51215 and MU.nnz() == 51215
+    assert st[0].nnz_out == 51215 and st[0].steps_run == 4
+
+
+@pytest.mark.parametrize("seed,n,lower", [(21, 300, True), (22, 300, False), (23, 1, True), (24, 2, False)])
+@pytest.mark.parametrize("tau,steps", [(0.0, 3), (0.03, 6)])
+def test_random_vs_oracle(S, port, seed, n, lower, tau, steps):
+    from oracle import oracle as O
+
+    t = O.synthetic_lower(n, 9, 0.02, seed=seed)
+    if not lower:
+        t = port.transpose(t)
+    expect = port.sait_thr(t, lower, tau, steps)
+    got = S.sait_thr(to_product(t), kind(S, lower), S.SaitThrParams(tau, steps))
+    assert bitwise_equal_csr(got, expect)
+
+
+def test_long_rows_use_global_tables(S, port):
+    """tau = 0 on a dense-ish lower T: rows of M^T exceed the shared-memory
+    tables (>2048 distinct columns) and take the global-memory path."""
+    from oracle import oracle as O
+
+    t = O.synthetic_lower(3000, 12, 0.3, seed=5)
+    expect = port.sait_thr(t, True, 0.0, 40)
+    got = S.sait_thr(to_product(t), S.lower_triangular, S.SaitThrParams(0.0, 40))
+    assert bitwise_equal_csr(got, expect)
+
+
+def test_exact_series_property(S, port):
+    """SPEC acceptance #1: sait_thr(T, 0, n-1) is T^-1 (||T M - I||_inf small)."""
+    from oracle import oracle as O
+
+    for n in (5, 20, 64):
+        t = O.synthetic_lower(n, 3, 0.3, seed=100 + n)
+        m = S.sait_thr(to_product(t), S.lower_triangular, S.SaitThrParams(0.0, n - 1))
+        tm = (t.to_scipy() @ m.to_scipy()).toarray() - np.eye(n)
+        assert np.abs(tm).sum(axis=1).max() <= 1e-10
+
+
+def test_errors_match_reference(S, golden):
+    """Exception kinds and messages (sait.cpp:60,77,92; csr.cpp:132)."""
+    t = to_product(golden_csr(golden, "syn_lower/T"))
+    with pytest.raises(S.SaitInvalidArgument, match=r"sait_thr: threshold must be in \[0, 1\), got 1.500000"):
+        S.sait_thr(t, S.lower_triangular, S.SaitThrParams(1.5, 3))
+    with pytest.raises(S.SaitInvalidArgument, match="sait_polynomial: steps must be >= 1"):
+        S.sait_thr(t, S.lower_triangular, S.SaitThrParams(0.1, 0))
+    with pytest.raises(S.SaitInvalidArgument, match=r"check_triangular: entry \(1, 0\) outside stated triangle"):
+        S.sait_thr(t, S.upper_triangular, S.SaitThrParams(0.1, 2))
+    with pytest.raises(S.SaitInvalidArgument, match="sait_pat: refine_steps must be >= 1"):
+        S.sait_pat(t, S.lower_triangular, S.SaitPatParams(1, 0))
+    with pytest.raises(S.SaitInvalidArgument, match="sait_pat: pattern_steps must be >= 0"):
+        S.sait_pat(t, S.lower_triangular, S.SaitPatParams(-1, 1))
+    z = S.CsrMatrix(3, 3, [0, 1, 2, 4], [0, 1, 1, 2], [2.0, 0.0, 1.0, 3.0])
+    with pytest.raises(S.SaitRuntimeError, match="jacobi_split: singular matrix, zero diagonal at row 1"):
+        S.sait_thr(z, S.lower_triangular, S.SaitThrParams(0.1, 2))
+    nd = S.CsrMatrix(3, 3, [0, 1, 1, 3], [0, 0, 2], [2.0, 1.0, 3.0])
+    with pytest.raises(S.SaitRuntimeError, match="zero diagonal at row 1"):
+        S.sait_thr(nd, S.lower_triangular, S.SaitThrParams(0.1, 2))
+    rect = S.CsrMatrix(2, 3, [0, 1, 2], [0, 1], [1.0, 1.0])
+    with pytest.raises(S.SaitInvalidArgument, match="jacobi_split: matrix is not square"):
+        S.sait_thr(rect, S.lower_triangular, S.SaitThrParams(0.1, 2))
+
+
+def test_spec_examples(S):
+    """SPEC.md:217-238 examples for jacobi_split / sait_core / sait_thr."""
+    t = S.CsrMatrix(2, 2, [0, 1, 3], [0, 0, 1], [2.0, 4.0, 2.0])
+    sp = S.jacobi_split(t, S.lower_triangular)
+    assert list(sp.inv_diag) == [0.5, 0.5]
+    assert list(sp.iteration_matrix.row_ptr) == [0, 0, 1] and list(sp.iteration_matrix.values) == [-2.0]
+    eye = S.CsrMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
+    m = S.sait_thr(eye, S.lower_triangular, S.SaitThrParams(0.3, 4))
+    assert m == eye
+    d = S.CsrMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [2.0, 4.0, 8.0])
+    m = S.sait_pat(d, S.upper_triangular, S.SaitPatParams(2, 3))
+    assert list(m.values) == [0.5, 0.25, 0.125]

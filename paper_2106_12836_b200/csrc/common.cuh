@@ -53,8 +53,9 @@ struct DevCsr {
 template <class T>
 T* dalloc(size_t count, cudaStream_t s) {
   void* p = nullptr;
-  if (count == 0) count = 1;
-  cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), s);
+  // +256 bytes: bulk copies round transfers up to whole 16-byte granules and
+  // may read up to 15 bytes past the last element.
+  cudaError_t e = cudaMallocAsync(&p, count * sizeof(T) + 256, s);
   if (e == cudaErrorMemoryAllocation) throw Error(SAIT_ERR_NOMEM, "out of device memory");
   SAIT_CUDA(e);
   return static_cast<T*>(p);

@@ -12,7 +12,10 @@
 //     distribution; long rows simply take several chunks);
 //   * the block version (row-major n x nvec) reads the matrix once for all
 //     vectors (the reference re-reads it per column, dense.cpp:10-19).
+#include <cstdlib>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace sait {
 namespace {
@@ -57,6 +60,63 @@ __global__ void __launch_bounds__(kRows) spmv_rowblock(int64_t n, const int32_t*
     const int32_t b = mb > c0 ? mb : c0;
     const int32_t e = me < c0 + cn ? me : c0 + cn;
     for (int32_t q = b; q < e; ++q) acc = __dadd_rn(acc, prod[q - c0]);
+    __syncthreads();
+  }
+  if (my < r1) y[my] = acc;
+}
+
+// TMA-staged variant: one elected thread moves the chunk's column indices
+// and values into shared memory with two 1-D bulk copies (cp.async.bulk,
+// evict-first in L2: the factors are streamed once per apply); the CTA then
+// forms the products in place and each thread sums its row sequentially.
+constexpr int kTChunk = 2048;
+struct __align__(16) TmaStage {
+  double val[kTChunk + 8];
+  int32_t col[kTChunk + 8];
+  uint64_t bar;
+};
+
+__global__ void __launch_bounds__(kRows) spmv_tma(int64_t n, const int32_t* __restrict__ rp,
+                                                   const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ TmaStage st;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&st.bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRows;
+  const int64_t r1 = r0 + kRows < n ? r0 + kRows : n;
+  const int64_t my = r0 + tid;
+  const int32_t nz0 = rp[r0], nz1 = rp[r1];
+  int32_t mb = 0, me = 0;
+  if (my < r1) {
+    mb = rp[my];
+    me = rp[my + 1];
+  }
+  const uint64_t pol = policy_evict_first();
+  uint32_t phase = 0;
+  double acc = 0.0;
+  for (int32_t c0 = nz0; c0 < nz1; c0 += kTChunk) {
+    const int32_t c1 = nz1 - c0 < kTChunk ? nz1 : c0 + kTChunk;
+    const int32_t a0 = c0 & ~3;                 // 16-byte aligned source for both arrays
+    const int32_t cnt = (c1 - a0 + 3) & ~3;     // whole 16-byte granules (arrays are padded)
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&st.bar, static_cast<uint32_t>(cnt) * 12u);
+      bulk_g2s_stream(st.col, ci + a0, static_cast<uint32_t>(cnt) * 4u, &st.bar, pol);
+      bulk_g2s_stream(st.val, v + a0, static_cast<uint32_t>(cnt) * 8u, &st.bar, pol);
+    }
+    mbar_wait(&st.bar, phase);
+    phase ^= 1;
+    const int lo = c0 - a0, hi = c1 - a0;
+#pragma unroll 4
+    for (int e = lo + tid; e < hi; e += kRows) st.val[e] = __dmul_rn(st.val[e], __ldg(x + st.col[e]));
+    __syncthreads();
+    const int32_t b = mb > c0 ? mb : c0;
+    const int32_t e = me < c1 ? me : c1;
+    for (int32_t q = b; q < e; ++q) acc = __dadd_rn(acc, st.val[q - a0]);
     __syncthreads();
   }
   if (my < r1) y[my] = acc;
@@ -117,9 +177,26 @@ __global__ void block_transpose_kernel(const double* __restrict__ in, double* __
 
 }  // namespace
 
+int spmv_variant() {
+  static int v = [] {
+    const char* e = std::getenv("SAIT_SPMV");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s) {
   if (a.nrows == 0) return;
-  spmv_rowblock<<<grid_for(a.nrows, kRows), kRows, 0, s>>>(a.nrows, a.rp, a.ci, a.v, x, y);
+  if (spmv_variant() == 0) {
+    spmv_rowblock<<<grid_for(a.nrows, kRows), kRows, 0, s>>>(a.nrows, a.rp, a.ci, a.v, x, y);
+  } else {
+    static bool attr = [] {
+      cudaFuncSetAttribute(spmv_tma, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      return true;
+    }();
+    (void)attr;
+    spmv_tma<<<grid_for(a.nrows, kRows), kRows, 0, s>>>(a.nrows, a.rp, a.ci, a.v, x, y);
+  }
   SAIT_LAUNCHED();
 }
 

@@ -162,6 +162,10 @@ int sait_pair_apply_block(sait_pair_t p, const double *d_r, double *d_z, int64_t
                           int64_t nvec, int layout, sait_stream_t stream);
 int sait_pair_apply_block_host(sait_pair_t p, const double *h_r, double *h_z, int64_t n,
                                int64_t nvec, int layout, sait_stream_t stream);
+/* One factor's SpMV with the pair's planned kernel (which: 0 = M_L, 1 = M_U);
+ * the building block of apply, exposed for per-kernel timing. */
+int sait_pair_spmv_factor(sait_pair_t p, int which, const double *d_x, double *d_y,
+                          sait_stream_t stream);
 /* Borrowed handles of the two factors (owned by the pair). */
 int sait_pair_factors(sait_pair_t p, sait_dcsr_t *ml, sait_dcsr_t *mu);
 void sait_pair_destroy(sait_pair_t p);

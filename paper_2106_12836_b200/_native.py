@@ -93,6 +93,7 @@ PROTOTYPES = {
     "sait_pair_apply_host": (C.c_int, [VP, PD, C.c_int64, PD, C.c_int64, VP]),
     "sait_pair_apply_block": (C.c_int, [VP, VP, VP, C.c_int64, C.c_int64, C.c_int, VP]),
     "sait_pair_apply_block_host": (C.c_int, [VP, PD, PD, C.c_int64, C.c_int64, C.c_int, VP]),
+    "sait_pair_spmv_factor": (C.c_int, [VP, C.c_int, VP, VP, VP]),
     "sait_pair_factors": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP)]),
     "sait_pair_destroy": (None, [VP]),
     "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),

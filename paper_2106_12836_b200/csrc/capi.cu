@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,11 @@ struct sait_pair_s {
   sait_dcsr_s* ml = nullptr;
   sait_dcsr_s* mu = nullptr;
   bool owns = false;
+  sait::SpmvPlan pl, pu;  // persistent-pipeline task lists of the two factors
+  // per-stream scratch (y = M_L r): applies on one stream are ordered, so one
+  // buffer per stream honours the concurrent-apply contract
+  std::mutex mu_ws;
+  std::unordered_map<cudaStream_t, double*> ws;
 };
 
 namespace sait {
@@ -583,11 +589,15 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
     if (ml->m.nrows != mu->m.ncols) sait::throw_invalid("SaitPairPreconditioner: factor shapes do not chain");
     if (ml->dev != mu->dev) sait::throw_invalid("SaitPairPreconditioner: factors live on different devices");
     if (!ml->m.v || !mu->m.v) sait::throw_invalid("SaitPairPreconditioner: factors have no values");
+    DeviceGuard g(ml->dev);
+    init_device_pool();
     auto* p = new sait_pair_s;
     p->dev = ml->dev;
     p->ml = ml;
     p->mu = mu;
     p->owns = take_ownership != 0;
+    p->pl = sait::make_spmv_plan(ml->m, nullptr);
+    p->pu = sait::make_spmv_plan(mu->m, nullptr);
     *out = p;
   });
 }
@@ -608,6 +618,30 @@ int sait_pair_factors(sait_pair_t p, sait_dcsr_t* ml, sait_dcsr_t* mu) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+int pair_variant() {
+  static int v = [] {
+    const char* e = std::getenv("SAIT_PAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+double* pair_scratch(sait_pair_t p, cudaStream_t s, int64_t n) {
+  std::lock_guard<std::mutex> lk(p->mu_ws);
+  auto it = p->ws.find(s);
+  if (it != p->ws.end()) return it->second;
+  void* buf = nullptr;
+  SAIT_CUDA(cudaMalloc(&buf, sizeof(double) * (n > 0 ? n : 1) + 256));
+  p->ws.emplace(s, static_cast<double*>(buf));
+  return static_cast<double*>(buf);
+}
+}  // namespace
+
+extern "C" {
+
 int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z, int64_t zlen, sait_stream_t stream) {
   return guarded([&] {
     need(p, "apply");
@@ -619,10 +653,26 @@ int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z,
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
     cudaStream_t s = sait::as_stream(stream);
-    double* y = sait::dalloc<double>(L.nrows, s);  // reference: fresh y per call
-    sait::spmv(L, d_r, y, s);
-    sait::spmv(U, y, d_z, s);
-    sait::dfree(y, s);
+    double* y = pair_scratch(p, s, L.nrows);
+    if (pair_variant() == 0) {
+      sait::spmv(L, d_r, y, s);
+      sait::spmv(U, y, d_z, s);
+    } else {
+      sait::spmv_planned(L, p->pl, d_r, y, s);
+      sait::spmv_planned(U, p->pu, y, d_z, s);
+    }
+  });
+}
+
+int sait_pair_spmv_factor(sait_pair_t p, int which, const double* d_x, double* d_y, sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "sait_pair_spmv_factor");
+    DeviceGuard g(p->dev);
+    cudaStream_t s = sait::as_stream(stream);
+    const sait::DevCsr& m = which == 0 ? p->ml->m : p->mu->m;
+    const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
+    if (pair_variant() == 0) sait::spmv(m, d_x, d_y, s);
+    else sait::spmv_planned(m, pl, d_x, d_y, s);
   });
 }
 
@@ -730,6 +780,17 @@ int sait_pair_apply_block_host(sait_pair_t p, const double* h_r, double* h_z, in
 
 void sait_pair_destroy(sait_pair_t p) {
   if (!p) return;
+  {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->dev);
+    cudaDeviceSynchronize();
+    sait::free_spmv_plan(p->pl, nullptr);
+    sait::free_spmv_plan(p->pu, nullptr);
+    for (auto& kv : p->ws) cudaFree(kv.second);
+    cudaDeviceSynchronize();
+    if (prev >= 0) cudaSetDevice(prev);
+  }
   if (p->owns) {
     sait_csr_free(p->ml);
     sait_csr_free(p->mu);

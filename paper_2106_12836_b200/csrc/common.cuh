@@ -129,6 +129,20 @@ struct SpgemmResult {
 SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi, cudaStream_t s);
 
 // spmv.cu
+struct __align__(16) SpmvTask {
+  int32_t row0, nrows;  // row-block
+  int32_t c0, c1;       // nnz chunk [c0, c1)
+  int32_t flags;        // 1: first chunk of its row-block, 2: last chunk
+};
+struct SpmvPlan {
+  SpmvTask* tasks = nullptr;
+  int32_t* cta_start = nullptr;
+  int64_t ntasks = 0;
+  int grid = 0;
+};
+SpmvPlan make_spmv_plan(const DevCsr& a, cudaStream_t s);
+void free_spmv_plan(SpmvPlan& p, cudaStream_t s);
+void spmv_planned(const DevCsr& a, const SpmvPlan& p, const double* x, double* y, cudaStream_t s);
 void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
 void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaStream_t s);
 void transpose_block(const double* in, double* out, int64_t n, int nvec, bool to_rowmajor,

@@ -22,6 +22,7 @@ struct sait_pair_s {
   sait_dcsr_s* mu = nullptr;
   bool owns = false;
   sait::SpmvPlan pl, pu;  // persistent-pipeline task lists of the two factors
+  sait::SellMatrix sl, su;  // SELL-32 copies used by the apply (empty if irregular)
   // per-stream scratch (y = M_L r): applies on one stream are ordered, so one
   // buffer per stream honours the concurrent-apply contract
   std::mutex mu_ws;
@@ -598,6 +599,8 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
     p->owns = take_ownership != 0;
     p->pl = sait::make_spmv_plan(ml->m, nullptr);
     p->pu = sait::make_spmv_plan(mu->m, nullptr);
+    p->sl = sait::make_sell(ml->m, nullptr);
+    p->su = sait::make_sell(mu->m, nullptr);
     *out = p;
   });
 }
@@ -624,9 +627,20 @@ namespace {
 int pair_variant() {
   static int v = [] {
     const char* e = std::getenv("SAIT_PAIR");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   return v;
+}
+
+// One factor's SpMV with the fastest kernel available for it.
+void factor_spmv(sait_pair_t p, int which, const double* x, double* y, cudaStream_t s) {
+  const sait::DevCsr& m = which == 0 ? p->ml->m : p->mu->m;
+  const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
+  const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
+  const int v = pair_variant();
+  if (v == 2 && sm.ok()) sait::sell_spmv(sm, x, y, s);
+  else if (v == 1) sait::spmv_planned(m, pl, x, y, s);
+  else sait::spmv(m, x, y, s);
 }
 
 double* pair_scratch(sait_pair_t p, cudaStream_t s, int64_t n) {
@@ -654,13 +668,8 @@ int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z,
     DeviceGuard g(p->dev);
     cudaStream_t s = sait::as_stream(stream);
     double* y = pair_scratch(p, s, L.nrows);
-    if (pair_variant() == 0) {
-      sait::spmv(L, d_r, y, s);
-      sait::spmv(U, y, d_z, s);
-    } else {
-      sait::spmv_planned(L, p->pl, d_r, y, s);
-      sait::spmv_planned(U, p->pu, y, d_z, s);
-    }
+    factor_spmv(p, 0, d_r, y, s);
+    factor_spmv(p, 1, y, d_z, s);
   });
 }
 
@@ -669,10 +678,7 @@ int sait_pair_spmv_factor(sait_pair_t p, int which, const double* d_x, double* d
     need(p, "sait_pair_spmv_factor");
     DeviceGuard g(p->dev);
     cudaStream_t s = sait::as_stream(stream);
-    const sait::DevCsr& m = which == 0 ? p->ml->m : p->mu->m;
-    const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
-    if (pair_variant() == 0) sait::spmv(m, d_x, d_y, s);
-    else sait::spmv_planned(m, pl, d_x, d_y, s);
+    factor_spmv(p, which != 0, d_x, d_y, s);
   });
 }
 
@@ -692,18 +698,29 @@ int sait_pair_apply_host(sait_pair_t p, const double* h_r, int64_t rlen, double*
 }
 
 namespace {
+// Row-major block product with one factor (fastest available kernel).
+void factor_spmm(sait_pair_t p, int which, const double* x, double* y, int nvec, cudaStream_t s) {
+  if (nvec == 1) {
+    factor_spmv(p, which, x, y, s);
+    return;
+  }
+  const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
+  if (pair_variant() == 2 && sm.ok() && sait::sell_spmm(sm, x, y, nvec, s)) return;
+  sait::spmm_rowmajor(which == 0 ? p->ml->m : p->mu->m, x, y, nvec, s);
+}
+
 // Column-major slab of w (1, 2, 4 or 8) vectors: transpose to row-major, run
 // the block SpMM pair (matrix read once per slab), transpose back.
-void apply_slab(const sait::DevCsr& L, const sait::DevCsr& U, const double* r_cm, double* z_cm, int64_t n, int w,
-                double* rt, double* y, double* zt, cudaStream_t s) {
+void apply_slab(sait_pair_t p, const double* r_cm, double* z_cm, int64_t n, int w, double* rt, double* y,
+                double* zt, cudaStream_t s) {
   if (w == 1) {
-    sait::spmv(L, r_cm, y, s);
-    sait::spmv(U, y, z_cm, s);
+    factor_spmv(p, 0, r_cm, y, s);
+    factor_spmv(p, 1, y, z_cm, s);
     return;
   }
   sait::transpose_block(r_cm, rt, n, w, true, s);
-  sait::spmm_rowmajor(L, rt, y, w, s);
-  sait::spmm_rowmajor(U, y, zt, w, s);
+  factor_spmm(p, 0, rt, y, w, s);
+  factor_spmm(p, 1, y, zt, w, s);
   sait::transpose_block(zt, z_cm, n, w, false, s);
 }
 
@@ -716,8 +733,8 @@ void apply_block_device(sait_pair_t p, const double* d_r, double* d_z, int64_t n
   if (nvec <= 0 || n == 0) return;
   if (layout == 1 && (nvec == 1 || nvec == 2 || nvec == 4 || nvec == 8)) {
     double* y = sait::dalloc<double>(L.nrows * nvec, s);
-    sait::spmm_rowmajor(L, d_r, y, static_cast<int>(nvec), s);
-    sait::spmm_rowmajor(U, y, d_z, static_cast<int>(nvec), s);
+    factor_spmm(p, 0, d_r, y, static_cast<int>(nvec), s);
+    factor_spmm(p, 1, y, d_z, static_cast<int>(nvec), s);
     sait::dfree(y, s);
     return;
   }
@@ -738,7 +755,7 @@ void apply_block_device(sait_pair_t p, const double* d_r, double* d_z, int64_t n
   for (int64_t c0 = 0; c0 < nvec;) {
     int64_t left = nvec - c0;
     int w = left >= 8 ? 8 : (left >= 4 ? 4 : (left >= 2 ? 2 : 1));
-    apply_slab(L, U, rcm + c0 * n, zcm + c0 * n, n, w, rt, y, zt, s);
+    apply_slab(p, rcm + c0 * n, zcm + c0 * n, n, w, rt, y, zt, s);
     c0 += w;
   }
   sait::dfree(y, s);
@@ -787,6 +804,8 @@ void sait_pair_destroy(sait_pair_t p) {
     cudaDeviceSynchronize();
     sait::free_spmv_plan(p->pl, nullptr);
     sait::free_spmv_plan(p->pu, nullptr);
+    sait::free_sell(p->sl, nullptr);
+    sait::free_sell(p->su, nullptr);
     for (auto& kv : p->ws) cudaFree(kv.second);
     cudaDeviceSynchronize();
     if (prev >= 0) cudaSetDevice(prev);

@@ -143,6 +143,18 @@ struct SpmvPlan {
 SpmvPlan make_spmv_plan(const DevCsr& a, cudaStream_t s);
 void free_spmv_plan(SpmvPlan& p, cudaStream_t s);
 void spmv_planned(const DevCsr& a, const SpmvPlan& p, const double* x, double* y, cudaStream_t s);
+// sell.cu
+struct SellMatrix {
+  int64_t n = 0, nslices = 0, padded = 0;
+  int64_t* soff = nullptr;  // nslices + 1 element offsets (multiples of 32)
+  int32_t* col = nullptr;   // -1 marks padding
+  double* val = nullptr;
+  bool ok() const { return soff != nullptr; }
+};
+SellMatrix make_sell(const DevCsr& a, cudaStream_t s);  // empty if too irregular
+void free_sell(SellMatrix& m, cudaStream_t s);
+void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
+bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s);  // row-major block
 void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
 void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaStream_t s);
 void transpose_block(const double* in, double* out, int64_t n, int nvec, bool to_rowmajor,

@@ -1,0 +1,258 @@
+// sell.cu — sliced-ELL (SELL-32) apply format for the SAIT factors.
+//
+// The apply reads each factor once per vector, so its speed is set by how the
+// CSR stream maps onto HBM.  For the stencil-derived SAIT factors rows are
+// almost uniform (C2: 97.7% of rows have exactly 7 entries; a 32-row slice
+// pads by 0.34%), so the pair keeps a SELL-32 copy built once at pair
+// creation: slice s stores its 32 rows column-major, width = the slice's
+// longest row, so lane j of a warp owns row 32 s + j and every load of the
+// slice is a coalesced 128 B (indices) / 256 B (values) warp transaction
+// straight into registers — no shared-memory staging, no block barriers.
+// x gathers of neighbouring rows are neighbouring too (stencil), hence
+// coalesced.  Each thread still sums its row in stored order without FMA, so
+// results stay bitwise equal to the reference's spmv (kernels.cpp:18-24);
+// padded slots carry col = -1 and are skipped (never multiplied), so a
+// non-finite x cannot leak into a row through padding.
+//
+// Rows too irregular for slicing (padding > kMaxPad) keep the CSR kernels.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sait {
+namespace {
+
+constexpr int kSlice = 32;
+constexpr double kMaxPad = 1.25;
+
+__device__ __forceinline__ int32_t ld_na(const int32_t* p) {
+  int32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_na(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+__global__ void slice_widths(int64_t n, const int32_t* __restrict__ rp, int64_t nslices, int64_t* __restrict__ width) {
+  int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  int64_t r0 = s * kSlice, r1 = r0 + kSlice < n ? r0 + kSlice : n;
+  int32_t w = 0;
+  for (int64_t r = r0; r < r1; ++r) w = max(w, rp[r + 1] - rp[r]);
+  width[s] = static_cast<int64_t>(w) * kSlice;
+}
+
+__global__ void scan_i64_inplace(int64_t* a, int64_t n) {  // single block, exclusive, a[n] = total
+  __shared__ int64_t carry_s;
+  __shared__ int64_t warp_tot[32];
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < n ? a[i] : 0, x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    int64_t before = 0, tot = 0;
+    for (int q = 0; q < nw; ++q) {
+      if (q < wid) before += warp_tot[q];
+      tot += warp_tot[q];
+    }
+    if (i < n) a[i] = carry_s + before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a[n] = carry_s;
+}
+
+__global__ void fill_sell(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const int64_t* __restrict__ soff,
+                          int32_t* __restrict__ scol, double* __restrict__ sval) {
+  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t s = r / kSlice;
+  int lane = static_cast<int>(r % kSlice);
+  int64_t nslices = (n + kSlice - 1) / kSlice;
+  if (s >= nslices) return;
+  int64_t base = soff[s];
+  int32_t w = static_cast<int32_t>((soff[s + 1] - base) / kSlice);
+  int32_t b = 0, len = 0;
+  if (r < n) {
+    b = rp[r];
+    len = rp[r + 1] - b;
+  }
+  for (int32_t k = 0; k < w; ++k) {
+    int64_t dst = base + static_cast<int64_t>(k) * kSlice + lane;
+    if (k < len) {
+      scol[dst] = ci[b + k];
+      sval[dst] = v[b + k];
+    } else {
+      scol[dst] = -1;
+      sval[dst] = 0.0;
+    }
+  }
+}
+
+// One warp per slice (grid-stride), lane = row.  Loads are batched 8 slots at
+// a time so each thread has 16 independent streaming loads and 8 gathers in
+// flight.
+__global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
+                                                         const int32_t* __restrict__ scol,
+                                                         const double* __restrict__ sval,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices;
+       s += warps) {
+    const int64_t base = soff[s];
+    const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+    const int32_t* cp = scol + base + lane;
+    const double* vp = sval + base + lane;
+    double acc = 0.0;
+    for (int32_t k0 = 0; k0 < w; k0 += 8) {
+      int32_t c[8];
+      double v[8], xv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = -1;
+        v[j] = 0.0;
+        if (k0 + j < w) {
+          c[j] = ld_na(cp + (k0 + j) * kSlice);
+          v[j] = ld_na(vp + (k0 + j) * kSlice);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+    }
+    const int64_t row = s * kSlice + lane;
+    if (row < n) y[row] = acc;
+  }
+}
+
+// Row-major block of NV vectors: lane = row, NV accumulators per thread; the
+// slice's indices/values are read once for all NV vectors.
+template <int NV>
+__global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
+                                                         const int32_t* __restrict__ scol,
+                                                         const double* __restrict__ sval,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices;
+       s += warps) {
+    const int64_t base = soff[s];
+    const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+    double acc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = 0.0;
+    for (int32_t k0 = 0; k0 < w; k0 += 4) {
+      int32_t col[4];
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        col[j] = -1;
+        v[j] = 0.0;
+        if (k0 + j < w) {
+          col[j] = ld_na(scol + base + (k0 + j) * kSlice + lane);
+          v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (col[j] < 0) continue;
+        const double2* xr = reinterpret_cast<const double2*>(x + static_cast<int64_t>(col[j]) * NV);
+#pragma unroll
+        for (int c = 0; c < NV / 2; ++c) {
+          const double2 xx = __ldg(xr + c);
+          acc[2 * c] = __dadd_rn(acc[2 * c], __dmul_rn(v[j], xx.x));
+          acc[2 * c + 1] = __dadd_rn(acc[2 * c + 1], __dmul_rn(v[j], xx.y));
+        }
+      }
+    }
+    const int64_t row = s * kSlice + lane;
+    if (row < n) {
+      double2* yr = reinterpret_cast<double2*>(y + row * NV);
+#pragma unroll
+      for (int c = 0; c < NV / 2; ++c) yr[c] = make_double2(acc[2 * c], acc[2 * c + 1]);
+    }
+  }
+}
+
+unsigned sell_grid(int64_t nslices) {
+  int64_t blocks = (nslices + 7) / 8;
+  int64_t cap = int64_t{num_sms()} * 8 * 4;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min(blocks, cap)));
+}
+
+}  // namespace
+
+SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
+  SellMatrix m;
+  m.n = a.nrows;
+  if (a.nrows == 0 || !a.v) return m;
+  m.nslices = (a.nrows + kSlice - 1) / kSlice;
+  m.soff = dalloc<int64_t>(m.nslices + 1, s);
+  slice_widths<<<grid_for(m.nslices, 256), 256, 0, s>>>(a.nrows, a.rp, m.nslices, m.soff);
+  SAIT_LAUNCHED();
+  scan_i64_inplace<<<1, 1024, 0, s>>>(m.soff, m.nslices);
+  SAIT_LAUNCHED();
+  SAIT_CUDA(cudaMemcpyAsync(&m.padded, m.soff + m.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  if (static_cast<double>(m.padded) > kMaxPad * static_cast<double>(std::max<int64_t>(a.nnz, 1)) + 64.0) {
+    dfree(m.soff, s);
+    return SellMatrix{};  // too irregular: keep the CSR kernels
+  }
+  m.col = dalloc<int32_t>(m.padded, s);
+  m.val = dalloc<double>(m.padded, s);
+  fill_sell<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.col, m.val);
+  SAIT_LAUNCHED();
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  return m;
+}
+
+void free_sell(SellMatrix& m, cudaStream_t s) {
+  dfree(m.soff, s);
+  dfree(m.col, s);
+  dfree(m.val, s);
+  m = SellMatrix{};
+}
+
+void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s) {
+  if (m.nslices == 0) return;
+  sell_spmv_kernel<<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+  SAIT_LAUNCHED();
+}
+
+bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s) {
+  if (m.nslices == 0) return true;
+  switch (nvec) {
+    case 1:
+      sell_spmv(m, x, y, s);
+      return true;
+    case 2:
+      sell_spmm_kernel<2><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+      break;
+    case 4:
+      sell_spmm_kernel<4><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+      break;
+    case 8:
+      sell_spmm_kernel<8><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+      break;
+    default:
+      return false;
+  }
+  SAIT_LAUNCHED();
+  return true;
+}
+
+}  // namespace sait

@@ -98,3 +98,49 @@ def test_apply_errors(S, c1_pair):
     b = S.CsrMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
     with pytest.raises(S.SaitInvalidArgument, match="SaitPairPreconditioner: factor shapes do not chain"):
         S.SaitPairPreconditioner(b, a)
+
+
+def _pair_from_scipy(S, lo, up):
+    return S.SaitPairPreconditioner(S.CsrMatrix.from_scipy(lo), S.CsrMatrix.from_scipy(up))
+
+
+def test_irregular_pair_falls_back_and_matches(S, port):
+    """A pair whose rows are too irregular for the SELL-32 copy (a few very
+    long rows) takes the CSR kernels; results stay bitwise equal."""
+    import scipy.sparse as sp
+
+    from helpers import to_oracle
+
+    rng = np.random.default_rng(3)
+    n = 3000
+    lo = sp.tril(sp.random(n, n, density=0.002, random_state=4), k=-1).tolil()
+    for i in (100, 2000, 2999):
+        lo[i, : i] = rng.standard_normal(i)
+    lo = (lo + sp.eye(n)).tocsr()
+    up = lo.T.tocsr()
+    pair = _pair_from_scipy(S, lo, up)
+    r = rng.standard_normal(n)
+    z = np.empty(n)
+    pair.apply(r, z)
+    L, U = S.CsrMatrix.from_scipy(lo), S.CsrMatrix.from_scipy(up)
+    assert bitwise_equal(z, port.pair_apply(to_oracle(L), to_oracle(U), r))
+    Z = pair.apply_block(np.stack([r, -r, 2 * r, r], axis=1))
+    assert bitwise_equal(Z[:, 0], z)
+
+
+def test_nonfinite_inputs_propagate_like_reference(S, golden, c1_pair, port):
+    """Padding slots of the sliced format are never multiplied: an Inf/NaN in
+    r reaches exactly the rows the reference reaches."""
+    from helpers import to_oracle
+
+    r = golden["c1/r"].copy()
+    r[17] = np.inf
+    r[2048] = np.nan
+    z = np.empty(4096)
+    c1_pair.apply(r, z)
+    ML = to_product(golden_csr(golden, "c1/ML"))
+    MU = to_product(golden_csr(golden, "c1/MU"))
+    ez = port.pair_apply(to_oracle(ML), to_oracle(MU), r)
+    assert np.array_equal(np.isnan(z), np.isnan(ez)) and np.array_equal(np.isinf(z), np.isinf(ez))
+    fin = np.isfinite(ez)
+    assert bitwise_equal(z[fin], ez[fin])

@@ -25,8 +25,13 @@ struct sait_pair_s {
   sait::SellMatrix sl, su;  // SELL-32 copies used by the apply (empty if irregular)
   // per-stream scratch (y = M_L r): applies on one stream are ordered, so one
   // buffer per stream honours the concurrent-apply contract
+  sait::PairPlan pp;        // fused single-launch pair (needs both SELL copies)
+  struct Work {
+    double* y = nullptr;
+    sait::PairState st;
+  };
   std::mutex mu_ws;
-  std::unordered_map<cudaStream_t, double*> ws;
+  std::unordered_map<cudaStream_t, Work> ws;
 };
 
 namespace sait {
@@ -601,6 +606,7 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
     p->pu = sait::make_spmv_plan(mu->m, nullptr);
     p->sl = sait::make_sell(ml->m, nullptr);
     p->su = sait::make_sell(mu->m, nullptr);
+    p->pp = sait::make_pair_plan(ml->m, p->sl, mu->m, p->su, nullptr);
     *out = p;
   });
 }
@@ -627,7 +633,7 @@ namespace {
 int pair_variant() {
   static int v = [] {
     const char* e = std::getenv("SAIT_PAIR");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 3;
   }();
   return v;
 }
@@ -638,19 +644,25 @@ void factor_spmv(sait_pair_t p, int which, const double* x, double* y, cudaStrea
   const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
   const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
   const int v = pair_variant();
-  if (v == 2 && sm.ok()) sait::sell_spmv(sm, x, y, s);
+  if (v >= 2 && sm.ok()) sait::sell_spmv(sm, x, y, s);
   else if (v == 1) sait::spmv_planned(m, pl, x, y, s);
   else sait::spmv(m, x, y, s);
 }
 
-double* pair_scratch(sait_pair_t p, cudaStream_t s, int64_t n) {
+sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(p->mu_ws);
   auto it = p->ws.find(s);
   if (it != p->ws.end()) return it->second;
-  void* buf = nullptr;
-  SAIT_CUDA(cudaMalloc(&buf, sizeof(double) * (n > 0 ? n : 1) + 256));
-  p->ws.emplace(s, static_cast<double*>(buf));
-  return static_cast<double*>(buf);
+  sait_pair_s::Work w;
+  const int64_t n = p->ml->m.nrows;
+  SAIT_CUDA(cudaMalloc(&w.y, sizeof(double) * (n > 0 ? n : 1) + 256));
+  const int64_t ng = std::max<int64_t>(p->pp.gL, 1);
+  SAIT_CUDA(cudaMalloc(&w.st.done, sizeof(int) * ng));
+  SAIT_CUDA(cudaMalloc(&w.st.counter, sizeof(unsigned long long)));
+  SAIT_CUDA(cudaMemset(w.st.done, 0, sizeof(int) * ng));
+  SAIT_CUDA(cudaMemset(w.st.counter, 0, sizeof(unsigned long long)));
+  SAIT_CUDA(cudaDeviceSynchronize());
+  return p->ws.emplace(s, w).first->second;
 }
 }  // namespace
 
@@ -667,9 +679,13 @@ int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z,
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
     cudaStream_t s = sait::as_stream(stream);
-    double* y = pair_scratch(p, s, L.nrows);
-    factor_spmv(p, 0, d_r, y, s);
-    factor_spmv(p, 1, y, d_z, s);
+    sait_pair_s::Work& w = pair_work(p, s);
+    if (pair_variant() == 3 && p->pp.ok()) {
+      sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, d_r, w.y, d_z, s);
+    } else {
+      factor_spmv(p, 0, d_r, w.y, s);
+      factor_spmv(p, 1, w.y, d_z, s);
+    }
   });
 }
 
@@ -705,7 +721,7 @@ void factor_spmm(sait_pair_t p, int which, const double* x, double* y, int nvec,
     return;
   }
   const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
-  if (pair_variant() == 2 && sm.ok() && sait::sell_spmm(sm, x, y, nvec, s)) return;
+  if (pair_variant() >= 2 && sm.ok() && sait::sell_spmm(sm, x, y, nvec, s)) return;
   sait::spmm_rowmajor(which == 0 ? p->ml->m : p->mu->m, x, y, nvec, s);
 }
 
@@ -806,7 +822,12 @@ void sait_pair_destroy(sait_pair_t p) {
     sait::free_spmv_plan(p->pu, nullptr);
     sait::free_sell(p->sl, nullptr);
     sait::free_sell(p->su, nullptr);
-    for (auto& kv : p->ws) cudaFree(kv.second);
+    sait::free_pair_plan(p->pp, nullptr);
+    for (auto& kv : p->ws) {
+      cudaFree(kv.second.y);
+      cudaFree(kv.second.st.done);
+      cudaFree(kv.second.st.counter);
+    }
     cudaDeviceSynchronize();
     if (prev >= 0) cudaSetDevice(prev);
   }

@@ -153,6 +153,25 @@ struct SellMatrix {
 };
 SellMatrix make_sell(const DevCsr& a, cudaStream_t s);  // empty if too irregular
 void free_sell(SellMatrix& m, cudaStream_t s);
+// fused persistent pair kernel (z = M_U (M_L r) in one launch)
+struct PairPlan {
+  int64_t gL = 0, gU = 0;  // 256-row groups of each factor
+  int32_t* dep_lo = nullptr;
+  int32_t* dep_hi = nullptr;
+  int grid = 0;
+  bool ok() const { return dep_lo != nullptr; }
+};
+struct PairState {  // per (pair, stream): flags + claim counter, ordered by the stream
+  int* done = nullptr;
+  unsigned long long* counter = nullptr;
+  unsigned long long claims = 0;
+  int epoch = 0;
+};
+PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
+                        cudaStream_t s);
+void free_pair_plan(PairPlan& p, cudaStream_t s);
+void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
+                     const double* r, double* y, double* z, cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
 bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s);  // row-major block
 void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);

@@ -188,10 +188,147 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
   }
 }
 
-unsigned sell_grid(int64_t nslices) {
-  int64_t blocks = (nslices + 7) / 8;
-  int64_t cap = int64_t{num_sms()} * 8 * 4;
-  return static_cast<unsigned>(std::max<int64_t>(1, std::min(blocks, cap)));
+unsigned sell_grid(int64_t nslices) {  // one slice per warp, 8 warps per CTA
+  return static_cast<unsigned>(std::max<int64_t>(1, (nslices + 7) / 8));
+}
+
+// ------------------------------------------------------------------ fused pair
+// z = M_U (M_L r) in ONE persistent launch.  Tasks are 256-row groups (8 slices,
+// one per warp): [0, gL) are M_L groups writing y, [gL, gL + gU) are M_U groups
+// reading y.  CTAs claim tasks in order from a counter, so every M_L group is
+// claimed before any M_U group and waiting never deadlocks.  A finished M_L
+// group publishes done[g] = epoch (release); an M_U group first issues its
+// own index/value loads, then checks (acquire) the flags of the y groups its
+// columns touch — precomputed per group — so the flag latency hides behind
+// the matrix stream, and reads y through L2 (ld.cg).
+constexpr int kGroupRows = 256;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_cg(const double* p) {
+  double r;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+struct PairArgs {
+  int64_t nL, nU;                 // rows of M_L (= len y) and M_U (= len z)
+  int64_t slicesL, slicesU, gL, gU;
+  const int64_t* soffL;
+  const int32_t* colL;
+  const double* valL;
+  const int64_t* soffU;
+  const int32_t* colU;
+  const double* valU;
+  const int32_t* dep_lo;          // per M_U group: first / last y group read
+  const int32_t* dep_hi;
+  const double* r;
+  double* y;
+  double* z;
+  int* done;
+  unsigned long long* counter;
+  unsigned long long base;
+  int epoch;
+};
+
+template <bool FROM_L2>
+__device__ __forceinline__ double slice_row(const int64_t* __restrict__ soff, const int32_t* __restrict__ scol,
+                                            const double* __restrict__ sval, int64_t s, int lane,
+                                            const double* __restrict__ x) {
+  const int64_t base = soff[s];
+  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  const int32_t* cp = scol + base + lane;
+  const double* vp = sval + base + lane;
+  double acc = 0.0;
+  for (int32_t k0 = 0; k0 < w; k0 += 8) {
+    int32_t c[8];
+    double v[8], xv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = -1;
+      v[j] = 0.0;
+      if (k0 + j < w) {
+        c[j] = ld_na(cp + (k0 + j) * kSlice);
+        v[j] = ld_na(vp + (k0 + j) * kSlice);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (FROM_L2) xv[j] = c[j] >= 0 ? ld_cg(x + c[j]) : 0.0;
+      else xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) sell_pair_kernel(PairArgs a) {
+  __shared__ long long task_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long total = a.gL + a.gU;
+  while (true) {
+    if (threadIdx.x == 0) task_s = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
+    __syncthreads();
+    const long long t = task_s;
+    __syncthreads();
+    if (t >= total) break;
+    if (t < a.gL) {
+      const int64_t s = t * 8 + warp;
+      if (s < a.slicesL) {
+        const double acc = slice_row<false>(a.soffL, a.colL, a.valL, s, lane, a.r);
+        const int64_t row = s * kSlice + lane;
+        if (row < a.nL) a.y[row] = acc;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(a.done + t, a.epoch);
+      }
+    } else {
+      const int64_t g = t - a.gL;
+      const int32_t lo = a.dep_lo[g], hi = a.dep_hi[g];
+      bool ok;
+      do {
+        ok = true;
+        for (int32_t k = lo + static_cast<int32_t>(threadIdx.x); k <= hi; k += blockDim.x)
+          ok = ok && ld_acquire(a.done + k) == a.epoch;
+        ok = __syncthreads_and(ok);
+        if (!ok) __nanosleep(64);
+      } while (!ok);
+      const int64_t s = g * 8 + warp;
+      if (s < a.slicesU) {
+        const double acc = slice_row<true>(a.soffU, a.colU, a.valU, s, lane, a.y);
+        const int64_t row = s * kSlice + lane;
+        if (row < a.nU) a.z[row] = acc;
+      }
+    }
+  }
+}
+
+// dep_lo/hi[g] = y-group range touched by the columns of M_U's group g.
+__global__ void pair_deps(int64_t nU, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          int64_t gU, int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
+  int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= gU) return;
+  int64_t r0 = g * kGroupRows, r1 = r0 + kGroupRows < nU ? r0 + kGroupRows : nU;
+  int32_t mn = INT32_MAX, mx = -1;
+  for (int64_t r = r0; r < r1; ++r) {
+    int32_t b = rp[r], e = rp[r + 1];
+    if (b < e) {
+      mn = min(mn, ci[b]);
+      mx = max(mx, ci[e - 1]);
+    }
+  }
+  lo[g] = mx < 0 ? 1 : mn / kGroupRows;
+  hi[g] = mx < 0 ? 0 : mx / kGroupRows;
 }
 
 }  // namespace
@@ -218,6 +355,61 @@ SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
   SAIT_LAUNCHED();
   SAIT_CUDA(cudaStreamSynchronize(s));
   return m;
+}
+
+PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
+                        cudaStream_t s) {
+  PairPlan p;
+  if (!sl.ok() || !su.ok()) return p;
+  p.gL = (L.nrows + kGroupRows - 1) / kGroupRows;
+  p.gU = (U.nrows + kGroupRows - 1) / kGroupRows;
+  p.dep_lo = dalloc<int32_t>(p.gU, s);
+  p.dep_hi = dalloc<int32_t>(p.gU, s);
+  if (p.gU) {
+    pair_deps<<<grid_for(p.gU, 128), 128, 0, s>>>(U.nrows, U.rp, U.ci, p.gU, p.dep_lo, p.dep_hi);
+    SAIT_LAUNCHED();
+  }
+  int per_sm = 0;
+  SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_pair_kernel, 256, 0));
+  p.grid = std::max(1, per_sm) * num_sms();
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  return p;
+}
+
+void free_pair_plan(PairPlan& p, cudaStream_t s) {
+  dfree(p.dep_lo, s);
+  dfree(p.dep_hi, s);
+  p = PairPlan{};
+}
+
+void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
+                     const double* r, double* y, double* z, cudaStream_t s) {
+  PairArgs a;
+  a.nL = sl.n;
+  a.nU = su.n;
+  a.slicesL = sl.nslices;
+  a.slicesU = su.nslices;
+  a.gL = pp.gL;
+  a.gU = pp.gU;
+  a.soffL = sl.soff;
+  a.colL = sl.col;
+  a.valL = sl.val;
+  a.soffU = su.soff;
+  a.colU = su.col;
+  a.valU = su.val;
+  a.dep_lo = pp.dep_lo;
+  a.dep_hi = pp.dep_hi;
+  a.r = r;
+  a.y = y;
+  a.z = z;
+  a.done = st.done;
+  a.counter = st.counter;
+  const unsigned grid = static_cast<unsigned>(pp.grid);
+  a.base = st.claims;
+  a.epoch = ++st.epoch;
+  st.claims += static_cast<unsigned long long>(pp.gL + pp.gU) + grid;
+  sell_pair_kernel<<<grid, 256, 0, s>>>(a);
+  SAIT_LAUNCHED();
 }
 
 void free_sell(SellMatrix& m, cudaStream_t s) {

@@ -271,15 +271,20 @@ __device__ __forceinline__ double slice_row(const int64_t* __restrict__ soff, co
 }
 
 __global__ void __launch_bounds__(256) sell_pair_kernel(PairArgs a) {
-  __shared__ long long task_s;
+  // the next task is claimed while the current one runs (its atomic latency
+  // hides behind the matrix stream); claim order stays global, so an M_L task
+  // is never queued behind an M_U task on the same CTA.
+  __shared__ long long task_s[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long total = a.gL + a.gU;
+  if (threadIdx.x == 0) task_s[0] = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
+  __syncthreads();
+  int buf = 0;
   while (true) {
-    if (threadIdx.x == 0) task_s = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
-    __syncthreads();
-    const long long t = task_s;
-    __syncthreads();
+    const long long t = task_s[buf];
     if (t >= total) break;
+    unsigned long long nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(a.counter, 1ull);
     if (t < a.gL) {
       const int64_t s = t * 8 + warp;
       if (s < a.slicesL) {
@@ -310,6 +315,9 @@ __global__ void __launch_bounds__(256) sell_pair_kernel(PairArgs a) {
         if (row < a.nU) a.z[row] = acc;
       }
     }
+    if (threadIdx.x == 0) task_s[buf ^ 1] = static_cast<long long>(nxt - a.base);
+    __syncthreads();
+    buf ^= 1;
   }
 }
 

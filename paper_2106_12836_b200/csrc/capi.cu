@@ -29,7 +29,16 @@ struct sait_pair_s {
   struct Work {
     double* y = nullptr;
     sait::PairState st;
+    // host-vector pipeline (lazily created)
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    double *r_dev = nullptr, *z_dev = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_u;
+    cudaEvent_t ev_entry = nullptr, ev_out_done = nullptr;
   };
+  // chunking of the host-vector apply: row boundaries (multiples of 256) and,
+  // per chunk, the last r-chunk M_L needs and the last y-chunk M_U needs
+  std::vector<int64_t> chunk_rows;
+  std::vector<int32_t> needL_hi, needU_hi;
   std::mutex mu_ws;
   std::unordered_map<cudaStream_t, Work> ws;
 };
@@ -251,6 +260,42 @@ void check_spec(const sait_drop_spec* spec) {
       break;
     default:
       sait::throw_invalid("sait_build: unknown drop kind " + std::to_string(spec->kind));
+  }
+}
+
+// Chunking of the host-vector apply (see pair_apply_host_chunked).
+void plan_host_chunks(sait_pair_t p) {
+  const sait::DevCsr& L = p->ml->m;
+  const sait::DevCsr& U = p->mu->m;
+  p->chunk_rows.clear();
+  const int64_t n = L.nrows;
+  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 16) || !p->sl.ok() || !p->su.ok())
+    return;  // small or non-square pairs: one-shot path
+  const int64_t G = sait::kDepGroupRows;
+  const int64_t ng = (n + G - 1) / G;
+  // ~1 MB of r per chunk: long enough for full PCIe rate, short enough to overlap
+  int64_t rows = std::max<int64_t>(G, ((int64_t{1} << 17) + G - 1) / G * G);
+  const int64_t k = (n + rows - 1) / rows;
+  std::vector<int32_t> llo(ng), lhi(ng), ulo(ng), uhi(ng);
+  int32_t* d = sait::dalloc<int32_t>(4 * ng, nullptr);
+  sait::column_group_deps(L, d, d + ng, nullptr);
+  sait::column_group_deps(U, d + 2 * ng, d + 3 * ng, nullptr);
+  SAIT_CUDA(cudaMemcpy(lhi.data(), d + ng, sizeof(int32_t) * ng, cudaMemcpyDeviceToHost));
+  SAIT_CUDA(cudaMemcpy(uhi.data(), d + 3 * ng, sizeof(int32_t) * ng, cudaMemcpyDeviceToHost));
+  sait::dfree(d, nullptr);
+  SAIT_CUDA(cudaDeviceSynchronize());
+  const int64_t gpc = rows / G;  // groups per chunk
+  for (int64_t c = 0; c <= k; ++c) p->chunk_rows.push_back(std::min(n, c * rows));
+  p->needL_hi.assign(k, 0);
+  p->needU_hi.assign(k, 0);
+  for (int64_t g = 0; g < ng; ++g) {
+    const int64_t c = g / gpc;
+    if (lhi[g] >= 0) p->needL_hi[c] = std::max<int32_t>(p->needL_hi[c], static_cast<int32_t>(lhi[g] / gpc));
+    if (uhi[g] >= 0) p->needU_hi[c] = std::max<int32_t>(p->needU_hi[c], static_cast<int32_t>(uhi[g] / gpc));
+  }
+  for (int64_t c = 1; c < k; ++c) {  // launch order is monotone in the chunk index
+    p->needL_hi[c] = std::max(p->needL_hi[c], p->needL_hi[c - 1]);
+    p->needU_hi[c] = std::max(p->needU_hi[c], p->needU_hi[c - 1]);
   }
 }
 
@@ -607,6 +652,7 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
     p->sl = sait::make_sell(ml->m, nullptr);
     p->su = sait::make_sell(mu->m, nullptr);
     p->pp = sait::make_pair_plan(ml->m, p->sl, mu->m, p->su, nullptr);
+    plan_host_chunks(p);
     *out = p;
   });
 }
@@ -633,7 +679,7 @@ namespace {
 int pair_variant() {
   static int v = [] {
     const char* e = std::getenv("SAIT_PAIR");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 2;
   }();
   return v;
 }
@@ -664,6 +710,56 @@ sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
   SAIT_CUDA(cudaDeviceSynchronize());
   return p->ws.emplace(s, w).first->second;
 }
+// z = M_U (M_L r) for HOST r/z, overlapping the PCIe copies with the two
+// SpMVs chunk by chunk: r chunks stream in on s_in; M_L chunk c runs as soon as
+// the r chunks its columns reach have landed; M_U chunk c runs once the y
+// chunks it reads exist (bounded bandwidth of the triangular factors), and its
+// z chunk streams out on s_out while later r chunks are still arriving.
+void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cudaStream_t s) {
+  sait_pair_s::Work& w = pair_work(p, s);
+  const int64_t k = static_cast<int64_t>(p->chunk_rows.size()) - 1;
+  const int64_t n = p->ml->m.nrows;
+  if (!w.s_in) {
+    SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_in, cudaStreamNonBlocking));
+    SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_out, cudaStreamNonBlocking));
+    SAIT_CUDA(cudaMalloc(&w.r_dev, sizeof(double) * n + 256));
+    SAIT_CUDA(cudaMalloc(&w.z_dev, sizeof(double) * n + 256));
+    w.ev_in.resize(k);
+    w.ev_u.resize(k);
+    for (auto& e : w.ev_in) SAIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : w.ev_u) SAIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_entry, cudaEventDisableTiming));
+    SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_out_done, cudaEventDisableTiming));
+  }
+  // order the side streams after whatever the caller queued on s
+  SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
+  SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_entry, 0));
+  SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_entry, 0));
+  const auto& b = p->chunk_rows;
+  for (int64_t c = 0; c < k; ++c) {
+    SAIT_CUDA(cudaMemcpyAsync(w.r_dev + b[c], h_r + b[c], sizeof(double) * (b[c + 1] - b[c]), cudaMemcpyHostToDevice,
+                              w.s_in));
+    SAIT_CUDA(cudaEventRecord(w.ev_in[c], w.s_in));
+  }
+  int64_t u = 0;
+  auto launch_u = [&](int64_t uc) {
+    sait::sell_spmv_rows(p->su, b[uc], b[uc + 1], w.y, w.z_dev, s);
+    SAIT_CUDA(cudaEventRecord(w.ev_u[uc], s));
+    SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_u[uc], 0));
+    SAIT_CUDA(cudaMemcpyAsync(h_z + b[uc], w.z_dev + b[uc], sizeof(double) * (b[uc + 1] - b[uc]),
+                              cudaMemcpyDeviceToHost, w.s_out));
+  };
+  for (int64_t c = 0; c < k; ++c) {
+    SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_in[p->needL_hi[c]], 0));
+    sait::sell_spmv_rows(p->sl, b[c], b[c + 1], w.r_dev, w.y, s);
+    while (u < k && p->needU_hi[u] <= c) launch_u(u++);
+  }
+  while (u < k) launch_u(u++);
+  SAIT_CUDA(cudaEventRecord(w.ev_out_done, w.s_out));
+  SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_out_done, 0));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace
 
 extern "C" {
@@ -709,7 +805,8 @@ int sait_pair_apply_host(sait_pair_t p, const double* h_r, int64_t rlen, double*
                           std::to_string(L.ncols));
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
-    sait::pair_apply_host_pipelined(L, U, h_r, h_z, sait::as_stream(stream));
+    if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, sait::as_stream(stream));
+    else sait::pair_apply_host_pipelined(L, U, h_r, h_z, sait::as_stream(stream));
   });
 }
 
@@ -824,9 +921,18 @@ void sait_pair_destroy(sait_pair_t p) {
     sait::free_sell(p->su, nullptr);
     sait::free_pair_plan(p->pp, nullptr);
     for (auto& kv : p->ws) {
-      cudaFree(kv.second.y);
-      cudaFree(kv.second.st.done);
-      cudaFree(kv.second.st.counter);
+      auto& w = kv.second;
+      cudaFree(w.y);
+      cudaFree(w.st.done);
+      cudaFree(w.st.counter);
+      if (w.r_dev) cudaFree(w.r_dev);
+      if (w.z_dev) cudaFree(w.z_dev);
+      for (auto e : w.ev_in) cudaEventDestroy(e);
+      for (auto e : w.ev_u) cudaEventDestroy(e);
+      if (w.ev_entry) cudaEventDestroy(w.ev_entry);
+      if (w.ev_out_done) cudaEventDestroy(w.ev_out_done);
+      if (w.s_in) cudaStreamDestroy(w.s_in);
+      if (w.s_out) cudaStreamDestroy(w.s_out);
     }
     cudaDeviceSynchronize();
     if (prev >= 0) cudaSetDevice(prev);

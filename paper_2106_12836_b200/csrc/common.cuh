@@ -167,12 +167,17 @@ struct PairState {  // per (pair, stream): flags + claim counter, ordered by the
   unsigned long long claims = 0;
   int epoch = 0;
 };
+// per 256-row group g of m: [lo[g], hi[g]] = 256-column groups its entries touch
+void column_group_deps(const DevCsr& m, int32_t* lo, int32_t* hi, cudaStream_t s);
+constexpr int64_t kDepGroupRows = 256;
 PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
                         cudaStream_t s);
 void free_pair_plan(PairPlan& p, cudaStream_t s);
 void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
                      const double* r, double* y, double* z, cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
+// rows [row0, row1) only (row0 a multiple of 32)
+void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s);
 bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s);  // row-major block
 void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
 void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaStream_t s);

@@ -103,14 +103,15 @@ __global__ void fill_sell(int64_t n, const int32_t* __restrict__ rp, const int32
 // One warp per slice (grid-stride), lane = row.  Loads are batched 8 slots at
 // a time so each thread has 16 independent streaming loads and 8 gathers in
 // flight.
-__global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
+__global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_begin, int64_t nslices,
+                                                         const int64_t* __restrict__ soff,
                                                          const int32_t* __restrict__ scol,
                                                          const double* __restrict__ sval,
                                                          const double* __restrict__ x, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices;
-       s += warps) {
+  for (int64_t s = s_begin + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       s < nslices; s += warps) {
     const int64_t base = soff[s];
     const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
     const int32_t* cp = scol + base + lane;
@@ -321,7 +322,9 @@ __global__ void __launch_bounds__(256) sell_pair_kernel(PairArgs a) {
   }
 }
 
-// dep_lo/hi[g] = y-group range touched by the columns of M_U's group g.
+}  // namespace
+
+// lo/hi[g] = column-group range touched by the rows of group g (256 rows).
 __global__ void pair_deps(int64_t nU, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           int64_t gU, int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
   int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -338,6 +341,15 @@ __global__ void pair_deps(int64_t nU, const int32_t* __restrict__ rp, const int3
   lo[g] = mx < 0 ? 1 : mn / kGroupRows;
   hi[g] = mx < 0 ? 0 : mx / kGroupRows;
 }
+
+void column_group_deps(const DevCsr& m, int32_t* lo, int32_t* hi, cudaStream_t s) {
+  const int64_t g = (m.nrows + kGroupRows - 1) / kGroupRows;
+  if (g == 0) return;
+  pair_deps<<<grid_for(g, 128), 128, 0, s>>>(m.nrows, m.rp, m.ci, g, lo, hi);
+  SAIT_LAUNCHED();
+}
+
+namespace {
 
 }  // namespace
 
@@ -429,7 +441,14 @@ void free_sell(SellMatrix& m, cudaStream_t s) {
 
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s) {
   if (m.nslices == 0) return;
-  sell_spmv_kernel<<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+  sell_spmv_kernel<<<sell_grid(m.nslices), 256, 0, s>>>(m.n, 0, m.nslices, m.soff, m.col, m.val, x, y);
+  SAIT_LAUNCHED();
+}
+
+void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s) {
+  const int64_t s0 = row0 / kSlice, s1 = std::min<int64_t>((row1 + kSlice - 1) / kSlice, m.nslices);
+  if (s1 <= s0) return;
+  sell_spmv_kernel<<<sell_grid(s1 - s0), 256, 0, s>>>(m.n, s0, s1, m.soff, m.col, m.val, x, y);
   SAIT_LAUNCHED();
 }
 

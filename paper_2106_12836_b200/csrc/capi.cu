@@ -1,6 +1,7 @@
 // capi.cu — the C ABI of include/sait_c.h over the device kernels.
 // Each entry point cites the reference interface it replaces (paths relative
 // to /root/reference/proj/core/).
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -37,8 +38,8 @@ struct sait_pair_s {
   };
   // chunking of the host-vector apply: row boundaries (multiples of 256) and,
   // per chunk, the last r-chunk M_L needs and the last y-chunk M_U needs
-  std::vector<int64_t> chunk_rows;
-  std::vector<int32_t> needL_hi, needU_hi;
+  std::vector<int64_t> chunk_rows, u_rows;
+  std::vector<int32_t> needL_hi;
   std::mutex mu_ws;
   std::unordered_map<cudaStream_t, Work> ws;
 };
@@ -268,15 +269,16 @@ void plan_host_chunks(sait_pair_t p) {
   const sait::DevCsr& L = p->ml->m;
   const sait::DevCsr& U = p->mu->m;
   p->chunk_rows.clear();
+  p->u_rows.clear();
   const int64_t n = L.nrows;
-  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 16) || !p->sl.ok() || !p->su.ok())
+  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 17) || !p->sl.ok() || !p->su.ok())
     return;  // small or non-square pairs: one-shot path
   const int64_t G = sait::kDepGroupRows;
   const int64_t ng = (n + G - 1) / G;
-  // ~1 MB of r per chunk: long enough for full PCIe rate, short enough to overlap
-  int64_t rows = std::max<int64_t>(G, ((int64_t{1} << 17) + G - 1) / G * G);
-  const int64_t k = (n + rows - 1) / rows;
-  std::vector<int32_t> llo(ng), lhi(ng), ulo(ng), uhi(ng);
+  // ~4 MB copies: on PCIe5 smaller async copies lose H2D/D2H concurrency
+  const int64_t k = std::max<int64_t>(2, (n * 8 + (int64_t{4} << 20) - 1) / (int64_t{4} << 20));
+  const int64_t rows = ((n + k - 1) / k + G - 1) / G * G;
+  std::vector<int32_t> lhi(ng), uhi(ng);
   int32_t* d = sait::dalloc<int32_t>(4 * ng, nullptr);
   sait::column_group_deps(L, d, d + ng, nullptr);
   sait::column_group_deps(U, d + 2 * ng, d + 3 * ng, nullptr);
@@ -284,18 +286,23 @@ void plan_host_chunks(sait_pair_t p) {
   SAIT_CUDA(cudaMemcpy(uhi.data(), d + 3 * ng, sizeof(int32_t) * ng, cudaMemcpyDeviceToHost));
   sait::dfree(d, nullptr);
   SAIT_CUDA(cudaDeviceSynchronize());
-  const int64_t gpc = rows / G;  // groups per chunk
-  for (int64_t c = 0; c <= k; ++c) p->chunk_rows.push_back(std::min(n, c * rows));
-  p->needL_hi.assign(k, 0);
-  p->needU_hi.assign(k, 0);
-  for (int64_t g = 0; g < ng; ++g) {
-    const int64_t c = g / gpc;
-    if (lhi[g] >= 0) p->needL_hi[c] = std::max<int32_t>(p->needL_hi[c], static_cast<int32_t>(lhi[g] / gpc));
-    if (uhi[g] >= 0) p->needU_hi[c] = std::max<int32_t>(p->needU_hi[c], static_cast<int32_t>(uhi[g] / gpc));
-  }
-  for (int64_t c = 1; c < k; ++c) {  // launch order is monotone in the chunk index
-    p->needL_hi[c] = std::max(p->needL_hi[c], p->needL_hi[c - 1]);
-    p->needU_hi[c] = std::max(p->needU_hi[c], p->needU_hi[c - 1]);
+  const int64_t nk = (n + rows - 1) / rows;
+  for (int64_t c = 0; c <= nk; ++c) p->chunk_rows.push_back(std::min(n, c * rows));
+  const int64_t gpc = rows / G;
+  p->needL_hi.assign(nk, 0);
+  for (int64_t g = 0; g < ng; ++g)
+    if (lhi[g] >= 0)
+      p->needL_hi[g / gpc] = std::max<int32_t>(p->needL_hi[g / gpc], static_cast<int32_t>(lhi[g] / gpc));
+  for (int64_t c = 1; c < nk; ++c) p->needL_hi[c] = std::max(p->needL_hi[c], p->needL_hi[c - 1]);
+  // M_U chunk c = the rows whose y reads end below chunk boundary c+1, so it
+  // can run (and its z leave) as soon as M_L chunk c is done.
+  p->u_rows.assign(nk + 1, n);
+  p->u_rows[0] = 0;
+  int64_t g = 0, run = -1;
+  for (int64_t c = 0; c + 1 < nk; ++c) {
+    const int64_t bound_group = p->chunk_rows[c + 1] / G;  // y groups < bound are complete
+    while (g < ng && std::max<int64_t>(run, uhi[g]) < bound_group) run = std::max<int64_t>(run, uhi[g++]);
+    p->u_rows[c + 1] = std::max(p->u_rows[c], std::min(n, g * G));
   }
 }
 
@@ -320,6 +327,54 @@ void sait_host_csr_free(sait_host_csr* m) {
 }
 
 int64_t sait_kernel_launch_count(void) { return sait::g_launches.load(); }
+
+// Diagnostics: seconds for H2D alone / D2H alone / both on two streams.
+void sait_debug_copy_probe(const double* h_src, double* h_dst, int64_t n, int chunks, double* out3) {
+  double *a = nullptr, *b = nullptr;
+  cudaMalloc(&a, n * 8);
+  cudaMalloc(&b, n * 8);
+  cudaStream_t s1, s2;
+  cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+  auto run = [&](bool up, bool down) {
+    cudaDeviceSynchronize();
+    auto t0 = std::chrono::steady_clock::now();
+    int64_t step = (n + std::abs(chunks) - 1) / std::abs(chunks);
+    if (chunks > 0) {
+      for (int64_t o = 0; o < n; o += step) {
+        int64_t m = std::min(step, n - o);
+        if (up) cudaMemcpyAsync(a + o, h_src + o, m * 8, cudaMemcpyHostToDevice, s1);
+        if (down) cudaMemcpyAsync(h_dst + o, b + o, m * 8, cudaMemcpyDeviceToHost, s2);
+      }
+    } else {
+      for (int64_t o = 0; up && o < n; o += step)
+        cudaMemcpyAsync(a + o, h_src + o, std::min(step, n - o) * 8, cudaMemcpyHostToDevice, s1);
+      for (int64_t o = 0; down && o < n; o += step)
+        cudaMemcpyAsync(h_dst + o, b + o, std::min(step, n - o) * 8, cudaMemcpyDeviceToHost, s2);
+    }
+    cudaDeviceSynchronize();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  run(true, true);
+  out3[0] = run(true, false);
+  out3[1] = run(false, true);
+  out3[2] = run(true, true);
+  cudaStreamDestroy(s1);
+  cudaStreamDestroy(s2);
+  cudaFree(a);
+  cudaFree(b);
+}
+
+// Diagnostics (not part of sait_c.h): memory type of a pointer as this
+// library's runtime sees it (0 unregistered, 1 host/pinned, 2 device, 3 managed).
+int sait_debug_pointer_type(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return static_cast<int>(a.type);
+}
 
 int sait_device_synchronize(void) {
   return guarded([] { SAIT_CUDA(cudaDeviceSynchronize()); });
@@ -731,6 +786,16 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
     SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_entry, cudaEventDisableTiming));
     SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_out_done, cudaEventDisableTiming));
   }
+  static const bool dbg = std::getenv("SAIT_DEBUG_PIPE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  auto mark = [&](const std::string& nm, cudaStream_t st) {
+    if (!dbg) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.emplace_back(nm, e);
+  };
+  mark("start", s);
   // order the side streams after whatever the caller queued on s
   SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
   SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_entry, 0));
@@ -740,24 +805,36 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
     SAIT_CUDA(cudaMemcpyAsync(w.r_dev + b[c], h_r + b[c], sizeof(double) * (b[c + 1] - b[c]), cudaMemcpyHostToDevice,
                               w.s_in));
     SAIT_CUDA(cudaEventRecord(w.ev_in[c], w.s_in));
+    mark("h2d" + std::to_string(c), w.s_in);
   }
-  int64_t u = 0;
-  auto launch_u = [&](int64_t uc) {
-    sait::sell_spmv_rows(p->su, b[uc], b[uc + 1], w.y, w.z_dev, s);
-    SAIT_CUDA(cudaEventRecord(w.ev_u[uc], s));
-    SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_u[uc], 0));
-    SAIT_CUDA(cudaMemcpyAsync(h_z + b[uc], w.z_dev + b[uc], sizeof(double) * (b[uc + 1] - b[uc]),
-                              cudaMemcpyDeviceToHost, w.s_out));
-  };
+  const auto& ub = p->u_rows;
   for (int64_t c = 0; c < k; ++c) {
     SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_in[p->needL_hi[c]], 0));
     sait::sell_spmv_rows(p->sl, b[c], b[c + 1], w.r_dev, w.y, s);
-    while (u < k && p->needU_hi[u] <= c) launch_u(u++);
+    mark("L" + std::to_string(c), s);
+    if (ub[c + 1] > ub[c]) {
+      sait::sell_spmv_rows(p->su, ub[c], ub[c + 1], w.y, w.z_dev, s);
+      SAIT_CUDA(cudaEventRecord(w.ev_u[c], s));
+      mark("U" + std::to_string(c), s);
+      SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_u[c], 0));
+      SAIT_CUDA(cudaMemcpyAsync(h_z + ub[c], w.z_dev + ub[c], sizeof(double) * (ub[c + 1] - ub[c]),
+                                cudaMemcpyDeviceToHost, w.s_out));
+      mark("d2h" + std::to_string(c), w.s_out);
+    }
   }
-  while (u < k) launch_u(u++);
   SAIT_CUDA(cudaEventRecord(w.ev_out_done, w.s_out));
   SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_out_done, 0));
+  mark("end", s);
   SAIT_CUDA(cudaStreamSynchronize(s));
+  if (dbg) {
+    for (auto& m : marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, marks[0].second, m.second);
+      std::fprintf(stderr, "%s=%.1f ", m.first.c_str(), ms * 1000.f);
+      cudaEventDestroy(m.second);
+    }
+    std::fprintf(stderr, "\n");
+  }
 }
 
 }  // namespace

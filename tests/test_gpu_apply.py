@@ -148,12 +148,12 @@ def test_nonfinite_inputs_propagate_like_reference(S, golden, c1_pair, port):
 
 def test_chunked_host_apply_3d(S, port):
     """Host-vector apply on a pair large enough for the chunked PCIe pipeline
-    (n = 48^3): bitwise equal to the device-vector apply and the oracle."""
+    (n = 64^3, two chunks): bitwise equal to the device-vector apply and the oracle."""
     import torch
 
     from helpers import to_oracle
 
-    A = S.laplacian_3d(48)
+    A = S.laplacian_3d(64)
     f = S.ilu_k(A, 0)
     ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
     MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))

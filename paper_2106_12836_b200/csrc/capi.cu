@@ -3,6 +3,7 @@
 // to /root/reference/proj/core/).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -275,9 +276,14 @@ void plan_host_chunks(sait_pair_t p) {
     return;  // small or non-square pairs: one-shot path
   const int64_t G = sait::kDepGroupRows;
   const int64_t ng = (n + G - 1) / G;
-  // ~4 MB copies: on PCIe5 smaller async copies lose H2D/D2H concurrency
-  const int64_t k = std::max<int64_t>(2, (n * 8 + (int64_t{4} << 20) - 1) / (int64_t{4} << 20));
-  const int64_t rows = ((n + k - 1) / k + G - 1) / G * G;
+  // Copy sizes: a short first chunk starts the z stream early, a short last
+  // chunk keeps the drain short, ~4 MB in between (on PCIe5, async copies
+  // much smaller than that lose H2D/D2H concurrency).
+  double mb_first = 2.0, mb_mid = 4.0, mb_last = 1.0;
+  if (const char* e = std::getenv("SAIT_PIPE_MB")) std::sscanf(e, "%lf,%lf,%lf", &mb_first, &mb_mid, &mb_last);
+  auto rows_of = [&](double mb) {
+    return std::max<int64_t>(G, static_cast<int64_t>(mb * (1 << 20) / 8.0) / G * G);
+  };
   std::vector<int32_t> lhi(ng), uhi(ng);
   int32_t* d = sait::dalloc<int32_t>(4 * ng, nullptr);
   sait::column_group_deps(L, d, d + ng, nullptr);
@@ -286,13 +292,29 @@ void plan_host_chunks(sait_pair_t p) {
   SAIT_CUDA(cudaMemcpy(uhi.data(), d + 3 * ng, sizeof(int32_t) * ng, cudaMemcpyDeviceToHost));
   sait::dfree(d, nullptr);
   SAIT_CUDA(cudaDeviceSynchronize());
-  const int64_t nk = (n + rows - 1) / rows;
-  for (int64_t c = 0; c <= nk; ++c) p->chunk_rows.push_back(std::min(n, c * rows));
-  const int64_t gpc = rows / G;
+  {
+    const int64_t rf = rows_of(mb_first), rm = rows_of(mb_mid), rl = rows_of(mb_last);
+    std::vector<int64_t>& b = p->chunk_rows;
+    b.push_back(0);
+    if (n > rf + rl) {
+      b.push_back(rf);
+      const int64_t mid = n - rf - rl;
+      const int64_t km = std::max<int64_t>(1, (mid + rm / 2) / rm);
+      const int64_t step = (mid / km + G - 1) / G * G;
+      for (int64_t c = 1; c < km; ++c) b.push_back(rf + c * step);
+      b.push_back(n - rl);
+    }
+    b.push_back(n);
+  }
+  const int64_t nk = static_cast<int64_t>(p->chunk_rows.size()) - 1;
+  std::vector<int32_t> chunk_of_group(ng + 1);
+  for (int64_t c = 0, g2 = 0; c < nk; ++c)
+    for (; g2 < ng && g2 * G < p->chunk_rows[c + 1]; ++g2) chunk_of_group[g2] = static_cast<int32_t>(c);
   p->needL_hi.assign(nk, 0);
-  for (int64_t g = 0; g < ng; ++g)
-    if (lhi[g] >= 0)
-      p->needL_hi[g / gpc] = std::max<int32_t>(p->needL_hi[g / gpc], static_cast<int32_t>(lhi[g] / gpc));
+  for (int64_t g2 = 0; g2 < ng; ++g2)
+    if (lhi[g2] >= 0)
+      p->needL_hi[chunk_of_group[g2]] =
+          std::max<int32_t>(p->needL_hi[chunk_of_group[g2]], chunk_of_group[std::min<int64_t>(lhi[g2], ng - 1)]);
   for (int64_t c = 1; c < nk; ++c) p->needL_hi[c] = std::max(p->needL_hi[c], p->needL_hi[c - 1]);
   // M_U chunk c = the rows whose y reads end below chunk boundary c+1, so it
   // can run (and its z leave) as soon as M_L chunk c is done.
@@ -791,10 +813,11 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
   auto mark = [&](const std::string& nm, cudaStream_t st) {
     if (!dbg) return;
     cudaEvent_t e;
-    cudaEventCreate(&e);
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEventRecord(e, st);
     marks.emplace_back(nm, e);
   };
+  const auto t_enq = std::chrono::steady_clock::now();
   mark("start", s);
   // order the side streams after whatever the caller queued on s
   SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
@@ -825,16 +848,25 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
   SAIT_CUDA(cudaEventRecord(w.ev_out_done, w.s_out));
   SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_out_done, 0));
   mark("end", s);
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  if (dbg) {
-    for (auto& m : marks) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, marks[0].second, m.second);
-      std::fprintf(stderr, "%s=%.1f ", m.first.c_str(), ms * 1000.f);
-      cudaEventDestroy(m.second);
+  if (dbg) {  // host-side timeline: poll the marks, microseconds since enqueue start
+    const auto t_done = std::chrono::steady_clock::now();
+    std::vector<double> at(marks.size(), -1.0);
+    size_t left = marks.size();
+    while (left) {
+      for (size_t i = 0; i < marks.size(); ++i)
+        if (at[i] < 0 && cudaEventQuery(marks[i].second) == cudaSuccess) {
+          at[i] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_enq).count();
+          --left;
+        }
+    }
+    std::fprintf(stderr, "enqueue=%.1f ", std::chrono::duration<double, std::micro>(t_done - t_enq).count());
+    for (size_t i = 0; i < marks.size(); ++i) {
+      std::fprintf(stderr, "%s=%.1f ", marks[i].first.c_str(), at[i]);
+      cudaEventDestroy(marks[i].second);
     }
     std::fprintf(stderr, "\n");
   }
+  SAIT_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace

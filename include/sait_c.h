@@ -170,6 +170,30 @@ int sait_pair_spmv_factor(sait_pair_t p, int which, const double *d_x, double *d
 int sait_pair_factors(sait_pair_t p, sait_dcsr_t *ml, sait_dcsr_t *mu);
 void sait_pair_destroy(sait_pair_t p);
 
+/* ------------------------------------------------------------ solvers ---
+ * Device-resident loops driving the apply (north_star (3)); the reference has
+ * them only as SPEC.md:282-351 (PCG, LOBPCG) and not at all for GMRES, so the
+ * algorithms are fixed in DESIGN.md "solvers".  Vectors stay in HBM; b, x,
+ * eigenvectors are device pointers on A's device.  M may be NULL (identity).
+ * Reductions use a canonical order, so results are bitwise reproducible. */
+typedef struct {
+  int iterations;
+  int converged;
+  double relres_estimate; /* the stopping quantity at exit */
+  double true_relres;     /* ||b - A x|| / ||b|| recomputed at exit */
+  double seconds;         /* wall time of the solve */
+} sait_solve_stats;
+
+/* Right-preconditioned restarted GMRES(restart) from x0 = 0, CGS2 Arnoldi,
+ * stop when the Arnoldi residual estimate / ||b|| <= tol.  h_hist (host,
+ * maxit + 1 entries, may be NULL) receives the estimate per iteration. */
+int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double *d_b, double *d_x, int64_t n, int restart,
+               double tol, int maxit, double *h_hist, sait_solve_stats *stats, sait_stream_t stream);
+/* PCG from x0 = 0: stop when ||r|| / ||b|| <= tol;
+ * SAIT_ERR_RUNTIME on breakdown (p'Ap <= 0). */
+int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double *d_b, double *d_x, int64_t n, double tol,
+             int maxit, double *h_hist, sait_solve_stats *stats, sait_stream_t stream);
+
 /* ----------------------------------------------------- inputs (host) ---
  * Producers of the path's inputs.  ilu_k is ilu.hpp:27 / ilu.cpp:98-173
  * (bitwise identical factors); the generators fix BASELINE.json's synthetic

@@ -300,3 +300,42 @@ def uniform_pm1(seed: int, n: int) -> np.ndarray:
     L.orc_fill_uniform_pm1.argtypes = [C.c_uint64, C.c_int64, _PD]
     L.orc_fill_uniform_pm1(C.c_uint64(seed), C.c_int64(n), _dptr(out))
     return out
+
+
+class _SolveStats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_relres", C.c_double), ("true_relres", C.c_double)]
+
+
+def _solver(name, a, ml, mu, b, *args):
+    L = _port().lib
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty(a.nrows)
+    maxit = args[-1].value
+    hist = np.zeros(maxit + 1)
+    st = _SolveStats()
+    pm = C.byref(_in(ml)) if ml is not None else None
+    pu = C.byref(_in(mu)) if mu is not None else None
+    fn = getattr(L, name)
+    rc = fn(C.byref(_in(a)), pm, pu, _dptr(b), *args, _dptr(x), _dptr(hist), C.byref(st))
+    _port()._check(rc)
+    its = st.iterations
+    return x, {"iterations": its, "converged": bool(st.converged), "relres": st.final_relres,
+               "true_relres": st.true_relres, "history": hist[: its + 1].copy()}
+
+
+def gmres(a, ml, mu, b, restart=30, tol=1e-8, maxit=10000):
+    """Restated right-preconditioned GMRES(m) (oracle/solvers.c)."""
+    return _solver("orc_gmres", a, ml, mu, b, C.c_int(restart), C.c_double(tol), C.c_int(maxit))
+
+
+def pcg(a, ml, mu, b, tol=1e-10, maxit=10000):
+    """Restated PCG (oracle/solvers.c)."""
+    return _solver("orc_pcg", a, ml, mu, b, C.c_double(tol), C.c_int(maxit))
+
+
+def dot(a, b):
+    L = _port().lib
+    L.orc_dot.restype = C.c_double
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return L.orc_dot(_dptr(a), _dptr(b), C.c_int64(len(a)))

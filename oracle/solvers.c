@@ -1,2 +1,258 @@
-/* solvers.c — placeholder, filled in with the solver restatement */
+/*
+ * solvers.c — CPU restatement of the solver loops that drive the SAIT apply
+ * (TEST INFRASTRUCTURE ONLY, see sait_oracle.h).
+ *
+ * The reference has no solver code: PCG / LOBPCG exist only in SPEC.md:282-351
+ * and GMRES is not specified at all (SPEC.md:347 lists it as a non-goal while
+ * BASELINE.json configs 1 and 3 require GMRES(30)).  Iteration-count parity is
+ * therefore UNPINNED against the reference; these restatements fix the
+ * algorithms and define the canonical reduction order
+ * that the device kernels reproduce, so GPU and CPU agree bit for bit.
+ *
+ * Canonical dot (orc_dot): blocks of 2048 elements; in block b, "thread" t
+ * (0..255) sums a[i]*b[i] for i = 2048 b + t + 256 k, k = 0..7 in order,
+ * starting from 0.0; the 256 per-thread sums are combined by a butterfly
+ * within each 32-lane warp (offsets 16,8,4,2,1: v[l] += v[l^off], result at
+ * lane 0) and then across the 8 warp results (offsets 4,2,1).  The block
+ * partials P_b are reduced the same way by one 256-thread block whose thread
+ * t first sums P_t, P_{t+256}, ... in order from 0.0.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include "sait_oracle.h"
+
+#define DOT_T 256
+#define DOT_K 8
+#define DOT_B (DOT_T * DOT_K)
+
+/* butterfly over 32 lanes then over 8 warp leaders; v has DOT_T entries */
+static double block_tree(double *v) {
+  double w[8];
+  for (int warp = 0; warp < 8; ++warp) {
+    double l[32];
+    memcpy(l, v + 32 * warp, sizeof l);
+    for (int off = 16; off >= 1; off >>= 1) {
+      double nl[32];
+      for (int i = 0; i < 32; ++i) nl[i] = l[i] + l[i ^ off];
+      memcpy(l, nl, sizeof l);
+    }
+    w[warp] = l[0];
+  }
+  for (int off = 4; off >= 1; off >>= 1) {
+    double nw[8];
+    for (int i = 0; i < 8; ++i) nw[i] = w[i] + w[i ^ off];
+    memcpy(w, nw, sizeof w);
+  }
+  return w[0];
+}
+
+double orc_dot(const double *a, const double *b, int64_t n) {
+  int64_t nb = (n + DOT_B - 1) / DOT_B;
+  if (nb < 1) nb = 1;
+  double *part = (double *)malloc((size_t)nb * sizeof(double));
+  double v[DOT_T];
+  for (int64_t blk = 0; blk < nb; ++blk) {
+    for (int t = 0; t < DOT_T; ++t) {
+      double s = 0.0;
+      for (int k = 0; k < DOT_K; ++k) {
+        int64_t i = blk * DOT_B + t + (int64_t)DOT_T * k;
+        if (i < n) s = s + a[i] * b[i];
+      }
+      v[t] = s;
+    }
+    part[blk] = block_tree(v);
+  }
+  for (int t = 0; t < DOT_T; ++t) {
+    double s = 0.0;
+    for (int64_t q = t; q < nb; q += DOT_T) s = s + part[q];
+    v[t] = s;
+  }
+  double r = block_tree(v);
+  free(part);
+  return r;
+}
+
+static double nrm(const double *a, int64_t n) { return sqrt(orc_dot(a, a, n)); }
+
+/* z = M r for the SAIT pair, or a copy when no preconditioner */
+static void precond(const orc_csr *ml, const orc_csr *mu, const double *r, double *z, int64_t n) {
+  if (ml && mu) orc_pair_apply(ml, mu, r, z);
+  else memcpy(z, r, (size_t)n * sizeof(double));
+}
+
+/*
+ * Right-preconditioned restarted GMRES(m) from x0 = 0:
+ * Arnoldi on A M with classical Gram-Schmidt applied twice (CGS2), Givens
+ * rotations on the Hessenberg column, stop when the Arnoldi residual estimate
+ * |g_{i+1}| / ||b|| <= tol (checked every iteration), x += M (V y) at the end
+ * of each cycle, true residual recomputed at every restart and at exit.
+ * hist[k] = relative residual estimate after k iterations (hist[0] = 1).
+ */
+int orc_gmres(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double *b, int m,
+              double tol, int maxit, double *x, double *hist, orc_solve_stats *st) {
+  int64_t n = a->nrows;
+  double *V = (double *)calloc((size_t)(m + 1) * (size_t)n, sizeof(double));
+  double *w = (double *)malloc((size_t)n * sizeof(double));
+  double *z = (double *)malloc((size_t)n * sizeof(double));
+  double *u = (double *)malloc((size_t)n * sizeof(double));
+  double *H = (double *)calloc((size_t)(m + 1) * (size_t)m, sizeof(double)); /* H[row * m + col] */
+  double *cs = (double *)calloc((size_t)m, sizeof(double));
+  double *sn = (double *)calloc((size_t)m, sizeof(double));
+  double *g = (double *)calloc((size_t)m + 1, sizeof(double));
+  double *h = (double *)calloc((size_t)m + 2, sizeof(double));
+  double *h2 = (double *)calloc((size_t)m + 2, sizeof(double));
+  double *y = (double *)calloc((size_t)m, sizeof(double));
+  memset(x, 0, (size_t)n * sizeof(double));
+  double bnorm = nrm(b, n);
+  int its = 0, conv = 0;
+  double est = 1.0;
+  if (hist) hist[0] = 1.0;
+  if (bnorm == 0.0) {
+    conv = 1;
+    est = 0.0;
+  }
+  memcpy(w, b, (size_t)n * sizeof(double)); /* r0 = b - A*0 */
+  double beta = bnorm;
+  while (!conv && its < maxit) {
+    for (int64_t e = 0; e < n; ++e) V[e] = w[e] / beta;
+    memset(g, 0, (size_t)(m + 1) * sizeof(double));
+    g[0] = beta;
+    int k = 0;
+    for (int i = 0; i < m && its < maxit; ++i) {
+      double *vi = V + (int64_t)i * n;
+      precond(ml, mu, vi, z, n);
+      orc_spmv(a, z, n, w, n);
+      /* CGS2 */
+      for (int pass = 0; pass < 2; ++pass) {
+        double *hh = pass == 0 ? h : h2;
+        for (int j = 0; j <= i; ++j) hh[j] = orc_dot(V + (int64_t)j * n, w, n);
+        for (int64_t e = 0; e < n; ++e) {
+          double t = w[e];
+          for (int j = 0; j <= i; ++j) t = t - hh[j] * V[(int64_t)j * n + e];
+          w[e] = t;
+        }
+      }
+      for (int j = 0; j <= i; ++j) h[j] = h[j] + h2[j];
+      h[i + 1] = nrm(w, n);
+      if (h[i + 1] != 0.0) {
+        double *vn = V + (int64_t)(i + 1) * n;
+        for (int64_t e = 0; e < n; ++e) vn[e] = w[e] / h[i + 1];
+      }
+      /* Givens */
+      for (int j = 0; j < i; ++j) {
+        double t0 = cs[j] * h[j] + sn[j] * h[j + 1];
+        double t1 = -sn[j] * h[j] + cs[j] * h[j + 1];
+        h[j] = t0;
+        h[j + 1] = t1;
+      }
+      double den = sqrt(h[i] * h[i] + h[i + 1] * h[i + 1]);
+      if (den == 0.0) {
+        cs[i] = 1.0;
+        sn[i] = 0.0;
+      } else {
+        cs[i] = h[i] / den;
+        sn[i] = h[i + 1] / den;
+      }
+      h[i] = den;
+      h[i + 1] = 0.0;
+      g[i + 1] = -sn[i] * g[i];
+      g[i] = cs[i] * g[i];
+      for (int j = 0; j <= i; ++j) H[j * m + i] = h[j];
+      ++its;
+      k = i + 1;
+      est = fabs(g[i + 1]) / bnorm;
+      if (hist) hist[its] = est;
+      if (est <= tol) {
+        conv = 1;
+        break;
+      }
+    }
+    /* y = H(0:k,0:k) \ g(0:k), back substitution */
+    for (int ii = k - 1; ii >= 0; --ii) {
+      double t = g[ii];
+      for (int jj = ii + 1; jj < k; ++jj) t = t - H[ii * m + jj] * y[jj];
+      y[ii] = t / H[ii * m + ii];
+    }
+    /* x += M (V y) */
+    for (int64_t e = 0; e < n; ++e) {
+      double t = y[0] * V[e];
+      for (int j = 1; j < k; ++j) t = t + y[j] * V[(int64_t)j * n + e];
+      u[e] = t;
+    }
+    precond(ml, mu, u, z, n);
+    for (int64_t e = 0; e < n; ++e) x[e] = x[e] + z[e];
+    /* true residual */
+    orc_spmv(a, x, n, z, n);
+    for (int64_t e = 0; e < n; ++e) w[e] = b[e] - z[e];
+    beta = nrm(w, n);
+    if (beta == 0.0) conv = 1;
+  }
+  if (st) {
+    st->iterations = its;
+    st->converged = conv;
+    st->final_relres = est;
+    st->true_relres = bnorm == 0.0 ? 0.0 : beta / bnorm;
+  }
+  free(V); free(w); free(z); free(u); free(H); free(cs); free(sn); free(g); free(h); free(h2); free(y);
+  return ORC_OK;
+}
+
+/*
+ * PCG from x0 = 0, stop when ||r_k|| / ||b|| <= tol on the
+ * recurrence residual; breakdown p'Ap <= 0 -> runtime error.  hist as GMRES.
+ */
+int orc_pcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double *b, double tol,
+            int maxit, double *x, double *hist, orc_solve_stats *st) {
+  int64_t n = a->nrows;
+  double *r = (double *)malloc((size_t)n * sizeof(double));
+  double *z = (double *)malloc((size_t)n * sizeof(double));
+  double *p = (double *)malloc((size_t)n * sizeof(double));
+  double *q = (double *)malloc((size_t)n * sizeof(double));
+  memset(x, 0, (size_t)n * sizeof(double));
+  memcpy(r, b, (size_t)n * sizeof(double));
+  double bnorm = nrm(b, n), rel = 1.0;
+  int its = 0, conv = bnorm == 0.0, rc = ORC_OK;
+  if (hist) hist[0] = 1.0;
+  if (!conv) {
+    precond(ml, mu, r, z, n);
+    memcpy(p, z, (size_t)n * sizeof(double));
+    double rz = orc_dot(r, z, n);
+    while (its < maxit) {
+      orc_spmv(a, p, n, q, n);
+      double pq = orc_dot(p, q, n);
+      if (!(pq > 0.0)) {
+        rc = ORC_RUNTIME_ERROR;
+        break;
+      }
+      double alpha = rz / pq;
+      for (int64_t e = 0; e < n; ++e) {
+        x[e] = x[e] + alpha * p[e];
+        r[e] = r[e] - alpha * q[e];
+      }
+      ++its;
+      rel = nrm(r, n) / bnorm;
+      if (hist) hist[its] = rel;
+      if (rel <= tol) {
+        conv = 1;
+        break;
+      }
+      precond(ml, mu, r, z, n);
+      double rz2 = orc_dot(r, z, n);
+      double beta = rz2 / rz;
+      rz = rz2;
+      for (int64_t e = 0; e < n; ++e) p[e] = z[e] + beta * p[e];
+    }
+  }
+  if (st) {
+    orc_spmv(a, x, n, q, n);
+    for (int64_t e = 0; e < n; ++e) q[e] = b[e] - q[e];
+    st->iterations = its;
+    st->converged = conv;
+    st->final_relres = bnorm == 0.0 ? 0.0 : rel;
+    st->true_relres = bnorm == 0.0 ? 0.0 : nrm(q, n) / bnorm;
+  }
+  free(r); free(z); free(p); free(q);
+  return rc;
+}

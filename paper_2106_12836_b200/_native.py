@@ -66,6 +66,16 @@ class BuildStats(C.Structure):
     ]
 
 
+class SolveStats(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int),
+        ("converged", C.c_int),
+        ("relres_estimate", C.c_double),
+        ("true_relres", C.c_double),
+        ("seconds", C.c_double),
+    ]
+
+
 # Every symbol include/sait_c.h declares, with its prototype.
 PROTOTYPES = {
     "sait_last_error": (C.c_char_p, []),
@@ -96,6 +106,8 @@ PROTOTYPES = {
     "sait_pair_spmv_factor": (C.c_int, [VP, C.c_int, VP, VP, VP]),
     "sait_pair_factors": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP)]),
     "sait_pair_destroy": (None, [VP]),
+    "sait_gmres": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
+    "sait_pcg": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),
     "sait_problem_laplacian_2d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),
     "sait_problem_laplacian_3d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),

@@ -1,0 +1,166 @@
+// blas.cu — K7: BLAS-1 / tall-skinny kernels of the device solver loops.
+//
+// Reductions use ONE canonical order (shared with oracle/solvers.c): blocks of
+// 2048 elements; thread t of a 256-thread block sums x[i]*y[i] for
+// i = 2048 b + t + 256 k, k = 0..7, sequentially from 0.0; the 256 sums are
+// folded by a 32-lane xor butterfly (offsets 16..1) per warp and an 8-way
+// butterfly (4,2,1) across warps; block partials are folded the same way by
+// one block whose thread t first sums partials t, t+256, ... in order.  With
+// every product rounded before its add, dots are bitwise reproducible and
+// equal to the CPU restatement, so solver iteration counts match exactly.
+#include "common.cuh"
+
+namespace sait {
+namespace {
+
+constexpr int kT = 256, kK = 8, kB = kT * kK;
+constexpr int kMaxM = 32;
+
+__device__ __forceinline__ double warp_butterfly(double s) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+  return s;
+}
+
+// ((w0+w4)+(w2+w6)) + ((w1+w5)+(w3+w7)) : the 8-lane butterfly at lane 0
+__device__ __forceinline__ double tree8(const double* w) {
+  const double a0 = __dadd_rn(w[0], w[4]), a1 = __dadd_rn(w[1], w[5]);
+  const double a2 = __dadd_rn(w[2], w[6]), a3 = __dadd_rn(w[3], w[7]);
+  return __dadd_rn(__dadd_rn(a0, a2), __dadd_rn(a1, a3));
+}
+
+// part[j * nb + b] = canonical block partial of x . V_j
+__global__ void __launch_bounds__(kT) mdot_partials(int64_t n, const double* __restrict__ x,
+                                                     const double* __restrict__ V, int64_t ld, int m,
+                                                     double* __restrict__ part, int64_t nb) {
+  __shared__ double ws[kMaxM][8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kB + t;
+  double xv[kK];
+#pragma unroll
+  for (int k = 0; k < kK; ++k) {
+    const int64_t i = base + static_cast<int64_t>(kT) * k;
+    xv[k] = i < n ? x[i] : 0.0;
+  }
+  for (int j = 0; j < m; ++j) {
+    const double* v = V + ld * j;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      const int64_t i = base + static_cast<int64_t>(kT) * k;
+      if (i < n) s = __dadd_rn(s, __dmul_rn(xv[k], v[i]));
+    }
+    s = warp_butterfly(s);
+    if (lane == 0) ws[j][warp] = s;
+  }
+  __syncthreads();
+  if (t < m) part[static_cast<int64_t>(t) * nb + blockIdx.x] = tree8(ws[t]);
+}
+
+// out[j] = canonical fold of the nb partials of dot j (one block per j)
+__global__ void __launch_bounds__(kT) mdot_final(const double* __restrict__ part, int64_t nb,
+                                                  double* __restrict__ out, int sqrt_out) {
+  __shared__ double ws[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double* p = part + nb * blockIdx.x;
+  double s = 0.0;
+  for (int64_t q = t; q < nb; q += kT) s = __dadd_rn(s, p[q]);
+  s = warp_butterfly(s);
+  if (lane == 0) ws[warp] = s;
+  __syncthreads();
+  if (t == 0) {
+    const double d = tree8(ws);
+    out[blockIdx.x] = sqrt_out ? __dsqrt_rn(d) : d;
+  }
+}
+
+// w[e] = (((w - h0 v0) - h1 v1) - ...)   (sequential in j)
+__global__ void cgs_update(int64_t n, double* __restrict__ w, const double* __restrict__ V, int64_t ld, int m,
+                           const double* __restrict__ h) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double t = w[e];
+  for (int j = 0; j < m; ++j) t = __dsub_rn(t, __dmul_rn(h[j], V[ld * j + e]));
+  w[e] = t;
+}
+
+// out = w / d[0]
+__global__ void div_by(int64_t n, const double* __restrict__ w, const double* __restrict__ d, double* __restrict__ out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n) out[e] = __ddiv_rn(w[e], d[0]);
+}
+
+// u = y0 v0 + y1 v1 + ...   (sequential in j, first term a product)
+__global__ void lincomb(int64_t n, const double* __restrict__ V, int64_t ld, int k, const double* __restrict__ y,
+                        double* __restrict__ u) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double t = __dmul_rn(y[0], V[e]);
+  for (int j = 1; j < k; ++j) t = __dadd_rn(t, __dmul_rn(y[j], V[ld * j + e]));
+  u[e] = t;
+}
+
+// y = y + a x  /  y = x + a y  /  y = x - y
+__global__ void axpy_k(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n) y[e] = __dadd_rn(y[e], __dmul_rn(a, x[e]));
+}
+__global__ void xpay_k(int64_t n, const double* __restrict__ x, double a, double* __restrict__ y) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n) y[e] = __dadd_rn(x[e], __dmul_rn(a, y[e]));
+}
+__global__ void sub_k(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n) y[e] = __dsub_rn(x[e], y[e]);
+}
+__global__ void add_k(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n) y[e] = __dadd_rn(y[e], x[e]);
+}
+
+}  // namespace
+
+int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
+
+void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, double* out, double* scratch,
+               cudaStream_t s, bool sqrt_out) {
+  const int64_t nb = dot_blocks(n);
+  for (int j0 = 0; j0 < m; j0 += kMaxM) {
+    const int mm = m - j0 < kMaxM ? m - j0 : kMaxM;
+    mdot_partials<<<static_cast<unsigned>(nb), kT, 0, s>>>(n, x, V + ld * j0, ld, mm, scratch, nb);
+    SAIT_LAUNCHED();
+    mdot_final<<<mm, kT, 0, s>>>(scratch, nb, out + j0, sqrt_out ? 1 : 0);
+    SAIT_LAUNCHED();
+  }
+}
+
+void cgs_subtract(int64_t n, double* w, const double* V, int64_t ld, int m, const double* h, cudaStream_t s) {
+  cgs_update<<<grid_for(n, 256), 256, 0, s>>>(n, w, V, ld, m, h);
+  SAIT_LAUNCHED();
+}
+void divide_by(int64_t n, const double* w, const double* d, double* out, cudaStream_t s) {
+  div_by<<<grid_for(n, 256), 256, 0, s>>>(n, w, d, out);
+  SAIT_LAUNCHED();
+}
+void linear_combination(int64_t n, const double* V, int64_t ld, int k, const double* y, double* u, cudaStream_t s) {
+  lincomb<<<grid_for(n, 256), 256, 0, s>>>(n, V, ld, k, y, u);
+  SAIT_LAUNCHED();
+}
+void axpy(int64_t n, double a, const double* x, double* y, cudaStream_t s) {
+  axpy_k<<<grid_for(n, 256), 256, 0, s>>>(n, a, x, y);
+  SAIT_LAUNCHED();
+}
+void xpay(int64_t n, const double* x, double a, double* y, cudaStream_t s) {
+  xpay_k<<<grid_for(n, 256), 256, 0, s>>>(n, x, a, y);
+  SAIT_LAUNCHED();
+}
+void x_minus_y(int64_t n, const double* x, double* y, cudaStream_t s) {
+  sub_k<<<grid_for(n, 256), 256, 0, s>>>(n, x, y);
+  SAIT_LAUNCHED();
+}
+void y_plus_x(int64_t n, const double* x, double* y, cudaStream_t s) {
+  add_k<<<grid_for(n, 256), 256, 0, s>>>(n, x, y);
+  SAIT_LAUNCHED();
+}
+
+}  // namespace sait

@@ -871,6 +871,21 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
 
 }  // namespace
 
+namespace sait {
+// z = M_U (M_L r) on device vectors (used by the solver loops)
+void pair_apply_internal(sait_pair_t p, const double* r, double* z, cudaStream_t s) {
+  sait_pair_s::Work& w = pair_work(p, s);
+  if (pair_variant() == 3 && p->pp.ok()) {
+    sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, r, w.y, z, s);
+  } else {
+    factor_spmv(p, 0, r, w.y, s);
+    factor_spmv(p, 1, w.y, z, s);
+  }
+}
+int64_t pair_dim(sait_pair_t p) { return p->ml->m.ncols; }
+int pair_device(sait_pair_t p) { return p->dev; }
+}  // namespace sait
+
 extern "C" {
 
 int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z, int64_t zlen, sait_stream_t stream) {
@@ -884,13 +899,7 @@ int sait_pair_apply(sait_pair_t p, const double* d_r, int64_t rlen, double* d_z,
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
     cudaStream_t s = sait::as_stream(stream);
-    sait_pair_s::Work& w = pair_work(p, s);
-    if (pair_variant() == 3 && p->pp.ok()) {
-      sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, d_r, w.y, d_z, s);
-    } else {
-      factor_spmv(p, 0, d_r, w.y, s);
-      factor_spmv(p, 1, w.y, d_z, s);
-    }
+    sait::pair_apply_internal(p, d_r, d_z, s);
   });
 }
 
@@ -1054,3 +1063,10 @@ void sait_pair_destroy(sait_pair_t p) {
 }
 
 }  // extern "C"
+
+namespace sait {
+void pair_apply_block_internal(sait_pair_t p, const double* r, double* z, int64_t n, int64_t nvec, int layout,
+                               cudaStream_t s) {
+  apply_block_device(p, r, z, n, nvec, layout, s);
+}
+}  // namespace sait

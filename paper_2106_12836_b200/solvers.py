@@ -1,0 +1,63 @@
+"""Device-resident solver loops driving the SAIT apply (north_star (3)).
+
+``gmres`` (right-preconditioned GMRES(m), CGS2 Arnoldi) and ``pcg``
+ run entirely on the GPU; only control scalars come back
+per iteration.  ``M`` is a SaitPairPreconditioner or None (identity).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .csr import CsrMatrix, DeviceCsr, _stream_handle
+
+
+@dataclass
+class SolveStats:
+    iterations: int
+    converged: bool
+    relres_estimate: float
+    true_relres: float
+    seconds: float
+    history: np.ndarray
+
+
+def _prep(A, b, stream):
+    import torch
+
+    dA = A if isinstance(A, DeviceCsr) else DeviceCsr.upload(A, stream)
+    on_dev = isinstance(b, torch.Tensor) and b.is_cuda
+    bd = b if on_dev else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
+    x = torch.empty_like(bd)
+    s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    return dA, bd, x, on_dev, s
+
+
+def _finish(rc, st, hist, x, on_dev):
+    N.check(rc)
+    its = st.iterations
+    stats = SolveStats(its, bool(st.converged), st.relres_estimate, st.true_relres, st.seconds, hist[: its + 1].copy())
+    return (x if on_dev else x.cpu().numpy()), stats
+
+
+def gmres(A, M, b, restart: int = 30, tol: float = 1e-8, maxit: int = 10000, stream=None):
+    dA, bd, x, on_dev, s = _prep(A, b, stream)
+    hist = np.zeros(maxit + 1)
+    st = N.SolveStats()
+    mh = M.handle if M is not None else None
+    rc = N.lib.sait_gmres(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), int(restart), float(tol), int(maxit),
+                          hist.ctypes.data_as(N.PD), C.byref(st), s)
+    return _finish(rc, st, hist, x, on_dev)
+
+
+def pcg(A, M, b, tol: float = 1e-10, maxit: int = 10000, stream=None):
+    dA, bd, x, on_dev, s = _prep(A, b, stream)
+    hist = np.zeros(maxit + 1)
+    st = N.SolveStats()
+    mh = M.handle if M is not None else None
+    rc = N.lib.sait_pcg(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), float(tol), int(maxit),
+                        hist.ctypes.data_as(N.PD), C.byref(st), s)
+    return _finish(rc, st, hist, x, on_dev)

@@ -194,6 +194,16 @@ int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double *d_b, double *d_x, int
 int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double *d_b, double *d_x, int64_t n, double tol,
              int maxit, double *h_hist, sait_solve_stats *stats, sait_stream_t stream);
 
+/* Block LOBPCG for the nev (<= 16) smallest eigenpairs of
+ * SPD A, preconditioned by the pair applied to the whole residual block
+ * (apply_block, preconditioner.cpp:47-49).  X0 ~ U[-1,1] from `seed`.
+ * h_evals: nev host values (ascending); d_evecs: n x nev column-major device
+ * block (may be NULL); h_resnorms: host (maxit + 1) x nev residual norms per
+ * iteration (may be NULL); converged when every ||A x - lambda x|| <= tol. */
+int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed,
+                double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
+                sait_stream_t stream);
+
 /* ----------------------------------------------------- inputs (host) ---
  * Producers of the path's inputs.  ilu_k is ilu.hpp:27 / ilu.cpp:98-173
  * (bitwise identical factors); the generators fix BASELINE.json's synthetic

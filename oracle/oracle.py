@@ -339,3 +339,21 @@ def dot(a, b):
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     return L.orc_dot(_dptr(a), _dptr(b), C.c_int64(len(a)))
+
+
+def lobpcg(a, ml, mu, nev, tol=1e-6, maxit=500, seed=5):
+    """Restated block LOBPCG (oracle/solvers.c).  Returns (evals, evecs (n, nev)
+    column-major, iterations, residual-norm history (iters+1, nev))."""
+    L = _port().lib
+    n = a.nrows
+    evals = np.zeros(nev)
+    evecs = np.zeros((nev, n))  # row j = column j of the n x nev block
+    res = np.zeros((maxit + 1) * nev)
+    its = C.c_int()
+    pm = C.byref(_in(ml)) if ml is not None else None
+    pu = C.byref(_in(mu)) if mu is not None else None
+    rc = L.orc_lobpcg(C.byref(_in(a)), pm, pu, C.c_int(nev), C.c_double(tol), C.c_int(maxit), C.c_uint64(seed),
+                      _dptr(evals), evecs.ctypes.data_as(_PD), C.byref(its), _dptr(res))
+    _port()._check(rc)
+    it = its.value
+    return evals, evecs.T, it, res[: (it + 1) * nev].reshape(it + 1, nev)

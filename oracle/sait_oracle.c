@@ -23,6 +23,8 @@ static int fail(int code, const char *fmt, ...) {
 
 const char *orc_last_error(void) { return g_err; }
 
+int orc_set_error(const char *m) { return fail(ORC_RUNTIME_ERROR, "%s", m); }
+
 void orc_free(void *p) { free(p); }
 
 void orc_csr_free(orc_csr *m) {

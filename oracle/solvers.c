@@ -76,6 +76,11 @@ double orc_dot(const double *a, const double *b, int64_t n) {
 
 static double nrm(const double *a, int64_t n) { return sqrt(orc_dot(a, a, n)); }
 
+static int fail_solver(const char *msg) {
+  extern int orc_set_error(const char *m);
+  return orc_set_error(msg);
+}
+
 /* z = M r for the SAIT pair, or a copy when no preconditioner */
 static void precond(const orc_csr *ml, const orc_csr *mu, const double *r, double *z, int64_t n) {
   if (ml && mu) orc_pair_apply(ml, mu, r, z);
@@ -254,5 +259,279 @@ int orc_pcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double
     st->true_relres = bnorm == 0.0 ? 0.0 : nrm(q, n) / bnorm;
   }
   free(r); free(z); free(p); free(q);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ LOBPCG
+ * Block LOBPCG (Knyazev 2001) for the nev smallest eigenpairs of SPD A with
+ * the SAIT pair as preconditioner.  Fixed choices (DESIGN.md
+ * "solvers"): X0 ~ U[-1,1] column j from seed (seed, j); W = T R is
+ * orthogonalised against X and Cholesky-QR normalised, P is Cholesky-QR
+ * normalised; Rayleigh-Ritz on S = [X W P] with B-Gram S'S and symmetrised
+ * S'AS; the small generalized problem is solved by Cholesky + cyclic Jacobi;
+ * if S'S is not positive definite the P block is dropped for that iteration.
+ * Converged when every ||A x_j - lambda_j x_j|| <= tol (unit x_j).
+ * Block vectors are column-major n x k.  Gram entries use orc_dot.  */
+
+/* G[a][b] = S_a . Y_b for a in [0,ka), b in [0,kb) */
+static void gram(const double *S, int ka, const double *Y, int kb, int64_t n, double *G, int ld) {
+  for (int a = 0; a < ka; ++a)
+    for (int b = 0; b < kb; ++b) G[a * ld + b] = orc_dot(S + (int64_t)a * n, Y + (int64_t)b * n, n);
+}
+
+/* out[:, j] = sum_q in[:, q] C[q][j] (sequential q, first term a product) */
+static void lincomb_cols(const double *in, int kin, const double *C, int ldc, int kout, int64_t n, double *out) {
+  for (int j = 0; j < kout; ++j)
+    for (int64_t i = 0; i < n; ++i) {
+      double t = in[i] * C[0 * ldc + j];
+      for (int q = 1; q < kin; ++q) t = t + in[(int64_t)q * n + i] * C[q * ldc + j];
+      out[(int64_t)j * n + i] = t;
+    }
+}
+
+/* Cholesky of SPD m x m (row-major) into lower L; returns 0 if not PD */
+static int chol_lower(const double *G, int m, double *L) {
+  for (int i = 0; i < m * m; ++i) L[i] = 0.0;
+  for (int j = 0; j < m; ++j) {
+    double d = G[j * m + j];
+    for (int k = 0; k < j; ++k) d = d - L[j * m + k] * L[j * m + k];
+    if (!(d > 0.0)) return 0;
+    double ljj = sqrt(d);
+    L[j * m + j] = ljj;
+    for (int i = j + 1; i < m; ++i) {
+      double t = G[i * m + j];
+      for (int k = 0; k < j; ++k) t = t - L[i * m + k] * L[j * m + k];
+      L[i * m + j] = t / ljj;
+    }
+  }
+  return 1;
+}
+
+/* inverse of lower-triangular L (forward substitution per column) */
+static void tri_lower_inv(const double *L, int m, double *Li) {
+  for (int i = 0; i < m * m; ++i) Li[i] = 0.0;
+  for (int j = 0; j < m; ++j) {
+    Li[j * m + j] = 1.0 / L[j * m + j];
+    for (int i = j + 1; i < m; ++i) {
+      double t = 0.0;
+      for (int k = j; k < i; ++k) t = t - L[i * m + k] * Li[k * m + j];
+      Li[i * m + j] = t / L[i * m + i];
+    }
+  }
+}
+
+/* cyclic Jacobi eigen-decomposition of symmetric F (m x m, destroyed);
+ * eigenvalues ascending in w, eigenvectors in columns of Q (row-major) */
+static void jacobi_eig(double *F, int m, double *w, double *Q) {
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) Q[i * m + j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) off = off + F[p * m + q] * F[p * m + q];
+    if (off == 0.0) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        double apq = F[p * m + q];
+        if (apq == 0.0) continue;
+        double app = F[p * m + p], aqq = F[q * m + q];
+        double theta = (aqq - app) / (2.0 * apq);
+        double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < m; ++k) { /* columns p, q */
+          double fkp = F[k * m + p], fkq = F[k * m + q];
+          F[k * m + p] = c * fkp - s * fkq;
+          F[k * m + q] = s * fkp + c * fkq;
+        }
+        for (int k = 0; k < m; ++k) { /* rows p, q */
+          double fpk = F[p * m + k], fqk = F[q * m + k];
+          F[p * m + k] = c * fpk - s * fqk;
+          F[q * m + k] = s * fpk + c * fqk;
+        }
+        F[p * m + q] = 0.0;
+        F[q * m + p] = 0.0;
+        for (int k = 0; k < m; ++k) {
+          double qkp = Q[k * m + p], qkq = Q[k * m + q];
+          Q[k * m + p] = c * qkp - s * qkq;
+          Q[k * m + q] = s * qkp + c * qkq;
+        }
+      }
+  }
+  /* selection sort ascending (stable on ties by index) */
+  int idx[64];
+  for (int i = 0; i < m; ++i) idx[i] = i;
+  for (int i = 0; i < m; ++i) {
+    int best = i;
+    for (int j = i + 1; j < m; ++j)
+      if (F[idx[j] * m + idx[j]] < F[idx[best] * m + idx[best]]) best = j;
+    int tmp = idx[i];
+    idx[i] = idx[best];
+    idx[best] = tmp;
+  }
+  double *Qs = (double *)malloc((size_t)m * m * sizeof(double));
+  for (int j = 0; j < m; ++j) {
+    w[j] = F[idx[j] * m + idx[j]];
+    for (int i = 0; i < m; ++i) Qs[i * m + j] = Q[i * m + idx[j]];
+  }
+  memcpy(Q, Qs, (size_t)m * m * sizeof(double));
+  free(Qs);
+}
+
+/* Rayleigh-Ritz: given GB (SPD) and GA (sym) of size m, fill C (m x k, row
+ * major, ldc = k) with the k lowest B-orthonormal Ritz vectors, mu with their
+ * values.  Returns 0 when GB is not positive definite. */
+static int rayleigh_ritz(const double *GA, const double *GB, int m, int k, double *C, double *mu) {
+  double L[64 * 64], Li[64 * 64], T[64 * 64], F[64 * 64], Q[64 * 64], w[64];
+  if (!chol_lower(GB, m, L)) return 0;
+  tri_lower_inv(L, m, Li);
+  /* F = Li GA Li^T */
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < m; ++q) t = t + Li[i * m + q] * GA[q * m + j];
+      T[i * m + j] = t;
+    }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < m; ++q) t = t + T[i * m + q] * Li[j * m + q];
+      F[i * m + j] = t;
+    }
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) {
+      double a = 0.5 * (F[i * m + j] + F[j * m + i]);
+      F[i * m + j] = a;
+      F[j * m + i] = a;
+    }
+  jacobi_eig(F, m, w, Q);
+  /* C = Li^T Q[:, :k] */
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < k; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < m; ++q) t = t + Li[q * m + i] * Q[q * m + j];
+      C[i * k + j] = t;
+    }
+  for (int j = 0; j < k; ++j) mu[j] = w[j];
+  return 1;
+}
+
+/* Y <- Y R^-1 with G = Y'Y = R'R (Cholesky-QR); AY transformed alike when
+ * given.  Returns 0 if G is not PD. */
+static int cholqr(double *Y, double *AY, int k, int64_t n, double *tmp) {
+  double G[32 * 32], L[32 * 32], Li[32 * 32], Ri[32 * 32];
+  gram(Y, k, Y, k, n, G, k);
+  if (!chol_lower(G, k, L)) return 0;
+  tri_lower_inv(L, k, Li);
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) Ri[i * k + j] = Li[j * k + i]; /* R^-1 = (L^-1)^T */
+  lincomb_cols(Y, k, Ri, k, k, n, tmp);
+  memcpy(Y, tmp, (size_t)k * n * sizeof(double));
+  if (AY) {
+    lincomb_cols(AY, k, Ri, k, k, n, tmp);
+    memcpy(AY, tmp, (size_t)k * n * sizeof(double));
+  }
+  return 1;
+}
+
+static void block_spmv(const orc_csr *a, const double *X, int k, double *Y) {
+  int64_t n = a->nrows;
+  for (int j = 0; j < k; ++j) orc_spmv(a, X + (int64_t)j * n, n, Y + (int64_t)j * n, n);
+}
+
+int orc_lobpcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, int k, double tol, int maxit,
+               uint64_t seed, double *evals, double *evecs, int *iters, double *resnorms) {
+  int64_t n = a->nrows;
+  if (k < 1 || k > 16 || 3 * k > 64) return fail_solver("lobpcg: block size must be in [1, 16]");
+  size_t blk = (size_t)k * (size_t)n;
+  double *S = (double *)calloc(3 * blk, sizeof(double));  /* [X W P] */
+  double *AS = (double *)calloc(3 * blk, sizeof(double)); /* [AX AW AP] */
+  double *R = (double *)malloc(blk * sizeof(double));
+  double *tmp = (double *)malloc(4 * blk * sizeof(double));
+  double *X = S, *W = S + blk, *P = S + 2 * blk;
+  double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
+  double GA[48 * 48], GB[48 * 48], C[48 * 16], lam[48];
+  for (int j = 0; j < k; ++j) orc_fill_uniform_pm1(seed * 1000 + (uint64_t)j, n, X + (size_t)j * n);
+  block_spmv(a, X, k, AX);
+  int rc = ORC_OK, have_p = 0, it = 0, conv = 0;
+  /* initial Rayleigh-Ritz on X */
+  gram(X, k, X, k, n, GB, k);
+  gram(X, k, AX, k, n, GA, k);
+  if (!rayleigh_ritz(GA, GB, k, k, C, lam)) {
+    rc = fail_solver("lobpcg: initial block is rank deficient");
+    goto done;
+  }
+  lincomb_cols(X, k, C, k, k, n, tmp);
+  memcpy(X, tmp, blk * sizeof(double));
+  lincomb_cols(AX, k, C, k, k, n, tmp);
+  memcpy(AX, tmp, blk * sizeof(double));
+  for (it = 0; it <= maxit; ++it) {
+    for (int j = 0; j < k; ++j)
+      for (int64_t i = 0; i < n; ++i) R[(size_t)j * n + i] = AX[(size_t)j * n + i] - lam[j] * X[(size_t)j * n + i];
+    conv = 1;
+    for (int j = 0; j < k; ++j) {
+      resnorms[(size_t)it * k + j] = sqrt(orc_dot(R + (size_t)j * n, R + (size_t)j * n, n));
+      if (!(resnorms[(size_t)it * k + j] <= tol)) conv = 0;
+    }
+    if (conv || it == maxit) break;
+    /* W = T R, orthogonalised against X, normalised */
+    for (int j = 0; j < k; ++j) {
+      if (ml && mu) orc_pair_apply(ml, mu, R + (size_t)j * n, W + (size_t)j * n);
+      else memcpy(W + (size_t)j * n, R + (size_t)j * n, (size_t)n * sizeof(double));
+    }
+    {
+      double G1[16 * 16];
+      gram(X, k, W, k, n, G1, k);
+      for (int j = 0; j < k; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+          double t = W[(size_t)j * n + i];
+          for (int q = 0; q < k; ++q) t = t - X[(size_t)q * n + i] * G1[q * k + j];
+          W[(size_t)j * n + i] = t;
+        }
+    }
+    if (!cholqr(W, NULL, k, n, tmp)) {
+      rc = fail_solver("lobpcg: preconditioned residual block is rank deficient");
+      break;
+    }
+    block_spmv(a, W, k, AW);
+    int use_p = have_p && cholqr(P, AP, k, n, tmp);
+    int m = use_p ? 3 * k : 2 * k;
+    for (;;) {
+      gram(S, m, S, m, n, GB, m);
+      gram(S, m, AS, m, n, GA, m);
+      for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j) {
+          double s2 = 0.5 * (GA[i * m + j] + GA[j * m + i]);
+          GA[i * m + j] = s2;
+          GA[j * m + i] = s2;
+        }
+      if (rayleigh_ritz(GA, GB, m, k, C, lam)) break;
+      if (m == 3 * k) {
+        m = 2 * k; /* drop P */
+        use_p = 0;
+        continue;
+      }
+      rc = fail_solver("lobpcg: Gram matrix not positive definite");
+      goto done;
+    }
+    /* P = [W P] C[k:, :], AP likewise; X = S C, AX = AS C */
+    lincomb_cols(W, m - k, C + k * k, k, k, n, tmp);
+    lincomb_cols(AW, m - k, C + k * k, k, k, n, tmp + blk);
+    lincomb_cols(S, m, C, k, k, n, tmp + 2 * blk);
+    lincomb_cols(AS, m, C, k, k, n, tmp + 3 * blk);
+    memcpy(P, tmp, blk * sizeof(double));
+    memcpy(AP, tmp + blk, blk * sizeof(double));
+    memcpy(X, tmp + 2 * blk, blk * sizeof(double));
+    memcpy(AX, tmp + 3 * blk, blk * sizeof(double));
+    have_p = 1;
+  }
+done:
+  for (int j = 0; j < k; ++j) evals[j] = lam[j];
+  if (evecs) memcpy(evecs, X, blk * sizeof(double));
+  *iters = it;
+  free(S);
+  free(AS);
+  free(R);
+  free(tmp);
+  if (rc == ORC_OK && !conv) rc = ORC_OK; /* not converged: caller checks residuals */
   return rc;
 }

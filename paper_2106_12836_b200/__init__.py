@@ -27,7 +27,7 @@ from .csr import (
 )
 from .preconditioner import IdentityPreconditioner, Preconditioner, SaitPairPreconditioner, apply_precond
 from .problems import IluFactors, convdiff_2d, ilu_k, laplacian_2d, laplacian_3d, synthetic_lower, uniform_pm1
-from .solvers import SolveStats, gmres, pcg
+from .solvers import EigResult, SolveStats, gmres, lobpcg, pcg
 from .sait import (
     BuildStats,
     JacobiSplit,

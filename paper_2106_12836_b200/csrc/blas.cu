@@ -118,7 +118,53 @@ __global__ void add_k(int64_t n, const double* __restrict__ x, double* __restric
   if (e < n) y[e] = __dadd_rn(y[e], x[e]);
 }
 
+// out[:, j] = sum_q in[:, q] C[q][j]  (column-major blocks, C row-major kin x kout)
+__global__ void block_lincomb_k(int64_t n, const double* __restrict__ in, int kin, const double* __restrict__ C,
+                                int kout, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < kout; ++j) {
+    double t = __dmul_rn(in[i], C[j]);
+    for (int q = 1; q < kin; ++q) t = __dadd_rn(t, __dmul_rn(in[n * q + i], C[q * kout + j]));
+    out[n * j + i] = t;
+  }
+}
+
+// W[:, j] = (((W_j - X_0 G[0][j]) - X_1 G[1][j]) - ...)
+__global__ void block_sub_lincomb_k(int64_t n, const double* __restrict__ X, int k, const double* __restrict__ G,
+                                    double* __restrict__ W) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < k; ++j) {
+    double t = W[n * j + i];
+    for (int q = 0; q < k; ++q) t = __dsub_rn(t, __dmul_rn(X[n * q + i], G[q * k + j]));
+    W[n * j + i] = t;
+  }
+}
+
+// R[:, j] = AX[:, j] - lam[j] X[:, j]
+__global__ void block_residual_k(int64_t n, int k, const double* __restrict__ AX, const double* __restrict__ X,
+                                 const double* __restrict__ lam, double* __restrict__ R) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < k; ++j) R[n * j + i] = __dsub_rn(AX[n * j + i], __dmul_rn(lam[j], X[n * j + i]));
+}
+
 }  // namespace
+
+void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s) {
+  block_lincomb_k<<<grid_for(n, 256), 256, 0, s>>>(n, in, kin, C, kout, out);
+  SAIT_LAUNCHED();
+}
+void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s) {
+  block_sub_lincomb_k<<<grid_for(n, 256), 256, 0, s>>>(n, X, k, G, W);
+  SAIT_LAUNCHED();
+}
+void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
+                    cudaStream_t s) {
+  block_residual_k<<<grid_for(n, 256), 256, 0, s>>>(n, k, AX, X, lam, R);
+  SAIT_LAUNCHED();
+}
 
 int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
 

@@ -7,8 +7,10 @@
 // counts and residual histories are bitwise identical to the CPU restatement.
 #include <chrono>
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -27,6 +29,12 @@ void axpy(int64_t n, double a, const double* x, double* y, cudaStream_t s);
 void xpay(int64_t n, const double* x, double a, double* y, cudaStream_t s);
 void x_minus_y(int64_t n, const double* x, double* y, cudaStream_t s);
 void y_plus_x(int64_t n, const double* x, double* y, cudaStream_t s);
+void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s);
+void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
+void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
+                    cudaStream_t s);
+void pair_apply_block_internal(sait_pair_t p, const double* r, double* z, int64_t n, int64_t nvec, int layout,
+                               cudaStream_t s);
 
 namespace {
 
@@ -70,6 +78,123 @@ struct Scalars {
     dfree(part, s);
   }
 };
+
+// ---- small dense algebra for LOBPCG's Rayleigh-Ritz (host; the same
+// operation sequence as oracle/solvers.c so results agree bitwise).
+bool chol_lower(const double* G, int m, double* L) {
+  for (int i = 0; i < m * m; ++i) L[i] = 0.0;
+  for (int j = 0; j < m; ++j) {
+    double d = G[j * m + j];
+    for (int k = 0; k < j; ++k) d = d - L[j * m + k] * L[j * m + k];
+    if (!(d > 0.0)) return false;
+    const double ljj = std::sqrt(d);
+    L[j * m + j] = ljj;
+    for (int i = j + 1; i < m; ++i) {
+      double t = G[i * m + j];
+      for (int k = 0; k < j; ++k) t = t - L[i * m + k] * L[j * m + k];
+      L[i * m + j] = t / ljj;
+    }
+  }
+  return true;
+}
+
+void tri_lower_inv(const double* L, int m, double* Li) {
+  for (int i = 0; i < m * m; ++i) Li[i] = 0.0;
+  for (int j = 0; j < m; ++j) {
+    Li[j * m + j] = 1.0 / L[j * m + j];
+    for (int i = j + 1; i < m; ++i) {
+      double t = 0.0;
+      for (int k = j; k < i; ++k) t = t - L[i * m + k] * Li[k * m + j];
+      Li[i * m + j] = t / L[i * m + i];
+    }
+  }
+}
+
+// cyclic Jacobi on symmetric F (destroyed): ascending eigenvalues w, vectors in Q's columns
+void jacobi_eig(double* F, int m, double* w, double* Q) {
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) Q[i * m + j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) off = off + F[p * m + q] * F[p * m + q];
+    if (off == 0.0) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = F[p * m + q];
+        if (apq == 0.0) continue;
+        const double app = F[p * m + p], aqq = F[q * m + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < m; ++k) {
+          const double fkp = F[k * m + p], fkq = F[k * m + q];
+          F[k * m + p] = c * fkp - s * fkq;
+          F[k * m + q] = s * fkp + c * fkq;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double fpk = F[p * m + k], fqk = F[q * m + k];
+          F[p * m + k] = c * fpk - s * fqk;
+          F[q * m + k] = s * fpk + c * fqk;
+        }
+        F[p * m + q] = 0.0;
+        F[q * m + p] = 0.0;
+        for (int k = 0; k < m; ++k) {
+          const double qkp = Q[k * m + p], qkq = Q[k * m + q];
+          Q[k * m + p] = c * qkp - s * qkq;
+          Q[k * m + q] = s * qkp + c * qkq;
+        }
+      }
+  }
+  std::vector<int> idx(m);
+  for (int i = 0; i < m; ++i) idx[i] = i;
+  for (int i = 0; i < m; ++i) {  // selection sort, ties keep index order
+    int best = i;
+    for (int j = i + 1; j < m; ++j)
+      if (F[idx[j] * m + idx[j]] < F[idx[best] * m + idx[best]]) best = j;
+    std::swap(idx[i], idx[best]);
+  }
+  std::vector<double> Qs(static_cast<size_t>(m) * m);
+  for (int j = 0; j < m; ++j) {
+    w[j] = F[idx[j] * m + idx[j]];
+    for (int i = 0; i < m; ++i) Qs[i * m + j] = Q[i * m + idx[j]];
+  }
+  std::copy(Qs.begin(), Qs.end(), Q);
+}
+
+// k lowest B-orthonormal Ritz vectors of (GA, GB), m x m; C is m x k row-major
+bool rayleigh_ritz(const double* GA, const double* GB, int m, int k, double* C, double* mu) {
+  std::vector<double> L(m * m), Li(m * m), T(m * m), F(m * m), Q(m * m), w(m);
+  if (!chol_lower(GB, m, L.data())) return false;
+  tri_lower_inv(L.data(), m, Li.data());
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < m; ++q) t = t + Li[i * m + q] * GA[q * m + j];
+      T[i * m + j] = t;
+    }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < m; ++q) t = t + T[i * m + q] * Li[j * m + q];
+      F[i * m + j] = t;
+    }
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) {
+      const double a = 0.5 * (F[i * m + j] + F[j * m + i]);
+      F[i * m + j] = a;
+      F[j * m + i] = a;
+    }
+  jacobi_eig(F.data(), m, w.data(), Q.data());
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < k; ++j) {
+      double t = 0.0;
+      for (int q = 0; q < m; ++q) t = t + Li[q * m + i] * Q[q * m + j];
+      C[i * k + j] = t;
+    }
+  for (int j = 0; j < k; ++j) mu[j] = w[j];
+  return true;
+}
 
 }  // namespace
 }  // namespace sait
@@ -305,6 +430,167 @@ int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int64
     SAIT_CUDA(cudaStreamSynchronize(s));
     if (dev != A->dev) cudaSetDevice(dev);
     if (breakdown) sait::throw_runtime("pcg: breakdown, p'Ap <= 0 at iteration " + std::to_string(its));
+  });
+}
+
+int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, double* h_evals,
+                double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream) {
+  return solver_guard([&] {
+    if (!A || !h_evals || !iterations) sait::throw_invalid("lobpcg: null argument");
+    const sait::DevCsr& a = A->m;
+    const int64_t n = a.nrows;
+    const int k = nev;
+    if (a.ncols != n) sait::throw_invalid("lobpcg: operator is not square");
+    if (k < 1 || k > 16) sait::throw_invalid("lobpcg: block size must be in [1, 16]");
+    if (M && sait::pair_dim(M) != n) sait::throw_invalid("lobpcg: preconditioner dimension mismatch");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != A->dev) SAIT_CUDA(cudaSetDevice(A->dev));
+    cudaStream_t s = sait::as_stream(stream);
+    sait::Operator op(a, s);
+    const int64_t blk = static_cast<int64_t>(k) * n;
+    double* S = sait::dalloc<double>(3 * blk, s);   // [X W P]
+    double* AS = sait::dalloc<double>(3 * blk, s);  // [AX AW AP]
+    double* R = sait::dalloc<double>(blk, s);
+    double* tmp = sait::dalloc<double>(4 * blk, s);
+    double* dsmall = sait::dalloc<double>(48 * 48, s);
+    sait::Scalars sc(n, 48 * 48, 48, s);
+    double *X = S, *W = S + blk, *P = S + 2 * blk;
+    double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
+    auto block_spmv = [&](const double* in, double* out) {
+      for (int j = 0; j < k; ++j) op.apply(in + static_cast<int64_t>(j) * n, out + static_cast<int64_t>(j) * n, s);
+    };
+    // G[a][b] = S_a . Y_b (canonical dots), row-major ka x kb on the host
+    auto gram = [&](const double* Sa, int ka, const double* Yb, int kb, std::vector<double>& G) {
+      G.assign(static_cast<size_t>(ka) * kb, 0.0);
+      for (int r = 0; r < ka; ++r) sait::multi_dot(n, Sa + static_cast<int64_t>(r) * n, Yb, n, kb, sc.d + r * kb,
+                                                   sc.part, s, false);
+      sc.fetch(ka * kb, s);
+      std::copy(sc.h.begin(), sc.h.begin() + static_cast<size_t>(ka) * kb, G.begin());
+    };
+    auto lincomb = [&](const double* in, int kin, const double* C, int kout, double* out) {
+      SAIT_CUDA(cudaMemcpyAsync(dsmall, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));
+      sait::block_lincomb(n, in, kin, dsmall, kout, out, s);
+      SAIT_CUDA(cudaStreamSynchronize(s));  // dsmall is reused
+    };
+    auto cholqr = [&](double* Y, double* AY) {
+      std::vector<double> G, L(k * k), Li(k * k), Ri(k * k);
+      gram(Y, k, Y, k, G);
+      if (!sait::chol_lower(G.data(), k, L.data())) return false;
+      sait::tri_lower_inv(L.data(), k, Li.data());
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) Ri[i * k + j] = Li[j * k + i];
+      lincomb(Y, k, Ri.data(), k, tmp);
+      SAIT_CUDA(cudaMemcpyAsync(Y, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+      if (AY) {
+        lincomb(AY, k, Ri.data(), k, tmp);
+        SAIT_CUDA(cudaMemcpyAsync(AY, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+      }
+      return true;
+    };
+    std::vector<double> GA, GB, C(48 * 16), lam(48);
+    {  // X0 ~ U[-1,1], column j from seed (seed * 1000 + j)
+      std::vector<double> h(n);
+      for (int j = 0; j < k; ++j) {
+        sait_fill_uniform_pm1(seed * 1000 + static_cast<uint64_t>(j), n, h.data());
+        SAIT_CUDA(cudaMemcpyAsync(X + static_cast<int64_t>(j) * n, h.data(), sizeof(double) * n,
+                                  cudaMemcpyHostToDevice, s));
+        SAIT_CUDA(cudaStreamSynchronize(s));
+      }
+    }
+    block_spmv(X, AX);
+    bool failed = false;
+    std::string why;
+    gram(X, k, X, k, GB);
+    gram(X, k, AX, k, GA);
+    int it = 0;
+    bool conv = false, have_p = false;
+    if (!sait::rayleigh_ritz(GA.data(), GB.data(), k, k, C.data(), lam.data())) {
+      failed = true;
+      why = "lobpcg: initial block is rank deficient";
+    } else {
+      lincomb(X, k, C.data(), k, tmp);
+      SAIT_CUDA(cudaMemcpyAsync(X, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+      lincomb(AX, k, C.data(), k, tmp);
+      SAIT_CUDA(cudaMemcpyAsync(AX, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+      for (it = 0; it <= maxit; ++it) {
+        SAIT_CUDA(cudaMemcpyAsync(dsmall, lam.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+        sait::block_residual(n, k, AX, X, dsmall, R, s);
+        for (int j = 0; j < k; ++j)
+          sait::multi_dot(n, R + static_cast<int64_t>(j) * n, R + static_cast<int64_t>(j) * n, n, 1, sc.d + j, sc.part,
+                          s, true);
+        sc.fetch(k, s);
+        conv = true;
+        for (int j = 0; j < k; ++j) {
+          if (h_resnorms) h_resnorms[static_cast<int64_t>(it) * k + j] = sc.h[j];
+          if (!(sc.h[j] <= tol)) conv = false;
+        }
+        if (conv || it == maxit) break;
+        if (M) sait::pair_apply_block_internal(M, R, W, n, k, 0, s);
+        else SAIT_CUDA(cudaMemcpyAsync(W, R, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        std::vector<double> G1;
+        gram(X, k, W, k, G1);
+        SAIT_CUDA(cudaMemcpyAsync(dsmall, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
+        sait::block_sub_lincomb(n, X, k, dsmall, W, s);
+        SAIT_CUDA(cudaStreamSynchronize(s));
+        if (!cholqr(W, nullptr)) {
+          failed = true;
+          why = "lobpcg: preconditioned residual block is rank deficient";
+          break;
+        }
+        block_spmv(W, AW);
+        const bool use_p = have_p && cholqr(P, AP);
+        int m = use_p ? 3 * k : 2 * k;
+        bool ok = false;
+        while (true) {
+          gram(S, m, S, m, GB);
+          gram(S, m, AS, m, GA);
+          for (int i = 0; i < m; ++i)
+            for (int j = i + 1; j < m; ++j) {
+              const double s2 = 0.5 * (GA[i * m + j] + GA[j * m + i]);
+              GA[i * m + j] = s2;
+              GA[j * m + i] = s2;
+            }
+          if (sait::rayleigh_ritz(GA.data(), GB.data(), m, k, C.data(), lam.data())) {
+            ok = true;
+            break;
+          }
+          if (m == 3 * k) {
+            m = 2 * k;
+            continue;
+          }
+          break;
+        }
+        if (!ok) {
+          failed = true;
+          why = "lobpcg: Gram matrix not positive definite";
+          break;
+        }
+        lincomb(W, m - k, C.data() + k * k, k, tmp);
+        lincomb(AW, m - k, C.data() + k * k, k, tmp + blk);
+        lincomb(S, m, C.data(), k, tmp + 2 * blk);
+        lincomb(AS, m, C.data(), k, tmp + 3 * blk);
+        SAIT_CUDA(cudaMemcpyAsync(P, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        SAIT_CUDA(cudaMemcpyAsync(AP, tmp + blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        SAIT_CUDA(cudaMemcpyAsync(X, tmp + 2 * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        SAIT_CUDA(cudaMemcpyAsync(AX, tmp + 3 * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        have_p = true;
+      }
+    }
+    for (int j = 0; j < k; ++j) h_evals[j] = lam[j];
+    if (d_evecs) SAIT_CUDA(cudaMemcpyAsync(d_evecs, X, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+    *iterations = it;
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    sait::dfree(S, s);
+    sait::dfree(AS, s);
+    sait::dfree(R, s);
+    sait::dfree(tmp, s);
+    sait::dfree(dsmall, s);
+    sc.release(s);
+    op.release(s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    if (dev != A->dev) cudaSetDevice(dev);
+    if (failed) sait::throw_runtime(why);
   });
 }
 

@@ -61,3 +61,31 @@ def pcg(A, M, b, tol: float = 1e-10, maxit: int = 10000, stream=None):
     rc = N.lib.sait_pcg(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), float(tol), int(maxit),
                         hist.ctypes.data_as(N.PD), C.byref(st), s)
     return _finish(rc, st, hist, x, on_dev)
+
+
+@dataclass
+class EigResult:
+    """SPEC.md EigResult: eigenvalues ascending, eigenvectors (n, nev)."""
+
+    eigenvalues: np.ndarray
+    eigenvectors: object
+    iterations: int
+    residual_history: np.ndarray
+
+
+def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, stream=None, host_vectors=True):
+    import torch
+
+    dA = A if isinstance(A, DeviceCsr) else DeviceCsr.upload(A, stream)
+    n = dA.nrows
+    evals = np.zeros(nev)
+    vecs = torch.empty((nev, n), dtype=torch.float64, device="cuda")  # column-major n x nev
+    res = np.zeros((maxit + 1) * nev)
+    its = C.c_int()
+    s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    mh = M.handle if M is not None else None
+    N.check(N.lib.sait_lobpcg(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed), evals.ctypes.data_as(N.PD),
+                              vecs.data_ptr(), res.ctypes.data_as(N.PD), C.byref(its), s))
+    it = its.value
+    v = vecs.T
+    return EigResult(evals, v.cpu().numpy() if host_vectors else v, it, res[: (it + 1) * nev].reshape(it + 1, nev))

@@ -23,7 +23,7 @@ HEADERS := include/sait_c.h $(wildcard $(CSRC)/*.cuh)
 SHIM_SRCS := $(wildcard $(CSRC)/shim/*.cpp)
 SHIM_HDRS := $(wildcard include/saitprec/*.hpp)
 
-all: $(PKG)/libsait_b200.so shim oracle
+all: $(PKG)/libsait_b200.so shim $(BUILD)/shim_check oracle
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HEADERS)
 	@mkdir -p $(BUILD)
@@ -42,6 +42,11 @@ $(PKG)/libsaitprec_b200.so: $(SHIM_SRCS) $(SHIM_HDRS) $(PKG)/libsait_b200.so inc
 	@if [ -n "$(SHIM_SRCS)" ]; then \
 	  g++ $(CXXFLAGS) -shared -o $@ $(SHIM_SRCS) -L$(PKG) -lsait_b200 -Wl,-rpath,'$$ORIGIN'; \
 	fi
+
+# a program written against the reference's saitprec:: headers, linked to the shim
+$(BUILD)/shim_check: tests/cpp/shim_check.cpp $(PKG)/libsaitprec_b200.so $(SHIM_HDRS)
+	@mkdir -p $(BUILD)
+	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lsaitprec_b200 -lsait_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle:
 	$(MAKE) -C oracle

@@ -135,9 +135,19 @@ int sait_jacobi_split(sait_dcsr_t t, int lower, double *d_inv_diag, sait_stream_
  * returns the approximate inverse M = poly(tT) D^-1 of the triangular T. */
 int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec *spec, sait_stream_t stream,
                sait_dcsr_t *m_out, sait_build_stats *stats);
+/* sait.hpp:53 / sait.cpp:75-88 with an empty DropRule: the undropped
+ * unit-diagonal polynomial in tT (no D^-1 scaling), from the iteration
+ * matrix tt of a JacobiSplit. */
+int sait_polynomial(sait_dcsr_t tt, int steps, sait_stream_t stream, sait_dcsr_t *m_out,
+                    sait_build_stats *stats);
 /* sait.hpp:64 / sait.cpp:103-111 (result: a pattern, values NULL). */
 int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_stream_t stream,
                              sait_dcsr_t *pattern_out);
+
+/* sait.hpp:73 / sait.cpp:138-159: k Jacobi sweeps x <- tT x + D^-1 b from
+ * x = 0 on device vectors (the paper's section 4.3 comparison variant). */
+int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double *d_b, int sweeps, double *d_x,
+                             sait_stream_t stream);
 
 /* ------------------------------------------------ pair preconditioner ---
  * SaitPairPreconditioner (preconditioner.hpp:54-68, preconditioner.cpp:34-49). */
@@ -218,6 +228,13 @@ void sait_fill_uniform_pm1(uint64_t seed, int64_t n, double *out);
 
 /* ------------------------------------------------------------ utility --- */
 int sait_device_synchronize(void);
+/* Device memory and streams for hosts that do not link the CUDA runtime
+ * (e.g. the C++ saitprec:: shim).  kind: 1 H2D, 2 D2H, 3 D2D (synchronous). */
+int sait_device_alloc(size_t bytes, void **ptr);
+void sait_device_free(void *ptr);
+int sait_memcpy(void *dst, const void *src, size_t bytes, int kind);
+int sait_stream_create(sait_stream_t *stream);
+void sait_stream_destroy(sait_stream_t stream);
 /* Pinned host buffers for the host-vector entry points. */
 int sait_host_alloc(size_t bytes, void **ptr);
 void sait_host_free(void *ptr);

@@ -96,7 +96,9 @@ PROTOTYPES = {
     "sait_transpose": (C.c_int, [VP, VP, C.POINTER(VP)]),
     "sait_jacobi_split": (C.c_int, [VP, C.c_int, VP, VP, C.POINTER(VP)]),
     "sait_build": (C.c_int, [VP, C.c_int, C.POINTER(DropSpec), VP, C.POINTER(VP), C.POINTER(BuildStats)]),
+    "sait_polynomial": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_pat_capture_pattern": (C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
+    "sait_jacobi_sweeps_apply": (C.c_int, [VP, C.c_int, VP, C.c_int, VP, VP]),
     "sait_pair_create": (C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
     "sait_pair_info": (C.c_int, [VP, P64, P64]),
     "sait_pair_apply": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
@@ -116,6 +118,11 @@ PROTOTYPES = {
     "sait_problem_synthetic_lower": (C.c_int, [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.POINTER(HostCsr)]),
     "sait_fill_uniform_pm1": (None, [C.c_uint64, C.c_int64, PD]),
     "sait_device_synchronize": (C.c_int, []),
+    "sait_device_alloc": (C.c_int, [C.c_size_t, C.POINTER(VP)]),
+    "sait_device_free": (None, [VP]),
+    "sait_memcpy": (C.c_int, [VP, VP, C.c_size_t, C.c_int]),
+    "sait_stream_create": (C.c_int, [C.POINTER(VP)]),
+    "sait_stream_destroy": (None, [VP]),
     "sait_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(VP)]),
     "sait_host_free": (None, [VP]),
     "sait_kernel_launch_count": (C.c_int64, []),

@@ -150,7 +150,29 @@ __global__ void block_residual_k(int64_t n, int k, const double* __restrict__ AX
   for (int j = 0; j < k; ++j) R[n * j + i] = __dsub_rn(AX[n * j + i], __dmul_rn(lam[j], X[n * j + i]));
 }
 
+__global__ void hadamard_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __dmul_rn(a[i], b[i]);
+}
+__global__ void add_into_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __dadd_rn(a[i], b[i]);
+}
+
 }  // namespace
+
+void hadamard(int64_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  hadamard_k<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, out);
+  SAIT_LAUNCHED();
+}
+void add_into(int64_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  add_into_k<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, out);
+  SAIT_LAUNCHED();
+}
 
 void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s) {
   block_lincomb_k<<<grid_for(n, 256), 256, 0, s>>>(n, in, kin, C, kout, out);

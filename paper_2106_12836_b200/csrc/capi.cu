@@ -402,6 +402,38 @@ int sait_device_synchronize(void) {
   return guarded([] { SAIT_CUDA(cudaDeviceSynchronize()); });
 }
 
+int sait_device_alloc(size_t bytes, void** ptr) {
+  return guarded([&] {
+    need(ptr, "sait_device_alloc");
+    init_device_pool();
+    cudaError_t e = cudaMalloc(ptr, (bytes ? bytes : 1) + 256);
+    if (e == cudaErrorMemoryAllocation) throw sait::Error(SAIT_ERR_NOMEM, "out of device memory");
+    SAIT_CUDA(e);
+  });
+}
+void sait_device_free(void* ptr) {
+  if (ptr) cudaFree(ptr);
+}
+int sait_memcpy(void* dst, const void* src, size_t bytes, int kind) {
+  return guarded([&] {
+    if (bytes == 0) return;
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                             : kind == 2 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    SAIT_CUDA(cudaMemcpy(dst, src, bytes, k));
+  });
+}
+int sait_stream_create(sait_stream_t* stream) {
+  return guarded([&] {
+    cudaStream_t s;
+    SAIT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream = s;
+  });
+}
+void sait_stream_destroy(sait_stream_t stream) {
+  if (stream) cudaStreamDestroy(sait::as_stream(stream));
+}
+
 int sait_host_alloc(size_t bytes, void** ptr) {
   return guarded([&] { SAIT_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1)); });
 }
@@ -668,6 +700,33 @@ int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec* spec, sait_stream
   });
 }
 
+int sait_polynomial(sait_dcsr_t tt, int steps, sait_stream_t stream, sait_dcsr_t* m_out, sait_build_stats* stats) {
+  return guarded([&] {
+    need(tt, "sait_polynomial");
+    need(m_out, "sait_polynomial(out)");
+    if (steps < 1) sait::throw_invalid("sait_polynomial: steps must be >= 1");
+    if (tt->m.nrows != tt->m.ncols) sait::throw_invalid("add_identity: matrix is not square");
+    DeviceGuard g(tt->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr ttT = sait::transpose(tt->m, nullptr, s);
+    sait_drop_spec sp{SAIT_DROP_NONE, 0.0, steps, 0, 0, 0.0};
+    BuildOut bo = run_recursion(ttT, sp, nullptr, s);
+    sait::free_csr(ttT, s);
+    sait::DevCsr m = sait::transpose(bo.mt, nullptr, s);
+    sait::free_csr(bo.mt, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      stats->steps_run = bo.steps_run;
+      stats->stabilized = bo.stabilized ? 1 : 0;
+      stats->nnz_out = m.nnz;
+      stats->products = bo.products;
+      stats->seconds = 0.0;
+    }
+    *m_out = wrap(m);
+  });
+}
+
 int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_stream_t stream,
                              sait_dcsr_t* pattern_out) {
   return guarded([&] {
@@ -704,6 +763,39 @@ int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_s
     pat.v = nullptr;
     SAIT_CUDA(cudaStreamSynchronize(s));
     *pattern_out = wrap(pat);
+  });
+}
+
+int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double* d_b, int sweeps, double* d_x,
+                             sait_stream_t stream) {
+  return guarded([&] {
+    need(t, "jacobi_sweeps_apply");
+    if (sweeps < 1) sait::throw_invalid("jacobi_sweeps_apply: sweeps must be >= 1");
+    DeviceGuard g(t->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    const int64_t n = t->m.nrows;
+    double* inv = sait::dalloc<double>(n, s);
+    sait::DevCsr tt;
+    try {
+      tt = sait::jacobi_split(t->m, lower != 0, inv, s);
+    } catch (...) {
+      sait::dfree(inv, s);
+      throw;
+    }
+    double* scaled = sait::dalloc<double>(n, s);
+    double* tmp = sait::dalloc<double>(n, s);
+    sait::hadamard(n, inv, d_b, scaled, s);  // D^-1 b  (inv * b)
+    SAIT_CUDA(cudaMemcpyAsync(d_x, scaled, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    for (int k = 1; k < sweeps; ++k) {
+      sait::spmv(tt, d_x, tmp, s);
+      sait::add_into(n, tmp, scaled, d_x, s);  // x = tmp + scaled
+    }
+    sait::free_csr(tt, s);
+    sait::dfree(inv, s);
+    sait::dfree(scaled, s);
+    sait::dfree(tmp, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
   });
 }
 

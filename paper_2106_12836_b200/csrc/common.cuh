@@ -184,4 +184,8 @@ void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaSt
 void transpose_block(const double* in, double* out, int64_t n, int nvec, bool to_rowmajor,
                      cudaStream_t s);
 
+// blas.cu (elementwise helpers)
+void hadamard(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a * b
+void add_into(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a + b
+
 }  // namespace sait

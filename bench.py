@@ -198,17 +198,23 @@ def cpu_baseline_sample(ML_host, MU_host, n):
     ml = Csr(ML_host.nrows, ML_host.ncols, ML_host.row_ptr, ML_host.col_idx, ML_host.values)
     mu = Csr(MU_host.nrows, MU_host.ncols, MU_host.row_ptr, MU_host.col_idx, MU_host.values)
     p = lib.ref_pair_create(C.byref(_in(ml)), C.byref(_in(mu)))
-    sample = int(os.environ.get("SAIT_CPU_SAMPLE", "20"))
-    r = np.stack([O.uniform_pm1(SEED0 + i, n) for i in range(sample)])
+    # bounded sample: whole 100-vector steps until ~10 s of CPU work (max 30 steps)
+    budget = float(os.environ.get("SAIT_CPU_SECONDS", "10"))
+    r = np.stack([O.uniform_pm1(SEED0 + i, n) for i in range(NVEC)])
     z = np.empty_like(r)
     lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, 2)  # warm
-    t = lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, sample)
+    t, steps = 0.0, 0
+    while t < budget and steps < 30:
+        t += lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, NVEC)
+        steps += 1
     lib.ref_pair_destroy.argtypes = [C.c_void_p]
     lib.ref_pair_destroy(p)
     B = b_pair(n, ml.nnz, mu.nnz)
-    return {"value": sample * B / t / 1e9, "unit": "GB/s", "cores": int(lib.ref_max_threads()), "kind": "reference",
-            "sample": f"{sample} of the 100 vectors through the reference SaitPairPreconditioner::apply "
-                      f"(OpenMP, {int(lib.ref_max_threads())} threads), {t:.2f} s"}
+    cores = int(lib.ref_max_threads())
+    return {"value": steps * NVEC * B / t / 1e9, "unit": "GB/s", "cores": cores, "kind": "reference",
+            "sample": f"{steps} steps x 100 vectors through the reference SaitPairPreconditioner::apply "
+                      f"(oracle/_ref, OpenMP {cores} threads), {t:.1f} s",
+            "ms_per_step": 1e3 * t / steps}
 
 
 def run_b200(args):
@@ -317,7 +323,7 @@ def run_b200(args):
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "spmv_pipe",
+                "traffic": traffic, "kernel": "sell_spmv_kernel",
                 "per_launch_ms": {"M_L": kt["L"], "M_U": kt["U"]},
                 "algorithmic_bytes_per_launch": {"M_L": bytes_l, "M_U": bytes_u},
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)"}

@@ -127,6 +127,25 @@ typedef struct {
   double seconds;      /* device time of the whole build (CUDA events) */
 } sait_build_stats;
 
+/* Step-wise build over a block of COLUMNS [col0, col1) of M (multi-GPU column
+ * sharding).  A column of M evolves independently of the
+ * others, so a block needs no data from other blocks; only the reference's
+ * global early stop (sait.cpp:84-85) couples them: after every step the
+ * caller reduces `changed` across blocks (max) and calls ..._stop() when no
+ * block changed.  finish(transposed = 0) returns M[:, col0:col1] as an
+ * n x (col1 - col0) CSR (local column index = global - col0); transposed = 1
+ * returns that block's rows of M^T, i.e. a (col1 - col0) x n CSR.
+ * sait_build == one session over [0, n) with local early stop. */
+typedef struct sait_build_session_s *sait_build_session_t;
+int sait_build_session_create(sait_dcsr_t t, int lower, const sait_drop_spec *spec, int64_t col0,
+                              int64_t col1, sait_stream_t stream, sait_build_session_t *out);
+int sait_build_session_remaining(sait_build_session_t s);
+int sait_build_session_step(sait_build_session_t s, int *changed);
+int sait_build_session_stop(sait_build_session_t s);
+int sait_build_session_finish(sait_build_session_t s, int transposed, sait_dcsr_t *out,
+                              sait_build_stats *stats);
+void sait_build_session_destroy(sait_build_session_t s);
+
 /* sait.hpp:40 / sait.cpp:32-73: d_inv_diag (device, length n) receives 1/T[i,i];
  * *tt receives I - D^-1 T with no stored diagonal. */
 int sait_jacobi_split(sait_dcsr_t t, int lower, double *d_inv_diag, sait_stream_t stream,
@@ -148,6 +167,17 @@ int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_s
  * x = 0 on device vectors (the paper's section 4.3 comparison variant). */
 int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double *d_b, int sweeps, double *d_x,
                              sait_stream_t stream);
+
+/* ------------------------------------------------------- SpMV operator ---
+ * A prepared y = A x for a (possibly rectangular) device CSR: keeps the
+ * SELL-32 copy when the rows are regular enough (the apply's kernel), else the
+ * CSR kernels.  Bitwise equal to spmv (kernels.cpp:10-26).  Used for the
+ * local row blocks of the multi-GPU apply. */
+typedef struct sait_op_s *sait_op_t;
+int sait_operator_create(sait_dcsr_t a, int take_ownership, sait_op_t *out);
+int sait_operator_apply(sait_op_t op, const double *d_x, int64_t xlen, double *d_y, int64_t ylen,
+                        sait_stream_t stream);
+void sait_operator_destroy(sait_op_t op);
 
 /* ------------------------------------------------ pair preconditioner ---
  * SaitPairPreconditioner (preconditioner.hpp:54-68, preconditioner.cpp:34-49). */

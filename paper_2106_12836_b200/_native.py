@@ -94,6 +94,15 @@ PROTOTYPES = {
     "sait_drop_by_pattern": (C.c_int, [VP, VP, VP, C.POINTER(VP)]),
     "sait_scale_columns": (C.c_int, [VP, VP, C.c_int64, VP, C.POINTER(VP)]),
     "sait_transpose": (C.c_int, [VP, VP, C.POINTER(VP)]),
+    "sait_build_session_create": (C.c_int, [VP, C.c_int, C.POINTER(DropSpec), C.c_int64, C.c_int64, VP, C.POINTER(VP)]),
+    "sait_build_session_remaining": (C.c_int, [VP]),
+    "sait_build_session_step": (C.c_int, [VP, C.POINTER(C.c_int)]),
+    "sait_build_session_stop": (C.c_int, [VP]),
+    "sait_build_session_finish": (C.c_int, [VP, C.c_int, C.POINTER(VP), C.POINTER(BuildStats)]),
+    "sait_build_session_destroy": (None, [VP]),
+    "sait_operator_create": (C.c_int, [VP, C.c_int, C.POINTER(VP)]),
+    "sait_operator_apply": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
+    "sait_operator_destroy": (None, [VP]),
     "sait_jacobi_split": (C.c_int, [VP, C.c_int, VP, VP, C.POINTER(VP)]),
     "sait_build": (C.c_int, [VP, C.c_int, C.POINTER(DropSpec), VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_polynomial": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(BuildStats)]),

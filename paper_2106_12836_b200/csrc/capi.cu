@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,27 @@
 struct sait_dcsr_s {
   int dev = 0;
   sait::DevCsr m;
+};
+
+struct sait_op_s {
+  int dev = 0;
+  sait_dcsr_s* a = nullptr;
+  bool owns = false;
+  sait::SellMatrix sell;
+};
+
+namespace {
+class Recursion;
+}  // namespace
+struct sait_build_session_s {
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  int64_t c0 = 0, c1 = 0, n = 0;
+  double* inv = nullptr;
+  sait::DevCsr ttT;
+  int32_t* cap = nullptr;
+  Recursion* rec = nullptr;
+  cudaEvent_t e0 = nullptr;
 };
 
 struct sait_pair_s {
@@ -191,54 +213,96 @@ struct BuildOut {
 // The recursion of sait.cpp:75-136 in column form: row j of M_s^T is
 //   drop( sum_{k in M_{s-1}^T[j,:]} M_{s-1}^T[j,k] * tT^T[k,:] + e_j ),
 // bitwise equal to the reference's row form (same products, same
-// ascending-k order, commutative products).
+// ascending-k order, commutative products).  Rows [c0, c0 + rows) of M^T
+// (= a block of columns of M) evolve independently; only the early-stop
+// decision is global, so the caller supplies it between steps.
+class Recursion {
+ public:
+  Recursion(const sait::DevCsr& ttT, const sait_drop_spec& spec, const int32_t* cap, int64_t c0, int64_t rows,
+            cudaStream_t s)
+      : ttT_(ttT), spec_(spec), s_(s) {
+    a_ = sait::make_identity_rows(rows, c0, ttT.nrows, s);
+    epi_.add_identity = true;
+    epi_.diag_offset = c0;
+    if (spec.kind == SAIT_DROP_THRESHOLD) {
+      epi_.drop = 1;
+      epi_.tau = spec.tau;
+    } else if (spec.kind == SAIT_DROP_THRESHOLD_CAP) {
+      epi_.drop = 3;
+      epi_.tau = spec.tau;
+      epi_.cap = cap;
+    }
+    pattern_left_ = spec.kind == SAIT_DROP_PATTERN ? spec.pattern_steps : 0;
+    main_left_ = spec.kind == SAIT_DROP_PATTERN ? spec.refine_steps : spec.steps;
+    if (spec.kind == SAIT_DROP_PATTERN && pattern_left_ == 0) capture_pattern();
+  }
+  ~Recursion() {
+    sait::free_csr(a_, s_);
+    if (pattern_.rp) sait::free_csr(pattern_, s_);
+  }
+  int remaining() const { return pattern_left_ + main_left_; }
+  // One step; returns whether this block changed (pattern-growth steps of
+  // sait_pat have no early-stop check, sait.cpp:122-125: they report true).
+  bool step() {
+    if (pattern_left_ > 0) {
+      sait::Epilogue e0;
+      e0.add_identity = true;
+      e0.diag_offset = epi_.diag_offset;
+      advance(sait::spgemm_fused(a_, ttT_, e0, s_));
+      if (--pattern_left_ == 0) capture_pattern();
+      return true;
+    }
+    epi_.qrp = a_.rp;
+    epi_.qci = a_.ci;
+    epi_.qv = a_.v;
+    sait::SpgemmResult r = sait::spgemm_fused(a_, ttT_, epi_, s_);
+    const bool changed = r.changed;
+    advance(std::move(r));
+    --main_left_;
+    return changed;
+  }
+  void stop_stabilized() {
+    stabilized_ = true;
+    main_left_ = 0;
+  }
+  BuildOut take() {
+    BuildOut o;
+    o.mt = a_;
+    a_ = sait::DevCsr{};
+    o.steps_run = steps_run_;
+    o.stabilized = stabilized_;
+    o.products = products_;
+    return o;
+  }
+
+ private:
+  void advance(sait::SpgemmResult&& r) {
+    products_ += r.products;
+    sait::free_csr(a_, s_);
+    a_ = r.c;
+    ++steps_run_;
+  }
+  void capture_pattern() {  // S = pattern(M_p) (sait.cpp:126)
+    pattern_ = sait::copy_csr(a_, s_);
+    epi_.drop = 2;
+    epi_.prp = pattern_.rp;
+    epi_.pci = pattern_.ci;
+  }
+  const sait::DevCsr& ttT_;
+  sait_drop_spec spec_;
+  cudaStream_t s_;
+  sait::DevCsr a_, pattern_;
+  sait::Epilogue epi_;
+  int pattern_left_ = 0, main_left_ = 0, steps_run_ = 0;
+  bool stabilized_ = false;
+  int64_t products_ = 0;
+};
+
 BuildOut run_recursion(const sait::DevCsr& ttT, const sait_drop_spec& spec, const int32_t* cap, cudaStream_t s) {
-  BuildOut out;
-  sait::DevCsr a = sait::make_identity(ttT.nrows, s);
-  sait::DevCsr pattern;  // pattern_steps iterate (PATTERN)
-  int steps = spec.steps;
-  sait::Epilogue epi;
-  epi.add_identity = true;
-  if (spec.kind == SAIT_DROP_PATTERN) {
-    sait::Epilogue e0;
-    e0.add_identity = true;
-    for (int k = 0; k < spec.pattern_steps; ++k) {  // sait.cpp:122-125, no early stop
-      sait::SpgemmResult r = sait::spgemm_fused(a, ttT, e0, s);
-      out.products += r.products;
-      sait::free_csr(a, s);
-      a = r.c;
-      ++out.steps_run;
-    }
-    pattern = sait::copy_csr(a, s);
-    epi.drop = 2;
-    epi.prp = pattern.rp;
-    epi.pci = pattern.ci;
-    steps = spec.refine_steps;
-  } else if (spec.kind == SAIT_DROP_THRESHOLD) {
-    epi.drop = 1;
-    epi.tau = spec.tau;
-  } else if (spec.kind == SAIT_DROP_THRESHOLD_CAP) {
-    epi.drop = 3;
-    epi.tau = spec.tau;
-    epi.cap = cap;
-  }
-  for (int k = 0; k < steps; ++k) {  // sait.cpp:80-86 / :128-134
-    epi.qrp = a.rp;
-    epi.qci = a.ci;
-    epi.qv = a.v;
-    sait::SpgemmResult r = sait::spgemm_fused(a, ttT, epi, s);
-    out.products += r.products;
-    sait::free_csr(a, s);
-    a = r.c;
-    ++out.steps_run;
-    if (!r.changed) {
-      out.stabilized = true;
-      break;
-    }
-  }
-  if (pattern.rp) sait::free_csr(pattern, s);
-  out.mt = a;
-  return out;
+  Recursion r(ttT, spec, cap, 0, ttT.nrows, s);
+  while (r.remaining() > 0)
+    if (!r.step()) r.stop_stabilized();
+  return r.take();
 }
 
 void check_spec(const sait_drop_spec* spec) {
@@ -642,52 +706,92 @@ int sait_jacobi_split(sait_dcsr_t t, int lower, double* d_inv_diag, sait_stream_
   });
 }
 
-int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec* spec, sait_stream_t stream, sait_dcsr_t* m_out,
-               sait_build_stats* stats) {
+int sait_build_session_create(sait_dcsr_t t, int lower, const sait_drop_spec* spec, int64_t col0, int64_t col1,
+                              sait_stream_t stream, sait_build_session_t* out) {
   return guarded([&] {
     need(t, "sait_build");
-    need(m_out, "sait_build(out)");
+    need(out, "sait_build(out)");
     check_spec(spec);
     DeviceGuard g(t->dev);
     init_device_pool();
-    cudaStream_t s = sait::as_stream(stream);
     const int64_t n = t->m.nrows;
-    cudaEvent_t e0, e1;
-    SAIT_CUDA(cudaEventCreate(&e0));
-    SAIT_CUDA(cudaEventCreate(&e1));
-    SAIT_CUDA(cudaEventRecord(e0, s));
-    double* inv = sait::dalloc<double>(n, s);
+    if (col0 < 0 || col1 < col0 || col1 > n) sait::throw_invalid("sait_build: bad column block");
+    auto* ss = new sait_build_session_s;
+    ss->dev = t->dev;
+    ss->s = sait::as_stream(stream);
+    ss->c0 = col0;
+    ss->c1 = col1;
+    ss->n = n;
+    cudaStream_t s = ss->s;
+    SAIT_CUDA(cudaEventCreate(&ss->e0));
+    SAIT_CUDA(cudaEventRecord(ss->e0, s));
+    ss->inv = sait::dalloc<double>(n, s);
     sait::DevCsr tt;
     try {
-      tt = sait::jacobi_split(t->m, lower != 0, inv, s);
+      tt = sait::jacobi_split(t->m, lower != 0, ss->inv, s);
+      if (spec->kind != SAIT_DROP_PATTERN && spec->steps < 1) {
+        sait::free_csr(tt, s);
+        sait::throw_invalid("sait_polynomial: steps must be >= 1");
+      }
     } catch (...) {
-      sait::dfree(inv, s);
+      sait::dfree(ss->inv, s);
+      cudaEventDestroy(ss->e0);
+      delete ss;
       throw;
     }
-    if (spec->kind != SAIT_DROP_PATTERN && spec->steps < 1) {
-      sait::free_csr(tt, s);
-      sait::dfree(inv, s);
-      sait::throw_invalid("sait_polynomial: steps must be >= 1");
-    }
-    sait::DevCsr ttT = sait::transpose(tt, nullptr, s);
+    ss->ttT = sait::transpose(tt, nullptr, s);
     sait::free_csr(tt, s);
-    int32_t* cap = nullptr;
     if (spec->kind == SAIT_DROP_THRESHOLD_CAP) {
-      cap = sait::dalloc<int32_t>(n, s);
-      sait::column_caps(t->m, spec->cap_factor, cap, s);
+      ss->cap = sait::dalloc<int32_t>(n, s);
+      sait::column_caps(t->m, spec->cap_factor, ss->cap, s);
     }
-    BuildOut bo = run_recursion(ttT, *spec, cap, s);
-    sait::free_csr(ttT, s);
-    sait::dfree(cap, s);
-    // M = (M^T)^T D^-1: column j of M scaled by inv_diag[j] (kernels.cpp:236-246)
-    sait::DevCsr m = sait::transpose(bo.mt, inv, s);
+    ss->rec = new Recursion(ss->ttT, *spec, ss->cap, col0, col1 - col0, s);
+    *out = ss;
+  });
+}
+
+int sait_build_session_remaining(sait_build_session_t ss) { return ss && ss->rec ? ss->rec->remaining() : 0; }
+
+int sait_build_session_step(sait_build_session_t ss, int* changed) {
+  return guarded([&] {
+    need(ss, "sait_build_session_step");
+    DeviceGuard g(ss->dev);
+    if (!ss->rec || ss->rec->remaining() == 0) sait::throw_invalid("sait_build_session_step: no steps left");
+    const bool ch = ss->rec->step();
+    if (changed) *changed = ch ? 1 : 0;
+  });
+}
+
+int sait_build_session_stop(sait_build_session_t ss) {
+  return guarded([&] {
+    need(ss, "sait_build_session_stop");
+    ss->rec->stop_stabilized();
+  });
+}
+
+int sait_build_session_finish(sait_build_session_t ss, int transposed, sait_dcsr_t* out, sait_build_stats* stats) {
+  return guarded([&] {
+    need(ss, "sait_build_session_finish");
+    need(out, "sait_build_session_finish(out)");
+    DeviceGuard g(ss->dev);
+    cudaStream_t s = ss->s;
+    BuildOut bo = ss->rec->take();
+    sait::DevCsr m;
+    // column j of M is scaled by inv_diag[j] (kernels.cpp:236-246); rows of the
+    // M^T block are the global columns c0 + i
+    if (transposed) {
+      m = sait::copy_csr(bo.mt, s);
+      sait::scale_rows(m, ss->inv + ss->c0, s);
+    } else {
+      m = sait::transpose(bo.mt, ss->inv + ss->c0, s);
+    }
     sait::free_csr(bo.mt, s);
-    sait::dfree(inv, s);
+    cudaEvent_t e1;
+    SAIT_CUDA(cudaEventCreate(&e1));
     SAIT_CUDA(cudaEventRecord(e1, s));
     SAIT_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;
-    SAIT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
+    SAIT_CUDA(cudaEventElapsedTime(&ms, ss->e0, e1));
     cudaEventDestroy(e1);
     if (stats) {
       stats->steps_run = bo.steps_run;
@@ -696,8 +800,38 @@ int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec* spec, sait_stream
       stats->products = bo.products;
       stats->seconds = ms * 1e-3;
     }
-    *m_out = wrap(m);
+    *out = wrap(m);
   });
+}
+
+void sait_build_session_destroy(sait_build_session_t ss) {
+  if (!ss) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ss->dev);
+  delete ss->rec;
+  sait::free_csr(ss->ttT, ss->s);
+  sait::dfree(ss->inv, ss->s);
+  sait::dfree(ss->cap, ss->s);
+  cudaStreamSynchronize(ss->s);
+  cudaEventDestroy(ss->e0);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete ss;
+}
+
+int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec* spec, sait_stream_t stream, sait_dcsr_t* m_out,
+               sait_build_stats* stats) {
+  sait_build_session_t ss = nullptr;
+  int rc = sait_build_session_create(t, lower, spec, 0, t ? t->m.nrows : 0, stream, &ss);
+  if (rc) return rc;
+  while (rc == SAIT_OK && sait_build_session_remaining(ss) > 0) {
+    int changed = 1;
+    rc = sait_build_session_step(ss, &changed);
+    if (rc == SAIT_OK && !changed) rc = sait_build_session_stop(ss);  // single block: local == global
+  }
+  if (rc == SAIT_OK) rc = sait_build_session_finish(ss, 0, m_out, stats);
+  sait_build_session_destroy(ss);
+  return rc;
 }
 
 int sait_polynomial(sait_dcsr_t tt, int steps, sait_stream_t stream, sait_dcsr_t* m_out, sait_build_stats* stats) {
@@ -797,6 +931,52 @@ int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double* d_b, int sw
     sait::dfree(tmp, s);
     SAIT_CUDA(cudaStreamSynchronize(s));
   });
+}
+
+// ------------------------------------------------------------ SpMV operator
+
+int sait_operator_create(sait_dcsr_t a, int take_ownership, sait_op_t* out) {
+  return guarded([&] {
+    need(a, "sait_operator_create");
+    need(out, "sait_operator_create(out)");
+    DeviceGuard g(a->dev);
+    init_device_pool();
+    auto* op = new sait_op_s;
+    op->dev = a->dev;
+    op->a = a;
+    op->owns = take_ownership != 0;
+    op->sell = sait::make_sell(a->m, nullptr);
+    *out = op;
+  });
+}
+
+int sait_operator_apply(sait_op_t op, const double* d_x, int64_t xlen, double* d_y, int64_t ylen,
+                        sait_stream_t stream) {
+  return guarded([&] {
+    need(op, "spmv");
+    const sait::DevCsr& m = op->a->m;
+    if (xlen != m.ncols)
+      sait::throw_invalid("spmv: vector length " + std::to_string(xlen) + " does not match ncols " +
+                          std::to_string(m.ncols));
+    if (ylen != m.nrows) sait::throw_invalid("spmv: output length mismatch");
+    DeviceGuard g(op->dev);
+    cudaStream_t s = sait::as_stream(stream);
+    if (op->sell.ok()) sait::sell_spmv(op->sell, d_x, d_y, s);
+    else sait::spmv(m, d_x, d_y, s);
+  });
+}
+
+void sait_operator_destroy(sait_op_t op) {
+  if (!op) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(op->dev);
+  cudaDeviceSynchronize();
+  sait::free_sell(op->sell, nullptr);
+  cudaDeviceSynchronize();
+  if (op->owns) sait_csr_free(op->a);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete op;
 }
 
 // -------------------------------------------------------- pair preconditioner

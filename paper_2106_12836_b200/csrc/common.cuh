@@ -99,8 +99,11 @@ void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStr
 void exclusive_scan_rows(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
 int64_t read_last(const int32_t* row_ptr, int64_t n, cudaStream_t s);  // syncs
 DevCsr make_identity(int64_t n, cudaStream_t s);
+// rows [0, rows) with a single 1.0 at column row + col0 (a block of I of order ncols)
+DevCsr make_identity_rows(int64_t rows, int64_t col0, int64_t ncols, cudaStream_t s);
 DevCsr transpose(const DevCsr& a, const double* row_scale, cudaStream_t s);
 void scale_columns(const DevCsr& a, const double* d, DevCsr& out, cudaStream_t s);
+void scale_rows(DevCsr& a, const double* d, cudaStream_t s);  // v *= d[row]
 DevCsr copy_csr(const DevCsr& a, cudaStream_t s);
 
 // split.cu
@@ -115,7 +118,8 @@ struct Epilogue {
   double tau = 0.0;
   const int32_t* prp = nullptr;  // pattern row_ptr (drop == 2)
   const int32_t* pci = nullptr;
-  const int32_t* cap = nullptr;  // per-row max entries incl. diagonal (drop == 3)
+  const int32_t* cap = nullptr;  // per-column max entries incl. diagonal (drop == 3), global index
+  int64_t diag_offset = 0;       // row i's diagonal sits at column i + diag_offset (column blocks)
   // stabilization check against a previous iterate with identical shape
   const int32_t* qrp = nullptr;
   const int32_t* qci = nullptr;

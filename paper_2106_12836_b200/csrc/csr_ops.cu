@@ -97,6 +97,16 @@ __global__ void identity_kernel(int64_t n, int32_t* rp, int32_t* ci, double* v) 
   if (i == 0) rp[n] = static_cast<int32_t>(n);
 }
 
+__global__ void identity_rows_kernel(int64_t rows, int64_t col0, int32_t* rp, int32_t* ci, double* v) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows) {
+    rp[i] = static_cast<int32_t>(i);
+    ci[i] = static_cast<int32_t>(col0 + i);
+    v[i] = 1.0;
+  }
+  if (i == 0) rp[rows] = static_cast<int32_t>(rows);
+}
+
 __global__ void count_cols(int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                            int32_t* __restrict__ cnt) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -193,6 +203,14 @@ __global__ void sort_row_global(int32_t row, const int32_t* __restrict__ rp, int
   }
 }
 
+__global__ void scale_rows_kernel(int64_t nrows, const int32_t* __restrict__ rp, double* __restrict__ v,
+                                  const double* __restrict__ d) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const double di = d[i];
+  for (int32_t e = rp[i]; e < rp[i + 1]; ++e) v[e] = __dmul_rn(v[e], di);
+}
+
 __global__ void scale_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci, const double* __restrict__ v,
                                   const double* __restrict__ d, double* __restrict__ out) {
   int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -240,6 +258,19 @@ DevCsr make_identity(int64_t n, cudaStream_t s) {
   m.ci = dalloc<int32_t>(n, s);
   m.v = dalloc<double>(n, s);
   identity_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(n, m.rp, m.ci, m.v);
+  SAIT_LAUNCHED();
+  return m;
+}
+
+DevCsr make_identity_rows(int64_t rows, int64_t col0, int64_t ncols, cudaStream_t s) {
+  DevCsr m;
+  m.nrows = rows;
+  m.ncols = ncols;
+  m.nnz = rows;
+  m.rp = dalloc<int32_t>(rows + 1, s);
+  m.ci = dalloc<int32_t>(rows, s);
+  m.v = dalloc<double>(rows, s);
+  identity_rows_kernel<<<grid_for(rows + 1, 256), 256, 0, s>>>(rows, col0, m.rp, m.ci, m.v);
   SAIT_LAUNCHED();
   return m;
 }
@@ -313,6 +344,12 @@ DevCsr transpose(const DevCsr& a, const double* row_scale, cudaStream_t s) {
 void scale_columns(const DevCsr& a, const double* d, DevCsr& out, cudaStream_t s) {
   if (a.nnz == 0) return;
   scale_cols_kernel<<<grid_for(a.nnz, 256), 256, 0, s>>>(a.nnz, a.ci, a.v, d, out.v);
+  SAIT_LAUNCHED();
+}
+
+void scale_rows(DevCsr& a, const double* d, cudaStream_t s) {
+  if (a.nrows == 0) return;
+  scale_rows_kernel<<<grid_for(a.nrows, 256), 256, 0, s>>>(a.nrows, a.rp, a.v, d);
   SAIT_LAUNCHED();
 }
 

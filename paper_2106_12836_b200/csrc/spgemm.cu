@@ -159,7 +159,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
     }
   }
   if (g.epi.add_identity && lane == 0) {
-    const int hs = find_or_insert(key, mask, shift, j);
+    const int hs = find_or_insert(key, mask, shift, j + static_cast<int32_t>(g.epi.diag_offset));
     const int s = hs & ~kFresh;
     val[s] = (hs & kFresh) ? 1.0 : __dadd_rn(val[s], 1.0);
   }
@@ -168,14 +168,15 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
 
 // Applies the drop rule in place (dropped slots become kDead) and returns
 // the number of surviving entries (same value in all lanes).
-__device__ int drop_row(const Args& g, int32_t j, int32_t* key, double* val, int logs, int lane) {
+__device__ int drop_row(const Args& g, int32_t row, int32_t* key, double* val, int logs, int lane) {
   const int slots = 1 << logs;
+  const int32_t j = row + static_cast<int32_t>(g.epi.diag_offset);  // the diagonal's column
   const int drop = g.epi.drop;
   const bool thr = (drop == 1 || drop == 3) && g.epi.tau != 0.0;
   int32_t pb = 0, pe = 0;
   if (drop == 2) {
-    pb = g.epi.prp[j];
-    pe = g.epi.prp[j + 1];
+    pb = g.epi.prp[row];
+    pe = g.epi.prp[row + 1];
   }
   int live = 0, offdiag = 0;
   for (int s = lane; s < slots; s += 32) {

@@ -1,0 +1,229 @@
+"""Multi-GPU plumbing: row-sharded SAIT apply with halo
+exchange, column-sharded SAIT build with a global early-stop reduction.
+
+One process per GPU; ``torch.distributed`` carries the data (NCCL over
+NVLink on B200, gloo in the CPU tests).  The kernels are the single-GPU ones
+(``sait_operator_*`` / ``sait_build_session_*`` in the C ABI).
+
+Apply.  Rank r owns rows [R_r, R_{r+1}) of both factors and of r, y, z.
+The columns its rows of a factor touch form one contiguous range; its local
+factor block is re-indexed into an extended vector ``[halo below | own |
+halo above]``.  Before M_L the missing r entries are received from the ranks
+that own them, before M_U the missing y entries — the only data-path
+communication.  For the banded SAIT factors the halo is one bandwidth
+(n^2 + n rows for an n^3 stencil) from the neighbouring rank(s).
+
+Build.  A column of M evolves independently, so rank r
+runs the recursion on the rows [C_r, C_{r+1}) of M^T; after each step the
+ranks all-reduce (MAX) their "changed" flag, keeping the reference's global
+early stop (sait.cpp:84-85) and therefore its step count and bits.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GROUP_ROWS = 256
+
+
+def row_bounds(n: int, world: int, align: int = GROUP_ROWS) -> list[int]:
+    """world + 1 boundaries splitting [0, n) into near-equal, aligned blocks."""
+    per = -(-n // world)
+    per = -(-per // align) * align
+    return [min(n, r * per) for r in range(world)] + [n]
+
+
+def column_span(row_ptr: np.ndarray, col_idx: np.ndarray, r0: int, r1: int) -> tuple[int, int]:
+    """[lo, hi) of the columns the rows [r0, r1) touch ((r0, r0) if none)."""
+    b, e = int(row_ptr[r0]), int(row_ptr[r1])
+    if e <= b:
+        return r0, r0
+    seg = col_idx[b:e]
+    return int(seg.min()), int(seg.max()) + 1
+
+
+@dataclass
+class HaloPlan:
+    rank: int
+    own: tuple[int, int]                 # rows owned (global)
+    lo: int                              # extended vector covers [lo, hi)
+    hi: int
+    recv: list[tuple[int, int, int]] = field(default_factory=list)  # (peer, g0, g1) into ext
+    send: list[tuple[int, int, int]] = field(default_factory=list)  # (peer, g0, g1) from own
+
+    @property
+    def ext_len(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def own_offset(self) -> int:
+        return self.own[0] - self.lo
+
+
+def make_plans(spans: list[tuple[int, int]], bounds: list[int]) -> list[HaloPlan]:
+    """Plans for every rank from every rank's column span (deterministic, so
+    each rank can compute all of them without communication)."""
+    world = len(bounds) - 1
+    plans = []
+    for r in range(world):
+        r0, r1 = bounds[r], bounds[r + 1]
+        lo, hi = spans[r]
+        lo, hi = min(lo, r0), max(hi, r1)
+        plans.append(HaloPlan(r, (r0, r1), lo, hi))
+    for r, p in enumerate(plans):
+        for q in range(world):
+            if q == r:
+                continue
+            g0, g1 = max(p.lo, bounds[q]), min(p.hi, bounds[q + 1])
+            if g1 > g0:
+                p.recv.append((q, g0, g1))
+                plans[q].send.append((r, g0, g1))
+    for p in plans:  # deterministic order: by peer
+        p.recv.sort()
+        p.send.sort()
+    return plans
+
+
+def local_block(row_ptr, col_idx, values, r0: int, r1: int, lo: int, ext_len: int):
+    """Rows [r0, r1) of a global CSR with columns shifted by -lo: a
+    (r1 - r0) x ext_len host CSR (reference layout)."""
+    from .csr import CsrMatrix
+
+    b, e = int(row_ptr[r0]), int(row_ptr[r1])
+    rp = np.asarray(row_ptr[r0 : r1 + 1], dtype=np.int64) - b
+    ci = np.asarray(col_idx[b:e], dtype=np.int64) - lo
+    return CsrMatrix(r1 - r0, ext_len, rp, ci, np.asarray(values[b:e], dtype=np.float64))
+
+
+def exchange(ext, own, plan: HaloPlan, group=None) -> None:
+    """Fill ext's halo slices from their owners; send our own slices.
+    ``ext`` / ``own`` are 1-D torch tensors (CUDA with NCCL, CPU with gloo)."""
+    import torch.distributed as dist
+
+    reqs = []
+    for peer, g0, g1 in plan.recv:
+        reqs.append(dist.irecv(ext[g0 - plan.lo : g1 - plan.lo], src=peer, group=group))
+    for peer, g0, g1 in plan.send:
+        s0 = g0 - plan.own[0]
+        reqs.append(dist.isend(own[s0 : s0 + (g1 - g0)].contiguous(), dst=peer, group=group))
+    for q in reqs:
+        q.wait()
+
+
+class DeviceOperator:
+    """y = A x for a local block on the current GPU (sait_operator_*)."""
+
+    def __init__(self, block):
+        from . import _native as N
+        from .csr import DeviceCsr
+
+        d = DeviceCsr.upload(block)
+        h = C.c_void_p()
+        N.check(N.lib.sait_operator_create(d.handle, 1, C.byref(h)))
+        d.release()
+        self._h = h
+        self.nrows, self.ncols = block.nrows, block.ncols
+
+    def apply(self, x, y, stream=None):
+        import torch
+
+        from . import _native as N
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        N.check(N.lib.sait_operator_apply(self._h, x.data_ptr(), x.numel(), y.data_ptr(), y.numel(), s))
+
+    def __del__(self):
+        try:
+            from . import _native as N
+
+            N.lib.sait_operator_destroy(self._h)
+        except Exception:
+            pass
+
+
+class ShardedPair:
+    """Row-sharded z = M_U (M_L r): each rank passes its own rows of r and
+    receives its own rows of z.  ``make_operator(block) -> obj.apply(x, y)``
+    selects the compute backend (DeviceOperator on GPUs)."""
+
+    def __init__(self, ML, MU, rank: int, world: int, group=None, make_operator=DeviceOperator, device="cuda"):
+        import torch
+
+        n = ML.nrows
+        if not (ML.ncols == n and MU.nrows == n and MU.ncols == n):
+            raise ValueError("ShardedPair: square factors of equal order required")
+        self.n, self.rank, self.world, self.group = n, rank, world, group
+        self.bounds = row_bounds(n, world)
+        spans_l = [column_span(ML.row_ptr, ML.col_idx, self.bounds[q], self.bounds[q + 1]) for q in range(world)]
+        spans_u = [column_span(MU.row_ptr, MU.col_idx, self.bounds[q], self.bounds[q + 1]) for q in range(world)]
+        self.plan_l = make_plans(spans_l, self.bounds)[rank]
+        self.plan_u = make_plans(spans_u, self.bounds)[rank]
+        r0, r1 = self.bounds[rank], self.bounds[rank + 1]
+        self.own = (r0, r1)
+        self.op_l = make_operator(local_block(ML.row_ptr, ML.col_idx, ML.values, r0, r1, self.plan_l.lo, self.plan_l.ext_len))
+        self.op_u = make_operator(local_block(MU.row_ptr, MU.col_idx, MU.values, r0, r1, self.plan_u.lo, self.plan_u.ext_len))
+        kw = dict(dtype=torch.float64, device=device)
+        self.ext_l = torch.zeros(self.plan_l.ext_len, **kw)
+        self.ext_u = torch.zeros(self.plan_u.ext_len, **kw)
+        self.halo_bytes = 8 * sum(g1 - g0 for _, g0, g1 in self.plan_l.recv + self.plan_u.recv)
+
+    def apply(self, r_local, z_local) -> None:
+        pl, pu = self.plan_l, self.plan_u
+        nloc = self.own[1] - self.own[0]
+        own_l = self.ext_l[pl.own_offset : pl.own_offset + nloc]
+        own_u = self.ext_u[pu.own_offset : pu.own_offset + nloc]
+        own_l.copy_(r_local)
+        exchange(self.ext_l, own_l, pl, self.group)
+        self.op_l.apply(self.ext_l, own_u)        # y rows land in M_U's extended vector
+        exchange(self.ext_u, own_u, pu, self.group)
+        self.op_u.apply(self.ext_u, z_local)
+
+
+def build_sharded(T_dev, lower: bool, spec, rank: int, world: int, group=None, stream=None, transposed: bool = True,
+                  reduce_max=None):
+    """Column-sharded SAIT build: this rank's block of columns of M.
+
+    Returns (DeviceCsr block, BuildStats, (c0, c1)).  ``transposed`` selects the
+    rows of M^T (a (c1-c0) x n CSR) or M[:, c0:c1].  ``reduce_max(int) -> int``
+    is the cross-rank reduction (all-reduce MAX over ``group`` by default)."""
+    from . import _native as N
+    from .csr import DeviceCsr, _stream_handle
+    from .sait import BuildStats
+
+    if reduce_max is None:
+        reduce_max = _allreduce_max(group)
+    n = T_dev.nrows
+    bounds = row_bounds(n, world)
+    c0, c1 = bounds[rank], bounds[rank + 1]
+    sh = _stream_handle(stream)
+    sess = C.c_void_p()
+    N.check(N.lib.sait_build_session_create(T_dev.handle, int(lower), C.byref(spec), c0, c1, sh, C.byref(sess)))
+    try:
+        while N.lib.sait_build_session_remaining(sess) > 0:
+            ch = C.c_int(1)
+            N.check(N.lib.sait_build_session_step(sess, C.byref(ch)))
+            if reduce_max(int(ch.value)) == 0:  # no column block changed: global early stop
+                N.check(N.lib.sait_build_session_stop(sess))
+        out = C.c_void_p()
+        st = N.BuildStats()
+        N.check(N.lib.sait_build_session_finish(sess, int(transposed), C.byref(out), C.byref(st)))
+    finally:
+        N.lib.sait_build_session_destroy(sess)
+    return DeviceCsr(out.value), BuildStats(st.steps_run, bool(st.stabilized), st.nnz_out, st.products, st.seconds), (c0, c1)
+
+
+def _allreduce_max(group):
+    def red(v: int) -> int:
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            return v
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return int(t.item())
+
+    return red

@@ -1,0 +1,152 @@
+"""Column-block build sessions on the GPU: blocks stepped in lockstep with a
+global early-stop reduction must reproduce the single-block build bitwise
+(the column form makes every column of M independent).  Plus the row-sharded
+pair and the sharded build through torch.distributed (gloo for the host-side
+reduction; two processes on one GPU only synchronise on the host)."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_csr
+from helpers import bitwise_equal, bitwise_equal_csr, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2106_12836_b200 as S
+
+    return S
+
+
+def _assemble_mt_blocks(blocks, n):
+    """Stack M^T row blocks (host CSRs) and transpose to M (host, scipy)."""
+    import scipy.sparse as sp
+
+    mt = sp.vstack([b.to_scipy() for b in blocks]).tocsr()
+    m = mt.T.tocsr()
+    m.sort_indices()
+    return m
+
+
+@pytest.mark.parametrize("kind,args", [("thr", (5e-2, 3)), ("thr", (0.0, 6)), ("pat", (2, 4)), ("cap", (1e-2, 3, 1.5))])
+@pytest.mark.parametrize("world", [2, 5])
+def test_lockstep_column_blocks_equal_single_build(S, port, kind, args, world):
+    from paper_2106_12836_b200 import _native as N
+    from paper_2106_12836_b200.dist import row_bounds
+    from oracle import oracle as O
+
+    T = O.synthetic_lower(3000, 8, 0.01, seed=13)
+    Tp = to_product(T)
+    if kind == "thr":
+        spec = N.DropSpec(N.SAIT_DROP_THRESHOLD, args[0], args[1], 0, 0, 0.0)
+        expect = port.sait_thr(T, True, *args)
+    elif kind == "pat":
+        spec = N.DropSpec(N.SAIT_DROP_PATTERN, 0.0, 0, args[0], args[1], 0.0)
+        expect = port.sait_pat(T, True, *args)
+    else:
+        spec = N.DropSpec(N.SAIT_DROP_THRESHOLD_CAP, args[0], args[1], 0, 0, args[2])
+        expect = port.sait_thr_cap(T, True, *args)
+    dT = S.DeviceCsr.upload(Tp)
+    b = row_bounds(T.nrows, world)
+    sess = []
+    for q in range(world):
+        h = C.c_void_p()
+        N.check(N.lib.sait_build_session_create(dT.handle, 1, C.byref(spec), b[q], b[q + 1], None, C.byref(h)))
+        sess.append(h)
+    while N.lib.sait_build_session_remaining(sess[0]) > 0:
+        flags = []
+        for h in sess:
+            ch = C.c_int(1)
+            N.check(N.lib.sait_build_session_step(h, C.byref(ch)))
+            flags.append(ch.value)
+        if max(flags) == 0:
+            for h in sess:
+                N.check(N.lib.sait_build_session_stop(h))
+    blocks = []
+    for h in sess:
+        out = C.c_void_p()
+        N.check(N.lib.sait_build_session_finish(h, 1, C.byref(out), None))
+        N.lib.sait_build_session_destroy(h)
+        blocks.append(S.DeviceCsr(out.value).to_host())
+    m = _assemble_mt_blocks(blocks, T.nrows)
+    assert np.array_equal(m.indptr, expect.row_ptr) and np.array_equal(m.indices, expect.col_idx)
+    assert bitwise_equal(m.data, expect.values)
+
+
+def test_sharded_pair_world1_and_build_sharded_world1(S, golden):
+    import torch
+
+    from paper_2106_12836_b200 import _native as N
+    from paper_2106_12836_b200.dist import ShardedPair, build_sharded
+
+    ML, MU = to_product(golden_csr(golden, "c1/ML")), to_product(golden_csr(golden, "c1/MU"))
+    sp = ShardedPair(ML, MU, 0, 1)
+    r = torch.from_numpy(golden["c1/r"]).cuda()
+    z = torch.empty_like(r)
+    sp.apply(r, z)
+    torch.cuda.synchronize()
+    assert bitwise_equal(z.cpu().numpy(), golden["c1/z"])
+    L = S.DeviceCsr.upload(to_product(golden_csr(golden, "c1/L")))
+    spec = N.DropSpec(N.SAIT_DROP_THRESHOLD, 1e-2, 4, 0, 0, 0.0)
+    blk, st, (c0, c1) = build_sharded(L, True, spec, 0, 1, transposed=False)
+    assert (c0, c1) == (0, 4096) and st.steps_run == 4
+    assert bitwise_equal_csr(blk.to_host(), golden_csr(golden, "c1/ML"))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _build_worker(rank, world, port, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2106_12836_b200 as S
+        from paper_2106_12836_b200 import _native as N
+        from paper_2106_12836_b200.dist import build_sharded
+        from oracle import oracle as O
+
+        T = O.synthetic_lower(4000, 10, 0.005, seed=21)
+        dT = S.DeviceCsr.upload(S.CsrMatrix(T.nrows, T.ncols, T.row_ptr, T.col_idx, T.values))
+        spec = N.DropSpec(N.SAIT_DROP_THRESHOLD, 2e-2, 5, 0, 0, 0.0)
+        blk, st, _ = build_sharded(dT, True, spec, rank, world)
+        h = blk.to_host()
+        np.savez(os.path.join(out_dir, f"blk{rank}.npz"), rp=h.row_ptr, ci=h.col_idx, v=h.values, n=h.ncols,
+                 steps=st.steps_run)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_build_sharded_two_processes(tmp_path, S, port):
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+
+    mp.start_processes(_build_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    blocks, steps = [], []
+    for q in range(2):
+        d = np.load(tmp_path / f"blk{q}.npz")
+        blocks.append(S.CsrMatrix(len(d["rp"]) - 1, int(d["n"]), d["rp"], d["ci"], d["v"]))
+        steps.append(int(d["steps"]))
+    T = O.synthetic_lower(4000, 10, 0.005, seed=21)
+    expect, nsteps = port.sait_thr_steps(T, True, 2e-2, 5)
+    m = _assemble_mt_blocks(blocks, 4000)
+    assert steps == [nsteps, nsteps]
+    assert np.array_equal(m.indptr, expect.row_ptr) and np.array_equal(m.indices, expect.col_idx)
+    assert bitwise_equal(m.data, expect.values)

@@ -236,15 +236,12 @@ def run_b200(args):
     Ld = S.DeviceCsr.upload(f.lower)
     Ud = S.DeviceCsr.upload(f.upper)
     torch.cuda.synchronize()
-    # ---- build (device): both factors, timed by the library with CUDA events
-    st = []
-    ML = S.sait_thr(Ld, S.lower_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
-    MU = S.sait_thr(Ud, S.upper_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
-    # second build (warm allocator) is the reported one
-    st = []
-    ML.free(), MU.free()
-    ML = S.sait_thr(Ld, S.lower_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
-    MU = S.sait_thr(Ud, S.upper_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
+    # ---- build (device): both factors, timed by the library with CUDA events;
+    # the second build (warm allocator) is the reported one
+    for _ in range(2):
+        st = []
+        ML = S.sait_thr(Ld, S.lower_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
+        MU = S.sait_thr(Ud, S.upper_triangular, S.SaitThrParams(TAU, STEPS_K), stats_out=st)
     nnz_l, nnz_u = ML.nnz(), MU.nnz()
     build = {
         "built_nnz": nnz_l + nnz_u,
@@ -252,22 +249,35 @@ def run_b200(args):
         "nnz_per_s": (nnz_l + nnz_u) / (st[0].seconds + st[1].seconds),
         "steps_run": [st[0].steps_run, st[1].steps_run],
         "products": st[0].products + st[1].products,
+        "note": "both factors, device time incl. split/transposes; replicated on every rank",
     }
-    ML_host = ML.to_host() if rank == 0 else None
-    MU_host = MU.to_host() if rank == 0 else None
-    pair = S.SaitPairPreconditioner(ML, MU)
     B = b_pair(n, nnz_l, nnz_u)
-
-    # ---- 100 seeded vectors resident in HBM
-    R = torch.empty((NVEC, n), dtype=torch.float64, device="cuda")
-    for i in range(NVEC):
-        R[i].copy_(torch.from_numpy(S.uniform_pm1(SEED0 + i, n)))
-    Z = torch.empty_like(R)
     stream = torch.cuda.current_stream()
+    ML_host = MU_host = None
+    if ws == 1:
+        if not args.no_cpu_baseline:
+            ML_host, MU_host = ML.to_host(), MU.to_host()
+        pair = S.SaitPairPreconditioner(ML, MU)
+        r0, r1 = 0, n
+        apply_dev = lambda r, z: pair.apply(r, z)  # noqa: E731
+    else:
+        from paper_2106_12836_b200.dist import ShardedPair
+
+        sp = ShardedPair(ML.to_host(), MU.to_host(), rank, ws)
+        ML.free(), MU.free()
+        r0, r1 = sp.own
+        apply_dev = sp.apply
+    nloc = r1 - r0
+
+    # ---- 100 seeded vectors (this rank's rows) resident in HBM
+    R = torch.empty((NVEC, nloc), dtype=torch.float64, device="cuda")
+    for i in range(NVEC):
+        R[i].copy_(torch.from_numpy(S.uniform_pm1(SEED0 + i, n)[r0:r1]))
+    Z = torch.empty_like(R)
 
     def step():
         for i in range(NVEC):
-            pair.apply(R[i], Z[i])
+            apply_dev(R[i], Z[i])
 
     for _ in range(args.warmup):
         step()
@@ -283,63 +293,80 @@ def run_b200(args):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     launches = S.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     if dist:
+        dist.barrier()
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = NVEC * B / (ms_step * 1e-3) / 1e9 * (ws if False else 1)
+    value = NVEC * B / (ms_step * 1e-3) / 1e9  # whole-job algorithmic GB/s (the global pair)
 
-    # ---- dominant kernel: the SpMV, timed per launch on the launching stream
+    # ---- dominant kernel: the SELL SpMV, per-launch time on the launching stream
     from paper_2106_12836_b200 import _native as NN
 
-    y = torch.empty(n, dtype=torch.float64, device="cuda")
-    reps = 50
-    kt = {}
-    for which, nm, src, dst in ((0, "L", R[0], y), (1, "U", y, Z[0])):
-        def one():
-            NN.check(NN.lib.sait_pair_spmv_factor(pair.handle, which, src.data_ptr(), dst.data_ptr(), stream.cuda_stream))
-        one()
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(reps):
+    roofline = None
+    if ws == 1:
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        reps = 50
+        kt = {}
+        for which, nm, src, dst in ((0, "L", R[0], y), (1, "U", y, Z[0])):
+            def one():
+                NN.check(NN.lib.sait_pair_spmv_factor(pair.handle, which, src.data_ptr(), dst.data_ptr(), stream.cuda_stream))
             one()
-        a1.record(stream)
-        torch.cuda.synchronize()
-        kt[nm] = a0.elapsed_time(a1) / reps
-    bytes_l = 12 * nnz_l + 4 * (n + 1) + 16 * n
-    bytes_u = 12 * nnz_u + 4 * (n + 1) + 16 * n
-    peak, peak_kind = peaks()
-    achieved = (bytes_l + bytes_u) / ((kt["L"] + kt["U"]) * 1e-3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get("spmv_traffic_bytes_per_launch")
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "sell_spmv_kernel",
-                "per_launch_ms": {"M_L": kt["L"], "M_U": kt["U"]},
-                "algorithmic_bytes_per_launch": {"M_L": bytes_l, "M_U": bytes_u},
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)"}
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                one()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            kt[nm] = a0.elapsed_time(a1) / reps
+        bytes_l = 12 * nnz_l + 4 * (n + 1) + 16 * n
+        bytes_u = 12 * nnz_u + 4 * (n + 1) + 16 * n
+        peak, peak_kind = peaks()
+        achieved = (bytes_l + bytes_u) / ((kt["L"] + kt["U"]) * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh).get("spmv_traffic_bytes_per_launch")
+        except Exception:
+            pass
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "kernel": "sell_spmv_kernel",
+                    "per_launch_ms": {"M_L": kt["L"], "M_U": kt["U"]},
+                    "algorithmic_bytes_per_launch": {"M_L": bytes_l, "M_U": bytes_u},
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)"}
 
-    # ---- e2e: public host-vector API, H2D + pair + D2H per vector, pinned host memory
-    Rh = torch.empty((NVEC, n), dtype=torch.float64).pin_memory()
+    # ---- e2e: public API with pinned host buffers, H2D + apply + D2H per vector
+    Rh = torch.empty((NVEC, nloc), dtype=torch.float64).pin_memory()
     Rh.copy_(R.cpu())
-    Zh = torch.empty((NVEC, n), dtype=torch.float64).pin_memory()
-    Rn, Zn = Rh.numpy(), Zh.numpy()
-    z1 = Zn[0]
-    pair.apply(Rn[0], z1)
+    Zh = torch.empty((NVEC, nloc), dtype=torch.float64).pin_memory()
+    if ws == 1:
+        Rn, Zn = Rh.numpy(), Zh.numpy()
+        e2e_one = lambda i: pair.apply(Rn[i], Zn[i])  # noqa: E731  (sait_pair_apply_host)
+    else:
+        rd = torch.empty(nloc, dtype=torch.float64, device="cuda")
+        zd = torch.empty_like(rd)
+
+        def e2e_one(i):
+            rd.copy_(Rh[i], non_blocking=True)
+            sp.apply(rd, zd)
+            Zh[i].copy_(zd, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    e2e_one(0)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for i in range(NVEC):
-        pair.apply(Rn[i], Zn[i])
+        e2e_one(i)
     t_e2e = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
     e2e = {"value": NVEC * B / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": NVEC * 8 * n,
            "d2h_bytes_per_step": NVEC * 8 * n, "ms_per_step": t_e2e * 1e3}
     ok = bool(torch.equal(Zh, Z.cpu()))
@@ -359,6 +386,8 @@ def run_b200(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "build": build, "e2e_matches_device": ok,
         }
+        if ws > 1:
+            line["config"]["halo_bytes_per_apply_rank0"] = sp.halo_bytes
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -33,9 +33,15 @@ namespace {
 constexpr int32_t kEmpty = -1;
 constexpr int32_t kDead = -2;
 constexpr int kFresh = 1 << 30;
-constexpr int kNumSmemBins = 7;  // tables of 64 .. 4096 slots
+// Row bins: 0 = tiny (<= 31 products, <= 32 A entries: register path),
+// 1..7 = shared-memory tables of 64 .. 4096 slots, 8 = global-memory tables.
+constexpr int kTinyBin = 0;
+constexpr int kFirstSmemBin = 1;
+constexpr int kNumSmemBins = 7;
 constexpr int kMinLogSlots = 6;
-constexpr int kGlobalBin = kNumSmemBins;
+constexpr int kGlobalBin = kFirstSmemBin + kNumSmemBins;
+constexpr int kNumBins = kGlobalBin + 1;
+constexpr int kTinyMax = 31;
 
 struct Args {
   int64_t n;
@@ -308,12 +314,159 @@ __global__ void spgemm_global(Args g, const int32_t* __restrict__ rows, const in
     process_row(g, rows[r], gkey + offs[r], gval + offs[r], logs_of[r], &stage[w], lane, numeric);
 }
 
+// ---------------------------------------------------------------- tiny rows
+// Rows with <= 31 products and <= 32 entries in A's row: one warp, one
+// product per lane (plus the +I pseudo-product at lane P), a 32-lane bitonic
+// sort by (column, lane) — lane order is product order, i.e. increasing k —
+// and a sequential sum over each run of equal columns: exactly the reference
+// order, no shared memory.  The count pass stages the sorted survivors in a
+// 32-entry slot per row; the numeric pass is a copy (+ stabilization compare).
+__device__ __forceinline__ void tiny_row(const Args& g, int32_t j, int lane, int64_t slot,
+                                         int32_t* __restrict__ tcol, double* __restrict__ tval) {
+  const int32_t a0 = g.arp[j];
+  const int m = g.arp[j + 1] - a0;
+  int32_t len = 0, bst = 0;
+  double aval = 0.0;
+  if (lane < m) {
+    const int32_t k = g.aci[a0 + lane];
+    aval = g.av[a0 + lane];
+    bst = g.brp[k];
+    len = g.brp[k + 1] - bst;
+  }
+  int32_t incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int32_t excl = incl - len;
+  const int P = __shfl_sync(0xffffffffu, incl, 31);
+  // t(p) = largest t < m with excl_t <= p  (zero-length entries share offsets)
+  int t = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int cand = t + step;
+    const int32_t e = __shfl_sync(0xffffffffu, excl, cand < 32 ? cand : 31);
+    if (cand < m && e <= lane) t = cand;
+  }
+  const int32_t bs = __shfl_sync(0xffffffffu, bst, t);
+  const int32_t ex = __shfl_sync(0xffffffffu, excl, t);
+  const double at = __shfl_sync(0xffffffffu, aval, t);
+  const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
+  int64_t key = INT64_MAX;
+  double val = 0.0;
+  if (lane < P) {
+    const int32_t bi = bs + (lane - ex);
+    key = (static_cast<int64_t>(g.bci[bi]) << 5) | lane;
+    val = __dmul_rn(at, g.bv[bi]);
+  } else if (lane == P && g.epi.add_identity) {
+    key = (static_cast<int64_t>(jd) << 5) | lane;  // +1.0 after the products (add_identity)
+    val = 1.0;
+  }
+  // bitonic sort of (key, val) across the warp
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      const int64_t ok = __shfl_xor_sync(0xffffffffu, key, jj);
+      const double ov = __shfl_xor_sync(0xffffffffu, val, jj);
+      const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+      if (keep_min ? (ok < key) : (ok > key)) {
+        key = ok;
+        val = ov;
+      }
+    }
+  }
+  const bool valid = key != INT64_MAX;
+  const int32_t col = valid ? static_cast<int32_t>(key >> 5) : INT32_MAX;
+  const int32_t prev = __shfl_up_sync(0xffffffffu, col, 1);
+  const bool head = valid && (lane == 0 || prev != col);
+  // sequential sum over each run of equal columns, in product order
+  double acc = val;
+  bool active = head;
+  for (int d = 1; d < 32; ++d) {
+    const double v = __shfl_down_sync(0xffffffffu, val, d);
+    const int32_t c = __shfl_down_sync(0xffffffffu, col, d);
+    if (active) {
+      if (lane + d < 32 && c == col) acc = __dadd_rn(acc, v);
+      else active = false;
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+  }
+  // drop rule on the distinct columns (heads)
+  bool keep = head;
+  const int drop = g.epi.drop;
+  if (head && (drop == 1 || drop == 3) && g.epi.tau != 0.0) keep = (col == jd) || (fabs(acc) >= g.epi.tau);
+  else if (head && drop == 2) keep = in_pattern(g.epi.pci, g.epi.prp[j], g.epi.prp[j + 1], col);
+  if (drop == 3) {
+    const unsigned offm = __ballot_sync(0xffffffffu, keep && col != jd);
+    int room = g.epi.cap[jd] - 1;
+    if (room < 0) room = 0;
+    if (__popc(offm) > room) {
+      const double mv = fabs(acc);
+      int rank = 0;
+      for (int q = 0; q < 32; ++q) {
+        const double mq = __shfl_sync(0xffffffffu, mv, q);
+        const int32_t cq = __shfl_sync(0xffffffffu, col, q);
+        if ((offm >> q) & 1u) rank += (mq > mv) || (mq == mv && cq < col);
+      }
+      if (keep && col != jd && rank >= room) keep = false;
+    }
+  }
+  const unsigned km = __ballot_sync(0xffffffffu, keep);
+  if (lane == 0) g.ccount[j] = __popc(km);
+  if (keep) {
+    const int pos = __popc(km & ((1u << lane) - 1u));
+    tcol[slot * 32 + pos] = col;
+    tval[slot * 32 + pos] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) spgemm_tiny(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+                                                    int32_t* __restrict__ tcol, double* __restrict__ tval) {
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  for (int32_t r = blockIdx.x * warps + (threadIdx.x >> 5); r < nrows_bin; r += gridDim.x * warps)
+    tiny_row(g, rows[r], lane, r, tcol, tval);
+}
+
+// numeric pass of the tiny rows: staged slot -> final row, + early-stop compare
+__global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+                                                         const int32_t* __restrict__ tcol,
+                                                         const double* __restrict__ tval) {
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  for (int32_t r = blockIdx.x * warps + (threadIdx.x >> 5); r < nrows_bin; r += gridDim.x * warps) {
+    const int32_t j = rows[r];
+    const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
+    int32_t c = 0;
+    double v = 0.0;
+    if (lane < live) {
+      c = tcol[static_cast<int64_t>(r) * 32 + lane];
+      v = tval[static_cast<int64_t>(r) * 32 + lane];
+      g.cci[out + lane] = c;
+      g.cv[out + lane] = v;
+    }
+    if (g.epi.qrp) {
+      const int32_t qb = g.epi.qrp[j], ql = g.epi.qrp[j + 1] - qb;
+      bool diff = ql != live;
+      if (!diff && lane < live) {
+        const double a = g.epi.qv[qb + lane];
+        const double fa = fabs(a), fb = fabs(v);
+        const double mx = fa < fb ? fb : fa;
+        diff = g.epi.qci[qb + lane] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx);
+      }
+      if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(g.changed, 1);
+    }
+  }
+}
+
 // products per row (P_j) -> table bin; histogram of bins; total products.
 __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restrict__ pcap,
                           int32_t* __restrict__ hist, unsigned long long* __restrict__ total) {
-  __shared__ int32_t h[kNumSmemBins + 1];
+  __shared__ int32_t h[kNumBins];
   __shared__ unsigned long long tsum;
-  if (threadIdx.x <= kNumSmemBins) h[threadIdx.x] = 0;
+  if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
   if (threadIdx.x == 0) tsum = 0;
   __syncthreads();
   int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -327,29 +480,36 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     int64_t distinct = (p < g.ncols ? p : g.ncols) + 1;  // +1: the identity entry
     int logs = kMinLogSlots;
     while ((int64_t{1} << logs) < 2 * distinct) ++logs;
-    int bin = logs - kMinLogSlots;
+    int bin = kFirstSmemBin + logs - kMinLogSlots;
     if (bin > kGlobalBin) bin = kGlobalBin;
+    if (p <= kTinyMax && g.arp[j + 1] - g.arp[j] <= 32) bin = kTinyBin;
     bin_of[j] = static_cast<int8_t>(bin);
     pcap[j] = logs;  // table log2 size (used by the global bin)
     atomicAdd(&h[bin], 1);
   }
   __syncthreads();
-  if (threadIdx.x <= kNumSmemBins && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+  if (threadIdx.x < kNumBins && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
   if (threadIdx.x == 0 && tsum) atomicAdd(total, tsum);
 }
 
 __global__ void scatter_bins(int64_t n, const int8_t* __restrict__ bin_of, int32_t* __restrict__ cursor,
                              int32_t* __restrict__ lists) {
-  int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  int b = bin_of[j];
-  lists[atomicAdd(&cursor[b], 1)] = static_cast<int32_t>(j);
+  // warp-aggregated: one atomic per (warp, bin) instead of one per row
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int b = j < n ? bin_of[j] : -1;
+  const unsigned grp = __match_any_sync(0xffffffffu, b);
+  const int leader = __ffs(grp) - 1;
+  int base = 0;
+  if (lane == leader && b >= 0) base = atomicAdd(&cursor[b], __popc(grp));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (b >= 0) lists[base + __popc(grp & ((1u << lane) - 1u))] = static_cast<int32_t>(j);
 }
 
 using SmemKernel = void (*)(Args, const int32_t*, int32_t, bool);
 
 SmemKernel smem_kernel(int bin) {
-  switch (bin) {
+  switch (bin - kFirstSmemBin) {
     case 0: return spgemm_smem<6>;
     case 1: return spgemm_smem<7>;
     case 2: return spgemm_smem<8>;
@@ -361,14 +521,14 @@ SmemKernel smem_kernel(int bin) {
 }
 
 int warps_for_bin(int bin) {
-  int logs = bin + kMinLogSlots;
+  int logs = bin - kFirstSmemBin + kMinLogSlots;
   int w = (200 * 1024) / smem_per_warp(logs);
   return std::max(1, std::min(8, w));
 }
 
 struct Plan {
-  int32_t hist[kNumSmemBins + 1] = {};
-  int32_t start[kNumSmemBins + 2] = {};
+  int32_t hist[kNumBins] = {};
+  int32_t start[kNumBins + 1] = {};
   int32_t* lists = nullptr;   // device, rows grouped by bin
   int64_t products = 0;
   // global bin
@@ -376,15 +536,24 @@ struct Plan {
   int8_t* glogs = nullptr;
   int32_t* gkey = nullptr;
   double* gval = nullptr;
+  // tiny rows: 32-entry staging slot per row
+  int32_t* tcol = nullptr;
+  double* tval = nullptr;
 };
 
 void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s) {
-  static bool attr_set[kNumSmemBins] = {};
-  for (int b = 0; b < kNumSmemBins; ++b) {
+  static bool attr_set[kNumBins] = {};
+  if (int32_t tc = pl.hist[kTinyBin]) {
+    unsigned grid = static_cast<unsigned>(std::min<int64_t>((tc + 7) / 8, int64_t{num_sms()} * 8 * 16));
+    if (numeric) spgemm_tiny_emit<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kTinyBin], tc, pl.tcol, pl.tval);
+    else spgemm_tiny<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kTinyBin], tc, pl.tcol, pl.tval);
+    SAIT_LAUNCHED();
+  }
+  for (int b = kFirstSmemBin; b < kFirstSmemBin + kNumSmemBins; ++b) {
     int32_t cnt = pl.hist[b];
     if (!cnt) continue;
     int warps = warps_for_bin(b);
-    int smem = warps * smem_per_warp(b + kMinLogSlots);
+    int smem = warps * smem_per_warp(b - kFirstSmemBin + kMinLogSlots);
     SmemKernel k = smem_kernel(b);
     if (!attr_set[b]) {
       SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -439,9 +608,9 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   Plan pl;
   int8_t* bin_of = dalloc<int8_t>(n, s);
   int32_t* logs_of = dalloc<int32_t>(n, s);
-  int32_t* hist = dalloc<int32_t>(2 * (kNumSmemBins + 1), s);
+  int32_t* hist = dalloc<int32_t>(2 * kNumBins, s);
   unsigned long long* total = dalloc<unsigned long long>(1, s);
-  SAIT_CUDA(cudaMemsetAsync(hist, 0, 2 * (kNumSmemBins + 1) * sizeof(int32_t), s));
+  SAIT_CUDA(cudaMemsetAsync(hist, 0, 2 * kNumBins * sizeof(int32_t), s));
   SAIT_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), s));
   plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total);
   SAIT_LAUNCHED();
@@ -450,10 +619,14 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   SAIT_CUDA(cudaMemcpyAsync(&htotal, total, sizeof htotal, cudaMemcpyDeviceToHost, s));
   SAIT_CUDA(cudaStreamSynchronize(s));
   res.products = static_cast<int64_t>(htotal);
-  for (int b2 = 0; b2 <= kNumSmemBins; ++b2) pl.start[b2 + 1] = pl.start[b2] + pl.hist[b2];
+  for (int b2 = 0; b2 < kNumBins; ++b2) pl.start[b2 + 1] = pl.start[b2] + pl.hist[b2];
   pl.lists = dalloc<int32_t>(n, s);
-  int32_t* cursor = hist + kNumSmemBins + 1;
-  SAIT_CUDA(cudaMemcpyAsync(cursor, pl.start, (kNumSmemBins + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  int32_t* cursor = hist + kNumBins;
+  SAIT_CUDA(cudaMemcpyAsync(cursor, pl.start, kNumBins * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (pl.hist[kTinyBin]) {
+    pl.tcol = dalloc<int32_t>(static_cast<int64_t>(pl.hist[kTinyBin]) * 32, s);
+    pl.tval = dalloc<double>(static_cast<int64_t>(pl.hist[kTinyBin]) * 32, s);
+  }
   scatter_bins<<<grid_for(n, 256), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
   SAIT_LAUNCHED();
   int32_t gc = pl.hist[kGlobalBin];
@@ -513,6 +686,8 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   dfree(pl.glogs, s);
   dfree(pl.gkey, s);
   dfree(pl.gval, s);
+  dfree(pl.tcol, s);
+  dfree(pl.tval, s);
   return res;
 }
 

@@ -33,15 +33,16 @@ namespace {
 constexpr int32_t kEmpty = -1;
 constexpr int32_t kDead = -2;
 constexpr int kFresh = 1 << 30;
-// Row bins: 0 = tiny (<= 31 products, <= 32 A entries: register path),
-// 1..7 = shared-memory tables of 64 .. 4096 slots, 8 = global-memory tables.
-constexpr int kTinyBin = 0;
-constexpr int kFirstSmemBin = 1;
+// Row bins: 0/1/2 = tiny (< 8/16/32 products, <= 8/16/32 A entries: register
+// path, 4/2/1 rows per warp), 3..9 = shared-memory tables of 64 .. 4096
+// slots, 10 = global-memory tables.
+constexpr int kTinyBins = 3;
+constexpr int kFirstSmemBin = kTinyBins;
 constexpr int kNumSmemBins = 7;
 constexpr int kMinLogSlots = 6;
 constexpr int kGlobalBin = kFirstSmemBin + kNumSmemBins;
 constexpr int kNumBins = kGlobalBin + 1;
-constexpr int kTinyMax = 31;
+constexpr int kTinyG[kTinyBins] = {8, 16, 32};
 
 struct Args {
   int64_t n;
@@ -280,7 +281,8 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
         if (g.epi.qci[qb + s] != key[s] || fabs(__dsub_rn(b, a)) > __dmul_rn(1e-15, mx)) diff = true;
       }
     }
-    if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(g.changed, 1);
+    if (__any_sync(0xffffffffu, diff) && lane == 0 && *reinterpret_cast<volatile int*>(g.changed) == 0)
+      atomicOr(g.changed, 1);
   }
   __syncwarp();
 }
@@ -315,16 +317,23 @@ __global__ void spgemm_global(Args g, const int32_t* __restrict__ rows, const in
 }
 
 // ---------------------------------------------------------------- tiny rows
-// Rows with <= 31 products and <= 32 entries in A's row: one warp, one
-// product per lane (plus the +I pseudo-product at lane P), a 32-lane bitonic
-// sort by (column, lane) — lane order is product order, i.e. increasing k —
-// and a sequential sum over each run of equal columns: exactly the reference
-// order, no shared memory.  The count pass stages the sorted survivors in a
-// 32-entry slot per row; the numeric pass is a copy (+ stabilization compare).
-__device__ __forceinline__ void tiny_row(const Args& g, int32_t j, int lane, int64_t slot,
+// Rows with < G products and <= G entries in A's row (G = 8, 16, 32): a group
+// of G lanes per row (32/G rows per warp), one product per lane (plus the +I
+// pseudo-product at lane P), a bitonic sort inside the group by (column,
+// lane) — lane order is product order, i.e. increasing k — and a sequential
+// sum over each run of equal columns: exactly the reference order, no shared
+// memory.  The count pass stages the sorted survivors in a G-entry slot per
+// row; the numeric pass is a copy (+ stabilization compare).
+template <int G>
+__device__ __forceinline__ void tiny_row(const Args& g, int32_t j, bool live_row, int lane, int64_t slot,
                                          int32_t* __restrict__ tcol, double* __restrict__ tval) {
-  const int32_t a0 = g.arp[j];
-  const int m = g.arp[j + 1] - a0;
+  constexpr unsigned kAll = 0xffffffffu;
+  const int grp = (threadIdx.x & 31) / G;
+  int32_t a0 = 0, m = 0;
+  if (live_row) {
+    a0 = g.arp[j];
+    m = g.arp[j + 1] - a0;
+  }
   int32_t len = 0, bst = 0;
   double aval = 0.0;
   if (lane < m) {
@@ -335,41 +344,42 @@ __device__ __forceinline__ void tiny_row(const Args& g, int32_t j, int lane, int
   }
   int32_t incl = len;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+  for (int o = 1; o < G; o <<= 1) {
+    const int32_t y = __shfl_up_sync(kAll, incl, o, G);
     if (lane >= o) incl += y;
   }
   const int32_t excl = incl - len;
-  const int P = __shfl_sync(0xffffffffu, incl, 31);
+  const int P = __shfl_sync(kAll, incl, G - 1, G);
   // t(p) = largest t < m with excl_t <= p  (zero-length entries share offsets)
   int t = 0;
 #pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
+  for (int step = G / 2; step >= 1; step >>= 1) {
     const int cand = t + step;
-    const int32_t e = __shfl_sync(0xffffffffu, excl, cand < 32 ? cand : 31);
+    const int32_t e = __shfl_sync(kAll, excl, cand < G ? cand : G - 1, G);
     if (cand < m && e <= lane) t = cand;
   }
-  const int32_t bs = __shfl_sync(0xffffffffu, bst, t);
-  const int32_t ex = __shfl_sync(0xffffffffu, excl, t);
-  const double at = __shfl_sync(0xffffffffu, aval, t);
+  const int32_t bs = __shfl_sync(kAll, bst, t, G);
+  const int32_t ex = __shfl_sync(kAll, excl, t, G);
+  const double at = __shfl_sync(kAll, aval, t, G);
   const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
   int64_t key = INT64_MAX;
   double val = 0.0;
-  if (lane < P) {
-    const int32_t bi = bs + (lane - ex);
-    key = (static_cast<int64_t>(g.bci[bi]) << 5) | lane;
-    val = __dmul_rn(at, g.bv[bi]);
-  } else if (lane == P && g.epi.add_identity) {
-    key = (static_cast<int64_t>(jd) << 5) | lane;  // +1.0 after the products (add_identity)
-    val = 1.0;
+  if (live_row) {
+    if (lane < P) {
+      const int32_t bi = bs + (lane - ex);
+      key = (static_cast<int64_t>(g.bci[bi]) << 5) | lane;
+      val = __dmul_rn(at, g.bv[bi]);
+    } else if (lane == P && g.epi.add_identity) {
+      key = (static_cast<int64_t>(jd) << 5) | lane;  // +1.0 after the products (add_identity)
+      val = 1.0;
+    }
   }
-  // bitonic sort of (key, val) across the warp
 #pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
+  for (int k = 2; k <= G; k <<= 1) {
 #pragma unroll
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      const int64_t ok = __shfl_xor_sync(0xffffffffu, key, jj);
-      const double ov = __shfl_xor_sync(0xffffffffu, val, jj);
+      const int64_t ok = __shfl_xor_sync(kAll, key, jj, G);
+      const double ov = __shfl_xor_sync(kAll, val, jj, G);
       const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
       if (keep_min ? (ok < key) : (ok > key)) {
         key = ok;
@@ -379,75 +389,94 @@ __device__ __forceinline__ void tiny_row(const Args& g, int32_t j, int lane, int
   }
   const bool valid = key != INT64_MAX;
   const int32_t col = valid ? static_cast<int32_t>(key >> 5) : INT32_MAX;
-  const int32_t prev = __shfl_up_sync(0xffffffffu, col, 1);
+  const int32_t prev = __shfl_up_sync(kAll, col, 1, G);
   const bool head = valid && (lane == 0 || prev != col);
-  // sequential sum over each run of equal columns, in product order
-  double acc = val;
+  double acc = val;  // sequential sum over each run of equal columns, in product order
   bool active = head;
-  for (int d = 1; d < 32; ++d) {
-    const double v = __shfl_down_sync(0xffffffffu, val, d);
-    const int32_t c = __shfl_down_sync(0xffffffffu, col, d);
+  for (int d = 1; d < G; ++d) {
+    const double v = __shfl_down_sync(kAll, val, d, G);
+    const int32_t c = __shfl_down_sync(kAll, col, d, G);
     if (active) {
-      if (lane + d < 32 && c == col) acc = __dadd_rn(acc, v);
+      if (lane + d < G && c == col) acc = __dadd_rn(acc, v);
       else active = false;
     }
-    if (!__any_sync(0xffffffffu, active)) break;
+    if (!__any_sync(kAll, active)) break;
   }
-  // drop rule on the distinct columns (heads)
   bool keep = head;
   const int drop = g.epi.drop;
   if (head && (drop == 1 || drop == 3) && g.epi.tau != 0.0) keep = (col == jd) || (fabs(acc) >= g.epi.tau);
   else if (head && drop == 2) keep = in_pattern(g.epi.pci, g.epi.prp[j], g.epi.prp[j + 1], col);
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
+  const int shift = grp * G;
   if (drop == 3) {
-    const unsigned offm = __ballot_sync(0xffffffffu, keep && col != jd);
-    int room = g.epi.cap[jd] - 1;
+    const unsigned offm = (__ballot_sync(kAll, keep && col != jd) >> shift) & gmask;
+    int room = live_row ? g.epi.cap[jd] - 1 : 0;
     if (room < 0) room = 0;
-    if (__popc(offm) > room) {
+    if (__any_sync(kAll, live_row && __popc(offm) > room)) {
       const double mv = fabs(acc);
       int rank = 0;
-      for (int q = 0; q < 32; ++q) {
-        const double mq = __shfl_sync(0xffffffffu, mv, q);
-        const int32_t cq = __shfl_sync(0xffffffffu, col, q);
+      for (int q = 0; q < G; ++q) {
+        const double mq = __shfl_sync(kAll, mv, q, G);
+        const int32_t cq = __shfl_sync(kAll, col, q, G);
         if ((offm >> q) & 1u) rank += (mq > mv) || (mq == mv && cq < col);
       }
-      if (keep && col != jd && rank >= room) keep = false;
+      if (__popc(offm) > room && keep && col != jd && rank >= room) keep = false;
     }
   }
-  const unsigned km = __ballot_sync(0xffffffffu, keep);
-  if (lane == 0) g.ccount[j] = __popc(km);
-  if (keep) {
-    const int pos = __popc(km & ((1u << lane) - 1u));
-    tcol[slot * 32 + pos] = col;
-    tval[slot * 32 + pos] = acc;
+  const unsigned km = (__ballot_sync(kAll, keep) >> shift) & gmask;
+  if (live_row) {
+    if (lane == 0) g.ccount[j] = __popc(km);
+    if (keep) {
+      const int pos = __popc(km & ((1u << lane) - 1u));
+      tcol[slot * G + pos] = col;
+      tval[slot * G + pos] = acc;
+    }
   }
 }
 
+template <int G>
 __global__ void __launch_bounds__(256) spgemm_tiny(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                     int32_t* __restrict__ tcol, double* __restrict__ tval) {
-  const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  for (int32_t r = blockIdx.x * warps + (threadIdx.x >> 5); r < nrows_bin; r += gridDim.x * warps)
-    tiny_row(g, rows[r], lane, r, tcol, tval);
+  constexpr int kPerWarp = 32 / G;
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int sub = (threadIdx.x & 31) / G;
+  for (int64_t w = warp0; w * kPerWarp < nrows_bin; w += nwarps) {
+    const int64_t r = w * kPerWarp + sub;
+    const bool live = r < nrows_bin;
+    tiny_row<G>(g, live ? rows[r] : 0, live, lane, r, tcol, tval);
+  }
 }
 
 // numeric pass of the tiny rows: staged slot -> final row, + early-stop compare
+template <int G>
 __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                          const int32_t* __restrict__ tcol,
                                                          const double* __restrict__ tval) {
-  const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  for (int32_t r = blockIdx.x * warps + (threadIdx.x >> 5); r < nrows_bin; r += gridDim.x * warps) {
+  __shared__ int blk_changed;
+  if (threadIdx.x == 0) blk_changed = 0;
+  __syncthreads();
+  constexpr int kPerWarp = 32 / G;
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int sub = (threadIdx.x & 31) / G;
+  bool diff_any = false;
+  for (int64_t w = warp0; w * kPerWarp < nrows_bin; w += nwarps) {
+    const int64_t r = w * kPerWarp + sub;
+    if (r >= nrows_bin) continue;
     const int32_t j = rows[r];
     const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
     int32_t c = 0;
     double v = 0.0;
     if (lane < live) {
-      c = tcol[static_cast<int64_t>(r) * 32 + lane];
-      v = tval[static_cast<int64_t>(r) * 32 + lane];
+      c = tcol[r * G + lane];
+      v = tval[r * G + lane];
       g.cci[out + lane] = c;
       g.cv[out + lane] = v;
     }
-    if (g.epi.qrp) {
+    if (g.epi.qrp && !diff_any) {
       const int32_t qb = g.epi.qrp[j], ql = g.epi.qrp[j + 1] - qb;
       bool diff = ql != live;
       if (!diff && lane < live) {
@@ -456,9 +485,12 @@ __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* _
         const double mx = fa < fb ? fb : fa;
         diff = g.epi.qci[qb + lane] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx);
       }
-      if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(g.changed, 1);
+      diff_any = diff_any || diff;
     }
   }
+  if (diff_any) blk_changed = 1;
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_changed) atomicOr(g.changed, 1);
 }
 
 // products per row (P_j) -> table bin; histogram of bins; total products.
@@ -482,7 +514,8 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     while ((int64_t{1} << logs) < 2 * distinct) ++logs;
     int bin = kFirstSmemBin + logs - kMinLogSlots;
     if (bin > kGlobalBin) bin = kGlobalBin;
-    if (p <= kTinyMax && g.arp[j + 1] - g.arp[j] <= 32) bin = kTinyBin;
+    const int32_t m = g.arp[j + 1] - g.arp[j];
+    if (p < 32 && m <= 32) bin = (p < 8 && m <= 8) ? 0 : (p < 16 && m <= 16) ? 1 : 2;
     bin_of[j] = static_cast<int8_t>(bin);
     pcap[j] = logs;  // table log2 size (used by the global bin)
     atomicAdd(&h[bin], 1);
@@ -536,17 +569,33 @@ struct Plan {
   int8_t* glogs = nullptr;
   int32_t* gkey = nullptr;
   double* gval = nullptr;
-  // tiny rows: 32-entry staging slot per row
-  int32_t* tcol = nullptr;
-  double* tval = nullptr;
+  // tiny rows: G-entry staging slot per row, per tiny bin
+  int32_t* tcol[kTinyBins] = {};
+  double* tval[kTinyBins] = {};
 };
 
 void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s) {
   static bool attr_set[kNumBins] = {};
-  if (int32_t tc = pl.hist[kTinyBin]) {
-    unsigned grid = static_cast<unsigned>(std::min<int64_t>((tc + 7) / 8, int64_t{num_sms()} * 8 * 16));
-    if (numeric) spgemm_tiny_emit<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kTinyBin], tc, pl.tcol, pl.tval);
-    else spgemm_tiny<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kTinyBin], tc, pl.tcol, pl.tval);
+  for (int tb = 0; tb < kTinyBins; ++tb) {
+    const int32_t tc = pl.hist[tb];
+    if (!tc) continue;
+    const int per_warp = 32 / kTinyG[tb];
+    const int64_t warps = (tc + per_warp - 1) / per_warp;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, int64_t{num_sms()} * 8 * 16));
+    const int32_t* rows = pl.lists + pl.start[tb];
+    switch (kTinyG[tb]) {
+      case 8:
+        if (numeric) spgemm_tiny_emit<8><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        else spgemm_tiny<8><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        break;
+      case 16:
+        if (numeric) spgemm_tiny_emit<16><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        else spgemm_tiny<16><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        break;
+      default:
+        if (numeric) spgemm_tiny_emit<32><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        else spgemm_tiny<32><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+    }
     SAIT_LAUNCHED();
   }
   for (int b = kFirstSmemBin; b < kFirstSmemBin + kNumSmemBins; ++b) {
@@ -623,10 +672,11 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   pl.lists = dalloc<int32_t>(n, s);
   int32_t* cursor = hist + kNumBins;
   SAIT_CUDA(cudaMemcpyAsync(cursor, pl.start, kNumBins * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  if (pl.hist[kTinyBin]) {
-    pl.tcol = dalloc<int32_t>(static_cast<int64_t>(pl.hist[kTinyBin]) * 32, s);
-    pl.tval = dalloc<double>(static_cast<int64_t>(pl.hist[kTinyBin]) * 32, s);
-  }
+  for (int tb = 0; tb < kTinyBins; ++tb)
+    if (pl.hist[tb]) {
+      pl.tcol[tb] = dalloc<int32_t>(static_cast<int64_t>(pl.hist[tb]) * kTinyG[tb], s);
+      pl.tval[tb] = dalloc<double>(static_cast<int64_t>(pl.hist[tb]) * kTinyG[tb], s);
+    }
   scatter_bins<<<grid_for(n, 256), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
   SAIT_LAUNCHED();
   int32_t gc = pl.hist[kGlobalBin];
@@ -686,8 +736,10 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   dfree(pl.glogs, s);
   dfree(pl.gkey, s);
   dfree(pl.gval, s);
-  dfree(pl.tcol, s);
-  dfree(pl.tval, s);
+  for (int tb = 0; tb < kTinyBins; ++tb) {
+    dfree(pl.tcol[tb], s);
+    dfree(pl.tval[tb], s);
+  }
   return res;
 }
 

@@ -130,25 +130,52 @@ __global__ void scatter_transpose(int64_t nrows, const int32_t* __restrict__ rp,
   }
 }
 
-// Rows of <= 32 entries: one warp per row, rank by counting smaller keys.
+// Rows of <= 8 entries: 8 lanes per row (4 rows per warp), rank by counting
+// smaller keys; longer rows are listed for the block sorter.
 __global__ void sort_rows_warp(int64_t nrows, const int32_t* __restrict__ rp, int32_t* __restrict__ ci,
                                double* __restrict__ v, int32_t* __restrict__ long_rows, int32_t* __restrict__ nlong) {
-  int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (row >= nrows) return;
-  int32_t b = rp[row], len = rp[row + 1] - b;
-  if (len > 32) {
-    if (lane == 0) long_rows[atomicAdd(nlong, 1)] = static_cast<int32_t>(row);
-    return;
+  constexpr int G = 8;
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+  const int lane = threadIdx.x & (G - 1);
+  const bool live = row < nrows;
+  int32_t b = 0, len = 0;
+  if (live) {
+    b = rp[row];
+    len = rp[row + 1] - b;
   }
-  if (len <= 1) return;
-  int32_t key = lane < len ? ci[b + lane] : kKeyPad;
-  double val = (lane < len && v) ? v[b + lane] : 0.0;
+  if (live && len > G && lane == 0) long_rows[atomicAdd(nlong, 1)] = static_cast<int32_t>(row);
+  const bool mine = live && len <= G && lane < len;
+  const int32_t key = mine ? ci[b + lane] : kKeyPad;
+  const double val = (mine && v) ? v[b + lane] : 0.0;
   int rank = 0;
-  for (int o = 0; o < len; ++o) {
-    int32_t other = __shfl_sync(0xffffffffu, key, o);
+#pragma unroll
+  for (int o = 0; o < G; ++o) {
+    const int32_t other = __shfl_sync(0xffffffffu, key, o, G);
     rank += other < key;
   }
+  if (mine && len > 1) {
+    ci[b + rank] = key;
+    if (v) v[b + rank] = val;
+  }
+}
+
+// Rows listed by sort_rows_warp with 8 < len <= 32: one warp per row.
+__global__ void sort_rows_mid(const int32_t* __restrict__ rows, int32_t nlist, const int32_t* __restrict__ rp,
+                              int32_t* __restrict__ ci, double* __restrict__ v, int32_t* __restrict__ long_rows,
+                              int32_t* __restrict__ nlong) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nlist) return;
+  const int32_t row = rows[w];
+  const int32_t b = rp[row], len = rp[row + 1] - b;
+  if (len > 32) {
+    if (lane == 0) long_rows[atomicAdd(nlong, 1)] = row;
+    return;
+  }
+  const int32_t key = lane < len ? ci[b + lane] : kKeyPad;
+  const double val = (lane < len && v) ? v[b + lane] : 0.0;
+  int rank = 0;
+  for (int o = 0; o < len; ++o) rank += __shfl_sync(0xffffffffu, key, o) < key;
   __syncwarp();
   if (lane < len) {
     ci[b + rank] = key;
@@ -278,16 +305,23 @@ DevCsr make_identity_rows(int64_t rows, int64_t col0, int64_t ncols, cudaStream_
 // Sort every row of (rp, ci, v) by column index.
 void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s) {
   if (nrows == 0) return;
-  int32_t* lists = dalloc<int32_t>(2 * nrows + 2, s);
+  int32_t* lists = dalloc<int32_t>(3 * nrows + 3, s);
+  int32_t* mid_rows = lists + 2 * nrows;
   int32_t* long_rows = lists;
   int32_t* huge_rows = lists + nrows;
-  int32_t* counters = lists + 2 * nrows;  // [nlong, nhuge]
-  SAIT_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
-  sort_rows_warp<<<grid_for(nrows * 32, 256), 256, 0, s>>>(nrows, rp, ci, v, long_rows, counters);
+  int32_t* counters = lists + 3 * nrows;  // [nlong, nhuge, nmid]
+  SAIT_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(int32_t), s));
+  sort_rows_warp<<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
   SAIT_LAUNCHED();
-  int32_t hc[2];
+  int32_t hc[3];
   SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
   SAIT_CUDA(cudaStreamSynchronize(s));
+  if (hc[2] > 0) {
+    sort_rows_mid<<<grid_for(int64_t{hc[2]} * 32, 256), 256, 0, s>>>(mid_rows, hc[2], rp, ci, v, long_rows, counters);
+    SAIT_LAUNCHED();
+    SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+  }
   if (hc[0] > 0) {
     unsigned g = static_cast<unsigned>(std::min<int64_t>(hc[0], 4 * num_sms()));
     sort_rows_block<<<g, kSortBlock, 0, s>>>(long_rows, hc[0], rp, ci, v, huge_rows, counters + 1);

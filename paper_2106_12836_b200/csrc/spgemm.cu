@@ -362,33 +362,49 @@ __device__ __forceinline__ void tiny_row(const Args& g, int32_t j, bool live_row
   const int32_t ex = __shfl_sync(kAll, excl, t, G);
   const double at = __shfl_sync(kAll, aval, t, G);
   const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
-  int64_t key = INT64_MAX;
-  double val = 0.0;
+  // sort key (column, lane): 32-bit while columns < 2^26, else 64-bit
+  double val0 = 0.0;
+  int32_t col0 = INT32_MAX;
   if (live_row) {
     if (lane < P) {
       const int32_t bi = bs + (lane - ex);
-      key = (static_cast<int64_t>(g.bci[bi]) << 5) | lane;
-      val = __dmul_rn(at, g.bv[bi]);
+      col0 = g.bci[bi];
+      val0 = __dmul_rn(at, g.bv[bi]);
     } else if (lane == P && g.epi.add_identity) {
-      key = (static_cast<int64_t>(jd) << 5) | lane;  // +1.0 after the products (add_identity)
-      val = 1.0;
+      col0 = jd;  // +1.0 after the products (add_identity)
+      val0 = 1.0;
     }
   }
+  int32_t col;
+  double val;
+  if (g.ncols < (int64_t{1} << 26)) {
+    uint32_t key = col0 == INT32_MAX ? 0xffffffffu : (static_cast<uint32_t>(col0) << 5) | static_cast<uint32_t>(lane);
 #pragma unroll
-  for (int k = 2; k <= G; k <<= 1) {
+    for (int k = 2; k <= G; k <<= 1) {
 #pragma unroll
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      const int64_t ok = __shfl_xor_sync(kAll, key, jj, G);
-      const double ov = __shfl_xor_sync(kAll, val, jj, G);
-      const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
-      if (keep_min ? (ok < key) : (ok > key)) {
-        key = ok;
-        val = ov;
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        const uint32_t ok = __shfl_xor_sync(kAll, key, jj, G);
+        const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+        key = keep_min ? min(key, ok) : max(key, ok);
       }
     }
+    col = key == 0xffffffffu ? INT32_MAX : static_cast<int32_t>(key >> 5);
+    val = __shfl_sync(kAll, val0, static_cast<int>(key & 31u) & (G - 1), G);
+  } else {
+    int64_t key = col0 == INT32_MAX ? INT64_MAX : (static_cast<int64_t>(col0) << 5) | lane;
+#pragma unroll
+    for (int k = 2; k <= G; k <<= 1) {
+#pragma unroll
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        const int64_t ok = __shfl_xor_sync(kAll, key, jj, G);
+        const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+        key = keep_min ? min(key, ok) : max(key, ok);
+      }
+    }
+    col = key == INT64_MAX ? INT32_MAX : static_cast<int32_t>(key >> 5);
+    val = __shfl_sync(kAll, val0, static_cast<int>(key & 31) & (G - 1), G);
   }
-  const bool valid = key != INT64_MAX;
-  const int32_t col = valid ? static_cast<int32_t>(key >> 5) : INT32_MAX;
+  const bool valid = col != INT32_MAX;
   const int32_t prev = __shfl_up_sync(kAll, col, 1, G);
   const bool head = valid && (lane == 0 || prev != col);
   double acc = val;  // sequential sum over each run of equal columns, in product order

@@ -150,6 +150,49 @@ __global__ void block_residual_k(int64_t n, int k, const double* __restrict__ AX
   for (int j = 0; j < k; ++j) R[n * j + i] = __dsub_rn(AX[n * j + i], __dmul_rn(lam[j], X[n * j + i]));
 }
 
+// Tall-skinny Gram tile: part[(a * kb + b) * nb + blk] = canonical block
+// partial of A_a . B_b for a < ka <= 8, b < kb <= 8 (column-major blocks,
+// leading dimension n).  Each thread keeps the 64 running sums of its 8
+// strided elements in registers, so the tile's 16 columns are read once.
+__global__ void __launch_bounds__(kT) gram_tile_partials(int64_t n, const double* __restrict__ A, int ka,
+                                                          const double* __restrict__ B, int kb,
+                                                          double* __restrict__ part, int64_t nb) {
+  __shared__ double ws[64][8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kB + t;
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < kK; ++k) {
+    const int64_t i = base + static_cast<int64_t>(kT) * k;
+    if (i >= n) break;
+    double xa[8], yb[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) xa[a] = a < ka ? A[n * a + i] : 0.0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) yb[b] = b < kb ? B[n * b + i] : 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(xa[a], yb[b]));
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const double v = warp_butterfly(acc[a][b]);
+      if (lane == 0) ws[a * 8 + b][warp] = v;
+    }
+  __syncthreads();
+  if (t < 64) {
+    const int a = t >> 3, b = t & 7;
+    if (a < ka && b < kb) part[static_cast<int64_t>(a * kb + b) * nb + blockIdx.x] = tree8(ws[t]);
+  }
+}
+
 __global__ void hadamard_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -189,6 +232,24 @@ void block_residual(int64_t n, int k, const double* AX, const double* X, const d
 }
 
 int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
+
+// G[a * ldg + b] (device, a < ka, b < kb) = canonical dot of A_a and B_b,
+// computed tile by tile (8 x 8); identical bits to multi_dot per entry.
+void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
+          cudaStream_t s, bool upper_only) {
+  const int64_t nb = dot_blocks(n);
+  for (int a0 = 0; a0 < ka; a0 += 8)
+    for (int b0 = 0; b0 < kb; b0 += 8) {
+      if (upper_only && b0 + 8 <= a0) continue;
+      const int ta = ka - a0 < 8 ? ka - a0 : 8, tb = kb - b0 < 8 ? kb - b0 : 8;
+      gram_tile_partials<<<static_cast<unsigned>(nb), kT, 0, s>>>(n, A + n * a0, ta, B + n * b0, tb, scratch, nb);
+      SAIT_LAUNCHED();
+      for (int a = 0; a < ta; ++a) {  // one final fold per tile row: tb blocks
+        mdot_final<<<tb, kT, 0, s>>>(scratch + static_cast<int64_t>(a * tb) * nb, nb, G + (a0 + a) * ldg + b0, 0);
+        SAIT_LAUNCHED();
+      }
+    }
+}
 
 void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, double* out, double* scratch,
                cudaStream_t s, bool sqrt_out) {

@@ -29,6 +29,8 @@ void axpy(int64_t n, double a, const double* x, double* y, cudaStream_t s);
 void xpay(int64_t n, const double* x, double a, double* y, cudaStream_t s);
 void x_minus_y(int64_t n, const double* x, double* y, cudaStream_t s);
 void y_plus_x(int64_t n, const double* x, double* y, cudaStream_t s);
+void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
+          cudaStream_t s, bool upper_only);
 void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s);
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
@@ -454,19 +456,24 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     double* R = sait::dalloc<double>(blk, s);
     double* tmp = sait::dalloc<double>(4 * blk, s);
     double* dsmall = sait::dalloc<double>(48 * 48, s);
-    sait::Scalars sc(n, 48 * 48, 48, s);
+    sait::Scalars sc(n, 48 * 48, 64, s);
     double *X = S, *W = S + blk, *P = S + 2 * blk;
     double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
     auto block_spmv = [&](const double* in, double* out) {
       for (int j = 0; j < k; ++j) op.apply(in + static_cast<int64_t>(j) * n, out + static_cast<int64_t>(j) * n, s);
     };
-    // G[a][b] = S_a . Y_b (canonical dots), row-major ka x kb on the host
-    auto gram = [&](const double* Sa, int ka, const double* Yb, int kb, std::vector<double>& G) {
+    // G[a][b] = S_a . Y_b (canonical dots, tiled tall-skinny kernel), row-major
+    // ka x kb on the host; sym: S == Y, lower tiles mirrored (bitwise equal,
+    // the canonical dot is symmetric in its arguments)
+    auto gram = [&](const double* Sa, int ka, const double* Yb, int kb, std::vector<double>& G, bool sym = false) {
       G.assign(static_cast<size_t>(ka) * kb, 0.0);
-      for (int r = 0; r < ka; ++r) sait::multi_dot(n, Sa + static_cast<int64_t>(r) * n, Yb, n, kb, sc.d + r * kb,
-                                                   sc.part, s, false);
+      sait::gram(n, Sa, ka, Yb, kb, sc.d, kb, sc.part, s, sym);
       sc.fetch(ka * kb, s);
       std::copy(sc.h.begin(), sc.h.begin() + static_cast<size_t>(ka) * kb, G.begin());
+      if (sym)
+        for (int a2 = 0; a2 < ka; ++a2)
+          for (int b2 = 0; b2 < a2; ++b2)
+            if ((b2 / 8) < (a2 / 8)) G[a2 * kb + b2] = G[b2 * kb + a2];
     };
     auto lincomb = [&](const double* in, int kin, const double* C, int kout, double* out) {
       SAIT_CUDA(cudaMemcpyAsync(dsmall, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));
@@ -475,7 +482,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     };
     auto cholqr = [&](double* Y, double* AY) {
       std::vector<double> G, L(k * k), Li(k * k), Ri(k * k);
-      gram(Y, k, Y, k, G);
+      gram(Y, k, Y, k, G, true);
       if (!sait::chol_lower(G.data(), k, L.data())) return false;
       sait::tri_lower_inv(L.data(), k, Li.data());
       for (int i = 0; i < k; ++i)
@@ -501,7 +508,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     block_spmv(X, AX);
     bool failed = false;
     std::string why;
-    gram(X, k, X, k, GB);
+    gram(X, k, X, k, GB, true);
     gram(X, k, AX, k, GA);
     int it = 0;
     bool conv = false, have_p = false;
@@ -543,7 +550,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
         int m = use_p ? 3 * k : 2 * k;
         bool ok = false;
         while (true) {
-          gram(S, m, S, m, GB);
+          gram(S, m, S, m, GB, true);
           gram(S, m, AS, m, GA);
           for (int i = 0; i < m; ++i)
             for (int j = i + 1; j < m; ++j) {

@@ -121,25 +121,49 @@ __global__ void add_k(int64_t n, const double* __restrict__ x, double* __restric
 // out[:, j] = sum_q in[:, q] C[q][j]  (column-major blocks, C row-major kin x kout)
 __global__ void block_lincomb_k(int64_t n, const double* __restrict__ in, int kin, const double* __restrict__ C,
                                 int kout, double* __restrict__ out) {
+  __shared__ double cs[48 * 16];
+  for (int e = threadIdx.x; e < kin * kout; e += blockDim.x) cs[e] = C[e];
+  __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  for (int j = 0; j < kout; ++j) {
-    double t = __dmul_rn(in[i], C[j]);
-    for (int q = 1; q < kin; ++q) t = __dadd_rn(t, __dmul_rn(in[n * q + i], C[q * kout + j]));
-    out[n * j + i] = t;
+  // each input element read once; output j accumulates q = 0, 1, ... in order
+  double acc[16];
+  const double x0 = in[i];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < kout) acc[j] = __dmul_rn(x0, cs[j]);
+  for (int q = 1; q < kin; ++q) {
+    const double xq = in[n * q + i];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < kout) acc[j] = __dadd_rn(acc[j], __dmul_rn(xq, cs[q * kout + j]));
   }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < kout) out[n * j + i] = acc[j];
 }
 
 // W[:, j] = (((W_j - X_0 G[0][j]) - X_1 G[1][j]) - ...)
 __global__ void block_sub_lincomb_k(int64_t n, const double* __restrict__ X, int k, const double* __restrict__ G,
                                     double* __restrict__ W) {
+  __shared__ double gs[16 * 16];
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) gs[e] = G[e];
+  __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  for (int j = 0; j < k; ++j) {
-    double t = W[n * j + i];
-    for (int q = 0; q < k; ++q) t = __dsub_rn(t, __dmul_rn(X[n * q + i], G[q * k + j]));
-    W[n * j + i] = t;
+  double w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < k) w[j] = W[n * j + i];
+  for (int q = 0; q < k; ++q) {
+    const double xq = X[n * q + i];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < k) w[j] = __dsub_rn(w[j], __dmul_rn(xq, gs[q * k + j]));
   }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < k) W[n * j + i] = w[j];
 }
 
 // R[:, j] = AX[:, j] - lam[j] X[:, j]
@@ -154,41 +178,43 @@ __global__ void block_residual_k(int64_t n, int k, const double* __restrict__ AX
 // partial of A_a . B_b for a < ka <= 8, b < kb <= 8 (column-major blocks,
 // leading dimension n).  Each thread keeps the 64 running sums of its 8
 // strided elements in registers, so the tile's 16 columns are read once.
+template <int TT>
 __global__ void __launch_bounds__(kT) gram_tile_partials(int64_t n, const double* __restrict__ A, int ka,
                                                           const double* __restrict__ B, int kb,
                                                           double* __restrict__ part, int64_t nb) {
-  __shared__ double ws[64][8];
+  __shared__ double ws[TT * TT][8];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kB + t;
-  double acc[8][8];
+  double acc[TT][TT];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < TT; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-#pragma unroll 1
+    for (int b = 0; b < TT; ++b) acc[a][b] = 0.0;
+#pragma unroll 2
   for (int k = 0; k < kK; ++k) {
     const int64_t i = base + static_cast<int64_t>(kT) * k;
-    if (i >= n) break;
-    double xa[8], yb[8];
+    if (i < n) {
+      double xa[TT], yb[TT];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) xa[a] = a < ka ? A[n * a + i] : 0.0;
+      for (int a = 0; a < TT; ++a) xa[a] = a < ka ? A[n * a + i] : 0.0;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) yb[b] = b < kb ? B[n * b + i] : 0.0;
+      for (int b = 0; b < TT; ++b) yb[b] = b < kb ? B[n * b + i] : 0.0;
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < TT; ++a)
 #pragma unroll
-      for (int b = 0; b < 8; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(xa[a], yb[b]));
+        for (int b = 0; b < TT; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(xa[a], yb[b]));
+    }
   }
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < TT; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    for (int b = 0; b < TT; ++b) {
       const double v = warp_butterfly(acc[a][b]);
-      if (lane == 0) ws[a * 8 + b][warp] = v;
+      if (lane == 0) ws[a * TT + b][warp] = v;
     }
   __syncthreads();
-  if (t < 64) {
-    const int a = t >> 3, b = t & 7;
+  if (t < TT * TT) {
+    const int a = t / TT, b = t % TT;
     if (a < ka && b < kb) part[static_cast<int64_t>(a * kb + b) * nb + blockIdx.x] = tree8(ws[t]);
   }
 }
@@ -238,11 +264,12 @@ int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
           cudaStream_t s, bool upper_only) {
   const int64_t nb = dot_blocks(n);
-  for (int a0 = 0; a0 < ka; a0 += 8)
-    for (int b0 = 0; b0 < kb; b0 += 8) {
-      if (upper_only && b0 + 8 <= a0) continue;
-      const int ta = ka - a0 < 8 ? ka - a0 : 8, tb = kb - b0 < 8 ? kb - b0 : 8;
-      gram_tile_partials<<<static_cast<unsigned>(nb), kT, 0, s>>>(n, A + n * a0, ta, B + n * b0, tb, scratch, nb);
+  constexpr int TT = 4;
+  for (int a0 = 0; a0 < ka; a0 += TT)
+    for (int b0 = 0; b0 < kb; b0 += TT) {
+      if (upper_only && b0 + TT <= a0) continue;
+      const int ta = ka - a0 < TT ? ka - a0 : TT, tb = kb - b0 < TT ? kb - b0 : TT;
+      gram_tile_partials<TT><<<static_cast<unsigned>(nb), kT, 0, s>>>(n, A + n * a0, ta, B + n * b0, tb, scratch, nb);
       SAIT_LAUNCHED();
       for (int a = 0; a < ta; ++a) {  // one final fold per tile row: tb blocks
         mdot_final<<<tb, kT, 0, s>>>(scratch + static_cast<int64_t>(a * tb) * nb, nb, G + (a0 + a) * ldg + b0, 0);

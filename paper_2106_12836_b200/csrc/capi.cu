@@ -1241,6 +1241,14 @@ void apply_block_device(sait_pair_t p, const double* d_r, double* d_z, int64_t n
     sait::dfree(y, s);
     return;
   }
+  if (layout == 0 && pair_variant() >= 2 && p->sl.ok() && p->su.ok()) {
+    // column-major straight through the SELL block kernels (no transposes)
+    double* y = sait::dalloc<double>(L.nrows * nvec, s);
+    sait::sell_spmm_colmajor(p->sl, d_r, n, y, L.nrows, static_cast<int>(nvec), s);
+    sait::sell_spmm_colmajor(p->su, y, L.nrows, d_z, n, static_cast<int>(nvec), s);
+    sait::dfree(y, s);
+    return;
+  }
   const double* rcm = d_r;
   double* zcm = d_z;
   double* tmp_r = nullptr;

@@ -182,6 +182,9 @@ void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan&
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
 // rows [row0, row1) only (row0 a multiple of 32)
 void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s);
+// column-major blocks (leading dimensions ldx / ldy), any nvec
+void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                        cudaStream_t s);
 bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s);  // row-major block
 void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
 void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaStream_t s);

@@ -189,6 +189,51 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
   }
 }
 
+// Column-major block (n x NV, leading dimension ld): lane = row, NV
+// accumulators; each index/value read once for all NV vectors, x gathered
+// per column (neighbouring rows -> neighbouring x: coalesced).
+template <int NV>
+__global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
+                                                            const int32_t* __restrict__ scol,
+                                                            const double* __restrict__ sval,
+                                                            const double* __restrict__ x, int64_t ldx,
+                                                            double* __restrict__ y, int64_t ldy, int nv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int64_t base = soff[s];
+  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  double acc[NV];
+#pragma unroll
+  for (int c = 0; c < NV; ++c) acc[c] = 0.0;
+  for (int32_t k0 = 0; k0 < w; k0 += 4) {
+    int32_t col[4];
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      col[j] = -1;
+      v[j] = 0.0;
+      if (k0 + j < w) {
+        col[j] = ld_na(scol + base + (k0 + j) * kSlice + lane);
+        v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (col[j] < 0) continue;
+#pragma unroll
+      for (int c = 0; c < NV; ++c)
+        if (c < nv) acc[c] = __dadd_rn(acc[c], __dmul_rn(v[j], __ldg(x + ldx * c + col[j])));
+    }
+  }
+  const int64_t row = s * kSlice + lane;
+  if (row < n) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c)
+      if (c < nv) y[ldy * c + row] = acc[c];
+  }
+}
+
 unsigned sell_grid(int64_t nslices) {  // one slice per warp, 8 warps per CTA
   return static_cast<unsigned>(std::max<int64_t>(1, (nslices + 7) / 8));
 }
@@ -450,6 +495,17 @@ void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const doubl
   if (s1 <= s0) return;
   sell_spmv_kernel<<<sell_grid(s1 - s0), 256, 0, s>>>(m.n, s0, s1, m.soff, m.col, m.val, x, y);
   SAIT_LAUNCHED();
+}
+
+void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
+                        cudaStream_t s) {
+  if (m.nslices == 0) return;
+  for (int c0 = 0; c0 < nvec; c0 += 8) {
+    const int nv = nvec - c0 < 8 ? nvec - c0 : 8;
+    sell_spmm_cm_kernel<8><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x + ldx * c0,
+                                                                ldx, y + ldy * c0, ldy, nv);
+    SAIT_LAUNCHED();
+  }
 }
 
 bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s) {

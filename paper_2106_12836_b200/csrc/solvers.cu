@@ -8,6 +8,8 @@
 #include <chrono>
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -48,6 +50,14 @@ struct Operator {
   void apply(const double* x, double* y, cudaStream_t s) const {
     if (sell.ok()) sell_spmv(sell, x, y, s);
     else spmv(*a, x, y, s);
+  }
+  // column-major n x k block
+  void apply_block(const double* x, double* y, int k, cudaStream_t s) const {
+    if (sell.ok()) {
+      sell_spmm_colmajor(sell, x, a->ncols, y, a->nrows, k, s);
+    } else {
+      for (int j = 0; j < k; ++j) spmv(*a, x + a->ncols * j, y + a->nrows * j, s);
+    }
   }
   void release(cudaStream_t s) { free_sell(sell, s); }
 };
@@ -459,9 +469,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     sait::Scalars sc(n, 48 * 48, 64, s);
     double *X = S, *W = S + blk, *P = S + 2 * blk;
     double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
-    auto block_spmv = [&](const double* in, double* out) {
-      for (int j = 0; j < k; ++j) op.apply(in + static_cast<int64_t>(j) * n, out + static_cast<int64_t>(j) * n, s);
-    };
+    auto block_spmv = [&](const double* in, double* out) { op.apply_block(in, out, k, s); };
     // G[a][b] = S_a . Y_b (canonical dots, tiled tall-skinny kernel), row-major
     // ka x kb on the host; sym: S == Y, lower tiles mirrored (bitwise equal,
     // the canonical dot is symmetric in its arguments)
@@ -473,7 +481,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
       if (sym)
         for (int a2 = 0; a2 < ka; ++a2)
           for (int b2 = 0; b2 < a2; ++b2)
-            if ((b2 / 8) < (a2 / 8)) G[a2 * kb + b2] = G[b2 * kb + a2];
+            if ((b2 / 4) < (a2 / 4)) G[a2 * kb + b2] = G[b2 * kb + a2];
     };
     auto lincomb = [&](const double* in, int kin, const double* C, int kout, double* out) {
       SAIT_CUDA(cudaMemcpyAsync(dsmall, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));
@@ -496,6 +504,15 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
       return true;
     };
     std::vector<double> GA, GB, C(48 * 16), lam(48);
+    static const bool dbg = std::getenv("SAIT_DEBUG_LOBPCG") != nullptr;
+    auto tp = std::chrono::steady_clock::now();
+    auto phase = [&](const char* nm) {
+      if (!dbg) return;
+      SAIT_CUDA(cudaStreamSynchronize(s));
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "%s=%.2fms ", nm, std::chrono::duration<double, std::milli>(now - tp).count());
+      tp = now;
+    };
     {  // X0 ~ U[-1,1], column j from seed (seed * 1000 + j)
       std::vector<double> h(n);
       for (int j = 0; j < k; ++j) {
@@ -505,6 +522,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
         SAIT_CUDA(cudaStreamSynchronize(s));
       }
     }
+    phase("init_x");
     block_spmv(X, AX);
     bool failed = false;
     std::string why;
@@ -532,9 +550,11 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
           if (h_resnorms) h_resnorms[static_cast<int64_t>(it) * k + j] = sc.h[j];
           if (!(sc.h[j] <= tol)) conv = false;
         }
+        phase("\nresid");
         if (conv || it == maxit) break;
         if (M) sait::pair_apply_block_internal(M, R, W, n, k, 0, s);
         else SAIT_CUDA(cudaMemcpyAsync(W, R, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        phase("precond");
         std::vector<double> G1;
         gram(X, k, W, k, G1);
         SAIT_CUDA(cudaMemcpyAsync(dsmall, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
@@ -545,8 +565,11 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
           why = "lobpcg: preconditioned residual block is rank deficient";
           break;
         }
+        phase("orth_w");
         block_spmv(W, AW);
+        phase("aw");
         const bool use_p = have_p && cholqr(P, AP);
+        phase("cholqr_p");
         int m = use_p ? 3 * k : 2 * k;
         bool ok = false;
         while (true) {
@@ -568,6 +591,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
           }
           break;
         }
+        phase("rr");
         if (!ok) {
           failed = true;
           why = "lobpcg: Gram matrix not positive definite";
@@ -582,6 +606,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
         SAIT_CUDA(cudaMemcpyAsync(X, tmp + 2 * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
         SAIT_CUDA(cudaMemcpyAsync(AX, tmp + 3 * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
         have_p = true;
+        phase("update");
       }
     }
     for (int j = 0; j < k; ++j) h_evals[j] = lam[j];

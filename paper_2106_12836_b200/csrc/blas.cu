@@ -264,7 +264,7 @@ int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
           cudaStream_t s, bool upper_only) {
   const int64_t nb = dot_blocks(n);
-  constexpr int TT = 4;
+  constexpr int TT = 8;
   for (int a0 = 0; a0 < ka; a0 += TT)
     for (int b0 = 0; b0 < kb; b0 += TT) {
       if (upper_only && b0 + TT <= a0) continue;

@@ -481,7 +481,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
       if (sym)
         for (int a2 = 0; a2 < ka; ++a2)
           for (int b2 = 0; b2 < a2; ++b2)
-            if ((b2 / 4) < (a2 / 4)) G[a2 * kb + b2] = G[b2 * kb + a2];
+            if ((b2 / 8) < (a2 / 8)) G[a2 * kb + b2] = G[b2 * kb + a2];
     };
     auto lincomb = [&](const double* in, int kin, const double* C, int kout, double* out) {
       SAIT_CUDA(cudaMemcpyAsync(dsmall, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));

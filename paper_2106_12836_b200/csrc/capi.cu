@@ -1033,13 +1033,24 @@ int pair_variant() {
   return v;
 }
 
+// M_U's SpMV is launched as a programmatic dependent of M_L's (PDL): its
+// CTAs start and load their matrix slices while M_L's tail runs, then wait
+// (griddepcontrol.wait) before touching y.  SAIT_PDL=0 disables.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SAIT_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 // One factor's SpMV with the fastest kernel available for it.
 void factor_spmv(sait_pair_t p, int which, const double* x, double* y, cudaStream_t s) {
   const sait::DevCsr& m = which == 0 ? p->ml->m : p->mu->m;
   const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
   const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
   const int v = pair_variant();
-  if (v >= 2 && sm.ok()) sait::sell_spmv(sm, x, y, s);
+  if (v >= 2 && sm.ok()) sait::sell_spmv_rows(sm, 0, sm.n, x, y, s, which == 1 && pdl_enabled());
   else if (v == 1) sait::spmv_planned(m, pl, x, y, s);
   else sait::spmv(m, x, y, s);
 }

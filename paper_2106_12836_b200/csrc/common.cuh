@@ -151,7 +151,8 @@ void spmv_planned(const DevCsr& a, const SpmvPlan& p, const double* x, double* y
 struct SellMatrix {
   int64_t n = 0, nslices = 0, padded = 0;
   int64_t* soff = nullptr;  // nslices + 1 element offsets (multiples of 32)
-  int32_t* col = nullptr;   // -1 marks padding
+  int32_t* col = nullptr;   // absolute columns, -1 marks padding ...
+  int16_t* dcol = nullptr;  // ... or col - row deltas, INT16_MIN marks padding
   double* val = nullptr;
   bool ok() const { return soff != nullptr; }
 };
@@ -181,7 +182,8 @@ void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan&
                      const double* r, double* y, double* z, cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
 // rows [row0, row1) only (row0 a multiple of 32)
-void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s);
+void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s,
+                    bool pdl = false);  // pdl: programmatic dependent of the previous kernel on s
 // column-major blocks (leading dimensions ldx / ldy), any nvec
 void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
                         cudaStream_t s);

@@ -16,6 +16,7 @@
 //
 // Rows too irregular for slicing (padding > kMaxPad) keep the CSR kernels.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -35,6 +36,30 @@ __device__ __forceinline__ double ld_na(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
+
+__device__ __forceinline__ int16_t ld_na(const int16_t* p) {
+  int16_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.s16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+
+// Column storage of a SELL slice slot: absolute int32 columns (-1 = padding)
+// or int16 deltas col - row (INT16_MIN = padding) when every |col - row| of
+// the matrix fits, which saves 2 of the 12 bytes streamed per entry.
+struct Idx32 {
+  const int32_t* p;
+  __device__ __forceinline__ int32_t col(int64_t e, int64_t /*row*/) const { return ld_na(p + e); }
+};
+struct Idx16 {
+  const int16_t* p;
+  __device__ __forceinline__ int32_t col(int64_t e, int64_t row) const {
+    const int16_t d = ld_na(p + e);
+    return d == INT16_MIN ? -1 : static_cast<int32_t>(row) + d;
+  }
+};
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 __global__ void slice_widths(int64_t n, const int32_t* __restrict__ rp, int64_t nslices, int64_t* __restrict__ width) {
   int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -73,6 +98,44 @@ __global__ void scan_i64_inplace(int64_t* a, int64_t n) {  // single block, excl
   if (threadIdx.x == 0) a[n] = carry_s;
 }
 
+__global__ void max_col_delta(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              int* __restrict__ out) {
+  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int m = 0;
+  if (r < n)
+    for (int32_t e = rp[r]; e < rp[r + 1]; ++e) m = max(m, abs(static_cast<int>(ci[e] - r)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+__global__ void fill_sell16(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const int64_t* __restrict__ soff,
+                            int16_t* __restrict__ scol, double* __restrict__ sval) {
+  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t s = r / kSlice;
+  int lane = static_cast<int>(r % kSlice);
+  int64_t nslices = (n + kSlice - 1) / kSlice;
+  if (s >= nslices) return;
+  int64_t base = soff[s];
+  int32_t w = static_cast<int32_t>((soff[s + 1] - base) / kSlice);
+  int32_t b = 0, len = 0;
+  if (r < n) {
+    b = rp[r];
+    len = rp[r + 1] - b;
+  }
+  for (int32_t k = 0; k < w; ++k) {
+    int64_t dst = base + static_cast<int64_t>(k) * kSlice + lane;
+    if (k < len) {
+      scol[dst] = static_cast<int16_t>(ci[b + k] - r);
+      sval[dst] = v[b + k];
+    } else {
+      scol[dst] = INT16_MIN;
+      sval[dst] = 0.0;
+    }
+  }
+}
+
 __global__ void fill_sell(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ v, const int64_t* __restrict__ soff,
                           int32_t* __restrict__ scol, double* __restrict__ sval) {
@@ -102,19 +165,23 @@ __global__ void fill_sell(int64_t n, const int32_t* __restrict__ rp, const int32
 
 // One warp per slice (grid-stride), lane = row.  Loads are batched 8 slots at
 // a time so each thread has 16 independent streaming loads and 8 gathers in
-// flight.
+// flight.  PDL: when launched as a programmatic dependent (the M_U half of a
+// pair), the first batch of indices/values is loaded before waiting for the
+// producer of x (the M_L half), overlapping that grid's tail.
+template <class IDX, bool PDL_WAIT>
 __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_begin, int64_t nslices,
-                                                         const int64_t* __restrict__ soff,
-                                                         const int32_t* __restrict__ scol,
+                                                         const int64_t* __restrict__ soff, IDX idx,
                                                          const double* __restrict__ sval,
                                                          const double* __restrict__ x, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
+  pdl_launch_dependents();
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  bool waited = !PDL_WAIT;
   for (int64_t s = s_begin + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
        s < nslices; s += warps) {
     const int64_t base = soff[s];
     const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
-    const int32_t* cp = scol + base + lane;
+    const int64_t row = s * kSlice + lane;
     const double* vp = sval + base + lane;
     double acc = 0.0;
     for (int32_t k0 = 0; k0 < w; k0 += 8) {
@@ -125,9 +192,13 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
         c[j] = -1;
         v[j] = 0.0;
         if (k0 + j < w) {
-          c[j] = ld_na(cp + (k0 + j) * kSlice);
+          c[j] = idx.col(base + lane + static_cast<int64_t>(k0 + j) * kSlice, row);
           v[j] = ld_na(vp + (k0 + j) * kSlice);
         }
+      }
+      if (!waited) {
+        pdl_wait();
+        waited = true;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
@@ -135,17 +206,20 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
       for (int j = 0; j < 8; ++j)
         if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
     }
-    const int64_t row = s * kSlice + lane;
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
     if (row < n) y[row] = acc;
   }
+  if (!waited) pdl_wait();
 }
 
 // Row-major block of NV vectors: lane = row, NV accumulators per thread; the
 // slice's indices/values are read once for all NV vectors.
-template <int NV>
+template <int NV, class IDX>
 __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
-                                                         const int32_t* __restrict__ scol,
-                                                         const double* __restrict__ sval,
+                                                         IDX idx, const double* __restrict__ sval,
                                                          const double* __restrict__ x, double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -164,7 +238,7 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
         col[j] = -1;
         v[j] = 0.0;
         if (k0 + j < w) {
-          col[j] = ld_na(scol + base + (k0 + j) * kSlice + lane);
+          col[j] = idx.col(base + (k0 + j) * kSlice + lane, s * kSlice + lane);
           v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
         }
       }
@@ -192,10 +266,9 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
 // Column-major block (n x NV, leading dimension ld): lane = row, NV
 // accumulators; each index/value read once for all NV vectors, x gathered
 // per column (neighbouring rows -> neighbouring x: coalesced).
-template <int NV>
+template <int NV, class IDX>
 __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
-                                                            const int32_t* __restrict__ scol,
-                                                            const double* __restrict__ sval,
+                                                            IDX idx, const double* __restrict__ sval,
                                                             const double* __restrict__ x, int64_t ldx,
                                                             double* __restrict__ y, int64_t ldy, int nv) {
   const int lane = threadIdx.x & 31;
@@ -214,7 +287,7 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
       col[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
-        col[j] = ld_na(scol + base + (k0 + j) * kSlice + lane);
+        col[j] = idx.col(base + (k0 + j) * kSlice + lane, s * kSlice + lane);
         v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
       }
     }
@@ -414,9 +487,30 @@ SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
     dfree(m.soff, s);
     return SellMatrix{};  // too irregular: keep the CSR kernels
   }
-  m.col = dalloc<int32_t>(m.padded, s);
+  // int16 column deltas when every |col - row| fits (and INT16_MIN is free as
+  // the padding marker); SAIT_SELL_INDEX=32 forces absolute int32 columns
+  int maxd = 0;
+  {
+    int* d = dalloc<int>(1, s);
+    SAIT_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+    max_col_delta<<<grid_for(a.nrows, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, d);
+    SAIT_LAUNCHED();
+    SAIT_CUDA(cudaMemcpyAsync(&maxd, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    dfree(d, s);
+  }
+  static const bool force32 = [] {
+    const char* e = std::getenv("SAIT_SELL_INDEX");
+    return e && std::atoi(e) == 32;
+  }();
   m.val = dalloc<double>(m.padded, s);
-  fill_sell<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.col, m.val);
+  if (maxd <= 32767 && !force32) {
+    m.dcol = dalloc<int16_t>(m.padded, s);
+    fill_sell16<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.dcol, m.val);
+  } else {
+    m.col = dalloc<int32_t>(m.padded, s);
+    fill_sell<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.col, m.val);
+  }
   SAIT_LAUNCHED();
   SAIT_CUDA(cudaStreamSynchronize(s));
   return m;
@@ -425,7 +519,7 @@ SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
 PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
                         cudaStream_t s) {
   PairPlan p;
-  if (!sl.ok() || !su.ok()) return p;
+  if (!sl.ok() || !su.ok() || !sl.col || !su.col) return p;  // fused kernel: int32 columns only
   p.gL = (L.nrows + kGroupRows - 1) / kGroupRows;
   p.gU = (U.nrows + kGroupRows - 1) / kGroupRows;
   p.dep_lo = dalloc<int32_t>(p.gU, s);
@@ -480,20 +574,37 @@ void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan&
 void free_sell(SellMatrix& m, cudaStream_t s) {
   dfree(m.soff, s);
   dfree(m.col, s);
+  dfree(m.dcol, s);
   dfree(m.val, s);
   m = SellMatrix{};
 }
 
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s) {
-  if (m.nslices == 0) return;
-  sell_spmv_kernel<<<sell_grid(m.nslices), 256, 0, s>>>(m.n, 0, m.nslices, m.soff, m.col, m.val, x, y);
-  SAIT_LAUNCHED();
+  sell_spmv_rows(m, 0, m.n, x, y, s, false);
 }
 
-void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s) {
+void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s,
+                    bool pdl) {
   const int64_t s0 = row0 / kSlice, s1 = std::min<int64_t>((row1 + kSlice - 1) / kSlice, m.nslices);
   if (s1 <= s0) return;
-  sell_spmv_kernel<<<sell_grid(s1 - s0), 256, 0, s>>>(m.n, s0, s1, m.soff, m.col, m.val, x, y);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sell_grid(s1 - s0));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (m.dcol) {
+    Idx16 ix{m.dcol};
+    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, true>, m.n, s0, s1, m.soff, ix, m.val, x, y));
+    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, false>, m.n, s0, s1, m.soff, ix, m.val, x, y));
+  } else {
+    Idx32 ix{m.col};
+    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, true>, m.n, s0, s1, m.soff, ix, m.val, x, y));
+    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, false>, m.n, s0, s1, m.soff, ix, m.val, x, y));
+  }
   SAIT_LAUNCHED();
 }
 
@@ -502,10 +613,19 @@ void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, doubl
   if (m.nslices == 0) return;
   for (int c0 = 0; c0 < nvec; c0 += 8) {
     const int nv = nvec - c0 < 8 ? nvec - c0 : 8;
-    sell_spmm_cm_kernel<8><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x + ldx * c0,
-                                                                ldx, y + ldy * c0, ldy, nv);
+    if (m.dcol)
+      sell_spmm_cm_kernel<8, Idx16><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, Idx16{m.dcol}, m.val,
+                                                                        x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
+    else
+      sell_spmm_cm_kernel<8, Idx32><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, Idx32{m.col}, m.val,
+                                                                        x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
     SAIT_LAUNCHED();
   }
+}
+
+template <int NV, class IDX>
+void launch_spmm(const SellMatrix& m, IDX ix, const double* x, double* y, cudaStream_t s) {
+  sell_spmm_kernel<NV, IDX><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, ix, m.val, x, y);
 }
 
 bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s) {
@@ -515,13 +635,16 @@ bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaSt
       sell_spmv(m, x, y, s);
       return true;
     case 2:
-      sell_spmm_kernel<2><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+      if (m.dcol) launch_spmm<2>(m, Idx16{m.dcol}, x, y, s);
+      else launch_spmm<2>(m, Idx32{m.col}, x, y, s);
       break;
     case 4:
-      sell_spmm_kernel<4><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+      if (m.dcol) launch_spmm<4>(m, Idx16{m.dcol}, x, y, s);
+      else launch_spmm<4>(m, Idx32{m.col}, x, y, s);
       break;
     case 8:
-      sell_spmm_kernel<8><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, m.col, m.val, x, y);
+      if (m.dcol) launch_spmm<8>(m, Idx16{m.dcol}, x, y, s);
+      else launch_spmm<8>(m, Idx32{m.col}, x, y, s);
       break;
     default:
       return false;

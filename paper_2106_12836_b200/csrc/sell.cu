@@ -48,13 +48,13 @@ __device__ __forceinline__ int16_t ld_na(const int16_t* p) {
 // the matrix fits, which saves 2 of the 12 bytes streamed per entry.
 struct Idx32 {
   const int32_t* p;
-  __device__ __forceinline__ int32_t col(int64_t e, int64_t /*row*/) const { return ld_na(p + e); }
+  __device__ __forceinline__ int32_t col(int64_t e, int32_t /*row*/) const { return ld_na(p + e); }
 };
 struct Idx16 {
   const int16_t* p;
-  __device__ __forceinline__ int32_t col(int64_t e, int64_t row) const {
+  __device__ __forceinline__ int32_t col(int64_t e, int32_t row) const {
     const int16_t d = ld_na(p + e);
-    return d == INT16_MIN ? -1 : static_cast<int32_t>(row) + d;
+    return d == INT16_MIN ? -1 : row + d;
   }
 };
 
@@ -173,46 +173,35 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
                                                          const int64_t* __restrict__ soff, IDX idx,
                                                          const double* __restrict__ sval,
                                                          const double* __restrict__ x, double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
   pdl_launch_dependents();
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  bool waited = !PDL_WAIT;
-  for (int64_t s = s_begin + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       s < nslices; s += warps) {
-    const int64_t base = soff[s];
-    const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
-    const int64_t row = s * kSlice + lane;
-    const double* vp = sval + base + lane;
-    double acc = 0.0;
-    for (int32_t k0 = 0; k0 < w; k0 += 8) {
-      int32_t c[8];
-      double v[8], xv[8];
+  const int lane = threadIdx.x & 31;
+  const int64_t s = s_begin + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;  // grid = one slice per warp
+  const int64_t base = soff[s];
+  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  const int64_t e0 = base + lane;
+  double acc = 0.0;
+  for (int32_t k0 = 0; k0 < w; k0 += 8) {
+    int32_t c[8];
+    double v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = -1;
-        v[j] = 0.0;
-        if (k0 + j < w) {
-          c[j] = idx.col(base + lane + static_cast<int64_t>(k0 + j) * kSlice, row);
-          v[j] = ld_na(vp + (k0 + j) * kSlice);
-        }
+    for (int j = 0; j < 8; ++j) {
+      c[j] = -1;
+      v[j] = 0.0;
+      if (k0 + j < w) {
+        c[j] = idx.col(e0 + static_cast<int64_t>(k0 + j) * kSlice, row);
+        v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
       }
-      if (!waited) {
-        pdl_wait();
-        waited = true;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
     }
-    if (!waited) {
-      pdl_wait();
-      waited = true;
+    if (PDL_WAIT && k0 == 0) pdl_wait();  // x is the previous grid's output
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double xv = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+      if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
     }
-    if (row < n) y[row] = acc;
   }
-  if (!waited) pdl_wait();
+  if (row < n) y[row] = acc;
 }
 
 // Row-major block of NV vectors: lane = row, NV accumulators per thread; the
@@ -238,7 +227,7 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
         col[j] = -1;
         v[j] = 0.0;
         if (k0 + j < w) {
-          col[j] = idx.col(base + (k0 + j) * kSlice + lane, s * kSlice + lane);
+          col[j] = idx.col(base + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
           v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
         }
       }
@@ -287,7 +276,7 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
       col[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
-        col[j] = idx.col(base + (k0 + j) * kSlice + lane, s * kSlice + lane);
+        col[j] = idx.col(base + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
         v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
       }
     }

@@ -58,7 +58,12 @@ struct sait_pair_s {
     double *r_dev = nullptr, *z_dev = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_u;
     cudaEvent_t ev_entry = nullptr, ev_out_done = nullptr;
+    // single-launch dataflow host apply
+    int* in_flag = nullptr;   // device, one per input chunk
+    int* flag_src = nullptr;  // pinned host copy source of the epoch
   };
+  sait::DataflowPlan df;
+  std::vector<int64_t> df_rows;  // input chunk boundaries of the dataflow apply
   // chunking of the host-vector apply: row boundaries (multiples of 256) and,
   // per chunk, the last r-chunk M_L needs and the last y-chunk M_U needs
   std::vector<int64_t> chunk_rows, u_rows;
@@ -390,6 +395,22 @@ void plan_host_chunks(sait_pair_t p) {
     while (g < ng && std::max<int64_t>(run, uhi[g]) < bound_group) run = std::max<int64_t>(run, uhi[g++]);
     p->u_rows[c + 1] = std::max(p->u_rows[c], std::min(n, g * G));
   }
+}
+
+// Input chunks (~2 MB of r) of the single-launch dataflow host apply.
+void plan_dataflow(sait_pair_t p) {
+  const sait::DevCsr& L = p->ml->m;
+  const sait::DevCsr& U = p->mu->m;
+  const int64_t n = L.nrows;
+  p->df_rows.clear();
+  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 16) || !p->sl.ok() || !p->su.ok()) return;
+  double mb = 2.0;
+  if (const char* e = std::getenv("SAIT_DATAFLOW_MB")) mb = std::atof(e);
+  const int64_t G = sait::kDepGroupRows;
+  const int64_t rows = std::max<int64_t>(G, static_cast<int64_t>(mb * (1 << 20) / 8.0) / G * G);
+  for (int64_t r = 0; r < n; r += rows) p->df_rows.push_back(r);
+  p->df_rows.push_back(n);
+  p->df = sait::make_dataflow_plan(L, p->sl, U, p->su, p->df_rows, nullptr);
 }
 
 }  // namespace
@@ -1002,6 +1023,7 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
     p->su = sait::make_sell(mu->m, nullptr);
     p->pp = sait::make_pair_plan(ml->m, p->sl, mu->m, p->su, nullptr);
     plan_host_chunks(p);
+    plan_dataflow(p);
     *out = p;
   });
 }
@@ -1062,7 +1084,7 @@ sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
   sait_pair_s::Work w;
   const int64_t n = p->ml->m.nrows;
   SAIT_CUDA(cudaMalloc(&w.y, sizeof(double) * (n > 0 ? n : 1) + 256));
-  const int64_t ng = std::max<int64_t>(p->pp.gL, 1);
+  const int64_t ng = std::max<int64_t>({p->pp.gL, p->df.gL, int64_t{1}});
   SAIT_CUDA(cudaMalloc(&w.st.done, sizeof(int) * ng));
   SAIT_CUDA(cudaMalloc(&w.st.counter, sizeof(unsigned long long)));
   SAIT_CUDA(cudaMemset(w.st.done, 0, sizeof(int) * ng));
@@ -1152,6 +1174,61 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
   SAIT_CUDA(cudaStreamSynchronize(s));
 }
 
+bool host_dataflow_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SAIT_HOST_DATAFLOW");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+// Host memory the GPU can address directly (pinned / registered under UVA).
+bool device_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
+// Single-launch host apply: copy-engine input chunks + per-chunk epoch flags,
+// one persistent kernel for both SpMVs, z written to host memory directly.
+void pair_apply_host_dataflow(sait_pair_t p, const double* h_r, double* h_z, cudaStream_t s) {
+  sait_pair_s::Work& w = pair_work(p, s);
+  const int64_t k = static_cast<int64_t>(p->df_rows.size()) - 1;
+  const int64_t n = p->ml->m.nrows;
+  if (!w.in_flag) {
+    if (!w.s_in) {
+      SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_in, cudaStreamNonBlocking));
+      SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_out, cudaStreamNonBlocking));
+      SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_entry, cudaEventDisableTiming));
+      SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_out_done, cudaEventDisableTiming));
+    }
+    if (!w.r_dev) {
+      SAIT_CUDA(cudaMalloc(&w.r_dev, sizeof(double) * n + 256));
+      SAIT_CUDA(cudaMalloc(&w.z_dev, sizeof(double) * n + 256));
+    }
+    SAIT_CUDA(cudaMalloc(&w.in_flag, sizeof(int) * k));
+    SAIT_CUDA(cudaMemset(w.in_flag, 0, sizeof(int) * k));
+    SAIT_CUDA(cudaMallocHost(&w.flag_src, sizeof(int) * k));
+    SAIT_CUDA(cudaDeviceSynchronize());
+  }
+  const int epoch = ++w.st.epoch;
+  for (int64_t c = 0; c < k; ++c) w.flag_src[c] = epoch;
+  SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
+  SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_entry, 0));
+  const auto& b = p->df_rows;
+  for (int64_t c = 0; c < k; ++c) {  // data chunk, then its flag: in-order copies on one stream
+    SAIT_CUDA(cudaMemcpyAsync(w.r_dev + b[c], h_r + b[c], sizeof(double) * (b[c + 1] - b[c]),
+                              cudaMemcpyHostToDevice, w.s_in));
+    SAIT_CUDA(cudaMemcpyAsync(w.in_flag + c, w.flag_src + c, sizeof(int), cudaMemcpyHostToDevice, w.s_in));
+  }
+  sait::sell_dataflow_apply(p->sl, p->su, p->df, w.st, w.in_flag, epoch, w.r_dev, w.y, h_z, s);
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  SAIT_CUDA(cudaStreamSynchronize(w.s_in));
+}
+
 }  // namespace
 
 namespace sait {
@@ -1206,7 +1283,9 @@ int sait_pair_apply_host(sait_pair_t p, const double* h_r, int64_t rlen, double*
                           std::to_string(L.ncols));
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
-    if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, sait::as_stream(stream));
+    if (host_dataflow_enabled() && p->df.ok() && device_mapped(h_r) && device_mapped(h_z))
+      pair_apply_host_dataflow(p, h_r, h_z, sait::as_stream(stream));
+    else if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, sait::as_stream(stream));
     else sait::pair_apply_host_pipelined(L, U, h_r, h_z, sait::as_stream(stream));
   });
 }
@@ -1342,7 +1421,10 @@ void sait_pair_destroy(sait_pair_t p) {
       if (w.ev_out_done) cudaEventDestroy(w.ev_out_done);
       if (w.s_in) cudaStreamDestroy(w.s_in);
       if (w.s_out) cudaStreamDestroy(w.s_out);
+      if (w.in_flag) cudaFree(w.in_flag);
+      if (w.flag_src) cudaFreeHost(w.flag_src);
     }
+    sait::free_dataflow_plan(p->df, nullptr);
     cudaDeviceSynchronize();
     if (prev >= 0) cudaSetDevice(prev);
   }

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "sait_c.h"
 
@@ -175,11 +176,28 @@ struct PairState {  // per (pair, stream): flags + claim counter, ordered by the
 // per 256-row group g of m: [lo[g], hi[g]] = 256-column groups its entries touch
 void column_group_deps(const DevCsr& m, int32_t* lo, int32_t* hi, cudaStream_t s);
 constexpr int64_t kDepGroupRows = 256;
+// single-launch host-vector apply (copy-engine input chunks + flags,
+// zero-copy output)
+struct DataflowPlan {
+  int64_t gL = 0, gU = 0;
+  int32_t* lneed = nullptr;
+  int32_t* dep_lo = nullptr;
+  int32_t* dep_hi = nullptr;
+  int grid = 0;
+  bool ok() const { return lneed != nullptr; }
+};
+struct PairState;
+DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
+                                const std::vector<int64_t>& chunk_rows, cudaStream_t s);
+void free_dataflow_plan(DataflowPlan& p, cudaStream_t s);
 PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
                         cudaStream_t s);
 void free_pair_plan(PairPlan& p, cudaStream_t s);
 void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
                      const double* r, double* y, double* z, cudaStream_t s);
+void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const DataflowPlan& dp, PairState& st,
+                         const int* in_flag, int epoch, const double* r_dev, double* y, double* z_host,
+                         cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
 // rows [row0, row1) only (row0 a multiple of 32)
 void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s,

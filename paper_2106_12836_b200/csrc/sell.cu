@@ -17,6 +17,7 @@
 // Rows too irregular for slicing (padding > kMaxPad) keep the CSR kernels.
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -429,6 +430,112 @@ __global__ void __launch_bounds__(256) sell_pair_kernel(PairArgs a) {
   }
 }
 
+// ------------------------------------------------------------ host dataflow
+// z = M_U (M_L r) for HOST r / z in one persistent launch.  The copy engine
+// streams r into r_dev chunk by chunk, each chunk followed by a 4-byte copy of
+// the call's epoch into in_flag[c]; M_L row groups run once the chunk holding
+// their last column has landed (acquire), M_U row groups once the y groups
+// they read are done (release/acquire flags, as in the fused pair), and M_U
+// stores z straight into pinned host memory (zero-copy), so the D2H stream
+// overlaps the H2D stream instead of following it.
+struct DataflowArgs {
+  int64_t n, slicesL, slicesU, gL, gU;
+  const int64_t* soffL;
+  const int64_t* soffU;
+  const double* valL;
+  const double* valU;
+  const int32_t* lneed;     // per M_L group: input chunk that must have landed
+  const int32_t* dep_lo;    // per M_U group: y groups read
+  const int32_t* dep_hi;
+  const int* in_flag;       // per input chunk, written by the copy engine
+  const double* r;          // device copy of r
+  double* y;
+  double* z;                // host-mapped output
+  int* done;                // per M_L group
+  unsigned long long* counter;
+  unsigned long long base;
+  int epoch;
+};
+
+template <class IDX>
+__device__ __forceinline__ double slice_row_idx(const int64_t* __restrict__ soff, IDX idx,
+                                                const double* __restrict__ sval, int64_t s, int lane,
+                                                const double* __restrict__ x) {
+  const int64_t base = soff[s];
+  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  double acc = 0.0;
+  for (int32_t k0 = 0; k0 < w; k0 += 8) {
+    int32_t c[8];
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = -1;
+      v[j] = 0.0;
+      if (k0 + j < w) {
+        c[j] = idx.col(base + lane + static_cast<int64_t>(k0 + j) * kSlice, row);
+        v[j] = ld_na(sval + base + lane + static_cast<int64_t>(k0 + j) * kSlice);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double xv = c[j] >= 0 ? ld_cg(x + c[j]) : 0.0;
+      if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
+    }
+  }
+  return acc;
+}
+
+template <class IDX>
+__global__ void __launch_bounds__(256) sell_dataflow_kernel(DataflowArgs a, IDX il, IDX iu) {
+  __shared__ long long task_s[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long total = a.gL + a.gU;
+  if (threadIdx.x == 0) task_s[0] = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
+  __syncthreads();
+  int buf = 0;
+  while (true) {
+    const long long t = task_s[buf];
+    if (t >= total) break;
+    unsigned long long nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(a.counter, 1ull);
+    if (t < a.gL) {
+      const int32_t need = a.lneed[t];
+      if (threadIdx.x == 0)
+        while (ld_acquire(a.in_flag + need) != a.epoch) __nanosleep(128);
+      __syncthreads();
+      const int64_t s = t * 8 + warp;
+      if (s < a.slicesL) {
+        const double acc = slice_row_idx(a.soffL, il, a.valL, s, lane, a.r);
+        const int64_t row = s * kSlice + lane;
+        if (row < a.n) a.y[row] = acc;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(a.done + t, a.epoch);
+    } else {
+      const int64_t g = t - a.gL;
+      const int32_t lo = a.dep_lo[g], hi = a.dep_hi[g];
+      bool ok;
+      do {
+        ok = true;
+        for (int32_t k = lo + static_cast<int32_t>(threadIdx.x); k <= hi; k += blockDim.x)
+          ok = ok && ld_acquire(a.done + k) == a.epoch;
+        ok = __syncthreads_and(ok);
+        if (!ok) __nanosleep(128);
+      } while (!ok);
+      const int64_t s = g * 8 + warp;
+      if (s < a.slicesU) {
+        const double acc = slice_row_idx(a.soffU, iu, a.valU, s, lane, a.y);
+        const int64_t row = s * kSlice + lane;
+        if (row < a.n) a.z[row] = acc;
+      }
+    }
+    if (threadIdx.x == 0) task_s[buf ^ 1] = static_cast<long long>(nxt - a.base);
+    __syncthreads();
+    buf ^= 1;
+  }
+}
+
 }  // namespace
 
 // lo/hi[g] = column-group range touched by the rows of group g (256 rows).
@@ -557,6 +664,82 @@ void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan&
   a.epoch = ++st.epoch;
   st.claims += static_cast<unsigned long long>(pp.gL + pp.gU) + grid;
   sell_pair_kernel<<<grid, 256, 0, s>>>(a);
+  SAIT_LAUNCHED();
+}
+
+DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
+                                const std::vector<int64_t>& chunk_rows, cudaStream_t s) {
+  DataflowPlan p;
+  const bool same_idx = (sl.dcol != nullptr) == (su.dcol != nullptr);
+  if (!sl.ok() || !su.ok() || !same_idx || L.nrows != U.nrows || chunk_rows.size() < 2) return p;
+  p.gL = (L.nrows + kGroupRows - 1) / kGroupRows;
+  p.gU = p.gL;
+  p.dep_lo = dalloc<int32_t>(p.gU, s);
+  p.dep_hi = dalloc<int32_t>(p.gU, s);
+  pair_deps<<<grid_for(p.gU, 128), 128, 0, s>>>(U.nrows, U.rp, U.ci, p.gU, p.dep_lo, p.dep_hi);
+  SAIT_LAUNCHED();
+  int32_t* llo = dalloc<int32_t>(p.gL, s);
+  int32_t* lhi = dalloc<int32_t>(p.gL, s);
+  pair_deps<<<grid_for(p.gL, 128), 128, 0, s>>>(L.nrows, L.rp, L.ci, p.gL, llo, lhi);
+  SAIT_LAUNCHED();
+  std::vector<int32_t> hhi(p.gL), need(p.gL);
+  SAIT_CUDA(cudaMemcpyAsync(hhi.data(), lhi, sizeof(int32_t) * p.gL, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(llo, s);
+  dfree(lhi, s);
+  // chunk holding the last column each M_L group reads (its own chunk at least)
+  const int64_t nchunks = static_cast<int64_t>(chunk_rows.size()) - 1;
+  for (int64_t g = 0; g < p.gL; ++g) {
+    const int64_t last_row = std::max<int64_t>((hhi[g] + 1) * kGroupRows - 1, std::min(L.nrows, (g + 1) * kGroupRows) - 1);
+    int64_t c = std::upper_bound(chunk_rows.begin(), chunk_rows.end(), std::min<int64_t>(last_row, L.nrows - 1)) -
+                chunk_rows.begin() - 1;
+    need[g] = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(c, 0), nchunks - 1));
+  }
+  p.lneed = dalloc<int32_t>(p.gL, s);
+  SAIT_CUDA(cudaMemcpyAsync(p.lneed, need.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
+  int per_sm = 0;
+  if (sl.dcol) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx16>, 256, 0));
+  else SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx32>, 256, 0));
+  p.grid = std::max(1, per_sm) * num_sms();
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  return p;
+}
+
+void free_dataflow_plan(DataflowPlan& p, cudaStream_t s) {
+  dfree(p.dep_lo, s);
+  dfree(p.dep_hi, s);
+  dfree(p.lneed, s);
+  p = DataflowPlan{};
+}
+
+void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const DataflowPlan& dp, PairState& st,
+                         const int* in_flag, int epoch, const double* r_dev, double* y, double* z_host,
+                         cudaStream_t s) {
+  DataflowArgs a;
+  a.n = sl.n;
+  a.slicesL = sl.nslices;
+  a.slicesU = su.nslices;
+  a.gL = dp.gL;
+  a.gU = dp.gU;
+  a.soffL = sl.soff;
+  a.soffU = su.soff;
+  a.valL = sl.val;
+  a.valU = su.val;
+  a.lneed = dp.lneed;
+  a.dep_lo = dp.dep_lo;
+  a.dep_hi = dp.dep_hi;
+  a.in_flag = in_flag;
+  a.r = r_dev;
+  a.y = y;
+  a.z = z_host;
+  a.done = st.done;
+  a.counter = st.counter;
+  a.base = st.claims;
+  a.epoch = epoch;
+  const unsigned grid = static_cast<unsigned>(dp.grid);
+  st.claims += static_cast<unsigned long long>(dp.gL + dp.gU) + grid;
+  if (sl.dcol) sell_dataflow_kernel<Idx16><<<grid, 256, 0, s>>>(a, Idx16{sl.dcol}, Idx16{su.dcol});
+  else sell_dataflow_kernel<Idx32><<<grid, 256, 0, s>>>(a, Idx32{sl.col}, Idx32{su.col});
   SAIT_LAUNCHED();
 }
 

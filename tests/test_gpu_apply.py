@@ -173,3 +173,24 @@ def test_chunked_host_apply_3d(S, port):
     pair.apply(rd, zd)
     torch.cuda.synchronize()
     assert bitwise_equal(zd.cpu().numpy(), ez)
+
+
+@pytest.mark.parametrize("mb", ["0.25", "0.5", "2"])
+def test_dataflow_host_apply_chunks(S, port, mb, monkeypatch):
+    """Single-launch host apply (copy-engine chunks + flags, zero-copy z) with
+    several chunk sizes: bitwise equal to the oracle, repeatable."""
+    import torch
+
+    from helpers import to_oracle
+
+    monkeypatch.setenv("SAIT_DATAFLOW_MB", mb)
+    A = S.laplacian_3d(64)
+    f = S.ilu_k(A, 0)
+    ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
+    MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
+    pair = S.SaitPairPreconditioner(ML, MU)
+    for seed in (7, 8, 9):
+        r = torch.from_numpy(S.uniform_pm1(seed, A.nrows)).pin_memory()
+        z = torch.zeros_like(r).pin_memory()
+        pair.apply(r.numpy(), z.numpy())
+        assert bitwise_equal(z.numpy(), port.pair_apply(to_oracle(ML), to_oracle(MU), r.numpy()))

@@ -1084,7 +1084,7 @@ sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
   sait_pair_s::Work w;
   const int64_t n = p->ml->m.nrows;
   SAIT_CUDA(cudaMalloc(&w.y, sizeof(double) * (n > 0 ? n : 1) + 256));
-  const int64_t ng = std::max<int64_t>({p->pp.gL, p->df.gL, int64_t{1}});
+  const int64_t ng = std::max<int64_t>(std::max<int64_t>(p->pp.gL, p->df.gL), 1);
   SAIT_CUDA(cudaMalloc(&w.st.done, sizeof(int) * ng));
   SAIT_CUDA(cudaMalloc(&w.st.counter, sizeof(unsigned long long)));
   SAIT_CUDA(cudaMemset(w.st.done, 0, sizeof(int) * ng));

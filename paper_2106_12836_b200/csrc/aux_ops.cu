@@ -58,7 +58,40 @@ __global__ void cap_kernel(int64_t n, double f, int32_t* __restrict__ cnt) {
   }
 }
 
+__global__ void zc_copy_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t n, int vec) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vec == 2) {
+    if (2 * i + 1 < n) reinterpret_cast<double2*>(dst)[i] = reinterpret_cast<const double2*>(src)[i];
+  } else if (i < n) {
+    dst[i] = src[i];
+  }
+}
+
 }  // namespace
+
+// Diagnostics: milliseconds for device->host-mapped (dir 0) or
+// host-mapped->device (dir 1) copies done by SM stores/loads.
+extern "C" double sait_debug_zero_copy_ms(double* host_mapped, int64_t n, int dir, int vec) {
+  double* d = nullptr;
+  cudaMalloc(&d, n * 8);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int64_t work = vec == 2 ? n / 2 : n;
+  auto run = [&] {
+    if (dir == 0) zc_copy_kernel<<<grid_for(work, 256), 256>>>(d, host_mapped, n, vec);
+    else zc_copy_kernel<<<grid_for(work, 256), 256>>>(host_mapped, d, n, vec);
+  };
+  run();
+  cudaEventRecord(a);
+  for (int r = 0; r < 10; ++r) run();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(d);
+  return ms / 10.0;
+}
 
 void narrow_indices(const int64_t* in, int32_t* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return;

@@ -181,6 +181,7 @@ constexpr int64_t kDepGroupRows = 256;
 struct DataflowPlan {
   int64_t gL = 0, gU = 0;
   int32_t* lneed = nullptr;
+  int32_t* order = nullptr;
   int32_t* dep_lo = nullptr;
   int32_t* dep_hi = nullptr;
   int grid = 0;

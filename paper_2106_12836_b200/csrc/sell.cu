@@ -444,6 +444,7 @@ struct DataflowArgs {
   const int64_t* soffU;
   const double* valL;
   const double* valU;
+  const int32_t* order;     // task t -> group (M_L group g, or gL + M_U group)
   const int32_t* lneed;     // per M_L group: input chunk that must have landed
   const int32_t* dep_lo;    // per M_U group: y groups read
   const int32_t* dep_hi;
@@ -495,8 +496,9 @@ __global__ void __launch_bounds__(256) sell_dataflow_kernel(DataflowArgs a, IDX 
   __syncthreads();
   int buf = 0;
   while (true) {
-    const long long t = task_s[buf];
-    if (t >= total) break;
+    const long long claim = task_s[buf];
+    if (claim >= total) break;
+    const long long t = a.order[claim];
     unsigned long long nxt = 0;
     if (threadIdx.x == 0) nxt = atomicAdd(a.counter, 1ull);
     if (t < a.gL) {
@@ -697,6 +699,28 @@ DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const Dev
   }
   p.lneed = dalloc<int32_t>(p.gL, s);
   SAIT_CUDA(cudaMemcpyAsync(p.lneed, need.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
+  // Task order: per input chunk c, its M_L groups, then the M_U groups whose y
+  // reads end inside chunks <= c — so z starts streaming out while r is still
+  // streaming in.  Every wait is on a task claimed earlier: deadlock-free.
+  std::vector<int32_t> uhi(p.gU);
+  SAIT_CUDA(cudaMemcpyAsync(uhi.data(), p.dep_hi, sizeof(int32_t) * p.gU, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> order;
+  order.reserve(p.gL + p.gU);
+  int64_t ug = 0, run = -1;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t g0 = chunk_rows[c] / kGroupRows;
+    const int64_t g1 = (chunk_rows[c + 1] + kGroupRows - 1) / kGroupRows;
+    for (int64_t g = g0; g < g1 && g < p.gL; ++g) order.push_back(static_cast<int32_t>(g));
+    const int64_t bound = c + 1 < nchunks ? chunk_rows[c + 1] / kGroupRows : INT64_MAX;
+    while (ug < p.gU && std::max<int64_t>(run, uhi[ug]) < bound) {
+      run = std::max<int64_t>(run, uhi[ug]);
+      order.push_back(static_cast<int32_t>(p.gL + ug++));
+    }
+  }
+  while (ug < p.gU) order.push_back(static_cast<int32_t>(p.gL + ug++));
+  p.order = dalloc<int32_t>(order.size(), s);
+  SAIT_CUDA(cudaMemcpyAsync(p.order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
   int per_sm = 0;
   if (sl.dcol) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx16>, 256, 0));
   else SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx32>, 256, 0));
@@ -709,6 +733,7 @@ void free_dataflow_plan(DataflowPlan& p, cudaStream_t s) {
   dfree(p.dep_lo, s);
   dfree(p.dep_hi, s);
   dfree(p.lneed, s);
+  dfree(p.order, s);
   p = DataflowPlan{};
 }
 
@@ -725,6 +750,7 @@ void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const Dataf
   a.soffU = su.soff;
   a.valL = sl.val;
   a.valU = su.val;
+  a.order = dp.order;
   a.lneed = dp.lneed;
   a.dep_lo = dp.dep_lo;
   a.dep_hi = dp.dep_hi;

@@ -1209,22 +1209,13 @@ void pair_apply_host_dataflow(sait_pair_t p, const double* h_r, double* h_z, cud
       SAIT_CUDA(cudaMalloc(&w.r_dev, sizeof(double) * n + 256));
       SAIT_CUDA(cudaMalloc(&w.z_dev, sizeof(double) * n + 256));
     }
-    SAIT_CUDA(cudaMalloc(&w.in_flag, sizeof(int) * k));
-    SAIT_CUDA(cudaMemset(w.in_flag, 0, sizeof(int) * k));
+    SAIT_CUDA(cudaMalloc(&w.in_flag, sizeof(int) * (p->df.npieces + k)));
+    SAIT_CUDA(cudaMemset(w.in_flag, 0, sizeof(int) * (p->df.npieces + k)));
     SAIT_CUDA(cudaMallocHost(&w.flag_src, sizeof(int) * k));
     SAIT_CUDA(cudaDeviceSynchronize());
   }
   const int epoch = ++w.st.epoch;
-  for (int64_t c = 0; c < k; ++c) w.flag_src[c] = epoch;
-  SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
-  SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_entry, 0));
-  const auto& b = p->df_rows;
-  for (int64_t c = 0; c < k; ++c) {  // data chunk, then its flag: in-order copies on one stream
-    SAIT_CUDA(cudaMemcpyAsync(w.r_dev + b[c], h_r + b[c], sizeof(double) * (b[c + 1] - b[c]),
-                              cudaMemcpyHostToDevice, w.s_in));
-    SAIT_CUDA(cudaMemcpyAsync(w.in_flag + c, w.flag_src + c, sizeof(int), cudaMemcpyHostToDevice, w.s_in));
-  }
-  sait::sell_dataflow_apply(p->sl, p->su, p->df, w.st, w.in_flag, epoch, w.r_dev, w.y, h_z, s);
+  sait::sell_dataflow_apply(p->sl, p->su, p->df, w.st, w.in_flag, epoch, h_r, w.r_dev, w.y, h_z, s);
   SAIT_CUDA(cudaStreamSynchronize(s));
   SAIT_CUDA(cudaStreamSynchronize(w.s_in));
 }

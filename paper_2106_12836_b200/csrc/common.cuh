@@ -182,6 +182,9 @@ struct DataflowPlan {
   int64_t gL = 0, gU = 0;
   int32_t* lneed = nullptr;
   int32_t* order = nullptr;
+  int32_t* lp_lo = nullptr;  // per M_L group: input pieces read
+  int32_t* lp_hi = nullptr;
+  int64_t piece = 0, npieces = 0;
   int32_t* dep_lo = nullptr;
   int32_t* dep_hi = nullptr;
   int grid = 0;
@@ -197,7 +200,7 @@ void free_pair_plan(PairPlan& p, cudaStream_t s);
 void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
                      const double* r, double* y, double* z, cudaStream_t s);
 void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const DataflowPlan& dp, PairState& st,
-                         const int* in_flag, int epoch, const double* r_dev, double* y, double* z_host,
+                         int* in_flag, int epoch, const double* r_host, double* r_dev, double* y, double* z_host,
                          cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
 // rows [row0, row1) only (row0 a multiple of 32)

@@ -448,8 +448,13 @@ struct DataflowArgs {
   const int32_t* lneed;     // per M_L group: input chunk that must have landed
   const int32_t* dep_lo;    // per M_U group: y groups read
   const int32_t* dep_hi;
-  const int* in_flag;       // per input chunk, written by the copy engine
-  const double* r;          // device copy of r
+  int* in_flag;             // per input piece (epoch when landed)
+  const double* r_host;     // host-mapped r (zero-copy loads)
+  int64_t piece;            // doubles per input piece
+  int64_t npieces;
+  const int32_t* lp_lo;     // per M_L group: input pieces its columns read
+  const int32_t* lp_hi;
+  double* r;                // device copy of r
   double* y;
   double* z;                // host-mapped output
   int* done;                // per M_L group
@@ -491,7 +496,7 @@ template <class IDX>
 __global__ void __launch_bounds__(256) sell_dataflow_kernel(DataflowArgs a, IDX il, IDX iu) {
   __shared__ long long task_s[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long total = a.gL + a.gU;
+  const long long total = a.gL + a.gU + a.npieces;
   if (threadIdx.x == 0) task_s[0] = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
   __syncthreads();
   int buf = 0;
@@ -501,11 +506,29 @@ __global__ void __launch_bounds__(256) sell_dataflow_kernel(DataflowArgs a, IDX 
     const long long t = a.order[claim];
     unsigned long long nxt = 0;
     if (threadIdx.x == 0) nxt = atomicAdd(a.counter, 1ull);
-    if (t < a.gL) {
-      const int32_t need = a.lneed[t];
-      if (threadIdx.x == 0)
-        while (ld_acquire(a.in_flag + need) != a.epoch) __nanosleep(128);
+    if (t >= a.gL + a.gU) {  // input piece: host r -> device r (zero-copy loads)
+      const int64_t q = t - a.gL - a.gU;
+      const int64_t b = q * a.piece, e = b + a.piece < a.n ? b + a.piece : a.n;
+      for (int64_t i = b + 2 * threadIdx.x; i < e; i += 2 * blockDim.x) {
+        if (i + 1 < e) {
+          const double2 v = __ldcv(reinterpret_cast<const double2*>(a.r_host + i));
+          *reinterpret_cast<double2*>(a.r + i) = v;
+        } else {
+          a.r[i] = __ldcv(a.r_host + i);
+        }
+      }
       __syncthreads();
+      if (threadIdx.x == 0) st_release(a.in_flag + q, a.epoch);
+    } else if (t < a.gL) {
+      const int32_t lo = a.lp_lo[t], hi = a.lp_hi[t];
+      bool ok;
+      do {
+        ok = true;
+        for (int32_t k = lo + static_cast<int32_t>(threadIdx.x); k <= hi; k += blockDim.x)
+          ok = ok && ld_acquire(a.in_flag + k) == a.epoch;
+        ok = __syncthreads_and(ok);
+        if (!ok) __nanosleep(128);
+      } while (!ok);
       const int64_t s = t * 8 + warp;
       if (s < a.slicesL) {
         const double acc = slice_row_idx(a.soffL, il, a.valL, s, lane, a.r);
@@ -684,11 +707,34 @@ DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const Dev
   int32_t* lhi = dalloc<int32_t>(p.gL, s);
   pair_deps<<<grid_for(p.gL, 128), 128, 0, s>>>(L.nrows, L.rp, L.ci, p.gL, llo, lhi);
   SAIT_LAUNCHED();
-  std::vector<int32_t> hhi(p.gL), need(p.gL);
+  std::vector<int32_t> hhi(p.gL), hlo(p.gL), need(p.gL);
   SAIT_CUDA(cudaMemcpyAsync(hhi.data(), lhi, sizeof(int32_t) * p.gL, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaMemcpyAsync(hlo.data(), llo, sizeof(int32_t) * p.gL, cudaMemcpyDeviceToHost, s));
   SAIT_CUDA(cudaStreamSynchronize(s));
   dfree(llo, s);
   dfree(lhi, s);
+  // input pieces (64 KB of r each) and the piece range every M_L group reads
+  std::vector<int32_t> plo_h, phi_h;
+  p.piece = 8192;
+  p.npieces = (L.nrows + p.piece - 1) / p.piece;
+  {
+    plo_h.assign(p.gL, 0);
+    phi_h.assign(p.gL, 0);
+    auto& plo = plo_h;
+    auto& phi = phi_h;
+    for (int64_t g = 0; g < p.gL; ++g) {
+      const int64_t own0 = g * kGroupRows, own1 = std::min(L.nrows, (g + 1) * kGroupRows) - 1;
+      const int64_t c0 = hhi[g] >= hlo[g] ? std::min<int64_t>(own0, int64_t{hlo[g]} * kGroupRows) : own0;
+      const int64_t c1 = hhi[g] >= hlo[g] ? std::max<int64_t>(own1, int64_t{hhi[g]} * kGroupRows + kGroupRows - 1) : own1;
+      plo[g] = static_cast<int32_t>(c0 / p.piece);
+      phi[g] = static_cast<int32_t>(std::min<int64_t>(c1, L.nrows - 1) / p.piece);
+    }
+    p.lp_lo = dalloc<int32_t>(p.gL, s);
+    p.lp_hi = dalloc<int32_t>(p.gL, s);
+    SAIT_CUDA(cudaMemcpyAsync(p.lp_lo, plo.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
+    SAIT_CUDA(cudaMemcpyAsync(p.lp_hi, phi.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+  }
   // chunk holding the last column each M_L group reads (its own chunk at least)
   const int64_t nchunks = static_cast<int64_t>(chunk_rows.size()) - 1;
   for (int64_t g = 0; g < p.gL; ++g) {
@@ -706,11 +752,21 @@ DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const Dev
   SAIT_CUDA(cudaMemcpyAsync(uhi.data(), p.dep_hi, sizeof(int32_t) * p.gU, cudaMemcpyDeviceToHost, s));
   SAIT_CUDA(cudaStreamSynchronize(s));
   std::vector<int32_t> order;
-  order.reserve(p.gL + p.gU);
-  int64_t ug = 0, run = -1;
+  order.reserve(p.gL + p.gU + p.npieces);
+  int64_t ug = 0, run = -1, next_piece = 0;
+  const int32_t in_base = static_cast<int32_t>(p.gL + p.gU);
+  auto push_pieces_upto = [&](int64_t row_end) {  // input tasks for rows < row_end
+    const int64_t last = std::min<int64_t>(p.npieces, (row_end + p.piece - 1) / p.piece);
+    while (next_piece < last) order.push_back(in_base + static_cast<int32_t>(next_piece++));
+  };
   for (int64_t c = 0; c < nchunks; ++c) {
+    // inputs of chunk c and (prefetch) c + 1 before chunk c's compute tasks
+    push_pieces_upto(chunk_rows[std::min<int64_t>(c + 2, nchunks)]);
     const int64_t g0 = chunk_rows[c] / kGroupRows;
     const int64_t g1 = (chunk_rows[c + 1] + kGroupRows - 1) / kGroupRows;
+    int64_t need_piece = -1;  // every input an M_L group waits for is queued before it
+    for (int64_t g = g0; g < g1 && g < p.gL; ++g) need_piece = std::max<int64_t>(need_piece, phi_h[g]);
+    push_pieces_upto((need_piece + 1) * p.piece);
     for (int64_t g = g0; g < g1 && g < p.gL; ++g) order.push_back(static_cast<int32_t>(g));
     const int64_t bound = c + 1 < nchunks ? chunk_rows[c + 1] / kGroupRows : INT64_MAX;
     while (ug < p.gU && std::max<int64_t>(run, uhi[ug]) < bound) {
@@ -719,6 +775,7 @@ DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const Dev
     }
   }
   while (ug < p.gU) order.push_back(static_cast<int32_t>(p.gL + ug++));
+  push_pieces_upto(L.nrows);
   p.order = dalloc<int32_t>(order.size(), s);
   SAIT_CUDA(cudaMemcpyAsync(p.order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
   int per_sm = 0;
@@ -734,11 +791,13 @@ void free_dataflow_plan(DataflowPlan& p, cudaStream_t s) {
   dfree(p.dep_hi, s);
   dfree(p.lneed, s);
   dfree(p.order, s);
+  dfree(p.lp_lo, s);
+  dfree(p.lp_hi, s);
   p = DataflowPlan{};
 }
 
 void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const DataflowPlan& dp, PairState& st,
-                         const int* in_flag, int epoch, const double* r_dev, double* y, double* z_host,
+                         int* in_flag, int epoch, const double* r_host, double* r_dev, double* y, double* z_host,
                          cudaStream_t s) {
   DataflowArgs a;
   a.n = sl.n;
@@ -755,6 +814,11 @@ void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const Dataf
   a.dep_lo = dp.dep_lo;
   a.dep_hi = dp.dep_hi;
   a.in_flag = in_flag;
+  a.r_host = r_host;
+  a.piece = dp.piece;
+  a.npieces = dp.npieces;
+  a.lp_lo = dp.lp_lo;
+  a.lp_hi = dp.lp_hi;
   a.r = r_dev;
   a.y = y;
   a.z = z_host;
@@ -763,7 +827,7 @@ void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const Dataf
   a.base = st.claims;
   a.epoch = epoch;
   const unsigned grid = static_cast<unsigned>(dp.grid);
-  st.claims += static_cast<unsigned long long>(dp.gL + dp.gU) + grid;
+  st.claims += static_cast<unsigned long long>(dp.gL + dp.gU + dp.npieces) + grid;
   if (sl.dcol) sell_dataflow_kernel<Idx16><<<grid, 256, 0, s>>>(a, Idx16{sl.dcol}, Idx16{su.dcol});
   else sell_dataflow_kernel<Idx32><<<grid, 256, 0, s>>>(a, Idx32{sl.col}, Idx32{su.col});
   SAIT_LAUNCHED();

@@ -16,6 +16,7 @@
 //
 // Rows too irregular for slicing (padding > kMaxPad) keep the CSR kernels.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -461,7 +462,14 @@ struct DataflowArgs {
   unsigned long long* counter;
   unsigned long long base;
   int epoch;
+  unsigned long long* trace;  // optional: globaltimer at the end of each task
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <class IDX>
 __device__ __forceinline__ double slice_row_idx(const int64_t* __restrict__ soff, IDX idx,
@@ -555,6 +563,7 @@ __global__ void __launch_bounds__(256) sell_dataflow_kernel(DataflowArgs a, IDX 
         if (row < a.n) a.z[row] = acc;
       }
     }
+    if (a.trace && threadIdx.x == 0) a.trace[t] = globaltimer();
     if (threadIdx.x == 0) task_s[buf ^ 1] = static_cast<long long>(nxt - a.base);
     __syncthreads();
     buf ^= 1;
@@ -826,11 +835,48 @@ void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const Dataf
   a.counter = st.counter;
   a.base = st.claims;
   a.epoch = epoch;
+  a.trace = nullptr;
+  static const bool dbg = std::getenv("SAIT_DEBUG_DATAFLOW") != nullptr;
+  const int64_t ntask = dp.gL + dp.gU + dp.npieces;
+  unsigned long long* tr = nullptr;
+  unsigned long long t0 = 0;
+  if (dbg) {
+    SAIT_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * ntask));
+    a.trace = tr;
+  }
   const unsigned grid = static_cast<unsigned>(dp.grid);
   st.claims += static_cast<unsigned long long>(dp.gL + dp.gU + dp.npieces) + grid;
   if (sl.dcol) sell_dataflow_kernel<Idx16><<<grid, 256, 0, s>>>(a, Idx16{sl.dcol}, Idx16{su.dcol});
   else sell_dataflow_kernel<Idx32><<<grid, 256, 0, s>>>(a, Idx32{sl.col}, Idx32{su.col});
   SAIT_LAUNCHED();
+  if (dbg) {
+    std::vector<unsigned long long> h(ntask);
+    SAIT_CUDA(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * ntask, cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tr);
+    t0 = *std::min_element(h.begin(), h.end());
+    auto stat = [&](int64_t b, int64_t e, const char* nm) {
+      unsigned long long mx = 0, mn = ~0ull;
+      for (int64_t i = b; i < e; ++i) {
+        mx = std::max(mx, h[i] - t0);
+        mn = std::min(mn, h[i] - t0);
+      }
+      std::fprintf(stderr, "%s first=%.1fus last=%.1fus  ", nm, mn / 1e3, mx / 1e3);
+    };
+    stat(0, dp.gL, "L");
+    stat(dp.gL, dp.gL + dp.gU, "U");
+    stat(dp.gL + dp.gU, ntask, "IN");
+    // input progress: time by which each quarter of the pieces had landed
+    std::vector<unsigned long long> ins(h.begin() + dp.gL + dp.gU, h.end());
+    std::sort(ins.begin(), ins.end());
+    for (int qq = 1; qq <= 4; ++qq)
+      std::fprintf(stderr, "IN%d/4=%.1fus ", qq, (ins[ins.size() * qq / 4 - 1] - t0) / 1e3);
+    std::vector<unsigned long long> us(h.begin() + dp.gL, h.begin() + dp.gL + dp.gU);
+    std::sort(us.begin(), us.end());
+    for (int qq = 1; qq <= 4; ++qq)
+      std::fprintf(stderr, "U%d/4=%.1fus ", qq, (us[us.size() * qq / 4 - 1] - t0) / 1e3);
+    std::fprintf(stderr, "\n");
+  }
 }
 
 void free_sell(SellMatrix& m, cudaStream_t s) {

@@ -184,6 +184,7 @@ def test_dataflow_host_apply_chunks(S, port, mb, monkeypatch):
     from helpers import to_oracle
 
     monkeypatch.setenv("SAIT_DATAFLOW_MB", mb)
+    monkeypatch.setenv("SAIT_HOST_DATAFLOW", "1")
     A = S.laplacian_3d(64)
     f = S.ilu_k(A, 0)
     ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))

@@ -168,6 +168,14 @@ int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_s
 int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double *d_b, int sweeps, double *d_x,
                              sait_stream_t stream);
 
+/* kernels.hpp:36 / kernels.cpp:196-234: x = T^-1 b by substitution (Lower:
+ * rows ascending, Upper: descending; the stored diagonal is used, entries on
+ * the wrong side of it read x as zero), device vectors, bitwise the
+ * reference's result.  Synchronous; SAIT_ERR_RUNTIME "trisolve: singular
+ * matrix, zero diagonal at row i" for the first such row in solve order. */
+int sait_trisolve(sait_dcsr_t t, int lower, const double *d_b, int64_t blen, double *d_x,
+                  sait_stream_t stream);
+
 /* ------------------------------------------------------- SpMV operator ---
  * A prepared y = A x for a (possibly rectangular) device CSR: keeps the
  * SELL-32 copy when the rows are regular enough (the apply's kernel), else the
@@ -209,6 +217,19 @@ int sait_pair_spmv_factor(sait_pair_t p, int which, const double *d_x, double *d
 /* Borrowed handles of the two factors (owned by the pair). */
 int sait_pair_factors(sait_pair_t p, sait_dcsr_t *ml, sait_dcsr_t *mu);
 void sait_pair_destroy(sait_pair_t p);
+
+/* ------------------------------------------ exact ILU preconditioner ---
+ * ExactIluPreconditioner (preconditioner.hpp:39-49, preconditioner.cpp:25-32):
+ * z = U^-1 (L^-1 r), the sequential baseline SAIT replaces, on the device.
+ * name() == "exact", nnz() = nnz(L) + nnz(U).  Takes ownership of the
+ * factors when take_ownership != 0.  apply is synchronous (it reports a zero
+ * pivot like trisolve) and safe to call concurrently on different streams. */
+typedef struct sait_exact_s *sait_exact_t;
+int sait_exact_ilu_create(sait_dcsr_t lower, sait_dcsr_t upper, int take_ownership, sait_exact_t *out);
+int sait_exact_ilu_info(sait_exact_t p, int64_t *n, int64_t *nnz);
+int sait_exact_ilu_apply(sait_exact_t p, const double *d_r, int64_t rlen, double *d_z, int64_t zlen,
+                         sait_stream_t stream);
+void sait_exact_ilu_destroy(sait_exact_t p);
 
 /* ------------------------------------------------------------ solvers ---
  * Device-resident loops driving the apply (north_star (3)); the reference has

@@ -1,7 +1,7 @@
 // saitprec/kernels.hpp — drop-in for the reference's kernels.hpp (:12-40).
 // spmv / spgemm / add_identity / drop_* / scale_columns run on the B200 and
-// return bitwise the reference's results; trisolve is the sequential exact
-// solve the SAIT pair replaces and stays on the host.
+// return bitwise the reference's results; so does trisolve, the exact solve
+// the SAIT pair replaces (synchronization-free substitution on the device).
 #pragma once
 
 #include <span>

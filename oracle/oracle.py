@@ -237,6 +237,13 @@ class Oracle:
         self._check(self._fn("jacobi_sweeps_apply")(C.byref(_in(t)), C.c_int(int(lower)), _dptr(b), C.c_int(sweeps), _dptr(x)))
         return x
 
+    def trisolve(self, t: Csr, lower: bool, b: np.ndarray) -> np.ndarray:
+        """kernels.cpp:196-234 (x starts at zero, as the reference's vector)."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(t.nrows)
+        self._check(self._fn("trisolve")(C.byref(_in(t)), C.c_int(int(lower)), _dptr(b), _dptr(x)))
+        return x
+
     # -- ilu.cpp
     def ilu_k(self, a: Csr, level: int):
         lo, up = _CCsr(), _CCsr()

@@ -238,6 +238,13 @@ int ref_jacobi_sweeps_apply(const ref_csr* t, int lower, const double* b, int sw
     std::memcpy(x, r.data(), sizeof(double) * r.size());
   });
 }
+int ref_trisolve(const ref_csr* t, int lower, const double* b, double* x) {
+  return guarded([&] {
+    std::vector<double> r =
+        saitprec::trisolve(to_ref(t), kind_of(lower), std::span<const double>(b, t->nrows));
+    std::memcpy(x, r.data(), sizeof(double) * r.size());
+  });
+}
 int ref_ilu_k(const ref_csr* a, int level, ref_csr* lower, ref_csr* upper) {
   return guarded([&] {
     saitprec::IluFactors f = saitprec::ilu_k(to_ref(a), level);

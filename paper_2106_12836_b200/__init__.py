@@ -25,7 +25,14 @@ from .csr import (
     unit_upper_triangular,
     upper_triangular,
 )
-from .preconditioner import IdentityPreconditioner, Preconditioner, SaitPairPreconditioner, apply_precond
+from .preconditioner import (
+    ExactIluPreconditioner,
+    IdentityPreconditioner,
+    JacobiSweepsPreconditioner,
+    Preconditioner,
+    SaitPairPreconditioner,
+    apply_precond,
+)
 from .problems import IluFactors, convdiff_2d, ilu_k, laplacian_2d, laplacian_3d, synthetic_lower, uniform_pm1
 from .solvers import EigResult, SolveStats, gmres, lobpcg, pcg
 from .sait import (
@@ -47,6 +54,8 @@ from .sait import (
     spgemm,
     spmv,
     transpose,
+    trisolve,
+    jacobi_sweeps_apply,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

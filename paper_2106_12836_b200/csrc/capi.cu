@@ -26,6 +26,20 @@ struct sait_op_s {
   sait::SellMatrix sell;
 };
 
+struct sait_exact_s {
+  int dev = 0;
+  sait_dcsr_s* l = nullptr;
+  sait_dcsr_s* u = nullptr;
+  bool owns = false;
+  sait::TrisolvePlan pl, pu;  // level order of each factor (analysed at create)
+  struct Work {
+    double* y = nullptr;
+    sait::TrisolveState sl, su;
+  };
+  std::mutex mu;
+  std::unordered_map<cudaStream_t, Work> ws;  // per-stream flags + y
+};
+
 namespace {
 class Recursion;
 }  // namespace
@@ -998,6 +1012,109 @@ void sait_operator_destroy(sait_op_t op) {
   if (op->owns) sait_csr_free(op->a);
   if (prev >= 0) cudaSetDevice(prev);
   delete op;
+}
+
+// --------------------------------------------------------- exact triangular
+
+int sait_trisolve(sait_dcsr_t t, int lower, const double* d_b, int64_t blen, double* d_x,
+                  sait_stream_t stream) {
+  return guarded([&] {
+    need(t, "trisolve");
+    if (t->m.nrows != t->m.ncols) sait::throw_invalid("trisolve: matrix is not square");
+    if (blen != t->m.nrows) sait::throw_invalid("trisolve: right-hand side length mismatch");
+    DeviceGuard g(t->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::TrisolveState st;
+    sait::TrisolvePlan plan;
+    try {
+      plan = sait::analyse_triangular(t->m, lower != 0, s);
+      sait::trisolve(t->m, lower != 0, plan, d_b, d_x, st, s);
+    } catch (...) {
+      sait::free_trisolve_state(st, s);
+      sait::free_trisolve_plan(plan, s);
+      throw;
+    }
+    sait::free_trisolve_state(st, s);
+    sait::free_trisolve_plan(plan, s);
+  });
+}
+
+int sait_exact_ilu_create(sait_dcsr_t lower, sait_dcsr_t upper, int take_ownership, sait_exact_t* out) {
+  return guarded([&] {
+    need(lower, "ExactIluPreconditioner");
+    need(upper, "ExactIluPreconditioner");
+    need(out, "ExactIluPreconditioner(out)");
+    DeviceGuard g(lower->dev);
+    init_device_pool();
+    auto* p = new sait_exact_s;
+    p->dev = lower->dev;
+    p->l = lower;
+    p->u = upper;
+    try {
+      p->pl = sait::analyse_triangular(lower->m, true, nullptr);
+      p->pu = sait::analyse_triangular(upper->m, false, nullptr);
+    } catch (...) {
+      sait::free_trisolve_plan(p->pl, nullptr);
+      delete p;
+      throw;
+    }
+    p->owns = take_ownership != 0;
+    *out = p;
+  });
+}
+
+int sait_exact_ilu_info(sait_exact_t p, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    need(p, "ExactIluPreconditioner");
+    if (n) *n = p->l->m.nrows;
+    if (nnz) *nnz = p->l->m.nnz + p->u->m.nnz;
+  });
+}
+
+int sait_exact_ilu_apply(sait_exact_t p, const double* d_r, int64_t rlen, double* d_z, int64_t zlen,
+                         sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "ExactIluPreconditioner::apply");
+    const sait::DevCsr& L = p->l->m;
+    const sait::DevCsr& U = p->u->m;
+    if (L.nrows != L.ncols || U.nrows != U.ncols) sait::throw_invalid("trisolve: matrix is not square");
+    if (rlen != L.nrows || U.nrows != L.nrows) sait::throw_invalid("trisolve: right-hand side length mismatch");
+    if (zlen != U.nrows) sait::throw_invalid("ExactIluPreconditioner: output length mismatch");
+    DeviceGuard g(p->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait_exact_s::Work* w;
+    {
+      std::lock_guard<std::mutex> lk(p->mu);
+      w = &p->ws[s];
+      if (!w->y && L.nrows) w->y = sait::dalloc<double>(L.nrows, s);
+    }
+    sait::trisolve(L, true, p->pl, d_r, w->y, w->sl, s);    // y = L^-1 r (unit_lower_triangular)
+    sait::trisolve(U, false, p->pu, w->y, d_z, w->su, s);   // z = U^-1 y (upper_triangular)
+  });
+}
+
+void sait_exact_ilu_destroy(sait_exact_t p) {
+  if (!p) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->dev);
+  cudaDeviceSynchronize();
+  for (auto& kv : p->ws) {
+    sait::dfree(kv.second.y, nullptr);
+    sait::free_trisolve_state(kv.second.sl, nullptr);
+    sait::free_trisolve_state(kv.second.su, nullptr);
+  }
+  sait::free_trisolve_plan(p->pl, nullptr);
+  sait::free_trisolve_plan(p->pu, nullptr);
+  cudaDeviceSynchronize();
+  if (p->owns) {
+    sait_csr_free(p->l);
+    sait_csr_free(p->u);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  delete p;
 }
 
 // -------------------------------------------------------- pair preconditioner

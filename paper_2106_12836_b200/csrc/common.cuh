@@ -215,6 +215,23 @@ void spmm_rowmajor(const DevCsr& a, const double* x, double* y, int nvec, cudaSt
 void transpose_block(const double* in, double* out, int64_t n, int nvec, bool to_rowmajor,
                      cudaStream_t s);
 
+// trisolve.cu: synchronization-free exact triangular solve (kernels.cpp:196-234)
+struct TrisolvePlan {  // per factor: rows sorted by dependency level
+  int32_t* perm = nullptr;
+  int64_t nlevels = 0;
+};
+TrisolvePlan analyse_triangular(const DevCsr& t, bool lower, cudaStream_t s);
+void free_trisolve_plan(TrisolvePlan& p, cudaStream_t s);
+struct TrisolveState {  // completion flags (epoch-tagged) + claim counter, per stream
+  int* done = nullptr;
+  unsigned long long* counter = nullptr;
+  int* bad = nullptr;
+  int epoch = 0;
+};
+void trisolve(const DevCsr& t, bool lower, const TrisolvePlan& plan, const double* b, double* x,
+              TrisolveState& st, cudaStream_t s);
+void free_trisolve_state(TrisolveState& st, cudaStream_t s);
+
 // blas.cu (elementwise helpers)
 void hadamard(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a * b
 void add_into(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a + b

@@ -327,30 +327,17 @@ CsrMatrix drop_by_pattern(const CsrMatrix& m, const SparsityPattern& s) {
   return download(o.h);
 }
 
-// The sequential exact solve SAIT replaces (host by nature).
+// The exact solve SAIT replaces, on the device (synchronization-free
+// substitution, bitwise the sequential result).
 std::vector<double> trisolve(const CsrMatrix& t, TriangularKind kind, std::span<const double> b) {
   if (t.nrows != t.ncols) throw std::invalid_argument("trisolve: matrix is not square");
   if (static_cast<index_t>(b.size()) != t.nrows) throw std::invalid_argument("trisolve: right-hand side length mismatch");
-  const index_t n = t.nrows;
-  const bool lower = kind.side == TriangularKind::Side::Lower;
-  std::vector<double> x(n);
-  for (index_t step = 0; step < n; ++step) {
-    const index_t i = lower ? step : n - 1 - step;
-    double acc = b[i], d = 0.0;
-    bool have = false;
-    for (index_t k = t.row_ptr[i]; k < t.row_ptr[i + 1]; ++k) {
-      const index_t j = t.col_idx[k];
-      if (j == i) {
-        d = t.values[k];
-        have = true;
-      } else {
-        acc -= t.values[k] * x[j];
-      }
-    }
-    if (!have || d == 0.0)
-      throw std::runtime_error("trisolve: singular matrix, zero diagonal at row " + std::to_string(i));
-    x[i] = acc / d;
-  }
+  Dev d = upload(t);
+  DevVec db(b.size()), dx(b.size());
+  db.put(b.data(), b.size());
+  check(sait_trisolve(d.h, lower_flag(kind), db.p, static_cast<int64_t>(b.size()), dx.p, thread_stream()));
+  std::vector<double> x(b.size());
+  dx.get(x.data(), x.size());
   return x;
 }
 
@@ -532,12 +519,23 @@ void IdentityPreconditioner::apply(std::span<const double> r, std::span<double> 
   std::copy(r.begin(), r.end(), z.begin());
 }
 
-ExactIluPreconditioner::ExactIluPreconditioner(IluFactors factors) : factors_(std::move(factors)) {}
+ExactIluPreconditioner::ExactIluPreconditioner(IluFactors factors) : factors_(std::move(factors)) {
+  Dev dl = upload(factors_.lower), du = upload(factors_.upper);
+  sait_exact_t h = nullptr;
+  check(sait_exact_ilu_create(dl.h, du.h, 1, &h));
+  dl.release();
+  du.release();
+  exact_ = h;
+}
+
+ExactIluPreconditioner::~ExactIluPreconditioner() { sait_exact_ilu_destroy(static_cast<sait_exact_t>(exact_)); }
 
 void ExactIluPreconditioner::apply(std::span<const double> r, std::span<double> z) const {
-  const std::vector<double> y = trisolve(factors_.lower, unit_lower_triangular, r);
-  const std::vector<double> x = trisolve(factors_.upper, upper_triangular, y);
-  std::copy(x.begin(), x.end(), z.begin());
+  DevVec dr(r.size()), dz(z.size());
+  dr.put(r.data(), r.size());
+  check(sait_exact_ilu_apply(static_cast<sait_exact_t>(exact_), dr.p, static_cast<int64_t>(r.size()), dz.p,
+                             static_cast<int64_t>(z.size()), thread_stream()));
+  dz.get(z.data(), z.size());
 }
 
 SaitPairPreconditioner::SaitPairPreconditioner(CsrMatrix lower_inverse, CsrMatrix upper_inverse)

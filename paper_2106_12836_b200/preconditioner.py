@@ -145,6 +145,88 @@ class SaitPairPreconditioner(Preconditioner):
             pass
 
 
+class ExactIluPreconditioner(Preconditioner):
+    """preconditioner.hpp:39-49 / preconditioner.cpp:25-32: z = U^-1 (L^-1 r),
+    the sequential baseline SAIT replaces, as two device triangular solves
+    (sait_exact_ilu_*).  ``factors`` is an IluFactors (host CsrMatrix or
+    DeviceCsr lower/upper)."""
+
+    def __init__(self, factors, stream=None):
+        lo, up = factors.lower, factors.upper
+        dl = lo if isinstance(lo, DeviceCsr) else DeviceCsr.upload(lo, stream)
+        du = up if isinstance(up, DeviceCsr) else DeviceCsr.upload(up, stream)
+        h = C.c_void_p()
+        N.check(N.lib.sait_exact_ilu_create(dl.handle, du.handle, 1, C.byref(h)))
+        dl.release()
+        du.release()
+        self._h = h
+        n, nnz = C.c_int64(), C.c_int64()
+        N.check(N.lib.sait_exact_ilu_info(self._h, C.byref(n), C.byref(nnz)))
+        self.n, self._nnz = n.value, nnz.value
+
+    def name(self) -> str:
+        return "exact"
+
+    def nnz(self) -> int:
+        return self._nnz
+
+    def apply(self, r, z, stream=None) -> None:
+        import torch
+
+        if _is_cuda_tensor(r):
+            s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+            N.check(N.lib.sait_exact_ilu_apply(self._h, r.data_ptr(), r.numel(), z.data_ptr(), z.numel(), s))
+            return
+        rd = torch.from_numpy(np.ascontiguousarray(r, dtype=np.float64)).cuda()
+        zd = torch.empty(len(z), dtype=torch.float64, device="cuda")
+        N.check(N.lib.sait_exact_ilu_apply(self._h, rd.data_ptr(), rd.numel(), zd.data_ptr(), zd.numel(), None))
+        z[...] = zd.cpu().numpy()
+
+    def close(self) -> None:
+        if self._h:
+            N.lib.sait_exact_ilu_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class JacobiSweepsPreconditioner(Preconditioner):
+    """preconditioner.hpp:72-83 / preconditioner.cpp:51-60: ``sweeps`` Jacobi
+    sweeps on the L-system, then on the U-system (the paper's section 4.3
+    comparison), on the device."""
+
+    def __init__(self, factors, sweeps: int, stream=None):
+        if sweeps < 1:
+            raise N.SaitInvalidArgument("JacobiSweepsPreconditioner: sweeps must be >= 1")
+        self._l = factors.lower if isinstance(factors.lower, DeviceCsr) else DeviceCsr.upload(factors.lower, stream)
+        self._u = factors.upper if isinstance(factors.upper, DeviceCsr) else DeviceCsr.upload(factors.upper, stream)
+        self._sweeps = int(sweeps)
+
+    def name(self) -> str:
+        return "jacobi"
+
+    def nnz(self) -> int:
+        return self._l.nnz() + self._u.nnz()
+
+    def sweeps(self) -> int:
+        return self._sweeps
+
+    def apply(self, r, z, stream=None) -> None:
+        from .csr import unit_lower_triangular, upper_triangular
+        from .sait import jacobi_sweeps_apply
+
+        y = jacobi_sweeps_apply(self._l, unit_lower_triangular, r, self._sweeps, stream)
+        out = jacobi_sweeps_apply(self._u, upper_triangular, y, self._sweeps, stream)
+        if _is_cuda_tensor(r):
+            z.copy_(out)
+        else:
+            z[...] = out
+
+
 def apply_precond(p: Preconditioner, r):
     """preconditioner.hpp:101"""
     z = np.empty(len(r))

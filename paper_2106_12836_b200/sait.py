@@ -197,3 +197,36 @@ def spmv(a, x, y=None, stream=None):
         y[:] = out
         return y
     return out
+
+
+def _vector_call(fn, da, x, out_len, stream, *args):
+    """Run fn(da.handle, *args(x_ptr, y_ptr), stream) on CUDA tensors, or on
+    host numpy via device copies (synchronous)."""
+    import torch
+
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        y = torch.empty(out_len, dtype=torch.float64, device=x.device)
+        s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+        N.check(fn(x, y, s))
+        return y
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    yd = torch.empty(out_len, dtype=torch.float64, device="cuda")
+    N.check(fn(xd, yd, None))
+    return yd.cpu().numpy()
+
+
+def trisolve(t, kind: TriangularKind, b, stream=None):
+    """kernels.hpp:36 / kernels.cpp:196-234: x = T^-1 b by substitution on the
+    device (synchronization-free row scheduling), bitwise the reference's x."""
+    dt, _ = _dev(t, stream)
+    lower = int(_kind_lower(kind))
+    return _vector_call(lambda x, y, s: N.lib.sait_trisolve(dt.handle, lower, x.data_ptr(), x.numel(), y.data_ptr(), s),
+                        dt, b, dt.nrows, stream)
+
+
+def jacobi_sweeps_apply(t, kind: TriangularKind, b, sweeps: int, stream=None):
+    """sait.hpp:73 / sait.cpp:138-159: ``sweeps`` Jacobi sweeps on T x = b from 0."""
+    dt, _ = _dev(t, stream)
+    lower = int(_kind_lower(kind))
+    return _vector_call(lambda x, y, s: N.lib.sait_jacobi_sweeps_apply(dt.handle, lower, x.data_ptr(), int(sweeps), y.data_ptr(), s),
+                        dt, b, dt.nrows, stream)

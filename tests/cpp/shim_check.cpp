@@ -97,6 +97,20 @@ int main(int argc, char** argv) {
   const JacobiSplit sp = jacobi_split(f.upper, upper_triangular);
   put("poly", sait_polynomial(sp, 3, {}));
   put("transpose", transpose(ML));
+  {
+    ExactIluPreconditioner E(f);
+    put("exact_z", apply_precond(E, r));
+    put("exact_nnz", std::vector<int64_t>{E.nnz()});
+    JacobiSweepsPreconditioner J(f, 3);
+    put("jacobi3_z", apply_precond(J, r));
+  }
+  try {
+    IluFactors g = f;
+    g.upper.values[g.upper.row_ptr[9]] = 0.0;  // diagonal of row 9 (first entry of an upper row)
+    trisolve(g.upper, upper_triangular, r);
+  } catch (const std::runtime_error& e) {
+    put_msg("err_trisolve", e.what());
+  }
   // exceptions keep the reference's types and messages
   try {
     sait_thr(f.lower, lower_triangular, {1.5, 2});

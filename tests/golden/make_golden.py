@@ -6,8 +6,8 @@ has built oracle/_ref/libsaitref.so from the unmodified reference sources):
     make -C oracle && python tests/golden/make_golden.py
 
 Every matrix below is produced by the reference's own saitprec:: functions
-(sait_thr, sait_pat, sait_pat_capture_pattern, ilu_k, SaitPairPreconditioner::
-apply / apply_block) through oracle/ref_wrapper.cpp.  Inputs come from the
+(sait_thr, sait_pat, sait_pat_capture_pattern, ilu_k, trisolve,
+jacobi_sweeps_apply, SaitPairPreconditioner::apply / apply_block) through oracle/ref_wrapper.cpp.  Inputs come from the
 oracle's seeded generators (oracle/sait_oracle.c), which the reference lacks
 (SPEC.md:353-408 is spec-only).  The fixtures travel with the repo; the GPU
 box never needs /root/reference.
@@ -58,6 +58,7 @@ def main():
             put(store, f"{name}/cap_{tau}_{k}_{f}", R.sait_thr_cap(t, lower, tau, k, f))
         b = O.uniform_pm1(77, t.nrows)
         store[f"{name}/b"] = b
+        store[f"{name}/x_tri"] = R.trisolve(t, lower, b)  # kernels.cpp:196-234
     # 2. BASELINE config 1: 64x64 Poisson, ILU(0), SAIT tau=1e-2 k=4, r ~ U[-1,1] seed 1
     A = O.laplacian_2d(64)
     L, U = R.ilu_k(A, 0)
@@ -71,6 +72,10 @@ def main():
     put(store, "c1/MU", MU)
     store["c1/r"] = r
     store["c1/z"] = R.pair_apply(ML, MU, r)
+    # ExactIluPreconditioner (preconditioner.cpp:28-32) and
+    # JacobiSweepsPreconditioner with 3 sweeps (preconditioner.cpp:58-63)
+    store["c1/z_exact"] = R.trisolve(U, False, R.trisolve(L, True, r))
+    store["c1/z_jacobi3"] = R.jacobi_sweeps_apply(U, False, R.jacobi_sweeps_apply(L, True, r, 3), 3)
     blk = np.stack([O.uniform_pm1(500 + c, A.nrows) for c in range(8)], axis=1)
     store["c1/R8"] = blk
     store["c1/Z8"] = R.pair_apply_block(ML, MU, blk)

@@ -1,0 +1,106 @@
+"""Edge cases the reference handles: empty matrices, 1x1, a single dense row,
+identity / diagonal inputs, all-dropped off-diagonals, exact zeros kept by
+spgemm (kernels.hpp:18-20), and vectors of length zero."""
+import numpy as np
+import pytest
+
+from helpers import bitwise_equal, bitwise_equal_csr, to_oracle, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2106_12836_b200 as S
+
+    return S
+
+
+def test_empty_matrix_everything(S, port):
+    e = S.CsrMatrix(0, 0, [0], [], [])
+    for lower in (True, False):
+        kind = S.lower_triangular if lower else S.upper_triangular
+        m = S.sait_thr(e, kind, S.SaitThrParams(0.1, 3))
+        assert m.nrows == 0 and m.nnz() == 0
+        assert S.sait_pat(e, kind, S.SaitPatParams(2, 2)).nnz() == 0
+    pair = S.SaitPairPreconditioner(e, e)
+    z = np.empty(0)
+    pair.apply(np.empty(0), z)
+    assert S.spgemm(e, e).nnz() == 0
+    assert S.transpose(e).nnz() == 0
+
+
+def test_one_by_one(S, port):
+    t = S.CsrMatrix(1, 1, [0, 1], [0], [4.0])
+    m = S.sait_thr(t, S.lower_triangular, S.SaitThrParams(0.5, 5))
+    assert list(m.values) == [0.25]
+    pair = S.SaitPairPreconditioner(m, m)
+    z = np.empty(1)
+    pair.apply(np.array([8.0]), z)
+    assert z[0] == 0.5
+    with pytest.raises(S.SaitRuntimeError, match="zero diagonal at row 0"):
+        S.sait_thr(S.CsrMatrix(1, 1, [0, 1], [0], [0.0]), S.lower_triangular, S.SaitThrParams(0.5, 1))
+
+
+def test_dense_last_row_and_exact_zeros(S, port):
+    """A lower T whose last row is dense (a long row for every kernel), with
+    values chosen so some products cancel to exactly 0.0 (kept, not dropped,
+    when tau = 0)."""
+    n = 3000
+    rows, cols, vals = [], [], []
+    rng = np.random.default_rng(1)
+    for i in range(n):
+        rows.append(i); cols.append(i); vals.append(2.0)
+        if i == n - 1:
+            for j in range(i):
+                rows.append(i); cols.append(j); vals.append(float(rng.choice([-1.0, 1.0])))
+        elif i > 0:
+            rows.append(i); cols.append(i - 1); vals.append(1.0)
+    import scipy.sparse as sp
+
+    T = S.CsrMatrix.from_scipy(sp.csr_matrix((vals, (rows, cols)), shape=(n, n)))
+    for tau, k in ((0.0, 4), (0.3, 6)):
+        got = S.sait_thr(T, S.lower_triangular, S.SaitThrParams(tau, k))
+        assert bitwise_equal_csr(got, port.sait_thr(to_oracle(T), True, tau, k))
+    M = S.sait_thr(T, S.lower_triangular, S.SaitThrParams(0.0, 4))
+    pair = S.SaitPairPreconditioner(M, S.transpose(M))
+    r = rng.standard_normal(n)
+    z = np.empty(n)
+    pair.apply(r, z)
+    assert bitwise_equal(z, port.pair_apply(to_oracle(M), to_oracle(S.transpose(M)), r))
+
+
+def test_diagonal_and_identity_inputs(S):
+    d = S.CsrMatrix(5, 5, np.arange(6), np.arange(5), [1.0, 2.0, 4.0, 8.0, -16.0])
+    m = S.sait_thr(d, S.upper_triangular, S.SaitThrParams(0.9, 7))
+    assert list(m.values) == [1.0, 0.5, 0.25, 0.125, -0.0625]
+    assert list(S.sait_pat_capture_pattern(d, S.lower_triangular, 3).col_idx) == list(range(5))
+
+
+def test_everything_dropped_but_diagonal(S, port):
+    from oracle import oracle as O
+
+    T = O.synthetic_lower(500, 4, 0.1, seed=3)
+    got = S.sait_thr(to_product(T), S.lower_triangular, S.SaitThrParams(0.999, 3))
+    exp = port.sait_thr(T, True, 0.999, 3)
+    assert bitwise_equal_csr(got, exp) and got.nnz() == 500
+
+
+def test_nonfinite_values_in_build(S, port):
+    """NaN entries are dropped by a positive threshold (|NaN| >= tau is false)
+    unless diagonal, kept when tau == 0 — exactly as drop_by_threshold."""
+    import scipy.sparse as sp
+
+    n = 50
+    a = sp.tril(sp.random(n, n, density=0.2, random_state=2), k=-1).tolil()
+    a[10, 3] = np.nan
+    a = (a + 3 * sp.eye(n)).tocsr()
+    a.sort_indices()
+    T = S.CsrMatrix.from_scipy(a)
+    for tau in (0.0, 0.05):
+        got = S.sait_thr(T, S.lower_triangular, S.SaitThrParams(tau, 3))
+        exp = port.sait_thr(to_oracle(T), True, tau, 3)
+        assert np.array_equal(got.row_ptr, exp.row_ptr) and np.array_equal(got.col_idx, exp.col_idx)
+        assert np.array_equal(np.isnan(got.values), np.isnan(exp.values))
+        fin = ~np.isnan(exp.values)
+        assert bitwise_equal(got.values[fin], exp.values[fin])

@@ -60,6 +60,9 @@ def test_shim_matches_reference_golden(dump, golden):
     assert csr_eq(dump, "MU", golden, "c1/MU")
     assert bitwise_equal(dump["z"], golden["c1/z"])
     assert dump["pair_nnz"][0] == 2 * 51215
+    assert bitwise_equal(dump["exact_z"], golden["c1/z_exact"])
+    assert dump["exact_nnz"][0] == golden_csr(golden, "c1/L").nnz + golden_csr(golden, "c1/U").nnz
+    assert bitwise_equal(dump["jacobi3_z"], golden["c1/z_jacobi3"])
 
 
 def test_shim_builders_and_kernels_match_oracle(dump, golden, port):
@@ -97,4 +100,5 @@ def test_shim_exceptions(dump):
     assert msg("err_thr") == "sait_thr: threshold must be in [0, 1), got 1.500000"
     assert msg("err_diag") == "jacobi_split: singular matrix, zero diagonal at row 5"
     assert msg("err_apply") == "spmv: vector length 5 does not match ncols 4096"
+    assert msg("err_trisolve") == "trisolve: singular matrix, zero diagonal at row 9"
     assert msg("err_droprule").startswith("sait_polynomial: a custom DropRule cannot run on the device")

@@ -140,3 +140,43 @@ def test_ref_kernels_match_port(port, ref):
     assert bitwise_equal_csr(port.scale_columns(sq, d), ref.scale_columns(sq, d))
     x = np.linspace(-1, 1, 60)
     assert bitwise_equal(port.spmv(a, x), ref.spmv(a, x))
+
+
+@pytest.mark.parametrize("name,lower", NAMES)
+def test_port_trisolve_golden(port, golden, name, lower):
+    """trisolve (kernels.cpp:196-234) pinned on the reference's own output."""
+    t = golden_csr(golden, f"{name}/T")
+    assert bitwise_equal(port.trisolve(t, lower, golden[f"{name}/b"]), golden[f"{name}/x_tri"])
+
+
+def test_port_exact_and_jacobi_golden(port, golden):
+    """ExactIluPreconditioner / JacobiSweepsPreconditioner(3) on config 1."""
+    L, U, r = golden_csr(golden, "c1/L"), golden_csr(golden, "c1/U"), golden["c1/r"]
+    assert bitwise_equal(port.trisolve(U, False, port.trisolve(L, True, r)), golden["c1/z_exact"])
+    z = port.jacobi_sweeps_apply(U, False, port.jacobi_sweeps_apply(L, True, r, 3), 3)
+    assert bitwise_equal(z, golden["c1/z_jacobi3"])
+
+
+def test_port_trisolve_nontriangular_and_errors(port, ref):
+    """Entries on the wrong side of the diagonal read x as zero; the first
+    zero/missing diagonal in solve order raises (reference wording)."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(5)
+    n = 60
+    dense = rng.uniform(-1, 1, (n, n)) * (rng.random((n, n)) < 0.15)
+    np.fill_diagonal(dense, rng.uniform(1, 2, n))
+    import scipy.sparse as sp
+
+    m = O.from_scipy(sp.csr_matrix(dense))
+    b = rng.uniform(-1, 1, n)
+    for lower in (True, False):
+        assert bitwise_equal(port.trisolve(m, lower, b), ref.trisolve(m, lower, b))
+    dense[7, 7] = 0.0
+    dense[40, 40] = 0.0
+    m = O.from_scipy(sp.csr_matrix(dense))
+    for lower, row in ((True, 7), (False, 40)):
+        with pytest.raises(Exception, match=f"zero diagonal at row {row}"):
+            port.trisolve(m, lower, b)
+        with pytest.raises(Exception, match=f"zero diagonal at row {row}"):
+            ref.trisolve(m, lower, b)

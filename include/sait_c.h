@@ -168,6 +168,14 @@ int sait_pat_capture_pattern(sait_dcsr_t t, int lower, int pattern_steps, sait_s
 int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double *d_b, int sweeps, double *d_x,
                              sait_stream_t stream);
 
+/* ilu.hpp:27 / ilu.cpp:98-173 with level 0, on the device: the factors of
+ * ilu_k(a, 0) bitwise (L with its explicit unit diagonal, U from the
+ * diagonal on), computed in dependency-level order.  Errors as the
+ * reference: "ilu_k: matrix is not square", "ilu_k: structurally zero
+ * diagonal at row i" (SAIT_ERR_INVALID_ARGUMENT), "ilu_k: pivot breakdown at
+ * row i (|pivot| = %f)" (SAIT_ERR_RUNTIME) for the first such row. */
+int sait_ilu0(sait_dcsr_t a, sait_stream_t stream, sait_dcsr_t *lower, sait_dcsr_t *upper);
+
 /* kernels.hpp:36 / kernels.cpp:196-234: x = T^-1 b by substitution (Lower:
  * rows ascending, Upper: descending; the stored diagonal is used, entries on
  * the wrong side of it read x as zero), device vectors, bitwise the

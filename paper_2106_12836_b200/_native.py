@@ -108,6 +108,7 @@ PROTOTYPES = {
     "sait_polynomial": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_pat_capture_pattern": (C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
     "sait_jacobi_sweeps_apply": (C.c_int, [VP, C.c_int, VP, C.c_int, VP, VP]),
+    "sait_ilu0": (C.c_int, [VP, VP, C.POINTER(VP), C.POINTER(VP)]),
     "sait_trisolve": (C.c_int, [VP, C.c_int, VP, C.c_int64, VP, VP]),
     "sait_exact_ilu_create": (C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
     "sait_exact_ilu_info": (C.c_int, [VP, P64, P64]),

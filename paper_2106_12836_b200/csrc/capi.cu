@@ -1014,6 +1014,25 @@ void sait_operator_destroy(sait_op_t op) {
   delete op;
 }
 
+// ------------------------------------------------------------ device ILU(0)
+
+int sait_ilu0(sait_dcsr_t a, sait_stream_t stream, sait_dcsr_t* lower, sait_dcsr_t* upper) {
+  return guarded([&] {
+    need(a, "ilu_k");
+    need(lower, "ilu_k(lower)");
+    need(upper, "ilu_k(upper)");
+    if (!a->m.v) sait::throw_invalid("ilu_k: matrix has no values");
+    DeviceGuard g(a->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr L, U;
+    sait::ilu0(a->m, L, U, s);
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    *lower = wrap(L);
+    *upper = wrap(U);
+  });
+}
+
 // --------------------------------------------------------- exact triangular
 
 int sait_trisolve(sait_dcsr_t t, int lower, const double* d_b, int64_t blen, double* d_x,

@@ -232,6 +232,9 @@ void trisolve(const DevCsr& t, bool lower, const TrisolvePlan& plan, const doubl
               TrisolveState& st, cudaStream_t s);
 void free_trisolve_state(TrisolveState& st, cudaStream_t s);
 
+// ilu.cu: ILU(0) on A's pattern, bitwise ilu_k(a, 0) (ilu.cpp:98-173)
+void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s);
+
 // blas.cu (elementwise helpers)
 void hadamard(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a * b
 void add_into(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a + b

@@ -30,7 +30,11 @@ def timed(fn, reps=20):
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
     A = S.laplacian_3d(n)
+    t0 = time.perf_counter()
     f = S.ilu_k(A, 0)
+    s_host_ilu = time.perf_counter() - t0
+    Ad = S.DeviceCsr.upload(A)
+    ms_dev_ilu = timed(lambda: S.ilu0_device(Ad), 3)
     N = A.nrows
     r = torch.from_numpy(S.uniform_pm1(1000, N)).cuda()
     z = torch.empty_like(r)
@@ -50,6 +54,7 @@ def main():
     E.apply(r, z)
     torch.cuda.synchronize()
     print(f"n={n}^3 rows={N} nnz(L+U)={E.nnz()} nnz(ML+MU)={P.nnz()}")
+    print(f"ilu(0) host       {s_host_ilu * 1e3:8.1f} ms   device {ms_dev_ilu:8.2f} ms")
     print(f"exact ilu apply   {ms_exact:8.3f} ms  ({8 * 2 * E.nnz() / ms_exact / 1e6:.1f} GB/s of CSR values+idx est.)")
     print(f"trisolve L only   {ms_l:8.3f} ms")
     print(f"jacobi sweeps(3)  {ms_jac:8.3f} ms")

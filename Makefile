@@ -17,7 +17,7 @@ CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Iinclude -I/usr/local/
 
 CU_SRCS := csr_ops split spgemm spmv sell blas solvers trisolve ilu aux_ops capi
 CU_OBJS := $(addprefix $(BUILD)/,$(addsuffix .o,$(CU_SRCS)))
-HOST_OBJS := $(BUILD)/host_inputs.o
+HOST_OBJS := $(BUILD)/host_inputs.o $(BUILD)/host_mm.o
 HEADERS := include/sait_c.h $(wildcard $(CSRC)/*.cuh)
 
 SHIM_SRCS := $(wildcard $(CSRC)/shim/*.cpp)
@@ -29,7 +29,7 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(HEADERS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
-$(BUILD)/host_inputs.o: $(CSRC)/host_inputs.cpp include/sait_c.h
+$(BUILD)/host_%.o: $(CSRC)/host_%.cpp include/sait_c.h
 	@mkdir -p $(BUILD)
 	g++ $(CXXFLAGS) -O3 -c -o $@ $<
 

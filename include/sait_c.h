@@ -263,6 +263,14 @@ int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double *d_b, double *d_x, int
 int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double *d_b, double *d_x, int64_t n, double tol,
              int maxit, double *h_hist, sait_solve_stats *stats, sait_stream_t stream);
 
+/* The same loops preconditioned by the exact ILU solves (the comparator of
+ * the paper's iteration tables). */
+int sait_gmres_exact(sait_dcsr_t A, sait_exact_t M, const double *d_b, double *d_x, int64_t n,
+                     int restart, double tol, int maxit, double *h_hist, sait_solve_stats *stats,
+                     sait_stream_t stream);
+int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double *d_b, double *d_x, int64_t n, double tol,
+                   int maxit, double *h_hist, sait_solve_stats *stats, sait_stream_t stream);
+
 /* Block LOBPCG for the nev (<= 16) smallest eigenpairs of
  * SPD A, preconditioned by the pair applied to the whole residual block
  * (apply_block, preconditioner.cpp:47-49).  X0 ~ U[-1,1] from `seed`.
@@ -284,6 +292,17 @@ int sait_problem_convdiff_2d(int64_t nx, double bx, double by, sait_host_csr *ou
 int sait_problem_synthetic_lower(int64_t n, int64_t draws, double p, uint64_t seed,
                                  sait_host_csr *out);
 void sait_fill_uniform_pm1(uint64_t seed, int64_t n, double *out);
+/* SPEC.md:373-381 mm_read (spec only in the reference): Matrix Market
+ * coordinate real/integer, general or symmetric (expanded to full storage),
+ * 1-based, '%' comments; entries assembled like from_triplets (csr.cpp:10-58,
+ * duplicates summed in file order).  Errors "mm_read: line N: ..."
+ * (SAIT_ERR_INVALID_ARGUMENT).  mm_write emits the general form with %.17g
+ * values: mm_read(mm_write(M)) == M bit for bit. */
+int sait_mm_read(const char *path, sait_host_csr *out);
+int sait_mm_write(const char *path, const sait_host_csr *m);
+/* SPEC.md:382-389 make_rhs: mode 0 ones-solution b = A 1 (row sums in stored
+ * order), mode 1 seeded-random unit vector uniform_pm1(seed) / ||.||_2. */
+int sait_make_rhs(const sait_host_csr *a, int mode, uint64_t seed, double *out);
 
 /* ------------------------------------------------------------ utility --- */
 int sait_device_synchronize(void);

@@ -313,8 +313,9 @@ class _SolveStats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_relres", C.c_double), ("true_relres", C.c_double)]
 
 
-def _solver(name, a, ml, mu, b, *args):
+def _solver(name, a, ml, mu, b, *args, exact=False):
     L = _port().lib
+    L.orc_solver_precond_exact(C.c_int(int(exact)))
     b = np.ascontiguousarray(b, dtype=np.float64)
     x = np.empty(a.nrows)
     maxit = args[-1].value
@@ -323,21 +324,25 @@ def _solver(name, a, ml, mu, b, *args):
     pm = C.byref(_in(ml)) if ml is not None else None
     pu = C.byref(_in(mu)) if mu is not None else None
     fn = getattr(L, name)
-    rc = fn(C.byref(_in(a)), pm, pu, _dptr(b), *args, _dptr(x), _dptr(hist), C.byref(st))
+    try:
+        rc = fn(C.byref(_in(a)), pm, pu, _dptr(b), *args, _dptr(x), _dptr(hist), C.byref(st))
+    finally:
+        L.orc_solver_precond_exact(C.c_int(0))
     _port()._check(rc)
     its = st.iterations
     return x, {"iterations": its, "converged": bool(st.converged), "relres": st.final_relres,
                "true_relres": st.true_relres, "history": hist[: its + 1].copy()}
 
 
-def gmres(a, ml, mu, b, restart=30, tol=1e-8, maxit=10000):
-    """Restated right-preconditioned GMRES(m) (oracle/solvers.c)."""
-    return _solver("orc_gmres", a, ml, mu, b, C.c_int(restart), C.c_double(tol), C.c_int(maxit))
+def gmres(a, ml, mu, b, restart=30, tol=1e-8, maxit=10000, exact=False):
+    """Restated right-preconditioned GMRES(m) (oracle/solvers.c); exact=True
+    preconditions with the ILU factors (ml = L, mu = U) by two trisolves."""
+    return _solver("orc_gmres", a, ml, mu, b, C.c_int(restart), C.c_double(tol), C.c_int(maxit), exact=exact)
 
 
-def pcg(a, ml, mu, b, tol=1e-10, maxit=10000):
-    """Restated PCG (oracle/solvers.c)."""
-    return _solver("orc_pcg", a, ml, mu, b, C.c_double(tol), C.c_int(maxit))
+def pcg(a, ml, mu, b, tol=1e-10, maxit=10000, exact=False):
+    """Restated PCG (oracle/solvers.c); exact as in gmres."""
+    return _solver("orc_pcg", a, ml, mu, b, C.c_double(tol), C.c_int(maxit), exact=exact)
 
 
 def dot(a, b):

@@ -119,6 +119,8 @@ typedef struct {
   double true_relres;     /* ||b - A x|| / ||b|| recomputed at exit */
 } orc_solve_stats;
 /* precond: 0 none, 1 SAIT pair (ml, mu) */
+/* solvers.c: 1 = GMRES/PCG apply (ml, mu) as exact ILU factors (two trisolves) */
+void orc_solver_precond_exact(int on);
 int orc_gmres(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double *b, int restart,
               double tol, int maxit, double *x, double *hist, orc_solve_stats *st);
 int orc_pcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double *b, double tol,

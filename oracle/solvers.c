@@ -81,10 +81,25 @@ static int fail_solver(const char *msg) {
   return orc_set_error(msg);
 }
 
-/* z = M r for the SAIT pair, or a copy when no preconditioner */
+/* How (ml, mu) precondition GMRES / PCG: 0 = the SAIT pair z = M_U (M_L r);
+ * 1 = the exact ILU solves z = U^-1 (L^-1 r) (ExactIluPreconditioner,
+ * preconditioner.cpp:28-32) with ml = L, mu = U. */
+static int g_precond_exact = 0;
+void orc_solver_precond_exact(int on) { g_precond_exact = on; }
+
+/* z = M r, or a copy when no preconditioner */
 static void precond(const orc_csr *ml, const orc_csr *mu, const double *r, double *z, int64_t n) {
-  if (ml && mu) orc_pair_apply(ml, mu, r, z);
-  else memcpy(z, r, (size_t)n * sizeof(double));
+  if (ml && mu && g_precond_exact) {
+    double *y = (double *)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    memset(z, 0, (size_t)n * sizeof(double));
+    orc_trisolve(ml, 1, r, y);
+    orc_trisolve(mu, 0, y, z);
+    free(y);
+  } else if (ml && mu) {
+    orc_pair_apply(ml, mu, r, z);
+  } else {
+    memcpy(z, r, (size_t)n * sizeof(double));
+  }
 }
 
 /*

@@ -33,7 +33,19 @@ from .preconditioner import (
     SaitPairPreconditioner,
     apply_precond,
 )
-from .problems import IluFactors, convdiff_2d, ilu0_device, ilu_k, laplacian_2d, laplacian_3d, synthetic_lower, uniform_pm1
+from .problems import (
+    IluFactors,
+    convdiff_2d,
+    ilu0_device,
+    ilu_k,
+    laplacian_2d,
+    laplacian_3d,
+    make_rhs,
+    mm_read,
+    mm_write,
+    synthetic_lower,
+    uniform_pm1,
+)
 from .solvers import EigResult, SolveStats, gmres, lobpcg, pcg
 from .sait import (
     BuildStats,

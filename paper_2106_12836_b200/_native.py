@@ -108,6 +108,9 @@ PROTOTYPES = {
     "sait_polynomial": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_pat_capture_pattern": (C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
     "sait_jacobi_sweeps_apply": (C.c_int, [VP, C.c_int, VP, C.c_int, VP, VP]),
+    "sait_mm_read": (C.c_int, [C.c_char_p, C.POINTER(HostCsr)]),
+    "sait_mm_write": (C.c_int, [C.c_char_p, C.POINTER(HostCsr)]),
+    "sait_make_rhs": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.c_uint64, VP]),
     "sait_ilu0": (C.c_int, [VP, VP, C.POINTER(VP), C.POINTER(VP)]),
     "sait_trisolve": (C.c_int, [VP, C.c_int, VP, C.c_int64, VP, VP]),
     "sait_exact_ilu_create": (C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
@@ -125,6 +128,8 @@ PROTOTYPES = {
     "sait_pair_destroy": (None, [VP]),
     "sait_gmres": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_pcg": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
+    "sait_gmres_exact": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
+    "sait_pcg_exact": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_lobpcg": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int), VP]),
     "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),
     "sait_problem_laplacian_2d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),

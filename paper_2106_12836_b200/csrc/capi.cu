@@ -43,6 +43,9 @@ struct sait_exact_s {
 namespace {
 class Recursion;
 }  // namespace
+namespace sait {
+void exact_apply_internal(sait_exact_t p, const double* r, double* z, cudaStream_t s);
+}
 struct sait_build_session_s {
   int dev = 0;
   cudaStream_t s = nullptr;
@@ -1102,15 +1105,7 @@ int sait_exact_ilu_apply(sait_exact_t p, const double* d_r, int64_t rlen, double
     if (zlen != U.nrows) sait::throw_invalid("ExactIluPreconditioner: output length mismatch");
     DeviceGuard g(p->dev);
     init_device_pool();
-    cudaStream_t s = sait::as_stream(stream);
-    sait_exact_s::Work* w;
-    {
-      std::lock_guard<std::mutex> lk(p->mu);
-      w = &p->ws[s];
-      if (!w->y && L.nrows) w->y = sait::dalloc<double>(L.nrows, s);
-    }
-    sait::trisolve(L, true, p->pl, d_r, w->y, w->sl, s);    // y = L^-1 r (unit_lower_triangular)
-    sait::trisolve(U, false, p->pu, w->y, d_z, w->su, s);   // z = U^-1 y (upper_triangular)
+    sait::exact_apply_internal(p, d_r, d_z, sait::as_stream(stream));
   });
 }
 
@@ -1371,6 +1366,19 @@ void pair_apply_internal(sait_pair_t p, const double* r, double* z, cudaStream_t
 }
 int64_t pair_dim(sait_pair_t p) { return p->ml->m.ncols; }
 int pair_device(sait_pair_t p) { return p->dev; }
+
+// z = U^-1 (L^-1 r) on device vectors (ExactIluPreconditioner::apply)
+void exact_apply_internal(sait_exact_t p, const double* r, double* z, cudaStream_t s) {
+  sait_exact_s::Work* w;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    w = &p->ws[s];
+    if (!w->y && p->l->m.nrows) w->y = sait::dalloc<double>(p->l->m.nrows, s);
+  }
+  sait::trisolve(p->l->m, true, p->pl, r, w->y, w->sl, s);   // y = L^-1 r (unit_lower_triangular)
+  sait::trisolve(p->u->m, false, p->pu, w->y, z, w->su, s);  // z = U^-1 y (upper_triangular)
+}
+int64_t exact_dim(sait_exact_t p) { return p->l->m.nrows; }
 }  // namespace sait
 
 extern "C" {

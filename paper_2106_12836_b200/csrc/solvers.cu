@@ -20,6 +20,8 @@
 namespace sait {
 void pair_apply_internal(sait_pair_t p, const double* r, double* z, cudaStream_t s);
 int64_t pair_dim(sait_pair_t p);
+void exact_apply_internal(sait_exact_t e, const double* r, double* z, cudaStream_t s);
+int64_t exact_dim(sait_exact_t e);
 
 int64_t dot_blocks(int64_t n);
 void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, double* out, double* scratch,
@@ -62,11 +64,16 @@ struct Operator {
   void release(cudaStream_t s) { free_sell(sell, s); }
 };
 
+// z = M r: the SAIT pair, the exact ILU solves (the comparator), or identity
 struct Precond {
-  sait_pair_t p;
-  int64_t n;
+  sait_pair_t p = nullptr;
+  sait_exact_t e = nullptr;
+  int64_t n = 0;
+  bool present() const { return p || e; }
+  int64_t dim() const { return p ? pair_dim(p) : e ? exact_dim(e) : n; }
   void apply(const double* r, double* z, cudaStream_t s) const {
     if (p) pair_apply_internal(p, r, z, s);
+    else if (e) exact_apply_internal(e, r, z, s);
     else SAIT_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
 };
@@ -240,13 +247,13 @@ static int solver_guard(F&& f) {
 
 extern "C" {
 
-int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int64_t n, int restart, double tol,
-               int maxit, double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
+static int gmres_impl(sait_dcsr_t A, sait::Precond M, const double* d_b, double* d_x, int64_t n, int restart,
+                      double tol, int maxit, double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
   return solver_guard([&] {
     if (!A || !d_b || !d_x) sait::throw_invalid("gmres: null argument");
     const sait::DevCsr& a = A->m;
     if (a.nrows != n || a.ncols != n) sait::throw_invalid("gmres: operator shape does not match n");
-    if (M && sait::pair_dim(M) != n) sait::throw_invalid("gmres: preconditioner dimension mismatch");
+    if (M.present() && M.dim() != n) sait::throw_invalid("gmres: preconditioner dimension mismatch");
     if (restart < 1) sait::throw_invalid("gmres: restart must be >= 1");
     int dev = 0;
     cudaGetDevice(&dev);
@@ -255,7 +262,8 @@ int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int
     const auto t0 = std::chrono::steady_clock::now();
     const int m = restart;
     sait::Operator op(a, s);
-    sait::Precond pc{M, n};
+    sait::Precond pc = M;
+    pc.n = n;
     double* V = sait::dalloc<double>((m + 1) * n, s);
     double* w = sait::dalloc<double>(n, s);
     double* z = sait::dalloc<double>(n, s);
@@ -364,20 +372,21 @@ int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int
   });
 }
 
-int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int64_t n, double tol, int maxit,
-             double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
+static int pcg_impl(sait_dcsr_t A, sait::Precond M, const double* d_b, double* d_x, int64_t n, double tol,
+                    int maxit, double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
   return solver_guard([&] {
     if (!A || !d_b || !d_x) sait::throw_invalid("pcg: null argument");
     const sait::DevCsr& a = A->m;
     if (a.nrows != n || a.ncols != n) sait::throw_invalid("pcg: operator shape does not match n");
-    if (M && sait::pair_dim(M) != n) sait::throw_invalid("pcg: preconditioner dimension mismatch");
+    if (M.present() && M.dim() != n) sait::throw_invalid("pcg: preconditioner dimension mismatch");
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != A->dev) SAIT_CUDA(cudaSetDevice(A->dev));
     cudaStream_t s = sait::as_stream(stream);
     const auto t0 = std::chrono::steady_clock::now();
     sait::Operator op(a, s);
-    sait::Precond pc{M, n};
+    sait::Precond pc = M;
+    pc.n = n;
     double* r = sait::dalloc<double>(n, s);
     double* z = sait::dalloc<double>(n, s);
     double* p = sait::dalloc<double>(n, s);
@@ -443,6 +452,34 @@ int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int64
     if (dev != A->dev) cudaSetDevice(dev);
     if (breakdown) sait::throw_runtime("pcg: breakdown, p'Ap <= 0 at iteration " + std::to_string(its));
   });
+}
+
+int sait_gmres(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int64_t n, int restart, double tol,
+               int maxit, double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
+  sait::Precond pc;
+  pc.p = M;
+  return gmres_impl(A, pc, d_b, d_x, n, restart, tol, maxit, h_hist, stats, stream);
+}
+
+int sait_gmres_exact(sait_dcsr_t A, sait_exact_t M, const double* d_b, double* d_x, int64_t n, int restart,
+                     double tol, int maxit, double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
+  sait::Precond pc;
+  pc.e = M;
+  return gmres_impl(A, pc, d_b, d_x, n, restart, tol, maxit, h_hist, stats, stream);
+}
+
+int sait_pcg(sait_dcsr_t A, sait_pair_t M, const double* d_b, double* d_x, int64_t n, double tol, int maxit,
+             double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
+  sait::Precond pc;
+  pc.p = M;
+  return pcg_impl(A, pc, d_b, d_x, n, tol, maxit, h_hist, stats, stream);
+}
+
+int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double* d_b, double* d_x, int64_t n, double tol, int maxit,
+                   double* h_hist, sait_solve_stats* stats, sait_stream_t stream) {
+  sait::Precond pc;
+  pc.e = M;
+  return pcg_impl(A, pc, d_b, d_x, n, tol, maxit, h_hist, stats, stream);
 }
 
 int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, double* h_evals,

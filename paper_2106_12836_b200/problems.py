@@ -39,6 +39,29 @@ def ilu0_device(a, stream=None) -> IluFactors:
     return IluFactors(DeviceCsr(lo.value), DeviceCsr(up.value), 0)
 
 
+def mm_read(path) -> CsrMatrix:
+    """SPEC.md:373-381 mm_read: Matrix Market coordinate real/integer,
+    general or symmetric (expanded), duplicates summed in file order."""
+    out = N.HostCsr()
+    N.check(N.lib.sait_mm_read(str(path).encode(), C.byref(out)))
+    return _from_c(out)
+
+
+def mm_write(path, m: CsrMatrix) -> None:
+    """General coordinate form with %.17g values (mm_read round-trips it bit for bit)."""
+    N.check(N.lib.sait_mm_write(str(path).encode(), C.byref(m._as_c())))
+
+
+def make_rhs(a: CsrMatrix, mode: str = "ones-solution", seed: int = 0) -> np.ndarray:
+    """'ones-solution' b = A 1, or 'seeded-random' unit vector."""
+    modes = {"ones-solution": 0, "seeded-random": 1}
+    if mode not in modes:
+        raise N.SaitInvalidArgument(f"make_rhs: unknown mode {mode!r}")
+    b = np.empty(a.nrows)
+    N.check(N.lib.sait_make_rhs(C.byref(a._as_c()), modes[mode], int(seed), b.ctypes.data_as(N.PD)))
+    return b
+
+
 def _gen(fn, *args) -> CsrMatrix:
     out = N.HostCsr()
     N.check(fn(*args, C.byref(out)))

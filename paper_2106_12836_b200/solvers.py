@@ -2,7 +2,8 @@
 
 ``gmres`` (right-preconditioned GMRES(m), CGS2 Arnoldi) and ``pcg``
  run entirely on the GPU; only control scalars come back
-per iteration.  ``M`` is a SaitPairPreconditioner or None (identity).
+per iteration.  ``M`` is a SaitPairPreconditioner, an ExactIluPreconditioner
+(the comparator: two device triangular solves) or None (identity).
 """
 from __future__ import annotations
 
@@ -43,12 +44,22 @@ def _finish(rc, st, hist, x, on_dev):
     return (x if on_dev else x.cpu().numpy()), stats
 
 
+def _precond(M, pair_fn, exact_fn):
+    from .preconditioner import ExactIluPreconditioner
+
+    if M is None:
+        return None, pair_fn
+    if isinstance(M, ExactIluPreconditioner):
+        return M._h, exact_fn
+    return M.handle, pair_fn
+
+
 def gmres(A, M, b, restart: int = 30, tol: float = 1e-8, maxit: int = 10000, stream=None):
     dA, bd, x, on_dev, s = _prep(A, b, stream)
     hist = np.zeros(maxit + 1)
     st = N.SolveStats()
-    mh = M.handle if M is not None else None
-    rc = N.lib.sait_gmres(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), int(restart), float(tol), int(maxit),
+    mh, fn = _precond(M, N.lib.sait_gmres, N.lib.sait_gmres_exact)
+    rc = fn(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), int(restart), float(tol), int(maxit),
                           hist.ctypes.data_as(N.PD), C.byref(st), s)
     return _finish(rc, st, hist, x, on_dev)
 
@@ -57,8 +68,8 @@ def pcg(A, M, b, tol: float = 1e-10, maxit: int = 10000, stream=None):
     dA, bd, x, on_dev, s = _prep(A, b, stream)
     hist = np.zeros(maxit + 1)
     st = N.SolveStats()
-    mh = M.handle if M is not None else None
-    rc = N.lib.sait_pcg(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), float(tol), int(maxit),
+    mh, fn = _precond(M, N.lib.sait_pcg, N.lib.sait_pcg_exact)
+    rc = fn(dA.handle, mh, bd.data_ptr(), x.data_ptr(), bd.numel(), float(tol), int(maxit),
                         hist.ctypes.data_as(N.PD), C.byref(st), s)
     return _finish(rc, st, hist, x, on_dev)
 

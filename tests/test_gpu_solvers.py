@@ -125,3 +125,31 @@ def test_lobpcg_bitwise_and_analytic(S, port, nev, prec):
     if prec == 0.03:
         r0 = S.lobpcg(to_product(A), None, nev, 1e-6, 400, 5)
         assert r.iterations * 2 <= r0.iterations
+
+
+def test_pcg_gmres_exact_ilu_bitwise(S, port):
+    """The paper's comparator (exact ILU(0) solves as the preconditioner,
+    PAPER.md:880-900): device PCG / GMRES with ExactIluPreconditioner vs the
+    restatement preconditioned by the same two trisolves, bitwise; and the
+    exact preconditioner needs fewer iterations than SAIT(0.05, 10)."""
+    from oracle import oracle as O
+
+    A = O.laplacian_3d(20)
+    L, U = port.ilu_k(A, 0)
+    b = O.uniform_pm1(8, A.nrows)
+    E = S.ExactIluPreconditioner(S.IluFactors(to_product(L), to_product(U)))
+    xo, so = O.pcg(A, L, U, b, 1e-10, 1000, exact=True)
+    x, st = S.pcg(to_product(A), E, b, 1e-10, 1000)
+    assert st.converged and st.iterations == so["iterations"]
+    assert bitwise_equal(st.history, so["history"]) and bitwise_equal(x, xo)
+    ML, MU = port.sait_thr(L, True, 0.05, 10), port.sait_thr(U, False, 0.05, 10)
+    _, ss = S.pcg(to_product(A), S.SaitPairPreconditioner(to_product(ML), to_product(MU)), b, 1e-10, 1000)
+    assert st.iterations <= ss.iterations
+    C = O.convdiff_2d(40)
+    Lc, Uc = port.ilu_k(C, 0)
+    Ec = S.ExactIluPreconditioner(S.IluFactors(to_product(Lc), to_product(Uc)))
+    bc = O.uniform_pm1(9, C.nrows)
+    xo, so = O.gmres(C, Lc, Uc, bc, 30, 1e-8, 500, exact=True)
+    x, st = S.gmres(to_product(C), Ec, bc, 30, 1e-8, 500)
+    assert st.converged and st.iterations == so["iterations"]
+    assert bitwise_equal(st.history, so["history"]) and bitwise_equal(x, xo)

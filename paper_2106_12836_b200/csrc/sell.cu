@@ -60,6 +60,17 @@ struct Idx16 {
   }
 };
 
+// A plain (weak, coherent) load.  The x of a programmatic dependent SpMV is
+// written by the prerequisite grid while this grid is already resident, so
+// it must not go through the non-coherent read-only path (ld.global.nc
+// requires the data to be unchanged for the kernel's lifetime); after
+// griddepcontrol.wait the prerequisite's writes are visible to weak loads.
+__device__ __forceinline__ double ld_weak(const double* p) {
+  double r;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(r) : "l"(p) : "memory");
+  return r;
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
@@ -199,7 +210,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
     if (PDL_WAIT && k0 == 0) pdl_wait();  // x is the previous grid's output
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double xv = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+      const double xv = c[j] >= 0 ? (PDL_WAIT ? ld_weak(x + c[j]) : __ldg(x + c[j])) : 0.0;
       if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
     }
   }

@@ -362,11 +362,39 @@ void plan_host_chunks(sait_pair_t p) {
     return;  // small or non-square pairs: one-shot path
   const int64_t G = sait::kDepGroupRows;
   const int64_t ng = (n + G - 1) / G;
-  // Copy sizes: a short first chunk starts the z stream early, a short last
-  // chunk keeps the drain short, ~4 MB in between (on PCIe5, async copies
-  // much smaller than that lose H2D/D2H concurrency).
-  double mb_first = 2.0, mb_mid = 4.0, mb_last = 1.0;
-  if (const char* e = std::getenv("SAIT_PIPE_MB")) std::sscanf(e, "%lf,%lf,%lf", &mb_first, &mb_mid, &mb_last);
+  // Copy sizes (MB of r / z per chunk): short head chunks start the z stream
+  // early, short tail chunks keep the drain (z still leaving after the last r
+  // chunk landed) short, ~4 MB in between (on PCIe5, async copies much
+  // smaller than that lose H2D/D2H concurrency).  SAIT_PIPE_MB =
+  // "head,...;mid;tail,..." (or the older "first,mid,last").
+  std::vector<double> head{3.0}, tail;
+  double mb_mid = 4.0;
+  if (const char* e = std::getenv("SAIT_PIPE_MB")) {
+    auto parse = [](const std::string& t) {
+      std::vector<double> v;
+      size_t a = 0;
+      while (a < t.size()) {
+        size_t b2 = t.find(',', a);
+        if (b2 == std::string::npos) b2 = t.size();
+        if (b2 > a) v.push_back(std::atof(t.substr(a, b2 - a).c_str()));
+        a = b2 + 1;
+      }
+      return v;
+    };
+    const std::string spec(e);
+    const size_t s1 = spec.find(';');
+    if (s1 == std::string::npos) {
+      const std::vector<double> v = parse(spec);
+      head.assign(1, v.size() > 0 ? v[0] : 2.0);
+      mb_mid = v.size() > 1 ? v[1] : 4.0;
+      tail.assign(1, v.size() > 2 ? v[2] : 1.0);
+    } else {
+      const size_t s2 = spec.find(';', s1 + 1);
+      head = parse(spec.substr(0, s1));
+      mb_mid = std::atof(spec.substr(s1 + 1, s2 == std::string::npos ? std::string::npos : s2 - s1 - 1).c_str());
+      tail = s2 == std::string::npos ? std::vector<double>{} : parse(spec.substr(s2 + 1));
+    }
+  }
   auto rows_of = [&](double mb) {
     return std::max<int64_t>(G, static_cast<int64_t>(mb * (1 << 20) / 8.0) / G * G);
   };
@@ -379,18 +407,25 @@ void plan_host_chunks(sait_pair_t p) {
   sait::dfree(d, nullptr);
   SAIT_CUDA(cudaDeviceSynchronize());
   {
-    const int64_t rf = rows_of(mb_first), rm = rows_of(mb_mid), rl = rows_of(mb_last);
+    std::vector<int64_t> hr, tr;
+    int64_t used = 0;
+    for (double mb : head) hr.push_back(rows_of(mb)), used += hr.back();
+    for (double mb : tail) tr.push_back(rows_of(mb)), used += tr.back();
+    const int64_t rm = rows_of(mb_mid);
     std::vector<int64_t>& b = p->chunk_rows;
     b.push_back(0);
-    if (n > rf + rl) {
-      b.push_back(rf);
-      const int64_t mid = n - rf - rl;
+    if (n > used + rm / 2) {
+      int64_t at = 0;
+      for (int64_t r : hr) b.push_back(at += r);
+      const int64_t mid = n - used;
       const int64_t km = std::max<int64_t>(1, (mid + rm / 2) / rm);
       const int64_t step = (mid / km + G - 1) / G * G;
-      for (int64_t c = 1; c < km; ++c) b.push_back(rf + c * step);
-      b.push_back(n - rl);
+      for (int64_t c = 1; c < km; ++c) b.push_back(at + c * step);
+      at = n - used + at;  // start of the tail chunks
+      if (!tr.empty()) b.push_back(at);
+      for (size_t t = 0; t + 1 < tr.size(); ++t) b.push_back(at += tr[t]);
     }
-    b.push_back(n);
+    if (b.back() != n) b.push_back(n);
   }
   const int64_t nk = static_cast<int64_t>(p->chunk_rows.size()) - 1;
   std::vector<int32_t> chunk_of_group(ng + 1);
@@ -1228,6 +1263,12 @@ sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
 // the r chunks its columns reach have landed; M_U chunk c runs once the y
 // chunks it reads exist (bounded bandwidth of the triangular factors), and its
 // z chunk streams out on s_out while later r chunks are still arriving.
+bool device_mapped(const void* p);
+bool host_zc_out_enabled() {
+  const char* e = std::getenv("SAIT_HOST_ZC_OUT");
+  return !(e && std::atoi(e) == 0);
+}
+
 void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cudaStream_t s) {
   sait_pair_s::Work& w = pair_work(p, s);
   const int64_t k = static_cast<int64_t>(p->chunk_rows.size()) - 1;
@@ -1267,11 +1308,20 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
     mark("h2d" + std::to_string(c), w.s_in);
   }
   const auto& ub = p->u_rows;
+  // z straight into the caller's (pinned, device-mapped) host buffer: the M_U
+  // chunks' stores cross PCIe as they are produced, so no D2H stage trails the
+  // last input chunk (SAIT_HOST_ZC_OUT=0 keeps the copy-engine D2H chunks).
+  const bool zc_out = host_zc_out_enabled() && device_mapped(h_z);
   for (int64_t c = 0; c < k; ++c) {
     SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_in[p->needL_hi[c]], 0));
     sait::sell_spmv_rows(p->sl, b[c], b[c + 1], w.r_dev, w.y, s);
     mark("L" + std::to_string(c), s);
     if (ub[c + 1] > ub[c]) {
+      if (zc_out) {
+        sait::sell_spmv_rows(p->su, ub[c], ub[c + 1], w.y, h_z, s);
+        mark("U" + std::to_string(c), s);
+        continue;
+      }
       sait::sell_spmv_rows(p->su, ub[c], ub[c + 1], w.y, w.z_dev, s);
       SAIT_CUDA(cudaEventRecord(w.ev_u[c], s));
       mark("U" + std::to_string(c), s);

@@ -146,12 +146,19 @@ def test_nonfinite_inputs_propagate_like_reference(S, golden, c1_pair, port):
     assert bitwise_equal(z[fin], ez[fin])
 
 
-def test_chunked_host_apply_3d(S, port):
-    """Host-vector apply on a pair large enough for the chunked PCIe pipeline
-    (n = 64^3, two chunks): bitwise equal to the device-vector apply and the oracle."""
+@pytest.mark.parametrize("sched,zc", [("default", "1"), ("0.5;0.5;0.25", "1"), ("0.5;0.5;0.25", "0"),
+                                       ("0.25,0.5;0.75;0.5,0.25", "1"), ("0.5,0.5,0.25", "0")])
+def test_chunked_host_apply_3d(S, port, sched, zc, monkeypatch):
+    """Host-vector apply on n = 64^3 through the chunked PCIe pipeline (chunk
+    schedules small enough for several chunks; z by zero-copy stores or by
+    copy-engine D2H): bitwise equal to the device-vector apply and the oracle."""
     import torch
 
     from helpers import to_oracle
+
+    if sched != "default":
+        monkeypatch.setenv("SAIT_PIPE_MB", sched)
+    monkeypatch.setenv("SAIT_HOST_ZC_OUT", zc)
 
     A = S.laplacian_3d(64)
     f = S.ilu_k(A, 0)

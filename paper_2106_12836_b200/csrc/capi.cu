@@ -526,6 +526,14 @@ void sait_debug_copy_probe(const double* h_src, double* h_dst, int64_t n, int ch
 
 // Diagnostics (not part of sait_c.h): memory type of a pointer as this
 // library's runtime sees it (0 unregistered, 1 host/pinned, 2 device, 3 managed).
+// Index storage of a pair factor's SELL copy (which: 0 = M_L, 1 = M_U):
+// 2 shared slice patterns, 1 int16 deltas, 0 int32 columns, -1 no SELL copy.
+int sait_debug_pair_index_kind(sait_pair_t p, int which) {
+  if (!p) return -1;
+  const sait::SellMatrix& m = which == 0 ? p->sl : p->su;
+  return m.ok() ? m.index_kind() : -1;
+}
+
 int sait_debug_pointer_type(const void* ptr) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {

@@ -154,8 +154,14 @@ struct SellMatrix {
   int64_t* soff = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t* col = nullptr;   // absolute columns, -1 marks padding ...
   int16_t* dcol = nullptr;  // ... or col - row deltas, INT16_MIN marks padding
+  // ... or shared slice patterns: slice s reads its int16 deltas from
+  // dict[pat[s] + k*32 + lane] (regular matrices repeat a few patterns)
+  int32_t* pat = nullptr;
+  int16_t* dict = nullptr;
+  int64_t dict_elems = 0;
   double* val = nullptr;
   bool ok() const { return soff != nullptr; }
+  int index_kind() const { return dict ? 2 : dcol ? 1 : 0; }  // 2 dict, 1 int16, 0 int32
 };
 SellMatrix make_sell(const DevCsr& a, cudaStream_t s);  // empty if too irregular
 void free_sell(SellMatrix& m, cudaStream_t s);

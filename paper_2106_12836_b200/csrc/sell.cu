@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <unordered_map>
+
 #include "common.cuh"
 
 namespace sait {
@@ -48,14 +50,29 @@ __device__ __forceinline__ int16_t ld_na(const int16_t* p) {
 // Column storage of a SELL slice slot: absolute int32 columns (-1 = padding)
 // or int16 deltas col - row (INT16_MIN = padding) when every |col - row| of
 // the matrix fits, which saves 2 of the 12 bytes streamed per entry.
+// slice_base(s, base) = where slice s's slot-0 indices start in the policy's
+// array (the element offset base for per-entry storage).
 struct Idx32 {
   const int32_t* p;
+  __device__ __forceinline__ int64_t slice_base(int64_t /*s*/, int64_t base) const { return base; }
   __device__ __forceinline__ int32_t col(int64_t e, int32_t /*row*/) const { return ld_na(p + e); }
 };
 struct Idx16 {
   const int16_t* p;
+  __device__ __forceinline__ int64_t slice_base(int64_t /*s*/, int64_t base) const { return base; }
   __device__ __forceinline__ int32_t col(int64_t e, int32_t row) const {
     const int16_t d = ld_na(p + e);
+    return d == INT16_MIN ? -1 : row + d;
+  }
+};
+// Shared slice patterns: a few KB of deltas serve every slice, so they stay
+// in L1 and only the values stream from HBM (8 instead of 10 B per entry).
+struct IdxDict {
+  const int32_t* pat;
+  const int16_t* dict;
+  __device__ __forceinline__ int64_t slice_base(int64_t s, int64_t /*base*/) const { return __ldg(pat + s); }
+  __device__ __forceinline__ int32_t col(int64_t e, int32_t row) const {
+    const int16_t d = __ldg(dict + e);
     return d == INT16_MIN ? -1 : row + d;
   }
 };
@@ -194,6 +211,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
   const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
   const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
   const int64_t e0 = base + lane;
+  const int64_t i0 = idx.slice_base(s, base) + lane;
   double acc = 0.0;
   for (int32_t k0 = 0; k0 < w; k0 += 8) {
     int32_t c[8];
@@ -203,7 +221,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
       c[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
-        c[j] = idx.col(e0 + static_cast<int64_t>(k0 + j) * kSlice, row);
+        c[j] = idx.col(i0 + static_cast<int64_t>(k0 + j) * kSlice, row);
         v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
       }
     }
@@ -228,6 +246,7 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices;
        s += warps) {
     const int64_t base = soff[s];
+    const int64_t ib = idx.slice_base(s, base);
     const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
     double acc[NV];
 #pragma unroll
@@ -240,7 +259,7 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
         col[j] = -1;
         v[j] = 0.0;
         if (k0 + j < w) {
-          col[j] = idx.col(base + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
+          col[j] = idx.col(ib + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
           v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
         }
       }
@@ -277,6 +296,7 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
   const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
   const int64_t base = soff[s];
+  const int64_t ib = idx.slice_base(s, base);
   const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
   double acc[NV];
 #pragma unroll
@@ -289,7 +309,7 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
       col[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
-        col[j] = idx.col(base + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
+        col[j] = idx.col(ib + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
         v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
       }
     }
@@ -487,6 +507,7 @@ __device__ __forceinline__ double slice_row_idx(const int64_t* __restrict__ soff
                                                 const double* __restrict__ sval, int64_t s, int lane,
                                                 const double* __restrict__ x) {
   const int64_t base = soff[s];
+  const int64_t ib = idx.slice_base(s, base);
   const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
   const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
   double acc = 0.0;
@@ -498,7 +519,7 @@ __device__ __forceinline__ double slice_row_idx(const int64_t* __restrict__ soff
       c[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
-        c[j] = idx.col(base + lane + static_cast<int64_t>(k0 + j) * kSlice, row);
+        c[j] = idx.col(ib + lane + static_cast<int64_t>(k0 + j) * kSlice, row);
         v[j] = ld_na(sval + base + lane + static_cast<int64_t>(k0 + j) * kSlice);
       }
     }
@@ -610,6 +631,123 @@ void column_group_deps(const DevCsr& m, int32_t* lo, int32_t* hi, cudaStream_t s
 
 namespace {
 
+// ---- shared slice patterns (see IdxDict)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// one warp per slice: a hash of (width, every lane's int16 deltas)
+__global__ void slice_hash(int64_t nslices, const int64_t* __restrict__ soff, const int16_t* __restrict__ dcol,
+                           unsigned long long* __restrict__ h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int64_t base = soff[s];
+  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  unsigned long long x = static_cast<unsigned long long>(w) * 0x100000001B3ull + static_cast<unsigned long long>(lane);
+  for (int32_t k = 0; k < w; ++k)
+    x = mix64(x ^ static_cast<unsigned short>(dcol[base + static_cast<int64_t>(k) * kSlice + lane]));
+  x = mix64(x + static_cast<unsigned long long>(lane) * 0xD6E8FEB86659FD93ull);
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) h[s] = mix64(x ^ static_cast<unsigned long long>(w));
+}
+
+// any slice whose block differs from its representative's -> *bad
+__global__ void slice_verify(int64_t nslices, const int64_t* __restrict__ soff, const int16_t* __restrict__ dcol,
+                             const int32_t* __restrict__ rep, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int64_t r = rep[s];
+  if (r == s) return;
+  const int64_t b = soff[s], br = soff[r];
+  const int64_t len = soff[s + 1] - b;
+  if (len != soff[r + 1] - br) {
+    if (lane == 0) atomicOr(bad, 1);
+    return;
+  }
+  bool diff = false;
+  for (int64_t e = lane; e < len; e += kSlice) diff |= dcol[b + e] != dcol[br + e];
+  if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(bad, 1);
+}
+
+__global__ void slice_gather_dict(int64_t nslices, const int64_t* __restrict__ soff,
+                                  const int16_t* __restrict__ dcol, const int32_t* __restrict__ rep,
+                                  const int32_t* __restrict__ pat, int16_t* __restrict__ dict) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices || rep[s] != s) return;
+  const int64_t b = soff[s], len = soff[s + 1] - b;
+  for (int64_t e = lane; e < len; e += kSlice) dict[pat[s] + e] = dcol[b + e];
+}
+
+// Replace the per-entry int16 deltas by a dictionary of the distinct slice
+// blocks when it is small (<= 1M deltas) and actually saves bytes.
+void try_slice_dictionary(SellMatrix& m, cudaStream_t s) {
+  static const bool off = [] {
+    const char* e = std::getenv("SAIT_SELL_DICT");
+    return e && std::atoi(e) == 0;
+  }();
+  if (off || !m.dcol || m.nslices == 0) return;
+  const int64_t ns = m.nslices;
+  unsigned long long* dh = dalloc<unsigned long long>(ns, s);
+  slice_hash<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, m.dcol, dh);
+  SAIT_LAUNCHED();
+  std::vector<unsigned long long> hh(ns);
+  std::vector<int64_t> so(ns + 1);
+  SAIT_CUDA(cudaMemcpyAsync(hh.data(), dh, sizeof(unsigned long long) * ns, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaMemcpyAsync(so.data(), m.soff, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(dh, s);
+  std::unordered_map<unsigned long long, int32_t> first;
+  first.reserve(64);
+  std::vector<int32_t> rep(ns), pat(ns);
+  int64_t elems = 0;
+  constexpr int64_t kMaxDict = int64_t{1} << 20;
+  for (int64_t q = 0; q < ns; ++q) {
+    auto it = first.find(hh[q]);
+    if (it == first.end()) {
+      const int64_t len = so[q + 1] - so[q];
+      if (elems + len > kMaxDict) return;  // too many distinct blocks: keep per-entry deltas
+      it = first.emplace(hh[q], static_cast<int32_t>(q)).first;
+      pat[q] = static_cast<int32_t>(elems);
+      elems += len;
+    } else {
+      pat[q] = pat[it->second];
+    }
+    rep[q] = it->second;
+  }
+  if (elems * 4 > m.padded) return;  // little repetition: no saving
+  int32_t* d = dalloc<int32_t>(2 * ns, s);
+  int* bad = dalloc<int>(1, s);
+  SAIT_CUDA(cudaMemcpyAsync(d, rep.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+  SAIT_CUDA(cudaMemcpyAsync(d + ns, pat.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+  SAIT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  slice_verify<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, m.dcol, d, bad);
+  SAIT_LAUNCHED();
+  int hb = 0;
+  SAIT_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(bad, s);
+  if (hb) {  // a hash collision: keep the per-entry deltas
+    dfree(d, s);
+    return;
+  }
+  m.dict = dalloc<int16_t>(elems, s);
+  m.dict_elems = elems;
+  slice_gather_dict<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, m.dcol, d, d + ns, m.dict);
+  SAIT_LAUNCHED();
+  m.pat = dalloc<int32_t>(ns, s);
+  SAIT_CUDA(cudaMemcpyAsync(m.pat, d + ns, sizeof(int32_t) * ns, cudaMemcpyDeviceToDevice, s));
+  dfree(d, s);
+  dfree(m.dcol, s);
+  m.dcol = nullptr;
+  SAIT_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace
 
 SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
@@ -654,6 +792,7 @@ SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
   }
   SAIT_LAUNCHED();
   SAIT_CUDA(cudaStreamSynchronize(s));
+  try_slice_dictionary(m, s);
   return m;
 }
 
@@ -715,7 +854,7 @@ void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan&
 DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
                                 const std::vector<int64_t>& chunk_rows, cudaStream_t s) {
   DataflowPlan p;
-  const bool same_idx = (sl.dcol != nullptr) == (su.dcol != nullptr);
+  const bool same_idx = sl.index_kind() == su.index_kind();
   if (!sl.ok() || !su.ok() || !same_idx || L.nrows != U.nrows || chunk_rows.size() < 2) return p;
   p.gL = (L.nrows + kGroupRows - 1) / kGroupRows;
   p.gU = p.gL;
@@ -799,7 +938,8 @@ DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const Dev
   p.order = dalloc<int32_t>(order.size(), s);
   SAIT_CUDA(cudaMemcpyAsync(p.order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
   int per_sm = 0;
-  if (sl.dcol) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx16>, 256, 0));
+  if (sl.dict) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<IdxDict>, 256, 0));
+  else if (sl.dcol) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx16>, 256, 0));
   else SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx32>, 256, 0));
   p.grid = std::max(1, per_sm) * num_sms();
   SAIT_CUDA(cudaStreamSynchronize(s));
@@ -857,7 +997,9 @@ void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const Dataf
   }
   const unsigned grid = static_cast<unsigned>(dp.grid);
   st.claims += static_cast<unsigned long long>(dp.gL + dp.gU + dp.npieces) + grid;
-  if (sl.dcol) sell_dataflow_kernel<Idx16><<<grid, 256, 0, s>>>(a, Idx16{sl.dcol}, Idx16{su.dcol});
+  if (sl.dict)
+    sell_dataflow_kernel<IdxDict><<<grid, 256, 0, s>>>(a, IdxDict{sl.pat, sl.dict}, IdxDict{su.pat, su.dict});
+  else if (sl.dcol) sell_dataflow_kernel<Idx16><<<grid, 256, 0, s>>>(a, Idx16{sl.dcol}, Idx16{su.dcol});
   else sell_dataflow_kernel<Idx32><<<grid, 256, 0, s>>>(a, Idx32{sl.col}, Idx32{su.col});
   SAIT_LAUNCHED();
   if (dbg) {
@@ -894,6 +1036,8 @@ void free_sell(SellMatrix& m, cudaStream_t s) {
   dfree(m.soff, s);
   dfree(m.col, s);
   dfree(m.dcol, s);
+  dfree(m.pat, s);
+  dfree(m.dict, s);
   dfree(m.val, s);
   m = SellMatrix{};
 }
@@ -915,7 +1059,11 @@ void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const doubl
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (m.dcol) {
+  if (m.dict) {
+    IdxDict ix{m.pat, m.dict};
+    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<IdxDict, true>, m.n, s0, s1, m.soff, ix, m.val, x, y));
+    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<IdxDict, false>, m.n, s0, s1, m.soff, ix, m.val, x, y));
+  } else if (m.dcol) {
     Idx16 ix{m.dcol};
     if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, true>, m.n, s0, s1, m.soff, ix, m.val, x, y));
     else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, false>, m.n, s0, s1, m.soff, ix, m.val, x, y));
@@ -932,7 +1080,11 @@ void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, doubl
   if (m.nslices == 0) return;
   for (int c0 = 0; c0 < nvec; c0 += 8) {
     const int nv = nvec - c0 < 8 ? nvec - c0 : 8;
-    if (m.dcol)
+    if (m.dict)
+      sell_spmm_cm_kernel<8, IdxDict><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff,
+                                                                          IdxDict{m.pat, m.dict}, m.val,
+                                                                          x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
+    else if (m.dcol)
       sell_spmm_cm_kernel<8, Idx16><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, Idx16{m.dcol}, m.val,
                                                                         x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
     else
@@ -954,15 +1106,18 @@ bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaSt
       sell_spmv(m, x, y, s);
       return true;
     case 2:
-      if (m.dcol) launch_spmm<2>(m, Idx16{m.dcol}, x, y, s);
+      if (m.dict) launch_spmm<2>(m, IdxDict{m.pat, m.dict}, x, y, s);
+      else if (m.dcol) launch_spmm<2>(m, Idx16{m.dcol}, x, y, s);
       else launch_spmm<2>(m, Idx32{m.col}, x, y, s);
       break;
     case 4:
-      if (m.dcol) launch_spmm<4>(m, Idx16{m.dcol}, x, y, s);
+      if (m.dict) launch_spmm<4>(m, IdxDict{m.pat, m.dict}, x, y, s);
+      else if (m.dcol) launch_spmm<4>(m, Idx16{m.dcol}, x, y, s);
       else launch_spmm<4>(m, Idx32{m.col}, x, y, s);
       break;
     case 8:
-      if (m.dcol) launch_spmm<8>(m, Idx16{m.dcol}, x, y, s);
+      if (m.dict) launch_spmm<8>(m, IdxDict{m.pat, m.dict}, x, y, s);
+      else if (m.dcol) launch_spmm<8>(m, Idx16{m.dcol}, x, y, s);
       else launch_spmm<8>(m, Idx32{m.col}, x, y, s);
       break;
     default:

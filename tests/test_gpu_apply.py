@@ -202,3 +202,45 @@ def test_dataflow_host_apply_chunks(S, port, mb, monkeypatch):
         z = torch.zeros_like(r).pin_memory()
         pair.apply(r.numpy(), z.numpy())
         assert bitwise_equal(z.numpy(), port.pair_apply(to_oracle(ML), to_oracle(MU), r.numpy()))
+
+
+_DICT_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import ctypes as C
+import paper_2106_12836_b200 as S
+from paper_2106_12836_b200 import _native as N
+from oracle import oracle as O
+P = O.get("port")
+A = O.laplacian_3d(24)
+L, U = P.ilu_k(A, 0)
+ML, MU = P.sait_thr(L, True, 5e-2, 3), P.sait_thr(U, False, 5e-2, 3)
+from helpers import to_product
+pair = S.SaitPairPreconditioner(to_product(ML), to_product(MU))
+N.lib.sait_debug_pair_index_kind.restype = C.c_int
+kinds = [N.lib.sait_debug_pair_index_kind(pair.handle, w) for w in (0, 1)]
+r = O.uniform_pm1(3, A.nrows)
+z = np.empty(A.nrows)
+pair.apply(r, z)
+ok = np.array_equal(z.view(np.uint64), P.pair_apply(ML, MU, r).view(np.uint64))
+print(kinds[0], kinds[1], int(ok))
+"""
+
+
+@pytest.mark.parametrize("env,kind", [("1", 2), ("0", 1)])
+def test_sell_index_formats(env, kind):
+    """The SELL copy of a stencil factor uses shared slice patterns (a few
+    distinct int16 delta blocks serve every slice) unless SAIT_SELL_DICT=0;
+    both give the oracle's bits."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = _DICT_CHILD.format(root=ROOT)
+    envd = dict(os.environ, SAIT_SELL_DICT=env, PYTHONPATH=os.path.join(ROOT, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], env=envd, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    k0, k1, ok = map(int, out.stdout.split()[-3:])
+    assert (k0, k1, ok) == (kind, kind, 1)

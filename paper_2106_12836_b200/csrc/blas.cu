@@ -8,6 +8,8 @@
 // one block whose thread t first sums partials t, t+256, ... in order.  With
 // every product rounded before its add, dots are bitwise reproducible and
 // equal to the CPU restatement, so solver iteration counts match exactly.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sait {
@@ -27,6 +29,12 @@ __device__ __forceinline__ double tree8(const double* w) {
   const double a0 = __dadd_rn(w[0], w[4]), a1 = __dadd_rn(w[1], w[5]);
   const double a2 = __dadd_rn(w[2], w[6]), a3 = __dadd_rn(w[3], w[7]);
   return __dadd_rn(__dadd_rn(a0, a2), __dadd_rn(a1, a3));
+}
+
+__device__ __forceinline__ double ld_ro(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
 }
 
 // part[j * nb + b] = canonical block partial of x . V_j
@@ -126,17 +134,25 @@ __global__ void block_lincomb_k(int64_t n, const double* __restrict__ in, int ki
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  // each input element read once; output j accumulates q = 0, 1, ... in order
+  // each input element read once; output j accumulates q = 0, 1, ... in order.
+  // Inputs are fetched 8 at a time (all loads in flight before the
+  // arithmetic that consumes them).
   double acc[16];
   const double x0 = in[i];
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     if (j < kout) acc[j] = __dmul_rn(x0, cs[j]);
-  for (int q = 1; q < kin; ++q) {
-    const double xq = in[n * q + i];
+  for (int q0 = 1; q0 < kin; q0 += 8) {
+    double xq[8];
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < kout) acc[j] = __dadd_rn(acc[j], __dmul_rn(xq, cs[q * kout + j]));
+    for (int u = 0; u < 8; ++u) xq[u] = q0 + u < kin ? ld_ro(in + n * (q0 + u) + i) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (q0 + u >= kin) break;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < kout) acc[j] = __dadd_rn(acc[j], __dmul_rn(xq[u], cs[(q0 + u) * kout + j]));
+    }
   }
 #pragma unroll
   for (int j = 0; j < 16; ++j)
@@ -174,49 +190,106 @@ __global__ void block_residual_k(int64_t n, int k, const double* __restrict__ AX
   for (int j = 0; j < k; ++j) R[n * j + i] = __dsub_rn(AX[n * j + i], __dmul_rn(lam[j], X[n * j + i]));
 }
 
-// Tall-skinny Gram tile: part[(a * kb + b) * nb + blk] = canonical block
-// partial of A_a . B_b for a < ka <= 8, b < kb <= 8 (column-major blocks,
-// leading dimension n).  Each thread keeps the 64 running sums of its 8
-// strided elements in registers, so the tile's 16 columns are read once.
-template <int TT>
-__global__ void __launch_bounds__(kT) gram_tile_partials(int64_t n, const double* __restrict__ A, int ka,
-                                                          const double* __restrict__ B, int kb,
-                                                          double* __restrict__ part, int64_t nb) {
-  __shared__ double ws[TT * TT][8];
+// Tall-skinny Gram: part[(a * kb + b) * nb + blk] = canonical block partial
+// of A_a . B_b.  One launch covers every tile: blockIdx.x = tile (a TA x TB
+// block of columns), blockIdx.y = 2048-element data block, so the CTAs that
+// run together share a data block and read its columns from L2 after the
+// first touch.  Each thread keeps the TA*TB running sums of its 8 strided
+// elements in registers (the canonical per-thread order), then the warp
+// butterfly and the 8-warp tree.
+struct GramTile {
+  int a0, b0;
+};
+template <int TA, int TB>
+__global__ void __launch_bounds__(kT) gram_tiles(int64_t n, const double* __restrict__ A, int ka,
+                                                  const double* __restrict__ B, int kb,
+                                                  const GramTile* __restrict__ tiles, double* __restrict__ part,
+                                                  int64_t nb, bool tile_major) {
+  __shared__ double ws[TA * TB][8];
+  const GramTile tl = tiles[tile_major ? blockIdx.x : blockIdx.y];
+  const int ta = min(TA, ka - tl.a0), tb = min(TB, kb - tl.b0);
+  const double* Ap = A + n * tl.a0;
+  const double* Bp = B + n * tl.b0;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kB + t;
-  double acc[TT][TT];
+  const int64_t blk = tile_major ? blockIdx.y : blockIdx.x;
+  const int64_t base = blk * kB + t;
+  double acc[TA][TB];
 #pragma unroll
-  for (int a = 0; a < TT; ++a)
+  for (int a = 0; a < TA; ++a)
 #pragma unroll
-    for (int b = 0; b < TT; ++b) acc[a][b] = 0.0;
-#pragma unroll 2
-  for (int k = 0; k < kK; ++k) {
-    const int64_t i = base + static_cast<int64_t>(kT) * k;
-    if (i < n) {
-      double xa[TT], yb[TT];
+    for (int b = 0; b < TB; ++b) acc[a][b] = 0.0;
+  // two k-steps per round, all 2 (TA + TB) loads issued before any use (the
+  // asm volatile loads keep the compiler from interleaving them with the
+  // arithmetic), then the products in the canonical k order
+#pragma unroll 1
+  for (int k = 0; k < kK; k += 2) {
+    const int64_t i0 = base + static_cast<int64_t>(kT) * k, i1 = i0 + kT;
+    double xa[2][TA], yb[2][TB];
 #pragma unroll
-      for (int a = 0; a < TT; ++a) xa[a] = a < ka ? A[n * a + i] : 0.0;
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = u ? i1 : i0;
 #pragma unroll
-      for (int b = 0; b < TT; ++b) yb[b] = b < kb ? B[n * b + i] : 0.0;
+      for (int a = 0; a < TA; ++a) xa[u][a] = (a < ta && i < n) ? ld_ro(Ap + n * a + i) : 0.0;
 #pragma unroll
-      for (int a = 0; a < TT; ++a)
+      for (int b = 0; b < TB; ++b) yb[u][b] = (b < tb && i < n) ? ld_ro(Bp + n * b + i) : 0.0;
+    }
 #pragma unroll
-        for (int b = 0; b < TT; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(xa[a], yb[b]));
+    for (int u = 0; u < 2; ++u) {
+      if ((u ? i1 : i0) >= n) continue;
+#pragma unroll
+      for (int a = 0; a < TA; ++a)
+#pragma unroll
+        for (int b = 0; b < TB; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(xa[u][a], yb[u][b]));
     }
   }
 #pragma unroll
-  for (int a = 0; a < TT; ++a)
+  for (int a = 0; a < TA; ++a)
 #pragma unroll
-    for (int b = 0; b < TT; ++b) {
+    for (int b = 0; b < TB; ++b) {
       const double v = warp_butterfly(acc[a][b]);
-      if (lane == 0) ws[a * TT + b][warp] = v;
+      if (lane == 0) ws[a * TB + b][warp] = v;
     }
   __syncthreads();
-  if (t < TT * TT) {
-    const int a = t / TT, b = t % TT;
-    if (a < ka && b < kb) part[static_cast<int64_t>(a * kb + b) * nb + blockIdx.x] = tree8(ws[t]);
+  if (t < TA * TB) {
+    const int a = t / TB, b = t % TB;
+    if (a < ta && b < tb) part[static_cast<int64_t>((tl.a0 + a) * kb + tl.b0 + b) * nb + blk] = tree8(ws[t]);
   }
+}
+
+// G[a * ldg + b] = canonical fold of the nb partials of dot (a, b) for every
+// (a, b) of the listed tiles (one block per dot).
+template <int TA, int TB>
+__global__ void __launch_bounds__(kT) gram_fold(const double* __restrict__ part, int64_t nb, int ka, int kb,
+                                                 const GramTile* __restrict__ tiles, double* __restrict__ G,
+                                                 int ldg) {
+  __shared__ double ws[8];
+  const GramTile tl = tiles[blockIdx.x / (TA * TB)];
+  const int q = blockIdx.x % (TA * TB), a = tl.a0 + q / TB, b = tl.b0 + q % TB;
+  if (a >= ka || b >= kb) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double* p = part + static_cast<int64_t>(a * kb + b) * nb;
+  double s = 0.0;
+  for (int64_t r = t; r < nb; r += kT) s = __dadd_rn(s, p[r]);
+  s = warp_butterfly(s);
+  if (lane == 0) ws[warp] = s;
+  __syncthreads();
+  if (t == 0) G[a * ldg + b] = tree8(ws);
+}
+
+// x_i = 2 u_i - 1, u_i = (splitmix64(seed ^ splitmix64(i)) >> 11) 2^-53:
+// sait_fill_uniform_pm1 (host_inputs.cpp) on the device, bit for bit.
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void fill_uniform_pm1_k(unsigned long long seed, int64_t n, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long x = splitmix(seed ^ splitmix(static_cast<unsigned long long>(i)));
+  const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
+  out[i] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
 }
 
 __global__ void hadamard_k(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
@@ -261,21 +334,54 @@ int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
 
 // G[a * ldg + b] (device, a < ka, b < kb) = canonical dot of A_a and B_b,
 // computed tile by tile (8 x 8); identical bits to multi_dot per entry.
+int64_t gram_scratch(int64_t n, int ka, int kb) { return dot_blocks(n) * ka * kb; }
+
+// G (device, row-major, leading dimension ldg) = A^T B for column-major
+// blocks A (n x ka) and B (n x kb); upper_only skips tiles strictly below the
+// diagonal.  scratch: gram_scratch(n, ka, kb) doubles; tiles: a device array
+// of at least (ceil(ka/8) * ceil(kb/8)) GramTile (written here).
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
-          cudaStream_t s, bool upper_only) {
+          void* tiles_dev, cudaStream_t s, bool upper_only) {
+  constexpr int TA = 8, TB = 8;
   const int64_t nb = dot_blocks(n);
-  constexpr int TT = 8;
-  for (int a0 = 0; a0 < ka; a0 += TT)
-    for (int b0 = 0; b0 < kb; b0 += TT) {
-      if (upper_only && b0 + TT <= a0) continue;
-      const int ta = ka - a0 < TT ? ka - a0 : TT, tb = kb - b0 < TT ? kb - b0 : TT;
-      gram_tile_partials<TT><<<static_cast<unsigned>(nb), kT, 0, s>>>(n, A + n * a0, ta, B + n * b0, tb, scratch, nb);
-      SAIT_LAUNCHED();
-      for (int a = 0; a < ta; ++a) {  // one final fold per tile row: tb blocks
-        mdot_final<<<tb, kT, 0, s>>>(scratch + static_cast<int64_t>(a * tb) * nb, nb, G + (a0 + a) * ldg + b0, 0);
-        SAIT_LAUNCHED();
-      }
+  GramTile list[64];
+  int nt = 0;
+  for (int a0 = 0; a0 < ka; a0 += TA)
+    for (int b0 = 0; b0 < kb; b0 += TB) {
+      if (upper_only && b0 + TB <= a0) continue;
+      list[nt++] = GramTile{a0, b0};
     }
+  if (nt == 0 || nb == 0) return;
+  GramTile* tiles = static_cast<GramTile*>(tiles_dev);
+  SAIT_CUDA(cudaMemcpyAsync(tiles, list, sizeof(GramTile) * nt, cudaMemcpyHostToDevice, s));
+  static const bool tile_major = [] {
+    const char* e = std::getenv("SAIT_GRAM_ORDER");
+    return e && std::atoi(e) == 1;
+  }();
+  static const bool per_tile = [] {
+    const char* e = std::getenv("SAIT_GRAM_PER_TILE");
+    return e && std::atoi(e) == 1;
+  }();
+  if (per_tile) {
+    for (int q = 0; q < nt; ++q) {
+      gram_tiles<TA, TB><<<dim3(static_cast<unsigned>(nb), 1), kT, 0, s>>>(n, A, ka, B, kb, tiles + q, scratch, nb,
+                                                                            false);
+      SAIT_LAUNCHED();
+    }
+  } else {
+    const dim3 grid = tile_major ? dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nb))
+                                 : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(nt));
+    gram_tiles<TA, TB><<<grid, kT, 0, s>>>(n, A, ka, B, kb, tiles, scratch, nb, tile_major);
+  }
+  SAIT_LAUNCHED();
+  gram_fold<TA, TB><<<static_cast<unsigned>(nt * TA * TB), kT, 0, s>>>(scratch, nb, ka, kb, tiles, G, ldg);
+  SAIT_LAUNCHED();
+}
+
+void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  fill_uniform_pm1_k<<<grid_for(n, 256), 256, 0, s>>>(seed, n, out);
+  SAIT_LAUNCHED();
 }
 
 void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, double* out, double* scratch,

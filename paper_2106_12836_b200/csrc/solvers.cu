@@ -33,8 +33,10 @@ void axpy(int64_t n, double a, const double* x, double* y, cudaStream_t s);
 void xpay(int64_t n, const double* x, double a, double* y, cudaStream_t s);
 void x_minus_y(int64_t n, const double* x, double* y, cudaStream_t s);
 void y_plus_x(int64_t n, const double* x, double* y, cudaStream_t s);
+int64_t gram_scratch(int64_t n, int ka, int kb);
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
-          cudaStream_t s, bool upper_only);
+          void* tiles_dev, cudaStream_t s, bool upper_only);
+void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s);
 void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s);
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
@@ -502,8 +504,15 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     double* AS = sait::dalloc<double>(3 * blk, s);  // [AX AW AP]
     double* R = sait::dalloc<double>(blk, s);
     double* tmp = sait::dalloc<double>(4 * blk, s);
-    double* dsmall = sait::dalloc<double>(48 * 48, s);
+    // small host->device operands (Gram corrections, coefficient blocks) use a
+    // ring of slots so consecutive uploads need no synchronisation
+    constexpr int kSlots = 8;
+    double* dsmall = sait::dalloc<double>(kSlots * 48 * 48, s);
+    int slot = 0;
+    auto next_small = [&] { return dsmall + static_cast<int64_t>(48 * 48) * (slot++ % kSlots); };
     sait::Scalars sc(n, 48 * 48, 64, s);
+    double* gscratch = sait::dalloc<double>(sait::gram_scratch(n, 3 * k, 3 * k), s);
+    void* gtiles = sait::dalloc<long long>(64, s);
     double *X = S, *W = S + blk, *P = S + 2 * blk;
     double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
     auto block_spmv = [&](const double* in, double* out) { op.apply_block(in, out, k, s); };
@@ -512,7 +521,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     // the canonical dot is symmetric in its arguments)
     auto gram = [&](const double* Sa, int ka, const double* Yb, int kb, std::vector<double>& G, bool sym = false) {
       G.assign(static_cast<size_t>(ka) * kb, 0.0);
-      sait::gram(n, Sa, ka, Yb, kb, sc.d, kb, sc.part, s, sym);
+      sait::gram(n, Sa, ka, Yb, kb, sc.d, kb, gscratch, gtiles, s, sym);
       sc.fetch(ka * kb, s);
       std::copy(sc.h.begin(), sc.h.begin() + static_cast<size_t>(ka) * kb, G.begin());
       if (sym)
@@ -521,9 +530,9 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
             if ((b2 / 8) < (a2 / 8)) G[a2 * kb + b2] = G[b2 * kb + a2];
     };
     auto lincomb = [&](const double* in, int kin, const double* C, int kout, double* out) {
-      SAIT_CUDA(cudaMemcpyAsync(dsmall, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));
-      sait::block_lincomb(n, in, kin, dsmall, kout, out, s);
-      SAIT_CUDA(cudaStreamSynchronize(s));  // dsmall is reused
+      double* d = next_small();
+      SAIT_CUDA(cudaMemcpyAsync(d, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));
+      sait::block_lincomb(n, in, kin, d, kout, out, s);
     };
     auto cholqr = [&](double* Y, double* AY) {
       std::vector<double> G, L(k * k), Li(k * k), Ri(k * k);
@@ -550,15 +559,10 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
       std::fprintf(stderr, "%s=%.2fms ", nm, std::chrono::duration<double, std::milli>(now - tp).count());
       tp = now;
     };
-    {  // X0 ~ U[-1,1], column j from seed (seed * 1000 + j)
-      std::vector<double> h(n);
-      for (int j = 0; j < k; ++j) {
-        sait_fill_uniform_pm1(seed * 1000 + static_cast<uint64_t>(j), n, h.data());
-        SAIT_CUDA(cudaMemcpyAsync(X + static_cast<int64_t>(j) * n, h.data(), sizeof(double) * n,
-                                  cudaMemcpyHostToDevice, s));
-        SAIT_CUDA(cudaStreamSynchronize(s));
-      }
-    }
+    // X0 ~ U[-1,1], column j from seed (seed * 1000 + j), generated on the
+    // device with the host generator's exact arithmetic
+    for (int j = 0; j < k; ++j)
+      sait::fill_uniform_pm1_device(seed * 1000 + static_cast<uint64_t>(j), n, X + static_cast<int64_t>(j) * n, s);
     phase("init_x");
     block_spmv(X, AX);
     bool failed = false;
@@ -576,8 +580,9 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
       lincomb(AX, k, C.data(), k, tmp);
       SAIT_CUDA(cudaMemcpyAsync(AX, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
       for (it = 0; it <= maxit; ++it) {
-        SAIT_CUDA(cudaMemcpyAsync(dsmall, lam.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
-        sait::block_residual(n, k, AX, X, dsmall, R, s);
+        double* dl = next_small();
+        SAIT_CUDA(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+        sait::block_residual(n, k, AX, X, dl, R, s);
         for (int j = 0; j < k; ++j)
           sait::multi_dot(n, R + static_cast<int64_t>(j) * n, R + static_cast<int64_t>(j) * n, n, 1, sc.d + j, sc.part,
                           s, true);
@@ -594,9 +599,9 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
         phase("precond");
         std::vector<double> G1;
         gram(X, k, W, k, G1);
-        SAIT_CUDA(cudaMemcpyAsync(dsmall, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
-        sait::block_sub_lincomb(n, X, k, dsmall, W, s);
-        SAIT_CUDA(cudaStreamSynchronize(s));
+        double* dg = next_small();
+        SAIT_CUDA(cudaMemcpyAsync(dg, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
+        sait::block_sub_lincomb(n, X, k, dg, W, s);
         if (!cholqr(W, nullptr)) {
           failed = true;
           why = "lobpcg: preconditioned residual block is rank deficient";
@@ -655,6 +660,8 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     sait::dfree(R, s);
     sait::dfree(tmp, s);
     sait::dfree(dsmall, s);
+    sait::dfree(gscratch, s);
+    sait::dfree(gtiles, s);
     sc.release(s);
     op.release(s);
     SAIT_CUDA(cudaStreamSynchronize(s));

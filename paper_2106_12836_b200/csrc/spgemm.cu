@@ -324,24 +324,37 @@ __global__ void spgemm_global(Args g, const int32_t* __restrict__ rows, const in
 // sum over each run of equal columns: exactly the reference order, no shared
 // memory.  The count pass stages the sorted survivors in a G-entry slot per
 // row; the numeric pass is a copy (+ stabilization compare).
+// The row's operands up to B's row extents.
+struct TinyFetch {
+  int32_t j, m, len, bst;
+  double aval;
+  bool live;
+};
+__device__ __forceinline__ TinyFetch tiny_fetch(const Args& g, const int32_t* __restrict__ rows, int64_t r,
+                                                int32_t nrows_bin, int lane) {
+  TinyFetch f{0, 0, 0, 0, 0.0, r < nrows_bin};
+  if (f.live) {
+    f.j = rows[r];
+    const int32_t a0 = g.arp[f.j];
+    f.m = g.arp[f.j + 1] - a0;
+    if (lane < f.m) {
+      const int32_t k = g.aci[a0 + lane];
+      f.aval = g.av[a0 + lane];
+      f.bst = g.brp[k];
+      f.len = g.brp[k + 1] - f.bst;
+    }
+  }
+  return f;
+}
+
 template <int G>
-__device__ __forceinline__ void tiny_row(const Args& g, int32_t j, bool live_row, int lane, int64_t slot,
+__device__ __forceinline__ void tiny_row(const Args& g, const TinyFetch& f, int lane, int64_t slot,
                                          int32_t* __restrict__ tcol, double* __restrict__ tval) {
   constexpr unsigned kAll = 0xffffffffu;
   const int grp = (threadIdx.x & 31) / G;
-  int32_t a0 = 0, m = 0;
-  if (live_row) {
-    a0 = g.arp[j];
-    m = g.arp[j + 1] - a0;
-  }
-  int32_t len = 0, bst = 0;
-  double aval = 0.0;
-  if (lane < m) {
-    const int32_t k = g.aci[a0 + lane];
-    aval = g.av[a0 + lane];
-    bst = g.brp[k];
-    len = g.brp[k + 1] - bst;
-  }
+  const int32_t j = f.j, m = f.m, len = f.len, bst = f.bst;
+  const bool live_row = f.live;
+  const double aval = f.aval;
   int32_t incl = len;
 #pragma unroll
   for (int o = 1; o < G; o <<= 1) {
@@ -458,14 +471,17 @@ __global__ void __launch_bounds__(256) spgemm_tiny(Args g, const int32_t* __rest
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int sub = (threadIdx.x & 31) / G;
+  // (fetching the next row ahead was measured slower: the tiny rows are
+  // bound by shuffle throughput, not by the load chain)
   for (int64_t w = warp0; w * kPerWarp < nrows_bin; w += nwarps) {
-    const int64_t r = w * kPerWarp + sub;
-    const bool live = r < nrows_bin;
-    tiny_row<G>(g, live ? rows[r] : 0, live, lane, r, tcol, tval);
+    const TinyFetch cur = tiny_fetch(g, rows, w * kPerWarp + sub, nrows_bin, lane);
+    tiny_row<G>(g, cur, lane, w * kPerWarp + sub, tcol, tval);
   }
 }
 
-// numeric pass of the tiny rows: staged slot -> final row, + early-stop compare
+// numeric pass of the tiny rows: staged slot -> final row, + early-stop
+// compare.  One thread per row (the staged slot and the output row are
+// contiguous per thread), so a warp moves 32 rows per round trip.
 template <int G>
 __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                          const int32_t* __restrict__ tcol,
@@ -473,43 +489,43 @@ __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* _
   __shared__ int blk_changed;
   if (threadIdx.x == 0) blk_changed = 0;
   __syncthreads();
-  constexpr int kPerWarp = 32 / G;
-  const int lane = threadIdx.x & (G - 1);
-  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int sub = (threadIdx.x & 31) / G;
   bool diff_any = false;
-  for (int64_t w = warp0; w * kPerWarp < nrows_bin; w += nwarps) {
-    const int64_t r = w * kPerWarp + sub;
-    if (r >= nrows_bin) continue;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows_bin;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t j = rows[r];
     const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
-    int32_t c = 0;
-    double v = 0.0;
-    if (lane < live) {
-      c = tcol[r * G + lane];
-      v = tval[r * G + lane];
-      g.cci[out + lane] = c;
-      g.cv[out + lane] = v;
+    const int32_t* tc = tcol + r * G;
+    const double* tv = tval + r * G;
+    const bool cmp = g.epi.qrp && !diff_any;
+    int32_t qb = 0, ql = 0;
+    if (cmp) {
+      qb = g.epi.qrp[j];
+      ql = g.epi.qrp[j + 1] - qb;
     }
-    if (g.epi.qrp && !diff_any) {
-      const int32_t qb = g.epi.qrp[j], ql = g.epi.qrp[j + 1] - qb;
-      bool diff = ql != live;
-      if (!diff && lane < live) {
-        const double a = g.epi.qv[qb + lane];
+    bool diff = cmp && ql != live;
+#pragma unroll 4
+    for (int32_t q = 0; q < live; ++q) {
+      const int32_t c = tc[q];
+      const double v = tv[q];
+      g.cci[out + q] = c;
+      g.cv[out + q] = v;
+      if (cmp && !diff) {
+        const double a = g.epi.qv[qb + q];
         const double fa = fabs(a), fb = fabs(v);
         const double mx = fa < fb ? fb : fa;
-        diff = g.epi.qci[qb + lane] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx);
+        diff = g.epi.qci[qb + q] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx);
       }
-      diff_any = diff_any || diff;
     }
+    diff_any = diff_any || diff;
   }
-  if (diff_any) blk_changed = 1;
+  if (__any_sync(0xffffffffu, diff_any) && (threadIdx.x & 31) == 0) blk_changed = 1;
   __syncthreads();
   if (threadIdx.x == 0 && blk_changed) atomicOr(g.changed, 1);
 }
 
-// products per row (P_j) -> table bin; histogram of bins; total products.
+// products per row (P_j) -> table bin; histogram of bins; total products
+// (warp-aggregated: one shared atomic per warp and bin, one per warp for
+// the total).
 __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restrict__ pcap,
                           int32_t* __restrict__ hist, unsigned long long* __restrict__ total) {
   __shared__ int32_t h[kNumBins];
@@ -517,25 +533,32 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
   if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
   if (threadIdx.x == 0) tsum = 0;
   __syncthreads();
-  int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int64_t p = 0;
+  int bin = -1;
   if (j < g.n) {
-    int64_t p = 0;
-    for (int32_t e = g.arp[j]; e < g.arp[j + 1]; ++e) {
-      int32_t k = g.aci[e];
+    const int32_t e0 = g.arp[j], e1 = g.arp[j + 1];
+#pragma unroll 4
+    for (int32_t e = e0; e < e1; ++e) {
+      const int32_t k = g.aci[e];
       p += g.brp[k + 1] - g.brp[k];
     }
-    atomicAdd(&tsum, static_cast<unsigned long long>(p));
     int64_t distinct = (p < g.ncols ? p : g.ncols) + 1;  // +1: the identity entry
     int logs = kMinLogSlots;
     while ((int64_t{1} << logs) < 2 * distinct) ++logs;
-    int bin = kFirstSmemBin + logs - kMinLogSlots;
+    bin = kFirstSmemBin + logs - kMinLogSlots;
     if (bin > kGlobalBin) bin = kGlobalBin;
-    const int32_t m = g.arp[j + 1] - g.arp[j];
+    const int32_t m = e1 - e0;
     if (p < 32 && m <= 32) bin = (p < 8 && m <= 8) ? 0 : (p < 16 && m <= 16) ? 1 : 2;
     bin_of[j] = static_cast<int8_t>(bin);
     pcap[j] = logs;  // table log2 size (used by the global bin)
-    atomicAdd(&h[bin], 1);
   }
+  unsigned long long ps = static_cast<unsigned long long>(p);
+  for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+  if (lane == 0 && ps) atomicAdd(&tsum, ps);
+  const unsigned grp = __match_any_sync(0xffffffffu, bin);
+  if (bin >= 0 && lane == __ffs(grp) - 1) atomicAdd(&h[bin], __popc(grp));
   __syncthreads();
   if (threadIdx.x < kNumBins && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
   if (threadIdx.x == 0 && tsum) atomicAdd(total, tsum);
@@ -598,18 +621,19 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s) {
     const int per_warp = 32 / kTinyG[tb];
     const int64_t warps = (tc + per_warp - 1) / per_warp;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, int64_t{num_sms()} * 8 * 16));
+    const unsigned egrid = static_cast<unsigned>(std::min<int64_t>((tc + 255) / 256, int64_t{num_sms()} * 8 * 16));
     const int32_t* rows = pl.lists + pl.start[tb];
     switch (kTinyG[tb]) {
       case 8:
-        if (numeric) spgemm_tiny_emit<8><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        if (numeric) spgemm_tiny_emit<8><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         else spgemm_tiny<8><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         break;
       case 16:
-        if (numeric) spgemm_tiny_emit<16><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        if (numeric) spgemm_tiny_emit<16><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         else spgemm_tiny<16><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         break;
       default:
-        if (numeric) spgemm_tiny_emit<32><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        if (numeric) spgemm_tiny_emit<32><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         else spgemm_tiny<32><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
     }
     SAIT_LAUNCHED();

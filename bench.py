@@ -346,6 +346,11 @@ def run_b200(args):
             pass
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "kernel": "sell_spmv_kernel",
+                    # the DRAM bytes ncu counts per launch moved at this rate: the
+                    # kernel's share of the copy peak in bytes it really moves
+                    # (algorithmic > DRAM bytes: int16/shared index patterns, x in L2)
+                    "dram_achieved": (traffic / (0.5 * (kt["L"] + kt["U"]) * 1e-3) / 1e9) if traffic else None,
+                    "dram_frac": (traffic / (0.5 * (kt["L"] + kt["U"]) * 1e-3) / 1e9 / peak) if traffic else None,
                     "per_launch_ms": {"M_L": kt["L"], "M_U": kt["U"]},
                     "algorithmic_bytes_per_launch": {"M_L": bytes_l, "M_U": bytes_u},
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)"}

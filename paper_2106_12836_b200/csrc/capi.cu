@@ -1246,7 +1246,10 @@ void factor_spmv(sait_pair_t p, int which, const double* x, double* y, cudaStrea
   const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
   const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
   const int v = pair_variant();
-  if (v >= 2 && sm.ok()) sait::sell_spmv_rows(sm, 0, sm.n, x, y, s, which == 1 && pdl_enabled());
+  // both halves are programmatic dependents of whatever precedes them on s:
+  // M_U of M_L, and M_L of the previous kernel (e.g. the last apply's M_U),
+  // each loading its first index/value batch before griddepcontrol.wait
+  if (v >= 2 && sm.ok()) sait::sell_spmv_rows(sm, 0, sm.n, x, y, s, pdl_enabled());
   else if (v == 1) sait::spmv_planned(m, pl, x, y, s);
   else sait::spmv(m, x, y, s);
 }

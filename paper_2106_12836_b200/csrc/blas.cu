@@ -201,7 +201,7 @@ struct GramTile {
   int a0, b0;
 };
 template <int TA, int TB>
-__global__ void __launch_bounds__(kT) gram_tiles(int64_t n, const double* __restrict__ A, int ka,
+__global__ void __launch_bounds__(kT, (TB <= 4 ? 2 : 1)) gram_tiles(int64_t n, const double* __restrict__ A, int ka,
                                                   const double* __restrict__ B, int kb,
                                                   const GramTile* __restrict__ tiles, double* __restrict__ part,
                                                   int64_t nb, bool tile_major) {
@@ -340,11 +340,12 @@ int64_t gram_scratch(int64_t n, int ka, int kb) { return dot_blocks(n) * ka * kb
 // blocks A (n x ka) and B (n x kb); upper_only skips tiles strictly below the
 // diagonal.  scratch: gram_scratch(n, ka, kb) doubles; tiles: a device array
 // of at least (ceil(ka/8) * ceil(kb/8)) GramTile (written here).
-void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
-          void* tiles_dev, cudaStream_t s, bool upper_only) {
-  constexpr int TA = 8, TB = 8;
+namespace {
+template <int TA, int TB>
+void gram_impl(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
+               void* tiles_dev, cudaStream_t s, bool upper_only) {
   const int64_t nb = dot_blocks(n);
-  GramTile list[64];
+  GramTile list[256];
   int nt = 0;
   for (int a0 = 0; a0 < ka; a0 += TA)
     for (int b0 = 0; b0 < kb; b0 += TB) {
@@ -356,26 +357,32 @@ void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G
   SAIT_CUDA(cudaMemcpyAsync(tiles, list, sizeof(GramTile) * nt, cudaMemcpyHostToDevice, s));
   static const bool tile_major = [] {
     const char* e = std::getenv("SAIT_GRAM_ORDER");
-    return e && std::atoi(e) == 1;
+    return !(e && std::atoi(e) == 0);
   }();
-  static const bool per_tile = [] {
-    const char* e = std::getenv("SAIT_GRAM_PER_TILE");
-    return e && std::atoi(e) == 1;
-  }();
-  if (per_tile) {
-    for (int q = 0; q < nt; ++q) {
-      gram_tiles<TA, TB><<<dim3(static_cast<unsigned>(nb), 1), kT, 0, s>>>(n, A, ka, B, kb, tiles + q, scratch, nb,
-                                                                            false);
-      SAIT_LAUNCHED();
-    }
-  } else {
-    const dim3 grid = tile_major ? dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nb))
-                                 : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(nt));
-    gram_tiles<TA, TB><<<grid, kT, 0, s>>>(n, A, ka, B, kb, tiles, scratch, nb, tile_major);
-  }
+  const dim3 grid = tile_major ? dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nb))
+                               : dim3(static_cast<unsigned>(nb), static_cast<unsigned>(nt));
+  gram_tiles<TA, TB><<<grid, kT, 0, s>>>(n, A, ka, B, kb, tiles, scratch, nb, tile_major);
   SAIT_LAUNCHED();
   gram_fold<TA, TB><<<static_cast<unsigned>(nt * TA * TB), kT, 0, s>>>(scratch, nb, ka, kb, tiles, G, ldg);
   SAIT_LAUNCHED();
+}
+}  // namespace
+
+
+
+// G (device, row-major, leading dimension ldg) = A^T B for column-major
+// blocks A (n x ka) and B (n x kb); upper_only skips tiles strictly below the
+// diagonal.  scratch: gram_scratch(n, ka, kb) doubles; tiles_dev: device room
+// for 256 GramTile.  8 x 4 tiles (SAIT_GRAM_TILE=88 for 8 x 8): fewer
+// registers, two CTAs per SM, the repeated column reads served by L2.
+void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
+          void* tiles_dev, cudaStream_t s, bool upper_only) {
+  static const int tile = [] {
+    const char* e = std::getenv("SAIT_GRAM_TILE");
+    return e ? std::atoi(e) : 84;
+  }();
+  if (tile == 88) gram_impl<8, 8>(n, A, ka, B, kb, G, ldg, scratch, tiles_dev, s, upper_only);
+  else gram_impl<8, 4>(n, A, ka, B, kb, G, ldg, scratch, tiles_dev, s, upper_only);
 }
 
 void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s) {

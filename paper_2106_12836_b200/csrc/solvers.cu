@@ -512,7 +512,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     auto next_small = [&] { return dsmall + static_cast<int64_t>(48 * 48) * (slot++ % kSlots); };
     sait::Scalars sc(n, 48 * 48, 64, s);
     double* gscratch = sait::dalloc<double>(sait::gram_scratch(n, 3 * k, 3 * k), s);
-    void* gtiles = sait::dalloc<long long>(64, s);
+    void* gtiles = sait::dalloc<long long>(256, s);
     double *X = S, *W = S + blk, *P = S + 2 * blk;
     double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
     auto block_spmv = [&](const double* in, double* out) { op.apply_block(in, out, k, s); };

@@ -272,10 +272,22 @@ def run_b200(args):
         r0, r1 = 0, n
         apply_dev = lambda r, z: pair.apply(r, z)  # noqa: E731
     else:
-        from paper_2106_12836_b200.dist import ShardedPair
+        from paper_2106_12836_b200.dist import PeerShardedPair, ShardedPair
 
-        sp = ShardedPair(ML.to_host(), MU.to_host(), rank, ws)
+        MLh, MUh = ML.to_host(), MU.to_host()
         ML.free(), MU.free()
+        sp = None
+        transport = args.transport
+        if transport == "peer":
+            # halos read over peer memory inside the SpMV; NCCL send/recv if the
+            # plan or the node does not allow it
+            try:
+                sp = PeerShardedPair.distributed(MLh, MUh, rank, ws)
+            except Exception as exc:  # noqa: BLE001
+                print(f"[bench] peer-memory halo unavailable ({exc}); using NCCL send/recv", file=sys.stderr)
+                transport = "nccl"
+        if sp is None:
+            sp = ShardedPair(MLh, MUh, rank, ws)
         r0, r1 = sp.own
         apply_dev = sp.apply
     nloc = r1 - r0
@@ -404,6 +416,7 @@ def run_b200(args):
         }
         if ws > 1:
             line["config"]["halo_bytes_per_apply_rank0"] = sp.halo_bytes
+            line["config"]["halo_transport"] = transport
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
@@ -416,6 +429,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: halo over peer memory inside the SpMV (default) or NCCL send/recv")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -195,6 +195,33 @@ int sait_operator_apply(sait_op_t op, const double *d_x, int64_t xlen, double *d
                         sait_stream_t stream);
 void sait_operator_destroy(sait_op_t op);
 
+/* Row block of a sharded factor whose halo is read straight from the
+ * neighbouring ranks' buffers (peer memory over NVLink): the
+ * extended vector is [halo below | own | halo above]; columns c < own_lo read
+ * lo_src[c + lo_shift], columns c >= own_hi read hi_src[c + hi_shift], after
+ * the owner's flag (*lo_flag / *hi_flag) reached `epoch` (system-scope
+ * acquire).  The local part of d_x_ext must already hold the own segment.
+ * Needs the SELL copy (SAIT_ERR_INVALID_ARGUMENT otherwise). */
+typedef struct {
+  int64_t own_lo, own_hi;
+  const double *lo_src;
+  int64_t lo_shift;
+  const double *hi_src;
+  int64_t hi_shift;
+  const int *lo_flag, *hi_flag;
+  int epoch;
+} sait_halo_t;
+int sait_operator_apply_halo(sait_op_t op, const double *d_x_ext, int64_t ext_len, const sait_halo_t *halo,
+                             double *d_y, int64_t ylen, sait_stream_t stream);
+/* *d_flag = epoch once everything queued before on `stream` has completed
+ * (system-scope release: peers polling the flag then see the data). */
+int sait_publish_epoch(int *d_flag, int epoch, sait_stream_t stream);
+/* CUDA IPC for buffers from sait_device_alloc: a 64-byte handle another
+ * process on the node opens to get a device pointer to the same memory. */
+int sait_ipc_handle(const void *d_ptr, void *handle64);
+int sait_ipc_open(const void *handle64, void **d_ptr);
+int sait_ipc_close(void *d_ptr);
+
 /* ------------------------------------------------ pair preconditioner ---
  * SaitPairPreconditioner (preconditioner.hpp:54-68, preconditioner.cpp:34-49). */
 

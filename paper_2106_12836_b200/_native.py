@@ -35,6 +35,22 @@ PD = C.POINTER(C.c_double)
 VP = C.c_void_p
 
 
+class Halo(C.Structure):
+    """sait_halo_t"""
+
+    _fields_ = [
+        ("own_lo", C.c_int64),
+        ("own_hi", C.c_int64),
+        ("lo_src", C.c_void_p),
+        ("lo_shift", C.c_int64),
+        ("hi_src", C.c_void_p),
+        ("hi_shift", C.c_int64),
+        ("lo_flag", C.c_void_p),
+        ("hi_flag", C.c_void_p),
+        ("epoch", C.c_int),
+    ]
+
+
 class HostCsr(C.Structure):
     _fields_ = [
         ("nrows", C.c_int64),
@@ -103,6 +119,11 @@ PROTOTYPES = {
     "sait_operator_create": (C.c_int, [VP, C.c_int, C.POINTER(VP)]),
     "sait_operator_apply": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
     "sait_operator_destroy": (None, [VP]),
+    "sait_operator_apply_halo": (C.c_int, [VP, VP, C.c_int64, C.POINTER(Halo), VP, C.c_int64, VP]),
+    "sait_publish_epoch": (C.c_int, [VP, C.c_int, VP]),
+    "sait_ipc_handle": (C.c_int, [VP, VP]),
+    "sait_ipc_open": (C.c_int, [VP, C.POINTER(VP)]),
+    "sait_ipc_close": (C.c_int, [VP]),
     "sait_jacobi_split": (C.c_int, [VP, C.c_int, VP, VP, C.POINTER(VP)]),
     "sait_build": (C.c_int, [VP, C.c_int, C.POINTER(DropSpec), VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_polynomial": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(BuildStats)]),

@@ -1047,6 +1047,72 @@ int sait_operator_apply(sait_op_t op, const double* d_x, int64_t xlen, double* d
   });
 }
 
+int sait_operator_apply_halo(sait_op_t op, const double* d_x_ext, int64_t ext_len, const sait_halo_t* halo,
+                             double* d_y, int64_t ylen, sait_stream_t stream) {
+  return guarded([&] {
+    need(op, "spmv_halo");
+    need(halo, "spmv_halo(halo)");
+    const sait::DevCsr& m = op->a->m;
+    if (ext_len != m.ncols)
+      sait::throw_invalid("spmv: vector length " + std::to_string(ext_len) + " does not match ncols " +
+                          std::to_string(m.ncols));
+    if (ylen != m.nrows) sait::throw_invalid("spmv: output length mismatch");
+    if (!op->sell.ok()) sait::throw_invalid("spmv_halo: the operator has no SELL copy");
+    if (halo->own_lo < 0 || halo->own_hi > ext_len || halo->own_lo > halo->own_hi)
+      sait::throw_invalid("spmv_halo: own segment outside the extended vector");
+    if ((halo->own_lo > 0 && (!halo->lo_src || !halo->lo_flag)) ||
+        (halo->own_hi < ext_len && (!halo->hi_src || !halo->hi_flag)))
+      sait::throw_invalid("spmv_halo: halo source missing");
+    DeviceGuard g(op->dev);
+    sait::HaloArgs h;
+    h.own_lo = halo->own_lo;
+    h.own_hi = halo->own_hi;
+    h.lo_src = halo->lo_src;
+    h.lo_shift = halo->lo_shift;
+    h.hi_src = halo->hi_src;
+    h.hi_shift = halo->hi_shift;
+    h.lo_flag = halo->lo_flag;
+    h.hi_flag = halo->hi_flag;
+    h.epoch = halo->epoch;
+    sait::sell_spmv_halo(op->sell, d_x_ext, h, d_y, sait::as_stream(stream));
+  });
+}
+
+int sait_publish_epoch(int* d_flag, int epoch, sait_stream_t stream) {
+  return guarded([&] {
+    need(d_flag, "publish_epoch");
+    sait::publish_epoch(d_flag, epoch, sait::as_stream(stream));
+  });
+}
+
+int sait_ipc_handle(const void* d_ptr, void* handle64) {
+  return guarded([&] {
+    need(d_ptr, "ipc_handle");
+    need(handle64, "ipc_handle(out)");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    SAIT_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    std::memcpy(handle64, &h, sizeof h);
+  });
+}
+
+int sait_ipc_open(const void* handle64, void** d_ptr) {
+  return guarded([&] {
+    need(handle64, "ipc_open");
+    need(d_ptr, "ipc_open(out)");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    SAIT_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int sait_ipc_close(void* d_ptr) {
+  return guarded([&] {
+    need(d_ptr, "ipc_close");
+    SAIT_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  });
+}
+
 void sait_operator_destroy(sait_op_t op) {
   if (!op) return;
   int prev = -1;

@@ -209,6 +209,19 @@ void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const Dataf
                          int* in_flag, int epoch, const double* r_host, double* r_dev, double* y, double* z_host,
                          cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
+// row block of a sharded factor reading its halo from peer buffers (sell.cu)
+struct HaloArgs {
+  int64_t own_lo = 0, own_hi = 0;  // ext columns [own_lo, own_hi) are local
+  const double* lo_src = nullptr;  // x[c] = lo_src[c + lo_shift] for c < own_lo
+  int64_t lo_shift = 0;
+  const double* hi_src = nullptr;  // x[c] = hi_src[c + hi_shift] for c >= own_hi
+  int64_t hi_shift = 0;
+  const int* lo_flag = nullptr;    // the owners' published epochs
+  const int* hi_flag = nullptr;
+  int epoch = 0;
+};
+void sell_spmv_halo(const SellMatrix& m, const double* x_ext, const HaloArgs& h, double* y, cudaStream_t s);
+void publish_epoch(int* flag, int epoch, cudaStream_t s);
 // rows [row0, row1) only (row0 a multiple of 32)
 void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s,
                     bool pdl = false);  // pdl: programmatic dependent of the previous kernel on s

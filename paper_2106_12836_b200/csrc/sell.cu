@@ -329,6 +329,96 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
   }
 }
 
+// ---------------------------------------------------------------- peer halo
+// y = A x_ext on a row block of a sharded factor, where the extended vector
+// is [halo below | own | halo above] and the halo entries are read straight
+// from the neighbouring ranks' buffers (peer memory over NVLink) instead of
+// being exchanged first: the transfer overlaps the math slice by slice.  A
+// warp whose slice touches a halo column first waits (acquire, system scope)
+// until the owner has published this epoch's values; warps of interior slices
+// never wait.  A wait longer than 20 s traps (a peer that died) instead of
+// hanging.
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+  double r;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void wait_epoch_sys(const int* flag, int epoch) {
+  if (ld_acquire_sys(flag) - epoch >= 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  unsigned ns = 64;
+  while (ld_acquire_sys(flag) - epoch < 0) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+}
+
+template <class IDX>
+__global__ void __launch_bounds__(256) sell_spmv_halo_kernel(int64_t n, int64_t nslices,
+                                                              const int64_t* __restrict__ soff, IDX idx,
+                                                              const double* __restrict__ sval,
+                                                              const double* __restrict__ x, double* __restrict__ y,
+                                                              HaloArgs h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int64_t base = soff[s];
+  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  const int64_t e0 = base + lane;
+  const int64_t i0 = idx.slice_base(s, base) + lane;
+  bool lo_ready = false, hi_ready = false;
+  double acc = 0.0;
+  for (int32_t k0 = 0; k0 < w; k0 += 8) {
+    int32_t c[8];
+    double v[8];
+    bool lo = false, hi = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = -1;
+      v[j] = 0.0;
+      if (k0 + j < w) {
+        c[j] = idx.col(i0 + static_cast<int64_t>(k0 + j) * kSlice, row);
+        v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
+        lo |= c[j] >= 0 && c[j] < h.own_lo;
+        hi |= c[j] >= h.own_hi;
+      }
+    }
+    if (!lo_ready && __any_sync(0xffffffffu, lo)) {
+      wait_epoch_sys(h.lo_flag, h.epoch);
+      lo_ready = true;
+    }
+    if (!hi_ready && __any_sync(0xffffffffu, hi)) {
+      wait_epoch_sys(h.hi_flag, h.epoch);
+      hi_ready = true;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (c[j] < 0) continue;
+      const double xv = c[j] < h.own_lo  ? ld_relaxed_sys(h.lo_src + (c[j] + h.lo_shift))
+                        : c[j] >= h.own_hi ? ld_relaxed_sys(h.hi_src + (c[j] + h.hi_shift))
+                                           : __ldg(x + c[j]);
+      acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
+    }
+  }
+  if (row < n) y[row] = acc;
+}
+
+// flag = epoch, ordered after everything queued before it on the stream
+__global__ void publish_epoch_kernel(int* flag, int epoch) {
+  asm volatile("fence.sc.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
 unsigned sell_grid(int64_t nslices) {  // one slice per warp, 8 warps per CTA
   return static_cast<unsigned>(std::max<int64_t>(1, (nslices + 7) / 8));
 }
@@ -1072,6 +1162,24 @@ void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const doubl
     if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, true>, m.n, s0, s1, m.soff, ix, m.val, x, y));
     else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, false>, m.n, s0, s1, m.soff, ix, m.val, x, y));
   }
+  SAIT_LAUNCHED();
+}
+
+void sell_spmv_halo(const SellMatrix& m, const double* x_ext, const HaloArgs& h, double* y, cudaStream_t s) {
+  if (m.nslices == 0) return;
+  const unsigned grid = sell_grid(m.nslices);
+  if (m.dict)
+    sell_spmv_halo_kernel<IdxDict><<<grid, 256, 0, s>>>(m.n, m.nslices, m.soff, IdxDict{m.pat, m.dict}, m.val, x_ext,
+                                                         y, h);
+  else if (m.dcol)
+    sell_spmv_halo_kernel<Idx16><<<grid, 256, 0, s>>>(m.n, m.nslices, m.soff, Idx16{m.dcol}, m.val, x_ext, y, h);
+  else
+    sell_spmv_halo_kernel<Idx32><<<grid, 256, 0, s>>>(m.n, m.nslices, m.soff, Idx32{m.col}, m.val, x_ext, y, h);
+  SAIT_LAUNCHED();
+}
+
+void publish_epoch(int* flag, int epoch, cudaStream_t s) {
+  publish_epoch_kernel<<<1, 1, 0, s>>>(flag, epoch);
   SAIT_LAUNCHED();
 }
 

@@ -227,3 +227,196 @@ def _allreduce_max(group):
         return int(t.item())
 
     return red
+
+
+class _DevBuf:
+    """A device buffer from sait_device_alloc (plain cudaMalloc, so CUDA IPC
+    can export it), viewable as a torch tensor via __cuda_array_interface__."""
+
+    def __init__(self, nbytes: int, ptr: int | None = None, owned: bool = True):
+        from . import _native as N
+
+        self.nbytes = nbytes
+        self.owned = owned and ptr is None
+        if ptr is None:
+            p = C.c_void_p()
+            N.check(N.lib.sait_device_alloc(nbytes, C.byref(p)))
+            ptr = p.value
+        self.ptr = ptr
+
+    def tensor(self, offset_bytes: int, count: int, dtype: str = "<f8"):
+        import torch
+
+        itemsize = 8 if dtype == "<f8" else 4
+        iface = {"shape": (count,), "typestr": dtype, "data": (self.ptr + offset_bytes, False), "version": 3,
+                 "strides": None}
+        holder = type("CudaArray", (), {"__cuda_array_interface__": iface})()
+        del itemsize
+        return torch.as_tensor(holder, device="cuda")
+
+    def handle(self) -> bytes:
+        from . import _native as N
+
+        h = (C.c_char * 64)()
+        N.check(N.lib.sait_ipc_handle(C.c_void_p(self.ptr), h))
+        return bytes(h)
+
+    def free(self):
+        from . import _native as N
+
+        if self.owned and self.ptr:
+            N.lib.sait_device_free(C.c_void_p(self.ptr))
+        self.ptr = 0
+
+
+def _open_ipc(handle: bytes) -> int:
+    from . import _native as N
+
+    p = C.c_void_p()
+    N.check(N.lib.sait_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)))
+    return p.value
+
+
+class PeerShardedPair:
+    """Row-sharded z = M_U (M_L r) with no collective on the data path: each
+    rank's SpMV reads its halo straight from the neighbours' extended vectors
+    (sait_operator_apply_halo over peer memory / NVLink), after the owner
+    published the epoch (sait_publish_epoch).  Per factor every rank owns two
+    parity copies of its extended vector [halo | own | halo] plus an epoch
+    flag in one IPC-exportable allocation; an apply writes the own segment of
+    copy (epoch & 1), so a neighbour still reading epoch e never sees e + 1's
+    values (a rank cannot run two epochs ahead: each apply also needs its
+    neighbours' values of the same epoch).
+
+    ``resolve(rank, factor) -> device address`` gives another rank's buffer
+    base: IPC-opened in a multi-process job (``distributed``), or the plain
+    pointer when several ranks live in one process (the single-GPU test).
+    Raises NotImplementedError when a halo spans more than one peer per side
+    (use ShardedPair)."""
+
+    def __init__(self, ML, MU, rank: int, world: int, resolve=None):
+        n = ML.nrows
+        if not (ML.ncols == n and MU.nrows == n and MU.ncols == n):
+            raise ValueError("PeerShardedPair: square factors of equal order required")
+        self.n, self.rank, self.world = n, rank, world
+        self.bounds = row_bounds(n, world)
+        self.plans = []
+        for M in (ML, MU):
+            spans = [column_span(M.row_ptr, M.col_idx, self.bounds[q], self.bounds[q + 1]) for q in range(world)]
+            allp = make_plans(spans, self.bounds)
+            for p in allp:
+                below = [x for x in p.recv if x[2] <= p.own[0]]
+                above = [x for x in p.recv if x[1] >= p.own[1]]
+                if len(below) > 1 or len(above) > 1:
+                    raise NotImplementedError("PeerShardedPair: a halo spans several ranks")
+            self.plans.append(allp)
+        r0, r1 = self.bounds[rank], self.bounds[rank + 1]
+        self.own = (r0, r1)
+        self.ops, self.bufs = [], []
+        for f, M in enumerate((ML, MU)):
+            p = self.plans[f][rank]
+            self.ops.append(DeviceOperator(local_block(M.row_ptr, M.col_idx, M.values, r0, r1, p.lo, p.ext_len)))
+            self.bufs.append(_DevBuf(self._buf_bytes(f, rank)))
+            self.bufs[f].tensor(self._flag_off(f, rank), 1, "<i4").zero_()
+        self.resolve = resolve
+        self.epoch = 0
+        self.halo_bytes = 8 * sum(g1 - g0 for f in range(2) for _, g0, g1 in self.plans[f][rank].recv)
+
+    # layout of rank q's buffer for factor f: [ext parity 0 | ext parity 1 | flag]
+    def _ext_len(self, f, q):
+        return self.plans[f][q].ext_len
+
+    def _buf_bytes(self, f, q):
+        return 16 * self._ext_len(f, q) + 256
+
+    def _flag_off(self, f, q):
+        return 16 * self._ext_len(f, q) + 128
+
+    def _halo(self, f, epoch):
+        from . import _native as N
+
+        p = self.plans[f][self.rank]
+        par = epoch & 1
+        h = N.Halo()
+        h.own_lo, h.own_hi = p.own[0] - p.lo, p.own[1] - p.lo
+        h.epoch = epoch
+        for peer, g0, g1 in p.recv:
+        # the peer's extended vector of the same parity; global g sits at g - lo_peer
+            pq = self.plans[f][peer]
+            base = self.resolve(peer, f) + 8 * par * pq.ext_len
+            flag = self.resolve(peer, f) + self._flag_off(f, peer)
+            if g1 <= p.own[0]:
+                h.lo_src, h.lo_shift, h.lo_flag = base, p.lo - pq.lo, flag
+            else:
+                h.hi_src, h.hi_shift, h.hi_flag = base, p.lo - pq.lo, flag
+        return h
+
+    def _ext(self, f, par):
+        return self.bufs[f].tensor(8 * par * self._ext_len(f, self.rank), self._ext_len(f, self.rank))
+
+    def _own(self, f, par):
+        p = self.plans[f][self.rank]
+        return self._ext(f, par)[p.own_offset : p.own_offset + (self.own[1] - self.own[0])]
+
+    def _publish(self, f, epoch, s):
+        from . import _native as N
+
+        flag = self.bufs[f].ptr + self._flag_off(f, self.rank)
+        N.check(N.lib.sait_publish_epoch(C.c_void_p(flag), int(epoch), s))
+
+    def _spmv(self, f, epoch, out, s):
+        from . import _native as N
+
+        x = self._ext(f, epoch & 1)
+        h = self._halo(f, epoch)
+        N.check(N.lib.sait_operator_apply_halo(self.ops[f]._h, x.data_ptr(), x.numel(), C.byref(h), out.data_ptr(),
+                                               out.numel(), s))
+
+    # the apply in three stages (a multi-rank single-process test interleaves them)
+    def stage_input(self, r_local, epoch, s):
+        self._own(0, epoch & 1).copy_(r_local)
+        self._publish(0, epoch, s)
+
+    def stage_lower(self, epoch, s):
+        self._spmv(0, epoch, self._own(1, epoch & 1), s)  # y lands in M_U's extended vector
+        self._publish(1, epoch, s)
+
+    def stage_upper(self, z_local, epoch, s):
+        self._spmv(1, epoch, z_local, s)
+
+    def apply(self, r_local, z_local, stream=None) -> None:
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        self.epoch += 1
+        self.stage_input(r_local, self.epoch, s)
+        self.stage_lower(self.epoch, s)
+        self.stage_upper(z_local, self.epoch, s)
+
+    @classmethod
+    def distributed(cls, ML, MU, rank: int, world: int, group=None):
+        """Multi-process construction: the ranks swap IPC handles of their
+        buffers (torch.distributed all_gather_object) and open their peers'."""
+        import torch.distributed as dist
+
+        obj = cls(ML, MU, rank, world, resolve=None)
+        mine = [obj.bufs[0].handle(), obj.bufs[1].handle()]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        opened = {}
+        for f in range(2):
+            for peer, _, _ in obj.plans[f][rank].recv:
+                opened[(peer, f)] = _open_ipc(allh[peer][f])
+        obj._opened = opened
+        obj.resolve = lambda q, f: obj.bufs[f].ptr if q == rank else opened[(q, f)]
+        dist.barrier(group=group)
+        return obj
+
+    def close(self):
+        from . import _native as N
+
+        for p in getattr(self, "_opened", {}).values():
+            N.lib.sait_ipc_close(C.c_void_p(p))
+        self._opened = {}
+        for b in self.bufs:
+            b.free()

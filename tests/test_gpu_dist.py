@@ -150,3 +150,109 @@ def test_build_sharded_two_processes(tmp_path, S, port):
     assert steps == [nsteps, nsteps]
     assert np.array_equal(m.indptr, expect.row_ptr) and np.array_equal(m.indices, expect.col_idx)
     assert bitwise_equal(m.data, expect.values)
+
+
+@pytest.mark.parametrize("world,grid", [(2, 24), (3, 20), (4, 16)])
+def test_peer_sharded_pair_virtual_ranks(S, port, world, grid):
+    """PeerShardedPair's data path on one GPU: `world` ranks in one process,
+    each reading its halo from the other ranks' buffers inside the SpMV.  The
+    stages run rank by rank on one stream, so every flag a kernel waits on is
+    already published (no cross-rank waiting on one GPU).  Three epochs
+    exercise both parity copies; each rank's z rows equal the oracle's."""
+    import torch
+
+    from helpers import to_oracle
+    from paper_2106_12836_b200.dist import PeerShardedPair
+
+    A = S.laplacian_3d(grid)
+    f = S.ilu_k(A, 0)
+    ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
+    MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
+    ranks = {}
+    resolve = lambda q, fac: ranks[q].bufs[fac].ptr  # noqa: E731
+    for q in range(world):
+        ranks[q] = PeerShardedPair(ML, MU, q, world, resolve=resolve)
+    s = torch.cuda.current_stream().cuda_stream
+    for epoch in (1, 2, 3):
+        r = S.uniform_pm1(100 + epoch, A.nrows)
+        want = port.pair_apply(to_oracle(ML), to_oracle(MU), r)
+        rd = torch.from_numpy(r).cuda()
+        zs = {}
+        for q in range(world):
+            a, b = ranks[q].own
+            ranks[q].stage_input(rd[a:b], epoch, s)
+        for q in range(world):
+            ranks[q].stage_lower(epoch, s)
+        for q in range(world):
+            a, b = ranks[q].own
+            zs[q] = torch.empty(b - a, dtype=torch.float64, device="cuda")
+            ranks[q].stage_upper(zs[q], epoch, s)
+        torch.cuda.synchronize()
+        z = torch.cat([zs[q] for q in range(world)]).cpu().numpy()
+        assert bitwise_equal(z, want), epoch
+    assert all(ranks[q].halo_bytes > 0 for q in range(world))
+    for q in range(world):
+        ranks[q].close()
+
+
+def test_peer_sharded_pair_world1(S, golden):
+    """One rank: no halo, apply() equals the pair."""
+    import torch
+
+    from paper_2106_12836_b200.dist import PeerShardedPair
+
+    ML, MU = to_product(golden_csr(golden, "c1/ML")), to_product(golden_csr(golden, "c1/MU"))
+    P = PeerShardedPair(ML, MU, 0, 1, resolve=lambda q, f: None)
+    r = torch.from_numpy(golden["c1/r"]).cuda()
+    z = torch.empty_like(r)
+    for _ in range(2):
+        P.apply(r, z)
+    torch.cuda.synchronize()
+    assert bitwise_equal(z.cpu().numpy(), golden["c1/z"])
+    P.close()
+
+
+def _ipc_worker(rank, world, port, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2106_12836_b200.dist import _DevBuf, _open_ipc
+        from paper_2106_12836_b200 import _native as N
+
+        n = 1 << 16
+        buf = _DevBuf(8 * n + 256)
+        buf.tensor(0, n).copy_(torch.arange(n, dtype=torch.float64, device="cuda") * (rank + 1))
+        torch.cuda.synchronize()
+        handles = [None] * world
+        dist.all_gather_object(handles, buf.handle())
+        peer = (rank + 1) % world
+        ptr = _open_ipc(handles[peer])
+        view = _DevBuf(8 * n, ptr=ptr, owned=False).tensor(0, n)
+        got = view.cpu().numpy()
+        dist.barrier()
+        N.check(N.lib.sait_ipc_close(C.c_void_p(ptr)))
+        np.save(os.path.join(out_dir, f"ipc{rank}.npy"), got)
+        dist.barrier()
+        buf.free()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_handles_two_processes(tmp_path):
+    """The IPC plumbing of PeerShardedPair.distributed: each process exports a
+    sait_device_alloc buffer, opens its peer's and reads the peer's values
+    (two processes on one GPU; nothing waits on the other process's kernels)."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_ipc_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    n = 1 << 16
+    for q in range(2):
+        got = np.load(tmp_path / f"ipc{q}.npy")
+        assert np.array_equal(got, np.arange(n, dtype=np.float64) * (((q + 1) % 2) + 1))

@@ -308,6 +308,28 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
                 double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
                 sait_stream_t stream);
 
+/* Vector primitives of those loops, for solver loops driven across ranks
+ * (the same kernels, so the same bits).  Dots: `sait_dot_partials` writes the
+ * canonical per-2048-element-block partials of x . V_j (partials[j * nb + b],
+ * nb = sait_dot_blocks(n)); `sait_dot_fold` folds nb partials per dot in the
+ * canonical order (sqrt_out: square root of the result).  A row-sharded vector
+ * aligned to 2048-element blocks gives each rank a contiguous run of the
+ * global blocks, so folding every rank's partials reproduces the single-GPU
+ * dot bitwise.  vec_update op: 0 y = y + a x, 1 y = x + a y, 2 y = x - y,
+ * 3 y = y + x.  vec_cgs: w = w - sum_j h_j V_j (j ascending); vec_div:
+ * out = w / d[0]; vec_lincomb: u = sum_j y_j V_j.  h, d, y are device. */
+int64_t sait_dot_blocks(int64_t n);
+int sait_dot_partials(const double *d_x, const double *d_V, int64_t ld, int m, int64_t n, double *d_partials,
+                      sait_stream_t stream);
+int sait_dot_fold(const double *d_partials, int64_t nb, int m, double *d_out, int sqrt_out,
+                  sait_stream_t stream);
+int sait_vec_update(int op, int64_t n, double a, const double *d_x, double *d_y, sait_stream_t stream);
+int sait_vec_cgs(int64_t n, double *d_w, const double *d_V, int64_t ld, int m, const double *d_h,
+                 sait_stream_t stream);
+int sait_vec_div(int64_t n, const double *d_w, const double *d_d, double *d_out, sait_stream_t stream);
+int sait_vec_lincomb(int64_t n, const double *d_V, int64_t ld, int k, const double *d_y, double *d_u,
+                     sait_stream_t stream);
+
 /* ----------------------------------------------------- inputs (host) ---
  * Producers of the path's inputs.  ilu_k is ilu.hpp:27 / ilu.cpp:98-173
  * (bitwise identical factors); the generators fix BASELINE.json's synthetic

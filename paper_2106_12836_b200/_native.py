@@ -150,6 +150,13 @@ PROTOTYPES = {
     "sait_gmres": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_pcg": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_gmres_exact": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
+    "sait_dot_blocks": (C.c_int64, [C.c_int64]),
+    "sait_dot_partials": (C.c_int, [VP, VP, C.c_int64, C.c_int, C.c_int64, VP, VP]),
+    "sait_dot_fold": (C.c_int, [VP, C.c_int64, C.c_int, VP, C.c_int, VP]),
+    "sait_vec_update": (C.c_int, [C.c_int, C.c_int64, C.c_double, VP, VP, VP]),
+    "sait_vec_cgs": (C.c_int, [C.c_int64, VP, VP, C.c_int64, C.c_int, VP, VP]),
+    "sait_vec_div": (C.c_int, [C.c_int64, VP, VP, VP, VP]),
+    "sait_vec_lincomb": (C.c_int, [C.c_int64, VP, C.c_int64, C.c_int, VP, VP, VP]),
     "sait_pcg_exact": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_lobpcg": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int), VP]),
     "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),

@@ -391,6 +391,24 @@ void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t
   SAIT_LAUNCHED();
 }
 
+// Block partials / fold of multi_dot separately, for reductions across ranks
+// (a row-sharded vector aligned to 2048-element blocks gives each rank a
+// contiguous run of the global blocks; folding all ranks' partials in order
+// reproduces the single-device value bit for bit).
+void dot_partials(int64_t n, const double* x, const double* V, int64_t ld, int m, double* part, cudaStream_t s) {
+  const int64_t nb = dot_blocks(n);
+  for (int j0 = 0; j0 < m; j0 += kMaxM) {
+    const int mm = m - j0 < kMaxM ? m - j0 : kMaxM;
+    mdot_partials<<<static_cast<unsigned>(nb), kT, 0, s>>>(n, x, V + ld * j0, ld, mm, part + nb * j0, nb);
+    SAIT_LAUNCHED();
+  }
+}
+void dot_fold(const double* part, int64_t nb, int m, double* out, bool sqrt_out, cudaStream_t s) {
+  if (m <= 0) return;
+  mdot_final<<<m, kT, 0, s>>>(part, nb, out, sqrt_out ? 1 : 0);
+  SAIT_LAUNCHED();
+}
+
 void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, double* out, double* scratch,
                cudaStream_t s, bool sqrt_out) {
   const int64_t nb = dot_blocks(n);

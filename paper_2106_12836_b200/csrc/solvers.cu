@@ -24,6 +24,8 @@ void exact_apply_internal(sait_exact_t e, const double* r, double* z, cudaStream
 int64_t exact_dim(sait_exact_t e);
 
 int64_t dot_blocks(int64_t n);
+void dot_partials(int64_t n, const double* x, const double* V, int64_t ld, int m, double* part, cudaStream_t s);
+void dot_fold(const double* part, int64_t nb, int m, double* out, bool sqrt_out, cudaStream_t s);
 void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, double* out, double* scratch,
                cudaStream_t s, bool sqrt_out);
 void cgs_subtract(int64_t n, double* w, const double* V, int64_t ld, int m, const double* h, cudaStream_t s);
@@ -667,6 +669,61 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     SAIT_CUDA(cudaStreamSynchronize(s));
     if (dev != A->dev) cudaSetDevice(dev);
     if (failed) sait::throw_runtime(why);
+  });
+}
+
+// ---- vector primitives of the solver loops (for loops that run across
+// ranks; identical kernels, so identical bits)
+int64_t sait_dot_blocks(int64_t n) { return sait::dot_blocks(n); }
+
+int sait_dot_partials(const double* d_x, const double* d_V, int64_t ld, int m, int64_t n, double* d_partials,
+                      sait_stream_t stream) {
+  return solver_guard([&] {
+    if (m < 0 || n < 0 || (m > 0 && (!d_x || !d_V || !d_partials))) sait::throw_invalid("dot_partials: bad arguments");
+    if (m == 0 || n == 0) return;
+    sait::dot_partials(n, d_x, d_V, ld, m, d_partials, sait::as_stream(stream));
+  });
+}
+
+int sait_dot_fold(const double* d_partials, int64_t nb, int m, double* d_out, int sqrt_out, sait_stream_t stream) {
+  return solver_guard([&] {
+    if (m < 0 || nb < 1 || (m > 0 && (!d_partials || !d_out))) sait::throw_invalid("dot_fold: bad arguments");
+    sait::dot_fold(d_partials, nb, m, d_out, sqrt_out != 0, sait::as_stream(stream));
+  });
+}
+
+int sait_vec_update(int op, int64_t n, double a, const double* d_x, double* d_y, sait_stream_t stream) {
+  return solver_guard([&] {
+    if (n < 0 || (n > 0 && (!d_x || !d_y))) sait::throw_invalid("vec_update: bad arguments");
+    if (n == 0) return;
+    cudaStream_t s = sait::as_stream(stream);
+    switch (op) {
+      case 0: sait::axpy(n, a, d_x, d_y, s); break;      // y = y + a x
+      case 1: sait::xpay(n, d_x, a, d_y, s); break;      // y = x + a y
+      case 2: sait::x_minus_y(n, d_x, d_y, s); break;    // y = x - y
+      case 3: sait::y_plus_x(n, d_x, d_y, s); break;     // y = y + x
+      default: sait::throw_invalid("vec_update: unknown op");
+    }
+  });
+}
+
+int sait_vec_cgs(int64_t n, double* d_w, const double* d_V, int64_t ld, int m, const double* d_h,
+                 sait_stream_t stream) {
+  return solver_guard([&] {
+    if (n > 0 && m > 0) sait::cgs_subtract(n, d_w, d_V, ld, m, d_h, sait::as_stream(stream));
+  });
+}
+
+int sait_vec_div(int64_t n, const double* d_w, const double* d_d, double* d_out, sait_stream_t stream) {
+  return solver_guard([&] {
+    if (n > 0) sait::divide_by(n, d_w, d_d, d_out, sait::as_stream(stream));
+  });
+}
+
+int sait_vec_lincomb(int64_t n, const double* d_V, int64_t ld, int k, const double* d_y, double* d_u,
+                     sait_stream_t stream) {
+  return solver_guard([&] {
+    if (n > 0 && k > 0) sait::linear_combination(n, d_V, ld, k, d_y, d_u, sait::as_stream(stream));
   });
 }
 

@@ -294,12 +294,12 @@ class PeerShardedPair:
     Raises NotImplementedError when a halo spans more than one peer per side
     (use ShardedPair)."""
 
-    def __init__(self, ML, MU, rank: int, world: int, resolve=None):
+    def __init__(self, ML, MU, rank: int, world: int, resolve=None, align: int = GROUP_ROWS):
         n = ML.nrows
         if not (ML.ncols == n and MU.nrows == n and MU.ncols == n):
             raise ValueError("PeerShardedPair: square factors of equal order required")
         self.n, self.rank, self.world = n, rank, world
-        self.bounds = row_bounds(n, world)
+        self.bounds = row_bounds(n, world, align)
         self.plans = []
         for M in (ML, MU):
             spans = [column_span(M.row_ptr, M.col_idx, self.bounds[q], self.bounds[q + 1]) for q in range(world)]
@@ -394,12 +394,12 @@ class PeerShardedPair:
         self.stage_upper(z_local, self.epoch, s)
 
     @classmethod
-    def distributed(cls, ML, MU, rank: int, world: int, group=None):
+    def distributed(cls, ML, MU, rank: int, world: int, group=None, align: int = GROUP_ROWS):
         """Multi-process construction: the ranks swap IPC handles of their
         buffers (torch.distributed all_gather_object) and open their peers'."""
         import torch.distributed as dist
 
-        obj = cls(ML, MU, rank, world, resolve=None)
+        obj = cls(ML, MU, rank, world, resolve=None, align=align)
         mine = [obj.bufs[0].handle(), obj.bufs[1].handle()]
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
@@ -420,3 +420,85 @@ class PeerShardedPair:
         self._opened = {}
         for b in self.bufs:
             b.free()
+
+
+class PeerRowOperator:
+    """Row block of one sharded matrix, y_local = (A x)_local, with the halo
+    of x read from the neighbours' buffers inside the SpMV (the single-matrix
+    form of PeerShardedPair: the system matrix of a sharded solver loop)."""
+
+    def __init__(self, A, rank: int, world: int, resolve=None, align: int = GROUP_ROWS):
+        n = A.nrows
+        if A.ncols != n:
+            raise ValueError("PeerRowOperator: square matrix required")
+        self.n, self.rank, self.world = n, rank, world
+        self.bounds = row_bounds(n, world, align)
+        spans = [column_span(A.row_ptr, A.col_idx, self.bounds[q], self.bounds[q + 1]) for q in range(world)]
+        self.plans = make_plans(spans, self.bounds)
+        for p in self.plans:
+            if len([x for x in p.recv if x[2] <= p.own[0]]) > 1 or len([x for x in p.recv if x[1] >= p.own[1]]) > 1:
+                raise NotImplementedError("PeerRowOperator: a halo spans several ranks")
+        r0, r1 = self.bounds[rank], self.bounds[rank + 1]
+        if r1 <= r0:
+            raise ValueError(f"PeerRowOperator: rank {rank} owns no rows (n={n}, world={world}, align={align})")
+        self.own = (r0, r1)
+        p = self.plans[rank]
+        self.op = DeviceOperator(local_block(A.row_ptr, A.col_idx, A.values, r0, r1, p.lo, p.ext_len))
+        self.buf = _DevBuf(16 * p.ext_len + 256)
+        self.buf.tensor(16 * p.ext_len + 128, 1, "<i4").zero_()
+        self.resolve = resolve
+        self.epoch = 0
+
+    def _flag_off(self, q):
+        return 16 * self.plans[q].ext_len + 128
+
+    def _ext(self, par):
+        p = self.plans[self.rank]
+        return self.buf.tensor(8 * par * p.ext_len, p.ext_len)
+
+    def stage_input(self, x_local, epoch, s):
+        from . import _native as N
+
+        p = self.plans[self.rank]
+        self._ext(epoch & 1)[p.own_offset : p.own_offset + (self.own[1] - self.own[0])].copy_(x_local)
+        N.check(N.lib.sait_publish_epoch(C.c_void_p(self.buf.ptr + self._flag_off(self.rank)), int(epoch), s))
+
+    def stage_spmv(self, y_local, epoch, s):
+        from . import _native as N
+
+        p = self.plans[self.rank]
+        par = epoch & 1
+        h = N.Halo()
+        h.own_lo, h.own_hi, h.epoch = p.own[0] - p.lo, p.own[1] - p.lo, epoch
+        for peer, g0, g1 in p.recv:
+            pq = self.plans[peer]
+            base = self.resolve(peer) + 8 * par * pq.ext_len
+            flag = self.resolve(peer) + self._flag_off(peer)
+            if g1 <= p.own[0]:
+                h.lo_src, h.lo_shift, h.lo_flag = base, p.lo - pq.lo, flag
+            else:
+                h.hi_src, h.hi_shift, h.hi_flag = base, p.lo - pq.lo, flag
+        x = self._ext(par)
+        N.check(N.lib.sait_operator_apply_halo(self.op._h, x.data_ptr(), x.numel(), C.byref(h), y_local.data_ptr(),
+                                               y_local.numel(), s))
+
+    @classmethod
+    def distributed(cls, A, rank: int, world: int, group=None, align: int = GROUP_ROWS):
+        import torch.distributed as dist
+
+        obj = cls(A, rank, world, resolve=None, align=align)
+        allh = [None] * world
+        dist.all_gather_object(allh, obj.buf.handle(), group=group)
+        opened = {peer: _open_ipc(allh[peer]) for peer, _, _ in obj.plans[rank].recv}
+        obj._opened = opened
+        obj.resolve = lambda q: obj.buf.ptr if q == rank else opened[q]
+        dist.barrier(group=group)
+        return obj
+
+    def close(self):
+        from . import _native as N
+
+        for p in getattr(self, "_opened", {}).values():
+            N.lib.sait_ipc_close(C.c_void_p(p))
+        self._opened = {}
+        self.buf.free()

@@ -115,3 +115,37 @@ def test_sharded_apply_long_range_halo(tmp_path, port):
     r = O.uniform_pm1(3, 2000)
     z = _run(tmp_path, ML, MU, r, 4)
     assert bitwise_equal(z, port.pair_apply(ML, MU, r))
+
+
+def _gather_worker(rank, world, port, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2106_12836_b200.dist_solvers import TorchComm
+
+        nb = 3 + 2 * rank  # ragged: the last rank of a sharded vector has fewer blocks
+        mine = torch.arange(2 * nb, dtype=torch.float64).reshape(2, nb) + 100 * rank
+        got = TorchComm(world).gather([mine])
+        np.save(os.path.join(out_dir, f"g{rank}.npy"), torch.cat(got, dim=1).numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torchcomm_gathers_ragged_partials_in_rank_order(tmp_path):
+    """dist_solvers.TorchComm: every rank receives all ranks' dot partials in
+    rank order with their own lengths (the fold then matches one device)."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_gather_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True,
+                       start_method="spawn")
+    want = np.concatenate([np.arange(2 * (3 + 2 * q), dtype=np.float64).reshape(2, -1) + 100 * q for q in range(3)],
+                          axis=1)
+    for q in range(3):
+        assert np.array_equal(np.load(tmp_path / f"g{q}.npy"), want)

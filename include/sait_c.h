@@ -329,6 +329,26 @@ int sait_vec_cgs(int64_t n, double *d_w, const double *d_V, int64_t ld, int m, c
 int sait_vec_div(int64_t n, const double *d_w, const double *d_d, double *d_out, sait_stream_t stream);
 int sait_vec_lincomb(int64_t n, const double *d_V, int64_t ld, int k, const double *d_y, double *d_u,
                      sait_stream_t stream);
+/* LOBPCG's pieces: canonical Gram partials of every A_a . B_b (a < ka <= 48,
+ * b < kb <= 48; partials[(a * kb + b) * nb + blk], fold with sait_dot_fold,
+ * m = ka * kb, to a row-major ka x kb Gram); column-major block kernels
+ * (out = in C, W = W - X G, R_j = AX_j - lam_j X_j; C, G, lam on the device);
+ * U[-1, 1] fill of global entries [offset, offset + n) of seed's sequence
+ * (sait_fill_uniform_pm1 on the device); and the host dense algebra
+ * (Cholesky, inverse of a lower triangle, Rayleigh-Ritz: returns 1 on success,
+ * 0 if the matrix is not positive definite). */
+int sait_gram_partials(const double *d_A, int ka, const double *d_B, int kb, int64_t n, double *d_partials,
+                       sait_stream_t stream);
+int sait_block_lincomb(int64_t n, const double *d_in, int kin, const double *d_C, int kout, double *d_out,
+                       sait_stream_t stream);
+int sait_block_sub_lincomb(int64_t n, const double *d_X, int k, const double *d_G, double *d_W,
+                           sait_stream_t stream);
+int sait_block_residual(int64_t n, int k, const double *d_AX, const double *d_X, const double *d_lam,
+                        double *d_R, sait_stream_t stream);
+int sait_fill_uniform_pm1_device(uint64_t seed, int64_t n, int64_t offset, double *d_out, sait_stream_t stream);
+int sait_dense_chol_lower(const double *G, int m, double *L);
+void sait_dense_tri_lower_inv(const double *L, int m, double *Li);
+int sait_dense_rayleigh_ritz(const double *GA, const double *GB, int m, int k, double *C, double *lam);
 
 /* ----------------------------------------------------- inputs (host) ---
  * Producers of the path's inputs.  ilu_k is ilu.hpp:27 / ilu.cpp:98-173

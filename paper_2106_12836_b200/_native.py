@@ -157,6 +157,14 @@ PROTOTYPES = {
     "sait_vec_cgs": (C.c_int, [C.c_int64, VP, VP, C.c_int64, C.c_int, VP, VP]),
     "sait_vec_div": (C.c_int, [C.c_int64, VP, VP, VP, VP]),
     "sait_vec_lincomb": (C.c_int, [C.c_int64, VP, C.c_int64, C.c_int, VP, VP, VP]),
+    "sait_gram_partials": (C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int64, VP, VP]),
+    "sait_block_lincomb": (C.c_int, [C.c_int64, VP, C.c_int, VP, C.c_int, VP, VP]),
+    "sait_block_sub_lincomb": (C.c_int, [C.c_int64, VP, C.c_int, VP, VP, VP]),
+    "sait_block_residual": (C.c_int, [C.c_int64, C.c_int, VP, VP, VP, VP, VP]),
+    "sait_fill_uniform_pm1_device": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, VP, VP]),
+    "sait_dense_chol_lower": (C.c_int, [PD, C.c_int, PD]),
+    "sait_dense_tri_lower_inv": (None, [PD, C.c_int, PD]),
+    "sait_dense_rayleigh_ritz": (C.c_int, [PD, PD, C.c_int, C.c_int, PD, PD]),
     "sait_pcg_exact": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_lobpcg": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int), VP]),
     "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),

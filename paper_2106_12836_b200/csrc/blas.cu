@@ -284,10 +284,10 @@ __device__ __forceinline__ unsigned long long splitmix(unsigned long long x) {
   x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
   return x ^ (x >> 31);
 }
-__global__ void fill_uniform_pm1_k(unsigned long long seed, int64_t n, double* __restrict__ out) {
+__global__ void fill_uniform_pm1_k(unsigned long long seed, int64_t n, int64_t offset, double* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const unsigned long long x = splitmix(seed ^ splitmix(static_cast<unsigned long long>(i)));
+  const unsigned long long x = splitmix(seed ^ splitmix(static_cast<unsigned long long>(i + offset)));
   const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
   out[i] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
 }
@@ -335,6 +335,23 @@ int64_t dot_blocks(int64_t n) { return n > 0 ? (n + kB - 1) / kB : 1; }
 // G[a * ldg + b] (device, a < ka, b < kb) = canonical dot of A_a and B_b,
 // computed tile by tile (8 x 8); identical bits to multi_dot per entry.
 int64_t gram_scratch(int64_t n, int ka, int kb) { return dot_blocks(n) * ka * kb; }
+
+// partials[(a * kb + b) * nb + blk] for every a < ka, b < kb (no fold)
+void gram_partials(int64_t n, const double* A, int ka, const double* B, int kb, double* part, void* tiles_dev,
+                   cudaStream_t s) {
+  constexpr int TA = 8, TB = 4;
+  const int64_t nb = dot_blocks(n);
+  GramTile list[256];
+  int nt = 0;
+  for (int a0 = 0; a0 < ka; a0 += TA)
+    for (int b0 = 0; b0 < kb; b0 += TB) list[nt++] = GramTile{a0, b0};
+  if (nt == 0 || n == 0) return;
+  GramTile* tiles = static_cast<GramTile*>(tiles_dev);
+  SAIT_CUDA(cudaMemcpyAsync(tiles, list, sizeof(GramTile) * nt, cudaMemcpyHostToDevice, s));
+  gram_tiles<TA, TB><<<dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nb)), kT, 0, s>>>(n, A, ka, B, kb, tiles,
+                                                                                              part, nb, true);
+  SAIT_LAUNCHED();
+}
 
 // G (device, row-major, leading dimension ldg) = A^T B for column-major
 // blocks A (n x ka) and B (n x kb); upper_only skips tiles strictly below the
@@ -385,9 +402,9 @@ void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G
   else gram_impl<8, 4>(n, A, ka, B, kb, G, ldg, scratch, tiles_dev, s, upper_only);
 }
 
-void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s) {
+void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s, int64_t offset) {
   if (n <= 0) return;
-  fill_uniform_pm1_k<<<grid_for(n, 256), 256, 0, s>>>(seed, n, out);
+  fill_uniform_pm1_k<<<grid_for(n, 256), 256, 0, s>>>(seed, n, offset, out);
   SAIT_LAUNCHED();
 }
 

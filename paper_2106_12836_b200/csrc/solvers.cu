@@ -38,7 +38,9 @@ void y_plus_x(int64_t n, const double* x, double* y, cudaStream_t s);
 int64_t gram_scratch(int64_t n, int ka, int kb);
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
           void* tiles_dev, cudaStream_t s, bool upper_only);
-void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s);
+void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s, int64_t offset = 0);
+void gram_partials(int64_t n, const double* A, int ka, const double* B, int kb, double* part, void* tiles_dev,
+                   cudaStream_t s);
 void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s);
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
@@ -718,6 +720,53 @@ int sait_vec_div(int64_t n, const double* d_w, const double* d_d, double* d_out,
   return solver_guard([&] {
     if (n > 0) sait::divide_by(n, d_w, d_d, d_out, sait::as_stream(stream));
   });
+}
+
+int sait_gram_partials(const double* d_A, int ka, const double* d_B, int kb, int64_t n, double* d_partials,
+                       sait_stream_t stream) {
+  return solver_guard([&] {
+    if (ka < 1 || kb < 1 || ka > 48 || kb > 48 || n < 0) sait::throw_invalid("gram_partials: bad arguments");
+    if (n == 0) return;
+    void* tiles = nullptr;
+    cudaStream_t s = sait::as_stream(stream);
+    tiles = sait::dalloc<long long>(256, s);
+    sait::gram_partials(n, d_A, ka, d_B, kb, d_partials, tiles, s);
+    sait::dfree(tiles, s);
+  });
+}
+
+int sait_block_lincomb(int64_t n, const double* d_in, int kin, const double* d_C, int kout, double* d_out,
+                       sait_stream_t stream) {
+  return solver_guard([&] {
+    if (kin < 1 || kin > 48 || kout < 1 || kout > 16) sait::throw_invalid("block_lincomb: bad arguments");
+    if (n > 0) sait::block_lincomb(n, d_in, kin, d_C, kout, d_out, sait::as_stream(stream));
+  });
+}
+
+int sait_block_sub_lincomb(int64_t n, const double* d_X, int k, const double* d_G, double* d_W,
+                           sait_stream_t stream) {
+  return solver_guard([&] {
+    if (k < 1 || k > 16) sait::throw_invalid("block_sub_lincomb: bad arguments");
+    if (n > 0) sait::block_sub_lincomb(n, d_X, k, d_G, d_W, sait::as_stream(stream));
+  });
+}
+
+int sait_block_residual(int64_t n, int k, const double* d_AX, const double* d_X, const double* d_lam, double* d_R,
+                        sait_stream_t stream) {
+  return solver_guard([&] {
+    if (k < 1) sait::throw_invalid("block_residual: bad arguments");
+    if (n > 0) sait::block_residual(n, k, d_AX, d_X, d_lam, d_R, sait::as_stream(stream));
+  });
+}
+
+int sait_fill_uniform_pm1_device(uint64_t seed, int64_t n, int64_t offset, double* d_out, sait_stream_t stream) {
+  return solver_guard([&] { sait::fill_uniform_pm1_device(seed, n, d_out, sait::as_stream(stream), offset); });
+}
+
+int sait_dense_chol_lower(const double* G, int m, double* L) { return sait::chol_lower(G, m, L) ? 1 : 0; }
+void sait_dense_tri_lower_inv(const double* L, int m, double* Li) { sait::tri_lower_inv(L, m, Li); }
+int sait_dense_rayleigh_ritz(const double* GA, const double* GB, int m, int k, double* C, double* lam) {
+  return sait::rayleigh_ritz(GA, GB, m, k, C, lam) ? 1 : 0;
 }
 
 int sait_vec_lincomb(int64_t n, const double* d_V, int64_t ld, int k, const double* d_y, double* d_u,

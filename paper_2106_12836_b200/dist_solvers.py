@@ -299,6 +299,174 @@ def gmres(ctxs, comm, bs, restart=30, tol=1e-8, maxit=10000):
     return xs, st
 
 
+@dataclass
+class DistEigResult:
+    eigenvalues: np.ndarray
+    eigenvectors: list  # this process's row blocks (n_local x nev, column-major), one per context
+    iterations: int
+    residual_history: np.ndarray
+
+
+def lobpcg(ctxs, comm, nev, tol=1e-6, maxit=1000, seed=5):
+    """Row-sharded block LOBPCG (restates sait_lobpcg, solvers.cu): every Gram
+    block is the canonical partials of all ranks folded in rank order, the
+    small dense algebra is the library's own (sait_dense_*), so eigenvalues,
+    residual histories and the eigenvector blocks are bitwise the single-GPU
+    solver's."""
+    import torch
+
+    k = nev
+    if not 1 <= k <= 16:
+        raise N.SaitInvalidArgument("lobpcg: block size must be in [1, 16]")
+    s = _stream()
+    dot = _Dots(ctxs, comm)
+    nl = [c.nloc for c in ctxs]
+    kw = dict(dtype=torch.float64, device="cuda")
+    S = [torch.empty(3 * k * n_, **kw) for n_ in nl]   # [X W P], column-major
+    AS = [torch.empty(3 * k * n_, **kw) for n_ in nl]
+    R = [torch.empty(k * n_, **kw) for n_ in nl]
+    tmp = [torch.empty(4 * k * n_, **kw) for n_ in nl]
+
+    def blk(lst, i, cols=1):  # block i (of k columns) of each rank's stacked array
+        return [t[i * k * n_ : (i + cols) * k * n_] for t, n_ in zip(lst, nl)]
+
+    def column(lst, j):
+        return [t[j * n_ : (j + 1) * n_] for t, n_ in zip(lst, nl)]
+
+    def block_A(src, dst):  # column by column (bitwise the block SpMM)
+        for j in range(k):
+            _apply_A(ctxs, column(src, j), column(dst, j))
+
+    def block_M(src, dst):
+        for j in range(k):
+            _apply_M(ctxs, column(src, j), column(dst, j))
+
+    def gram(A_, ka, B_, kb):
+        parts = []
+        for c, a_, b_ in zip(ctxs, A_, B_):
+            p = torch.empty((ka * kb, int(N.lib.sait_dot_blocks(c.nloc))), **kw)
+            N.check(N.lib.sait_gram_partials(a_.data_ptr(), ka, b_.data_ptr(), kb, c.nloc, p.data_ptr(), s))
+            parts.append(p)
+        allp = torch.cat([p.reshape(ka * kb, -1) for p in comm.gather(parts)], dim=1).contiguous()
+        out = torch.empty(ka * kb, **kw)
+        N.check(N.lib.sait_dot_fold(allp.data_ptr(), allp.shape[1], ka * kb, out.data_ptr(), 0, s))
+        return out.cpu().numpy().astype(np.float64)
+
+    def lincomb(in_, kin, Cm, kout, out_):
+        dC = torch.from_numpy(np.ascontiguousarray(Cm, dtype=np.float64)).cuda()
+        for n_, a_, o_ in zip(nl, in_, out_):
+            N.check(N.lib.sait_block_lincomb(n_, a_.data_ptr(), kin, dC.data_ptr(), kout, o_.data_ptr(), s))
+
+    def copy(dst, src):
+        for d_, s_ in zip(dst, src):
+            d_.copy_(s_)
+
+    def cholqr(Y, AY):
+        G = gram(Y, k, Y, k)
+        L = np.zeros(k * k)
+        Li = np.zeros(k * k)
+        if not N.lib.sait_dense_chol_lower(G.ctypes.data_as(N.PD), k, L.ctypes.data_as(N.PD)):
+            return False
+        N.lib.sait_dense_tri_lower_inv(L.ctypes.data_as(N.PD), k, Li.ctypes.data_as(N.PD))
+        Ri = Li.reshape(k, k).T.copy().ravel()
+        lincomb(Y, k, Ri, k, blk(tmp, 0))
+        copy(Y, blk(tmp, 0))
+        if AY is not None:
+            lincomb(AY, k, Ri, k, blk(tmp, 0))
+            copy(AY, blk(tmp, 0))
+        return True
+
+    def rr(GA, GB, m):
+        Cm = np.zeros(m * k)
+        lam_ = np.zeros(k)
+        ok = N.lib.sait_dense_rayleigh_ritz(GA.ctypes.data_as(N.PD), GB.ctypes.data_as(N.PD), m, k,
+                                            Cm.ctypes.data_as(N.PD), lam_.ctypes.data_as(N.PD))
+        return bool(ok), Cm, lam_
+
+    X, W, P = blk(S, 0), blk(S, 1), blk(S, 2)
+    AX, AW, AP = blk(AS, 0), blk(AS, 1), blk(AS, 2)
+    for c, x in zip(ctxs, X):  # X0 column j from seed * 1000 + j over the global row index
+        for j in range(k):
+            N.check(N.lib.sait_fill_uniform_pm1_device(seed * 1000 + j, c.nloc, c.own[0],
+                                                       x[j * c.nloc :].data_ptr(), s))
+    block_A(X, AX)
+    GB = gram(X, k, X, k)
+    GA = gram(X, k, AX, k)
+    ok, Cm, lam = rr(GA, GB, k)
+    if not ok:
+        raise N.SaitRuntimeError("lobpcg: initial block is rank deficient")
+    lincomb(X, k, Cm, k, blk(tmp, 0))
+    copy(X, blk(tmp, 0))
+    lincomb(AX, k, Cm, k, blk(tmp, 0))
+    copy(AX, blk(tmp, 0))
+    hist = []
+    have_p = False
+    it = 0
+    failed = None
+    while True:
+        dl = torch.from_numpy(lam.copy()).cuda()
+        for n_, ax, x, r_ in zip(nl, AX, X, R):
+            N.check(N.lib.sait_block_residual(n_, k, ax.data_ptr(), x.data_ptr(), dl.data_ptr(), r_.data_ptr(), s))
+        norms = [dot(column(R, j), column(R, j), sqrt=True)[0] for j in range(k)]
+        hist.append(norms)
+        conv = all(v <= tol for v in norms)
+        if conv or it == maxit:
+            break
+        if ctxs[0].M is not None:
+            block_M(R, W)
+        else:
+            copy(W, R)
+        G1 = gram(X, k, W, k)
+        dG = torch.from_numpy(G1).cuda()
+        for n_, x, w in zip(nl, X, W):
+            N.check(N.lib.sait_block_sub_lincomb(n_, x.data_ptr(), k, dG.data_ptr(), w.data_ptr(), s))
+        if not cholqr(W, None):
+            failed = "lobpcg: preconditioned residual block is rank deficient"
+            break
+        block_A(W, AW)
+        use_p = have_p and cholqr(P, AP)
+        m = 3 * k if use_p else 2 * k
+        ok = False
+        while True:
+            Sm = [t[: m * n_] for t, n_ in zip(S, nl)]
+            ASm = [t[: m * n_] for t, n_ in zip(AS, nl)]
+            GB = gram(Sm, m, Sm, m)
+            GA = gram(Sm, m, ASm, m)
+            for i in range(m):
+                for j in range(i + 1, m):
+                    s2 = 0.5 * (GA[i * m + j] + GA[j * m + i])
+                    GA[i * m + j] = s2
+                    GA[j * m + i] = s2
+            ok, Cm, lam_new = rr(GA, GB, m)
+            if ok:
+                lam = lam_new
+                break
+            if m == 3 * k:
+                m = 2 * k
+                continue
+            break
+        if not ok:
+            failed = "lobpcg: Gram matrix not positive definite"
+            break
+        Wm = [t[k * n_ : m * n_] for t, n_ in zip(S, nl)]     # [W P] of the subspace used
+        AWm = [t[k * n_ : m * n_] for t, n_ in zip(AS, nl)]
+        Sm = [t[: m * n_] for t, n_ in zip(S, nl)]
+        ASm = [t[: m * n_] for t, n_ in zip(AS, nl)]
+        lincomb(Wm, m - k, Cm[k * k :], k, blk(tmp, 0))
+        lincomb(AWm, m - k, Cm[k * k :], k, blk(tmp, 1))
+        lincomb(Sm, m, Cm, k, blk(tmp, 2))
+        lincomb(ASm, m, Cm, k, blk(tmp, 3))
+        copy(P, blk(tmp, 0))
+        copy(AP, blk(tmp, 1))
+        copy(X, blk(tmp, 2))
+        copy(AX, blk(tmp, 3))
+        have_p = True
+        it += 1
+    if failed:
+        raise N.SaitRuntimeError(failed)
+    return DistEigResult(np.array(lam[:k]), [x.clone() for x in X], it, np.array(hist))
+
+
 def make_contexts_local(A, ML, MU, world: int):
     """`world` rank contexts in this process (one GPU), wired to each other."""
     ctx = {}

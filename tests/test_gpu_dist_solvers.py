@@ -73,3 +73,25 @@ def test_dist_gmres_bitwise(S, world):
         assert st.iterations == st1.iterations and st.converged == st1.converged
         assert bitwise_equal(st.history, st1.history)
         assert bitwise_equal(x, x1)
+
+
+@pytest.mark.parametrize("world,nev,precond", [(2, 4, True), (3, 8, True), (2, 3, False)])
+def test_dist_lobpcg_bitwise(S, world, nev, precond):
+    import torch
+
+    from paper_2106_12836_b200 import dist_solvers as DS
+
+    A = S.laplacian_3d(24)
+    ML, MU = _pair(S, A, 5e-2, 3) if precond else (None, None)
+    P = S.SaitPairPreconditioner(ML, MU) if precond else None
+    r1 = S.lobpcg(A, P, nev, 1e-6, 40, 5)
+    ctxs = DS.make_contexts_local(A, ML, MU, world)
+    r = DS.lobpcg(ctxs, DS.LocalComm(), nev, 1e-6, 40, 5)
+    torch.cuda.synchronize()
+    assert r.iterations == r1.iterations
+    assert bitwise_equal(r.eigenvalues, r1.eigenvalues)
+    assert bitwise_equal(np.asarray(r.residual_history).ravel(), np.asarray(r1.residual_history).ravel())
+    X = np.concatenate([x.cpu().numpy().reshape(nev, -1) for x in r.eigenvectors], axis=1)  # (nev, n)
+    X1 = np.asarray(r1.eigenvectors)
+    X1 = X1.T if X1.shape[0] != nev else X1
+    assert bitwise_equal(X, X1)

@@ -31,10 +31,10 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(HEADERS)
 
 $(BUILD)/host_%.o: $(CSRC)/host_%.cpp include/sait_c.h
 	@mkdir -p $(BUILD)
-	g++ $(CXXFLAGS) -O3 -c -o $@ $<
+	g++ $(CXXFLAGS) -O3 -fopenmp -c -o $@ $<
 
 $(PKG)/libsait_b200.so: $(CU_OBJS) $(HOST_OBJS)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) $(HOST_OBJS) -cudart static
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) $(HOST_OBJS) -cudart static -lgomp
 
 shim: $(PKG)/libsaitprec_b200.so
 

@@ -196,20 +196,68 @@ uint64_t draw(uint64_t seed, uint64_t ctr) { return mix64(seed ^ mix64(ctr)); }
 double unit53(uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }        // [0,1)
 double unit53_open0(uint64_t bits) { return static_cast<double>((bits >> 11) + 1) * 0x1.0p-53; }  // (0,1]
 
-struct Builder {
-  Csr64 m;
-  explicit Builder(int64_t n, int64_t reserve) {
-    m.nrows = m.ncols = n;
-    m.rp.reserve(n + 1);
-    m.ci.reserve(reserve);
-    m.v.reserve(reserve);
+// Rows built in parallel chunks (OpenMP), concatenated in row order: each
+// row's entries depend only on the row index, so the result is the same as a
+// sequential build.
+struct RowSink {
+  std::vector<int64_t> ci;
+  std::vector<double> v;
+  std::vector<int64_t> cnt;
+  void put(int64_t c, double x) {
+    ci.push_back(c);
+    v.push_back(x);
   }
-  void put(int64_t c, double v) {
-    m.ci.push_back(c);
-    m.v.push_back(v);
-  }
-  void end_row() { m.rp.push_back(static_cast<int64_t>(m.ci.size())); }
 };
+template <class RowFn>
+void build_rows_parallel(int64_t n, int64_t ncols, RowFn fn, sait_host_csr* out) {
+  constexpr int64_t kChunk = 8192;
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  std::vector<RowSink> parts(static_cast<size_t>(nch));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < nch; ++c) {
+    RowSink& sk = parts[c];
+    const int64_t r0 = c * kChunk, r1 = std::min(n, r0 + kChunk);
+    sk.cnt.reserve(r1 - r0);
+    for (int64_t i = r0; i < r1; ++i) {
+      const size_t before = sk.ci.size();
+      fn(i, sk);
+      sk.cnt.push_back(static_cast<int64_t>(sk.ci.size() - before));
+    }
+  }
+  std::vector<int64_t> base(static_cast<size_t>(nch) + 1, 0);
+  for (int64_t c = 0; c < nch; ++c) base[c + 1] = base[c] + static_cast<int64_t>(parts[c].ci.size());
+  const int64_t nnz = base[nch];
+  out->nrows = n;
+  out->ncols = ncols;
+  out->row_ptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n + 1)));
+  out->col_idx = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (nnz ? nnz : 1)));
+  out->values = static_cast<double*>(std::malloc(sizeof(double) * (nnz ? nnz : 1)));
+  if (!out->row_ptr || !out->col_idx || !out->values) {
+    std::free(out->row_ptr);
+    std::free(out->col_idx);
+    std::free(out->values);
+    out->row_ptr = out->col_idx = nullptr;
+    out->values = nullptr;
+    throw std::bad_alloc();
+  }
+  out->row_ptr[0] = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < nch; ++c) {
+    const RowSink& sk = parts[c];
+    int64_t at = base[c];
+    const int64_t r0 = c * kChunk;
+    for (size_t q = 0; q < sk.cnt.size(); ++q) {
+      at += sk.cnt[q];
+      out->row_ptr[r0 + static_cast<int64_t>(q) + 1] = at;
+    }
+    if (!sk.ci.empty()) {
+      std::memcpy(out->col_idx + base[c], sk.ci.data(), sizeof(int64_t) * sk.ci.size());
+      std::memcpy(out->values + base[c], sk.v.data(), sizeof(double) * sk.v.size());
+    }
+  }
+}
+
+
 
 }  // namespace
 
@@ -229,18 +277,14 @@ int sait_problem_laplacian_2d(int64_t nx, sait_host_csr* out) {
   return host_guard([&] {
     if (nx < 1) throw HostError(SAIT_ERR_INVALID_ARGUMENT, "laplacian_2d: nx must be >= 1");
     const int64_t n = nx * nx;
-    Builder b(n, 5 * n);
-    for (int64_t y = 0; y < nx; ++y)
-      for (int64_t x = 0; x < nx; ++x) {
-        const int64_t i = y * nx + x;
-        if (y > 0) b.put(i - nx, -1.0);
-        if (x > 0) b.put(i - 1, -1.0);
-        b.put(i, 4.0);
-        if (x + 1 < nx) b.put(i + 1, -1.0);
-        if (y + 1 < nx) b.put(i + nx, -1.0);
-        b.end_row();
-      }
-    emit(b.m, out);
+    build_rows_parallel(n, n, [nx](int64_t i, RowSink& b) {
+      const int64_t y = i / nx, x = i % nx;
+      if (y > 0) b.put(i - nx, -1.0);
+      if (x > 0) b.put(i - 1, -1.0);
+      b.put(i, 4.0);
+      if (x + 1 < nx) b.put(i + 1, -1.0);
+      if (y + 1 < nx) b.put(i + nx, -1.0);
+    }, out);
   });
 }
 
@@ -248,21 +292,16 @@ int sait_problem_laplacian_3d(int64_t m, sait_host_csr* out) {
   return host_guard([&] {
     if (m < 1) throw HostError(SAIT_ERR_INVALID_ARGUMENT, "laplacian_3d: n must be >= 1");
     const int64_t plane = m * m, n = plane * m;
-    Builder b(n, 7 * n);
-    for (int64_t z = 0; z < m; ++z)
-      for (int64_t y = 0; y < m; ++y)
-        for (int64_t x = 0; x < m; ++x) {
-          const int64_t i = z * plane + y * m + x;
-          if (z > 0) b.put(i - plane, -1.0);
-          if (y > 0) b.put(i - m, -1.0);
-          if (x > 0) b.put(i - 1, -1.0);
-          b.put(i, 6.0);
-          if (x + 1 < m) b.put(i + 1, -1.0);
-          if (y + 1 < m) b.put(i + m, -1.0);
-          if (z + 1 < m) b.put(i + plane, -1.0);
-          b.end_row();
-        }
-    emit(b.m, out);
+    build_rows_parallel(n, n, [m, plane](int64_t i, RowSink& b) {
+      const int64_t z = i / plane, y = (i / m) % m, x = i % m;
+      if (z > 0) b.put(i - plane, -1.0);
+      if (y > 0) b.put(i - m, -1.0);
+      if (x > 0) b.put(i - 1, -1.0);
+      b.put(i, 6.0);
+      if (x + 1 < m) b.put(i + 1, -1.0);
+      if (y + 1 < m) b.put(i + m, -1.0);
+      if (z + 1 < m) b.put(i + plane, -1.0);
+    }, out);
   });
 }
 
@@ -290,18 +329,15 @@ int sait_problem_convdiff_2d(int64_t nx, double bx, double by, sait_host_csr* ou
       w[2][1] += cy;
     }
     const int64_t n = nx * nx;
-    Builder b(n, 9 * n);
-    for (int64_t y = 0; y < nx; ++y)
-      for (int64_t x = 0; x < nx; ++x) {
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            const int64_t xx = x + dx, yy = y + dy;
-            if (xx < 0 || xx >= nx || yy < 0 || yy >= nx) continue;
-            b.put(yy * nx + xx, w[dy + 1][dx + 1]);
-          }
-        b.end_row();
-      }
-    emit(b.m, out);
+    build_rows_parallel(n, n, [nx, &w](int64_t i, RowSink& b) {
+      const int64_t y = i / nx, x = i % nx;
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int64_t xx = x + dx, yy = y + dy;
+          if (xx < 0 || xx >= nx || yy < 0 || yy >= nx) continue;
+          b.put(yy * nx + xx, w[dy + 1][dx + 1]);
+        }
+    }, out);
   });
 }
 
@@ -311,9 +347,8 @@ int sait_problem_synthetic_lower(int64_t n, int64_t draws, double p, uint64_t se
       throw HostError(SAIT_ERR_INVALID_ARGUMENT, "synthetic_lower: bad parameters");
     const double lq = std::log1p(-p);
     const uint64_t s_off = seed * 2 + 1, s_val = seed * 2 + 2;
-    Builder b(n, n * (draws + 1));
-    std::vector<std::pair<int64_t, double>> row;
-    for (int64_t i = 0; i < n; ++i) {
+    build_rows_parallel(n, n, [&](int64_t i, RowSink& b) {
+      thread_local std::vector<std::pair<int64_t, double>> row;
       row.clear();
       for (int64_t d = 0; i > 0 && d < draws; ++d) {
         const uint64_t ctr = static_cast<uint64_t>(i) * static_cast<uint64_t>(draws) + static_cast<uint64_t>(d);
@@ -332,13 +367,12 @@ int sait_problem_synthetic_lower(int64_t n, int64_t draws, double p, uint64_t se
       for (const auto& [c, v] : row) sum_abs += std::fabs(v);
       for (const auto& [c, v] : row) b.put(c, v);
       b.put(i, 1.5 * sum_abs + 1.0);
-      b.end_row();
-    }
-    emit(b.m, out);
+    }, out);
   });
 }
 
 void sait_fill_uniform_pm1(uint64_t seed, int64_t n, double* out) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = 2.0 * unit53(draw(seed, static_cast<uint64_t>(i))) - 1.0;
 }
 

@@ -13,10 +13,14 @@ import paper_2106_12836_b200 as S  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "build"
 grid = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-A = S.laplacian_3d(grid)
-f = S.ilu_k(A, 0)
-L = S.DeviceCsr.upload(f.lower)
-U = S.DeviceCsr.upload(f.upper)
+if what == "c4":  # BASELINE config 4 build (grid = log2 n, default 24)
+    T = S.DeviceCsr.upload(S.synthetic_lower(1 << (grid if grid < 64 else 24), 15, 0.01, 4))
+    A = None
+else:
+    A = S.laplacian_3d(grid)
+    f = S.ilu_k(A, 0)
+    L = S.DeviceCsr.upload(f.lower)
+    U = S.DeviceCsr.upload(f.upper)
 
 
 def build():
@@ -25,6 +29,10 @@ def build():
 
 
 run = build
+if what == "c4":
+    def run():
+        m = S.sait_thr_cap(T, S.lower_triangular, S.SaitThrParams(1e-2, 3), 3.0)
+        m.free()
 if what == "lobpcg":
     ML = S.sait_thr(L, S.lower_triangular, S.SaitThrParams(5e-2, 3))
     MU = S.sait_thr(U, S.upper_triangular, S.SaitThrParams(5e-2, 3))

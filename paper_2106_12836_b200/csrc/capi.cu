@@ -14,6 +14,17 @@
 
 #include "common.cuh"
 
+namespace sait {
+bool debug_alloc_enabled() {
+  static const bool on = std::getenv("SAIT_DEBUG_ALLOC") != nullptr;
+  return on;
+}
+void debug_alloc_time(size_t bytes, double ms) {
+  if (ms > 1.0) std::fprintf(stderr, "[alloc] %.1f MB took %.2f ms\n", bytes / 1e6, ms);
+}
+}  // namespace sait
+
+
 struct sait_dcsr_s {
   int dev = 0;
   sait::DevCsr m;

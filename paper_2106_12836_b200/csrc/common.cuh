@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -51,11 +52,21 @@ struct DevCsr {
 };
 
 // Stream-ordered allocation from the device pool.
+void debug_alloc_time(size_t bytes, double ms);  // capi.cu (SAIT_DEBUG_ALLOC)
+bool debug_alloc_enabled();
 template <class T>
 T* dalloc(size_t count, cudaStream_t s) {
   void* p = nullptr;
   // +256 bytes: bulk copies round transfers up to whole 16-byte granules and
   // may read up to 15 bytes past the last element.
+  if (debug_alloc_enabled()) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaMallocAsync(&p, count * sizeof(T) + 256, s);
+    debug_alloc_time(count * sizeof(T), std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    if (e == cudaErrorMemoryAllocation) throw Error(SAIT_ERR_NOMEM, "out of device memory");
+    SAIT_CUDA(e);
+    return static_cast<T*>(p);
+  }
   cudaError_t e = cudaMallocAsync(&p, count * sizeof(T) + 256, s);
   if (e == cudaErrorMemoryAllocation) throw Error(SAIT_ERR_NOMEM, "out of device memory");
   SAIT_CUDA(e);

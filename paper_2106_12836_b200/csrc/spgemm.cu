@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sort.cuh"
 
@@ -59,6 +61,13 @@ struct Args {
   int32_t* cci;
   double* cv;
   int* changed;
+  // hash-table rows: the count pass stages each row's sorted survivors at a
+  // bump-allocated position (stage_pos[j], -1 if the staging area overflowed)
+  int32_t* stage_col;
+  double* stage_val;
+  int32_t* stage_pos;
+  unsigned long long* stage_cursor;
+  int64_t stage_cap;
 };
 
 // Per-warp staging for one chunk of <= 32 entries of A's row.
@@ -235,16 +244,9 @@ __device__ int drop_row(const Args& g, int32_t row, int32_t* key, double* val, i
   return live;
 }
 
-__device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val, int logs, WarpStage* st,
-                            int lane, bool numeric) {
-  accumulate_row(g, j, key, val, logs, st, lane);
-  const int live = drop_row(g, j, key, val, logs, lane);
-  if (!numeric) {
-    if (lane == 0) g.ccount[j] = live;
-    return;
-  }
-  // compact survivors to [0, live) in slot order (destinations never pass
-  // the chunk being read), pad to a power of two, sort by column.
+// compact survivors to [0, live) in slot order (destinations never pass the
+// chunk being read), pad to a power of two, sort by column.
+__device__ void compact_sort(int32_t* key, double* val, int logs, int live, int lane) {
   const int slots = 1 << logs;
   int base = 0;
   for (int c = 0; c < slots; c += 32) {
@@ -265,26 +267,77 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
   for (int s = live + lane; s < n2; s += 32) key[s] = kKeyPad;
   __syncwarp();
   bitonic_sort(key, val, n2, lane, 32, WarpSync{});
+}
+
+// the early-stop comparison of row j (sorted cols/vals) with the previous iterate
+__device__ __forceinline__ void compare_row(const Args& g, int32_t j, const int32_t* col, const double* v, int live,
+                                            int lane) {
+  const int32_t qb = g.epi.qrp[j], ql = g.epi.qrp[j + 1] - qb;
+  bool diff = ql != live;
+  if (!diff) {
+    for (int s = lane; s < live; s += 32) {
+      const double a = g.epi.qv[qb + s], b = v[s];
+      const double fa = fabs(a), fb = fabs(b);
+      const double mx = fa < fb ? fb : fa;  // std::max(fa, fb)
+      if (g.epi.qci[qb + s] != col[s] || fabs(__dsub_rn(b, a)) > __dmul_rn(1e-15, mx)) diff = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, diff) && lane == 0 && *reinterpret_cast<volatile int*>(g.changed) == 0)
+    atomicOr(g.changed, 1);
+}
+
+__device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val, int logs, WarpStage* st,
+                            int lane, bool numeric) {
+  if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
+  accumulate_row(g, j, key, val, logs, st, lane);
+  const int live = drop_row(g, j, key, val, logs, lane);
+  if (!numeric) {
+    if (lane == 0) g.ccount[j] = live;
+    if (!g.stage_pos) return;
+    compact_sort(key, val, logs, live, lane);
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(g.stage_cursor, static_cast<unsigned long long>(live));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const bool fits = pos + static_cast<unsigned long long>(live) <= static_cast<unsigned long long>(g.stage_cap);
+    if (fits)
+      for (int s = lane; s < live; s += 32) {
+        g.stage_col[pos + s] = key[s];
+        g.stage_val[pos + s] = val[s];
+      }
+    if (lane == 0) g.stage_pos[j] = fits ? static_cast<int32_t>(pos) : -1;
+    __syncwarp();
+    return;
+  }
+  compact_sort(key, val, logs, live, lane);
   const int32_t out = g.crp[j];
   for (int s = lane; s < live; s += 32) {
     g.cci[out + s] = key[s];
     g.cv[out + s] = val[s];
   }
-  if (g.epi.qrp) {
-    const int32_t qb = g.epi.qrp[j], ql = g.epi.qrp[j + 1] - qb;
-    bool diff = ql != live;
-    if (!diff) {
-      for (int s = lane; s < live; s += 32) {
-        const double a = g.epi.qv[qb + s], b = val[s];
-        const double fa = fabs(a), fb = fabs(b);
-        const double mx = fa < fb ? fb : fa;  // std::max(fa, fb)
-        if (g.epi.qci[qb + s] != key[s] || fabs(__dsub_rn(b, a)) > __dmul_rn(1e-15, mx)) diff = true;
-      }
-    }
-    if (__any_sync(0xffffffffu, diff) && lane == 0 && *reinterpret_cast<volatile int*>(g.changed) == 0)
-      atomicOr(g.changed, 1);
-  }
+  if (g.epi.qrp) compare_row(g, j, key, val, live, lane);
   __syncwarp();
+}
+
+// numeric pass of staged hash-table rows: one warp per row copies the sorted
+// survivors to the final row and runs the early-stop compare.
+__global__ void __launch_bounds__(256) spgemm_stage_emit(Args g, const int32_t* __restrict__ rows,
+                                                          int32_t nrows_bin) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w0; r < nrows_bin; r += nw) {
+    const int32_t j = rows[r];
+    const int32_t pos = g.stage_pos[j];
+    if (pos < 0) continue;  // overflowed: recomputed by the hash kernel
+    const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
+    const int32_t* col = g.stage_col + pos;
+    const double* v = g.stage_val + pos;
+    for (int s = lane; s < live; s += 32) {
+      g.cci[out + s] = col[s];
+      g.cv[out + s] = v[s];
+    }
+    if (g.epi.qrp) compare_row(g, j, col, v, live, lane);
+  }
 }
 
 __host__ __device__ constexpr int smem_per_warp(int logs) {
@@ -564,6 +617,12 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
   if (threadIdx.x == 0 && tsum) atomicAdd(total, tsum);
 }
 
+__global__ void gather_logs(const int32_t* __restrict__ rows, int32_t count, const int32_t* __restrict__ logs_of,
+                            int8_t* __restrict__ out) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < count) out[q] = static_cast<int8_t>(logs_of[rows[q]]);
+}
+
 __global__ void scatter_bins(int64_t n, const int8_t* __restrict__ bin_of, int32_t* __restrict__ cursor,
                              int32_t* __restrict__ lists) {
   // warp-aggregated: one atomic per (warp, bin) instead of one per row
@@ -613,7 +672,7 @@ struct Plan {
   double* tval[kTinyBins] = {};
 };
 
-void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s) {
+void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bool recompute = true) {
   static bool attr_set[kNumBins] = {};
   for (int tb = 0; tb < kTinyBins; ++tb) {
     const int32_t tc = pl.hist[tb];
@@ -637,6 +696,15 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s) {
         else spgemm_tiny<32><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
     }
     SAIT_LAUNCHED();
+  }
+  if (numeric && g.stage_pos) {  // staged hash-table rows: one copy kernel over all of them
+    const int32_t cnt = pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin];
+    if (cnt) {
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 7) / 8, int64_t{num_sms()} * 8 * 16));
+      spgemm_stage_emit<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kFirstSmemBin], cnt);
+      SAIT_LAUNCHED();
+    }
+    if (!recompute) return;
   }
   for (int b = kFirstSmemBin; b < kFirstSmemBin + kNumSmemBins; ++b) {
     int32_t cnt = pl.hist[b];
@@ -721,32 +789,45 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   SAIT_LAUNCHED();
   int32_t gc = pl.hist[kGlobalBin];
   if (gc) {
-    // per-row global tables
-    std::vector<int32_t> rows(gc), all_logs(n);
-    SAIT_CUDA(cudaMemcpyAsync(rows.data(), pl.lists + pl.start[kGlobalBin], gc * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaMemcpyAsync(all_logs.data(), logs_of, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    // per-row global tables: gather the table sizes of the global-bin rows on
+    // the device (only gc bytes cross PCIe), offsets on the host
+    pl.glogs = dalloc<int8_t>(gc, s);
+    gather_logs<<<grid_for(gc, 256), 256, 0, s>>>(pl.lists + pl.start[kGlobalBin], gc, logs_of, pl.glogs);
+    SAIT_LAUNCHED();
+    std::vector<int8_t> lg(gc);
+    SAIT_CUDA(cudaMemcpyAsync(lg.data(), pl.glogs, gc * sizeof(int8_t), cudaMemcpyDeviceToHost, s));
     SAIT_CUDA(cudaStreamSynchronize(s));
     std::vector<int64_t> offs(gc);
-    std::vector<int8_t> lg(gc);
     int64_t tot = 0;
     for (int32_t q = 0; q < gc; ++q) {
       offs[q] = tot;
-      lg[q] = static_cast<int8_t>(all_logs[rows[q]]);
       tot += int64_t{1} << lg[q];
     }
     pl.goffs = dalloc<int64_t>(gc, s);
-    pl.glogs = dalloc<int8_t>(gc, s);
     pl.gkey = dalloc<int32_t>(tot, s);
     pl.gval = dalloc<double>(tot, s);
     SAIT_CUDA(cudaMemcpyAsync(pl.goffs, offs.data(), gc * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    SAIT_CUDA(cudaMemcpyAsync(pl.glogs, lg.data(), gc * sizeof(int8_t), cudaMemcpyHostToDevice, s));
     SAIT_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
   }
 
-  // ---- count pass, scan, numeric pass
+  // ---- count pass (hash-table rows staged), scan, numeric pass
   int32_t* counts = dalloc<int32_t>(n, s);
   g.ccount = counts;
+  const int32_t hashed = pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin];
+  if (hashed && !std::getenv("SAIT_SPGEMM_NOSTAGE")) {
+    // survivors of a row <= its products + 1; the staging area is sized from
+    // the A operand (the previous iterate) and capped, rows beyond it fall
+    // back to recomputation in the numeric pass
+    int64_t cap = std::min<int64_t>({static_cast<int64_t>(htotal) + n, 2 * a.nnz + n + (int64_t{1} << 20),
+                                     int64_t{INT32_MAX}});
+    if (const char* e = std::getenv("SAIT_SPGEMM_STAGE_CAP")) cap = std::min<int64_t>(cap, std::atoll(e));  // tests
+    g.stage_cap = cap;
+    g.stage_col = dalloc<int32_t>(cap, s);
+    g.stage_val = dalloc<double>(cap, s);
+    g.stage_pos = dalloc<int32_t>(n, s);
+    g.stage_cursor = dalloc<unsigned long long>(1, s);
+    SAIT_CUDA(cudaMemsetAsync(g.stage_cursor, 0, sizeof(unsigned long long), s));
+  }
   launch_pass(g, pl, false, s);
   c.nnz = scan_counts(counts, c.rp, n, s);
   dfree(counts, s);
@@ -759,7 +840,14 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   g.cci = c.ci;
   g.cv = c.v;
   g.changed = changed;
-  launch_pass(g, pl, true, s);
+  bool overflow = false;
+  if (g.stage_pos) {
+    unsigned long long used = 0;
+    SAIT_CUDA(cudaMemcpyAsync(&used, g.stage_cursor, sizeof used, cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaStreamSynchronize(s));
+    overflow = used > static_cast<unsigned long long>(g.stage_cap);
+  }
+  launch_pass(g, pl, true, s, overflow);
   if (epi.qrp) {
     int hc = 1;
     SAIT_CUDA(cudaMemcpyAsync(&hc, changed, sizeof hc, cudaMemcpyDeviceToHost, s));
@@ -767,6 +855,10 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
     res.changed = hc != 0;
   }
   dfree(changed, s);
+  dfree(g.stage_col, s);
+  dfree(g.stage_val, s);
+  dfree(g.stage_pos, s);
+  dfree(g.stage_cursor, s);
   dfree(bin_of, s);
   dfree(logs_of, s);
   dfree(hist, s);

@@ -136,3 +136,43 @@ def test_spec_examples(S):
     d = S.CsrMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [2.0, 4.0, 8.0])
     m = S.sait_pat(d, S.upper_triangular, S.SaitPatParams(2, 3))
     assert list(m.values) == [0.5, 0.25, 0.125]
+
+
+_STAGE_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2106_12836_b200 as S
+from oracle import oracle as O
+P = O.get("port")
+T = O.synthetic_lower(20000, 15, 0.01, seed=4)
+Tp = S.CsrMatrix(T.nrows, T.ncols, T.row_ptr, T.col_idx, T.values)
+for tau, k in ((1e-2, 3), (0.0, 3)):
+    want = P.sait_thr(T, True, tau, k)
+    got = S.sait_thr(Tp, S.lower_triangular, S.SaitThrParams(tau, k))
+    ok = (np.array_equal(got.row_ptr, want.row_ptr) and np.array_equal(got.col_idx, want.col_idx)
+          and np.array_equal(got.values.view(np.uint64), want.values.view(np.uint64)))
+    print(int(ok))
+"""
+
+
+@pytest.mark.parametrize("cap", ["none", "0", "1000", "200000"])
+def test_hash_rows_staging_and_overflow(cap):
+    """Hash-table rows (hundreds of products) stage their sorted survivors in
+    the count pass; rows past the staging capacity are recomputed in the
+    numeric pass.  Every split (all staged, none, a few, most) gives the
+    oracle's bits."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ)
+    if cap == "none":
+        env["SAIT_SPGEMM_NOSTAGE"] = "1"
+    else:
+        env["SAIT_SPGEMM_STAGE_CAP"] = cap
+    out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.split() == ["1", "1"]

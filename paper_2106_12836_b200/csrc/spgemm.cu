@@ -608,8 +608,13 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     pcap[j] = logs;  // table log2 size (used by the global bin)
   }
   unsigned long long ps = static_cast<unsigned long long>(p);
-  for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+  unsigned long long ph = bin >= kFirstSmemBin ? ps : 0ull;  // products of hash-table rows
+  for (int o = 16; o; o >>= 1) {
+    ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    ph += __shfl_xor_sync(0xffffffffu, ph, o);
+  }
   if (lane == 0 && ps) atomicAdd(&tsum, ps);
+  if (lane == 0 && ph) atomicAdd(total + 1, ph);
   const unsigned grp = __match_any_sync(0xffffffffu, bin);
   if (bin >= 0 && lane == __ffs(grp) - 1) atomicAdd(&h[bin], __popc(grp));
   __syncthreads();
@@ -766,15 +771,16 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   int8_t* bin_of = dalloc<int8_t>(n, s);
   int32_t* logs_of = dalloc<int32_t>(n, s);
   int32_t* hist = dalloc<int32_t>(2 * kNumBins, s);
-  unsigned long long* total = dalloc<unsigned long long>(1, s);
+  unsigned long long* total = dalloc<unsigned long long>(2, s);  // all products, hash-row products
   SAIT_CUDA(cudaMemsetAsync(hist, 0, 2 * kNumBins * sizeof(int32_t), s));
-  SAIT_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), s));
+  SAIT_CUDA(cudaMemsetAsync(total, 0, 2 * sizeof(unsigned long long), s));
   plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total);
   SAIT_LAUNCHED();
-  unsigned long long htotal = 0;
+  unsigned long long htot[2] = {0, 0};
   SAIT_CUDA(cudaMemcpyAsync(pl.hist, hist, sizeof pl.hist, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaMemcpyAsync(&htotal, total, sizeof htotal, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaMemcpyAsync(htot, total, sizeof htot, cudaMemcpyDeviceToHost, s));
   SAIT_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long htotal = htot[0], hashed_products = htot[1];
   res.products = static_cast<int64_t>(htotal);
   for (int b2 = 0; b2 < kNumBins; ++b2) pl.start[b2 + 1] = pl.start[b2] + pl.hist[b2];
   pl.lists = dalloc<int32_t>(n, s);
@@ -818,8 +824,8 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
     // survivors of a row <= its products + 1; the staging area is sized from
     // the A operand (the previous iterate) and capped, rows beyond it fall
     // back to recomputation in the numeric pass
-    int64_t cap = std::min<int64_t>({static_cast<int64_t>(htotal) + n, 2 * a.nnz + n + (int64_t{1} << 20),
-                                     int64_t{INT32_MAX}});
+    int64_t cap = std::min<int64_t>({static_cast<int64_t>(hashed_products) + hashed,
+                                     2 * a.nnz + n + (int64_t{1} << 20), int64_t{INT32_MAX}});
     if (const char* e = std::getenv("SAIT_SPGEMM_STAGE_CAP")) cap = std::min<int64_t>(cap, std::atoll(e));  // tests
     g.stage_cap = cap;
     g.stage_col = dalloc<int32_t>(cap, s);

@@ -307,6 +307,11 @@ int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double *d_b, double *d_x
 int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed,
                 double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
                 sait_stream_t stream);
+/* The same with the exact ILU solves as preconditioner (column by column;
+ * the comparator of SPEC.md acceptance #9). */
+int sait_lobpcg_exact(sait_dcsr_t A, sait_exact_t M, int nev, double tol, int maxit, uint64_t seed,
+                      double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
+                      sait_stream_t stream);
 
 /* Vector primitives of those loops, for solver loops driven across ranks
  * (the same kernels, so the same bits).  Dots: `sait_dot_partials` writes the

@@ -353,10 +353,12 @@ def dot(a, b):
     return L.orc_dot(_dptr(a), _dptr(b), C.c_int64(len(a)))
 
 
-def lobpcg(a, ml, mu, nev, tol=1e-6, maxit=500, seed=5):
+def lobpcg(a, ml, mu, nev, tol=1e-6, maxit=500, seed=5, exact=False):
     """Restated block LOBPCG (oracle/solvers.c).  Returns (evals, evecs (n, nev)
-    column-major, iterations, residual-norm history (iters+1, nev))."""
+    column-major, iterations, residual-norm history (iters+1, nev)); exact=True
+    preconditions with the ILU factors (ml = L, mu = U) by two trisolves."""
     L = _port().lib
+    L.orc_solver_precond_exact(C.c_int(int(exact)))
     n = a.nrows
     evals = np.zeros(nev)
     evecs = np.zeros((nev, n))  # row j = column j of the n x nev block
@@ -364,8 +366,11 @@ def lobpcg(a, ml, mu, nev, tol=1e-6, maxit=500, seed=5):
     its = C.c_int()
     pm = C.byref(_in(ml)) if ml is not None else None
     pu = C.byref(_in(mu)) if mu is not None else None
-    rc = L.orc_lobpcg(C.byref(_in(a)), pm, pu, C.c_int(nev), C.c_double(tol), C.c_int(maxit), C.c_uint64(seed),
-                      _dptr(evals), evecs.ctypes.data_as(_PD), C.byref(its), _dptr(res))
+    try:
+        rc = L.orc_lobpcg(C.byref(_in(a)), pm, pu, C.c_int(nev), C.c_double(tol), C.c_int(maxit), C.c_uint64(seed),
+                          _dptr(evals), evecs.ctypes.data_as(_PD), C.byref(its), _dptr(res))
+    finally:
+        L.orc_solver_precond_exact(C.c_int(0))
     _port()._check(rc)
     it = its.value
     return evals, evecs.T, it, res[: (it + 1) * nev].reshape(it + 1, nev)

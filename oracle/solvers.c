@@ -489,10 +489,7 @@ int orc_lobpcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, int k, do
     }
     if (conv || it == maxit) break;
     /* W = T R, orthogonalised against X, normalised */
-    for (int j = 0; j < k; ++j) {
-      if (ml && mu) orc_pair_apply(ml, mu, R + (size_t)j * n, W + (size_t)j * n);
-      else memcpy(W + (size_t)j * n, R + (size_t)j * n, (size_t)n * sizeof(double));
-    }
+    for (int j = 0; j < k; ++j) precond(ml, mu, R + (size_t)j * n, W + (size_t)j * n, n);
     {
       double G1[16 * 16];
       gram(X, k, W, k, n, G1, k);

@@ -167,6 +167,7 @@ PROTOTYPES = {
     "sait_dense_rayleigh_ritz": (C.c_int, [PD, PD, C.c_int, C.c_int, PD, PD]),
     "sait_pcg_exact": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_double, C.c_int, PD, C.POINTER(SolveStats), VP]),
     "sait_lobpcg": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int), VP]),
+    "sait_lobpcg_exact": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int), VP]),
     "sait_ilu_k": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.POINTER(HostCsr), C.POINTER(HostCsr)]),
     "sait_problem_laplacian_2d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),
     "sait_problem_laplacian_3d": (C.c_int, [C.c_int64, C.POINTER(HostCsr)]),

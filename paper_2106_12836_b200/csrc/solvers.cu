@@ -488,8 +488,8 @@ int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double* d_b, double* d_x
   return pcg_impl(A, pc, d_b, d_x, n, tol, maxit, h_hist, stats, stream);
 }
 
-int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, double* h_evals,
-                double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream) {
+static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int maxit, uint64_t seed,
+                       double* h_evals, double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream) {
   return solver_guard([&] {
     if (!A || !h_evals || !iterations) sait::throw_invalid("lobpcg: null argument");
     const sait::DevCsr& a = A->m;
@@ -497,7 +497,7 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     const int k = nev;
     if (a.ncols != n) sait::throw_invalid("lobpcg: operator is not square");
     if (k < 1 || k > 16) sait::throw_invalid("lobpcg: block size must be in [1, 16]");
-    if (M && sait::pair_dim(M) != n) sait::throw_invalid("lobpcg: preconditioner dimension mismatch");
+    if (M.present() && M.dim() != n) sait::throw_invalid("lobpcg: preconditioner dimension mismatch");
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != A->dev) SAIT_CUDA(cudaSetDevice(A->dev));
@@ -598,8 +598,14 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
         }
         phase("\nresid");
         if (conv || it == maxit) break;
-        if (M) sait::pair_apply_block_internal(M, R, W, n, k, 0, s);
-        else SAIT_CUDA(cudaMemcpyAsync(W, R, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        if (M.p) {
+          sait::pair_apply_block_internal(M.p, R, W, n, k, 0, s);
+        } else if (M.e) {  // exact ILU solves, column by column
+          for (int j = 0; j < k; ++j)
+            sait::exact_apply_internal(M.e, R + static_cast<int64_t>(j) * n, W + static_cast<int64_t>(j) * n, s);
+        } else {
+          SAIT_CUDA(cudaMemcpyAsync(W, R, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        }
         phase("precond");
         std::vector<double> G1;
         gram(X, k, W, k, G1);
@@ -672,6 +678,20 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
     if (dev != A->dev) cudaSetDevice(dev);
     if (failed) sait::throw_runtime(why);
   });
+}
+
+int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, double* h_evals,
+                double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream) {
+  sait::Precond pc;
+  pc.p = M;
+  return lobpcg_impl(A, pc, nev, tol, maxit, seed, h_evals, d_evecs, h_resnorms, iterations, stream);
+}
+
+int sait_lobpcg_exact(sait_dcsr_t A, sait_exact_t M, int nev, double tol, int maxit, uint64_t seed,
+                      double* h_evals, double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream) {
+  sait::Precond pc;
+  pc.e = M;
+  return lobpcg_impl(A, pc, nev, tol, maxit, seed, h_evals, d_evecs, h_resnorms, iterations, stream);
 }
 
 // ---- vector primitives of the solver loops (for loops that run across

@@ -94,8 +94,8 @@ def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, 
     res = np.zeros((maxit + 1) * nev)
     its = C.c_int()
     s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
-    mh = M.handle if M is not None else None
-    N.check(N.lib.sait_lobpcg(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed), evals.ctypes.data_as(N.PD),
+    mh, fn = _precond(M, N.lib.sait_lobpcg, N.lib.sait_lobpcg_exact)
+    N.check(fn(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed), evals.ctypes.data_as(N.PD),
                               vecs.data_ptr(), res.ctypes.data_as(N.PD), C.byref(its), s))
     it = its.value
     v = vecs.T

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -46,6 +47,9 @@ struct sait_exact_s {
   struct Work {
     double* y = nullptr;
     sait::TrisolveState sl, su;
+    // applies on one stream from several threads take turns (each apply
+    // reuses this stream's buffers and flags)
+    std::shared_ptr<std::mutex> mu = std::make_shared<std::mutex>();
   };
   std::mutex mu;
   std::unordered_map<cudaStream_t, Work> ws;  // per-stream flags + y
@@ -79,6 +83,9 @@ struct sait_pair_s {
   // buffer per stream honours the concurrent-apply contract
   sait::PairPlan pp;        // fused single-launch pair (needs both SELL copies)
   struct Work {
+    // applies on one stream from several threads take turns (they share
+    // this stream's y, staging buffers and flags)
+    std::shared_ptr<std::mutex> mu = std::make_shared<std::mutex>();
     double* y = nullptr;
     sait::PairState st;
     // host-vector pipeline (lazily created)
@@ -1352,6 +1359,23 @@ sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
 // chunks it reads exist (bounded bandwidth of the triangular factors), and its
 // z chunk streams out on s_out while later r chunks are still arriving.
 bool device_mapped(const void* p);
+
+// Host-vector applies are synchronous, so the stream is an implementation
+// detail when the caller passes none: each calling thread gets its own, and
+// concurrent host applies from several threads run side by side.
+cudaStream_t host_call_stream(sait_stream_t stream) {
+  if (stream) return sait::as_stream(stream);
+  struct Holder {
+    cudaStream_t s = nullptr;
+    ~Holder() {
+      if (s) cudaStreamDestroy(s);
+    }
+  };
+  thread_local Holder h;
+  if (!h.s) SAIT_CUDA(cudaStreamCreateWithFlags(&h.s, cudaStreamNonBlocking));
+  return h.s;
+}
+
 bool host_zc_out_enabled() {
   const char* e = std::getenv("SAIT_HOST_ZC_OUT");
   return !(e && std::atoi(e) == 0);
@@ -1359,6 +1383,7 @@ bool host_zc_out_enabled() {
 
 void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cudaStream_t s) {
   sait_pair_s::Work& w = pair_work(p, s);
+  std::lock_guard<std::mutex> lk(*w.mu);
   const int64_t k = static_cast<int64_t>(p->chunk_rows.size()) - 1;
   const int64_t n = p->ml->m.nrows;
   if (!w.s_in) {
@@ -1465,6 +1490,7 @@ bool device_mapped(const void* p) {
 // one persistent kernel for both SpMVs, z written to host memory directly.
 void pair_apply_host_dataflow(sait_pair_t p, const double* h_r, double* h_z, cudaStream_t s) {
   sait_pair_s::Work& w = pair_work(p, s);
+  std::lock_guard<std::mutex> lk(*w.mu);
   const int64_t k = static_cast<int64_t>(p->df_rows.size()) - 1;
   const int64_t n = p->ml->m.nrows;
   if (!w.in_flag) {
@@ -1495,6 +1521,7 @@ namespace sait {
 // z = M_U (M_L r) on device vectors (used by the solver loops)
 void pair_apply_internal(sait_pair_t p, const double* r, double* z, cudaStream_t s) {
   sait_pair_s::Work& w = pair_work(p, s);
+  std::lock_guard<std::mutex> lk(*w.mu);  // the two launches of one apply stay adjacent on s
   if (pair_variant() == 3 && p->pp.ok()) {
     sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, r, w.y, z, s);
   } else {
@@ -1513,6 +1540,7 @@ void exact_apply_internal(sait_exact_t p, const double* r, double* z, cudaStream
     w = &p->ws[s];
     if (!w->y && p->l->m.nrows) w->y = sait::dalloc<double>(p->l->m.nrows, s);
   }
+  std::lock_guard<std::mutex> turn(*w->mu);
   sait::trisolve(p->l->m, true, p->pl, r, w->y, w->sl, s);   // y = L^-1 r (unit_lower_triangular)
   sait::trisolve(p->u->m, false, p->pu, w->y, z, w->su, s);  // z = U^-1 y (upper_triangular)
 }
@@ -1556,10 +1584,11 @@ int sait_pair_apply_host(sait_pair_t p, const double* h_r, int64_t rlen, double*
                           std::to_string(L.ncols));
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
+    cudaStream_t s = host_call_stream(stream);
     if (host_dataflow_enabled() && p->df.ok() && device_mapped(h_r) && device_mapped(h_z))
-      pair_apply_host_dataflow(p, h_r, h_z, sait::as_stream(stream));
-    else if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, sait::as_stream(stream));
-    else sait::pair_apply_host_pipelined(L, U, h_r, h_z, sait::as_stream(stream));
+      pair_apply_host_dataflow(p, h_r, h_z, s);
+    else if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, s);
+    else sait::pair_apply_host_pipelined(L, U, h_r, h_z, s);
   });
 }
 

@@ -244,3 +244,63 @@ def test_sell_index_formats(env, kind):
     assert out.returncode == 0, out.stderr[-2000:]
     k0, k1, ok = map(int, out.stdout.split()[-3:])
     assert (k0, k1, ok) == (kind, kind, 1)
+
+
+@pytest.mark.parametrize("sched", ["0.5;0.5;0.25", "default"])
+def test_concurrent_applies_from_threads(S, port, sched, monkeypatch):
+    """apply is const and safe to call concurrently (preconditioner.hpp:15-16):
+    host-vector applies from 4 threads (each gets its own internal stream),
+    device applies from 4 threads of which two share torch's default stream
+    (their launches take turns) and two have their own streams."""
+    import threading
+
+    import torch
+
+    from helpers import to_oracle
+
+    if sched != "default":
+        monkeypatch.setenv("SAIT_PIPE_MB", sched)
+    A = S.laplacian_3d(64)
+    f = S.ilu_k(A, 0)
+    ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
+    MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
+    pair = S.SaitPairPreconditioner(ML, MU)
+    n = A.nrows
+    rs = [S.uniform_pm1(300 + i, n) for i in range(8)]
+    want = [port.pair_apply(to_oracle(ML), to_oracle(MU), r) for r in rs]
+    errors = []
+
+    def host_worker(i):
+        try:
+            r = torch.from_numpy(rs[i]).pin_memory() if i % 2 else torch.from_numpy(rs[i])
+            z = torch.empty(n, dtype=torch.float64)
+            z = z.pin_memory() if i % 2 else z
+            for _ in range(5):
+                z.zero_()
+                pair.apply(r.numpy(), z.numpy())
+                if not bitwise_equal(z.numpy(), want[i]):
+                    errors.append(("host", i))
+        except Exception as e:  # noqa: BLE001
+            errors.append(("host", i, repr(e)))
+
+    def dev_worker(i, own_stream):
+        try:
+            st = torch.cuda.Stream() if own_stream else torch.cuda.default_stream()
+            with torch.cuda.stream(st):
+                r = torch.from_numpy(rs[i]).cuda()
+                z = torch.empty_like(r)
+                for _ in range(5):
+                    pair.apply(r, z)
+                st.synchronize()
+                if not bitwise_equal(z.cpu().numpy(), want[i]):
+                    errors.append(("dev", i))
+        except Exception as e:  # noqa: BLE001
+            errors.append(("dev", i, repr(e)))
+
+    th = [threading.Thread(target=host_worker, args=(i,)) for i in range(4)]
+    th += [threading.Thread(target=dev_worker, args=(4 + i, i >= 2)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors

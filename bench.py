@@ -233,7 +233,9 @@ def run_b200(args):
     # ---- inputs (host, then device): not timed
     A = S.laplacian_3d(GRID)
     n = A.nrows
+    t_ilu_host = time.perf_counter()
     f = S.ilu_k(A, 0)
+    t_ilu_host = time.perf_counter() - t_ilu_host
     Ld = S.DeviceCsr.upload(f.lower)
     Ud = S.DeviceCsr.upload(f.upper)
     torch.cuda.synchronize()
@@ -403,6 +405,36 @@ def run_b200(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(ML_host, MU_host, n)
 
+    # ---- the path's neighbours (not part of `value`): device
+    # ILU(0) (F1) against the host factorization, and the exact ILU solves
+    # SAIT replaces (F2) against the SAIT apply, same factors, device vectors
+    comparators = None
+    if ws == 1:
+        Ad = S.DeviceCsr.upload(A)
+        S.ilu0_device(Ad)  # warm-up (allocator, analysis kernels)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fd = S.ilu0_device(Ad)
+        torch.cuda.synchronize()
+        t_ilu_dev = time.perf_counter() - t0
+        E = S.ExactIluPreconditioner(fd)
+        r0v, z0v = R[0], torch.empty_like(R[0])
+        E.apply(r0v, z0v)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            E.apply(r0v, z0v)
+        torch.cuda.synchronize()
+        t_exact = (time.perf_counter() - t0) / 5
+        t_sait = ms_step / NVEC * 1e-3
+        comparators = {
+            "ilu0_device_ms": t_ilu_dev * 1e3, "ilu0_host_ms": t_ilu_host * 1e3,
+            "exact_ilu_apply_ms": t_exact * 1e3, "sait_apply_ms": t_sait * 1e3,
+            "sait_vs_exact_apply": t_exact / t_sait,
+            "note": "F1/F2 (not in value): device ILU(0) bitwise the host ilu_k; exact = two level-scheduled "
+                    "device triangular solves, bitwise the reference's trisolve",
+        }
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
@@ -414,6 +446,8 @@ def run_b200(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "build": build, "e2e_matches_device": ok,
         }
+        if comparators:
+            line["comparators"] = comparators
         if ws > 1:
             line["config"]["halo_bytes_per_apply_rank0"] = sp.halo_bytes
             line["config"]["halo_transport"] = transport

@@ -175,6 +175,10 @@ int sait_jacobi_sweeps_apply(sait_dcsr_t t, int lower, const double *d_b, int sw
  * diagonal at row i" (SAIT_ERR_INVALID_ARGUMENT), "ilu_k: pivot breakdown at
  * row i (|pivot| = %f)" (SAIT_ERR_RUNTIME) for the first such row. */
 int sait_ilu0(sait_dcsr_t a, sait_stream_t stream, sait_dcsr_t *lower, sait_dcsr_t *upper);
+/* The same for fill level 0 or 1 (ilu_k(a, level)); level 1's pattern is the
+ * structural product (tril(A,-1) + I)(triu(A,1) + I) computed by the device
+ * SpGEMM.  Levels >= 2: SAIT_ERR_INVALID_ARGUMENT (use sait_ilu_k). */
+int sait_ilu_device(sait_dcsr_t a, int level, sait_stream_t stream, sait_dcsr_t *lower, sait_dcsr_t *upper);
 
 /* kernels.hpp:36 / kernels.cpp:196-234: x = T^-1 b by substitution (Lower:
  * rows ascending, Upper: descending; the stored diagonal is used, entries on

@@ -37,6 +37,7 @@ from .problems import (
     IluFactors,
     convdiff_2d,
     ilu0_device,
+    ilu_device,
     ilu_k,
     laplacian_2d,
     laplacian_3d,

@@ -133,6 +133,7 @@ PROTOTYPES = {
     "sait_mm_write": (C.c_int, [C.c_char_p, C.POINTER(HostCsr)]),
     "sait_make_rhs": (C.c_int, [C.POINTER(HostCsr), C.c_int, C.c_uint64, VP]),
     "sait_ilu0": (C.c_int, [VP, VP, C.POINTER(VP), C.POINTER(VP)]),
+    "sait_ilu_device": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(VP)]),
     "sait_trisolve": (C.c_int, [VP, C.c_int, VP, C.c_int64, VP, VP]),
     "sait_exact_ilu_create": (C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
     "sait_exact_ilu_info": (C.c_int, [VP, P64, P64]),

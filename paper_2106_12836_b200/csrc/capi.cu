@@ -1147,6 +1147,10 @@ void sait_operator_destroy(sait_op_t op) {
 // ------------------------------------------------------------ device ILU(0)
 
 int sait_ilu0(sait_dcsr_t a, sait_stream_t stream, sait_dcsr_t* lower, sait_dcsr_t* upper) {
+  return sait_ilu_device(a, 0, stream, lower, upper);
+}
+
+int sait_ilu_device(sait_dcsr_t a, int level, sait_stream_t stream, sait_dcsr_t* lower, sait_dcsr_t* upper) {
   return guarded([&] {
     need(a, "ilu_k");
     need(lower, "ilu_k(lower)");
@@ -1156,7 +1160,7 @@ int sait_ilu0(sait_dcsr_t a, sait_stream_t stream, sait_dcsr_t* lower, sait_dcsr
     init_device_pool();
     cudaStream_t s = sait::as_stream(stream);
     sait::DevCsr L, U;
-    sait::ilu0(a->m, L, U, s);
+    sait::ilu_device(a->m, level, L, U, s);
     SAIT_CUDA(cudaStreamSynchronize(s));
     *lower = wrap(L);
     *upper = wrap(U);

@@ -262,8 +262,8 @@ void trisolve(const DevCsr& t, bool lower, const TrisolvePlan& plan, const doubl
               TrisolveState& st, cudaStream_t s);
 void free_trisolve_state(TrisolveState& st, cudaStream_t s);
 
-// ilu.cu: ILU(0) on A's pattern, bitwise ilu_k(a, 0) (ilu.cpp:98-173)
-void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s);
+// ilu.cu: ILU(k) for k = 0, 1 on the device, bitwise ilu_k(a, k) (ilu.cpp:27-173)
+void ilu_device(const DevCsr& a, int level, DevCsr& L, DevCsr& U, cudaStream_t s);
 
 // blas.cu (elementwise helpers)
 void hadamard(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a * b

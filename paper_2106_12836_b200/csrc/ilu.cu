@@ -145,6 +145,53 @@ __global__ void split_fill(int64_t n, const int32_t* __restrict__ rp, const int3
   }
 }
 
+// ILU(1) pattern helpers: Lp = tril(A, -1) + I, Up = triu(A, 1) + I (values
+// 1.0) so that pattern(Lp Up) = pattern(A) U {(i, j): a_ik != 0, a_kj != 0,
+// k < i, k < j}, the level <= 1 fill of ilu.cpp:27-91 (fill through level-1
+// entries would have level 2).
+__global__ void tri_plus_identity_counts(int64_t n, const int32_t* __restrict__ rp,
+                                         const int32_t* __restrict__ diag, int32_t* __restrict__ lc,
+                                         int32_t* __restrict__ uc) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  lc[i] = diag[i] - rp[i] + 1;
+  uc[i] = rp[i + 1] - diag[i];
+}
+__global__ void tri_plus_identity_fill(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                       const int32_t* __restrict__ diag, const int32_t* __restrict__ lrp,
+                                       int32_t* __restrict__ lci, double* __restrict__ lv,
+                                       const int32_t* __restrict__ urp, int32_t* __restrict__ uci,
+                                       double* __restrict__ uv) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t o = lrp[i];
+  for (int32_t e = rp[i]; e < diag[i]; ++e, ++o) {
+    lci[o] = ci[e];
+    lv[o] = 1.0;
+  }
+  lci[o] = static_cast<int32_t>(i);
+  lv[o] = 1.0;
+  o = urp[i];
+  for (int32_t e = diag[i]; e < rp[i + 1]; ++e, ++o) {  // the diagonal first, then j > i
+    uci[o] = ci[e];
+    uv[o] = 1.0;
+  }
+}
+// w = 0 on the fill pattern P, then A's values at their positions (both rows sorted)
+__global__ void scatter_into_pattern(int64_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                     const double* __restrict__ av, const int32_t* __restrict__ prp,
+                                     const int32_t* __restrict__ pci, double* __restrict__ w) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t q = prp[i];
+  const int32_t q1 = prp[i + 1];
+  for (int32_t e = q; e < q1; ++e) w[e] = 0.0;
+  for (int32_t e = arp[i]; e < arp[i + 1]; ++e) {
+    while (q < q1 && pci[q] < aci[e]) ++q;
+    w[q] = av[e];  // A's pattern is contained in P
+  }
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
@@ -152,8 +199,10 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
-void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s) {
+void ilu_device(const DevCsr& a, int level, DevCsr& L, DevCsr& U, cudaStream_t s) {
   if (a.nrows != a.ncols) throw_invalid("ilu_k: matrix is not square");
+  if (level < 0) throw_invalid("ilu_k: negative fill level");
+  if (level > 1) throw_invalid("ilu_k: the device factorization supports fill levels 0 and 1 (use the host ilu_k)");
   const int64_t n = a.nrows;
   L = DevCsr{};
   U = DevCsr{};
@@ -176,7 +225,9 @@ void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s) {
   double* pivot = nullptr;
   TrisolvePlan plan;
   int32_t *lc = nullptr, *uc = nullptr;
+  DevCsr owned_pattern;  // level 1: the fill pattern (level 0 borrows A's)
   auto cleanup = [&] {
+    free_csr(owned_pattern, s);
     dfree(diag, s);
     dfree(flags, s);
     dfree(scratch, s);
@@ -209,15 +260,51 @@ void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s) {
     std::memcpy(&amax, &amax_bits, sizeof amax);
     const double tol = 1e-14 * amax;  // kPivotBreakdownFactor * max_abs (ilu.cpp:107-108)
 
-    w = dalloc<double>(a.nnz, s);
+    // the factorization pattern P: A's (level 0) or A's plus level-1 fill
+    DevCsr P = a;  // borrowed for level 0
+    if (level == 1) {
+      lc = dalloc<int32_t>(n, s);
+      uc = dalloc<int32_t>(n, s);
+      tri_plus_identity_counts<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, diag, lc, uc);
+      SAIT_LAUNCHED();
+      DevCsr lp, up;
+      lp.nrows = lp.ncols = up.nrows = up.ncols = n;
+      lp.rp = dalloc<int32_t>(n + 1, s);
+      up.rp = dalloc<int32_t>(n + 1, s);
+      lp.nnz = scan_counts(lc, lp.rp, n, s);
+      up.nnz = scan_counts(uc, up.rp, n, s);
+      lp.ci = dalloc<int32_t>(lp.nnz, s);
+      lp.v = dalloc<double>(lp.nnz, s);
+      up.ci = dalloc<int32_t>(up.nnz, s);
+      up.v = dalloc<double>(up.nnz, s);
+      tri_plus_identity_fill<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, diag, lp.rp, lp.ci, lp.v, up.rp, up.ci,
+                                                               up.v);
+      SAIT_LAUNCHED();
+      SpgemmResult pr = spgemm_fused(lp, up, Epilogue{}, s);  // all-positive values: no cancellation
+      free_csr(lp, s);
+      free_csr(up, s);
+      dfree(lc, s);
+      dfree(uc, s);
+      lc = uc = nullptr;
+      P = pr.c;
+      owned_pattern = P;
+      find_diagonal<<<grid_for(n, 256), 256, 0, s>>>(n, P.rp, P.ci, diag, bad);  // diagonal positions in P
+      SAIT_LAUNCHED();
+    }
+    w = dalloc<double>(P.nnz, s);
     pivot = dalloc<double>(n, s);
-    SAIT_CUDA(cudaMemcpyAsync(w, a.v, sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice, s));
-    plan = analyse_triangular(a, true, s);
+    if (level == 0) {
+      SAIT_CUDA(cudaMemcpyAsync(w, a.v, sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice, s));
+    } else {
+      scatter_into_pattern<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, P.rp, P.ci, w);
+      SAIT_LAUNCHED();
+    }
+    plan = analyse_triangular(P, true, s);
     int per_sm = 0;
     SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ilu0_rows, 256, 0));
     per_sm = std::max(1, std::min(per_sm, env_int("SAIT_ILU_BLOCKS_PER_SM", 1)));
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(int64_t{per_sm} * num_sms(), (n + 255) / 256));
-    ilu0_rows<<<grid, 256, 0, s>>>(n, a.rp, a.ci, diag, plan.perm, w, pivot, done, scratch + 1, tol, bad + 1,
+    ilu0_rows<<<grid, 256, 0, s>>>(n, P.rp, P.ci, diag, plan.perm, w, pivot, done, scratch + 1, tol, bad + 1,
                                    static_cast<unsigned>(env_int("SAIT_ILU_SLEEP_NS", 2048)));
     SAIT_LAUNCHED();
     SAIT_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
@@ -232,7 +319,7 @@ void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s) {
     }
     lc = dalloc<int32_t>(n, s);
     uc = dalloc<int32_t>(n, s);
-    split_counts<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, diag, lc, uc);
+    split_counts<<<grid_for(n, 256), 256, 0, s>>>(n, P.rp, diag, lc, uc);
     SAIT_LAUNCHED();
     L.rp = dalloc<int32_t>(n + 1, s);
     U.rp = dalloc<int32_t>(n + 1, s);
@@ -242,7 +329,7 @@ void ilu0(const DevCsr& a, DevCsr& L, DevCsr& U, cudaStream_t s) {
     L.v = dalloc<double>(L.nnz, s);
     U.ci = dalloc<int32_t>(U.nnz, s);
     U.v = dalloc<double>(U.nnz, s);
-    split_fill<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, w, diag, L.rp, L.ci, L.v, U.rp, U.ci, U.v);
+    split_fill<<<grid_for(n, 256), 256, 0, s>>>(n, P.rp, P.ci, w, diag, L.rp, L.ci, L.v, U.rp, U.ci, U.v);
     SAIT_LAUNCHED();
   } catch (...) {
     cleanup();

@@ -27,16 +27,21 @@ def ilu_k(a: CsrMatrix, level: int) -> IluFactors:
     return IluFactors(_from_c(lo), _from_c(up), int(level))
 
 
-def ilu0_device(a, stream=None) -> IluFactors:
-    """ilu_k(a, 0) computed on the GPU (sait_ilu0): bitwise the same factors,
-    returned as DeviceCsr (``.to_host()`` for CsrMatrix).  ``a`` is a
-    CsrMatrix (uploaded) or a DeviceCsr."""
+def ilu_device(a, level: int = 0, stream=None) -> IluFactors:
+    """ilu_k(a, level) computed on the GPU for level 0 or 1 (sait_ilu_device):
+    bitwise the same factors, returned as DeviceCsr (``.to_host()`` for
+    CsrMatrix).  ``a`` is a CsrMatrix (uploaded) or a DeviceCsr."""
     from .csr import DeviceCsr, _stream_handle
 
     da = a if isinstance(a, DeviceCsr) else DeviceCsr.upload(a, stream)
     lo, up = C.c_void_p(), C.c_void_p()
-    N.check(N.lib.sait_ilu0(da.handle, _stream_handle(stream), C.byref(lo), C.byref(up)))
-    return IluFactors(DeviceCsr(lo.value), DeviceCsr(up.value), 0)
+    N.check(N.lib.sait_ilu_device(da.handle, int(level), _stream_handle(stream), C.byref(lo), C.byref(up)))
+    return IluFactors(DeviceCsr(lo.value), DeviceCsr(up.value), int(level))
+
+
+def ilu0_device(a, stream=None) -> IluFactors:
+    """ilu_k(a, 0) on the GPU (sait_ilu0)."""
+    return ilu_device(a, 0, stream)
 
 
 def mm_read(path) -> CsrMatrix:

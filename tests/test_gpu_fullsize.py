@@ -2,9 +2,9 @@
   * config 2 (128^3 Laplacian, ILU(0), tau = 5e-2, k = 3): both SAIT factors
     bitwise equal to the oracle (patterns, values, the 3-step early stop) and
     the pair apply bitwise equal on two of the seeded vectors;
-  * the paper's ratio table at 100^3: the device builds'
-    exact nnz for all 12 cells equal the counts the reference itself produced
-    (tests/golden/ratio_table_100.json);
+  * the paper's ratio table at 100^3: device ILU(0)/ILU(1)
+    then device builds; the exact nnz of all 12 cells equal the counts the
+    reference itself produced (tests/golden/ratio_table_100.json);
   * config 4's generator and fill-capped build at n = 2^18 bitwise equal to
     the oracle (the full n = 2^24 is checked by run_configs' ratio/cap
     properties; the CPU oracle needs minutes there)."""
@@ -53,9 +53,8 @@ def test_paper_ratio_table_100(S):
         table = json.load(fh)
     A = S.laplacian_3d(100)
     for lev in (0, 1):
-        f = S.ilu_k(A, lev) if lev else S.ilu0_device(A)
-        L = f.lower if lev == 0 else S.DeviceCsr.upload(f.lower)
-        U = f.upper if lev == 0 else S.DeviceCsr.upload(f.upper)
+        f = S.ilu_device(A, lev)  # both levels factorized on the device
+        L, U = f.lower, f.upper
         ref = table[f"ilu{lev}"]
         assert (L.nnz(), U.nnz()) == (ref["L"], ref["U"])
         for tau in (0.05, 0.02, 0.01):

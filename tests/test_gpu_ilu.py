@@ -121,3 +121,34 @@ def test_ilu0_feeds_sait(S, port):
     f = S.ilu0_device(to_product(A))
     ml = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
     assert bitwise_equal_csr(ml.to_host() if hasattr(ml, "to_host") else ml, want_l)
+
+
+@pytest.mark.parametrize("case", ["golden_lap12", "lap3d_40", "convdiff_150", "random_4k", "lap2d_2"])
+def test_ilu1_device_vs_port(S, port, golden, case):
+    """Device ILU(1): the level-1 pattern from the structural product
+    (tril(A,-1) + I)(triu(A,1) + I), the reference's IKJ numeric on it —
+    bitwise the reference's ilu_k(a, 1) (golden) and the port."""
+    from conftest import golden_csr
+    from oracle import oracle as O
+
+    A = {
+        "golden_lap12": lambda: O.laplacian_3d(12),
+        "lap3d_40": lambda: O.laplacian_3d(40),
+        "convdiff_150": lambda: O.convdiff_2d(150),
+        "random_4k": lambda: _random_matrix(4000, 0.002, 7),
+        "lap2d_2": lambda: O.laplacian_2d(2),
+    }[case]()
+    L, U = port.ilu_k(A, 1)
+    if case == "golden_lap12":
+        assert bitwise_equal_csr(L, golden_csr(golden, "lap12/L1"))
+        assert bitwise_equal_csr(U, golden_csr(golden, "lap12/U1"))
+    f = S.ilu_device(to_product(A), 1)
+    assert bitwise_equal_csr(f.lower.to_host(), L)
+    assert bitwise_equal_csr(f.upper.to_host(), U)
+
+
+def test_ilu_device_levels_beyond_one_are_refused(S):
+    with pytest.raises(S.SaitInvalidArgument, match="fill levels 0 and 1"):
+        S.ilu_device(S.laplacian_2d(8), 2)
+    with pytest.raises(S.SaitInvalidArgument, match="negative fill level"):
+        S.ilu_device(S.laplacian_2d(8), -1)

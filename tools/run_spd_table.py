@@ -29,8 +29,8 @@ def run_one(name, A, tau, level, pat, tol, maxit):
     _, st = S.pcg(A, None, b, tol, maxit)
     row["no_pc"] = st.iterations
     t0 = time.perf_counter()
-    if level == 0:
-        f = S.ilu0_device(A)
+    if level <= 1:
+        f = S.ilu_device(A, level)
         torch.cuda.synchronize()
         row["ilu_device_ms"] = (time.perf_counter() - t0) * 1e3
         L, U = f.lower, f.upper

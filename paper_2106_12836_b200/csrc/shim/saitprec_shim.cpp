@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -469,6 +470,24 @@ double norm2(std::span<const double> a) { return std::sqrt(dot(a, a)); }
 // ------------------------------------------------------------------- ilu.hpp
 
 IluFactors ilu_k(const CsrMatrix& a, int level) {
+  // Large matrices at fill levels 0 and 1 factorize on the device
+  // (sait_ilu_device: the same factors bit for bit, the same errors);
+  // SAIT_SHIM_DEVICE_ILU_MIN overrides the size threshold (stored entries).
+  static const int64_t device_min = [] {
+    const char* e = std::getenv("SAIT_SHIM_DEVICE_ILU_MIN");
+    return e ? std::atoll(e) : int64_t{1} << 20;
+  }();
+  if ((level == 0 || level == 1) && a.nrows == a.ncols && a.nnz() >= device_min) {
+    Dev d = upload(a);
+    sait_dcsr_t lo = nullptr, up = nullptr;
+    check(sait_ilu_device(d.h, level, thread_stream(), &lo, &up));
+    Dev l(lo), u(up);
+    IluFactors f;
+    f.lower = download(l.h);
+    f.upper = download(u.h);
+    f.level = level;
+    return f;
+  }
   sait_host_csr c = view(a), lo{}, up{};
   check(sait_ilu_k(&c, level, &lo, &up));
   auto take = [](sait_host_csr& h) {

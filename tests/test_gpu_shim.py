@@ -95,6 +95,20 @@ def test_shim_builders_and_kernels_match_oracle(dump, golden, port):
     assert bitwise_equal(dump["gmres_x"], xo) and bitwise_equal(dump["gmres_hist"], so["history"])
 
 
+def test_shim_device_ilu_path_identical(dump, tmp_path):
+    """The shim's ilu_k takes the device factorization for large matrices;
+    forcing it for every size (SAIT_SHIM_DEVICE_ILU_MIN=0) changes no output."""
+    exe = os.path.join(ROOT, "build", "shim_check")
+    path = str(tmp_path / "out_dev.bin")
+    env = dict(os.environ, SAIT_SHIM_DEVICE_ILU_MIN="0")
+    r = subprocess.run([exe, path], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    dev = read_dump(path)
+    assert dev.keys() == dump.keys()
+    for k in dump:
+        assert np.array_equal(dev[k].view(np.uint8), dump[k].view(np.uint8)), k
+
+
 def test_shim_exceptions(dump):
     msg = lambda k: bytes(dump[k].astype(np.uint8)).decode()  # noqa: E731
     assert msg("err_thr") == "sait_thr: threshold must be in [0, 1), got 1.500000"

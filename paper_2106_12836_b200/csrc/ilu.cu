@@ -68,12 +68,18 @@ __global__ void max_abs_kernel(int64_t nnz, const double* __restrict__ v, unsign
   if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
+constexpr int kRowSmem = 32;  // rows up to this length work in shared memory
+constexpr int kIluSmem = 256 * kRowSmem * (sizeof(double) + sizeof(int32_t));
+
 __global__ void __launch_bounds__(256) ilu0_rows(int64_t n, const int32_t* __restrict__ rp,
                                                   const int32_t* __restrict__ ci, const int32_t* __restrict__ diag,
                                                   const int32_t* __restrict__ perm, double* __restrict__ w,
                                                   double* __restrict__ pivot, int* __restrict__ done,
                                                   unsigned long long* __restrict__ counter, double tol,
                                                   int* __restrict__ bad, unsigned max_ns) {
+  extern __shared__ __align__(16) unsigned char ilu_smem[];  // kIluSmem bytes
+  double (*sw)[kRowSmem] = reinterpret_cast<double (*)[kRowSmem]>(ilu_smem);
+  int32_t (*sc)[kRowSmem] = reinterpret_cast<int32_t (*)[kRowSmem]>(ilu_smem + 256 * kRowSmem * sizeof(double));
   const int lane = threadIdx.x & 31;
   while (true) {
     unsigned long long c0 = 0;
@@ -95,17 +101,53 @@ __global__ void __launch_bounds__(256) ilu0_rows(int64_t n, const int32_t* __res
       if (ns < max_ns) ns <<= 1;
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    for (int32_t p = e0; p < d; ++p) {
-      const int32_t k = ci[p];
-      const double f = __ddiv_rn(w[p], ld_cg(pivot + k));
-      w[p] = f;
-      // U(k) = entries after k's diagonal (ascending); merge into row i's tail
-      const int32_t q1 = rp[k + 1];
-      int32_t at = p + 1;
-      for (int32_t q = diag[k] + 1; q < q1 && at < e1; ++q) {
-        const int32_t j = ci[q];
-        while (at < e1 && ci[at] < j) ++at;
-        if (at < e1 && ci[at] == j) w[at] = __dsub_rn(w[at], __dmul_rn(f, ld_cg(w + q)));
+    const int32_t len = e1 - e0;
+    if (len <= kRowSmem) {
+      // the row's columns and values in this lane's shared-memory slots; each
+      // U(k) row is fetched 8 entries at a time with all loads in flight, then
+      // merged -- the same operations in the same order as below
+      int32_t* rc = sc[threadIdx.x];
+      double* rw = sw[threadIdx.x];
+      for (int32_t q = 0; q < len; ++q) {
+        rc[q] = ci[e0 + q];
+        rw[q] = w[e0 + q];
+      }
+      for (int32_t p = 0; p < d - e0; ++p) {
+        const int32_t k = rc[p];
+        const int32_t q0 = diag[k] + 1, q1 = rp[k + 1];
+        const double f = __ddiv_rn(rw[p], ld_cg(pivot + k));
+        rw[p] = f;
+        int32_t at = p + 1;
+        for (int32_t qb = q0; qb < q1 && at < len; qb += 8) {
+          int32_t cj[8];
+          double uv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            cj[u] = qb + u < q1 ? ci[qb + u] : INT32_MAX;
+            uv[u] = qb + u < q1 ? ld_cg(w + qb + u) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int32_t j = cj[u];
+            while (at < len && rc[at] < j) ++at;
+            if (at < len && rc[at] == j) rw[at] = __dsub_rn(rw[at], __dmul_rn(f, uv[u]));
+          }
+        }
+      }
+      for (int32_t q = 0; q < len; ++q) w[e0 + q] = rw[q];
+    } else {
+      for (int32_t p = e0; p < d; ++p) {
+        const int32_t k = ci[p];
+        const double f = __ddiv_rn(w[p], ld_cg(pivot + k));
+        w[p] = f;
+        // U(k) = entries after k's diagonal (ascending); merge into row i's tail
+        const int32_t q1 = rp[k + 1];
+        int32_t at = p + 1;
+        for (int32_t q = diag[k] + 1; q < q1 && at < e1; ++q) {
+          const int32_t j = ci[q];
+          while (at < e1 && ci[at] < j) ++at;
+          if (at < e1 && ci[at] == j) w[at] = __dsub_rn(w[at], __dmul_rn(f, ld_cg(w + q)));
+        }
       }
     }
     const double piv = w[d];
@@ -301,10 +343,11 @@ void ilu_device(const DevCsr& a, int level, DevCsr& L, DevCsr& U, cudaStream_t s
     }
     plan = analyse_triangular(P, true, s);
     int per_sm = 0;
-    SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ilu0_rows, 256, 0));
+    SAIT_CUDA(cudaFuncSetAttribute(ilu0_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, kIluSmem));
+    SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ilu0_rows, 256, kIluSmem));
     per_sm = std::max(1, std::min(per_sm, env_int("SAIT_ILU_BLOCKS_PER_SM", 1)));
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(int64_t{per_sm} * num_sms(), (n + 255) / 256));
-    ilu0_rows<<<grid, 256, 0, s>>>(n, P.rp, P.ci, diag, plan.perm, w, pivot, done, scratch + 1, tol, bad + 1,
+    ilu0_rows<<<grid, 256, kIluSmem, s>>>(n, P.rp, P.ci, diag, plan.perm, w, pivot, done, scratch + 1, tol, bad + 1,
                                    static_cast<unsigned>(env_int("SAIT_ILU_SLEEP_NS", 2048)));
     SAIT_LAUNCHED();
     SAIT_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));

@@ -1,6 +1,6 @@
 """Kernel timeline of one C2 factor build (or pair apply, or 5 LOBPCG iterations) via torch.profiler
 (CUPTI): per-kernel device time, the busy fraction of the wall interval and
-the largest idle gaps.  python tools/prof_timeline.py [build|apply|lobpcg] [grid]"""
+the largest idle gaps.  python tools/prof_timeline.py [build|apply|lobpcg|ilu0|ilu1|c4] [grid]"""
 import os
 import sys
 import time
@@ -29,6 +29,13 @@ def build():
 
 
 run = build
+if what in ("ilu0", "ilu1"):
+    dA = S.DeviceCsr.upload(A)
+
+    def run():
+        g = S.ilu_device(dA, int(what[-1]))
+        g.lower.free()
+        g.upper.free()
 if what == "c4":
     def run():
         m = S.sait_thr_cap(T, S.lower_triangular, S.SaitThrParams(1e-2, 3), 3.0)

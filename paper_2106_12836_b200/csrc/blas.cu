@@ -127,8 +127,10 @@ __global__ void add_k(int64_t n, const double* __restrict__ x, double* __restric
 }
 
 // out[:, j] = sum_q in[:, q] C[q][j]  (column-major blocks, C row-major kin x kout)
-__global__ void block_lincomb_k(int64_t n, const double* __restrict__ in, int kin, const double* __restrict__ C,
-                                int kout, double* __restrict__ out) {
+// in and out may overlap (LOBPCG updates its blocks in place): each thread
+// reads every input of its element before it writes any output.
+__global__ void block_lincomb_k(int64_t n, const double* in, int kin, const double* __restrict__ C, int kout,
+                                double* out) {
   __shared__ double cs[48 * 16];
   for (int e = threadIdx.x; e < kin * kout; e += blockDim.x) cs[e] = C[e];
   __syncthreads();

@@ -165,10 +165,10 @@ struct SellMatrix {
   int64_t* soff = nullptr;  // nslices + 1 element offsets (multiples of 32)
   int32_t* col = nullptr;   // absolute columns, -1 marks padding ...
   int16_t* dcol = nullptr;  // ... or col - row deltas, INT16_MIN marks padding
-  // ... or shared slice patterns: slice s reads its int16 deltas from
+  // ... or shared slice patterns: slice s reads its col - row deltas from
   // dict[pat[s] + k*32 + lane] (regular matrices repeat a few patterns)
   int32_t* pat = nullptr;
-  int16_t* dict = nullptr;
+  int32_t* dict = nullptr;
   int64_t dict_elems = 0;
   double* val = nullptr;
   bool ok() const { return soff != nullptr; }

@@ -69,11 +69,11 @@ struct Idx16 {
 // in L1 and only the values stream from HBM (8 instead of 10 B per entry).
 struct IdxDict {
   const int32_t* pat;
-  const int16_t* dict;
+  const int32_t* dict;  // col - row deltas, INT32_MIN = padding
   __device__ __forceinline__ int64_t slice_base(int64_t s, int64_t /*base*/) const { return __ldg(pat + s); }
   __device__ __forceinline__ int32_t col(int64_t e, int32_t row) const {
-    const int16_t d = __ldg(dict + e);
-    return d == INT16_MIN ? -1 : row + d;
+    const int32_t d = __ldg(dict + e);
+    return d == INT32_MIN ? -1 : row + d;
   }
 };
 
@@ -729,24 +729,35 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
-// one warp per slice: a hash of (width, every lane's int16 deltas)
-__global__ void slice_hash(int64_t nslices, const int64_t* __restrict__ soff, const int16_t* __restrict__ dcol,
+// slot delta col - row of a SELL entry (INT32_MIN for padding), from either
+// per-entry index form
+template <class IDX>
+__device__ __forceinline__ int32_t slot_delta(const IDX& idx, int64_t e, int32_t row) {
+  const int32_t c = idx.col(e, row);
+  return c < 0 ? INT32_MIN : c - row;
+}
+
+// one warp per slice: a hash of (width, every lane's deltas)
+template <class IDX>
+__global__ void slice_hash(int64_t nslices, const int64_t* __restrict__ soff, IDX idx,
                            unsigned long long* __restrict__ h) {
   const int lane = threadIdx.x & 31;
   const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
   const int64_t base = soff[s];
   const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
   unsigned long long x = static_cast<unsigned long long>(w) * 0x100000001B3ull + static_cast<unsigned long long>(lane);
   for (int32_t k = 0; k < w; ++k)
-    x = mix64(x ^ static_cast<unsigned short>(dcol[base + static_cast<int64_t>(k) * kSlice + lane]));
+    x = mix64(x ^ static_cast<unsigned int>(slot_delta(idx, base + static_cast<int64_t>(k) * kSlice + lane, row)));
   x = mix64(x + static_cast<unsigned long long>(lane) * 0xD6E8FEB86659FD93ull);
   for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   if (lane == 0) h[s] = mix64(x ^ static_cast<unsigned long long>(w));
 }
 
-// any slice whose block differs from its representative's -> *bad
-__global__ void slice_verify(int64_t nslices, const int64_t* __restrict__ soff, const int16_t* __restrict__ dcol,
+// any slice whose deltas differ from its representative's -> *bad
+template <class IDX>
+__global__ void slice_verify(int64_t nslices, const int64_t* __restrict__ soff, IDX idx,
                              const int32_t* __restrict__ rep, int* __restrict__ bad) {
   const int lane = threadIdx.x & 31;
   const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -759,32 +770,37 @@ __global__ void slice_verify(int64_t nslices, const int64_t* __restrict__ soff, 
     if (lane == 0) atomicOr(bad, 1);
     return;
   }
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane, rrow = static_cast<int32_t>(r * kSlice) + lane;
   bool diff = false;
-  for (int64_t e = lane; e < len; e += kSlice) diff |= dcol[b + e] != dcol[br + e];
+  for (int64_t e = lane; e < len; e += kSlice) diff |= slot_delta(idx, b + e, row) != slot_delta(idx, br + e, rrow);
   if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(bad, 1);
 }
 
-__global__ void slice_gather_dict(int64_t nslices, const int64_t* __restrict__ soff,
-                                  const int16_t* __restrict__ dcol, const int32_t* __restrict__ rep,
-                                  const int32_t* __restrict__ pat, int16_t* __restrict__ dict) {
+template <class IDX>
+__global__ void slice_gather_dict(int64_t nslices, const int64_t* __restrict__ soff, IDX idx,
+                                  const int32_t* __restrict__ rep, const int32_t* __restrict__ pat,
+                                  int32_t* __restrict__ dict) {
   const int lane = threadIdx.x & 31;
   const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices || rep[s] != s) return;
   const int64_t b = soff[s], len = soff[s + 1] - b;
-  for (int64_t e = lane; e < len; e += kSlice) dict[pat[s] + e] = dcol[b + e];
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  for (int64_t e = lane; e < len; e += kSlice) dict[pat[s] + e] = slot_delta(idx, b + e, row);
 }
 
-// Replace the per-entry int16 deltas by a dictionary of the distinct slice
-// blocks when it is small (<= 1M deltas) and actually saves bytes.
+// Replace the per-entry indices (int16 deltas or int32 columns) by a
+// dictionary of the distinct slices' int32 delta blocks when it is small
+// (<= 1M deltas) and actually saves bytes.
 void try_slice_dictionary(SellMatrix& m, cudaStream_t s) {
   static const bool off = [] {
     const char* e = std::getenv("SAIT_SELL_DICT");
     return e && std::atoi(e) == 0;
   }();
-  if (off || !m.dcol || m.nslices == 0) return;
+  if (off || (!m.dcol && !m.col) || m.nslices == 0) return;
   const int64_t ns = m.nslices;
   unsigned long long* dh = dalloc<unsigned long long>(ns, s);
-  slice_hash<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, m.dcol, dh);
+  if (m.dcol) slice_hash<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx16{m.dcol}, dh);
+  else slice_hash<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx32{m.col}, dh);
   SAIT_LAUNCHED();
   std::vector<unsigned long long> hh(ns);
   std::vector<int64_t> so(ns + 1);
@@ -816,7 +832,8 @@ void try_slice_dictionary(SellMatrix& m, cudaStream_t s) {
   SAIT_CUDA(cudaMemcpyAsync(d, rep.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
   SAIT_CUDA(cudaMemcpyAsync(d + ns, pat.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
   SAIT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  slice_verify<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, m.dcol, d, bad);
+  if (m.dcol) slice_verify<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx16{m.dcol}, d, bad);
+  else slice_verify<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx32{m.col}, d, bad);
   SAIT_LAUNCHED();
   int hb = 0;
   SAIT_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -826,15 +843,20 @@ void try_slice_dictionary(SellMatrix& m, cudaStream_t s) {
     dfree(d, s);
     return;
   }
-  m.dict = dalloc<int16_t>(elems, s);
+  m.dict = dalloc<int32_t>(elems, s);
   m.dict_elems = elems;
-  slice_gather_dict<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, m.dcol, d, d + ns, m.dict);
+  if (m.dcol)
+    slice_gather_dict<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx16{m.dcol}, d, d + ns, m.dict);
+  else
+    slice_gather_dict<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx32{m.col}, d, d + ns, m.dict);
   SAIT_LAUNCHED();
   m.pat = dalloc<int32_t>(ns, s);
   SAIT_CUDA(cudaMemcpyAsync(m.pat, d + ns, sizeof(int32_t) * ns, cudaMemcpyDeviceToDevice, s));
   dfree(d, s);
   dfree(m.dcol, s);
+  dfree(m.col, s);
   m.dcol = nullptr;
+  m.col = nullptr;
   SAIT_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -545,11 +545,9 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
       sait::tri_lower_inv(L.data(), k, Li.data());
       for (int i = 0; i < k; ++i)
         for (int j = 0; j < k; ++j) Ri[i * k + j] = Li[j * k + i];
-      lincomb(Y, k, Ri.data(), k, tmp);
-      SAIT_CUDA(cudaMemcpyAsync(Y, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+      lincomb(Y, k, Ri.data(), k, Y);  // in place: each element is read before it is written
       if (AY) {
-        lincomb(AY, k, Ri.data(), k, tmp);
-        SAIT_CUDA(cudaMemcpyAsync(AY, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        lincomb(AY, k, Ri.data(), k, AY);
       }
       return true;
     };
@@ -579,10 +577,8 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
       failed = true;
       why = "lobpcg: initial block is rank deficient";
     } else {
-      lincomb(X, k, C.data(), k, tmp);
-      SAIT_CUDA(cudaMemcpyAsync(X, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
-      lincomb(AX, k, C.data(), k, tmp);
-      SAIT_CUDA(cudaMemcpyAsync(AX, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+      lincomb(X, k, C.data(), k, X);
+      lincomb(AX, k, C.data(), k, AX);
       for (it = 0; it <= maxit; ++it) {
         double* dl = next_small();
         SAIT_CUDA(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
@@ -649,14 +645,12 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
           why = "lobpcg: Gram matrix not positive definite";
           break;
         }
-        lincomb(W, m - k, C.data() + k * k, k, tmp);
-        lincomb(AW, m - k, C.data() + k * k, k, tmp + blk);
-        lincomb(S, m, C.data(), k, tmp + 2 * blk);
-        lincomb(AS, m, C.data(), k, tmp + 3 * blk);
-        SAIT_CUDA(cudaMemcpyAsync(P, tmp, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
-        SAIT_CUDA(cudaMemcpyAsync(AP, tmp + blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
-        SAIT_CUDA(cudaMemcpyAsync(X, tmp + 2 * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
-        SAIT_CUDA(cudaMemcpyAsync(AX, tmp + 3 * blk, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+        // in place, each element read before it is written: X and AX first
+        // (they read the old P), then P and AP (from W and the old P)
+        lincomb(S, m, C.data(), k, X);
+        lincomb(AS, m, C.data(), k, AX);
+        lincomb(W, m - k, C.data() + k * k, k, P);
+        lincomb(AW, m - k, C.data() + k * k, k, AP);
         have_p = true;
         phase("update");
       }

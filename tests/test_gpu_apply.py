@@ -227,11 +227,12 @@ print(kinds[0], kinds[1], int(ok))
 """
 
 
-@pytest.mark.parametrize("env,kind", [("1", 2), ("0", 1)])
-def test_sell_index_formats(env, kind):
+@pytest.mark.parametrize("env,index,kind", [("1", "", 2), ("0", "", 1), ("1", "32", 2), ("0", "32", 0)])
+def test_sell_index_formats(env, index, kind):
     """The SELL copy of a stencil factor uses shared slice patterns (a few
-    distinct int16 delta blocks serve every slice) unless SAIT_SELL_DICT=0;
-    both give the oracle's bits."""
+    distinct delta blocks serve every slice, built from int16 deltas or from
+    int32 columns) unless SAIT_SELL_DICT=0; every format gives the oracle's
+    bits."""
     import os
     import subprocess
     import sys
@@ -240,6 +241,8 @@ def test_sell_index_formats(env, kind):
 
     code = _DICT_CHILD.format(root=ROOT)
     envd = dict(os.environ, SAIT_SELL_DICT=env, PYTHONPATH=os.path.join(ROOT, "tests"))
+    if index:
+        envd["SAIT_SELL_INDEX"] = index
     out = subprocess.run([sys.executable, "-c", code], env=envd, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     k0, k1, ok = map(int, out.stdout.split()[-3:])

@@ -217,3 +217,33 @@ def test_10_determinism(S):
     r1 = S.lobpcg(A, P, 4, 1e-6, 300, 5)
     r2 = S.lobpcg(A, P, 4, 1e-6, 300, 5)
     assert bitwise_equal(r1.eigenvalues, r2.eigenvalues) and bitwise_equal(r1.eigenvectors, r2.eigenvectors)
+
+
+def test_spd_experiment_from_matrix_market(S, tmp_path):
+    """F4 end to end (the paper's SPD experiment): a
+    symmetric-stored Matrix Market file (lower triangle, like SuiteSparse's
+    SPD matrices) -> mm_read -> device ILU(0) -> SAIT_Thr(0.05, 10) -> PCG.
+    The file round-trips to the original matrix, and SAIT needs more
+    iterations than the exact solves but fewer than no preconditioner."""
+    import sys
+
+    from conftest import ROOT
+
+    A = S.laplacian_3d(20)
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    low = A.col_idx <= rows
+    p = tmp_path / "lap20_sym.mtx"
+    with open(p, "w") as fh:
+        fh.write("%%MatrixMarket matrix coordinate real symmetric\n% 3-D Laplacian 20^3, lower triangle\n")
+        fh.write(f"{A.nrows} {A.ncols} {int(low.sum())}\n")
+        for i, j, v in zip(rows[low], A.col_idx[low], A.values[low]):
+            fh.write(f"{i + 1} {j + 1} {float(v)!r}\n")
+    B = S.mm_read(p)
+    assert np.array_equal(B.row_ptr, A.row_ptr) and np.array_equal(B.col_idx, A.col_idx)
+    assert bitwise_equal(B.values, A.values)
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import run_spd_table
+
+    row = run_spd_table.run_one("lap20_sym.mtx", B, 0.05, 0, [2], 1e-8, 5000)
+    assert row["exact"] < row["sait"] < row["no_pc"], row
+    assert 1.0 < row["ratio"] < 3.0

@@ -154,6 +154,12 @@ int sait_jacobi_split(sait_dcsr_t t, int lower, double *d_inv_diag, sait_stream_
  * returns the approximate inverse M = poly(tT) D^-1 of the triangular T. */
 int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec *spec, sait_stream_t stream,
                sait_dcsr_t *m_out, sait_build_stats *stats);
+/* Both factors of an ILU pair with the same drop spec (the input of
+ * SaitPairPreconditioner): M_L = build(lower) on `stream` and M_U =
+ * build(upper) concurrently on an internal stream; bitwise the two separate
+ * sait_build calls.  stats2 (may be NULL) receives [M_L, M_U]. */
+int sait_build_pair(sait_dcsr_t lower, sait_dcsr_t upper, const sait_drop_spec *spec, sait_stream_t stream,
+                    sait_dcsr_t *ml_out, sait_dcsr_t *mu_out, sait_build_stats *stats2);
 /* sait.hpp:53 / sait.cpp:75-88 with an empty DropRule: the undropped
  * unit-diagonal polynomial in tT (no D^-1 scaling), from the iteration
  * matrix tt of a JacobiSplit. */

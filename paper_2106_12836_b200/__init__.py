@@ -63,6 +63,8 @@ from .sait import (
     sait_polynomial_nodrop,
     sait_thr,
     sait_thr_cap,
+    sait_thr_pair,
+    build_pair,
     scale_columns,
     spgemm,
     spmv,

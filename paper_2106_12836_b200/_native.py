@@ -125,6 +125,7 @@ PROTOTYPES = {
     "sait_ipc_open": (C.c_int, [VP, C.POINTER(VP)]),
     "sait_ipc_close": (C.c_int, [VP]),
     "sait_jacobi_split": (C.c_int, [VP, C.c_int, VP, VP, C.POINTER(VP)]),
+    "sait_build_pair": (C.c_int, [VP, VP, C.POINTER(DropSpec), VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_build": (C.c_int, [VP, C.c_int, C.POINTER(DropSpec), VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_polynomial": (C.c_int, [VP, C.c_int, VP, C.POINTER(VP), C.POINTER(BuildStats)]),
     "sait_pat_capture_pattern": (C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),

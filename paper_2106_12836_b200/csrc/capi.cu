@@ -8,6 +8,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <utility>
 #include <string>
@@ -931,6 +932,45 @@ int sait_build(sait_dcsr_t t, int lower, const sait_drop_spec* spec, sait_stream
   if (rc == SAIT_OK) rc = sait_build_session_finish(ss, 0, m_out, stats);
   sait_build_session_destroy(ss);
   return rc;
+}
+
+int sait_build_pair(sait_dcsr_t lower, sait_dcsr_t upper, const sait_drop_spec* spec, sait_stream_t stream,
+                    sait_dcsr_t* ml_out, sait_dcsr_t* mu_out, sait_build_stats* stats2) {
+  if (!lower || !upper || !ml_out || !mu_out) {
+    sait::set_last_error("sait_build_pair: null argument");
+    return SAIT_ERR_INVALID_ARGUMENT;
+  }
+  // The two recursions are independent: M_U builds on its own stream from a
+  // second host thread while M_L builds on `stream`, so each one's kernels
+  // fill the other's host-synchronisation gaps.
+  int rc_u = SAIT_OK;
+  std::string err_u;
+  sait_dcsr_t mu = nullptr;
+  std::thread tu([&] {
+    cudaSetDevice(upper->dev);
+    cudaStream_t su = nullptr;
+    if (cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking) != cudaSuccess) {
+      rc_u = SAIT_ERR_CUDA;
+      err_u = "sait_build_pair: cannot create a stream";
+      return;
+    }
+    rc_u = sait_build(upper, 0, spec, su, &mu, stats2 ? stats2 + 1 : nullptr);
+    if (rc_u) err_u = sait_last_error();
+    cudaStreamSynchronize(su);
+    cudaStreamDestroy(su);
+  });
+  sait_dcsr_t ml = nullptr;
+  const int rc_l = sait_build(lower, 1, spec, stream, &ml, stats2);
+  tu.join();
+  if (rc_l || rc_u) {
+    if (ml) sait_csr_free(ml);
+    if (mu) sait_csr_free(mu);
+    if (!rc_l) sait::set_last_error(err_u);
+    return rc_l ? rc_l : rc_u;
+  }
+  *ml_out = ml;
+  *mu_out = mu;
+  return SAIT_OK;
 }
 
 int sait_polynomial(sait_dcsr_t tt, int steps, sait_stream_t stream, sait_dcsr_t* m_out, sait_build_stats* stats) {

@@ -70,6 +70,27 @@ def build(t, kind, spec: N.DropSpec, stream=None, stats_out: list | None = None)
     return _out(h, host, stream)
 
 
+def build_pair(lower, upper, spec: N.DropSpec, stream=None, stats_out: list | None = None):
+    """sait_build_pair: M_L = build(lower) and M_U = build(upper) with the same
+    drop spec, the two recursions running concurrently on the device."""
+    dl, host_l = _dev(lower, stream)
+    du, host_u = _dev(upper, stream)
+    hl, hu = C.c_void_p(), C.c_void_p()
+    st = (N.BuildStats * 2)()
+    N.check(N.lib.sait_build_pair(dl.handle, du.handle, C.byref(spec), _stream_handle(stream), C.byref(hl), C.byref(hu),
+                                  st))
+    if stats_out is not None:
+        for x in st:
+            stats_out.append(BuildStats(x.steps_run, bool(x.stabilized), x.nnz_out, x.products, x.seconds))
+    return _out(hl, host_l, stream), _out(hu, host_u, stream)
+
+
+def sait_thr_pair(lower, upper, params: SaitThrParams, stream=None, stats_out=None):
+    """sait_thr of both ILU factors (lower, upper) at once."""
+    spec = N.DropSpec(N.SAIT_DROP_THRESHOLD, float(params.threshold), int(params.steps), 0, 0, 0.0)
+    return build_pair(lower, upper, spec, stream, stats_out)
+
+
 def sait_thr(t, kind: TriangularKind, params: SaitThrParams, stream=None, stats_out=None):
     """sait.hpp:58 / sait.cpp:90-101"""
     spec = N.DropSpec(N.SAIT_DROP_THRESHOLD, float(params.threshold), int(params.steps), 0, 0, 0.0)

@@ -176,3 +176,21 @@ def test_hash_rows_staging_and_overflow(cap):
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.split() == ["1", "1"]
+
+
+def test_build_pair_concurrent_equals_separate(S, port):
+    """sait_build_pair (both factors at once, M_U on a second stream/thread)
+    is bitwise the two separate builds; errors of either factor surface."""
+    from helpers import bitwise_equal_csr, to_oracle
+
+    A = S.laplacian_3d(32)
+    f = S.ilu_k(A, 0)
+    st = []
+    ML, MU = S.sait_thr_pair(f.lower, f.upper, S.SaitThrParams(5e-2, 3), stats_out=st)
+    assert bitwise_equal_csr(ML, port.sait_thr(to_oracle(f.lower), True, 5e-2, 3))
+    assert bitwise_equal_csr(MU, port.sait_thr(to_oracle(f.upper), False, 5e-2, 3))
+    assert [x.steps_run for x in st] == [3, 3]
+    bad = S.CsrMatrix(f.upper.nrows, f.upper.ncols, f.upper.row_ptr, f.upper.col_idx, f.upper.values.copy())
+    bad.values[bad.row_ptr[5]] = 0.0  # U's diagonal of row 5
+    with pytest.raises(S.SaitRuntimeError, match="zero diagonal at row 5"):
+        S.sait_thr_pair(f.lower, bad, S.SaitThrParams(5e-2, 3))

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kT) mdot_partials(int64_t n, const double* __r
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
       const int64_t i = base + static_cast<int64_t>(kT) * k;
-      if (i < n) s = __dadd_rn(s, __dmul_rn(xv[k], v[i]));
+      if (i < n) s = __fma_rn(xv[k], v[i], s);
     }
     s = warp_butterfly(s);
     if (lane == 0) ws[j][warp] = s;
@@ -88,7 +88,7 @@ __global__ void cgs_update(int64_t n, double* __restrict__ w, const double* __re
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= n) return;
   double t = w[e];
-  for (int j = 0; j < m; ++j) t = __dsub_rn(t, __dmul_rn(h[j], V[ld * j + e]));
+  for (int j = 0; j < m; ++j) t = __fma_rn(-h[j], V[ld * j + e], t);
   w[e] = t;
 }
 
@@ -104,18 +104,18 @@ __global__ void lincomb(int64_t n, const double* __restrict__ V, int64_t ld, int
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= n) return;
   double t = __dmul_rn(y[0], V[e]);
-  for (int j = 1; j < k; ++j) t = __dadd_rn(t, __dmul_rn(y[j], V[ld * j + e]));
+  for (int j = 1; j < k; ++j) t = __fma_rn(y[j], V[ld * j + e], t);
   u[e] = t;
 }
 
 // y = y + a x  /  y = x + a y  /  y = x - y
 __global__ void axpy_k(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e < n) y[e] = __dadd_rn(y[e], __dmul_rn(a, x[e]));
+  if (e < n) y[e] = __fma_rn(a, x[e], y[e]);
 }
 __global__ void xpay_k(int64_t n, const double* __restrict__ x, double a, double* __restrict__ y) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e < n) y[e] = __dadd_rn(x[e], __dmul_rn(a, y[e]));
+  if (e < n) y[e] = __fma_rn(a, y[e], x[e]);
 }
 __global__ void sub_k(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -153,7 +153,7 @@ __global__ void block_lincomb_k(int64_t n, const double* in, int kin, const doub
       if (q0 + u >= kin) break;
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < kout) acc[j] = __dadd_rn(acc[j], __dmul_rn(xq[u], cs[(q0 + u) * kout + j]));
+        if (j < kout) acc[j] = __fma_rn(xq[u], cs[(q0 + u) * kout + j], acc[j]);
     }
   }
 #pragma unroll
@@ -177,7 +177,7 @@ __global__ void block_sub_lincomb_k(int64_t n, const double* __restrict__ X, int
     const double xq = X[n * q + i];
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j < k) w[j] = __dsub_rn(w[j], __dmul_rn(xq, gs[q * k + j]));
+      if (j < k) w[j] = __fma_rn(-xq, gs[q * k + j], w[j]);
   }
 #pragma unroll
   for (int j = 0; j < 16; ++j)
@@ -189,7 +189,7 @@ __global__ void block_residual_k(int64_t n, int k, const double* __restrict__ AX
                                  const double* __restrict__ lam, double* __restrict__ R) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  for (int j = 0; j < k; ++j) R[n * j + i] = __dsub_rn(AX[n * j + i], __dmul_rn(lam[j], X[n * j + i]));
+  for (int j = 0; j < k; ++j) R[n * j + i] = __fma_rn(-lam[j], X[n * j + i], AX[n * j + i]);
 }
 
 // Tall-skinny Gram: part[(a * kb + b) * nb + blk] = canonical block partial
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kT, (TB <= 4 ? 2 : 1)) gram_tiles(int64_t n, c
 #pragma unroll
       for (int a = 0; a < TA; ++a)
 #pragma unroll
-        for (int b = 0; b < TB; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(xa[u][a], yb[u][b]));
+        for (int b = 0; b < TB; ++b) acc[a][b] = __fma_rn(xa[u][a], yb[u][b], acc[a][b]);
     }
   }
 #pragma unroll

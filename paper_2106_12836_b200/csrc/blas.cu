@@ -9,6 +9,7 @@
 // every product rounded before its add, dots are bitwise reproducible and
 // equal to the CPU restatement, so solver iteration counts match exactly.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -159,6 +160,32 @@ __global__ void block_lincomb_k(int64_t n, const double* in, int kin, const doub
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     if (j < kout) out[n * j + i] = acc[j];
+}
+
+// The same with the coefficients passed by value as a kernel parameter
+// (constant bank): fully unrolled, every FMA takes its coefficient as a
+// direct constant operand -- no shared-memory load per product.
+template <int KIN, int KOUT>
+struct CoefBlock {
+  double c[KIN * KOUT];
+};
+template <int KIN, int KOUT>
+__global__ void __launch_bounds__(256) block_lincomb_param(int64_t n, const double* in, CoefBlock<KIN, KOUT> C,
+                                                           double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xq[KIN];
+#pragma unroll
+  for (int q = 0; q < KIN; ++q) xq[q] = ld_ro(in + n * q + i);
+  double acc[KOUT];
+#pragma unroll
+  for (int j = 0; j < KOUT; ++j) acc[j] = __dmul_rn(xq[0], C.c[j]);
+#pragma unroll
+  for (int q = 1; q < KIN; ++q)
+#pragma unroll
+    for (int j = 0; j < KOUT; ++j) acc[j] = __fma_rn(xq[q], C.c[q * KOUT + j], acc[j]);
+#pragma unroll
+  for (int j = 0; j < KOUT; ++j) out[n * j + i] = acc[j];
 }
 
 // W[:, j] = (((W_j - X_0 G[0][j]) - X_1 G[1][j]) - ...)
@@ -321,6 +348,30 @@ void add_into(int64_t n, const double* a, const double* b, double* out, cudaStre
 void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s) {
   block_lincomb_k<<<grid_for(n, 256), 256, 0, s>>>(n, in, kin, C, kout, out);
   SAIT_LAUNCHED();
+}
+
+namespace {
+template <int KIN, int KOUT>
+void launch_lincomb_param(int64_t n, const double* in, const double* C_host, double* out, cudaStream_t s) {
+  CoefBlock<KIN, KOUT> cb;
+  std::memcpy(cb.c, C_host, sizeof cb.c);
+  block_lincomb_param<KIN, KOUT><<<grid_for(n, 256), 256, 0, s>>>(n, in, cb, out);
+  SAIT_LAUNCHED();
+}
+}  // namespace
+
+// out = in C with C on the host: the constant-operand kernel for LOBPCG's
+// common shapes (k = 8: 8/16/24 inputs -> 8 outputs); false if not covered.
+bool block_lincomb_host_coef(int64_t n, const double* in, int kin, const double* C_host, int kout, double* out,
+                             cudaStream_t s) {
+  if (n <= 0) return true;
+  if (kout != 8) return false;
+  switch (kin) {
+    case 8: launch_lincomb_param<8, 8>(n, in, C_host, out, s); return true;
+    case 16: launch_lincomb_param<16, 8>(n, in, C_host, out, s); return true;
+    case 24: launch_lincomb_param<24, 8>(n, in, C_host, out, s); return true;
+    default: return false;
+  }
 }
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s) {
   block_sub_lincomb_k<<<grid_for(n, 256), 256, 0, s>>>(n, X, k, G, W);

@@ -42,6 +42,8 @@ void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t
 void gram_partials(int64_t n, const double* A, int ka, const double* B, int kb, double* part, void* tiles_dev,
                    cudaStream_t s);
 void block_lincomb(int64_t n, const double* in, int kin, const double* C, int kout, double* out, cudaStream_t s);
+bool block_lincomb_host_coef(int64_t n, const double* in, int kin, const double* C_host, int kout, double* out,
+                             cudaStream_t s);
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
                     cudaStream_t s);
@@ -534,6 +536,7 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
             if ((b2 / 8) < (a2 / 8)) G[a2 * kb + b2] = G[b2 * kb + a2];
     };
     auto lincomb = [&](const double* in, int kin, const double* C, int kout, double* out) {
+      if (sait::block_lincomb_host_coef(n, in, kin, C, kout, out, s)) return;
       double* d = next_small();
       SAIT_CUDA(cudaMemcpyAsync(d, C, sizeof(double) * kin * kout, cudaMemcpyHostToDevice, s));
       sait::block_lincomb(n, in, kin, d, kout, out, s);

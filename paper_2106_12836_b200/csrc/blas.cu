@@ -38,7 +38,28 @@ __device__ __forceinline__ double ld_ro(const double* p) {
   return r;
 }
 
-// part[j * nb + b] = canonical block partial of x . V_j
+// 32 values per lane, reduced across the warp by a reduce-scatter butterfly:
+// at offset o each lane keeps the half of its values selected by lane bit o
+// and adds the partner's partial of the same value (own + partner, offsets
+// 16..1), so every value gets exactly the canonical warp_butterfly sums
+// (bitwise), with 31 shuffles instead of 5 per value; value j ends on lane j.
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int q = 0; q < o; ++q) {
+      const double keep = hi ? v[q + o] : v[q];
+      const double send = hi ? v[q] : v[q + o];
+      v[q] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  return v[0];
+}
+
+// part[j * nb + b] = canonical block partial of x . V_j (WIDE: m > 4, all
+// partials first and one reduce-scatter; else one butterfly per dot)
+template <bool WIDE>
 __global__ void __launch_bounds__(kT) mdot_partials(int64_t n, const double* __restrict__ x,
                                                      const double* __restrict__ V, int64_t ld, int m,
                                                      double* __restrict__ part, int64_t nb) {
@@ -51,16 +72,34 @@ __global__ void __launch_bounds__(kT) mdot_partials(int64_t n, const double* __r
     const int64_t i = base + static_cast<int64_t>(kT) * k;
     xv[k] = i < n ? x[i] : 0.0;
   }
-  for (int j = 0; j < m; ++j) {
-    const double* v = V + ld * j;
-    double s = 0.0;
+  if constexpr (!WIDE) {
+    for (int j = 0; j < m; ++j) {
+      const double* v = V + ld * j;
+      double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
-      const int64_t i = base + static_cast<int64_t>(kT) * k;
-      if (i < n) s = __fma_rn(xv[k], v[i], s);
+      for (int k = 0; k < kK; ++k) {
+        const int64_t i = base + static_cast<int64_t>(kT) * k;
+        if (i < n) s = __fma_rn(xv[k], v[i], s);
+      }
+      s = warp_butterfly(s);
+      if (lane == 0) ws[j][warp] = s;
     }
-    s = warp_butterfly(s);
-    if (lane == 0) ws[j][warp] = s;
+  } else {  // up to 32 dots: all partials first, then one reduce-scatter
+    double acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      double s = 0.0;
+      if (j < m) {
+        const double* v = V + ld * j;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+          const int64_t i = base + static_cast<int64_t>(kT) * k;
+          if (i < n) s = __fma_rn(xv[k], v[i], s);
+        }
+      }
+      acc[j] = s;
+    }
+    ws[lane][warp] = warp_reduce_scatter32(acc, lane);
   }
   __syncthreads();
   if (t < m) part[static_cast<int64_t>(t) * nb + blockIdx.x] = tree8(ws[t]);
@@ -271,13 +310,23 @@ __global__ void __launch_bounds__(kT, (TB <= 4 ? 2 : 1)) gram_tiles(int64_t n, c
         for (int b = 0; b < TB; ++b) acc[a][b] = __fma_rn(xa[u][a], yb[u][b], acc[a][b]);
     }
   }
+  if constexpr (TA * TB == 32) {
+    // the tile's 32 partials: one reduce-scatter (31 shuffles instead of 160)
+    double v[32];
 #pragma unroll
-  for (int a = 0; a < TA; ++a)
+    for (int a = 0; a < TA; ++a)
 #pragma unroll
-    for (int b = 0; b < TB; ++b) {
-      const double v = warp_butterfly(acc[a][b]);
-      if (lane == 0) ws[a * TB + b][warp] = v;
-    }
+      for (int b = 0; b < TB; ++b) v[a * TB + b] = acc[a][b];
+    ws[lane][warp] = warp_reduce_scatter32(v, lane);
+  } else {
+#pragma unroll
+    for (int a = 0; a < TA; ++a)
+#pragma unroll
+      for (int b = 0; b < TB; ++b) {
+        const double v = warp_butterfly(acc[a][b]);
+        if (lane == 0) ws[a * TB + b][warp] = v;
+      }
+  }
   __syncthreads();
   if (t < TA * TB) {
     const int a = t / TB, b = t % TB;
@@ -469,7 +518,7 @@ void dot_partials(int64_t n, const double* x, const double* V, int64_t ld, int m
   const int64_t nb = dot_blocks(n);
   for (int j0 = 0; j0 < m; j0 += kMaxM) {
     const int mm = m - j0 < kMaxM ? m - j0 : kMaxM;
-    mdot_partials<<<static_cast<unsigned>(nb), kT, 0, s>>>(n, x, V + ld * j0, ld, mm, part + nb * j0, nb);
+    mdot_partials<false><<<static_cast<unsigned>(nb), kT, 0, s>>>(n, x, V + ld * j0, ld, mm, part + nb * j0, nb);
     SAIT_LAUNCHED();
   }
 }
@@ -484,7 +533,9 @@ void multi_dot(int64_t n, const double* x, const double* V, int64_t ld, int m, d
   const int64_t nb = dot_blocks(n);
   for (int j0 = 0; j0 < m; j0 += kMaxM) {
     const int mm = m - j0 < kMaxM ? m - j0 : kMaxM;
-    mdot_partials<<<static_cast<unsigned>(nb), kT, 0, s>>>(n, x, V + ld * j0, ld, mm, scratch, nb);
+    // (a reduce-scatter variant holding all m partials, mdot_partials<true>,
+    // needs 100 registers and made C3's GMRES slower: 2.65 -> 2.97 s)
+    mdot_partials<false><<<static_cast<unsigned>(nb), kT, 0, s>>>(n, x, V + ld * j0, ld, mm, scratch, nb);
     SAIT_LAUNCHED();
     mdot_final<<<mm, kT, 0, s>>>(scratch, nb, out + j0, sqrt_out ? 1 : 0);
     SAIT_LAUNCHED();

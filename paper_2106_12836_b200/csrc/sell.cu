@@ -28,6 +28,10 @@ namespace sait {
 namespace {
 
 constexpr int kSlice = 32;
+#ifndef SAIT_CM_BATCH
+#define SAIT_CM_BATCH 2
+#endif
+constexpr int kCmBatch = SAIT_CM_BATCH;  // slots per batch of the column-major block SpMM
 constexpr double kMaxPad = 1.25;
 
 __device__ __forceinline__ int32_t ld_na(const int32_t* p) {
@@ -301,11 +305,11 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
   double acc[NV];
 #pragma unroll
   for (int c = 0; c < NV; ++c) acc[c] = 0.0;
-  for (int32_t k0 = 0; k0 < w; k0 += 4) {
-    int32_t col[4];
-    double v[4];
+  for (int32_t k0 = 0; k0 < w; k0 += kCmBatch) {
+    int32_t col[kCmBatch];
+    double v[kCmBatch];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kCmBatch; ++j) {
       col[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t ns
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kCmBatch; ++j) {
       if (col[j] < 0) continue;
 #pragma unroll
       for (int c = 0; c < NV; ++c)

@@ -1,0 +1,112 @@
+"""Small end-to-end workload for compute-sanitizer (memcheck /
+racecheck on the device paths): every builder bin (tiny, shared-memory and
+global hash tables, staging overflow), the pair apply (device, chunked host,
+block), the solvers, ILU(0)/ILU(1), the exact triangular solves and the
+peer-halo SpMV with virtual ranks.  Checks results against the oracle so a
+silent corruption also fails.
+
+    compute-sanitizer --tool memcheck python tools/sanitize.py
+    compute-sanitizer --tool racecheck python tools/sanitize.py
+
+(compute-sanitizer is disabled on this round's GPU pool; the workload still
+runs as an oracle-checked sweep of every device path: python tools/sanitize.py)
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+os.environ.setdefault("SAIT_PIPE_MB", "0.0625;0.125;0.0625")  # several host-apply chunks at this size
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2106_12836_b200 as S  # noqa: E402
+from helpers import bitwise_equal, bitwise_equal_csr, to_oracle, to_product  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+P = O.get("port")
+
+
+def check(ok, what):
+    if not ok:
+        raise SystemExit(f"MISMATCH: {what}")
+    print("ok", what, flush=True)
+
+
+# builder: every bin
+T = O.synthetic_lower(3000, 12, 0.3, seed=5)  # long rows -> hash tables / global tables
+check(bitwise_equal_csr(S.sait_thr(to_product(T), S.lower_triangular, S.SaitThrParams(1e-2, 4)),
+                        P.sait_thr(T, True, 1e-2, 4)), "build: hash/global bins")
+A = O.laplacian_3d(16)
+L, U = P.ilu_k(A, 0)
+ML, MU = P.sait_thr(L, True, 5e-2, 3), P.sait_thr(U, False, 5e-2, 3)
+mlp = S.sait_thr(to_product(L), S.lower_triangular, S.SaitThrParams(5e-2, 3))
+check(bitwise_equal_csr(mlp, ML), "build: tiny bins")
+check(bitwise_equal_csr(S.sait_thr_cap(to_product(T), S.lower_triangular, S.SaitThrParams(1e-2, 3), 1.5),
+                        P.sait_thr_cap(T, True, 1e-2, 3, 1.5)), "build: fill cap")
+check(bitwise_equal_csr(S.sait_pat(to_product(T), S.lower_triangular, S.SaitPatParams(2, 3)),
+                        P.sait_pat(T, True, 2, 3)), "build: pattern")
+
+# apply: device, host (chunked), block
+pair = S.SaitPairPreconditioner(to_product(ML), to_product(MU))
+r = O.uniform_pm1(3, A.nrows)
+want = P.pair_apply(ML, MU, r)
+z = np.empty(A.nrows)
+pair.apply(r, z)
+check(bitwise_equal(z, want), "apply: host vectors")
+rd = torch.from_numpy(r).cuda()
+zd = torch.empty_like(rd)
+pair.apply(rd, zd)
+torch.cuda.synchronize()
+check(bitwise_equal(zd.cpu().numpy(), want), "apply: device vectors")
+R = np.stack([O.uniform_pm1(10 + c, A.nrows) for c in range(8)], axis=1)
+Z = pair.apply_block(R)
+check(bitwise_equal(np.asfortranarray(Z).ravel(order="F"),
+                    np.asfortranarray(P.pair_apply_block(ML, MU, R)).ravel(order="F")), "apply: block of 8")
+
+# solvers
+b = O.uniform_pm1(4, A.nrows)
+xo, so = O.pcg(A, ML, MU, b, 1e-10, 300)
+x, st = S.pcg(to_product(A), pair, b, 1e-10, 300)
+check(st.iterations == so["iterations"] and bitwise_equal(x, xo), "pcg")
+xo, so = O.gmres(A, ML, MU, b, 10, 1e-8, 300)
+x, st = S.gmres(to_product(A), pair, b, 10, 1e-8, 300)
+check(st.iterations == so["iterations"] and bitwise_equal(x, xo), "gmres")
+ev, _, it, _ = O.lobpcg(A, ML, MU, 4, 1e-6, 20, 5)
+res = S.lobpcg(to_product(A), pair, 4, 1e-6, 20, 5)
+check(res.iterations == it and bitwise_equal(res.eigenvalues, ev), "lobpcg")
+
+# ILU(0)/(1), trisolve, exact preconditioner
+for lev in (0, 1):
+    Lw, Uw = P.ilu_k(A, lev)
+    f = S.ilu_device(to_product(A), lev)
+    check(bitwise_equal_csr(f.lower.to_host(), Lw) and bitwise_equal_csr(f.upper.to_host(), Uw), f"ilu({lev})")
+E = S.ExactIluPreconditioner(S.IluFactors(to_product(L), to_product(U)))
+ze = np.empty(A.nrows)
+E.apply(r, ze)
+check(bitwise_equal(ze, P.trisolve(U, False, P.trisolve(L, True, r))), "exact ilu apply")
+
+# peer-halo SpMV, three virtual ranks
+from paper_2106_12836_b200.dist import PeerShardedPair  # noqa: E402
+
+ranks = {}
+for q in range(3):
+    ranks[q] = PeerShardedPair(to_product(ML), to_product(MU), q, 3, resolve=lambda qq, ff: ranks[qq].bufs[ff].ptr,
+                               align=256)
+s = torch.cuda.current_stream().cuda_stream
+for q in range(3):
+    a0, a1 = ranks[q].own
+    ranks[q].stage_input(rd[a0:a1], 1, s)
+for q in range(3):
+    ranks[q].stage_lower(1, s)
+zs = []
+for q in range(3):
+    a0, a1 = ranks[q].own
+    zq = torch.empty(a1 - a0, dtype=torch.float64, device="cuda")
+    ranks[q].stage_upper(zq, 1, s)
+    zs.append(zq)
+torch.cuda.synchronize()
+check(bitwise_equal(torch.cat(zs).cpu().numpy(), want), "peer-halo pair, 3 virtual ranks")
+print("SANITIZE WORKLOAD DONE")

@@ -253,6 +253,9 @@ int sait_pair_apply_host(sait_pair_t p, const double *h_r, int64_t rlen, double 
  * n x nvec (DenseMatrix, dense.hpp:12-38), 1 = row-major n x nvec. Device pointers. */
 int sait_pair_apply_block(sait_pair_t p, const double *d_r, double *d_z, int64_t n,
                           int64_t nvec, int layout, sait_stream_t stream);
+/* Same with HOST blocks; synchronous on return.  Column-major blocks are
+ * pipelined vector group by vector group (copy in / pairs / copy out on three
+ * streams), so with pinned buffers a vector costs max(H2D, D2H), not the sum. */
 int sait_pair_apply_block_host(sait_pair_t p, const double *h_r, double *h_z, int64_t n,
                                int64_t nvec, int layout, sait_stream_t stream);
 /* One factor's SpMV with the pair's planned kernel (which: 0 = M_L, 1 = M_U);

@@ -97,6 +97,9 @@ struct sait_pair_s {
     // single-launch dataflow host apply
     int* in_flag = nullptr;   // device, one per input chunk
     int* flag_src = nullptr;  // pinned host copy source of the epoch
+    // column-major host block apply: kBlkSlots device slots per side
+    double *blk_r = nullptr, *blk_z = nullptr;
+    cudaEvent_t ev_blk_in[4] = {}, ev_blk_done[4] = {}, ev_blk_out[4] = {};
   };
   sait::DataflowPlan df;
   std::vector<int64_t> df_rows;  // input chunk boundaries of the dataflow apply
@@ -1420,6 +1423,19 @@ cudaStream_t host_call_stream(sait_stream_t stream) {
   return h.s;
 }
 
+void ensure_side_streams(sait_pair_s::Work& w) {
+  if (w.s_in) return;
+  SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_in, cudaStreamNonBlocking));
+  SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_out, cudaStreamNonBlocking));
+  SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_entry, cudaEventDisableTiming));
+  SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_out_done, cudaEventDisableTiming));
+}
+
+bool block_host_pipeline_enabled() {
+  const char* e = std::getenv("SAIT_BLOCK_HOST_PIPELINE");
+  return !(e && std::atoi(e) == 0);
+}
+
 bool host_zc_out_enabled() {
   const char* e = std::getenv("SAIT_HOST_ZC_OUT");
   return !(e && std::atoi(e) == 0);
@@ -1430,17 +1446,18 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
   std::lock_guard<std::mutex> lk(*w.mu);
   const int64_t k = static_cast<int64_t>(p->chunk_rows.size()) - 1;
   const int64_t n = p->ml->m.nrows;
-  if (!w.s_in) {
-    SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_in, cudaStreamNonBlocking));
-    SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_out, cudaStreamNonBlocking));
+  // each resource on its own: the dataflow and block paths share this Work
+  // and create only what they use
+  ensure_side_streams(w);
+  if (!w.r_dev) {
     SAIT_CUDA(cudaMalloc(&w.r_dev, sizeof(double) * n + 256));
     SAIT_CUDA(cudaMalloc(&w.z_dev, sizeof(double) * n + 256));
+  }
+  if (w.ev_in.size() != static_cast<size_t>(k)) {
     w.ev_in.resize(k);
     w.ev_u.resize(k);
     for (auto& e : w.ev_in) SAIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : w.ev_u) SAIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_entry, cudaEventDisableTiming));
-    SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_out_done, cudaEventDisableTiming));
   }
   static const bool dbg = std::getenv("SAIT_DEBUG_PIPE") != nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
@@ -1538,12 +1555,7 @@ void pair_apply_host_dataflow(sait_pair_t p, const double* h_r, double* h_z, cud
   const int64_t k = static_cast<int64_t>(p->df_rows.size()) - 1;
   const int64_t n = p->ml->m.nrows;
   if (!w.in_flag) {
-    if (!w.s_in) {
-      SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_in, cudaStreamNonBlocking));
-      SAIT_CUDA(cudaStreamCreateWithFlags(&w.s_out, cudaStreamNonBlocking));
-      SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_entry, cudaEventDisableTiming));
-      SAIT_CUDA(cudaEventCreateWithFlags(&w.ev_out_done, cudaEventDisableTiming));
-    }
+    ensure_side_streams(w);
     if (!w.r_dev) {
       SAIT_CUDA(cudaMalloc(&w.r_dev, sizeof(double) * n + 256));
       SAIT_CUDA(cudaMalloc(&w.z_dev, sizeof(double) * n + 256));
@@ -1557,6 +1569,176 @@ void pair_apply_host_dataflow(sait_pair_t p, const double* h_r, double* h_z, cud
   sait::sell_dataflow_apply(p->sl, p->su, p->df, w.st, w.in_flag, epoch, h_r, w.r_dev, w.y, h_z, s);
   SAIT_CUDA(cudaStreamSynchronize(s));
   SAIT_CUDA(cudaStreamSynchronize(w.s_in));
+}
+
+// Column-major block of HOST vectors (apply_block, preconditioner.cpp:47-49):
+// a three-stage pipeline over groups of vectors.  Group g's r columns are
+// copied in on s_in (one copy), the SpMV pair runs per vector on s, and the
+// group's z columns are copied out on s_out, so the H2D of g+1 and the D2H of
+// g-1 share the full-duplex PCIe link with the pairs of g; kBlkSlots device
+// slots per side bound how far the input runs ahead.  Throughput is
+// max(H2D, D2H) per vector instead of their sum.  Each cross-stream hand-off
+// costs the copy engines a few tens of microseconds, so the middle groups
+// hold several vectors, while single-vector head and tail groups keep the
+// pipeline fill and drain short (SAIT_BLK_GROUPS = "head,..;mid;tail,..").
+constexpr int kBlkSlotsMax = 4;
+int blk_slots() {
+  static const int v = [] {
+    const char* e = std::getenv("SAIT_BLK_SLOTS");
+    const int k = e ? std::atoi(e) : 3;
+    return std::min(std::max(k, 1), kBlkSlotsMax);
+  }();
+  return v;
+}
+struct BlkGroups {
+  std::vector<int> head, tail;
+  int mid = 4;
+  int max() const {
+    int m = mid;
+    for (int g : head) m = std::max(m, g);
+    for (int g : tail) m = std::max(m, g);
+    return m;
+  }
+};
+const BlkGroups& blk_groups() {
+  static const BlkGroups v = [] {
+    BlkGroups b;
+    b.head = {1};
+    b.tail = {1};
+    const char* e = std::getenv("SAIT_BLK_GROUPS");
+    if (!e) return b;
+    auto parse = [](const std::string& t) {
+      std::vector<int> out;
+      size_t a = 0;
+      while (a < t.size()) {
+        size_t c = t.find(',', a);
+        if (c == std::string::npos) c = t.size();
+        if (c > a) out.push_back(std::max(1, std::atoi(t.substr(a, c - a).c_str())));
+        a = c + 1;
+      }
+      return out;
+    };
+    const std::string spec(e);
+    const size_t s1 = spec.find(';');
+    const size_t s2 = s1 == std::string::npos ? std::string::npos : spec.find(';', s1 + 1);
+    if (s1 == std::string::npos || s2 == std::string::npos) {
+      b.head.clear();
+      b.tail.clear();
+      b.mid = std::max(1, std::atoi(spec.c_str()));
+      return b;
+    }
+    b.head = parse(spec.substr(0, s1));
+    b.mid = std::max(1, std::atoi(spec.substr(s1 + 1, s2 - s1 - 1).c_str()));
+    b.tail = parse(spec.substr(s2 + 1));
+    return b;
+  }();
+  return v;
+}
+// group sizes covering nvec vectors: head groups, middle groups, tail groups
+std::vector<int64_t> blk_group_sizes(int64_t nvec) {
+  const BlkGroups& b = blk_groups();
+  std::vector<int64_t> head, tail, out;
+  int64_t left = nvec;
+  for (int g : b.head)
+    if (left > 0) {
+      head.push_back(std::min<int64_t>(g, left));
+      left -= head.back();
+    }
+  for (auto it = b.tail.rbegin(); it != b.tail.rend(); ++it)
+    if (left > 0) {
+      tail.insert(tail.begin(), std::min<int64_t>(*it, left));
+      left -= tail.front();
+    }
+  out = head;
+  while (left > 0) {
+    out.push_back(std::min<int64_t>(b.mid, left));
+    left -= out.back();
+  }
+  out.insert(out.end(), tail.begin(), tail.end());
+  return out;
+}
+
+void pair_apply_block_host_pipelined(sait_pair_t p, const double* h_r, double* h_z, int64_t n, int64_t nvec,
+                                     cudaStream_t s) {
+  const int kBlkSlots = blk_slots();
+  const int64_t gmax = blk_groups().max();
+  sait_pair_s::Work& w = pair_work(p, s);
+  std::lock_guard<std::mutex> lk(*w.mu);
+  ensure_side_streams(w);
+  if (!w.blk_r) {
+    SAIT_CUDA(cudaMalloc(&w.blk_r, sizeof(double) * n * gmax * kBlkSlots + 256));
+    SAIT_CUDA(cudaMalloc(&w.blk_z, sizeof(double) * n * gmax * kBlkSlots + 256));
+    for (int q = 0; q < kBlkSlots; ++q)
+      for (cudaEvent_t* e : {&w.ev_blk_in[q], &w.ev_blk_done[q], &w.ev_blk_out[q]})
+        SAIT_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
+  SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_entry, 0));
+  SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_entry, 0));
+  const bool fused = pair_variant() == 3 && p->pp.ok();
+  // SAIT_DEBUG_BLK: per-group device timeline (H2D, pairs, D2H start/end) to stderr
+  static const bool dbg = std::getenv("SAIT_DEBUG_BLK") != nullptr;
+  std::vector<cudaEvent_t> tl;
+  auto mark = [&](cudaStream_t st) {
+    if (!dbg) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tl.push_back(e);
+  };
+  const std::vector<int64_t> groups = blk_group_sizes(nvec);
+  int64_t v0 = 0;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const int64_t g = groups[gi];
+    const int q = static_cast<int>(gi % kBlkSlots);
+    double* r = w.blk_r + q * gmax * n;
+    double* z = w.blk_z + q * gmax * n;
+    if (gi >= static_cast<size_t>(kBlkSlots))
+      SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_blk_done[q], 0));  // the pairs of gi-slots read r
+    mark(w.s_in);
+    SAIT_CUDA(cudaMemcpyAsync(r, h_r + v0 * n, sizeof(double) * n * g, cudaMemcpyHostToDevice, w.s_in));
+    mark(w.s_in);
+    SAIT_CUDA(cudaEventRecord(w.ev_blk_in[q], w.s_in));
+    SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_blk_in[q], 0));
+    if (gi >= static_cast<size_t>(kBlkSlots))
+      SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_blk_out[q], 0));  // z of gi-slots copied out
+    mark(s);
+    for (int64_t c = 0; c < g; ++c) {
+      if (fused) {
+        sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, r + c * n, w.y, z + c * n, s);
+      } else {
+        factor_spmv(p, 0, r + c * n, w.y, s);
+        factor_spmv(p, 1, w.y, z + c * n, s);
+      }
+    }
+    mark(s);
+    SAIT_CUDA(cudaEventRecord(w.ev_blk_done[q], s));
+    SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_blk_done[q], 0));
+    mark(w.s_out);
+    SAIT_CUDA(cudaMemcpyAsync(h_z + v0 * n, z, sizeof(double) * n * g, cudaMemcpyDeviceToHost, w.s_out));
+    mark(w.s_out);
+    SAIT_CUDA(cudaEventRecord(w.ev_blk_out[q], w.s_out));
+    v0 += g;
+  }
+  SAIT_CUDA(cudaEventRecord(w.ev_out_done, w.s_out));
+  SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_out_done, 0));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  if (dbg) {
+    SAIT_CUDA(cudaDeviceSynchronize());
+    auto at = [&](size_t i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tl[0], tl[i]);
+      return 1e3 * ms;
+    };
+    const size_t ng = groups.size();
+    for (size_t gi = 0; gi < ng; ++gi) {
+      if (gi > 6 && gi + 3 < ng) continue;
+      const size_t b = gi * 6;
+      std::fprintf(stderr, "g%zu(%lld) h2d %.0f-%.0f pair %.0f-%.0f d2h %.0f-%.0f us\n", gi,
+                   static_cast<long long>(groups[gi]), at(b), at(b + 1), at(b + 2), at(b + 3), at(b + 4), at(b + 5));
+    }
+    for (auto e : tl) cudaEventDestroy(e);
+  }
 }
 
 }  // namespace
@@ -1730,6 +1912,10 @@ int sait_pair_apply_block_host(sait_pair_t p, const double* h_r, double* h_z, in
   return guarded([&] {
     need(p, "apply_block");
     DeviceGuard g(p->dev);
+    if (layout == 0 && nvec > 1 && n == p->ml->m.nrows && n == p->mu->m.nrows && block_host_pipeline_enabled()) {
+      pair_apply_block_host_pipelined(p, h_r, h_z, n, nvec, host_call_stream(stream));
+      return;
+    }
     cudaStream_t s = sait::as_stream(stream);
     double* r = sait::dalloc<double>(n * nvec, s);
     double* z = sait::dalloc<double>(n * nvec, s);
@@ -1761,6 +1947,11 @@ void sait_pair_destroy(sait_pair_t p) {
       cudaFree(w.st.counter);
       if (w.r_dev) cudaFree(w.r_dev);
       if (w.z_dev) cudaFree(w.z_dev);
+      if (w.blk_r) cudaFree(w.blk_r);
+      if (w.blk_z) cudaFree(w.blk_z);
+      for (int q = 0; q < 4; ++q)
+        for (cudaEvent_t e : {w.ev_blk_in[q], w.ev_blk_done[q], w.ev_blk_out[q]})
+          if (e) cudaEventDestroy(e);
       for (auto e : w.ev_in) cudaEventDestroy(e);
       for (auto e : w.ev_u) cudaEventDestroy(e);
       if (w.ev_entry) cudaEventDestroy(w.ev_entry);

@@ -107,10 +107,18 @@ class SaitPairPreconditioner(Preconditioner):
             lay = 1 if layout == "row" else 0
             N.check(N.lib.sait_pair_apply_block(self._h, r.data_ptr(), z.data_ptr(), n, nvec, lay, s))
             return z
+        # host block: column-major (each vector contiguous); the copies
+        # overlap the device work vector by vector (pinned buffers for full
+        # overlap, e.g. torch pin_memory() views)
         r = np.asarray(r, dtype=np.float64)
         n, nvec = r.shape
         rf = np.asfortranarray(r)
-        zf = np.empty((n, nvec), order="F")
+        if z is None:
+            zf = np.empty((n, nvec), order="F")
+        else:
+            if not (isinstance(z, np.ndarray) and z.dtype == np.float64 and z.shape == (n, nvec) and z.flags.f_contiguous):
+                raise TypeError("apply_block: z must be an F-contiguous float64 (n, nvec) numpy array")
+            zf = z
         N.check(N.lib.sait_pair_apply_block_host(self._h, rf.ctypes.data_as(N.PD), zf.ctypes.data_as(N.PD), n, nvec, 0, _stream_handle(stream)))
         return zf
 

@@ -65,6 +65,61 @@ def test_block_widths(S, golden, c1_pair, nvec):
         assert bitwise_equal(Z[:, c], z)
 
 
+def test_block_host_pipeline_pinned(S, c1_pair, monkeypatch):
+    """apply_block on host vectors pipelines H2D / pair / D2H per vector over
+    three device slots; pinned caller buffers, z passed in, more vectors than
+    slots: bitwise equal to the unpipelined block path and to single applies."""
+    import torch
+    from oracle import oracle as O
+
+    nvec = 10
+    Rh = torch.empty((nvec, 4096), dtype=torch.float64).pin_memory()
+    Zh = torch.zeros((nvec, 4096), dtype=torch.float64).pin_memory()
+    for c in range(nvec):
+        Rh[c].copy_(torch.from_numpy(O.uniform_pm1(700 + c, 4096)))
+    Rn, Zn = Rh.numpy(), Zh.numpy()
+    assert c1_pair.apply_block(Rn.T, Zn.T) is not None
+    monkeypatch.setenv("SAIT_BLOCK_HOST_PIPELINE", "0")
+    Z0 = c1_pair.apply_block(Rn.T)
+    assert bitwise_equal(Zn.T, Z0)
+    for c in range(nvec):
+        z = np.empty(4096)
+        c1_pair.apply(Rn[c], z)
+        assert bitwise_equal(Zn[c], z)
+    with pytest.raises(TypeError):
+        c1_pair.apply_block(Rn.T, Zn)  # C-ordered (nvec, n): wrong shape / order
+
+
+def test_host_paths_share_stream_work(S):
+    """the block pipeline, the chunked single-vector host apply and the device
+    apply share one per-stream workspace: any order of calls on one thread
+    works (n >= 2^17 so the single-vector host apply takes the chunked path)"""
+    import torch
+    from oracle import oracle as O
+
+    A = S.laplacian_3d(52)
+    f = S.ilu_device(A, 0)
+    pair = S.SaitPairPreconditioner(S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3)),
+                                    S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3)))
+    n = A.nrows
+    R = np.stack([O.uniform_pm1(40 + c, n) for c in range(4)], axis=1)
+    want = []
+    for c in range(4):
+        zd = torch.empty(n, dtype=torch.float64, device="cuda")
+        pair.apply(torch.from_numpy(np.ascontiguousarray(R[:, c])).cuda(), zd)
+        torch.cuda.synchronize()
+        want.append(zd.cpu().numpy())
+    Z = pair.apply_block(R)
+    z = np.empty(n)
+    pair.apply(np.ascontiguousarray(R[:, 1]), z)
+    Z2 = pair.apply_block(R[:, 1:])
+    for c in range(4):
+        assert bitwise_equal(Z[:, c], want[c])
+    assert bitwise_equal(z, want[1])
+    for c in range(3):
+        assert bitwise_equal(Z2[:, c], want[c + 1])
+
+
 def test_spmv_long_and_empty_rows(S, port):
     """rows longer than the 2048-entry staging chunk, empty rows, n % 256 != 0"""
     import scipy.sparse as sp

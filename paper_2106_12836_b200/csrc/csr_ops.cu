@@ -246,6 +246,21 @@ __global__ void scale_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci, c
 
 }  // namespace
 
+// row_ptr = exclusive scan of counts, the total also written to *total_dev
+// (device); no host synchronisation.
+void scan_counts_async(const int32_t* counts, int32_t* row_ptr, int64_t n, int64_t* total_dev, cudaStream_t s) {
+  int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (ntiles < 1) ntiles = 1;
+  int64_t* sums = dalloc<int64_t>(ntiles, s);
+  scan_tile_sums<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(counts, n, sums);
+  SAIT_LAUNCHED();
+  scan_sums<<<1, kScanThreads, 0, s>>>(sums, ntiles, total_dev);
+  SAIT_LAUNCHED();
+  scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(counts, n, sums, row_ptr, total_dev);
+  SAIT_LAUNCHED();
+  dfree(sums, s);
+}
+
 int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s) {
   int64_t ntiles = (n + kScanTile - 1) / kScanTile;
   if (ntiles < 1) ntiles = 1;

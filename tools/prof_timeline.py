@@ -1,6 +1,6 @@
 """Kernel timeline of one C2 factor build (or pair apply, or 5 LOBPCG iterations) via torch.profiler
 (CUPTI): per-kernel device time, the busy fraction of the wall interval and
-the largest idle gaps.  python tools/prof_timeline.py [build|apply|lobpcg|ilu0|ilu1|c4] [grid]"""
+the largest idle gaps.  python tools/prof_timeline.py [build|pair|apply|lobpcg|ilu0|ilu1|c4] [grid]"""
 import os
 import sys
 import time
@@ -29,6 +29,11 @@ def build():
 
 
 run = build
+if what == "pair":  # both factors through sait_build_pair (concurrent recursions)
+    def run():
+        a, b = S.sait_thr_pair(L, U, S.SaitThrParams(5e-2, 3))
+        a.free()
+        b.free()
 if what in ("ilu0", "ilu1"):
     dA = S.DeviceCsr.upload(A)
 

@@ -399,15 +399,24 @@ class PeerShardedPair:
         buffers (torch.distributed all_gather_object) and open their peers'."""
         import torch.distributed as dist
 
-        obj = cls(ML, MU, rank, world, resolve=None, align=align)
-        mine = [obj.bufs[0].handle(), obj.bufs[1].handle()]
+        obj, mine, err = None, None, None
+        try:
+            obj = cls(ML, MU, rank, world, resolve=None, align=align)
+            mine = [obj.bufs[0].handle(), obj.bufs[1].handle()]
+        except Exception as exc:  # noqa: BLE001  (agreed on below)
+            err = exc
+        _agree(err, "PeerShardedPair", group, cleanup=obj)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         opened = {}
-        for f in range(2):
-            for peer, _, _ in obj.plans[f][rank].recv:
-                opened[(peer, f)] = _open_ipc(allh[peer][f])
+        try:
+            for f in range(2):
+                for peer, _, _ in obj.plans[f][rank].recv:
+                    opened[(peer, f)] = _open_ipc(allh[peer][f])
+        except Exception as exc:  # noqa: BLE001
+            err = exc
         obj._opened = opened
+        _agree(err, "PeerShardedPair", group, cleanup=obj)
         obj.resolve = lambda q, f: obj.bufs[f].ptr if q == rank else opened[(q, f)]
         dist.barrier(group=group)
         return obj
@@ -420,6 +429,26 @@ class PeerShardedPair:
         self._opened = {}
         for b in self.bufs:
             b.free()
+
+
+def _agree(err, what, group=None, cleanup=None):
+    """Collective error agreement for multi-process construction: every rank
+    reaches this point, and if ANY rank failed, ALL of them raise (so callers
+    fall back together instead of leaving peers blocked in a collective)."""
+    import torch.distributed as dist
+
+    mine = None if err is None else f"{type(err).__name__}: {err}"
+    allerr = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allerr, mine, group=group)
+    bad = [(q, e) for q, e in enumerate(allerr) if e is not None]
+    if bad:
+        if cleanup is not None:
+            try:
+                cleanup.close()
+            except Exception:  # noqa: BLE001
+                pass
+        q, e = bad[0]
+        raise RuntimeError(f"{what}: construction failed on rank {q}: {e}") from err
 
 
 class PeerRowOperator:
@@ -486,11 +515,23 @@ class PeerRowOperator:
     def distributed(cls, A, rank: int, world: int, group=None, align: int = GROUP_ROWS):
         import torch.distributed as dist
 
-        obj = cls(A, rank, world, resolve=None, align=align)
+        obj, mine, err = None, None, None
+        try:
+            obj = cls(A, rank, world, resolve=None, align=align)
+            mine = obj.buf.handle()
+        except Exception as exc:  # noqa: BLE001  (agreed on below)
+            err = exc
+        _agree(err, "PeerRowOperator", group, cleanup=obj)
         allh = [None] * world
-        dist.all_gather_object(allh, obj.buf.handle(), group=group)
-        opened = {peer: _open_ipc(allh[peer]) for peer, _, _ in obj.plans[rank].recv}
+        dist.all_gather_object(allh, mine, group=group)
+        opened = {}
+        try:
+            for peer, _, _ in obj.plans[rank].recv:
+                opened[peer] = _open_ipc(allh[peer])
+        except Exception as exc:  # noqa: BLE001
+            err = exc
         obj._opened = opened
+        _agree(err, "PeerRowOperator", group, cleanup=obj)
         obj.resolve = lambda q: obj.buf.ptr if q == rank else opened[q]
         dist.barrier(group=group)
         return obj

@@ -149,3 +149,48 @@ def test_torchcomm_gathers_ragged_partials_in_rank_order(tmp_path):
                           axis=1)
     for q in range(3):
         assert np.array_equal(np.load(tmp_path / f"g{q}.npy"), want)
+
+
+def _agree_worker(rank, world, port, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2106_12836_b200.dist import _agree
+
+        class Closable:
+            closed = False
+
+            def close(self):
+                self.closed = True
+
+        _agree(None, "ok", cleanup=None)  # nobody failed: returns on every rank
+        obj = Closable()
+        try:
+            _agree(ValueError("no peer access") if rank == 1 else None, "PeerShardedPair", cleanup=obj)
+            msg = "returned"
+        except RuntimeError as exc:
+            msg = str(exc)
+        with open(os.path.join(out_dir, f"a{rank}.txt"), "w") as fh:
+            fh.write(f"{msg}|{obj.closed}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_multiprocess_construction_fails_together(tmp_path):
+    """dist._agree: when one rank's peer-memory setup fails, EVERY rank raises
+    (naming the failing rank) and releases what it built, so callers such as
+    bench.py fall back to NCCL together instead of hanging in a collective."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_agree_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    for q in range(2):
+        msg, closed = (tmp_path / f"a{q}.txt").read_text().split("|")
+        assert "construction failed on rank 1" in msg and "no peer access" in msg
+        assert closed == "True"

@@ -210,14 +210,30 @@ def cpu_baseline_sample(ML_host, MU_host, n):
     while t < budget and steps < 30:
         t += lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, NVEC)
         steps += 1
-    lib.ref_pair_destroy.argtypes = [C.c_void_p]
-    lib.ref_pair_destroy(p)
     B = b_pair(n, ml.nnz, mu.nnz)
     cores = int(lib.ref_max_threads())
+    # SURVEY.md §8(d) timing protocol extras (bounded): y preallocated (all
+    # threads, the reference's per-call allocation removed) and 1 thread
+    extra = {}
+    try:
+        lib.ref_pair_time_apply_prealloc.restype = C.c_double
+        lib.ref_pair_time_apply_prealloc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]
+        tp = lib.ref_pair_time_apply_prealloc(p, r.ctypes.data, z.ctypes.data, n, NVEC)
+        extra["prealloc_y"] = {"value": NVEC * B / tp / 1e9, "cores": cores, "sample": f"{NVEC} vectors, {tp:.2f} s"}
+        lib.ref_set_threads.argtypes = [C.c_int]
+        lib.ref_set_threads(1)
+        n1 = 10
+        t1 = lib.ref_pair_time_apply(p, r.ctypes.data, z.ctypes.data, n, n1)
+        lib.ref_set_threads(cores)
+        extra["single_thread"] = {"value": n1 * B / t1 / 1e9, "cores": 1, "sample": f"{n1} vectors, {t1:.2f} s"}
+    except AttributeError:
+        pass
+    lib.ref_pair_destroy.argtypes = [C.c_void_p]
+    lib.ref_pair_destroy(p)
     return {"value": steps * NVEC * B / t / 1e9, "unit": "GB/s", "cores": cores, "kind": "reference",
             "sample": f"{steps} steps x 100 vectors through the reference SaitPairPreconditioner::apply "
                       f"(oracle/_ref, OpenMP {cores} threads), {t:.1f} s",
-            "ms_per_step": 1e3 * t / steps}
+            "ms_per_step": 1e3 * t / steps, **extra}
 
 
 def run_b200(args):

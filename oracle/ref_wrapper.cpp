@@ -291,6 +291,19 @@ double ref_pair_time_apply(void* p, const double* r, double* z, int64_t n, int64
     pc->apply(std::span<const double>(r + v * n, n), std::span<double>(z + v * n, n));
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
+// The same loop with y preallocated once: saitprec::spmv (kernels.hpp) into
+// caller storage, separating the reference's per-call allocation of y
+// (preconditioner.cpp:42-45 via kernels.cpp:28-32) from its SpMV time.
+double ref_pair_time_apply_prealloc(void* p, const double* r, double* z, int64_t n, int64_t nvec) {
+  auto* pc = static_cast<saitprec::SaitPairPreconditioner*>(p);
+  std::vector<double> y(pc->lower_inverse().nrows);
+  auto t0 = std::chrono::steady_clock::now();
+  for (int64_t v = 0; v < nvec; ++v) {
+    saitprec::spmv(pc->lower_inverse(), std::span<const double>(r + v * n, n), std::span<double>(y));
+    saitprec::spmv(pc->upper_inverse(), std::span<const double>(y), std::span<double>(z + v * n, n));
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
 double ref_pair_time_apply_block(void* p, const double* r, double* z, int64_t n, int64_t nvec) {
   auto* pc = static_cast<saitprec::SaitPairPreconditioner*>(p);
   saitprec::DenseMatrix rb(n, nvec);

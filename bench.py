@@ -261,7 +261,10 @@ def run_b200(args):
     # recursions run concurrently), host wall time around the synchronous
     # call; one warm-up build, then the median of BUILD_REPS builds (the GPU
     # clocks ramp during the first build after the host-side setup)
-    secs = []
+    # the library's device pool grown once up front (sait_device_pool_reserve),
+    # as an application that builds repeatedly would do
+    S.reserve_device_pool(4 << 30)
+    secs, first = [], None
     for rep in range(1 + BUILD_REPS):
         st = []
         if rep:
@@ -273,6 +276,8 @@ def run_b200(args):
         torch.cuda.synchronize()
         if rep:
             secs.append(time.perf_counter() - t0)
+        else:
+            first = time.perf_counter() - t0
     nnz_l, nnz_u = ML.nnz(), MU.nnz()
     t_build = sorted(secs)[len(secs) // 2]
     build = {
@@ -280,6 +285,7 @@ def run_b200(args):
         "seconds": t_build,
         "nnz_per_s": (nnz_l + nnz_u) / t_build,
         "samples_s": [round(x, 6) for x in secs],
+        "first_build_s": round(first, 6),
         "steps_run": [st[0].steps_run, st[1].steps_run],
         "products": st[0].products + st[1].products,
         "note": "both factors built concurrently (sait_build_pair), wall time of the call incl. "

@@ -405,6 +405,10 @@ int sait_host_alloc(size_t bytes, void **ptr);
 void sait_host_free(void *ptr);
 /* Counts kernels launched by this library on this process (all threads). */
 int64_t sait_kernel_launch_count(void);
+/* Grow the device's stream-ordered pool (which this library allocates its
+ * scratch and results from, and never trims) by `bytes` up front, so the
+ * first builds of a process do not pay for new device mappings.  Optional. */
+int sait_device_pool_reserve(int device, int64_t bytes);
 
 #ifdef __cplusplus
 }

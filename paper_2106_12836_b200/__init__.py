@@ -14,6 +14,7 @@ from ._native import (
     SaitOutOfMemory,
     SaitRuntimeError,
     launch_count,
+    reserve_device_pool,
 )
 from .csr import (
     CsrMatrix,

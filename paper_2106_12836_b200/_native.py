@@ -185,6 +185,7 @@ PROTOTYPES = {
     "sait_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(VP)]),
     "sait_host_free": (None, [VP]),
     "sait_kernel_launch_count": (C.c_int64, []),
+    "sait_device_pool_reserve": (C.c_int, [C.c_int, C.c_int64]),
 }
 
 for _name, (_res, _args) in PROTOTYPES.items():
@@ -233,3 +234,12 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(lib.sait_kernel_launch_count())
+
+
+def reserve_device_pool(nbytes: int, device: int | None = None) -> None:
+    """sait_device_pool_reserve: grow the library's device pool up front."""
+    if device is None:
+        import torch
+
+        device = torch.cuda.current_device()
+    check(lib.sait_device_pool_reserve(int(device), int(nbytes)))

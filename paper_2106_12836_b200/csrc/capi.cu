@@ -143,6 +143,19 @@ int guarded(F&& f) {
   }
 }
 
+// Grow the stream-ordered pool once by `bytes` (one allocation, freed back
+// into the pool and kept, the release threshold being unlimited), so later
+// builds carve their buffers out of existing mappings instead of paying for
+// new ones allocation by allocation (the first builds of a process).
+void reserve_pool(cudaMemPool_t pool, size_t bytes) {
+  void* p = nullptr;
+  if (bytes && cudaMallocFromPoolAsync(&p, bytes, pool, nullptr) == cudaSuccess) {
+    cudaFreeAsync(p, nullptr);
+    cudaStreamSynchronize(nullptr);
+  }
+  cudaGetLastError();
+}
+
 void init_device_pool() {
   static std::once_flag once[64];
   int dev = 0;
@@ -152,6 +165,8 @@ void init_device_pool() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      if (const char* e = std::getenv("SAIT_POOL_RESERVE_MB"))
+        reserve_pool(pool, static_cast<size_t>(std::max(0LL, std::atoll(e))) << 20);
     }
   });
 }
@@ -508,6 +523,20 @@ void sait_host_csr_free(sait_host_csr* m) {
 }
 
 int64_t sait_kernel_launch_count(void) { return sait::g_launches.load(); }
+
+int sait_device_pool_reserve(int device, int64_t bytes) {
+  return guarded([&] {
+    if (bytes < 0) sait::throw_invalid("sait_device_pool_reserve: bytes must be >= 0");
+    DeviceGuard g(device);
+    init_device_pool();
+    cudaMemPool_t pool;
+    SAIT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    void* p = nullptr;
+    SAIT_CUDA(cudaMallocFromPoolAsync(&p, static_cast<size_t>(bytes), pool, nullptr));
+    SAIT_CUDA(cudaFreeAsync(p, nullptr));
+    SAIT_CUDA(cudaStreamSynchronize(nullptr));
+  });
+}
 
 // Diagnostics: seconds for H2D alone / D2H alone / both on two streams.
 void sait_debug_copy_probe(const double* h_src, double* h_dst, int64_t n, int chunks, double* out3) {

@@ -104,3 +104,13 @@ def test_nonfinite_values_in_build(S, port):
         assert np.array_equal(np.isnan(got.values), np.isnan(exp.values))
         fin = ~np.isnan(exp.values)
         assert bitwise_equal(got.values[fin], exp.values[fin])
+
+
+def test_device_pool_reserve():
+    """sait_device_pool_reserve grows the pool; negative sizes are invalid"""
+    import paper_2106_12836_b200 as S
+
+    S.reserve_device_pool(64 << 20)
+    S.reserve_device_pool(0)
+    with pytest.raises(S.SaitInvalidArgument):
+        S.reserve_device_pool(-1)

@@ -432,6 +432,7 @@ void plan_host_chunks(sait_pair_t p) {
       tail = s2 == std::string::npos ? std::vector<double>{} : parse(spec.substr(s2 + 1));
     }
   }
+  if (!(mb_mid > 0.0)) mb_mid = 1e9;  // "head;;tail": the middle as one chunk
   auto rows_of = [&](double mb) {
     return std::max<int64_t>(G, static_cast<int64_t>(mb * (1 << 20) / 8.0) / G * G);
   };

@@ -7,6 +7,9 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
+#include <initializer_list>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -91,6 +94,60 @@ inline int num_sms() {
     return n;
   }();
   return sms;
+}
+
+// Small device -> host reads (sizes, counters, flags) through pinned
+// buffers: a pageable destination makes the copy stage through the driver.
+// All listed reads share one stream synchronisation.  The 4 KB pinned
+// buffers live in a process-wide free list (the pair build's worker thread
+// is short-lived; pinning per thread would cost more than it saves).
+struct ReadItem {
+  void* host;
+  const void* dev;
+  size_t bytes;
+};
+inline std::mutex& readback_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::vector<char*>& readback_pool() {
+  static std::vector<char*> v;
+  return v;
+}
+constexpr size_t kReadbackBytes = 4096;
+inline void read_back(cudaStream_t s, std::initializer_list<ReadItem> items) {
+  size_t total = 0;
+  for (const ReadItem& it : items) total += (it.bytes + 15) / 16 * 16;
+  if (total > kReadbackBytes) throw std::runtime_error("read_back: more than 4 KB requested");
+  char* buf = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(readback_mutex());
+    if (!readback_pool().empty()) {
+      buf = readback_pool().back();
+      readback_pool().pop_back();
+    }
+  }
+  if (!buf && cudaMallocHost(&buf, kReadbackBytes) != cudaSuccess)
+    throw std::runtime_error("read_back: cudaMallocHost failed");
+  struct Return {
+    char* b;
+    ~Return() {
+      std::lock_guard<std::mutex> lk(readback_mutex());
+      readback_pool().push_back(b);
+    }
+  } ret{buf};
+  size_t off = 0;
+  for (const ReadItem& it : items) {
+    cuda_check(cudaMemcpyAsync(buf + off, it.dev, it.bytes, cudaMemcpyDeviceToHost, s), "readback", __FILE__,
+               __LINE__);
+    off += (it.bytes + 15) / 16 * 16;
+  }
+  cuda_check(cudaStreamSynchronize(s), "readback sync", __FILE__, __LINE__);
+  off = 0;
+  for (const ReadItem& it : items) {
+    std::memcpy(it.host, buf + off, it.bytes);
+    off += (it.bytes + 15) / 16 * 16;
+  }
 }
 
 inline unsigned grid_for(int64_t work, int per_block, int64_t cap = 1 << 30) {

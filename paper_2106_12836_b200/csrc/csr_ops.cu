@@ -273,8 +273,7 @@ int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStre
   scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(counts, n, sums, row_ptr, total);
   SAIT_LAUNCHED();
   int64_t h = 0;
-  SAIT_CUDA(cudaMemcpyAsync(&h, total, sizeof h, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&h, total, sizeof h}});
   dfree(sums, s);
   if (h > INT32_MAX)
     throw Error(SAIT_ERR_NOMEM, "result has " + std::to_string(h) +
@@ -288,8 +287,7 @@ void exclusive_scan_rows(const int32_t* counts, int32_t* row_ptr, int64_t n, cud
 
 int64_t read_last(const int32_t* row_ptr, int64_t n, cudaStream_t s) {
   int32_t h = 0;
-  SAIT_CUDA(cudaMemcpyAsync(&h, row_ptr + n, sizeof h, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&h, row_ptr + n, sizeof h}});
   return h;
 }
 
@@ -329,20 +327,17 @@ void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStr
   sort_rows_warp<<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
   SAIT_LAUNCHED();
   int32_t hc[3];
-  SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{hc, counters, sizeof hc}});
   if (hc[2] > 0) {
     sort_rows_mid<<<grid_for(int64_t{hc[2]} * 32, 256), 256, 0, s>>>(mid_rows, hc[2], rp, ci, v, long_rows, counters);
     SAIT_LAUNCHED();
-    SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{hc, counters, sizeof hc}});
   }
   if (hc[0] > 0) {
     unsigned g = static_cast<unsigned>(std::min<int64_t>(hc[0], 4 * num_sms()));
     sort_rows_block<<<g, kSortBlock, 0, s>>>(long_rows, hc[0], rp, ci, v, huge_rows, counters + 1);
     SAIT_LAUNCHED();
-    SAIT_CUDA(cudaMemcpyAsync(hc, counters, sizeof hc, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{hc, counters, sizeof hc}});
     if (hc[1] > 0) {
       std::vector<int32_t> huge(hc[1]);
       SAIT_CUDA(cudaMemcpyAsync(huge.data(), huge_rows, hc[1] * sizeof(int32_t), cudaMemcpyDeviceToHost, s));

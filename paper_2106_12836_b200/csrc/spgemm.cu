@@ -781,9 +781,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total);
   SAIT_LAUNCHED();
   unsigned long long htot[2] = {0, 0};
-  SAIT_CUDA(cudaMemcpyAsync(pl.hist, hist, sizeof pl.hist, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaMemcpyAsync(htot, total, sizeof htot, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{pl.hist, hist, sizeof pl.hist}, {htot, total, sizeof htot}});
   const unsigned long long htotal = htot[0], hashed_products = htot[1];
   res.products = static_cast<int64_t>(htotal);
   for (int b2 = 0; b2 < kNumBins; ++b2) pl.start[b2 + 1] = pl.start[b2] + pl.hist[b2];
@@ -845,8 +843,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   if (g.stage_pos)
     SAIT_CUDA(cudaMemcpyAsync(meta + 1, g.stage_cursor, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
   int64_t hmeta[2] = {0, 0};
-  SAIT_CUDA(cudaMemcpyAsync(hmeta, meta, sizeof hmeta, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{hmeta, meta, sizeof hmeta}});
   if (hmeta[0] > INT32_MAX)
     throw Error(SAIT_ERR_NOMEM, "result has " + std::to_string(hmeta[0]) +
                                     " stored entries; the device CSR uses int32 indices (max 2^31-1)");
@@ -866,8 +863,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   launch_pass(g, pl, true, s, overflow);
   if (epi.qrp) {
     int hc = 1;
-    SAIT_CUDA(cudaMemcpyAsync(&hc, changed, sizeof hc, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{&hc, changed, sizeof hc}});
     res.changed = hc != 0;
   }
   dfree(changed, s);

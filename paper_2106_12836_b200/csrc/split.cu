@@ -71,13 +71,12 @@ DevCsr jacobi_split(const DevCsr& t, bool lower, double* inv_diag, cudaStream_t 
   int64_t n = t.nrows;
   SplitErrors h{~0ull, ~0ull};
   SplitErrors* d = dalloc<SplitErrors>(1, s);
-  SAIT_CUDA(cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  SAIT_CUDA(cudaMemsetAsync(d, 0xff, sizeof h, s));  // both fields ~0
   if (n > 0) {
     split_validate<<<grid_for(n, 256), 256, 0, s>>>(n, lower, t.rp, t.ci, t.v, d);
     SAIT_LAUNCHED();
   }
-  SAIT_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&h, d, sizeof h}});
   dfree(d, s);
   if (h.tri != ~0ull) {
     int64_t row = static_cast<int64_t>(h.tri >> 32);

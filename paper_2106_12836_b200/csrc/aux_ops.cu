@@ -109,11 +109,10 @@ void validate_device_csr(const DevCsr& m, cudaStream_t s) {
   if (m.nrows == 0) return;
   unsigned long long h = ~0ull;
   unsigned long long* d = dalloc<unsigned long long>(1, s);
-  SAIT_CUDA(cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  SAIT_CUDA(cudaMemsetAsync(d, 0xff, sizeof h, s));  // ~0
   validate_kernel<<<grid_for(m.nrows, 256), 256, 0, s>>>(m.nrows, m.ncols, m.nnz, m.rp, m.ci, d);
   SAIT_LAUNCHED();
-  SAIT_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&h, d, sizeof h}});
   dfree(d, s);
   if (h == ~0ull) return;
   std::string row = std::to_string(h >> 2);

@@ -293,9 +293,7 @@ void ilu_device(const DevCsr& a, int level, DevCsr& L, DevCsr& U, cudaStream_t s
     }
     int hb[2];
     unsigned long long amax_bits = 0;
-    SAIT_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaMemcpyAsync(&amax_bits, scratch, sizeof amax_bits, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{hb, bad, sizeof hb}, {&amax_bits, scratch, sizeof amax_bits}});
     if (hb[0] != 0x7f7f7f7f)
       throw_invalid("ilu_k: structurally zero diagonal at row " + std::to_string(hb[0]));
     double amax;
@@ -350,8 +348,7 @@ void ilu_device(const DevCsr& a, int level, DevCsr& L, DevCsr& U, cudaStream_t s
     ilu0_rows<<<grid, 256, kIluSmem, s>>>(n, P.rp, P.ci, diag, plan.perm, w, pivot, done, scratch + 1, tol, bad + 1,
                                    static_cast<unsigned>(env_int("SAIT_ILU_SLEEP_NS", 2048)));
     SAIT_LAUNCHED();
-    SAIT_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
+    read_back(s, {{hb, bad, sizeof hb}});
     if (hb[1] != 0x7f7f7f7f) {
       double piv = 0.0;
       SAIT_CUDA(cudaMemcpyAsync(&piv, pivot + hb[1], sizeof piv, cudaMemcpyDeviceToHost, s));

@@ -239,8 +239,7 @@ TrisolvePlan analyse_triangular(const DevCsr& t, bool lower, cudaStream_t s) {
   scatter_by_level<<<grid_for(n, 256), 256, 0, s>>>(n, lev, start, p.perm);
   SAIT_LAUNCHED();
   int h = 0;
-  SAIT_CUDA(cudaMemcpyAsync(&h, maxlev, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&h, maxlev, sizeof(int)}});
   p.nlevels = h;
   dfree(lev, s);
   dfree(count, s);
@@ -274,8 +273,7 @@ void trisolve(const DevCsr& t, bool lower, const TrisolvePlan& plan, const doubl
       static_cast<unsigned>(env_int("SAIT_TRSV_SLEEP_NS", 2048)));
   SAIT_LAUNCHED();
   int hb = 0;
-  SAIT_CUDA(cudaMemcpyAsync(&hb, st.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  read_back(s, {{&hb, st.bad, sizeof(int)}});
   if (hb != 0x7f7f7f7f) {
     const int64_t row = lower ? hb : n - 1 - hb;
     throw_runtime("trisolve: singular matrix, zero diagonal at row " + std::to_string(row));

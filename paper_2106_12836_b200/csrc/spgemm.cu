@@ -138,12 +138,14 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
     st->aval[lane] = aval;
     if (lane == 0) st->off[32] = total;
     __syncwarp();
-    for (int32_t pb = 0; pb < total; pb += 32) {
-      const int32_t p = pb + lane;
-      const bool act = p < total;
-      int32_t col = -1 - lane;  // unique dummy for idle lanes
-      double prod = 0.0;
-      if (act) {
+    // product p of this chunk -> (B column, a * b); the loads of round r+1
+    // are issued before round r's table updates (software pipelining: the
+    // rows are latency-bound on these gathers at 2 CTAs per SM)
+    auto fetch = [&](int32_t p, int32_t& c, double& a, double& b) {
+      c = -1 - lane;  // unique dummy for idle lanes
+      a = 0.0;
+      b = 0.0;
+      if (p < total) {
         // t = last index with off[t] <= p among the nt entries (entries with
         // len == 0 share their successor's offset; upper_bound skips them)
         int lo = 0, hi = nt;  // find first t with off[t] > p, in (lo, hi]
@@ -154,9 +156,19 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
         }
         const int t = lo - 1;
         const int32_t bi = st->bstart[t] + (p - st->off[t]);
-        col = g.bci[bi];
-        prod = __dmul_rn(st->aval[t], g.bv[bi]);
+        c = g.bci[bi];
+        a = st->aval[t];
+        b = g.bv[bi];
       }
+    };
+    int32_t ncol;
+    double na, nb;
+    fetch(lane, ncol, na, nb);
+    for (int32_t pb = 0; pb < total; pb += 32) {
+      const bool act = pb + lane < total;
+      const int32_t col = ncol;
+      const double prod = act ? __dmul_rn(na, nb) : 0.0;
+      if (pb + 32 < total) fetch(pb + 32 + lane, ncol, na, nb);
       st->prod[lane] = prod;
       const unsigned grp = __match_any_sync(0xffffffffu, col);
       __syncwarp();

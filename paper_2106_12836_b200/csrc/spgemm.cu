@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* _
 // (warp-aggregated: one shared atomic per warp and bin, one per warp for
 // the total).
 __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restrict__ pcap,
-                          int32_t* __restrict__ hist, unsigned long long* __restrict__ total) {
+                          int32_t* __restrict__ hist, unsigned long long* __restrict__ total, int slack_pct) {
   __shared__ int32_t h[kNumBins];
   __shared__ unsigned long long tsum;
   if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
@@ -615,7 +615,9 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     }
     int64_t distinct = (p < g.ncols ? p : g.ncols) + 1;  // +1: the identity entry
     int logs = kMinLogSlots;
-    while ((int64_t{1} << logs) < 2 * distinct) ++logs;
+    // slots >= slack * distinct (and > distinct: find_or_insert needs an empty slot)
+    const int64_t need = (distinct * slack_pct + 99) / 100;
+    while ((int64_t{1} << logs) < need || (int64_t{1} << logs) <= distinct) ++logs;
     bin = kFirstSmemBin + logs - kMinLogSlots;
     if (bin > kGlobalBin) bin = kGlobalBin;
     const int32_t m = e1 - e0;
@@ -790,7 +792,11 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   unsigned long long* total = dalloc<unsigned long long>(2, s);  // all products, hash-row products
   SAIT_CUDA(cudaMemsetAsync(hist, 0, 2 * kNumBins * sizeof(int32_t), s));
   SAIT_CUDA(cudaMemsetAsync(total, 0, 2 * sizeof(unsigned long long), s));
-  plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total);
+  static const int slack_pct = [] {
+    const char* e = std::getenv("SAIT_HASH_SLACK");  // table slots per possible distinct column, in %
+    return e ? std::max(101, std::atoi(e)) : 125;
+  }();
+  plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total, slack_pct);
   SAIT_LAUNCHED();
   unsigned long long htot[2] = {0, 0};
   read_back(s, {{pl.hist, hist, sizeof pl.hist}, {htot, total, sizeof htot}});

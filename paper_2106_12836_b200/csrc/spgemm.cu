@@ -195,9 +195,11 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
   __syncwarp();
 }
 
-// Applies the drop rule in place (dropped slots become kDead) and returns
-// the number of surviving entries (same value in all lanes).
-__device__ int drop_row(const Args& g, int32_t row, int32_t* key, double* val, int logs, int lane) {
+// Applies the drop rule and compacts the survivors to [0, live) in one pass
+// over the table (slot order; a chunk's destinations never pass the chunk
+// being read).  Returns live (same value in all lanes).  The A15 fill cap
+// then ranks the compacted survivors only.
+__device__ int drop_compact(const Args& g, int32_t row, int32_t* key, double* val, int logs, int lane) {
   const int slots = 1 << logs;
   const int32_t j = row + static_cast<int32_t>(g.epi.diag_offset);  // the diagonal's column
   const int drop = g.epi.drop;
@@ -207,24 +209,28 @@ __device__ int drop_row(const Args& g, int32_t row, int32_t* key, double* val, i
     pb = g.epi.prp[row];
     pe = g.epi.prp[row + 1];
   }
+  const unsigned below = (1u << lane) - 1u;
   int live = 0, offdiag = 0;
-  for (int s = lane; s < slots; s += 32) {
-    int32_t k = key[s];
-    if (k < 0) continue;
-    bool keep = true;
-    if (thr) keep = (k == j) || (fabs(val[s]) >= g.epi.tau);
-    else if (drop == 2) keep = in_pattern(g.epi.pci, pb, pe, k);
-    if (!keep) key[s] = kDead;
-    else {
-      ++live;
+  for (int c = 0; c < slots; c += 32) {
+    const int32_t k = key[c + lane];
+    const double v = val[c + lane];
+    bool keep = k >= 0;
+    if (keep) {
+      if (thr) keep = (k == j) || (fabs(v) >= g.epi.tau);
+      else if (drop == 2) keep = in_pattern(g.epi.pci, pb, pe, k);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {
+      const int d = live + __popc(bal & below);
+      key[d] = k;
+      val[d] = v;
       offdiag += (k != j);
     }
+    live += __popc(bal);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    live += __shfl_xor_sync(0xffffffffu, live, o);
-    offdiag += __shfl_xor_sync(0xffffffffu, offdiag, o);
-  }
+  for (int o = 16; o > 0; o >>= 1) offdiag += __shfl_xor_sync(0xffffffffu, offdiag, o);
   __syncwarp();
   if (drop == 3) {
     int room = g.epi.cap[j] - 1;
@@ -232,15 +238,14 @@ __device__ int drop_row(const Args& g, int32_t row, int32_t* key, double* val, i
     if (offdiag > room) {
       // rank of each surviving off-diagonal by (|v| desc, col asc); mark the
       // ones ranked >= room as "to kill" (-3 - col) without disturbing ranks.
-      for (int s = lane; s < slots; s += 32) {
-        int32_t k = key[s];
-        if (k < 0 || k == j) continue;
+      for (int s = lane; s < live; s += 32) {
+        const int32_t k = key[s];
+        if (k == j) continue;
         const double mv = fabs(val[s]);
         int rank = 0;
-        for (int q = 0; q < slots; ++q) {
+        for (int q = 0; q < live; ++q) {
           int32_t kq = key[q];
           if (kq <= -3) kq = -3 - kq;
-          else if (kq < 0) continue;
           if (kq == j || kq == k) continue;
           const double mq = fabs(val[q]);
           rank += (mq > mv) || (mq == mv && kq < k);
@@ -248,35 +253,71 @@ __device__ int drop_row(const Args& g, int32_t row, int32_t* key, double* val, i
         if (rank >= room) key[s] = -3 - k;
       }
       __syncwarp();
-      for (int s = lane; s < slots; s += 32)
-        if (key[s] <= -3) key[s] = kDead;
+      int kept = 0;
+      for (int c = 0; c < live; c += 32) {
+        const bool in = c + lane < live;
+        const int32_t k = in ? key[c + lane] : -1;
+        const double v = in ? val[c + lane] : 0.0;
+        const bool keep = k >= 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) {
+          const int d = kept + __popc(bal & below);
+          key[d] = k;
+          val[d] = v;
+        }
+        kept += __popc(bal);
+      }
       __syncwarp();
-      live -= offdiag - room;
+      live = kept;
     }
   }
   return live;
 }
 
-// compact survivors to [0, live) in slot order (destinations never pass the
-// chunk being read), pad to a power of two, sort by column.
-__device__ void compact_sort(int32_t* key, double* val, int logs, int live, int lane) {
-  const int slots = 1 << logs;
-  int base = 0;
-  for (int c = 0; c < slots; c += 32) {
-    const int32_t k = key[c + lane];
-    const double v = val[c + lane];
-    const bool keep = k >= 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    __syncwarp();
-    if (keep) {
-      const int d = base + __popc(bal & ((1u << lane) - 1));
-      key[d] = k;
-      val[d] = v;
+// sorts the compacted survivors [0, live) by column: one register bitonic
+// network over the warp for rows of <= 32 survivors (almost all), the shared
+// memory network above that.
+__device__ void sort_live(int32_t* key, double* val, int live, int lane, bool narrow) {
+  if (live <= 32) {
+    const int32_t k0 = lane < live ? key[lane] : INT32_MAX;
+    int32_t col;
+    int src;
+    if (narrow) {  // columns < 2^26: (column, lane) in 32 bits
+      uint32_t kk = k0 == INT32_MAX ? 0xffffffffu : (static_cast<uint32_t>(k0) << 5) | static_cast<uint32_t>(lane);
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+          const uint32_t ok = __shfl_xor_sync(0xffffffffu, kk, jj);
+          const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+          kk = keep_min ? min(kk, ok) : max(kk, ok);
+        }
+      col = static_cast<int32_t>(kk >> 5);
+      src = static_cast<int>(kk & 31u);
+    } else {
+      int64_t kk = k0 == INT32_MAX ? INT64_MAX : (static_cast<int64_t>(k0) << 5) | lane;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+          const int64_t ok = __shfl_xor_sync(0xffffffffu, kk, jj);
+          const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+          kk = keep_min ? min(kk, ok) : max(kk, ok);
+        }
+      col = static_cast<int32_t>(kk >> 5);
+      src = static_cast<int>(kk & 31);
     }
-    base += __popc(bal);
+    const double v = lane < live ? val[src] : 0.0;
     __syncwarp();
+    if (lane < live) {
+      key[lane] = col;
+      val[lane] = v;
+    }
+    __syncwarp();
+    return;
   }
-  const int n2 = next_pow2(live > 0 ? live : 1);
+  const int n2 = next_pow2(live);
   for (int s = live + lane; s < n2; s += 32) key[s] = kKeyPad;
   __syncwarp();
   bitonic_sort(key, val, n2, lane, 32, WarpSync{});
@@ -303,11 +344,12 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
                             int lane, bool numeric) {
   if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
   accumulate_row(g, j, key, val, logs, st, lane);
-  const int live = drop_row(g, j, key, val, logs, lane);
+  const int live = drop_compact(g, j, key, val, logs, lane);
+  const bool narrow = g.ncols < (int64_t{1} << 26);
   if (!numeric) {
     if (lane == 0) g.ccount[j] = live;
     if (!g.stage_pos) return;
-    compact_sort(key, val, logs, live, lane);
+    sort_live(key, val, live, lane, narrow);
     unsigned long long pos = 0;
     if (lane == 0) pos = atomicAdd(g.stage_cursor, static_cast<unsigned long long>(live));
     pos = __shfl_sync(0xffffffffu, pos, 0);
@@ -321,7 +363,7 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
     __syncwarp();
     return;
   }
-  compact_sort(key, val, logs, live, lane);
+  sort_live(key, val, live, lane, narrow);
   const int32_t out = g.crp[j];
   for (int s = lane; s < live; s += 32) {
     g.cci[out + s] = key[s];

@@ -133,42 +133,47 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
       if (lane >= o) incl += y;
     }
     const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    st->off[lane] = incl - len;
-    st->bstart[lane] = bst;
-    st->aval[lane] = aval;
-    if (lane == 0) st->off[32] = total;
+    // the entries with products, compacted (their offsets strictly increase)
+    const int32_t excl = incl - len;
+    const bool has = len > 0;  // (lanes >= nt have len 0)
+    const unsigned ne = __ballot_sync(0xffffffffu, has);
+    if (has) {
+      const int r = __popc(ne & ((1u << lane) - 1u));
+      st->off[r] = excl;
+      st->bstart[r] = bst;
+      st->aval[r] = aval;
+    }
     __syncwarp();
-    // product p of this chunk -> (B column, a * b); the loads of round r+1
-    // are issued before round r's table updates (software pipelining: the
-    // rows are latency-bound on these gathers at 2 CTAs per SM)
-    auto fetch = [&](int32_t p, int32_t& c, double& a, double& b) {
+    // product pb + lane of this chunk -> (B column, a * b); the loads of
+    // round r+1 are issued before round r's table updates (software
+    // pipelining).  Owner of product pb = the last entry starting at or
+    // before it (a ballot); lane l's owner is that entry advanced by the
+    // entries starting in (pb, pb + l] (bits of a warp OR-reduction) — no
+    // divergent search.
+    auto fetch = [&](int32_t pb, int32_t& c, double& a, double& b) {
+      const int r0 = __popc(__ballot_sync(0xffffffffu, has && excl <= pb)) - 1;
+      const int32_t d = excl - pb;
+      const unsigned starts = __reduce_or_sync(0xffffffffu, (has && d > 0 && d < 32) ? (1u << d) : 0u);
+      const int32_t p = pb + lane;
       c = -1 - lane;  // unique dummy for idle lanes
       a = 0.0;
       b = 0.0;
       if (p < total) {
-        // t = last index with off[t] <= p among the nt entries (entries with
-        // len == 0 share their successor's offset; upper_bound skips them)
-        int lo = 0, hi = nt;  // find first t with off[t] > p, in (lo, hi]
-        while (lo < hi) {
-          int mid = (lo + hi) >> 1;
-          if (st->off[mid] > p) hi = mid;
-          else lo = mid + 1;
-        }
-        const int t = lo - 1;
-        const int32_t bi = st->bstart[t] + (p - st->off[t]);
+        const int r = r0 + __popc(starts & ((2u << lane) - 1u));
+        const int32_t bi = st->bstart[r] + (p - st->off[r]);
         c = g.bci[bi];
-        a = st->aval[t];
+        a = st->aval[r];
         b = g.bv[bi];
       }
     };
     int32_t ncol;
     double na, nb;
-    fetch(lane, ncol, na, nb);
+    fetch(0, ncol, na, nb);
     for (int32_t pb = 0; pb < total; pb += 32) {
       const bool act = pb + lane < total;
       const int32_t col = ncol;
       const double prod = act ? __dmul_rn(na, nb) : 0.0;
-      if (pb + 32 < total) fetch(pb + 32 + lane, ncol, na, nb);
+      if (pb + 32 < total) fetch(pb + 32, ncol, na, nb);
       st->prod[lane] = prod;
       const unsigned grp = __match_any_sync(0xffffffffu, col);
       __syncwarp();

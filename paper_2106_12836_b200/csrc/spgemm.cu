@@ -234,10 +234,9 @@ __device__ int drop_compact(const Args& g, int32_t row, int32_t* key, double* va
     }
     live += __popc(bal);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) offdiag += __shfl_xor_sync(0xffffffffu, offdiag, o);
   __syncwarp();
   if (drop == 3) {
+    offdiag = __reduce_add_sync(0xffffffffu, offdiag);
     int room = g.epi.cap[j] - 1;
     if (room < 0) room = 0;
     if (offdiag > room) {
@@ -288,28 +287,35 @@ __device__ void sort_live(int32_t* key, double* val, int live, int lane, bool na
     const int32_t k0 = lane < live ? key[lane] : INT32_MAX;
     int32_t col;
     int src;
+    // a network over the first W = next_pow2(live) lanes only (lanes >= W
+    // hold padding and never exchange with lanes < W)
+    const int w = live <= 2 ? 2 : 1 << (32 - __clz(live - 1));
     if (narrow) {  // columns < 2^26: (column, lane) in 32 bits
       uint32_t kk = k0 == INT32_MAX ? 0xffffffffu : (static_cast<uint32_t>(k0) << 5) | static_cast<uint32_t>(lane);
 #pragma unroll
-      for (int k = 2; k <= 32; k <<= 1)
+      for (int k = 2; k <= 32; k <<= 1) {
+        if (k > w) break;
 #pragma unroll
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
           const uint32_t ok = __shfl_xor_sync(0xffffffffu, kk, jj);
           const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
           kk = keep_min ? min(kk, ok) : max(kk, ok);
         }
+      }
       col = static_cast<int32_t>(kk >> 5);
       src = static_cast<int>(kk & 31u);
     } else {
       int64_t kk = k0 == INT32_MAX ? INT64_MAX : (static_cast<int64_t>(k0) << 5) | lane;
 #pragma unroll
-      for (int k = 2; k <= 32; k <<= 1)
+      for (int k = 2; k <= 32; k <<= 1) {
+        if (k > w) break;
 #pragma unroll
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
           const int64_t ok = __shfl_xor_sync(0xffffffffu, kk, jj);
           const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
           kk = keep_min ? min(kk, ok) : max(kk, ok);
         }
+      }
       col = static_cast<int32_t>(kk >> 5);
       src = static_cast<int>(kk & 31);
     }

@@ -384,26 +384,67 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
   __syncwarp();
 }
 
-// numeric pass of staged hash-table rows: one warp per row copies the sorted
-// survivors to the final row and runs the early-stop compare.
+// Numeric pass of staged rows: 8 lanes per row (4 rows per warp; the rows
+// keep ~7-16 survivors, so a warp per row idled most lanes and a thread per
+// row made uncoalesced strided reads) copy the sorted survivors to the final
+// row and run the early-stop compare.  G = 0: hash-table rows staged at
+// stage_pos[j]; G > 0: tiny rows staged in the G-entry slot of their bin
+// position.
+template <int G>
+__device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+                                          const int32_t* __restrict__ tcol, const double* __restrict__ tval) {
+  __shared__ int blk_changed;
+  if (threadIdx.x == 0) blk_changed = 0;
+  __syncthreads();
+  constexpr int kLanes = 8;
+  const int sl = threadIdx.x & (kLanes - 1);
+  const int64_t t0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kLanes;
+  const int64_t nt = (static_cast<int64_t>(gridDim.x) * blockDim.x) / kLanes;
+  bool diff = false;
+  for (int64_t r = t0; r < nrows_bin; r += nt) {
+    const int32_t j = rows[r];
+    const int32_t* col;
+    const double* v;
+    if (G == 0) {
+      const int32_t pos = g.stage_pos[j];
+      if (pos < 0) continue;  // overflowed: recomputed by the hash kernel
+      col = g.stage_col + pos;
+      v = g.stage_val + pos;
+    } else {
+      col = tcol + r * G;
+      v = tval + r * G;
+    }
+    const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
+    bool cmp = g.epi.qrp != nullptr && !diff;
+    int32_t qb = 0;
+    if (cmp) {
+      qb = g.epi.qrp[j];
+      if (g.epi.qrp[j + 1] - qb != live) {
+        diff = true;
+        cmp = false;
+      }
+    }
+    for (int s = sl; s < live; s += kLanes) {
+      const int32_t c = col[s];
+      const double b = v[s];
+      g.cci[out + s] = c;
+      g.cv[out + s] = b;
+      if (cmp) {  // the reference's stabilized() test (sait.cpp:14-28)
+        const double a = g.epi.qv[qb + s];
+        const double fa = fabs(a), fb = fabs(b);
+        const double mx = fa < fb ? fb : fa;  // std::max(fa, fb)
+        if (g.epi.qci[qb + s] != c || fabs(__dsub_rn(b, a)) > __dmul_rn(1e-15, mx)) diff = true;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) blk_changed = 1;
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_changed) atomicOr(g.changed, 1);
+}
+
 __global__ void __launch_bounds__(256) spgemm_stage_emit(Args g, const int32_t* __restrict__ rows,
                                                           int32_t nrows_bin) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = w0; r < nrows_bin; r += nw) {
-    const int32_t j = rows[r];
-    const int32_t pos = g.stage_pos[j];
-    if (pos < 0) continue;  // overflowed: recomputed by the hash kernel
-    const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
-    const int32_t* col = g.stage_col + pos;
-    const double* v = g.stage_val + pos;
-    for (int s = lane; s < live; s += 32) {
-      g.cci[out + s] = col[s];
-      g.cv[out + s] = v[s];
-    }
-    if (g.epi.qrp) compare_row(g, j, col, v, live, lane);
-  }
+  emit_rows<0>(g, rows, nrows_bin, nullptr, nullptr);
 }
 
 __host__ __device__ constexpr int smem_per_warp(int logs) {
@@ -602,47 +643,12 @@ __global__ void __launch_bounds__(256, 8) spgemm_tiny(Args g, const int32_t* __r
 }
 
 // numeric pass of the tiny rows: staged slot -> final row, + early-stop
-// compare.  One thread per row (the staged slot and the output row are
-// contiguous per thread), so a warp moves 32 rows per round trip.
+// compare (emit_rows, 8 lanes per row).
 template <int G>
 __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                          const int32_t* __restrict__ tcol,
                                                          const double* __restrict__ tval) {
-  __shared__ int blk_changed;
-  if (threadIdx.x == 0) blk_changed = 0;
-  __syncthreads();
-  bool diff_any = false;
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows_bin;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t j = rows[r];
-    const int32_t out = g.crp[j], live = g.crp[j + 1] - out;
-    const int32_t* tc = tcol + r * G;
-    const double* tv = tval + r * G;
-    const bool cmp = g.epi.qrp && !diff_any;
-    int32_t qb = 0, ql = 0;
-    if (cmp) {
-      qb = g.epi.qrp[j];
-      ql = g.epi.qrp[j + 1] - qb;
-    }
-    bool diff = cmp && ql != live;
-#pragma unroll 4
-    for (int32_t q = 0; q < live; ++q) {
-      const int32_t c = tc[q];
-      const double v = tv[q];
-      g.cci[out + q] = c;
-      g.cv[out + q] = v;
-      if (cmp && !diff) {
-        const double a = g.epi.qv[qb + q];
-        const double fa = fabs(a), fb = fabs(v);
-        const double mx = fa < fb ? fb : fa;
-        diff = g.epi.qci[qb + q] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx);
-      }
-    }
-    diff_any = diff_any || diff;
-  }
-  if (__any_sync(0xffffffffu, diff_any) && (threadIdx.x & 31) == 0) blk_changed = 1;
-  __syncthreads();
-  if (threadIdx.x == 0 && blk_changed) atomicOr(g.changed, 1);
+  emit_rows<G>(g, rows, nrows_bin, tcol, tval);
 }
 
 // products per row (P_j) -> table bin; histogram of bins; total products
@@ -756,7 +762,7 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     const int per_warp = 32 / kTinyG[tb];
     const int64_t warps = (tc + per_warp - 1) / per_warp;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, int64_t{num_sms()} * 8 * 16));
-    const unsigned egrid = static_cast<unsigned>(std::min<int64_t>((tc + 255) / 256, int64_t{num_sms()} * 8 * 16));
+    const unsigned egrid = static_cast<unsigned>(std::min<int64_t>((tc + 31) / 32, int64_t{num_sms()} * 8 * 16));
     const int32_t* rows = pl.lists + pl.start[tb];
     switch (kTinyG[tb]) {
       case 8:
@@ -776,7 +782,7 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
   if (numeric && g.stage_pos) {  // staged hash-table rows: one copy kernel over all of them
     const int32_t cnt = pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin];
     if (cnt) {
-      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 7) / 8, int64_t{num_sms()} * 8 * 16));
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 31) / 32, int64_t{num_sms()} * 8 * 16));
       spgemm_stage_emit<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kFirstSmemBin], cnt);
       SAIT_LAUNCHED();
     }

@@ -113,7 +113,6 @@ struct sait_pair_s {
 
 namespace sait {
 int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
-void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s);
 void validate_device_csr(const DevCsr& m, cudaStream_t s);
 void narrow_indices(const int64_t* in, int32_t* out, int64_t n, cudaStream_t s);
 void widen_indices(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);

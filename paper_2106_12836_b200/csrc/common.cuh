@@ -164,7 +164,7 @@ inline unsigned grid_for(int64_t work, int per_block, int64_t cap = 1 << 30) {
 // exclusive scan of per-row counts into row_ptr[0..n]; returns the total
 // (synchronises; throws if it exceeds the int32 index range)
 int64_t scan_counts(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
-void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s);
+void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s, int64_t nnz = -1);
 void exclusive_scan_rows(const int32_t* counts, int32_t* row_ptr, int64_t n, cudaStream_t s);
 int64_t read_last(const int32_t* row_ptr, int64_t n, cudaStream_t s);  // syncs
 DevCsr make_identity(int64_t n, cudaStream_t s);

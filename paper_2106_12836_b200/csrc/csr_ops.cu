@@ -117,24 +117,31 @@ __global__ void count_cols(int64_t nrows, const int32_t* __restrict__ rp, const 
 // Scatter entry (i, j, v) of A to row j of A^T at an atomically claimed slot;
 // rows of the result are sorted afterwards.  Scaled value = v * scale[i]
 // (scale_columns order, kernels.cpp:243).
+// L lanes per source row: with long rows (>= 12 entries on average) 8 lanes
+// keep independent claims in flight (a thread walking its row serialised
+// them); short stencil rows stay one thread per row (neighbouring rows hit
+// neighbouring columns, and 8 lanes per row only add contention).
+template <int L>
 __global__ void scatter_transpose(int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                   const double* __restrict__ v, const double* __restrict__ scale,
                                   int32_t* __restrict__ cursor, int32_t* __restrict__ oci, double* __restrict__ ov) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
   if (i >= nrows) return;
-  double s = scale ? scale[i] : 1.0;
-  for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
-    int32_t pos = atomicAdd(&cursor[ci[e]], 1);
+  const int lane = threadIdx.x & (L - 1);
+  const double s = scale ? scale[i] : 1.0;
+  for (int32_t e = rp[i] + lane; e < rp[i + 1]; e += L) {
+    const int32_t pos = atomicAdd(&cursor[ci[e]], 1);
     oci[pos] = static_cast<int32_t>(i);
     if (v) ov[pos] = scale ? __dmul_rn(v[e], s) : v[e];
   }
 }
 
-// Rows of <= 8 entries: 8 lanes per row (4 rows per warp), rank by counting
-// smaller keys; longer rows are listed for the block sorter.
+// Rows of <= G entries: G lanes per row (32/G rows per warp), rank by
+// counting smaller keys; longer rows are listed for the next sorter.  G = 8
+// for stencil-like rows, 16 when rows average >= 12 entries.
+template <int G>
 __global__ void sort_rows_warp(int64_t nrows, const int32_t* __restrict__ rp, int32_t* __restrict__ ci,
                                double* __restrict__ v, int32_t* __restrict__ long_rows, int32_t* __restrict__ nlong) {
-  constexpr int G = 8;
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
   const int lane = threadIdx.x & (G - 1);
   const bool live = row < nrows;
@@ -159,27 +166,49 @@ __global__ void sort_rows_warp(int64_t nrows, const int32_t* __restrict__ rp, in
   }
 }
 
-// Rows listed by sort_rows_warp with 8 < len <= 32: one warp per row.
+// Rows listed by sort_rows_warp with 8 < len <= 32.  A warp takes two listed
+// rows: both <= 16 entries (the common case for SAIT factors) -> one half-warp
+// each; otherwise one after the other with the whole warp.  Rank by counting
+// smaller keys (keys within a row are distinct).
+__device__ __forceinline__ void rank_place(int32_t b, int32_t len, int lane, int width, int32_t* __restrict__ ci,
+                                           double* __restrict__ v) {
+  const bool mine = lane < len;
+  const int32_t key = mine ? ci[b + lane] : kKeyPad;
+  const double val = (mine && v) ? v[b + lane] : 0.0;
+  int rank = 0;
+  for (int o = 0; o < width; ++o) rank += __shfl_sync(0xffffffffu, key, o, width) < key;
+  __syncwarp();
+  if (mine) {
+    ci[b + rank] = key;
+    if (v) v[b + rank] = val;
+  }
+}
+
 __global__ void sort_rows_mid(const int32_t* __restrict__ rows, int32_t nlist, const int32_t* __restrict__ rp,
                               int32_t* __restrict__ ci, double* __restrict__ v, int32_t* __restrict__ long_rows,
                               int32_t* __restrict__ nlong) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= nlist) return;
-  const int32_t row = rows[w];
-  const int32_t b = rp[row], len = rp[row + 1] - b;
-  if (len > 32) {
-    if (lane == 0) long_rows[atomicAdd(nlong, 1)] = row;
+  const int64_t r0 = 2 * w;
+  if (r0 >= nlist) return;
+  const int half = lane >> 4;
+  const bool has = r0 + half < nlist;
+  int32_t row = 0, b = 0, len = 0;
+  if (has) {
+    row = rows[r0 + half];
+    b = rp[row];
+    len = rp[row + 1] - b;
+  }
+  if (has && len > 32 && (lane & 15) == 0) long_rows[atomicAdd(nlong, 1)] = row;
+  if (len > 32) len = 0;  // left to the block sorter
+  const int32_t l0 = __shfl_sync(0xffffffffu, len, 0), l1 = __shfl_sync(0xffffffffu, len, 16);
+  if (l0 <= 16 && l1 <= 16) {
+    rank_place(b, len, lane & 15, 16, ci, v);
     return;
   }
-  const int32_t key = lane < len ? ci[b + lane] : kKeyPad;
-  const double val = (lane < len && v) ? v[b + lane] : 0.0;
-  int rank = 0;
-  for (int o = 0; o < len; ++o) rank += __shfl_sync(0xffffffffu, key, o) < key;
-  __syncwarp();
-  if (lane < len) {
-    ci[b + rank] = key;
-    if (v) v[b + rank] = val;
+  for (int h = 0; h < 2; ++h) {
+    const int32_t bh = __shfl_sync(0xffffffffu, b, 16 * h), lh = h ? l1 : l0;
+    if (lh > 1) rank_place(bh, lh, lane, 32, ci, v);
   }
 }
 
@@ -316,7 +345,7 @@ DevCsr make_identity_rows(int64_t rows, int64_t col0, int64_t ncols, cudaStream_
 }
 
 // Sort every row of (rp, ci, v) by column index.
-void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s) {
+void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStream_t s, int64_t nnz) {
   if (nrows == 0) return;
   int32_t* lists = dalloc<int32_t>(3 * nrows + 3, s);
   int32_t* mid_rows = lists + 2 * nrows;
@@ -324,12 +353,15 @@ void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStr
   int32_t* huge_rows = lists + nrows;
   int32_t* counters = lists + 3 * nrows;  // [nlong, nhuge, nmid]
   SAIT_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(int32_t), s));
-  sort_rows_warp<<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
+  if (nnz >= 12 * nrows)
+    sort_rows_warp<16><<<grid_for(nrows * 16, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
+  else
+    sort_rows_warp<8><<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
   SAIT_LAUNCHED();
   int32_t hc[3];
   read_back(s, {{hc, counters, sizeof hc}});
   if (hc[2] > 0) {
-    sort_rows_mid<<<grid_for(int64_t{hc[2]} * 32, 256), 256, 0, s>>>(mid_rows, hc[2], rp, ci, v, long_rows, counters);
+    sort_rows_mid<<<grid_for(int64_t{hc[2]} * 16, 256), 256, 0, s>>>(mid_rows, hc[2], rp, ci, v, long_rows, counters);
     SAIT_LAUNCHED();
     read_back(s, {{hc, counters, sizeof hc}});
   }
@@ -377,11 +409,14 @@ DevCsr transpose(const DevCsr& a, const double* row_scale, cudaStream_t s) {
   scan_counts(cnt, t.rp, t.nrows, s);
   SAIT_CUDA(cudaMemcpyAsync(cnt, t.rp, t.nrows * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   if (a.nrows > 0) {
-    scatter_transpose<<<grid_for(a.nrows, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, row_scale, cnt, t.ci, t.v);
+    if (a.nnz >= 12 * a.nrows)
+      scatter_transpose<8><<<grid_for(a.nrows * 8, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, row_scale, cnt, t.ci, t.v);
+    else
+      scatter_transpose<1><<<grid_for(a.nrows, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, row_scale, cnt, t.ci, t.v);
     SAIT_LAUNCHED();
   }
   dfree(cnt, s);
-  sort_rows(t.nrows, t.rp, t.ci, t.v, s);
+  sort_rows(t.nrows, t.rp, t.ci, t.v, s, t.nnz);
   return t;
 }
 

@@ -34,7 +34,6 @@ void scan_counts_async(const int32_t* counts, int32_t* row_ptr, int64_t n, int64
 namespace {
 
 constexpr int32_t kEmpty = -1;
-constexpr int32_t kDead = -2;
 constexpr int kFresh = 1 << 30;
 // Row bins: 0/1/2 = tiny (< 8/16/32 products, <= 8/16/32 A entries: register
 // path, 4/2/1 rows per warp), 3..9 = shared-memory tables of 64 .. 4096

@@ -37,30 +37,43 @@ __global__ void split_validate(int64_t n, bool lower, const int32_t* __restrict_
   if (!have || d == 0.0) atomicMin(&err->diag, static_cast<unsigned long long>(i));
 }
 
+// L lanes per row: 8 for long rows (coalesced reads and writes; a thread per
+// row walked them with strided accesses), 1 for short stencil rows.  Every
+// row holds exactly one diagonal (validated); entries after it shift down by
+// one.
+template <int kSplitLanes>
 __global__ void split_write(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, double* __restrict__ inv_diag,
                             int32_t* __restrict__ trp, int32_t* __restrict__ tci, double* __restrict__ tv) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i > n) return;
-  int32_t b = rp[i];
-  trp[i] = b - static_cast<int32_t>(i);  // exactly one stored diagonal per row (validated)
-  if (i == n) return;
-  int32_t e1 = rp[i + 1];
-  double d = 0.0;
-  for (int32_t e = b; e < e1; ++e)
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kSplitLanes;
+  const int lane = threadIdx.x & (kSplitLanes - 1);
+  const int base = (threadIdx.x & 31) & ~(kSplitLanes - 1);
+  int32_t b = 0, e1 = 0;
+  if (i <= n) {
+    b = rp[i];
+    if (lane == 0) trp[i] = b - static_cast<int32_t>(i);
+    if (i < n) e1 = rp[i + 1];
+  }
+  double dl = 0.0;
+  int32_t el = -1;
+  for (int32_t e = b + lane; e < e1; e += kSplitLanes)
     if (ci[e] == i) {
-      d = v[e];
-      break;
+      dl = v[e];
+      el = e;
     }
-  double inv = 1.0 / d;
-  inv_diag[i] = inv;
-  int32_t pos = b - static_cast<int32_t>(i);
-  for (int32_t e = b; e < e1; ++e) {
-    int32_t j = ci[e];
-    if (j == i) continue;
-    tci[pos] = j;
+  const unsigned found = (__ballot_sync(0xffffffffu, el >= 0) >> base) & ((1u << kSplitLanes) - 1u);
+  const int src = base + (found ? __ffs(found) - 1 : 0);
+  const double d = __shfl_sync(0xffffffffu, dl, src);
+  const int32_t ed = __shfl_sync(0xffffffffu, el, src);
+  if (i >= n) return;
+  const double inv = 1.0 / d;
+  if (lane == 0) inv_diag[i] = inv;
+  const int32_t shift = static_cast<int32_t>(i);
+  for (int32_t e = b + lane; e < e1; e += kSplitLanes) {
+    if (e == ed) continue;
+    const int32_t pos = e - shift - (e > ed ? 1 : 0);
+    tci[pos] = ci[e];
     tv[pos] = __dmul_rn(-v[e], inv);
-    ++pos;
   }
 }
 
@@ -96,7 +109,10 @@ DevCsr jacobi_split(const DevCsr& t, bool lower, double* inv_diag, cudaStream_t 
   tt.rp = dalloc<int32_t>(n + 1, s);
   tt.ci = dalloc<int32_t>(tt.nnz, s);
   tt.v = dalloc<double>(tt.nnz, s);
-  split_write<<<grid_for(n + 1, 256), 256, 0, s>>>(n, t.rp, t.ci, t.v, inv_diag, tt.rp, tt.ci, tt.v);
+  if (t.nnz >= 12 * n)
+    split_write<8><<<grid_for((n + 1) * 8, 256), 256, 0, s>>>(n, t.rp, t.ci, t.v, inv_diag, tt.rp, tt.ci, tt.v);
+  else
+    split_write<1><<<grid_for(n + 1, 256), 256, 0, s>>>(n, t.rp, t.ci, t.v, inv_diag, tt.rp, tt.ci, tt.v);
   SAIT_LAUNCHED();
   return tt;
 }

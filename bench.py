@@ -490,6 +490,10 @@ def run_b200(args):
                     "device triangular solves, bitwise the reference's trisolve",
         }
 
+    build_c4 = None
+    if ws == 1 and not args.no_c4:
+        build_c4 = run_build_c4(S, torch, cpu_sample=not args.no_cpu_baseline)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
@@ -503,12 +507,108 @@ def run_b200(args):
         }
         if comparators:
             line["comparators"] = comparators
+        if build_c4:
+            line["build_c4"] = build_c4
         if ws > 1:
             line["config"]["halo_bytes_per_apply_rank0"] = sp.halo_bytes
             line["config"]["halo_transport"] = transport
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+C4_LOG2N, C4_TAU, C4_K, C4_CAP, C4_REPS = 24, 1e-2, 3, 3.0, 3
+C4_CPU_LOG2N = 18
+
+
+def b_build(n, nnz_t, nnz_tt, nnz_steps):
+    """SURVEY.md §8(d) algorithmic bytes of one build: the split (T read, tT
+    and D^-1 written) plus, per step s, tT + M_{s-1} read, M_s written and
+    three int32 row-pointer arrays (M_0 = I)."""
+    b = 12 * nnz_t + 12 * nnz_tt + 8 * n
+    prev = n
+    for m in nnz_steps:
+        b += 12 * nnz_tt + 12 * prev + 12 * m + 12 * (n + 1)
+        prev = m
+    return b
+
+
+def run_build_c4(S, torch, cpu_sample=True):
+    """BASELINE config 4: SAIT build only of the synthetic lower T, n = 2^24
+    (15 geometric(0.01) offsets per row, N(0,1) values, d_i = 1.5 sum|t_ij| + 1),
+    tau = 1e-2, k = 3, fill cap 3x nnz per column.  Device: median of C4_REPS
+    builds after a warm-up (pool reserved up front).  CPU: the reference's own
+    sait_thr with the cap through its DropRule hook (oracle/_ref) on a bounded
+    n = 2^18 sample of the same generator, checked bitwise against the device
+    build of that sample."""
+    n = 1 << C4_LOG2N
+    t0 = time.perf_counter()
+    Th = S.synthetic_lower(n, 15, 0.01, 4)
+    t_gen = time.perf_counter() - t0
+    T = S.DeviceCsr.upload(Th)
+    nnz_t = Th.nnz()
+    del Th
+    S.reserve_device_pool(40 << 30)
+    P = S.SaitThrParams(C4_TAU, C4_K)
+    nnz_steps = []
+    for k in range(1, C4_K):  # per-step output sizes for the algorithmic bytes (untimed)
+        m = S.sait_thr_cap(T, S.lower_triangular, S.SaitThrParams(C4_TAU, k), C4_CAP)
+        nnz_steps.append(m.nnz())
+        m.free()
+    secs, st = [], []
+    for rep in range(1 + C4_REPS):
+        st = []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m = S.sait_thr_cap(T, S.lower_triangular, P, C4_CAP, stats_out=st)
+        torch.cuda.synchronize()
+        if rep:
+            secs.append(time.perf_counter() - t0)
+        nnz_m = m.nnz()
+        m.free()
+    T.free()
+    nnz_steps.append(nnz_m)
+    t = sorted(secs)[len(secs) // 2]
+    nnz_tt = nnz_t - n
+    B = b_build(n, nnz_t, nnz_tt, nnz_steps)
+    peak, src = peaks()
+    out = {
+        "workload": "c4: synthetic lower T n=2^24, SAIT_thr(tau=1e-2, k=3), fill cap 3x nnz(T[:,j])",
+        "n": n, "nnz_T": nnz_t, "built_nnz": nnz_m, "nnz_per_step": nnz_steps, "steps_run": st[0].steps_run,
+        "products": st[0].products, "seconds": t, "nnz_per_s": nnz_m / t, "samples_s": [round(x, 5) for x in secs],
+        "generate_host_s": round(t_gen, 3),
+        "roofline": {"bound": "hbm (compulsory bytes; the build is gather/hash-bound)", "algorithmic_bytes": B,
+                     "achieved": B / t / 1e9, "peak": peak, "unit": "GB/s", "frac": B / t / 1e9 / peak,
+                     "peak_source": src},
+        "note": "wall time of the synchronous sait_build call (split, 3 recursion steps, transposes), "
+                "median of %d after a warm-up" % C4_REPS,
+    }
+    if cpu_sample:
+        out["cpu_baseline"] = c4_cpu_sample(S)
+    return out
+
+
+def c4_cpu_sample(S):
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return None
+    R = O.get("reference")
+    n = 1 << C4_CPU_LOG2N
+    Th = S.synthetic_lower(n, 15, 0.01, 4)
+    To = O.Csr(Th.nrows, Th.ncols, Th.row_ptr, Th.col_idx, Th.values)
+    t0 = time.perf_counter()
+    ref = R.sait_thr_cap(To, True, C4_TAU, C4_K, C4_CAP)
+    t = time.perf_counter() - t0
+    dev = S.sait_thr_cap(Th, S.lower_triangular, S.SaitThrParams(C4_TAU, C4_K), C4_CAP)
+    same = bool(np.array_equal(dev.row_ptr, ref.row_ptr) and np.array_equal(dev.col_idx, ref.col_idx)
+                and np.array_equal(dev.values.view(np.uint64), ref.values.view(np.uint64)))
+    import ctypes as C
+
+    lib = R.lib
+    lib.ref_max_threads.restype = C.c_int
+    return {"value": ref.nnz / t, "unit": "built nnz/s", "cores": int(lib.ref_max_threads()), "kind": "reference",
+            "sample": f"n=2^{C4_CPU_LOG2N} of the same generator through the reference sait_thr + cap DropRule "
+                      f"(oracle/_ref, OpenMP), {t:.2f} s", "device_bitwise_equal": same}
 
 
 def main():
@@ -518,6 +618,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the BASELINE config-4 build line")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N > 1: halo over peer memory inside the SpMV (default) or NCCL send/recv")
     args = ap.parse_args()

@@ -704,18 +704,38 @@ __global__ void gather_logs(const int32_t* __restrict__ rows, int32_t count, con
   if (q < count) out[q] = static_cast<int8_t>(logs_of[rows[q]]);
 }
 
-__global__ void scatter_bins(int64_t n, const int8_t* __restrict__ bin_of, int32_t* __restrict__ cursor,
-                             int32_t* __restrict__ lists) {
-  // warp-aggregated: one atomic per (warp, bin) instead of one per row
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int b = j < n ? bin_of[j] : -1;
-  const unsigned grp = __match_any_sync(0xffffffffu, b);
-  const int leader = __ffs(grp) - 1;
-  int base = 0;
-  if (lane == leader && b >= 0) base = atomicAdd(&cursor[b], __popc(grp));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (b >= 0) lists[base + __popc(grp & ((1u << lane) - 1u))] = static_cast<int32_t>(j);
+// Rows -> per-bin lists.  Block-aggregated: a block takes 1024 consecutive
+// rows, counts them per bin in shared memory (warp-aggregated shared
+// atomics), claims one range per (block, bin) with a global atomic, then
+// scatters.  (One global atomic per (warp, bin) serialised ~65 K warps on a
+// handful of cursors: 46 us per 2 M-row launch.)
+constexpr int kBinRowsPerThread = 4;
+__global__ void __launch_bounds__(256) scatter_bins(int64_t n, const int8_t* __restrict__ bin_of,
+                                                    int32_t* __restrict__ cursor, int32_t* __restrict__ lists) {
+  __shared__ int32_t cnt[kNumBins];
+  __shared__ int32_t base[kNumBins];
+  if (threadIdx.x < kNumBins) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kBinRowsPerThread +
+                     static_cast<int64_t>(w) * 32 * kBinRowsPerThread;
+  int b[kBinRowsPerThread], pos[kBinRowsPerThread];
+#pragma unroll
+  for (int q = 0; q < kBinRowsPerThread; ++q) {
+    const int64_t j = j0 + q * 32 + lane;
+    b[q] = j < n ? bin_of[j] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, b[q]);
+    const int leader = __ffs(grp) - 1;
+    int lb = 0;
+    if (lane == leader && b[q] >= 0) lb = atomicAdd(&cnt[b[q]], __popc(grp));
+    pos[q] = __shfl_sync(0xffffffffu, lb, leader) + __popc(grp & ((1u << lane) - 1u));
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumBins && cnt[threadIdx.x]) base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], cnt[threadIdx.x]);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kBinRowsPerThread; ++q)
+    if (b[q] >= 0) lists[base[b[q]] + pos[q]] = static_cast<int32_t>(j0 + q * 32 + lane);
 }
 
 using SmemKernel = void (*)(Args, const int32_t*, int32_t, bool);
@@ -869,7 +889,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
       pl.tcol[tb] = dalloc<int32_t>(static_cast<int64_t>(pl.hist[tb]) * kTinyG[tb], s);
       pl.tval[tb] = dalloc<double>(static_cast<int64_t>(pl.hist[tb]) * kTinyG[tb], s);
     }
-  scatter_bins<<<grid_for(n, 256), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
+  scatter_bins<<<grid_for(n, 256 * kBinRowsPerThread), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
   SAIT_LAUNCHED();
   int32_t gc = pl.hist[kGlobalBin];
   if (gc) {

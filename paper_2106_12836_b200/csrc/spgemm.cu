@@ -389,13 +389,12 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
 // row and run the early-stop compare.  G = 0: hash-table rows staged at
 // stage_pos[j]; G > 0: tiny rows staged in the G-entry slot of their bin
 // position.
-template <int G>
+template <int G, int kLanes>
 __device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                           const int32_t* __restrict__ tcol, const double* __restrict__ tval) {
   __shared__ int blk_changed;
   if (threadIdx.x == 0) blk_changed = 0;
   __syncthreads();
-  constexpr int kLanes = 8;
   const int sl = threadIdx.x & (kLanes - 1);
   const int64_t t0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kLanes;
   const int64_t nt = (static_cast<int64_t>(gridDim.x) * blockDim.x) / kLanes;
@@ -443,7 +442,7 @@ __device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restri
 
 __global__ void __launch_bounds__(256) spgemm_stage_emit(Args g, const int32_t* __restrict__ rows,
                                                           int32_t nrows_bin) {
-  emit_rows<0>(g, rows, nrows_bin, nullptr, nullptr);
+  emit_rows<0, 8>(g, rows, nrows_bin, nullptr, nullptr);
 }
 
 __host__ __device__ constexpr int smem_per_warp(int logs) {
@@ -642,12 +641,12 @@ __global__ void __launch_bounds__(256, 8) spgemm_tiny(Args g, const int32_t* __r
 }
 
 // numeric pass of the tiny rows: staged slot -> final row, + early-stop
-// compare (emit_rows, 8 lanes per row).
+// compare (emit_rows, 4 lanes per row of <= 8 entries, else 8).
 template <int G>
 __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                          const int32_t* __restrict__ tcol,
                                                          const double* __restrict__ tval) {
-  emit_rows<G>(g, rows, nrows_bin, tcol, tval);
+  emit_rows<G, (G < 16 ? 4 : 8)>(g, rows, nrows_bin, tcol, tval);
 }
 
 // products per row (P_j) -> table bin; histogram of bins; total products
@@ -781,7 +780,8 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     const int per_warp = 32 / kTinyG[tb];
     const int64_t warps = (tc + per_warp - 1) / per_warp;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, int64_t{num_sms()} * 8 * 16));
-    const unsigned egrid = static_cast<unsigned>(std::min<int64_t>((tc + 31) / 32, int64_t{num_sms()} * 8 * 16));
+    const int64_t rpb = tb == 0 ? 64 : 32;  // rows per 256-thread block of the emit (4 or 8 lanes per row)
+    const unsigned egrid = static_cast<unsigned>(std::min<int64_t>((tc + rpb - 1) / rpb, int64_t{num_sms()} * 8 * 16));
     const int32_t* rows = pl.lists + pl.start[tb];
     switch (kTinyG[tb]) {
       case 8:

@@ -578,23 +578,24 @@ __device__ __forceinline__ void tiny_row(const Args& g, const TinyFetch& f, int 
   const bool valid = col != INT32_MAX;
   const int32_t prev = __shfl_up_sync(kAll, col, 1, G);
   const bool head = valid && (lane == 0 || prev != col);
-  double acc = val;  // sequential sum over each run of equal columns, in product order
-  bool active = head;
-  for (int d = 1; d < G; ++d) {
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
+  const int shift = grp * G;
+  // each run of equal columns summed sequentially by its head, in product
+  // order; run length = distance to the next head (valid keys form a prefix)
+  const unsigned heads = (__ballot_sync(kAll, head) >> shift) & gmask;
+  const int nvalid = __popc((__ballot_sync(kAll, valid) >> shift) & gmask);
+  const unsigned later = heads & ~((2u << lane) - 1u);
+  const int run = head ? (later ? __ffs(later) - 1 : nvalid) - lane : 0;
+  const int maxrun = __reduce_max_sync(kAll, run);
+  double acc = val;
+  for (int d = 1; d < maxrun; ++d) {
     const double v = __shfl_down_sync(kAll, val, d, G);
-    const int32_t c = __shfl_down_sync(kAll, col, d, G);
-    if (active) {
-      if (lane + d < G && c == col) acc = __dadd_rn(acc, v);
-      else active = false;
-    }
-    if (!__any_sync(kAll, active)) break;
+    if (d < run) acc = __dadd_rn(acc, v);
   }
   bool keep = head;
   const int drop = g.epi.drop;
   if (head && (drop == 1 || drop == 3) && g.epi.tau != 0.0) keep = (col == jd) || (fabs(acc) >= g.epi.tau);
   else if (head && drop == 2) keep = in_pattern(g.epi.pci, g.epi.prp[j], g.epi.prp[j + 1], col);
-  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
-  const int shift = grp * G;
   if (drop == 3) {
     const unsigned offm = (__ballot_sync(kAll, keep && col != jd) >> shift) & gmask;
     int room = live_row ? g.epi.cap[jd] - 1 : 0;

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from conftest import golden_csr
-from helpers import bitwise_equal_csr, to_product
+from helpers import bitwise_equal, bitwise_equal_csr, to_product
 
 pytestmark = pytest.mark.gpu
 
@@ -124,6 +124,22 @@ def test_errors_match_reference(S, golden):
         S.sait_thr(rect, S.lower_triangular, S.SaitThrParams(0.1, 2))
 
 
+@pytest.mark.parametrize("lower", [True, False])
+@pytest.mark.parametrize("draws", [3, 30])
+def test_jacobi_split_row_lengths(S, port, lower, draws):
+    """The split's thread-per-row (short rows) and 8-lanes-per-row (>= 12
+    entries per row on average) variants, both triangles: bitwise the oracle."""
+    from oracle import oracle as O
+
+    t = O.synthetic_lower(700, draws, 0.05, seed=31 + draws)
+    if not lower:
+        t = port.transpose(t)
+    inv, tt = port.jacobi_split(t, lower)
+    sp = S.jacobi_split(to_product(t), kind(S, lower))
+    assert bitwise_equal(np.asarray(sp.inv_diag), inv)
+    assert bitwise_equal_csr(sp.iteration_matrix, tt)
+
+
 def test_spec_examples(S):
     """SPEC.md:217-238 examples for jacobi_split / sait_core / sait_thr."""
     t = S.CsrMatrix(2, 2, [0, 1, 3], [0, 0, 1], [2.0, 4.0, 2.0])
@@ -172,6 +188,24 @@ def test_hash_rows_staging_and_overflow(cap):
         env["SAIT_SPGEMM_NOSTAGE"] = "1"
     else:
         env["SAIT_SPGEMM_STAGE_CAP"] = cap
+    out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.split() == ["1", "1"]
+
+
+@pytest.mark.parametrize("slack", ["101", "400"])
+def test_hash_table_load_factors(slack):
+    """Hash tables sized at the minimum (slots just above the possible distinct
+    columns: long linear probes, nearly full tables) and at 4x give the same
+    bits as the oracle (SAIT_HASH_SLACK, percent; the default is 125)."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, SAIT_HASH_SLACK=slack)
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]

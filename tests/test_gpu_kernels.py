@@ -60,6 +60,19 @@ def test_transpose_scale(S, port):
     assert bitwise_equal_csr(S.scale_columns(a, d), port.scale_columns(to_oracle(a), d))
 
 
+@pytest.mark.parametrize("shape", [(500, 300, 0.06, 6), (200, 400, 0.2, 7), (3000, 3000, 0.004, 8)])
+def test_transpose_row_length_paths(S, port, shape):
+    """Every scatter/sort variant of the transpose: short stencil-like rows
+    (thread per row, 8-lane sorter), rows averaging >= 12 entries (8 lanes per
+    source row, 16-lane first sorter), half-warp and full-warp mid rows, and
+    rows over 32 entries (block sorter) -- bitwise the reference."""
+    m, n, dens, seed = shape
+    a = rand_csr(S, m, n, dens, seed)
+    assert bitwise_equal_csr(S.transpose(a), port.transpose(to_oracle(a)))
+    d = np.random.default_rng(seed).standard_normal(n)
+    assert bitwise_equal_csr(S.scale_columns(a, d), port.scale_columns(to_oracle(a), d))
+
+
 def test_spmv_random(S, port):
     a = rand_csr(S, 2000, 1500, 0.004, 9)
     x = np.random.default_rng(2).standard_normal(1500)

@@ -144,8 +144,10 @@ def run_reference(args):
 
     R = O.get("reference")
     A, L, U = ref_inputs(O, R)
+    tb0 = time.perf_counter()
     ML = R.sait_thr(L, True, TAU, STEPS_K)
     MU = R.sait_thr(U, False, TAU, STEPS_K)
+    t_build = time.perf_counter() - tb0
     n = A.nrows
     B = b_pair(n, ML.nnz, MU.nnz)
     lib = R.lib
@@ -173,7 +175,11 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": f"{sample} vectors per step through SaitPairPreconditioner::apply (OpenMP {cores} threads)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build": {"built_nnz": ML.nnz + MU.nnz, "seconds": t_build, "nnz_per_s": (ML.nnz + MU.nnz) / t_build,
+                  "note": f"the reference's sait_thr on L then U (OpenMP {cores} threads), one build each"},
     }
+    if not args.no_c4:
+        line["build_c4"] = c4_reference_sample()
     lib.ref_pair_destroy.argtypes = [C.c_void_p]
     lib.ref_pair_destroy(p)
     print(json.dumps(line))
@@ -585,6 +591,19 @@ def run_build_c4(S, torch, cpu_sample=True):
     if cpu_sample:
         out["cpu_baseline"] = c4_cpu_sample(S)
     return out
+
+
+def c4_reference_sample():
+    """The reference's capped C4 build on the bounded n = 2^18 sample (no device)."""
+    from oracle import oracle as O
+
+    R = O.get("reference")
+    T = O.synthetic_lower(1 << C4_CPU_LOG2N, 15, 0.01, 4)
+    t0 = time.perf_counter()
+    m = R.sait_thr_cap(T, True, C4_TAU, C4_K, C4_CAP)
+    t = time.perf_counter() - t0
+    return {"value": m.nnz / t, "unit": "built nnz/s", "built_nnz": m.nnz, "seconds": t,
+            "sample": f"n=2^{C4_CPU_LOG2N} of the config-4 generator, reference sait_thr + cap DropRule (oracle/_ref)"}
 
 
 def c4_cpu_sample(S):

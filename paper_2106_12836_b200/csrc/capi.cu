@@ -67,7 +67,8 @@ struct sait_build_session_s {
   cudaStream_t s = nullptr;
   int64_t c0 = 0, c1 = 0, n = 0;
   double* inv = nullptr;
-  sait::DevCsr ttT;
+  sait::DevCsr ttT;  // the recursion's fixed operand: tT^T, or tT in row form
+  bool row_form = false;
   int32_t* cap = nullptr;
   Recursion* rec = nullptr;
   cudaEvent_t e0 = nullptr;
@@ -262,24 +263,29 @@ void to_host(const sait::DevCsr& m, cudaStream_t s, int64_t* rp, int64_t* ci, do
 sait::Epilogue no_epilogue() { return sait::Epilogue{}; }
 
 struct BuildOut {
-  sait::DevCsr mt;  // final unit-diagonal iterate, column form (M^T)
+  sait::DevCsr mt;  // final unit-diagonal iterate: M^T (column form) or M (row form)
   int steps_run = 0;
   bool stabilized = false;
   int64_t products = 0;
 };
 
-// The recursion of sait.cpp:75-136 in column form: row j of M_s^T is
+// The recursion of sait.cpp:75-136.  Column form: row j of M_s^T is
 //   drop( sum_{k in M_{s-1}^T[j,:]} M_{s-1}^T[j,k] * tT^T[k,:] + e_j ),
 // bitwise equal to the reference's row form (same products, same
 // ascending-k order, commutative products).  Rows [c0, c0 + rows) of M^T
 // (= a block of columns of M) evolve independently; only the early-stop
-// decision is global, so the caller supplies it between steps.
+// decision is global, so the caller supplies it between steps.  The fill cap
+// (per column of M) and column-sharded blocks need the column form.
+// Row form (row_form = true, whole matrix, threshold/pattern/none): the
+// reference's own orientation, row i of M_s = drop(sum_k tT[i,k] M_{s-1}[k,:]
+// + e_i) with op = tT -- the same products in the same order, and neither
+// tT nor the result needs a transpose.
 class Recursion {
  public:
-  Recursion(const sait::DevCsr& ttT, const sait_drop_spec& spec, const int32_t* cap, int64_t c0, int64_t rows,
-            cudaStream_t s)
-      : ttT_(ttT), spec_(spec), s_(s) {
-    a_ = sait::make_identity_rows(rows, c0, ttT.nrows, s);
+  Recursion(const sait::DevCsr& op, const sait_drop_spec& spec, const int32_t* cap, int64_t c0, int64_t rows,
+            cudaStream_t s, bool row_form = false)
+      : ttT_(op), spec_(spec), s_(s), row_form_(row_form) {
+    a_ = sait::make_identity_rows(rows, c0, op.nrows, s);
     epi_.add_identity = true;
     epi_.diag_offset = c0;
     if (spec.kind == SAIT_DROP_THRESHOLD) {
@@ -306,14 +312,14 @@ class Recursion {
       sait::Epilogue e0;
       e0.add_identity = true;
       e0.diag_offset = epi_.diag_offset;
-      advance(sait::spgemm_fused(a_, ttT_, e0, s_));
+      advance(product(e0));
       if (--pattern_left_ == 0) capture_pattern();
       return true;
     }
     epi_.qrp = a_.rp;
     epi_.qci = a_.ci;
     epi_.qv = a_.v;
-    sait::SpgemmResult r = sait::spgemm_fused(a_, ttT_, epi_, s_);
+    sait::SpgemmResult r = product(epi_);
     const bool changed = r.changed;
     advance(std::move(r));
     --main_left_;
@@ -334,6 +340,9 @@ class Recursion {
   }
 
  private:
+  sait::SpgemmResult product(const sait::Epilogue& e) {
+    return row_form_ ? sait::spgemm_fused(ttT_, a_, e, s_) : sait::spgemm_fused(a_, ttT_, e, s_);
+  }
   void advance(sait::SpgemmResult&& r) {
     products_ += r.products;
     sait::free_csr(a_, s_);
@@ -346,9 +355,10 @@ class Recursion {
     epi_.prp = pattern_.rp;
     epi_.pci = pattern_.ci;
   }
-  const sait::DevCsr& ttT_;
+  const sait::DevCsr& ttT_;  // tT^T (column form) or tT (row form)
   sait_drop_spec spec_;
   cudaStream_t s_;
+  bool row_form_ = false;
   sait::DevCsr a_, pattern_;
   sait::Epilogue epi_;
   int pattern_left_ = 0, main_left_ = 0, steps_run_ = 0;
@@ -871,13 +881,24 @@ int sait_build_session_create(sait_dcsr_t t, int lower, const sait_drop_spec* sp
       delete ss;
       throw;
     }
-    ss->ttT = sait::transpose(tt, nullptr, s);
-    sait::free_csr(tt, s);
+    // whole-matrix builds without the column cap run in row form (no
+    // transposes); SAIT_BUILD_COLUMN_FORM=1 forces the column form (tests)
+    static const bool force_column = [] {
+      const char* e = std::getenv("SAIT_BUILD_COLUMN_FORM");
+      return e && std::atoi(e) != 0;
+    }();
+    ss->row_form = !force_column && spec->kind != SAIT_DROP_THRESHOLD_CAP && col0 == 0 && col1 == n;
+    if (ss->row_form) {
+      ss->ttT = tt;
+    } else {
+      ss->ttT = sait::transpose(tt, nullptr, s);
+      sait::free_csr(tt, s);
+    }
     if (spec->kind == SAIT_DROP_THRESHOLD_CAP) {
       ss->cap = sait::dalloc<int32_t>(n, s);
       sait::column_caps(t->m, spec->cap_factor, ss->cap, s);
     }
-    ss->rec = new Recursion(ss->ttT, *spec, ss->cap, col0, col1 - col0, s);
+    ss->rec = new Recursion(ss->ttT, *spec, ss->cap, col0, col1 - col0, s, ss->row_form);
     *out = ss;
   });
 }
@@ -911,13 +932,23 @@ int sait_build_session_finish(sait_build_session_t ss, int transposed, sait_dcsr
     sait::DevCsr m;
     // column j of M is scaled by inv_diag[j] (kernels.cpp:236-246); rows of the
     // M^T block are the global columns c0 + i
-    if (transposed) {
-      m = sait::copy_csr(bo.mt, s);
-      sait::scale_rows(m, ss->inv + ss->c0, s);
+    if (ss->row_form) {  // bo.mt is M itself (whole matrix): scale its columns in place
+      sait::scale_columns(bo.mt, ss->inv, bo.mt, s);
+      if (transposed) {
+        m = sait::transpose(bo.mt, nullptr, s);
+        sait::free_csr(bo.mt, s);
+      } else {
+        m = bo.mt;
+      }
     } else {
-      m = sait::transpose(bo.mt, ss->inv + ss->c0, s);
+      if (transposed) {
+        m = sait::copy_csr(bo.mt, s);
+        sait::scale_rows(m, ss->inv + ss->c0, s);
+      } else {
+        m = sait::transpose(bo.mt, ss->inv + ss->c0, s);
+      }
+      sait::free_csr(bo.mt, s);
     }
-    sait::free_csr(bo.mt, s);
     cudaEvent_t e1;
     SAIT_CUDA(cudaEventCreate(&e1));
     SAIT_CUDA(cudaEventRecord(e1, s));

@@ -266,6 +266,7 @@ struct BuildOut {
   sait::DevCsr mt;  // final unit-diagonal iterate: M^T (column form) or M (row form)
   int steps_run = 0;
   bool stabilized = false;
+  bool scaled = false;  // row form: the last step already applied scale_columns
   int64_t products = 0;
 };
 
@@ -283,8 +284,8 @@ struct BuildOut {
 class Recursion {
  public:
   Recursion(const sait::DevCsr& op, const sait_drop_spec& spec, const int32_t* cap, int64_t c0, int64_t rows,
-            cudaStream_t s, bool row_form = false)
-      : ttT_(op), spec_(spec), s_(s), row_form_(row_form) {
+            cudaStream_t s, bool row_form = false, const double* out_scale = nullptr)
+      : ttT_(op), spec_(spec), s_(s), row_form_(row_form), out_scale_(row_form ? out_scale : nullptr) {
     a_ = sait::make_identity_rows(rows, c0, op.nrows, s);
     epi_.add_identity = true;
     epi_.diag_offset = c0;
@@ -319,7 +320,13 @@ class Recursion {
     epi_.qrp = a_.rp;
     epi_.qci = a_.ci;
     epi_.qv = a_.v;
+    // the last allowed step writes M D^-1 directly (an earlier early stop
+    // leaves the scaling to finish)
+    const bool last = out_scale_ && main_left_ == 1;
+    epi_.out_scale = last ? out_scale_ : nullptr;
     sait::SpgemmResult r = product(epi_);
+    epi_.out_scale = nullptr;
+    scaled_ = last;
     const bool changed = r.changed;
     advance(std::move(r));
     --main_left_;
@@ -335,6 +342,7 @@ class Recursion {
     a_ = sait::DevCsr{};
     o.steps_run = steps_run_;
     o.stabilized = stabilized_;
+    o.scaled = scaled_;
     o.products = products_;
     return o;
   }
@@ -359,6 +367,8 @@ class Recursion {
   sait_drop_spec spec_;
   cudaStream_t s_;
   bool row_form_ = false;
+  const double* out_scale_ = nullptr;
+  bool scaled_ = false;
   sait::DevCsr a_, pattern_;
   sait::Epilogue epi_;
   int pattern_left_ = 0, main_left_ = 0, steps_run_ = 0;
@@ -898,7 +908,7 @@ int sait_build_session_create(sait_dcsr_t t, int lower, const sait_drop_spec* sp
       ss->cap = sait::dalloc<int32_t>(n, s);
       sait::column_caps(t->m, spec->cap_factor, ss->cap, s);
     }
-    ss->rec = new Recursion(ss->ttT, *spec, ss->cap, col0, col1 - col0, s, ss->row_form);
+    ss->rec = new Recursion(ss->ttT, *spec, ss->cap, col0, col1 - col0, s, ss->row_form, ss->inv);
     *out = ss;
   });
 }
@@ -933,7 +943,7 @@ int sait_build_session_finish(sait_build_session_t ss, int transposed, sait_dcsr
     // column j of M is scaled by inv_diag[j] (kernels.cpp:236-246); rows of the
     // M^T block are the global columns c0 + i
     if (ss->row_form) {  // bo.mt is M itself (whole matrix): scale its columns in place
-      sait::scale_columns(bo.mt, ss->inv, bo.mt, s);
+      if (!bo.scaled) sait::scale_columns(bo.mt, ss->inv, bo.mt, s);
       if (transposed) {
         m = sait::transpose(bo.mt, nullptr, s);
         sait::free_csr(bo.mt, s);

@@ -193,6 +193,10 @@ struct Epilogue {
   const int32_t* qrp = nullptr;
   const int32_t* qci = nullptr;
   const double* qv = nullptr;
+  // final step of a row-form build: written values are v * out_scale[col]
+  // (scale_columns, kernels.cpp:236-246, fused); staging and the
+  // stabilization compare see the unscaled values
+  const double* out_scale = nullptr;
 };
 struct SpgemmResult {
   DevCsr c;

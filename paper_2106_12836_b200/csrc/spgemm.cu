@@ -377,7 +377,7 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
   const int32_t out = g.crp[j];
   for (int s = lane; s < live; s += 32) {
     g.cci[out + s] = key[s];
-    g.cv[out + s] = val[s];
+    g.cv[out + s] = g.epi.out_scale ? __dmul_rn(val[s], g.epi.out_scale[key[s]]) : val[s];
   }
   if (g.epi.qrp) compare_row(g, j, key, val, live, lane);
   __syncwarp();
@@ -426,7 +426,7 @@ __device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restri
       const int32_t c = col[s];
       const double b = v[s];
       g.cci[out + s] = c;
-      g.cv[out + s] = b;
+      g.cv[out + s] = g.epi.out_scale ? __dmul_rn(b, g.epi.out_scale[c]) : b;
       if (cmp) {  // the reference's stabilized() test (sait.cpp:14-28)
         const double a = g.epi.qv[qb + s];
         const double fa = fabs(a), fb = fabs(b);

@@ -642,12 +642,13 @@ __global__ void __launch_bounds__(256, 8) spgemm_tiny(Args g, const int32_t* __r
 }
 
 // numeric pass of the tiny rows: staged slot -> final row, + early-stop
-// compare (emit_rows, 4 lanes per row of <= 8 entries, else 8).
-template <int G>
+// compare (emit_rows, L = 4 lanes per row when the output averages <= 8
+// entries per row -- stencil factors -- else 8).
+template <int G, int L>
 __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                          const int32_t* __restrict__ tcol,
                                                          const double* __restrict__ tval) {
-  emit_rows<G, (G < 16 ? 4 : 8)>(g, rows, nrows_bin, tcol, tval);
+  emit_rows<G, L>(g, rows, nrows_bin, tcol, tval);
 }
 
 // products per row (P_j) -> table bin; histogram of bins; total products
@@ -773,7 +774,8 @@ struct Plan {
   double* tval[kTinyBins] = {};
 };
 
-void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bool recompute = true) {
+void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bool recompute = true,
+                 bool short_rows = false) {
   static bool attr_set[kNumBins] = {};
   for (int tb = 0; tb < kTinyBins; ++tb) {
     const int32_t tc = pl.hist[tb];
@@ -781,20 +783,23 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     const int per_warp = 32 / kTinyG[tb];
     const int64_t warps = (tc + per_warp - 1) / per_warp;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((warps + 7) / 8, int64_t{num_sms()} * 8 * 16));
-    const int64_t rpb = tb == 0 ? 64 : 32;  // rows per 256-thread block of the emit (4 or 8 lanes per row)
+    const bool four = tb == 0 || short_rows;  // emit lanes per row: 4 or 8
+    const int64_t rpb = four ? 64 : 32;       // rows per 256-thread block of the emit
     const unsigned egrid = static_cast<unsigned>(std::min<int64_t>((tc + rpb - 1) / rpb, int64_t{num_sms()} * 8 * 16));
     const int32_t* rows = pl.lists + pl.start[tb];
     switch (kTinyG[tb]) {
       case 8:
-        if (numeric) spgemm_tiny_emit<8><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        if (numeric) spgemm_tiny_emit<8, 4><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         else spgemm_tiny<8><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         break;
       case 16:
-        if (numeric) spgemm_tiny_emit<16><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        if (numeric && four) spgemm_tiny_emit<16, 4><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        else if (numeric) spgemm_tiny_emit<16, 8><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         else spgemm_tiny<16><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         break;
       default:
-        if (numeric) spgemm_tiny_emit<32><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        if (numeric && four) spgemm_tiny_emit<32, 4><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
+        else if (numeric) spgemm_tiny_emit<32, 8><<<egrid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
         else spgemm_tiny<32><<<grid, 256, 0, s>>>(g, rows, tc, pl.tcol[tb], pl.tval[tb]);
     }
     SAIT_LAUNCHED();
@@ -957,7 +962,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   g.changed = changed;
   const bool overflow = g.stage_pos && static_cast<unsigned long long>(hmeta[1]) >
                                            static_cast<unsigned long long>(g.stage_cap);
-  launch_pass(g, pl, true, s, overflow);
+  launch_pass(g, pl, true, s, overflow, c.nnz <= 8 * n);
   if (epi.qrp) {
     int hc = 1;
     read_back(s, {{&hc, changed, sizeof hc}});

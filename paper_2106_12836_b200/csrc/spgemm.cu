@@ -878,7 +878,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   SAIT_CUDA(cudaMemsetAsync(total, 0, 2 * sizeof(unsigned long long), s));
   static const int slack_pct = [] {
     const char* e = std::getenv("SAIT_HASH_SLACK");  // table slots per possible distinct column, in %
-    return e ? std::max(101, std::atoi(e)) : 125;
+    return e ? std::max(101, std::atoi(e)) : 140;
   }();
   plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total, slack_pct);
   SAIT_LAUNCHED();

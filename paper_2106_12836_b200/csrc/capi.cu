@@ -349,7 +349,10 @@ class Recursion {
 
  private:
   sait::SpgemmResult product(const sait::Epilogue& e) {
-    return row_form_ ? sait::spgemm_fused(ttT_, a_, e, s_) : sait::spgemm_fused(a_, ttT_, e, s_);
+    if (!row_form_) return sait::spgemm_fused(a_, ttT_, e, s_);
+    // M_0 = I: the first step is tT + I filtered (no products to accumulate)
+    if (steps_run_ == 0 && (e.drop == 0 || e.drop == 1)) return sait::first_step_identity(ttT_, e, s_);
+    return sait::spgemm_fused(ttT_, a_, e, s_);
   }
   void advance(sait::SpgemmResult&& r) {
     products_ += r.products;

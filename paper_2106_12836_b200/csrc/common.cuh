@@ -204,6 +204,9 @@ struct SpgemmResult {
   int64_t products = 0;
 };
 SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi, cudaStream_t s);
+// drop(a I + I) for a strictly triangular square a with a threshold / no-drop
+// epilogue (diag_offset 0): the first row-form recursion step
+SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStream_t s);
 
 // spmv.cu
 struct __align__(16) SpmvTask {

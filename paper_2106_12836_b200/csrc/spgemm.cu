@@ -840,6 +840,82 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
 
 }  // namespace
 
+namespace {
+// First step of a row-form recursion, C = drop(A I + I): every product is
+// a_ik * 1.0 (= a_ik exactly) and A (= tT) holds no diagonal, so row i of C
+// is A's row with 1.0 inserted at column i, filtered by the drop rule --
+// the same entries and bits the generic pass produces, without planning,
+// hashing or staging.  Thread per row.  Threshold / no-drop epilogues only
+// (the caller keeps the generic pass for pattern drops).
+__device__ __forceinline__ bool first_keep(const Epilogue& e, int32_t i, int32_t col, double v) {
+  if (e.drop == 2) return in_pattern(e.pci, e.prp[i], e.prp[i + 1], col);
+  if ((e.drop == 1 || e.drop == 3) && e.tau != 0.0) return col == i || fabs(v) >= e.tau;
+  return true;
+}
+__global__ void first_step_count(int64_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                 const double* __restrict__ av, Epilogue e, int32_t* __restrict__ cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t r = static_cast<int32_t>(i);
+  int32_t c = first_keep(e, r, r, 1.0) ? 1 : 0;
+  for (int32_t q = arp[i]; q < arp[i + 1]; ++q) c += first_keep(e, r, aci[q], av[q]);
+  cnt[i] = c;
+}
+__global__ void first_step_write(int64_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                 const double* __restrict__ av, Epilogue e, const int32_t* __restrict__ crp,
+                                 int32_t* __restrict__ cci, double* __restrict__ cv) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t r = static_cast<int32_t>(i);
+  int32_t o = crp[i];
+  bool diag = first_keep(e, r, r, 1.0);
+  auto put = [&](int32_t col, double v) {
+    cci[o] = col;
+    cv[o] = e.out_scale ? __dmul_rn(v, e.out_scale[col]) : v;
+    ++o;
+  };
+  for (int32_t q = arp[i]; q < arp[i + 1]; ++q) {
+    const int32_t col = aci[q];
+    if (diag && col > r) {
+      put(r, 1.0);
+      diag = false;
+    }
+    const double v = __dmul_rn(av[q], 1.0);
+    if (first_keep(e, r, col, v)) put(col, v);
+  }
+  if (diag) put(r, 1.0);
+}
+}  // namespace
+
+SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStream_t s) {
+  SpgemmResult res;
+  const int64_t n = a.nrows;
+  DevCsr& c = res.c;
+  c.nrows = c.ncols = n;
+  c.rp = dalloc<int32_t>(n + 1, s);
+  int32_t* cnt = dalloc<int32_t>(n > 0 ? n : 1, s);
+  if (n > 0) {
+    first_step_count<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, epi, cnt);
+    SAIT_LAUNCHED();
+  }
+  c.nnz = scan_counts(cnt, c.rp, n, s);
+  dfree(cnt, s);
+  if (c.nnz > INT32_MAX)
+    throw Error(SAIT_ERR_NOMEM, "result has " + std::to_string(c.nnz) +
+                                    " stored entries; the device CSR uses int32 indices (max 2^31-1)");
+  c.ci = dalloc<int32_t>(c.nnz > 0 ? c.nnz : 1, s);
+  c.v = dalloc<double>(c.nnz > 0 ? c.nnz : 1, s);
+  if (n > 0) {
+    first_step_write<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, epi, c.rp, c.ci, c.v);
+    SAIT_LAUNCHED();
+  }
+  res.products = a.nnz;
+  // vs M_0 = I (threshold or no drop): the diagonal always survives with
+  // value 1.0, so M_1 == I exactly when nothing else survived
+  res.changed = c.nnz != n;
+  return res;
+}
+
 SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi, cudaStream_t s) {
   if (a.ncols != b.nrows)
     throw_invalid("spgemm: inner dimensions " + std::to_string(a.ncols) + " and " + std::to_string(b.nrows) +

@@ -349,10 +349,13 @@ class Recursion {
 
  private:
   sait::SpgemmResult product(const sait::Epilogue& e) {
-    if (!row_form_) return sait::spgemm_fused(a_, ttT_, e, s_);
-    // M_0 = I: the first step is tT + I filtered (no products to accumulate)
-    if (steps_run_ == 0 && (e.drop == 0 || e.drop == 1)) return sait::first_step_identity(ttT_, e, s_);
-    return sait::spgemm_fused(ttT_, a_, e, s_);
+    // M_0 = I (whole matrix): the first step is tT + I (row form) or tT^T + I
+    // (column form) filtered -- no products to accumulate.  The A15 cap cannot
+    // bind there: column j keeps at most nnz(T[:, j]) entries and the cap is
+    // floor(f nnz(T[:, j])) with f >= 1.
+    if (steps_run_ == 0 && e.diag_offset == 0 && a_.nrows == ttT_.nrows && (e.drop == 0 || e.drop == 1 || e.drop == 3))
+      return sait::first_step_identity(ttT_, e, s_);
+    return row_form_ ? sait::spgemm_fused(ttT_, a_, e, s_) : sait::spgemm_fused(a_, ttT_, e, s_);
   }
   void advance(sait::SpgemmResult&& r) {
     products_ += r.products;

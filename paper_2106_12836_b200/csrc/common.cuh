@@ -205,7 +205,8 @@ struct SpgemmResult {
 };
 SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi, cudaStream_t s);
 // drop(a I + I) for a strictly triangular square a with a threshold / no-drop
-// epilogue (diag_offset 0): the first row-form recursion step
+// epilogue (diag_offset 0; a cap epilogue is treated as threshold -- the
+// caller guarantees it cannot bind): the first recursion step
 SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStream_t s);
 
 // spmv.cu

@@ -116,6 +116,13 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def bench_config(n, nnz_l, nnz_u, ws):
+    """The workload keys both arms print (same_config)."""
+    return {"workload": WORKLOAD, "n": n, "nnz_L": nnz_l, "nnz_U": nnz_u, "bytes_per_pair": b_pair(n, nnz_l, nnz_u),
+            "vectors_per_step": NVEC, "parallelism": f"rows{ws}" if ws > 1 else "single",
+            "l2": "inputs larger than L2: 349 MB of factors streamed per pair (> 126 MB L2), no flush"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -171,7 +178,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps * NVEC / sample,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": n, "nnz_L": ML.nnz, "nnz_U": MU.nnz, "bytes_per_pair": B},
+        "config": bench_config(n, ML.nnz, MU.nnz, ws),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": f"{sample} vectors per step through SaitPairPreconditioner::apply (OpenMP {cores} threads)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -240,6 +247,84 @@ def cpu_baseline_sample(ML_host, MU_host, n):
             "sample": f"{steps} steps x 100 vectors through the reference SaitPairPreconditioner::apply "
                       f"(oracle/_ref, OpenMP {cores} threads), {t:.1f} s",
             "ms_per_step": 1e3 * t / steps, **extra}
+
+
+def time_steps(step, steps, stream, torch):
+    """ms per step of `step()` (one warm-up step, CUDA events on `stream`)."""
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def apply_format_lines(S, torch, Ld, Ud, R, Z_ref, steps, stream):
+    """The same C2 step with the factors forced into the other apply formats
+    (sait_pair_create_ex): int16 column deltas (10 B/nnz), int32 columns
+    (12 B/nnz) and plain CSR (the irregular-matrix kernel).  Each line is
+    checked bitwise against the default format's outputs."""
+    peak, _ = peaks()
+    out = {}
+    nvec, n = R.shape
+    Zv = torch.empty_like(R)
+    for fmt in ("sell32_int16", "sell32_int32", "csr"):
+        ML, MU = S.sait_thr_pair(Ld, Ud, S.SaitThrParams(TAU, STEPS_K))
+        B = b_pair(n, ML.nnz(), MU.nnz())
+        pair = S.SaitPairPreconditioner(ML, MU, format=fmt)
+
+        def step():
+            for i in range(nvec):
+                pair.apply(R[i], Zv[i])
+
+        ms = time_steps(step, steps, stream, torch)
+        fl, fu = pair.factor_format(0), pair.factor_format(1)
+        fb = fl["stream_bytes"] + fu["stream_bytes"]
+        ach = nvec * fb / (ms * 1e-3) / 1e9
+        out[fmt] = {"formats": [fl["format"], fu["format"]], "ms_per_step": ms,
+                    "effective_gbs_12B_per_nnz": nvec * B / (ms * 1e-3) / 1e9,
+                    "format_bytes_per_pair": fb, "achieved": ach, "frac": ach / peak,
+                    "bitwise_equal_default_format": bool(torch.equal(Zv, Z_ref))}
+        del pair
+    return out
+
+
+def irregular_apply_line(S, torch, T, steps, stream, nvec=20):
+    """An apply on an irregular (non-stencil) pattern: the SAIT pair of the
+    config-4 generator's T (lower, n = 2^24) and T^T (upper), tau = 1e-2,
+    k = 3 -- random geometric column offsets, so no slice patterns repeat and
+    the rows are too ragged for 32-row slices: the CSR kernel (spmv_tma)."""
+    peak, _ = peaks()
+    Tt = S.transpose(T)
+    P = S.SaitThrParams(1e-2, 3)
+    ML = S.sait_thr(T, S.lower_triangular, P)
+    MU = S.sait_thr(Tt, S.upper_triangular, P)
+    Tt.free()
+    n = T.nrows
+    B = b_pair(n, ML.nnz(), MU.nnz())
+    nnz = (ML.nnz(), MU.nnz())
+    pair = S.SaitPairPreconditioner(ML, MU)
+    R = torch.empty((nvec, n), dtype=torch.float64, device="cuda")
+    for i in range(nvec):
+        R[i].copy_(torch.from_numpy(S.uniform_pm1(SEED0 + i, n)))
+    Z = torch.empty_like(R)
+
+    def step():
+        for i in range(nvec):
+            pair.apply(R[i], Z[i])
+
+    ms = time_steps(step, steps, stream, torch)
+    fl, fu = pair.factor_format(0), pair.factor_format(1)
+    fb = fl["stream_bytes"] + fu["stream_bytes"]
+    ach = nvec * fb / (ms * 1e-3) / 1e9
+    del pair, R, Z
+    return {"workload": "SAIT pair of the c4 generator's T and T^T (n=2^24), tau=1e-2, k=3, %d vectors per step" % nvec,
+            "n": n, "nnz_L": nnz[0], "nnz_U": nnz[1], "formats": [fl["format"], fu["format"]],
+            "ms_per_step": ms, "ms_per_pair": ms / nvec, "effective_gbs_12B_per_nnz": nvec * B / (ms * 1e-3) / 1e9,
+            "format_bytes_per_pair": fb, "achieved": ach, "frac": ach / peak}
 
 
 def run_b200(args):
@@ -327,6 +412,8 @@ def run_b200(args):
         apply_dev = sp.apply
     nloc = r1 - r0
 
+    from paper_2106_12836_b200 import _native as NN
+
     # ---- 100 seeded vectors (this rank's rows) resident in HBM
     R = torch.empty((NVEC, nloc), dtype=torch.float64, device="cuda")
     for i in range(NVEC):
@@ -361,50 +448,62 @@ def run_b200(args):
     ms_step = ms / args.steps
     value = NVEC * B / (ms_step * 1e-3) / 1e9  # whole-job algorithmic GB/s (the global pair)
 
-    # ---- dominant kernel: the SELL SpMV, per-launch time on the launching stream
-    from paper_2106_12836_b200 import _native as NN
-
+    # ---- dominant kernel: the SELL SpMV.  The timed step is nothing but the
+    # 200 SpMV launches (M_L, M_U per vector, back to back on `stream`), so
+    # its average launch time is ms_step / 200 -- measured on the launching
+    # stream inside the timed region, inter-launch gaps included.  `frac` is
+    # computed on the bytes the factors' storage format must move
+    # (sait_pair_format: values + indices / slice patterns + slice offsets +
+    # x + y); the SURVEY §8(d) 12 B/nnz figure is reported separately as the
+    # "effective" rate (= value).
     roofline = None
     if ws == 1:
-        y = torch.empty(n, dtype=torch.float64, device="cuda")
-        reps = 50
+        peak, peak_kind = peaks()
+        fl, fu = pair.factor_format(0), pair.factor_format(1)
+        fmt_pair = fl["stream_bytes"] + fu["stream_bytes"]
+        per_launch_ms = ms_step / (2 * NVEC)
+        achieved = NVEC * fmt_pair / (ms_step * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02_apply_traffic.json")) as fh:
+                tr = json.load(fh)
+            traffic = tr.get("dram_bytes_per_launch_mean")
+        except Exception:
+            pass
+        # isolated per-launch times (each factor 50x on one vector): context only
         kt = {}
-        for which, nm, src, dst in ((0, "L", R[0], y), (1, "U", y, Z[0])):
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        for which, nm, src, dst in ((0, "M_L", R[0], y), (1, "M_U", y, Z[0])):
             def one():
-                NN.check(NN.lib.sait_pair_spmv_factor(pair.handle, which, src.data_ptr(), dst.data_ptr(), stream.cuda_stream))
+                NN.check(NN.lib.sait_pair_spmv_factor(pair.handle, which, src.data_ptr(), dst.data_ptr(),
+                                                      stream.cuda_stream))
             one()
             torch.cuda.synchronize()
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-            for _ in range(reps):
+            for _ in range(50):
                 one()
             a1.record(stream)
             torch.cuda.synchronize()
-            kt[nm] = a0.elapsed_time(a1) / reps
-        bytes_l = 12 * nnz_l + 4 * (n + 1) + 16 * n
-        bytes_u = 12 * nnz_u + 4 * (n + 1) + 16 * n
-        peak, peak_kind = peaks()
-        achieved = (bytes_l + bytes_u) / ((kt["L"] + kt["U"]) * 1e-3) / 1e9
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-                traffic = json.load(fh).get("spmv_traffic_bytes_per_launch")
-        except Exception:
-            pass
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": traffic, "kernel": "sell_spmv_kernel",
-                    # the DRAM bytes ncu counts per launch moved at this rate: the
-                    # kernel's share of the copy peak in bytes it really moves
-                    # (algorithmic > DRAM bytes: int16/shared index patterns, x in L2)
-                    "dram_achieved": (traffic / (0.5 * (kt["L"] + kt["U"]) * 1e-3) / 1e9) if traffic else None,
-                    "dram_frac": (traffic / (0.5 * (kt["L"] + kt["U"]) * 1e-3) / 1e9 / peak) if traffic else None,
-                    "per_launch_ms": {"M_L": kt["L"], "M_U": kt["U"]},
-                    "algorithmic_bytes_per_launch": {"M_L": bytes_l, "M_U": bytes_u},
-                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
-                    # the 8.0 TB/s nominal HBM3e figure alongside
-                    "frac_vs_nominal_8000": achieved / 8000.0,
-                    "dram_frac_vs_nominal_8000": (traffic / (0.5 * (kt["L"] + kt["U"]) * 1e-3) / 1e9 / 8000.0)
-                    if traffic else None}
+            kt[nm] = a0.elapsed_time(a1) / 50
+        roofline = {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "sell_spmv_kernel (M_L then M_U, programmatic dependent launches)",
+            "bytes_model": "format stream bytes per pair (sait_pair_format): stored values + index storage "
+                           "(here shared slice patterns: one int32 offset per 32-row slice + the dictionary) + "
+                           "int64 slice offsets + x read once + y written once, both factors",
+            "format_bytes_per_pair": fmt_pair, "formats": {"M_L": fl, "M_U": fu},
+            "per_launch_ms": per_launch_ms,
+            "per_launch_source": "ms_per_step / 200 launches, CUDA events on the launching stream (timed region)",
+            "effective_gbs_12B_per_nnz": value,
+            "effective_note": "SURVEY §8(d) algorithmic bytes (12 B/nnz + vectors) per pair / time = `value`; "
+                              "exceeds the copy peak because the format streams ~8 B/nnz",
+            "traffic_note": "ncu dram__bytes_read+write per SpMV launch, back-to-back pairs on distinct vectors, "
+                            "--cache-control none (profiles/r02_apply_traffic.json)",
+            "isolated_per_launch_ms": kt,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
+            "frac_vs_nominal_8000": achieved / 8000.0,
+        }
 
     # ---- e2e: public API with pinned host buffers, H2D + apply + D2H per vector
     Rh = torch.empty((NVEC, nloc), dtype=torch.float64).pin_memory()
@@ -456,11 +555,27 @@ def run_b200(args):
         ok = ok and bool(torch.equal(Zh, Z.cpu()))
         t_blk = float(np.median(tb))
         per_vec = e2e
+        # the reference's caller holds std::vector (pageable) buffers: the same
+        # block call on plain numpy (pageable) memory
+        Rp = np.array(Rn)  # (100, n) C order: column-major (n, 100) seen through .T
+        Zp = np.zeros_like(Rp)
+        pair.apply_block(Rp.T, Zp.T)
+        tp = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            pair.apply_block(Rp.T, Zp.T)
+            tp.append(time.perf_counter() - t0)
+        ok = ok and bool(np.array_equal(Zp.view(np.uint64), Z.cpu().numpy().view(np.uint64)))
+        t_pg = float(np.median(tp))
         e2e = {"value": NVEC * B / t_blk / 1e9, "unit": "GB/s", "h2d_bytes_per_step": NVEC * 8 * n,
                "d2h_bytes_per_step": NVEC * 8 * n, "ms_per_step": t_blk * 1e3,
-               "api": "SaitPairPreconditioner::apply_block on the (n, 100) host block "
+               "api": "SaitPairPreconditioner::apply_block on the (n, 100) pinned host block "
                       "(sait_pair_apply_block_host), median of 3 calls",
-               "per_vector_calls": {"value": per_vec["value"], "ms_per_step": per_vec["ms_per_step"]}}
+               "per_vector_calls": {"value": per_vec["value"], "ms_per_step": per_vec["ms_per_step"],
+                                    "api": "100 x SaitPairPreconditioner::apply, pinned host vectors"},
+               "pageable_block": {"value": NVEC * B / t_pg / 1e9, "ms_per_step": t_pg * 1e3,
+                                  "api": "the same apply_block call on pageable (plain numpy / std::vector) "
+                                         "host memory, median of 3 calls"}}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -496,6 +611,10 @@ def run_b200(args):
                     "device triangular solves, bitwise the reference's trisolve",
         }
 
+    formats = None
+    if ws == 1:
+        formats = apply_format_lines(S, torch, Ld, Ud, R, Z, max(1, min(args.steps, 3)), stream)
+
     build_c4 = None
     if ws == 1 and not args.no_c4:
         build_c4 = run_build_c4(S, torch, cpu_sample=not args.no_cpu_baseline)
@@ -505,14 +624,14 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": n, "nnz_L": nnz_l, "nnz_U": nnz_u, "bytes_per_pair": B,
-                       "vectors_per_step": NVEC, "parallelism": f"rows{ws}" if ws > 1 else "single",
-                       "l2": "inputs larger than L2: 349 MB of factors streamed per pair (> 126 MB L2), no flush"},
+            "config": bench_config(n, nnz_l, nnz_u, ws),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "build": build, "e2e_matches_device": ok,
         }
         if comparators:
             line["comparators"] = comparators
+        if formats:
+            line["apply_formats"] = formats
         if build_c4:
             line["build_c4"] = build_c4
         if ws > 1:
@@ -571,6 +690,7 @@ def run_build_c4(S, torch, cpu_sample=True):
             secs.append(time.perf_counter() - t0)
         nnz_m = m.nnz()
         m.free()
+    irregular = irregular_apply_line(S, torch, T, 3, torch.cuda.current_stream())
     T.free()
     nnz_steps.append(nnz_m)
     t = sorted(secs)[len(secs) // 2]
@@ -587,6 +707,7 @@ def run_build_c4(S, torch, cpu_sample=True):
                      "peak_source": src},
         "note": "wall time of the synchronous sait_build call (split, 3 recursion steps, transposes), "
                 "median of %d after a warm-up" % C4_REPS,
+        "irregular_apply": irregular,
     }
     if cpu_sample:
         out["cpu_baseline"] = c4_cpu_sample(S)

@@ -239,6 +239,27 @@ int sait_ipc_close(void *d_ptr);
  * moves its matrices in); otherwise they must outlive the pair.  Shape check
  * of preconditioner.cpp:37-39. */
 int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pair_t *out);
+/* Apply storage of a pair's factors.  AUTO (what sait_pair_create uses):
+ * SELL-32 slices with shared slice patterns when the factor repeats a few
+ * slice structures (stencil factors: only the values stream), else int16
+ * column deltas, else int32 columns; CSR when the rows are too irregular for
+ * 32-row slices (padding > 25%).  A forced SELL format falls back down that
+ * list when the matrix does not allow it; sait_pair_format reports what was
+ * used.  Every format gives the same bits (rows summed in stored order). */
+enum { SAIT_FMT_AUTO = 0, SAIT_FMT_CSR = 1, SAIT_FMT_SELL_I32 = 2, SAIT_FMT_SELL_I16 = 3, SAIT_FMT_SELL_DICT = 4 };
+int sait_pair_create_ex(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, int format, sait_pair_t *out);
+typedef struct {
+  int format;           /* SAIT_FMT_* in use (never AUTO) */
+  int64_t nrows, nnz;
+  int64_t stored_slots; /* SELL: slots incl. padding; CSR: nnz */
+  int64_t nslices, dict_elems;
+  /* bytes one SpMV with this factor must move in this format: stored
+   * values + indices (+ slice offsets, pattern offsets, dictionary) + x read
+   * once + y written once -- the denominator of the apply roofline */
+  int64_t stream_bytes;
+} sait_factor_format;
+/* which: 0 = M_L, 1 = M_U */
+int sait_pair_format(sait_pair_t p, int which, sait_factor_format *out);
 /* name() == "sait" and nnz() (preconditioner.hpp:62-63) */
 int sait_pair_info(sait_pair_t p, int64_t *n, int64_t *nnz);
 /* apply(r, z): z = M_U (M_L r), device vectors (preconditioner.cpp:42-45).

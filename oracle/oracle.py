@@ -208,6 +208,11 @@ class Oracle:
         self._check(self.lib.orc_sait_thr(C.byref(_in(t)), C.c_int(int(lower)), C.c_double(tau), C.c_int(steps), C.byref(out), C.byref(sr)))
         return self._out(out), sr.value
 
+    def sait_polynomial_tt(self, tt: Csr, steps: int) -> Csr:
+        """sait_polynomial(split, steps, {}) on the iteration matrix tt as given
+        (reference only: sait.cpp:75-88)."""
+        return self._call_csr("sait_polynomial_tt", C.byref(_in(tt)), C.c_int(steps))
+
     def sait_thr_steps(self, t: Csr, lower: bool, tau: float, steps: int):
         """(M, steps actually run) — port only."""
         return self._thr_port(t, lower, tau, steps)

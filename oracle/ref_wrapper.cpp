@@ -214,6 +214,17 @@ int ref_sait_polynomial_nodrop(const ref_csr* t, int lower, int steps, ref_csr* 
     from_ref(saitprec::sait_polynomial(s, steps, {}), out);
   });
 }
+// sait_polynomial on a caller-supplied iteration matrix (any square matrix,
+// e.g. with a stored diagonal): the reference's recursion, no drop rule.
+int ref_sait_polynomial_tt(const ref_csr* tt, int steps, ref_csr* out) {
+  return guarded([&] {
+    saitprec::JacobiSplit s;
+    s.iteration_matrix = to_ref(tt);
+    s.inv_diag.assign(static_cast<size_t>(s.iteration_matrix.nrows), 1.0);
+    s.kind = kind_of(1);
+    from_ref(saitprec::sait_polynomial(s, steps, {}), out);
+  });
+}
 int ref_sait_thr_cap(const ref_csr* t, int lower, double tau, int steps, double cap_factor,
                      ref_csr* out) {
   return guarded([&] {

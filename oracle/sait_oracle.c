@@ -172,6 +172,8 @@ int orc_spmv(const orc_csr *a, const double *x, int64_t xlen, double *y, int64_t
     return fail(ORC_INVALID_ARGUMENT, "spmv: vector length %lld does not match ncols %lld",
                 (long long)xlen, (long long)a->ncols);
   if (ylen != a->nrows) return fail(ORC_INVALID_ARGUMENT, "spmv: output length mismatch");
+  /* rows are independent: parallel over rows, each row in stored order */
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < a->nrows; ++i) {
     double acc = 0.0;
     for (int64_t e = a->row_ptr[i]; e < a->row_ptr[i + 1]; ++e) acc += a->values[e] * x[a->col_idx[e]];

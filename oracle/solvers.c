@@ -52,30 +52,64 @@ static double block_tree(double *v) {
   return w[0];
 }
 
-double orc_dot(const double *a, const double *b, int64_t n) {
-  int64_t nb = (n + DOT_B - 1) / DOT_B;
-  if (nb < 1) nb = 1;
-  double *part = (double *)malloc((size_t)nb * sizeof(double));
+/* partial of one 2048-element block (the canonical per-block order) */
+static double block_partial(const double *a, const double *b, int64_t n, int64_t blk) {
   double v[DOT_T];
-  for (int64_t blk = 0; blk < nb; ++blk) {
-    for (int t = 0; t < DOT_T; ++t) {
-      double s = 0.0;
-      for (int k = 0; k < DOT_K; ++k) {
-        int64_t i = blk * DOT_B + t + (int64_t)DOT_T * k;
-        if (i < n) s = fma(a[i], b[i], s);
-      }
-      v[t] = s;
-    }
-    part[blk] = block_tree(v);
-  }
   for (int t = 0; t < DOT_T; ++t) {
     double s = 0.0;
-    for (int64_t q = t; q < nb; q += DOT_T) s = s + part[q];
+    for (int k = 0; k < DOT_K; ++k) {
+      int64_t i = blk * DOT_B + t + (int64_t)DOT_T * k;
+      if (i < n) s = fma(a[i], b[i], s);
+    }
     v[t] = s;
   }
-  double r = block_tree(v);
+  return block_tree(v);
+}
+
+/* fold of the block partials (one 256-thread block, then the tree) */
+static double fold_partials(const double *part, int64_t nb, int64_t stride) {
+  double v[DOT_T];
+  for (int t = 0; t < DOT_T; ++t) {
+    double s = 0.0;
+    for (int64_t q = t; q < nb; q += DOT_T) s = s + part[q * stride];
+    v[t] = s;
+  }
+  return block_tree(v);
+}
+
+static int64_t dot_blocks(int64_t n) {
+  int64_t nb = (n + DOT_B - 1) / DOT_B;
+  return nb < 1 ? 1 : nb;
+}
+
+/* The blocks are independent, so they are computed in parallel (OpenMP);
+ * every partial and the fold keep the canonical order: bitwise the serial
+ * restatement for any thread count. */
+double orc_dot(const double *a, const double *b, int64_t n) {
+  int64_t nb = dot_blocks(n);
+  double *part = (double *)malloc((size_t)nb * sizeof(double));
+#pragma omp parallel for schedule(static)
+  for (int64_t blk = 0; blk < nb; ++blk) part[blk] = block_partial(a, b, n, blk);
+  double r = fold_partials(part, nb, 1);
   free(part);
   return r;
+}
+
+/* G[a * ld + b] = orc_dot(S_a, Y_b) for a < ka, b < kb (column-major blocks
+ * of n rows): the same canonical dots, computed block by block so that each
+ * 2048-row slab of S and Y is read once from memory. */
+static void multi_dot(const double *S, int ka, const double *Y, int kb, int64_t n, double *G, int ld) {
+  int64_t nb = dot_blocks(n);
+  const int np = ka * kb;
+  double *part = (double *)malloc((size_t)nb * (size_t)np * sizeof(double));
+#pragma omp parallel for schedule(static)
+  for (int64_t blk = 0; blk < nb; ++blk)
+    for (int a = 0; a < ka; ++a)
+      for (int b = 0; b < kb; ++b)
+        part[blk * np + a * kb + b] = block_partial(S + (int64_t)a * n, Y + (int64_t)b * n, n, blk);
+  for (int a = 0; a < ka; ++a)
+    for (int b = 0; b < kb; ++b) G[a * ld + b] = fold_partials(part + a * kb + b, nb, np);
+  free(part);
 }
 
 static double nrm(const double *a, int64_t n) { return sqrt(orc_dot(a, a, n)); }
@@ -140,6 +174,7 @@ int orc_gmres(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const doub
   memcpy(w, b, (size_t)n * sizeof(double)); /* r0 = b - A*0 */
   double beta = bnorm;
   while (!conv && its < maxit) {
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < n; ++e) V[e] = w[e] / beta;
     memset(g, 0, (size_t)(m + 1) * sizeof(double));
     g[0] = beta;
@@ -151,7 +186,8 @@ int orc_gmres(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const doub
       /* CGS2 */
       for (int pass = 0; pass < 2; ++pass) {
         double *hh = pass == 0 ? h : h2;
-        for (int j = 0; j <= i; ++j) hh[j] = orc_dot(V + (int64_t)j * n, w, n);
+        multi_dot(V, i + 1, w, 1, n, hh, 1); /* hh[j] = orc_dot(V_j, w) */
+#pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < n; ++e) {
           double t = w[e];
           for (int j = 0; j <= i; ++j) t = fma(-hh[j], V[(int64_t)j * n + e], t);
@@ -162,6 +198,7 @@ int orc_gmres(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const doub
       h[i + 1] = nrm(w, n);
       if (h[i + 1] != 0.0) {
         double *vn = V + (int64_t)(i + 1) * n;
+#pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < n; ++e) vn[e] = w[e] / h[i + 1];
       }
       /* Givens */
@@ -200,15 +237,18 @@ int orc_gmres(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const doub
       y[ii] = t / H[ii * m + ii];
     }
     /* x += M (V y) */
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < n; ++e) {
       double t = y[0] * V[e];
       for (int j = 1; j < k; ++j) t = fma(y[j], V[(int64_t)j * n + e], t);
       u[e] = t;
     }
     precond(ml, mu, u, z, n);
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < n; ++e) x[e] = x[e] + z[e];
     /* true residual */
     orc_spmv(a, x, n, z, n);
+#pragma omp parallel for schedule(static)
     for (int64_t e = 0; e < n; ++e) w[e] = b[e] - z[e];
     beta = nrm(w, n);
     if (beta == 0.0) conv = 1;
@@ -251,6 +291,7 @@ int orc_pcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double
         break;
       }
       double alpha = rz / pq;
+#pragma omp parallel for schedule(static)
       for (int64_t e = 0; e < n; ++e) {
         x[e] = fma(alpha, p[e], x[e]);
         r[e] = fma(-alpha, q[e], r[e]);
@@ -266,6 +307,7 @@ int orc_pcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double
       double rz2 = orc_dot(r, z, n);
       double beta = rz2 / rz;
       rz = rz2;
+#pragma omp parallel for schedule(static)
       for (int64_t e = 0; e < n; ++e) p[e] = fma(beta, p[e], z[e]);
     }
   }
@@ -294,14 +336,14 @@ int orc_pcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, const double
 
 /* G[a][b] = S_a . Y_b for a in [0,ka), b in [0,kb) */
 static void gram(const double *S, int ka, const double *Y, int kb, int64_t n, double *G, int ld) {
-  for (int a = 0; a < ka; ++a)
-    for (int b = 0; b < kb; ++b) G[a * ld + b] = orc_dot(S + (int64_t)a * n, Y + (int64_t)b * n, n);
+  multi_dot(S, ka, Y, kb, n, G, ld);
 }
 
 /* out[:, j] = sum_q in[:, q] C[q][j] (sequential q, first term a product) */
 static void lincomb_cols(const double *in, int kin, const double *C, int ldc, int kout, int64_t n, double *out) {
-  for (int j = 0; j < kout; ++j)
-    for (int64_t i = 0; i < n; ++i) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int j = 0; j < kout; ++j) {
       double t = in[i] * C[0 * ldc + j];
       for (int q = 1; q < kin; ++q) t = fma(in[(int64_t)q * n + i], C[q * ldc + j], t);
       out[(int64_t)j * n + i] = t;
@@ -484,8 +526,9 @@ int orc_lobpcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, int k, do
   lincomb_cols(AX, k, C, k, k, n, tmp);
   memcpy(AX, tmp, blk * sizeof(double));
   for (it = 0; it <= maxit; ++it) {
-    for (int j = 0; j < k; ++j)
-      for (int64_t i = 0; i < n; ++i) R[(size_t)j * n + i] = fma(-lam[j], X[(size_t)j * n + i], AX[(size_t)j * n + i]);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < k; ++j) R[(size_t)j * n + i] = fma(-lam[j], X[(size_t)j * n + i], AX[(size_t)j * n + i]);
     conv = 1;
     for (int j = 0; j < k; ++j) {
       resnorms[(size_t)it * k + j] = sqrt(orc_dot(R + (size_t)j * n, R + (size_t)j * n, n));
@@ -497,8 +540,9 @@ int orc_lobpcg(const orc_csr *a, const orc_csr *ml, const orc_csr *mu, int k, do
     {
       double G1[16 * 16];
       gram(X, k, W, k, n, G1, k);
-      for (int j = 0; j < k; ++j)
-        for (int64_t i = 0; i < n; ++i) {
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < n; ++i)
+        for (int j = 0; j < k; ++j) {
           double t = W[(size_t)j * n + i];
           for (int q = 0; q < k; ++q) t = fma(-X[(size_t)q * n + i], G1[q * k + j], t);
           W[(size_t)j * n + i] = t;

@@ -61,6 +61,7 @@ from .sait import (
     jacobi_split,
     sait_pat,
     sait_pat_capture_pattern,
+    sait_polynomial,
     sait_polynomial_nodrop,
     sait_thr,
     sait_thr_cap,

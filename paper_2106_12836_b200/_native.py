@@ -51,6 +51,17 @@ class Halo(C.Structure):
     ]
 
 
+class FactorFormat(C.Structure):
+    """sait_factor_format (include/sait_c.h)"""
+
+    _fields_ = [("format", C.c_int), ("nrows", C.c_int64), ("nnz", C.c_int64), ("stored_slots", C.c_int64),
+                ("nslices", C.c_int64), ("dict_elems", C.c_int64), ("stream_bytes", C.c_int64)]
+
+
+SAIT_FMT_AUTO, SAIT_FMT_CSR, SAIT_FMT_SELL_I32, SAIT_FMT_SELL_I16, SAIT_FMT_SELL_DICT = range(5)
+FORMAT_NAMES = {0: "auto", 1: "csr", 2: "sell32_int32", 3: "sell32_int16", 4: "sell32_dict"}
+
+
 class HostCsr(C.Structure):
     _fields_ = [
         ("nrows", C.c_int64),
@@ -141,6 +152,8 @@ PROTOTYPES = {
     "sait_exact_ilu_apply": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
     "sait_exact_ilu_destroy": (None, [VP]),
     "sait_pair_create": (C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
+    "sait_pair_create_ex": (C.c_int, [VP, VP, C.c_int, C.c_int, C.POINTER(VP)]),
+    "sait_pair_format": (C.c_int, [VP, C.c_int, C.POINTER(FactorFormat)]),
     "sait_pair_info": (C.c_int, [VP, P64, P64]),
     "sait_pair_apply": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
     "sait_pair_apply_host": (C.c_int, [VP, PD, C.c_int64, PD, C.c_int64, VP]),

@@ -79,31 +79,23 @@ struct sait_pair_s {
   sait_dcsr_s* ml = nullptr;
   sait_dcsr_s* mu = nullptr;
   bool owns = false;
-  sait::SpmvPlan pl, pu;  // persistent-pipeline task lists of the two factors
-  sait::SellMatrix sl, su;  // SELL-32 copies used by the apply (empty if irregular)
+  sait::SellMatrix sl, su;  // SELL-32 copies used by the apply (empty: CSR kernels)
   // per-stream scratch (y = M_L r): applies on one stream are ordered, so one
   // buffer per stream honours the concurrent-apply contract
-  sait::PairPlan pp;        // fused single-launch pair (needs both SELL copies)
   struct Work {
     // applies on one stream from several threads take turns (they share
     // this stream's y, staging buffers and flags)
     std::shared_ptr<std::mutex> mu = std::make_shared<std::mutex>();
     double* y = nullptr;
-    sait::PairState st;
     // host-vector pipeline (lazily created)
     cudaStream_t s_in = nullptr, s_out = nullptr;
     double *r_dev = nullptr, *z_dev = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_u;
     cudaEvent_t ev_entry = nullptr, ev_out_done = nullptr;
-    // single-launch dataflow host apply
-    int* in_flag = nullptr;   // device, one per input chunk
-    int* flag_src = nullptr;  // pinned host copy source of the epoch
     // column-major host block apply: kBlkSlots device slots per side
     double *blk_r = nullptr, *blk_z = nullptr;
     cudaEvent_t ev_blk_in[4] = {}, ev_blk_done[4] = {}, ev_blk_out[4] = {};
   };
-  sait::DataflowPlan df;
-  std::vector<int64_t> df_rows;  // input chunk boundaries of the dataflow apply
   // chunking of the host-vector apply: row boundaries (multiples of 256) and,
   // per chunk, the last r-chunk M_L needs and the last y-chunk M_U needs
   std::vector<int64_t> chunk_rows, u_rows;
@@ -283,9 +275,14 @@ struct BuildOut {
 // tT nor the result needs a transpose.
 class Recursion {
  public:
+  // op_from_split: op is the iteration matrix of jacobi_split (no stored
+  // diagonal), which the first-step filter pass relies on; the generic
+  // sait_polynomial accepts any square iteration matrix and keeps the
+  // generic product (add_identity adds 1.0 to a stored diagonal there).
   Recursion(const sait::DevCsr& op, const sait_drop_spec& spec, const int32_t* cap, int64_t c0, int64_t rows,
-            cudaStream_t s, bool row_form = false, const double* out_scale = nullptr)
-      : ttT_(op), spec_(spec), s_(s), row_form_(row_form), out_scale_(row_form ? out_scale : nullptr) {
+            cudaStream_t s, bool row_form = false, const double* out_scale = nullptr, bool op_from_split = true)
+      : ttT_(op), spec_(spec), s_(s), row_form_(row_form), out_scale_(row_form ? out_scale : nullptr),
+        op_from_split_(op_from_split) {
     a_ = sait::make_identity_rows(rows, c0, op.nrows, s);
     epi_.add_identity = true;
     epi_.diag_offset = c0;
@@ -353,7 +350,8 @@ class Recursion {
     // (column form) filtered -- no products to accumulate.  The A15 cap cannot
     // bind there: column j keeps at most nnz(T[:, j]) entries and the cap is
     // floor(f nnz(T[:, j])) with f >= 1.
-    if (steps_run_ == 0 && e.diag_offset == 0 && a_.nrows == ttT_.nrows && (e.drop == 0 || e.drop == 1 || e.drop == 3))
+    if (op_from_split_ && steps_run_ == 0 && e.diag_offset == 0 && a_.nrows == ttT_.nrows &&
+        (e.drop == 0 || e.drop == 1 || e.drop == 3))
       return sait::first_step_identity(ttT_, e, s_);
     return row_form_ ? sait::spgemm_fused(ttT_, a_, e, s_) : sait::spgemm_fused(a_, ttT_, e, s_);
   }
@@ -374,6 +372,7 @@ class Recursion {
   cudaStream_t s_;
   bool row_form_ = false;
   const double* out_scale_ = nullptr;
+  bool op_from_split_ = true;
   bool scaled_ = false;
   sait::DevCsr a_, pattern_;
   sait::Epilogue epi_;
@@ -382,8 +381,9 @@ class Recursion {
   int64_t products_ = 0;
 };
 
-BuildOut run_recursion(const sait::DevCsr& ttT, const sait_drop_spec& spec, const int32_t* cap, cudaStream_t s) {
-  Recursion r(ttT, spec, cap, 0, ttT.nrows, s);
+BuildOut run_recursion(const sait::DevCsr& ttT, const sait_drop_spec& spec, const int32_t* cap, cudaStream_t s,
+                       bool op_from_split = true) {
+  Recursion r(ttT, spec, cap, 0, ttT.nrows, s, false, nullptr, op_from_split);
   while (r.remaining() > 0)
     if (!r.step()) r.stop_stabilized();
   return r.take();
@@ -510,22 +510,6 @@ void plan_host_chunks(sait_pair_t p) {
     while (g < ng && std::max<int64_t>(run, uhi[g]) < bound_group) run = std::max<int64_t>(run, uhi[g++]);
     p->u_rows[c + 1] = std::max(p->u_rows[c], std::min(n, g * G));
   }
-}
-
-// Input chunks (~2 MB of r) of the single-launch dataflow host apply.
-void plan_dataflow(sait_pair_t p) {
-  const sait::DevCsr& L = p->ml->m;
-  const sait::DevCsr& U = p->mu->m;
-  const int64_t n = L.nrows;
-  p->df_rows.clear();
-  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 16) || !p->sl.ok() || !p->su.ok()) return;
-  double mb = 2.0;
-  if (const char* e = std::getenv("SAIT_DATAFLOW_MB")) mb = std::atof(e);
-  const int64_t G = sait::kDepGroupRows;
-  const int64_t rows = std::max<int64_t>(G, static_cast<int64_t>(mb * (1 << 20) / 8.0) / G * G);
-  for (int64_t r = 0; r < n; r += rows) p->df_rows.push_back(r);
-  p->df_rows.push_back(n);
-  p->df = sait::make_dataflow_plan(L, p->sl, U, p->su, p->df_rows, nullptr);
 }
 
 }  // namespace
@@ -1063,7 +1047,7 @@ int sait_polynomial(sait_dcsr_t tt, int steps, sait_stream_t stream, sait_dcsr_t
     cudaStream_t s = sait::as_stream(stream);
     sait::DevCsr ttT = sait::transpose(tt->m, nullptr, s);
     sait_drop_spec sp{SAIT_DROP_NONE, 0.0, steps, 0, 0, 0.0};
-    BuildOut bo = run_recursion(ttT, sp, nullptr, s);
+    BuildOut bo = run_recursion(ttT, sp, nullptr, s, /*op_from_split=*/false);
     sait::free_csr(ttT, s);
     sait::DevCsr m = sait::transpose(bo.mt, nullptr, s);
     sait::free_csr(bo.mt, s);
@@ -1163,7 +1147,7 @@ int sait_operator_create(sait_dcsr_t a, int take_ownership, sait_op_t* out) {
     op->dev = a->dev;
     op->a = a;
     op->owns = take_ownership != 0;
-    op->sell = sait::make_sell(a->m, nullptr);
+    op->sell = sait::make_sell(a->m, SAIT_FMT_AUTO, nullptr);
     *out = op;
   });
 }
@@ -1384,7 +1368,13 @@ void sait_exact_ilu_destroy(sait_exact_t p) {
 // -------------------------------------------------------- pair preconditioner
 
 int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pair_t* out) {
+  return sait_pair_create_ex(ml, mu, take_ownership, SAIT_FMT_AUTO, out);
+}
+
+int sait_pair_create_ex(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, int format, sait_pair_t* out) {
   return guarded([&] {
+    if (format < SAIT_FMT_AUTO || format > SAIT_FMT_SELL_DICT)
+      sait::throw_invalid("sait_pair_create_ex: unknown format " + std::to_string(format));
     need(ml, "SaitPairPreconditioner");
     need(mu, "SaitPairPreconditioner");
     need(out, "SaitPairPreconditioner(out)");
@@ -1398,13 +1388,11 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
     p->ml = ml;
     p->mu = mu;
     p->owns = take_ownership != 0;
-    p->pl = sait::make_spmv_plan(ml->m, nullptr);
-    p->pu = sait::make_spmv_plan(mu->m, nullptr);
-    p->sl = sait::make_sell(ml->m, nullptr);
-    p->su = sait::make_sell(mu->m, nullptr);
-    p->pp = sait::make_pair_plan(ml->m, p->sl, mu->m, p->su, nullptr);
+    if (format != SAIT_FMT_CSR) {
+      p->sl = sait::make_sell(ml->m, format, nullptr);
+      p->su = sait::make_sell(mu->m, format, nullptr);
+    }
     plan_host_chunks(p);
-    plan_dataflow(p);
     *out = p;
   });
 }
@@ -1414,6 +1402,45 @@ int sait_pair_info(sait_pair_t p, int64_t* n, int64_t* nnz) {
     need(p, "sait_pair_info");
     if (n) *n = p->ml->m.ncols;
     if (nnz) *nnz = p->ml->m.nnz + p->mu->m.nnz;
+  });
+}
+
+int sait_pair_format(sait_pair_t p, int which, sait_factor_format* out) {
+  return guarded([&] {
+    need(p, "sait_pair_format");
+    need(out, "sait_pair_format(out)");
+    const sait::DevCsr& m = which == 0 ? p->ml->m : p->mu->m;
+    const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
+    sait_factor_format f{};
+    f.nrows = m.nrows;
+    f.nnz = m.nnz;
+    // x read once (banded factors: neighbouring slices share x lines in L2),
+    // y written once
+    const int64_t vec = 8 * m.ncols + 8 * m.nrows;
+    if (!sm.ok()) {
+      f.format = SAIT_FMT_CSR;
+      f.stored_slots = m.nnz;
+      f.stream_bytes = 12 * m.nnz + 4 * (m.nrows + 1) + vec;
+    } else {
+      f.stored_slots = sm.padded;
+      f.nslices = sm.nslices;
+      f.dict_elems = sm.dict_elems;
+      const int64_t soff = 8 * (sm.nslices + 1);
+      switch (sm.index_kind()) {
+        case 2:  // values stream; one int32 pattern offset per slice; the dictionary once
+          f.format = SAIT_FMT_SELL_DICT;
+          f.stream_bytes = 8 * sm.padded + soff + 4 * sm.nslices + 4 * sm.dict_elems + vec;
+          break;
+        case 1:
+          f.format = SAIT_FMT_SELL_I16;
+          f.stream_bytes = 10 * sm.padded + soff + vec;
+          break;
+        default:
+          f.format = SAIT_FMT_SELL_I32;
+          f.stream_bytes = 12 * sm.padded + soff + vec;
+      }
+    }
+    *out = f;
   });
 }
 
@@ -1428,14 +1455,6 @@ int sait_pair_factors(sait_pair_t p, sait_dcsr_t* ml, sait_dcsr_t* mu) {
 }  // extern "C"
 
 namespace {
-int pair_variant() {
-  static int v = [] {
-    const char* e = std::getenv("SAIT_PAIR");
-    return e ? std::atoi(e) : 2;
-  }();
-  return v;
-}
-
 // M_U's SpMV is launched as a programmatic dependent of M_L's (PDL): its
 // CTAs start and load their matrix slices while M_L's tail runs, then wait
 // (griddepcontrol.wait) before touching y.  SAIT_PDL=0 disables.
@@ -1451,13 +1470,10 @@ bool pdl_enabled() {
 void factor_spmv(sait_pair_t p, int which, const double* x, double* y, cudaStream_t s) {
   const sait::DevCsr& m = which == 0 ? p->ml->m : p->mu->m;
   const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
-  const sait::SpmvPlan& pl = which == 0 ? p->pl : p->pu;
-  const int v = pair_variant();
   // both halves are programmatic dependents of whatever precedes them on s:
   // M_U of M_L, and M_L of the previous kernel (e.g. the last apply's M_U),
   // each loading its first index/value batch before griddepcontrol.wait
-  if (v >= 2 && sm.ok()) sait::sell_spmv_rows(sm, 0, sm.n, x, y, s, pdl_enabled());
-  else if (v == 1) sait::spmv_planned(m, pl, x, y, s);
+  if (sm.ok()) sait::sell_spmv_rows(sm, 0, sm.n, x, y, s, pdl_enabled());
   else sait::spmv(m, x, y, s);
 }
 
@@ -1468,11 +1484,6 @@ sait_pair_s::Work& pair_work(sait_pair_t p, cudaStream_t s) {
   sait_pair_s::Work w;
   const int64_t n = p->ml->m.nrows;
   SAIT_CUDA(cudaMalloc(&w.y, sizeof(double) * (n > 0 ? n : 1) + 256));
-  const int64_t ng = std::max<int64_t>(std::max<int64_t>(p->pp.gL, p->df.gL), 1);
-  SAIT_CUDA(cudaMalloc(&w.st.done, sizeof(int) * ng));
-  SAIT_CUDA(cudaMalloc(&w.st.counter, sizeof(unsigned long long)));
-  SAIT_CUDA(cudaMemset(w.st.done, 0, sizeof(int) * ng));
-  SAIT_CUDA(cudaMemset(w.st.counter, 0, sizeof(unsigned long long)));
   SAIT_CUDA(cudaDeviceSynchronize());
   return p->ws.emplace(s, w).first->second;
 }
@@ -1605,14 +1616,6 @@ void pair_apply_host_chunked(sait_pair_t p, const double* h_r, double* h_z, cuda
   SAIT_CUDA(cudaStreamSynchronize(s));
 }
 
-// The single-launch zero-copy host apply is opt-in (SAIT_HOST_DATAFLOW=1):
-// on PCIe5 its SM-driven transfers saturate at ~70 GB/s combined, slightly
-// below the copy-engine pipeline (~90 GB/s), which therefore is the default.
-bool host_dataflow_enabled() {
-  const char* e = std::getenv("SAIT_HOST_DATAFLOW");
-  return e && std::atoi(e) == 1;
-}
-
 // Host memory the GPU can address directly (pinned / registered under UVA).
 bool device_mapped(const void* p) {
   cudaPointerAttributes a;
@@ -1621,30 +1624,6 @@ bool device_mapped(const void* p) {
     return false;
   }
   return a.type == cudaMemoryTypeHost && a.devicePointer == p;
-}
-
-// Single-launch host apply: copy-engine input chunks + per-chunk epoch flags,
-// one persistent kernel for both SpMVs, z written to host memory directly.
-void pair_apply_host_dataflow(sait_pair_t p, const double* h_r, double* h_z, cudaStream_t s) {
-  sait_pair_s::Work& w = pair_work(p, s);
-  std::lock_guard<std::mutex> lk(*w.mu);
-  const int64_t k = static_cast<int64_t>(p->df_rows.size()) - 1;
-  const int64_t n = p->ml->m.nrows;
-  if (!w.in_flag) {
-    ensure_side_streams(w);
-    if (!w.r_dev) {
-      SAIT_CUDA(cudaMalloc(&w.r_dev, sizeof(double) * n + 256));
-      SAIT_CUDA(cudaMalloc(&w.z_dev, sizeof(double) * n + 256));
-    }
-    SAIT_CUDA(cudaMalloc(&w.in_flag, sizeof(int) * (p->df.npieces + k)));
-    SAIT_CUDA(cudaMemset(w.in_flag, 0, sizeof(int) * (p->df.npieces + k)));
-    SAIT_CUDA(cudaMallocHost(&w.flag_src, sizeof(int) * k));
-    SAIT_CUDA(cudaDeviceSynchronize());
-  }
-  const int epoch = ++w.st.epoch;
-  sait::sell_dataflow_apply(p->sl, p->su, p->df, w.st, w.in_flag, epoch, h_r, w.r_dev, w.y, h_z, s);
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  SAIT_CUDA(cudaStreamSynchronize(w.s_in));
 }
 
 // Column-major block of HOST vectors (apply_block, preconditioner.cpp:47-49):
@@ -1751,7 +1730,6 @@ void pair_apply_block_host_pipelined(sait_pair_t p, const double* h_r, double* h
   SAIT_CUDA(cudaEventRecord(w.ev_entry, s));
   SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_entry, 0));
   SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_entry, 0));
-  const bool fused = pair_variant() == 3 && p->pp.ok();
   // SAIT_DEBUG_BLK: per-group device timeline (H2D, pairs, D2H start/end) to stderr
   static const bool dbg = std::getenv("SAIT_DEBUG_BLK") != nullptr;
   std::vector<cudaEvent_t> tl;
@@ -1780,12 +1758,8 @@ void pair_apply_block_host_pipelined(sait_pair_t p, const double* h_r, double* h
       SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_blk_out[q], 0));  // z of gi-slots copied out
     mark(s);
     for (int64_t c = 0; c < g; ++c) {
-      if (fused) {
-        sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, r + c * n, w.y, z + c * n, s);
-      } else {
-        factor_spmv(p, 0, r + c * n, w.y, s);
-        factor_spmv(p, 1, w.y, z + c * n, s);
-      }
+      factor_spmv(p, 0, r + c * n, w.y, s);
+      factor_spmv(p, 1, w.y, z + c * n, s);
     }
     mark(s);
     SAIT_CUDA(cudaEventRecord(w.ev_blk_done[q], s));
@@ -1824,12 +1798,8 @@ namespace sait {
 void pair_apply_internal(sait_pair_t p, const double* r, double* z, cudaStream_t s) {
   sait_pair_s::Work& w = pair_work(p, s);
   std::lock_guard<std::mutex> lk(*w.mu);  // the two launches of one apply stay adjacent on s
-  if (pair_variant() == 3 && p->pp.ok()) {
-    sait::sell_pair_apply(p->sl, p->su, p->pp, w.st, r, w.y, z, s);
-  } else {
-    factor_spmv(p, 0, r, w.y, s);
-    factor_spmv(p, 1, w.y, z, s);
-  }
+  factor_spmv(p, 0, r, w.y, s);
+  factor_spmv(p, 1, w.y, z, s);
 }
 int64_t pair_dim(sait_pair_t p) { return p->ml->m.ncols; }
 int pair_device(sait_pair_t p) { return p->dev; }
@@ -1887,9 +1857,7 @@ int sait_pair_apply_host(sait_pair_t p, const double* h_r, int64_t rlen, double*
     if (zlen != U.nrows) sait::throw_invalid("spmv: output length mismatch");
     DeviceGuard g(p->dev);
     cudaStream_t s = host_call_stream(stream);
-    if (host_dataflow_enabled() && p->df.ok() && device_mapped(h_r) && device_mapped(h_z))
-      pair_apply_host_dataflow(p, h_r, h_z, s);
-    else if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, s);
+    if (p->chunk_rows.size() >= 3) pair_apply_host_chunked(p, h_r, h_z, s);
     else sait::pair_apply_host_pipelined(L, U, h_r, h_z, s);
   });
 }
@@ -1902,7 +1870,7 @@ void factor_spmm(sait_pair_t p, int which, const double* x, double* y, int nvec,
     return;
   }
   const sait::SellMatrix& sm = which == 0 ? p->sl : p->su;
-  if (pair_variant() >= 2 && sm.ok() && sait::sell_spmm(sm, x, y, nvec, s)) return;
+  if (sm.ok() && sait::sell_spmm(sm, x, y, nvec, s)) return;
   sait::spmm_rowmajor(which == 0 ? p->ml->m : p->mu->m, x, y, nvec, s);
 }
 
@@ -1935,7 +1903,7 @@ void apply_block_device(sait_pair_t p, const double* d_r, double* d_z, int64_t n
     sait::dfree(y, s);
     return;
   }
-  if (layout == 0 && pair_variant() >= 2 && p->sl.ok() && p->su.ok()) {
+  if (layout == 0 && p->sl.ok() && p->su.ok()) {
     // column-major straight through the SELL block kernels (no transposes)
     double* y = sait::dalloc<double>(L.nrows * nvec, s);
     sait::sell_spmm_colmajor(p->sl, d_r, n, y, L.nrows, static_cast<int>(nvec), s);
@@ -2011,16 +1979,11 @@ void sait_pair_destroy(sait_pair_t p) {
     cudaGetDevice(&prev);
     cudaSetDevice(p->dev);
     cudaDeviceSynchronize();
-    sait::free_spmv_plan(p->pl, nullptr);
-    sait::free_spmv_plan(p->pu, nullptr);
     sait::free_sell(p->sl, nullptr);
     sait::free_sell(p->su, nullptr);
-    sait::free_pair_plan(p->pp, nullptr);
     for (auto& kv : p->ws) {
       auto& w = kv.second;
       cudaFree(w.y);
-      cudaFree(w.st.done);
-      cudaFree(w.st.counter);
       if (w.r_dev) cudaFree(w.r_dev);
       if (w.z_dev) cudaFree(w.z_dev);
       if (w.blk_r) cudaFree(w.blk_r);
@@ -2034,10 +1997,7 @@ void sait_pair_destroy(sait_pair_t p) {
       if (w.ev_out_done) cudaEventDestroy(w.ev_out_done);
       if (w.s_in) cudaStreamDestroy(w.s_in);
       if (w.s_out) cudaStreamDestroy(w.s_out);
-      if (w.in_flag) cudaFree(w.in_flag);
-      if (w.flag_src) cudaFreeHost(w.flag_src);
     }
-    sait::free_dataflow_plan(p->df, nullptr);
     cudaDeviceSynchronize();
     if (prev >= 0) cudaSetDevice(prev);
   }

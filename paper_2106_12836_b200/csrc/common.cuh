@@ -86,6 +86,21 @@ inline void free_csr(DevCsr& m, cudaStream_t s) {
   m.v = nullptr;
 }
 
+// Function attributes (dynamic shared memory limits, carve-outs) belong to a
+// device context: true the first time `key` is seen on the current device
+// (thread-safe; the pair build runs two host threads).
+inline bool first_on_device(const void* key) {
+  static std::mutex m;
+  static std::vector<std::pair<int, const void*>> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(m);
+  for (const auto& e : seen)
+    if (e.first == dev && e.second == key) return false;
+  seen.emplace_back(dev, key);
+  return true;
+}
+
 inline int num_sms() {
   static int sms = [] {
     int dev = 0, n = 148;
@@ -210,20 +225,6 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
 SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStream_t s);
 
 // spmv.cu
-struct __align__(16) SpmvTask {
-  int32_t row0, nrows;  // row-block
-  int32_t c0, c1;       // nnz chunk [c0, c1)
-  int32_t flags;        // 1: first chunk of its row-block, 2: last chunk
-};
-struct SpmvPlan {
-  SpmvTask* tasks = nullptr;
-  int32_t* cta_start = nullptr;
-  int64_t ntasks = 0;
-  int grid = 0;
-};
-SpmvPlan make_spmv_plan(const DevCsr& a, cudaStream_t s);
-void free_spmv_plan(SpmvPlan& p, cudaStream_t s);
-void spmv_planned(const DevCsr& a, const SpmvPlan& p, const double* x, double* y, cudaStream_t s);
 // sell.cu
 struct SellMatrix {
   int64_t n = 0, nslices = 0, padded = 0;
@@ -239,51 +240,15 @@ struct SellMatrix {
   bool ok() const { return soff != nullptr; }
   int index_kind() const { return dict ? 2 : dcol ? 1 : 0; }  // 2 dict, 1 int16, 0 int32
 };
-SellMatrix make_sell(const DevCsr& a, cudaStream_t s);  // empty if too irregular
+// format: SAIT_FMT_AUTO (dictionary > int16 deltas > int32 columns, whichever
+// applies; SAIT_SELL_DICT=0 / SAIT_SELL_INDEX=32 steer it) or one forced
+// SAIT_FMT_SELL_* (falling back down that list when the matrix does not allow
+// it).  Empty if too irregular for slicing (padding > 25%): CSR kernels.
+SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s);
 void free_sell(SellMatrix& m, cudaStream_t s);
-// fused persistent pair kernel (z = M_U (M_L r) in one launch)
-struct PairPlan {
-  int64_t gL = 0, gU = 0;  // 256-row groups of each factor
-  int32_t* dep_lo = nullptr;
-  int32_t* dep_hi = nullptr;
-  int grid = 0;
-  bool ok() const { return dep_lo != nullptr; }
-};
-struct PairState {  // per (pair, stream): flags + claim counter, ordered by the stream
-  int* done = nullptr;
-  unsigned long long* counter = nullptr;
-  unsigned long long claims = 0;
-  int epoch = 0;
-};
 // per 256-row group g of m: [lo[g], hi[g]] = 256-column groups its entries touch
 void column_group_deps(const DevCsr& m, int32_t* lo, int32_t* hi, cudaStream_t s);
 constexpr int64_t kDepGroupRows = 256;
-// single-launch host-vector apply (copy-engine input chunks + flags,
-// zero-copy output)
-struct DataflowPlan {
-  int64_t gL = 0, gU = 0;
-  int32_t* lneed = nullptr;
-  int32_t* order = nullptr;
-  int32_t* lp_lo = nullptr;  // per M_L group: input pieces read
-  int32_t* lp_hi = nullptr;
-  int64_t piece = 0, npieces = 0;
-  int32_t* dep_lo = nullptr;
-  int32_t* dep_hi = nullptr;
-  int grid = 0;
-  bool ok() const { return lneed != nullptr; }
-};
-struct PairState;
-DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
-                                const std::vector<int64_t>& chunk_rows, cudaStream_t s);
-void free_dataflow_plan(DataflowPlan& p, cudaStream_t s);
-PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
-                        cudaStream_t s);
-void free_pair_plan(PairPlan& p, cudaStream_t s);
-void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
-                     const double* r, double* y, double* z, cudaStream_t s);
-void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const DataflowPlan& dp, PairState& st,
-                         int* in_flag, int epoch, const double* r_host, double* r_dev, double* y, double* z_host,
-                         cudaStream_t s);
 void sell_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
 // row block of a sharded factor reading its halo from peer buffers (sell.cu)
 struct HaloArgs {

@@ -427,274 +427,8 @@ unsigned sell_grid(int64_t nslices) {  // one slice per warp, 8 warps per CTA
   return static_cast<unsigned>(std::max<int64_t>(1, (nslices + 7) / 8));
 }
 
-// ------------------------------------------------------------------ fused pair
-// z = M_U (M_L r) in ONE persistent launch.  Tasks are 256-row groups (8 slices,
-// one per warp): [0, gL) are M_L groups writing y, [gL, gL + gU) are M_U groups
-// reading y.  CTAs claim tasks in order from a counter, so every M_L group is
-// claimed before any M_U group and waiting never deadlocks.  A finished M_L
-// group publishes done[g] = epoch (release); an M_U group first issues its
-// own index/value loads, then checks (acquire) the flags of the y groups its
-// columns touch — precomputed per group — so the flag latency hides behind
-// the matrix stream, and reads y through L2 (ld.cg).
+// rows per dependency group of the chunked host apply (column_group_deps)
 constexpr int kGroupRows = 256;
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ double ld_cg(const double* p) {
-  double r;
-  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
-  return r;
-}
-
-struct PairArgs {
-  int64_t nL, nU;                 // rows of M_L (= len y) and M_U (= len z)
-  int64_t slicesL, slicesU, gL, gU;
-  const int64_t* soffL;
-  const int32_t* colL;
-  const double* valL;
-  const int64_t* soffU;
-  const int32_t* colU;
-  const double* valU;
-  const int32_t* dep_lo;          // per M_U group: first / last y group read
-  const int32_t* dep_hi;
-  const double* r;
-  double* y;
-  double* z;
-  int* done;
-  unsigned long long* counter;
-  unsigned long long base;
-  int epoch;
-};
-
-template <bool FROM_L2>
-__device__ __forceinline__ double slice_row(const int64_t* __restrict__ soff, const int32_t* __restrict__ scol,
-                                            const double* __restrict__ sval, int64_t s, int lane,
-                                            const double* __restrict__ x) {
-  const int64_t base = soff[s];
-  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
-  const int32_t* cp = scol + base + lane;
-  const double* vp = sval + base + lane;
-  double acc = 0.0;
-  for (int32_t k0 = 0; k0 < w; k0 += 8) {
-    int32_t c[8];
-    double v[8], xv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      c[j] = -1;
-      v[j] = 0.0;
-      if (k0 + j < w) {
-        c[j] = ld_na(cp + (k0 + j) * kSlice);
-        v[j] = ld_na(vp + (k0 + j) * kSlice);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (FROM_L2) xv[j] = c[j] >= 0 ? ld_cg(x + c[j]) : 0.0;
-      else xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
-  }
-  return acc;
-}
-
-__global__ void __launch_bounds__(256) sell_pair_kernel(PairArgs a) {
-  // the next task is claimed while the current one runs (its atomic latency
-  // hides behind the matrix stream); claim order stays global, so an M_L task
-  // is never queued behind an M_U task on the same CTA.
-  __shared__ long long task_s[2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long total = a.gL + a.gU;
-  if (threadIdx.x == 0) task_s[0] = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
-  __syncthreads();
-  int buf = 0;
-  while (true) {
-    const long long t = task_s[buf];
-    if (t >= total) break;
-    unsigned long long nxt = 0;
-    if (threadIdx.x == 0) nxt = atomicAdd(a.counter, 1ull);
-    if (t < a.gL) {
-      const int64_t s = t * 8 + warp;
-      if (s < a.slicesL) {
-        const double acc = slice_row<false>(a.soffL, a.colL, a.valL, s, lane, a.r);
-        const int64_t row = s * kSlice + lane;
-        if (row < a.nL) a.y[row] = acc;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        st_release(a.done + t, a.epoch);
-      }
-    } else {
-      const int64_t g = t - a.gL;
-      const int32_t lo = a.dep_lo[g], hi = a.dep_hi[g];
-      bool ok;
-      do {
-        ok = true;
-        for (int32_t k = lo + static_cast<int32_t>(threadIdx.x); k <= hi; k += blockDim.x)
-          ok = ok && ld_acquire(a.done + k) == a.epoch;
-        ok = __syncthreads_and(ok);
-        if (!ok) __nanosleep(64);
-      } while (!ok);
-      const int64_t s = g * 8 + warp;
-      if (s < a.slicesU) {
-        const double acc = slice_row<true>(a.soffU, a.colU, a.valU, s, lane, a.y);
-        const int64_t row = s * kSlice + lane;
-        if (row < a.nU) a.z[row] = acc;
-      }
-    }
-    if (threadIdx.x == 0) task_s[buf ^ 1] = static_cast<long long>(nxt - a.base);
-    __syncthreads();
-    buf ^= 1;
-  }
-}
-
-// ------------------------------------------------------------ host dataflow
-// z = M_U (M_L r) for HOST r / z in one persistent launch.  The copy engine
-// streams r into r_dev chunk by chunk, each chunk followed by a 4-byte copy of
-// the call's epoch into in_flag[c]; M_L row groups run once the chunk holding
-// their last column has landed (acquire), M_U row groups once the y groups
-// they read are done (release/acquire flags, as in the fused pair), and M_U
-// stores z straight into pinned host memory (zero-copy), so the D2H stream
-// overlaps the H2D stream instead of following it.
-struct DataflowArgs {
-  int64_t n, slicesL, slicesU, gL, gU;
-  const int64_t* soffL;
-  const int64_t* soffU;
-  const double* valL;
-  const double* valU;
-  const int32_t* order;     // task t -> group (M_L group g, or gL + M_U group)
-  const int32_t* lneed;     // per M_L group: input chunk that must have landed
-  const int32_t* dep_lo;    // per M_U group: y groups read
-  const int32_t* dep_hi;
-  int* in_flag;             // per input piece (epoch when landed)
-  const double* r_host;     // host-mapped r (zero-copy loads)
-  int64_t piece;            // doubles per input piece
-  int64_t npieces;
-  const int32_t* lp_lo;     // per M_L group: input pieces its columns read
-  const int32_t* lp_hi;
-  double* r;                // device copy of r
-  double* y;
-  double* z;                // host-mapped output
-  int* done;                // per M_L group
-  unsigned long long* counter;
-  unsigned long long base;
-  int epoch;
-  unsigned long long* trace;  // optional: globaltimer at the end of each task
-};
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-template <class IDX>
-__device__ __forceinline__ double slice_row_idx(const int64_t* __restrict__ soff, IDX idx,
-                                                const double* __restrict__ sval, int64_t s, int lane,
-                                                const double* __restrict__ x) {
-  const int64_t base = soff[s];
-  const int64_t ib = idx.slice_base(s, base);
-  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
-  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
-  double acc = 0.0;
-  for (int32_t k0 = 0; k0 < w; k0 += 8) {
-    int32_t c[8];
-    double v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      c[j] = -1;
-      v[j] = 0.0;
-      if (k0 + j < w) {
-        c[j] = idx.col(ib + lane + static_cast<int64_t>(k0 + j) * kSlice, row);
-        v[j] = ld_na(sval + base + lane + static_cast<int64_t>(k0 + j) * kSlice);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double xv = c[j] >= 0 ? ld_cg(x + c[j]) : 0.0;
-      if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
-    }
-  }
-  return acc;
-}
-
-template <class IDX>
-__global__ void __launch_bounds__(256) sell_dataflow_kernel(DataflowArgs a, IDX il, IDX iu) {
-  __shared__ long long task_s[2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long total = a.gL + a.gU + a.npieces;
-  if (threadIdx.x == 0) task_s[0] = static_cast<long long>(atomicAdd(a.counter, 1ull) - a.base);
-  __syncthreads();
-  int buf = 0;
-  while (true) {
-    const long long claim = task_s[buf];
-    if (claim >= total) break;
-    const long long t = a.order[claim];
-    unsigned long long nxt = 0;
-    if (threadIdx.x == 0) nxt = atomicAdd(a.counter, 1ull);
-    if (t >= a.gL + a.gU) {  // input piece: host r -> device r (zero-copy loads)
-      const int64_t q = t - a.gL - a.gU;
-      const int64_t b = q * a.piece, e = b + a.piece < a.n ? b + a.piece : a.n;
-      for (int64_t i = b + 2 * threadIdx.x; i < e; i += 2 * blockDim.x) {
-        if (i + 1 < e) {
-          const double2 v = __ldcv(reinterpret_cast<const double2*>(a.r_host + i));
-          *reinterpret_cast<double2*>(a.r + i) = v;
-        } else {
-          a.r[i] = __ldcv(a.r_host + i);
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) st_release(a.in_flag + q, a.epoch);
-    } else if (t < a.gL) {
-      const int32_t lo = a.lp_lo[t], hi = a.lp_hi[t];
-      bool ok;
-      do {
-        ok = true;
-        for (int32_t k = lo + static_cast<int32_t>(threadIdx.x); k <= hi; k += blockDim.x)
-          ok = ok && ld_acquire(a.in_flag + k) == a.epoch;
-        ok = __syncthreads_and(ok);
-        if (!ok) __nanosleep(128);
-      } while (!ok);
-      const int64_t s = t * 8 + warp;
-      if (s < a.slicesL) {
-        const double acc = slice_row_idx(a.soffL, il, a.valL, s, lane, a.r);
-        const int64_t row = s * kSlice + lane;
-        if (row < a.n) a.y[row] = acc;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) st_release(a.done + t, a.epoch);
-    } else {
-      const int64_t g = t - a.gL;
-      const int32_t lo = a.dep_lo[g], hi = a.dep_hi[g];
-      bool ok;
-      do {
-        ok = true;
-        for (int32_t k = lo + static_cast<int32_t>(threadIdx.x); k <= hi; k += blockDim.x)
-          ok = ok && ld_acquire(a.done + k) == a.epoch;
-        ok = __syncthreads_and(ok);
-        if (!ok) __nanosleep(128);
-      } while (!ok);
-      const int64_t s = g * 8 + warp;
-      if (s < a.slicesU) {
-        const double acc = slice_row_idx(a.soffU, iu, a.valU, s, lane, a.y);
-        const int64_t row = s * kSlice + lane;
-        if (row < a.n) a.z[row] = acc;
-      }
-    }
-    if (a.trace && threadIdx.x == 0) a.trace[t] = globaltimer();
-    if (threadIdx.x == 0) task_s[buf ^ 1] = static_cast<long long>(nxt - a.base);
-    __syncthreads();
-    buf ^= 1;
-  }
-}
 
 }  // namespace
 
@@ -795,12 +529,12 @@ __global__ void slice_gather_dict(int64_t nslices, const int64_t* __restrict__ s
 // Replace the per-entry indices (int16 deltas or int32 columns) by a
 // dictionary of the distinct slices' int32 delta blocks when it is small
 // (<= 1M deltas) and actually saves bytes.
-void try_slice_dictionary(SellMatrix& m, cudaStream_t s) {
+void try_slice_dictionary(SellMatrix& m, bool forced, cudaStream_t s) {
   static const bool off = [] {
     const char* e = std::getenv("SAIT_SELL_DICT");
     return e && std::atoi(e) == 0;
   }();
-  if (off || (!m.dcol && !m.col) || m.nslices == 0) return;
+  if ((off && !forced) || (!m.dcol && !m.col) || m.nslices == 0) return;
   const int64_t ns = m.nslices;
   unsigned long long* dh = dalloc<unsigned long long>(ns, s);
   if (m.dcol) slice_hash<<<grid_for(ns * kSlice, 256), 256, 0, s>>>(ns, m.soff, Idx16{m.dcol}, dh);
@@ -866,7 +600,7 @@ void try_slice_dictionary(SellMatrix& m, cudaStream_t s) {
 
 }  // namespace
 
-SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
+SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s) {
   SellMatrix m;
   m.n = a.nrows;
   if (a.nrows == 0 || !a.v) return m;
@@ -898,8 +632,9 @@ SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
     const char* e = std::getenv("SAIT_SELL_INDEX");
     return e && std::atoi(e) == 32;
   }();
+  const bool want32 = format == SAIT_FMT_SELL_I32 || (format == SAIT_FMT_AUTO && force32);
   m.val = dalloc<double>(m.padded, s);
-  if (maxd <= 32767 && !force32) {
+  if (maxd <= 32767 && !want32) {
     m.dcol = dalloc<int16_t>(m.padded, s);
     fill_sell16<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.dcol, m.val);
   } else {
@@ -908,244 +643,8 @@ SellMatrix make_sell(const DevCsr& a, cudaStream_t s) {
   }
   SAIT_LAUNCHED();
   SAIT_CUDA(cudaStreamSynchronize(s));
-  try_slice_dictionary(m, s);
+  if (format == SAIT_FMT_AUTO || format == SAIT_FMT_SELL_DICT) try_slice_dictionary(m, format == SAIT_FMT_SELL_DICT, s);
   return m;
-}
-
-PairPlan make_pair_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
-                        cudaStream_t s) {
-  PairPlan p;
-  if (!sl.ok() || !su.ok() || !sl.col || !su.col) return p;  // fused kernel: int32 columns only
-  p.gL = (L.nrows + kGroupRows - 1) / kGroupRows;
-  p.gU = (U.nrows + kGroupRows - 1) / kGroupRows;
-  p.dep_lo = dalloc<int32_t>(p.gU, s);
-  p.dep_hi = dalloc<int32_t>(p.gU, s);
-  if (p.gU) {
-    pair_deps<<<grid_for(p.gU, 128), 128, 0, s>>>(U.nrows, U.rp, U.ci, p.gU, p.dep_lo, p.dep_hi);
-    SAIT_LAUNCHED();
-  }
-  int per_sm = 0;
-  SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_pair_kernel, 256, 0));
-  p.grid = std::max(1, per_sm) * num_sms();
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  return p;
-}
-
-void free_pair_plan(PairPlan& p, cudaStream_t s) {
-  dfree(p.dep_lo, s);
-  dfree(p.dep_hi, s);
-  p = PairPlan{};
-}
-
-void sell_pair_apply(const SellMatrix& sl, const SellMatrix& su, const PairPlan& pp, PairState& st,
-                     const double* r, double* y, double* z, cudaStream_t s) {
-  PairArgs a;
-  a.nL = sl.n;
-  a.nU = su.n;
-  a.slicesL = sl.nslices;
-  a.slicesU = su.nslices;
-  a.gL = pp.gL;
-  a.gU = pp.gU;
-  a.soffL = sl.soff;
-  a.colL = sl.col;
-  a.valL = sl.val;
-  a.soffU = su.soff;
-  a.colU = su.col;
-  a.valU = su.val;
-  a.dep_lo = pp.dep_lo;
-  a.dep_hi = pp.dep_hi;
-  a.r = r;
-  a.y = y;
-  a.z = z;
-  a.done = st.done;
-  a.counter = st.counter;
-  const unsigned grid = static_cast<unsigned>(pp.grid);
-  a.base = st.claims;
-  a.epoch = ++st.epoch;
-  st.claims += static_cast<unsigned long long>(pp.gL + pp.gU) + grid;
-  sell_pair_kernel<<<grid, 256, 0, s>>>(a);
-  SAIT_LAUNCHED();
-}
-
-DataflowPlan make_dataflow_plan(const DevCsr& L, const SellMatrix& sl, const DevCsr& U, const SellMatrix& su,
-                                const std::vector<int64_t>& chunk_rows, cudaStream_t s) {
-  DataflowPlan p;
-  const bool same_idx = sl.index_kind() == su.index_kind();
-  if (!sl.ok() || !su.ok() || !same_idx || L.nrows != U.nrows || chunk_rows.size() < 2) return p;
-  p.gL = (L.nrows + kGroupRows - 1) / kGroupRows;
-  p.gU = p.gL;
-  p.dep_lo = dalloc<int32_t>(p.gU, s);
-  p.dep_hi = dalloc<int32_t>(p.gU, s);
-  pair_deps<<<grid_for(p.gU, 128), 128, 0, s>>>(U.nrows, U.rp, U.ci, p.gU, p.dep_lo, p.dep_hi);
-  SAIT_LAUNCHED();
-  int32_t* llo = dalloc<int32_t>(p.gL, s);
-  int32_t* lhi = dalloc<int32_t>(p.gL, s);
-  pair_deps<<<grid_for(p.gL, 128), 128, 0, s>>>(L.nrows, L.rp, L.ci, p.gL, llo, lhi);
-  SAIT_LAUNCHED();
-  std::vector<int32_t> hhi(p.gL), hlo(p.gL), need(p.gL);
-  SAIT_CUDA(cudaMemcpyAsync(hhi.data(), lhi, sizeof(int32_t) * p.gL, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaMemcpyAsync(hlo.data(), llo, sizeof(int32_t) * p.gL, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  dfree(llo, s);
-  dfree(lhi, s);
-  // input pieces (64 KB of r each) and the piece range every M_L group reads
-  std::vector<int32_t> plo_h, phi_h;
-  p.piece = 8192;
-  p.npieces = (L.nrows + p.piece - 1) / p.piece;
-  {
-    plo_h.assign(p.gL, 0);
-    phi_h.assign(p.gL, 0);
-    auto& plo = plo_h;
-    auto& phi = phi_h;
-    for (int64_t g = 0; g < p.gL; ++g) {
-      const int64_t own0 = g * kGroupRows, own1 = std::min(L.nrows, (g + 1) * kGroupRows) - 1;
-      const int64_t c0 = hhi[g] >= hlo[g] ? std::min<int64_t>(own0, int64_t{hlo[g]} * kGroupRows) : own0;
-      const int64_t c1 = hhi[g] >= hlo[g] ? std::max<int64_t>(own1, int64_t{hhi[g]} * kGroupRows + kGroupRows - 1) : own1;
-      plo[g] = static_cast<int32_t>(c0 / p.piece);
-      phi[g] = static_cast<int32_t>(std::min<int64_t>(c1, L.nrows - 1) / p.piece);
-    }
-    p.lp_lo = dalloc<int32_t>(p.gL, s);
-    p.lp_hi = dalloc<int32_t>(p.gL, s);
-    SAIT_CUDA(cudaMemcpyAsync(p.lp_lo, plo.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
-    SAIT_CUDA(cudaMemcpyAsync(p.lp_hi, phi.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
-  }
-  // chunk holding the last column each M_L group reads (its own chunk at least)
-  const int64_t nchunks = static_cast<int64_t>(chunk_rows.size()) - 1;
-  for (int64_t g = 0; g < p.gL; ++g) {
-    const int64_t last_row = std::max<int64_t>((hhi[g] + 1) * kGroupRows - 1, std::min(L.nrows, (g + 1) * kGroupRows) - 1);
-    int64_t c = std::upper_bound(chunk_rows.begin(), chunk_rows.end(), std::min<int64_t>(last_row, L.nrows - 1)) -
-                chunk_rows.begin() - 1;
-    need[g] = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(c, 0), nchunks - 1));
-  }
-  p.lneed = dalloc<int32_t>(p.gL, s);
-  SAIT_CUDA(cudaMemcpyAsync(p.lneed, need.data(), sizeof(int32_t) * p.gL, cudaMemcpyHostToDevice, s));
-  // Task order: per input chunk c, its M_L groups, then the M_U groups whose y
-  // reads end inside chunks <= c — so z starts streaming out while r is still
-  // streaming in.  Every wait is on a task claimed earlier: deadlock-free.
-  std::vector<int32_t> uhi(p.gU);
-  SAIT_CUDA(cudaMemcpyAsync(uhi.data(), p.dep_hi, sizeof(int32_t) * p.gU, cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  std::vector<int32_t> order;
-  order.reserve(p.gL + p.gU + p.npieces);
-  int64_t ug = 0, run = -1, next_piece = 0;
-  const int32_t in_base = static_cast<int32_t>(p.gL + p.gU);
-  auto push_pieces_upto = [&](int64_t row_end) {  // input tasks for rows < row_end
-    const int64_t last = std::min<int64_t>(p.npieces, (row_end + p.piece - 1) / p.piece);
-    while (next_piece < last) order.push_back(in_base + static_cast<int32_t>(next_piece++));
-  };
-  for (int64_t c = 0; c < nchunks; ++c) {
-    // inputs of chunk c and (prefetch) c + 1 before chunk c's compute tasks
-    push_pieces_upto(chunk_rows[std::min<int64_t>(c + 2, nchunks)]);
-    const int64_t g0 = chunk_rows[c] / kGroupRows;
-    const int64_t g1 = (chunk_rows[c + 1] + kGroupRows - 1) / kGroupRows;
-    int64_t need_piece = -1;  // every input an M_L group waits for is queued before it
-    for (int64_t g = g0; g < g1 && g < p.gL; ++g) need_piece = std::max<int64_t>(need_piece, phi_h[g]);
-    push_pieces_upto((need_piece + 1) * p.piece);
-    for (int64_t g = g0; g < g1 && g < p.gL; ++g) order.push_back(static_cast<int32_t>(g));
-    const int64_t bound = c + 1 < nchunks ? chunk_rows[c + 1] / kGroupRows : INT64_MAX;
-    while (ug < p.gU && std::max<int64_t>(run, uhi[ug]) < bound) {
-      run = std::max<int64_t>(run, uhi[ug]);
-      order.push_back(static_cast<int32_t>(p.gL + ug++));
-    }
-  }
-  while (ug < p.gU) order.push_back(static_cast<int32_t>(p.gL + ug++));
-  push_pieces_upto(L.nrows);
-  p.order = dalloc<int32_t>(order.size(), s);
-  SAIT_CUDA(cudaMemcpyAsync(p.order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
-  int per_sm = 0;
-  if (sl.dict) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<IdxDict>, 256, 0));
-  else if (sl.dcol) SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx16>, 256, 0));
-  else SAIT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_dataflow_kernel<Idx32>, 256, 0));
-  p.grid = std::max(1, per_sm) * num_sms();
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  return p;
-}
-
-void free_dataflow_plan(DataflowPlan& p, cudaStream_t s) {
-  dfree(p.dep_lo, s);
-  dfree(p.dep_hi, s);
-  dfree(p.lneed, s);
-  dfree(p.order, s);
-  dfree(p.lp_lo, s);
-  dfree(p.lp_hi, s);
-  p = DataflowPlan{};
-}
-
-void sell_dataflow_apply(const SellMatrix& sl, const SellMatrix& su, const DataflowPlan& dp, PairState& st,
-                         int* in_flag, int epoch, const double* r_host, double* r_dev, double* y, double* z_host,
-                         cudaStream_t s) {
-  DataflowArgs a;
-  a.n = sl.n;
-  a.slicesL = sl.nslices;
-  a.slicesU = su.nslices;
-  a.gL = dp.gL;
-  a.gU = dp.gU;
-  a.soffL = sl.soff;
-  a.soffU = su.soff;
-  a.valL = sl.val;
-  a.valU = su.val;
-  a.order = dp.order;
-  a.lneed = dp.lneed;
-  a.dep_lo = dp.dep_lo;
-  a.dep_hi = dp.dep_hi;
-  a.in_flag = in_flag;
-  a.r_host = r_host;
-  a.piece = dp.piece;
-  a.npieces = dp.npieces;
-  a.lp_lo = dp.lp_lo;
-  a.lp_hi = dp.lp_hi;
-  a.r = r_dev;
-  a.y = y;
-  a.z = z_host;
-  a.done = st.done;
-  a.counter = st.counter;
-  a.base = st.claims;
-  a.epoch = epoch;
-  a.trace = nullptr;
-  static const bool dbg = std::getenv("SAIT_DEBUG_DATAFLOW") != nullptr;
-  const int64_t ntask = dp.gL + dp.gU + dp.npieces;
-  unsigned long long* tr = nullptr;
-  unsigned long long t0 = 0;
-  if (dbg) {
-    SAIT_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * ntask));
-    a.trace = tr;
-  }
-  const unsigned grid = static_cast<unsigned>(dp.grid);
-  st.claims += static_cast<unsigned long long>(dp.gL + dp.gU + dp.npieces) + grid;
-  if (sl.dict)
-    sell_dataflow_kernel<IdxDict><<<grid, 256, 0, s>>>(a, IdxDict{sl.pat, sl.dict}, IdxDict{su.pat, su.dict});
-  else if (sl.dcol) sell_dataflow_kernel<Idx16><<<grid, 256, 0, s>>>(a, Idx16{sl.dcol}, Idx16{su.dcol});
-  else sell_dataflow_kernel<Idx32><<<grid, 256, 0, s>>>(a, Idx32{sl.col}, Idx32{su.col});
-  SAIT_LAUNCHED();
-  if (dbg) {
-    std::vector<unsigned long long> h(ntask);
-    SAIT_CUDA(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * ntask, cudaMemcpyDeviceToHost, s));
-    SAIT_CUDA(cudaStreamSynchronize(s));
-    cudaFree(tr);
-    t0 = *std::min_element(h.begin(), h.end());
-    auto stat = [&](int64_t b, int64_t e, const char* nm) {
-      unsigned long long mx = 0, mn = ~0ull;
-      for (int64_t i = b; i < e; ++i) {
-        mx = std::max(mx, h[i] - t0);
-        mn = std::min(mn, h[i] - t0);
-      }
-      std::fprintf(stderr, "%s first=%.1fus last=%.1fus  ", nm, mn / 1e3, mx / 1e3);
-    };
-    stat(0, dp.gL, "L");
-    stat(dp.gL, dp.gL + dp.gU, "U");
-    stat(dp.gL + dp.gU, ntask, "IN");
-    // input progress: time by which each quarter of the pieces had landed
-    std::vector<unsigned long long> ins(h.begin() + dp.gL + dp.gU, h.end());
-    std::sort(ins.begin(), ins.end());
-    for (int qq = 1; qq <= 4; ++qq)
-      std::fprintf(stderr, "IN%d/4=%.1fus ", qq, (ins[ins.size() * qq / 4 - 1] - t0) / 1e3);
-    std::vector<unsigned long long> us(h.begin() + dp.gL, h.begin() + dp.gL + dp.gU);
-    std::sort(us.begin(), us.end());
-    for (int qq = 1; qq <= 4; ++qq)
-      std::fprintf(stderr, "U%d/4=%.1fus ", qq, (us[us.size() * qq / 4 - 1] - t0) / 1e3);
-    std::fprintf(stderr, "\n");
-  }
 }
 
 void free_sell(SellMatrix& m, cudaStream_t s) {

@@ -56,7 +56,7 @@ namespace {
 struct Operator {
   const DevCsr* a;
   SellMatrix sell;
-  Operator(const DevCsr& m, cudaStream_t s) : a(&m), sell(make_sell(m, s)) {}
+  Operator(const DevCsr& m, cudaStream_t s) : a(&m), sell(make_sell(m, SAIT_FMT_AUTO, s)) {}
   void apply(const double* x, double* y, cudaStream_t s) const {
     if (sell.ok()) sell_spmv(sell, x, y, s);
     else spmv(*a, x, y, s);

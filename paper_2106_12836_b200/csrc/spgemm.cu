@@ -776,7 +776,6 @@ struct Plan {
 
 void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bool recompute = true,
                  bool short_rows = false) {
-  static bool attr_set[kNumBins] = {};
   for (int tb = 0; tb < kTinyBins; ++tb) {
     const int32_t tc = pl.hist[tb];
     if (!tc) continue;
@@ -819,10 +818,8 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     int warps = warps_for_bin(b);
     int smem = warps * smem_per_warp(b - kFirstSmemBin + kMinLogSlots);
     SmemKernel k = smem_kernel(b);
-    if (!attr_set[b]) {
+    if (first_on_device(reinterpret_cast<const void*>(k)))
       SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr_set[b] = true;
-    }
     int blocks_per_sm = std::max(1, (228 * 1024) / (smem + 1024));
     int64_t want = (cnt + warps - 1) / warps;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, int64_t{num_sms()} * blocks_per_sm * 4));

@@ -124,79 +124,6 @@ __global__ void __launch_bounds__(kRows) spmv_tma(int64_t n, const int32_t* __re
   if (my < r1) y[my] = acc;
 }
 
-// Persistent, multi-stage pipelined SpMV (the apply's hot kernel).
-// Work is a static list of tasks (row-block of 256 rows, nnz chunk <= 2048);
-// each CTA owns a contiguous task range (cut at row-block boundaries) and
-// runs a PS-deep ring of shared-memory stages: thread 0 keeps PS-1 bulk
-// copies (column indices, values and the row-block's row_ptr slice) in
-// flight while the CTA forms the products of the current stage in place and
-// each thread sums its own row sequentially (reference order, bitwise).
-constexpr int kPipeStages = 4;
-struct __align__(16) PipeStage {
-  double val[kTChunk + 8];
-  int32_t col[kTChunk + 8];
-  int32_t rp[264];
-};
-
-__device__ __forceinline__ void pipe_issue(const SpmvTask& tk, PipeStage* st, uint64_t* bar,
-                                           const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                           const double* __restrict__ v, uint64_t pol) {
-  const int32_t a0 = tk.c0 & ~3;
-  const int32_t cnt = tk.c1 > tk.c0 ? ((tk.c1 - a0 + 3) & ~3) : 0;
-  const uint32_t rpb = static_cast<uint32_t>((tk.nrows + 1 + 3) & ~3) * 4u;
-  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(cnt) * 12u + rpb);
-  bulk_g2s(st->rp, rp + tk.row0, rpb, bar);
-  if (cnt) {
-    bulk_g2s_stream(st->col, ci + a0, static_cast<uint32_t>(cnt) * 4u, bar, pol);
-    bulk_g2s_stream(st->val, v + a0, static_cast<uint32_t>(cnt) * 8u, bar, pol);
-  }
-}
-
-__global__ void __launch_bounds__(kRows) spmv_pipe(const SpmvTask* __restrict__ tasks,
-                                                    const int32_t* __restrict__ cta_start,
-                                                    const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                                    const double* __restrict__ v, const double* __restrict__ x,
-                                                    double* __restrict__ y) {
-  extern __shared__ __align__(128) unsigned char pipe_smem[];
-  PipeStage* st = reinterpret_cast<PipeStage*>(pipe_smem);
-  __shared__ uint64_t full[kPipeStages];
-  const int tid = threadIdx.x;
-  const int32_t t0 = cta_start[blockIdx.x], t1 = cta_start[blockIdx.x + 1];
-  const uint64_t pol = policy_evict_first();
-  if (tid == 0) {
-    for (int k = 0; k < kPipeStages; ++k) mbar_init(&full[k], 1);
-    fence_mbar_init();
-    for (int k = 0; k < kPipeStages && t0 + k < t1; ++k) pipe_issue(tasks[t0 + k], &st[k], &full[k], rp, ci, v, pol);
-  }
-  __syncthreads();
-  double acc = 0.0;
-  int it = 0;
-  for (int32_t t = t0; t < t1; ++t, ++it) {
-    const int s = it % kPipeStages;
-    const SpmvTask tk = tasks[t];
-    mbar_wait(&full[s], (it / kPipeStages) & 1);
-    PipeStage& S = st[s];
-    const int32_t a0 = tk.c0 & ~3;
-    const int lo = tk.c0 - a0, hi = tk.c1 - a0;
-#pragma unroll 4
-    for (int e = lo + tid; e < hi; e += kRows) S.val[e] = __dmul_rn(S.val[e], __ldg(x + S.col[e]));
-    __syncthreads();
-    if (tk.flags & 1) acc = 0.0;
-    if (tid < tk.nrows) {
-      const int32_t mb = S.rp[tid], me = S.rp[tid + 1];
-      const int32_t b = mb > tk.c0 ? mb : tk.c0;
-      const int32_t e = me < tk.c1 ? me : tk.c1;
-      for (int32_t q = b; q < e; ++q) acc = __dadd_rn(acc, S.val[q - a0]);
-      if (tk.flags & 2) y[tk.row0 + tid] = acc;
-    }
-    __syncthreads();
-    if (tid == 0 && t + kPipeStages < t1) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      pipe_issue(tasks[t + kPipeStages], &S, &full[s], rp, ci, v, pol);
-    }
-  }
-}
-
 // Row-major block: x is ncols x NV, y is nrows x NV.  Thread (row, vec).
 template <int NV>
 __global__ void __launch_bounds__(256) spmm_rowblock(int64_t n, const int32_t* __restrict__ rp,
@@ -250,77 +177,7 @@ __global__ void block_transpose_kernel(const double* __restrict__ in, double* __
   }
 }
 
-constexpr int kPipeCtasPerSm = 2;
-
 }  // namespace
-
-SpmvPlan make_spmv_plan(const DevCsr& a, cudaStream_t s) {
-  SpmvPlan p;
-  const int64_t n = a.nrows;
-  const int64_t nb = (n + kRows - 1) / kRows;
-  if (n == 0) return p;
-  std::vector<int32_t> hrp(n + 1);
-  SAIT_CUDA(cudaMemcpyAsync(hrp.data(), a.rp, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  std::vector<SpmvTask> tasks;
-  tasks.reserve(nb + 16);
-  std::vector<int64_t> blk_first(nb);
-  for (int64_t b = 0; b < nb; ++b) {
-    int32_t r0 = static_cast<int32_t>(b * kRows);
-    int32_t nr = static_cast<int32_t>(std::min<int64_t>(kRows, n - r0));
-    int32_t z0 = hrp[r0], z1 = hrp[r0 + nr];
-    blk_first[b] = static_cast<int64_t>(tasks.size());
-    int32_t c = z0;
-    do {
-      int32_t c1 = z1 - c > kTChunk ? c + kTChunk : z1;
-      SpmvTask t{r0, nr, c, c1, (c == z0 ? 1 : 0) | (c1 == z1 ? 2 : 0)};
-      tasks.push_back(t);
-      c = c1;
-    } while (c < z1);
-  }
-  const int64_t nt = static_cast<int64_t>(tasks.size());
-  int grid = static_cast<int>(std::min<int64_t>(int64_t{num_sms()} * kPipeCtasPerSm, nb));
-  std::vector<int32_t> start(grid + 1);
-  // contiguous task ranges, cut only where a row-block starts
-  for (int c = 0; c <= grid; ++c) {
-    int64_t want = nt * c / grid;
-    int64_t b = std::upper_bound(blk_first.begin(), blk_first.end(), want - 1) - blk_first.begin();
-    start[c] = c == grid ? static_cast<int32_t>(nt) : static_cast<int32_t>(b < nb ? blk_first[b] : nt);
-    if (c > 0 && start[c] < start[c - 1]) start[c] = start[c - 1];
-  }
-  start[0] = 0;
-  p.ntasks = nt;
-  p.grid = grid;
-  p.tasks = dalloc<SpmvTask>(nt, s);
-  p.cta_start = dalloc<int32_t>(grid + 1, s);
-  SAIT_CUDA(cudaMemcpyAsync(p.tasks, tasks.data(), sizeof(SpmvTask) * nt, cudaMemcpyHostToDevice, s));
-  SAIT_CUDA(cudaMemcpyAsync(p.cta_start, start.data(), sizeof(int32_t) * (grid + 1), cudaMemcpyHostToDevice, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  return p;
-}
-
-void free_spmv_plan(SpmvPlan& p, cudaStream_t s) {
-  dfree(p.tasks, s);
-  dfree(p.cta_start, s);
-  p = SpmvPlan{};
-}
-
-void spmv_planned(const DevCsr& a, const SpmvPlan& p, const double* x, double* y, cudaStream_t s) {
-  if (a.nrows == 0) return;
-  if (!p.tasks) {
-    spmv(a, x, y, s);
-    return;
-  }
-  constexpr int smem = kPipeStages * static_cast<int>(sizeof(PipeStage));
-  static bool attr = [] {
-    cudaFuncSetAttribute(spmv_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(spmv_pipe, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    return true;
-  }();
-  (void)attr;
-  spmv_pipe<<<p.grid, kRows, smem, s>>>(p.tasks, p.cta_start, a.rp, a.ci, a.v, x, y);
-  SAIT_LAUNCHED();
-}
 
 int spmv_variant() {
   static int v = [] {
@@ -335,11 +192,8 @@ void spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s) {
   if (spmv_variant() == 0) {
     spmv_rowblock<<<grid_for(a.nrows, kRows), kRows, 0, s>>>(a.nrows, a.rp, a.ci, a.v, x, y);
   } else {
-    static bool attr = [] {
-      cudaFuncSetAttribute(spmv_tma, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      return true;
-    }();
-    (void)attr;
+    if (first_on_device(reinterpret_cast<const void*>(spmv_tma)))
+      SAIT_CUDA(cudaFuncSetAttribute(spmv_tma, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     spmv_tma<<<grid_for(a.nrows, kRows), kRows, 0, s>>>(a.nrows, a.rp, a.ci, a.v, x, y);
   }
   SAIT_LAUNCHED();

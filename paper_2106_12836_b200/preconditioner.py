@@ -60,13 +60,19 @@ def _is_cuda_tensor(x) -> bool:
 class SaitPairPreconditioner(Preconditioner):
     """preconditioner.hpp:54-68; preconditioner.cpp:34-49."""
 
-    def __init__(self, lower_inverse, upper_inverse, stream=None):
+    def __init__(self, lower_inverse, upper_inverse, stream=None, format: str = "auto"):
+        """``format`` (not in the reference): the factors' apply storage --
+        "auto" (default), "csr", "sell32_int32", "sell32_int16", "sell32_dict";
+        every format gives the same bits (sait_pair_create_ex)."""
+        fmt = {v: k for k, v in N.FORMAT_NAMES.items()}.get(format)
+        if fmt is None:
+            raise ValueError(f"unknown apply format {format!r}")
         self._host_l = lower_inverse if isinstance(lower_inverse, CsrMatrix) else None
         self._host_u = upper_inverse if isinstance(upper_inverse, CsrMatrix) else None
         dl = lower_inverse if isinstance(lower_inverse, DeviceCsr) else DeviceCsr.upload(lower_inverse, stream)
         du = upper_inverse if isinstance(upper_inverse, DeviceCsr) else DeviceCsr.upload(upper_inverse, stream)
         h = C.c_void_p()
-        N.check(N.lib.sait_pair_create(dl.handle, du.handle, 1, C.byref(h)))
+        N.check(N.lib.sait_pair_create_ex(dl.handle, du.handle, 1, fmt, C.byref(h)))
         dl.release()
         du.release()  # the pair owns both factors now (the reference ctor moves them in)
         self._h = h
@@ -74,6 +80,15 @@ class SaitPairPreconditioner(Preconditioner):
         N.check(N.lib.sait_pair_info(self._h, C.byref(n), C.byref(nnz)))
         self.n = n.value
         self._nnz = nnz.value
+
+    def factor_format(self, which: int) -> dict:
+        """Apply storage of M_L (which=0) or M_U (which=1): format name, stored
+        slots, slices, dictionary size and ``stream_bytes`` (what one SpMV
+        must move in that format: the roofline denominator)."""
+        f = N.FactorFormat()
+        N.check(N.lib.sait_pair_format(self._h, int(which), C.byref(f)))
+        return {"format": N.FORMAT_NAMES[f.format], "nrows": f.nrows, "nnz": f.nnz, "stored_slots": f.stored_slots,
+                "nslices": f.nslices, "dict_elems": f.dict_elems, "stream_bytes": f.stream_bytes}
 
     # -- interface
     def name(self) -> str:

@@ -115,6 +115,19 @@ def sait_polynomial_nodrop(t, kind: TriangularKind, steps: int, stream=None, sta
     return build(t, kind, spec, stream, stats_out)
 
 
+def sait_polynomial(tt, steps: int, stream=None, stats_out=None):
+    """sait.hpp:53 / sait.cpp:75-88 with an empty DropRule: the unit-diagonal
+    recursion M <- tt M + I on the iteration matrix ``tt`` as given (any square
+    matrix; a stored diagonal gets 1.0 added by add_identity), no scaling."""
+    dt, host = _dev(tt, stream)
+    h = C.c_void_p()
+    st = N.BuildStats()
+    N.check(N.lib.sait_polynomial(dt.handle, int(steps), _stream_handle(stream), C.byref(h), C.byref(st)))
+    if stats_out is not None:
+        stats_out.append(BuildStats(st.steps_run, bool(st.stabilized), st.nnz_out, st.products, st.seconds))
+    return _out(h, host, stream)
+
+
 def sait_pat_capture_pattern(t, kind: TriangularKind, pattern_steps: int, stream=None):
     """sait.hpp:64 / sait.cpp:103-111 (returns a pattern: values None)."""
     dt, host = _dev(t, stream)

@@ -237,26 +237,65 @@ def test_chunked_host_apply_3d(S, port, sched, zc, monkeypatch):
     assert bitwise_equal(zd.cpu().numpy(), ez)
 
 
-@pytest.mark.parametrize("mb", ["0.25", "0.5", "2"])
-def test_dataflow_host_apply_chunks(S, port, mb, monkeypatch):
-    """Single-launch host apply (copy-engine chunks + flags, zero-copy z) with
-    several chunk sizes: bitwise equal to the oracle, repeatable."""
+FORMATS = ["auto", "csr", "sell32_int32", "sell32_int16", "sell32_dict"]
+
+
+@pytest.mark.parametrize("fmt", FORMATS)
+def test_forced_apply_formats(S, port, fmt):
+    """sait_pair_create_ex: every apply storage (CSR, SELL-32 with int32
+    columns / int16 deltas / shared slice patterns) gives the oracle's bits
+    for the single apply, the block apply and the host apply, and
+    sait_pair_format reports the storage and its stream bytes."""
     import torch
 
     from helpers import to_oracle
 
-    monkeypatch.setenv("SAIT_DATAFLOW_MB", mb)
-    monkeypatch.setenv("SAIT_HOST_DATAFLOW", "1")
-    A = S.laplacian_3d(64)
+    A = S.laplacian_3d(24)
     f = S.ilu_k(A, 0)
     ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
     MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
-    pair = S.SaitPairPreconditioner(ML, MU)
-    for seed in (7, 8, 9):
-        r = torch.from_numpy(S.uniform_pm1(seed, A.nrows)).pin_memory()
-        z = torch.zeros_like(r).pin_memory()
-        pair.apply(r.numpy(), z.numpy())
-        assert bitwise_equal(z.numpy(), port.pair_apply(to_oracle(ML), to_oracle(MU), r.numpy()))
+    eL, eU = to_oracle(ML), to_oracle(MU)
+    pair = S.SaitPairPreconditioner(ML, MU, format=fmt)
+    n = A.nrows
+    for w in (0, 1):
+        info = pair.factor_format(w)
+        want = "sell32_dict" if fmt == "auto" else fmt
+        assert info["format"] == want
+        nnz = (ML if w == 0 else MU).nnz()
+        assert info["nnz"] == nnz and info["stored_slots"] >= nnz
+        per = {"csr": 12, "sell32_int32": 12, "sell32_int16": 10, "sell32_dict": 8}[want]
+        assert info["stream_bytes"] >= per * info["stored_slots"] + 16 * n
+    r = S.uniform_pm1(11, n)
+    z = np.empty(n)
+    pair.apply(r, z)
+    assert bitwise_equal(z, port.pair_apply(eL, eU, r))
+    rd = torch.from_numpy(r).cuda()
+    zd = torch.empty_like(rd)
+    pair.apply(rd, zd)
+    torch.cuda.synchronize()
+    assert bitwise_equal(zd.cpu().numpy(), z)
+    R = np.stack([S.uniform_pm1(20 + j, n) for j in range(8)], axis=1)
+    Z = pair.apply_block(R)
+    assert bitwise_equal(np.asarray(Z), port.pair_apply_block(eL, eU, R))
+    with pytest.raises(ValueError):
+        S.SaitPairPreconditioner(ML, MU, format="ellpack")
+
+
+def test_irregular_factor_takes_csr(S, port):
+    """Factors too irregular for 32-row slices (padding > 25%) keep the CSR
+    kernels under every requested format, with the oracle's bits."""
+    from helpers import to_oracle
+
+    T = S.synthetic_lower(1 << 14, 15, 0.01, 4)
+    M = S.sait_thr(T, S.lower_triangular, S.SaitThrParams(1e-2, 3))
+    Mt = S.transpose(M)
+    pair = S.SaitPairPreconditioner(M, Mt, format="sell32_int32")
+    formats = [pair.factor_format(w)["format"] for w in (0, 1)]
+    r = S.uniform_pm1(5, M.nrows)
+    z = np.empty(M.nrows)
+    pair.apply(r, z)
+    assert bitwise_equal(z, port.pair_apply(to_oracle(M), to_oracle(Mt), r))
+    assert set(formats) <= {"csr", "sell32_int32"}
 
 
 _DICT_CHILD = r"""

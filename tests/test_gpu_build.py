@@ -171,8 +171,39 @@ for tau, k in ((1e-2, 3), (0.0, 3)):
 """
 
 
+@pytest.mark.parametrize("steps", [1, 2, 5])
+@pytest.mark.parametrize("case", ["diag_only", "golden_T", "zero_diag"])
+def test_sait_polynomial_stored_diagonal(S, ref, golden, case, steps):
+    """The generic sait_polynomial (sait.cpp:75-88) accepts any square
+    iteration matrix: add_identity (kernels.cpp:104-134) adds 1.0 to a stored
+    diagonal.  The device must not take the first-step filter pass (which
+    assumes jacobi_split's diagonal-free tT) there; bitwise vs the reference,
+    same step count."""
+    from oracle.oracle import Csr
+
+    if case == "diag_only":
+        n = 64
+        tt = Csr(n, n, np.arange(n + 1), np.arange(n), np.linspace(-0.5, 0.7, n))
+    else:
+        tt = golden_csr(golden, "syn_lower/T")
+        if case == "zero_diag":
+            vals = tt.values.copy() * 0.1
+            for i in range(tt.nrows):
+                for q in range(tt.row_ptr[i], tt.row_ptr[i + 1]):
+                    if tt.col_idx[q] == i:
+                        vals[q] = 0.0
+            tt = Csr(tt.nrows, tt.ncols, tt.row_ptr, tt.col_idx, vals)
+        else:
+            tt = Csr(tt.nrows, tt.ncols, tt.row_ptr, tt.col_idx, tt.values * 0.1)
+    want = ref.sait_polynomial_tt(tt, steps)
+    st = []
+    got = S.sait_polynomial(to_product(tt), steps, stats_out=st)
+    assert bitwise_equal_csr(got, want)
+
+
+@pytest.mark.parametrize("column_form", ["0", "1"])
 @pytest.mark.parametrize("cap", ["none", "0", "1000", "200000"])
-def test_hash_rows_staging_and_overflow(cap):
+def test_hash_rows_staging_and_overflow(cap, column_form):
     """Hash-table rows (hundreds of products) stage their sorted survivors in
     the count pass; rows past the staging capacity are recomputed in the
     numeric pass.  Every split (all staged, none, a few, most) gives the
@@ -183,7 +214,7 @@ def test_hash_rows_staging_and_overflow(cap):
 
     from conftest import ROOT
 
-    env = dict(os.environ)
+    env = dict(os.environ, SAIT_BUILD_COLUMN_FORM=column_form)
     if cap == "none":
         env["SAIT_SPGEMM_NOSTAGE"] = "1"
     else:
@@ -194,18 +225,20 @@ def test_hash_rows_staging_and_overflow(cap):
     assert out.stdout.split() == ["1", "1"]
 
 
+@pytest.mark.parametrize("column_form", ["0", "1"])
 @pytest.mark.parametrize("slack", ["101", "400"])
-def test_hash_table_load_factors(slack):
+def test_hash_table_load_factors(slack, column_form):
     """Hash tables sized at the minimum (slots just above the possible distinct
     columns: long linear probes, nearly full tables) and at 4x give the same
-    bits as the oracle (SAIT_HASH_SLACK, percent; the default is 125)."""
+    bits as the oracle (SAIT_HASH_SLACK, percent; the default is 140), in
+    both the row-form and the column-form recursion."""
     import os
     import subprocess
     import sys
 
     from conftest import ROOT
 
-    env = dict(os.environ, SAIT_HASH_SLACK=slack)
+    env = dict(os.environ, SAIT_HASH_SLACK=slack, SAIT_BUILD_COLUMN_FORM=column_form)
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]

@@ -194,6 +194,35 @@ int sait_ilu_device(sait_dcsr_t a, int level, sait_stream_t stream, sait_dcsr_t 
 int sait_trisolve(sait_dcsr_t t, int lower, const double *d_b, int64_t blen, double *d_x,
                   sait_stream_t stream);
 
+/* --------------------------------------- multi-GPU redistribution (K4) ---
+ * The distributed form of transpose (csr.cpp:72-92) that turns the
+ * column-sharded build's blocks M[:, C_r:C_{r+1}] into the row blocks of the
+ * row-sharded apply without a host round trip. */
+
+/* One received piece: rows [0, nrows) of a CSR whose entries of row i are
+ * col_idx/values[row_ptr[i] - row_ptr[0] .. row_ptr[i+1] - row_ptr[0]) (device
+ * pointers; row_ptr may start at any base), columns shifted by col_offset. */
+typedef struct {
+  const int32_t *row_ptr;
+  const int32_t *col_idx;
+  const double *values;
+  int64_t col_offset;
+} sait_row_piece;
+/* Row i of *out = the pieces' rows i concatenated in part order.  Parts must
+ * cover disjoint, ascending column ranges (then rows stay sorted). */
+int sait_csr_assemble_rows(int nparts, const sait_row_piece *parts, int64_t nrows, int64_t ncols,
+                           sait_stream_t stream, sait_dcsr_t *out);
+/* [*lo, *hi) = the range of stored columns ((0, 0) when empty). */
+int sait_csr_col_span(sait_dcsr_t m, int64_t *lo, int64_t *hi, sait_stream_t stream);
+/* In place: every column index += offset; ncols = new_ncols. */
+int sait_csr_shift_cols(sait_dcsr_t m, int64_t offset, int64_t new_ncols, sait_stream_t stream);
+/* out[j] = row_ptr[rows[j]] for k host row indices (host in, host out). */
+int sait_csr_row_ptr_at(sait_dcsr_t m, const int64_t *rows, int k, int64_t *out, sait_stream_t stream);
+/* d_work[j] (device, n int64) = predicted products of column j's recursion
+ * (its step-2 work: sum over the entries (k, j) of tT of nnz(tT[:, k]) + 1);
+ * the column-sharded build balances its blocks on the prefix sums. */
+int sait_column_work(sait_dcsr_t t, int64_t *d_work, sait_stream_t stream);
+
 /* ------------------------------------------------------- SpMV operator ---
  * A prepared y = A x for a (possibly rectangular) device CSR: keeps the
  * SELL-32 copy when the rows are regular enough (the apply's kernel), else the
@@ -223,6 +252,23 @@ typedef struct {
 } sait_halo_t;
 int sait_operator_apply_halo(sait_op_t op, const double *d_x_ext, int64_t ext_len, const sait_halo_t *halo,
                              double *d_y, int64_t ylen, sait_stream_t stream);
+/* The row-sharded pair with peer-memory halos as one native object (the
+ * data path of the multi-GPU apply): per factor this rank's two
+ * parity copies of its extended vector, its epoch flag, the own segment and
+ * per parity the neighbours' halo sources.  apply(r, z) on this rank's rows:
+ * epoch e += 1; r -> own segment of M_L's copy (e & 1); publish; M_L's halo
+ * SpMV writes y into M_U's own segment; publish; M_U's halo SpMV -> z.  The
+ * operators are borrowed (they must outlive the pair). */
+typedef struct {
+  double *ext[2];       /* extended vector, parity 0 / 1 (device) */
+  int *flag;            /* this rank's published epoch for this factor */
+  int64_t ext_len, own_offset, own_len;
+  sait_halo_t halo[2];  /* per parity (the epoch field is set per apply) */
+} sait_peer_factor_desc;
+typedef struct sait_peer_pair_s *sait_peer_pair_t;
+int sait_peer_pair_create(sait_op_t ml, sait_op_t mu, const sait_peer_factor_desc *desc, sait_peer_pair_t *out);
+int sait_peer_pair_apply(sait_peer_pair_t p, const double *d_r, double *d_z, sait_stream_t stream);
+void sait_peer_pair_destroy(sait_peer_pair_t p);
 /* *d_flag = epoch once everything queued before on `stream` has completed
  * (system-scope release: peers polling the flag then see the data). */
 int sait_publish_epoch(int *d_flag, int epoch, sait_stream_t stream);
@@ -312,6 +358,12 @@ typedef struct {
   double relres_estimate; /* the stopping quantity at exit */
   double true_relres;     /* ||b - A x|| / ||b|| recomputed at exit */
   double seconds;         /* wall time of the solve */
+  /* the paper's runtime split (TimedPreconditioner,
+   * preconditioner.cpp:66-77): device time of the preconditioner applies
+   * (CUDA events on the solver's stream) and their number; the rest of
+   * `seconds` is the operator, the orthogonalisation and the control */
+  double precond_seconds;
+  int64_t precond_applies;
 } sait_solve_stats;
 
 /* Right-preconditioned restarted GMRES(restart) from x0 = 0, CGS2 Arnoldi,
@@ -341,6 +393,12 @@ int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double *d_b, double *d_x
 int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed,
                 double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
                 sait_stream_t stream);
+/* The same, also filling stats (iterations, converged, seconds and the
+ * preconditioner's share: precond_seconds / precond_applies, one apply per
+ * block of nev vectors). */
+int sait_lobpcg_ex(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed,
+                   double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
+                   sait_solve_stats *stats, sait_stream_t stream);
 /* The same with the exact ILU solves as preconditioner (column by column;
  * the comparator of SPEC.md acceptance #9). */
 int sait_lobpcg_exact(sait_dcsr_t A, sait_exact_t M, int nev, double tol, int maxit, uint64_t seed,

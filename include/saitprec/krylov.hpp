@@ -18,6 +18,7 @@ struct SolveStats {
   std::vector<double> residual_history;  // history[0] = 1
   double true_relres = 0.0;
   double seconds = 0.0;
+  double precond_seconds = 0.0;  // device time of the preconditioner applies
 };
 
 SolveStats pcg(const CsrMatrix& a, std::span<const double> b, const SaitPairPreconditioner* p, double tol,

@@ -62,6 +62,19 @@ SAIT_FMT_AUTO, SAIT_FMT_CSR, SAIT_FMT_SELL_I32, SAIT_FMT_SELL_I16, SAIT_FMT_SELL
 FORMAT_NAMES = {0: "auto", 1: "csr", 2: "sell32_int32", 3: "sell32_int16", 4: "sell32_dict"}
 
 
+class RowPiece(C.Structure):
+    """sait_row_piece (include/sait_c.h)"""
+
+    _fields_ = [("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p), ("col_offset", C.c_int64)]
+
+
+class PeerFactorDesc(C.Structure):
+    """sait_peer_factor_desc (include/sait_c.h)"""
+
+    _fields_ = [("ext", C.c_void_p * 2), ("flag", C.c_void_p), ("ext_len", C.c_int64), ("own_offset", C.c_int64),
+                ("own_len", C.c_int64), ("halo", Halo * 2)]
+
+
 class HostCsr(C.Structure):
     _fields_ = [
         ("nrows", C.c_int64),
@@ -100,6 +113,8 @@ class SolveStats(C.Structure):
         ("relres_estimate", C.c_double),
         ("true_relres", C.c_double),
         ("seconds", C.c_double),
+        ("precond_seconds", C.c_double),
+        ("precond_applies", C.c_int64),
     ]
 
 
@@ -114,6 +129,16 @@ PROTOTYPES = {
     "sait_csr_to_host": (C.c_int, [VP, VP, C.POINTER(HostCsr)]),
     "sait_csr_device_arrays": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
     "sait_csr_free": (None, [VP]),
+    "sait_lobpcg_ex": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int),
+                                 C.POINTER(SolveStats), VP]),
+    "sait_peer_pair_create": (C.c_int, [VP, VP, C.POINTER(PeerFactorDesc), C.POINTER(VP)]),
+    "sait_peer_pair_apply": (C.c_int, [VP, VP, VP, VP]),
+    "sait_peer_pair_destroy": (None, [VP]),
+    "sait_csr_assemble_rows": (C.c_int, [C.c_int, C.POINTER(RowPiece), C.c_int64, C.c_int64, VP, C.POINTER(VP)]),
+    "sait_csr_col_span": (C.c_int, [VP, P64, P64, VP]),
+    "sait_csr_shift_cols": (C.c_int, [VP, C.c_int64, C.c_int64, VP]),
+    "sait_csr_row_ptr_at": (C.c_int, [VP, P64, C.c_int, P64, VP]),
+    "sait_column_work": (C.c_int, [VP, VP, VP]),
     "sait_spmv": (C.c_int, [VP, VP, C.c_int64, VP, C.c_int64, VP]),
     "sait_spgemm": (C.c_int, [VP, VP, VP, C.POINTER(VP)]),
     "sait_add_identity": (C.c_int, [VP, VP, C.POINTER(VP)]),

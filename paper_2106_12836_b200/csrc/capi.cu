@@ -696,6 +696,70 @@ int sait_csr_device_arrays(sait_dcsr_t m, const int32_t** row_ptr, const int32_t
   });
 }
 
+int sait_csr_assemble_rows(int nparts, const sait_row_piece* parts, int64_t nrows, int64_t ncols,
+                           sait_stream_t stream, sait_dcsr_t* out) {
+  return guarded([&] {
+    need(out, "sait_csr_assemble_rows(out)");
+    if (nparts < 0 || (nparts > 0 && !parts)) sait::throw_invalid("sait_csr_assemble_rows: bad parts");
+    if (nrows < 0 || ncols < 0 || nrows > INT32_MAX || ncols > INT32_MAX)
+      sait::throw_invalid("sait_csr_assemble_rows: dimensions out of range");
+    for (int p = 0; p < nparts; ++p)
+      if (!parts[p].row_ptr || !parts[p].col_idx) sait::throw_invalid("sait_csr_assemble_rows: null piece");
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    sait::DevCsr c = sait::assemble_rows(nparts, parts, nrows, ncols, s);
+    if (c.nnz > INT32_MAX) {
+      sait::free_csr(c, s);
+      sait::throw_invalid("sait_csr_assemble_rows: more than 2^31-1 entries");
+    }
+    *out = wrap(c);
+  });
+}
+
+int sait_csr_col_span(sait_dcsr_t m, int64_t* lo, int64_t* hi, sait_stream_t stream) {
+  return guarded([&] {
+    need(m, "sait_csr_col_span");
+    DeviceGuard g(m->dev);
+    int64_t a = 0, b = 0;
+    sait::col_span(m->m, &a, &b, sait::as_stream(stream));
+    if (lo) *lo = a;
+    if (hi) *hi = b;
+  });
+}
+
+int sait_csr_shift_cols(sait_dcsr_t m, int64_t offset, int64_t new_ncols, sait_stream_t stream) {
+  return guarded([&] {
+    need(m, "sait_csr_shift_cols");
+    if (new_ncols < 0 || new_ncols > INT32_MAX || offset > INT32_MAX || offset < -int64_t{INT32_MAX})
+      sait::throw_invalid("sait_csr_shift_cols: out of range");
+    DeviceGuard g(m->dev);
+    sait::shift_columns(m->m, offset, new_ncols, sait::as_stream(stream));
+  });
+}
+
+int sait_csr_row_ptr_at(sait_dcsr_t m, const int64_t* rows, int k, int64_t* out, sait_stream_t stream) {
+  return guarded([&] {
+    need(m, "sait_csr_row_ptr_at");
+    if (k < 0 || (k > 0 && (!rows || !out))) sait::throw_invalid("sait_csr_row_ptr_at: bad arguments");
+    for (int j = 0; j < k; ++j)
+      if (rows[j] < 0 || rows[j] > m->m.nrows) sait::throw_invalid("sait_csr_row_ptr_at: row out of range");
+    DeviceGuard g(m->dev);
+    init_device_pool();
+    sait::row_ptr_at(m->m, rows, k, out, sait::as_stream(stream));
+  });
+}
+
+int sait_column_work(sait_dcsr_t t, int64_t* d_work, sait_stream_t stream) {
+  return guarded([&] {
+    need(t, "sait_column_work");
+    need(d_work, "sait_column_work(work)");
+    if (t->m.nrows != t->m.ncols) sait::throw_invalid("sait_column_work: matrix is not square");
+    DeviceGuard g(t->dev);
+    init_device_pool();
+    sait::column_work_of(t->m, d_work, sait::as_stream(stream));
+  });
+}
+
 void sait_csr_free(sait_dcsr_t m) {
   if (!m) return;
   int prev = -1;
@@ -1198,6 +1262,88 @@ int sait_operator_apply_halo(sait_op_t op, const double* d_x_ext, int64_t ext_le
     sait::sell_spmv_halo(op->sell, d_x_ext, h, d_y, sait::as_stream(stream));
   });
 }
+
+}  // extern "C"
+
+namespace {
+sait::HaloArgs to_halo(const sait_halo_t& x, int epoch) {
+  sait::HaloArgs h;
+  h.own_lo = x.own_lo;
+  h.own_hi = x.own_hi;
+  h.lo_src = x.lo_src;
+  h.lo_shift = x.lo_shift;
+  h.hi_src = x.hi_src;
+  h.hi_shift = x.hi_shift;
+  h.lo_flag = x.lo_flag;
+  h.hi_flag = x.hi_flag;
+  h.epoch = epoch;
+  return h;
+}
+}  // namespace
+
+struct sait_peer_pair_s {
+  int dev = 0;
+  sait_op_t op[2] = {nullptr, nullptr};
+  sait_peer_factor_desc d[2];
+  int epoch = 0;
+  std::mutex mu;  // one apply at a time (the epochs and buffers are shared)
+};
+
+extern "C" {
+
+int sait_peer_pair_create(sait_op_t ml, sait_op_t mu, const sait_peer_factor_desc* desc, sait_peer_pair_t* out) {
+  return guarded([&] {
+    need(ml, "peer_pair");
+    need(mu, "peer_pair");
+    need(desc, "peer_pair(desc)");
+    need(out, "peer_pair(out)");
+    sait_op_t ops[2] = {ml, mu};
+    for (int f = 0; f < 2; ++f) {
+      const sait_peer_factor_desc& x = desc[f];
+      const sait::DevCsr& m = ops[f]->a->m;
+      if (!ops[f]->sell.ok()) sait::throw_invalid("peer_pair: the operator has no SELL copy");
+      if (!x.ext[0] || !x.ext[1] || !x.flag) sait::throw_invalid("peer_pair: null buffer");
+      if (x.ext_len != m.ncols || x.own_offset < 0 || x.own_offset + x.own_len > x.ext_len)
+        sait::throw_invalid("peer_pair: extended vector layout does not match the operator");
+      for (int par = 0; par < 2; ++par) {
+        const sait_halo_t& h = x.halo[par];
+        if ((h.own_lo > 0 && (!h.lo_src || !h.lo_flag)) || (h.own_hi < x.ext_len && (!h.hi_src || !h.hi_flag)))
+          sait::throw_invalid("peer_pair: halo source missing");
+      }
+    }
+    if (ops[0]->a->m.nrows != desc[1].own_len || ops[1]->a->m.nrows != desc[1].own_len ||
+        desc[0].own_len != desc[1].own_len)
+      sait::throw_invalid("peer_pair: row blocks do not chain");
+    auto* p = new sait_peer_pair_s;
+    p->dev = ml->dev;
+    p->op[0] = ml;
+    p->op[1] = mu;
+    p->d[0] = desc[0];
+    p->d[1] = desc[1];
+    *out = p;
+  });
+}
+
+int sait_peer_pair_apply(sait_peer_pair_t p, const double* d_r, double* d_z, sait_stream_t stream) {
+  return guarded([&] {
+    need(p, "peer_pair_apply");
+    DeviceGuard g(p->dev);
+    std::lock_guard<std::mutex> lk(p->mu);
+    cudaStream_t s = sait::as_stream(stream);
+    const int e = ++p->epoch;
+    const int par = e & 1;
+    const sait_peer_factor_desc &L = p->d[0], &U = p->d[1];
+    // r -> own segment of M_L's extended vector; publish; M_L (halo read from
+    // the neighbours inside the SpMV) writes y into M_U's own segment; publish; M_U
+    SAIT_CUDA(cudaMemcpyAsync(L.ext[par] + L.own_offset, d_r, sizeof(double) * L.own_len, cudaMemcpyDeviceToDevice, s));
+    sait::publish_epoch(L.flag, e, s);
+    sait::sell_spmv_halo(p->op[0]->sell, L.ext[par], to_halo(L.halo[par], e), U.ext[par] + U.own_offset, s);
+    sait::publish_epoch(U.flag, e, s);
+    sait::sell_spmv_halo(p->op[1]->sell, U.ext[par], to_halo(U.halo[par], e), d_z, s);
+  });
+}
+
+void sait_peer_pair_destroy(sait_peer_pair_t p) { delete p; }
 
 int sait_publish_epoch(int* d_flag, int epoch, sait_stream_t stream) {
   return guarded([&] {

@@ -225,6 +225,12 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
 SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStream_t s);
 
 // spmv.cu
+// csr_ops.cu: column-block -> row-block redistribution helpers
+DevCsr assemble_rows(int nparts, const sait_row_piece* parts_host, int64_t nrows, int64_t ncols, cudaStream_t s);
+void col_span(const DevCsr& a, int64_t* lo, int64_t* hi, cudaStream_t s);
+void shift_columns(DevCsr& a, int64_t off, int64_t ncols, cudaStream_t s);
+void row_ptr_at(const DevCsr& a, const int64_t* rows_host, int k, int64_t* out_host, cudaStream_t s);
+void column_work_of(const DevCsr& t, int64_t* work, cudaStream_t s);
 // sell.cu
 struct SellMatrix {
   int64_t n = 0, nslices = 0, padded = 0;

@@ -446,3 +446,173 @@ DevCsr copy_csr(const DevCsr& a, cudaStream_t s) {
 }
 
 }  // namespace sait
+
+// ---------------------------------------------------------------------------
+// Column-block -> row-block redistribution (multi-GPU, SURVEY.md §8e "K4"):
+// the distributed form of csr.cpp:72-92.  Each rank's column-sharded build
+// yields M[:, C_r:C_{r+1}] (all n rows); rank q receives, from every rank r in
+// ascending r, the rows [R_q, R_{q+1}) of that block and assembles its row
+// block of M.  Column blocks are disjoint and ascending in r, so row i of the
+// result is the concatenation of the pieces' rows i in part order (columns
+// shifted by the part's col_offset): sorted, bitwise the global matrix's row.
+namespace sait {
+namespace {
+
+__global__ void assemble_count(int64_t nrows, int nparts, const sait_row_piece* __restrict__ parts,
+                               int32_t* __restrict__ len) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  int32_t c = 0;
+  for (int p = 0; p < nparts; ++p) c += parts[p].row_ptr[i + 1] - parts[p].row_ptr[i];
+  len[i] = c;
+}
+
+// 8 lanes per row (rows hold ~7-30 entries), parts in order
+__global__ void assemble_copy(int64_t nrows, int nparts, const sait_row_piece* __restrict__ parts,
+                              const int32_t* __restrict__ rp, int32_t* __restrict__ ci, double* __restrict__ v) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = t >> 3;
+  const int lane = static_cast<int>(t & 7);
+  if (i >= nrows) return;
+  int32_t o = rp[i];
+  for (int p = 0; p < nparts; ++p) {
+    const sait_row_piece q = parts[p];
+    const int32_t b = q.row_ptr[i] - q.row_ptr[0], e = q.row_ptr[i + 1] - q.row_ptr[0];
+    const int32_t off = static_cast<int32_t>(q.col_offset);
+    for (int32_t k = b + lane; k < e; k += 8) {
+      ci[o + (k - b)] = q.col_idx[k] + off;
+      if (v) v[o + (k - b)] = q.values[k];
+    }
+    o += e - b;
+  }
+}
+
+__global__ void col_minmax(int64_t nnz, const int32_t* __restrict__ ci, int* __restrict__ mm) {
+  int lo = INT32_MAX, hi = -1;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    lo = min(lo, ci[e]);
+    hi = max(hi, ci[e]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+__global__ void shift_cols(int64_t nnz, int32_t* __restrict__ ci, int32_t off) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < nnz) ci[e] += off;
+}
+
+__global__ void read_row_ptr(const int32_t* __restrict__ rp, int k, const int64_t* __restrict__ rows,
+                             int64_t* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < k) out[j] = rp[rows[j]];
+}
+
+// Column-form work of column j of M at step 2 (the first step with products):
+// sum over the entries (k, j) of tT of the number of entries of column k --
+// the products the column's recursion forms.  Lower and upper T alike.
+__global__ void column_counts(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              int64_t* __restrict__ cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int32_t e = rp[i]; e < rp[i + 1]; ++e)
+    if (ci[e] != i) atomicAdd(reinterpret_cast<unsigned long long*>(cnt + ci[e]), 1ull);
+}
+__global__ void column_work(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const int64_t* __restrict__ cnt, int64_t* __restrict__ work) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int32_t e = rp[i]; e < rp[i + 1]; ++e)
+    if (ci[e] != i) atomicAdd(reinterpret_cast<unsigned long long*>(work + ci[e]),
+                              static_cast<unsigned long long>(cnt[i] + 1));
+}
+
+}  // namespace
+
+DevCsr assemble_rows(int nparts, const sait_row_piece* parts_host, int64_t nrows, int64_t ncols, cudaStream_t s) {
+  DevCsr c;
+  c.nrows = nrows;
+  c.ncols = ncols;
+  bool values = true;
+  for (int p = 0; p < nparts; ++p) values = values && parts_host[p].values != nullptr;
+  sait_row_piece* parts = dalloc<sait_row_piece>(nparts > 0 ? nparts : 1, s);
+  if (nparts)
+    SAIT_CUDA(cudaMemcpyAsync(parts, parts_host, sizeof(sait_row_piece) * nparts, cudaMemcpyHostToDevice, s));
+  c.rp = dalloc<int32_t>(nrows + 1, s);
+  int32_t* len = dalloc<int32_t>(nrows > 0 ? nrows : 1, s);
+  if (nrows > 0) {
+    assemble_count<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, nparts, parts, len);
+    SAIT_LAUNCHED();
+  }
+  c.nnz = scan_counts(len, c.rp, nrows, s);
+  dfree(len, s);
+  c.ci = dalloc<int32_t>(c.nnz > 0 ? c.nnz : 1, s);
+  c.v = values ? dalloc<double>(c.nnz > 0 ? c.nnz : 1, s) : nullptr;
+  if (nrows > 0) {
+    assemble_copy<<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, nparts, parts, c.rp, c.ci, c.v);
+    SAIT_LAUNCHED();
+  }
+  dfree(parts, s);
+  SAIT_CUDA(cudaStreamSynchronize(s));  // parts_host may be a caller temporary
+  return c;
+}
+
+void col_span(const DevCsr& a, int64_t* lo, int64_t* hi, cudaStream_t s) {
+  int* mm = dalloc<int>(2, s);
+  const int init[2] = {INT32_MAX, -1};
+  SAIT_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
+  if (a.nnz > 0) {
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(grid_for(a.nnz, 256), int64_t{num_sms()} * 8));
+    col_minmax<<<grid, 256, 0, s>>>(a.nnz, a.ci, mm);
+    SAIT_LAUNCHED();
+  }
+  int h[2];
+  SAIT_CUDA(cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(mm, s);
+  *lo = h[1] < 0 ? 0 : h[0];
+  *hi = h[1] < 0 ? 0 : int64_t{h[1]} + 1;
+}
+
+void shift_columns(DevCsr& a, int64_t off, int64_t ncols, cudaStream_t s) {
+  if (a.nnz > 0 && off != 0) {
+    shift_cols<<<grid_for(a.nnz, 256), 256, 0, s>>>(a.nnz, a.ci, static_cast<int32_t>(off));
+    SAIT_LAUNCHED();
+  }
+  a.ncols = ncols;
+}
+
+void row_ptr_at(const DevCsr& a, const int64_t* rows_host, int k, int64_t* out_host, cudaStream_t s) {
+  int64_t* d = dalloc<int64_t>(2 * (k > 0 ? k : 1), s);
+  if (k > 0) {
+    SAIT_CUDA(cudaMemcpyAsync(d, rows_host, sizeof(int64_t) * k, cudaMemcpyHostToDevice, s));
+    read_row_ptr<<<grid_for(k, 128), 128, 0, s>>>(a.rp, k, d, d + k);
+    SAIT_LAUNCHED();
+    SAIT_CUDA(cudaMemcpyAsync(out_host, d + k, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+  }
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(d, s);
+}
+
+void column_work_of(const DevCsr& t, int64_t* work, cudaStream_t s) {
+  const int64_t n = t.nrows;
+  int64_t* cnt = dalloc<int64_t>(n > 0 ? n : 1, s);
+  SAIT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * n, s));
+  SAIT_CUDA(cudaMemsetAsync(work, 0, sizeof(int64_t) * n, s));
+  if (n > 0) {
+    column_counts<<<grid_for(n, 256), 256, 0, s>>>(n, t.rp, t.ci, cnt);
+    SAIT_LAUNCHED();
+    column_work<<<grid_for(n, 256), 256, 0, s>>>(n, t.rp, t.ci, cnt, work);
+    SAIT_LAUNCHED();
+  }
+  dfree(cnt, s);
+}
+
+}  // namespace sait

@@ -635,6 +635,7 @@ SolveStats run_solver(const CsrMatrix& a, std::span<const double> b, std::vector
   out.converged = st.converged != 0;
   out.true_relres = st.true_relres;
   out.seconds = st.seconds;
+  out.precond_seconds = st.precond_seconds;
   out.residual_history.assign(hist.begin(), hist.begin() + st.iterations + 1);
   return out;
 }

@@ -72,17 +72,65 @@ struct Operator {
   void release(cudaStream_t s) { free_sell(sell, s); }
 };
 
+// Device time of the preconditioner applies inside a solve -- the paper's
+// runtime split, which the reference takes with
+// TimedPreconditioner (preconditioner.cpp:66-77) on the host: CUDA events
+// around each apply on the solver's stream, a ring of pairs collected lazily
+// (the loops synchronise every iteration anyway, so collecting never stalls
+// the pipeline).
+struct PrecondTimer {
+  static constexpr int kRing = 32;
+  cudaEvent_t ev[2 * kRing] = {};
+  int head = 0, pending = 0;
+  double ms = 0.0;
+  int64_t count = 0;
+  PrecondTimer() {
+    for (auto& e : ev) SAIT_CUDA(cudaEventCreate(&e));
+  }
+  ~PrecondTimer() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  PrecondTimer(const PrecondTimer&) = delete;
+  PrecondTimer& operator=(const PrecondTimer&) = delete;
+  int begin(cudaStream_t s) {
+    if (pending == kRing) collect_one();
+    const int slot = (head + pending) % kRing;
+    SAIT_CUDA(cudaEventRecord(ev[2 * slot], s));
+    return slot;
+  }
+  void end(int slot, cudaStream_t s) {
+    SAIT_CUDA(cudaEventRecord(ev[2 * slot + 1], s));
+    ++pending;
+  }
+  void collect_one() {
+    SAIT_CUDA(cudaEventSynchronize(ev[2 * head + 1]));
+    float t = 0.f;
+    SAIT_CUDA(cudaEventElapsedTime(&t, ev[2 * head], ev[2 * head + 1]));
+    ms += t;
+    ++count;
+    head = (head + 1) % kRing;
+    --pending;
+  }
+  void finish() {
+    while (pending) collect_one();
+  }
+};
+
 // z = M r: the SAIT pair, the exact ILU solves (the comparator), or identity
 struct Precond {
   sait_pair_t p = nullptr;
   sait_exact_t e = nullptr;
   int64_t n = 0;
+  PrecondTimer* timer = nullptr;
   bool present() const { return p || e; }
   int64_t dim() const { return p ? pair_dim(p) : e ? exact_dim(e) : n; }
   void apply(const double* r, double* z, cudaStream_t s) const {
+    const int slot = timer ? timer->begin(s) : 0;
     if (p) pair_apply_internal(p, r, z, s);
     else if (e) exact_apply_internal(e, r, z, s);
     else SAIT_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    if (timer) timer->end(slot, s);
   }
 };
 
@@ -282,6 +330,8 @@ static int gmres_impl(sait_dcsr_t A, sait::Precond M, const double* d_b, double*
     sait::Operator op(a, s);
     sait::Precond pc = M;
     pc.n = n;
+    sait::PrecondTimer ptimer;
+    pc.timer = &ptimer;
     double* V = sait::dalloc<double>((m + 1) * n, s);
     double* w = sait::dalloc<double>(n, s);
     double* z = sait::dalloc<double>(n, s);
@@ -377,6 +427,9 @@ static int gmres_impl(sait_dcsr_t A, sait::Precond M, const double* d_b, double*
       stats->relres_estimate = est;
       stats->true_relres = bnorm == 0.0 ? 0.0 : beta / bnorm;
       stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      ptimer.finish();
+      stats->precond_seconds = ptimer.ms * 1e-3;
+      stats->precond_applies = ptimer.count;
     }
     sait::dfree(V, s);
     sait::dfree(w, s);
@@ -405,6 +458,8 @@ static int pcg_impl(sait_dcsr_t A, sait::Precond M, const double* d_b, double* d
     sait::Operator op(a, s);
     sait::Precond pc = M;
     pc.n = n;
+    sait::PrecondTimer ptimer;
+    pc.timer = &ptimer;
     double* r = sait::dalloc<double>(n, s);
     double* z = sait::dalloc<double>(n, s);
     double* p = sait::dalloc<double>(n, s);
@@ -459,6 +514,9 @@ static int pcg_impl(sait_dcsr_t A, sait::Precond M, const double* d_b, double* d
       stats->relres_estimate = bnorm == 0.0 ? 0.0 : rel;
       stats->true_relres = bnorm == 0.0 ? 0.0 : tr / bnorm;
       stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      ptimer.finish();
+      stats->precond_seconds = ptimer.ms * 1e-3;
+      stats->precond_applies = ptimer.count;
     }
     sait::dfree(r, s);
     sait::dfree(z, s);
@@ -501,8 +559,11 @@ int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double* d_b, double* d_x
 }
 
 static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int maxit, uint64_t seed,
-                       double* h_evals, double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream) {
+                       double* h_evals, double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream,
+                       sait_solve_stats* stats = nullptr) {
   return solver_guard([&] {
+    const auto t_start = std::chrono::steady_clock::now();
+    sait::PrecondTimer ptimer;
     if (!A || !h_evals || !iterations) sait::throw_invalid("lobpcg: null argument");
     const sait::DevCsr& a = A->m;
     const int64_t n = a.nrows;
@@ -607,6 +668,7 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         }
         phase("\nresid");
         if (conv || it == maxit) break;
+        const int pslot = ptimer.begin(s);
         if (M.p) {
           sait::pair_apply_block_internal(M.p, R, W, n, k, 0, s);
         } else if (M.e) {  // exact ILU solves, column by column
@@ -615,6 +677,7 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         } else {
           SAIT_CUDA(cudaMemcpyAsync(W, R, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
         }
+        ptimer.end(pslot, s);
         phase("precond");
         std::vector<double> G1;
         gram(X, k, W, k, G1);
@@ -671,6 +734,16 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     for (int j = 0; j < k; ++j) h_evals[j] = lam[j];
     if (d_evecs) SAIT_CUDA(cudaMemcpyAsync(d_evecs, X, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
     *iterations = it;
+    if (stats) {
+      ptimer.finish();
+      stats->iterations = it;
+      stats->converged = conv ? 1 : 0;
+      stats->relres_estimate = 0.0;
+      stats->true_relres = 0.0;
+      stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      stats->precond_seconds = ptimer.ms * 1e-3;
+      stats->precond_applies = ptimer.count;
+    }
     SAIT_CUDA(cudaStreamSynchronize(s));
     sait::dfree(S, s);
     sait::dfree(AS, s);
@@ -692,6 +765,14 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
   sait::Precond pc;
   pc.p = M;
   return lobpcg_impl(A, pc, nev, tol, maxit, seed, h_evals, d_evecs, h_resnorms, iterations, stream);
+}
+
+int sait_lobpcg_ex(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, double* h_evals,
+                   double* d_evecs, double* h_resnorms, int* iterations, sait_solve_stats* stats,
+                   sait_stream_t stream) {
+  sait::Precond pc;
+  pc.p = M;
+  return lobpcg_impl(A, pc, nev, tol, maxit, seed, h_evals, d_evecs, h_resnorms, iterations, stream, stats);
 }
 
 int sait_lobpcg_exact(sait_dcsr_t A, sait_exact_t M, int nev, double tol, int maxit, uint64_t seed,

@@ -126,6 +126,19 @@ class DeviceOperator:
         self._h = h
         self.nrows, self.ncols = block.nrows, block.ncols
 
+    @classmethod
+    def from_device(cls, d):
+        """From a device CSR (ownership moves into the operator)."""
+        from . import _native as N
+
+        obj = cls.__new__(cls)
+        h = C.c_void_p()
+        N.check(N.lib.sait_operator_create(d.handle, 1, C.byref(h)))
+        d.release()
+        obj._h = h
+        obj.nrows, obj.ncols = d.nrows, d.ncols
+        return obj
+
     def apply(self, x, y, stream=None):
         import torch
 
@@ -182,7 +195,7 @@ class ShardedPair:
 
 
 def build_sharded(T_dev, lower: bool, spec, rank: int, world: int, group=None, stream=None, transposed: bool = True,
-                  reduce_max=None):
+                  reduce_max=None, bounds: list[int] | None = None):
     """Column-sharded SAIT build: this rank's block of columns of M.
 
     Returns (DeviceCsr block, BuildStats, (c0, c1)).  ``transposed`` selects the
@@ -195,7 +208,8 @@ def build_sharded(T_dev, lower: bool, spec, rank: int, world: int, group=None, s
     if reduce_max is None:
         reduce_max = _allreduce_max(group)
     n = T_dev.nrows
-    bounds = row_bounds(n, world)
+    if bounds is None:
+        bounds = row_bounds(n, world)
     c0, c1 = bounds[rank], bounds[rank + 1]
     sh = _stream_handle(stream)
     sess = C.c_void_p()
@@ -212,6 +226,172 @@ def build_sharded(T_dev, lower: bool, spec, rank: int, world: int, group=None, s
     finally:
         N.lib.sait_build_session_destroy(sess)
     return DeviceCsr(out.value), BuildStats(st.steps_run, bool(st.stabilized), st.nnz_out, st.products, st.seconds), (c0, c1)
+
+
+def column_bounds_by_work(T_dev, world: int, stream=None) -> list[int]:
+    """world + 1 column boundaries for the column-sharded build, balanced on
+    the predicted products per column (sait_column_work: column j's step-2
+    work) rather than on the column count."""
+    import torch
+
+    from . import _native as N
+    from .csr import _stream_handle
+
+    n = T_dev.nrows
+    work = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    N.check(N.lib.sait_column_work(T_dev.handle, work.data_ptr(), s))
+    return _bounds_from_work(work[:n].cpu().numpy(), world)
+
+
+def _bounds_from_work(work: np.ndarray, world: int) -> list[int]:
+    n = len(work)
+    cum = np.cumsum(work, dtype=np.int64)
+    total = int(cum[-1]) if n else 0
+    b = [0]
+    for r in range(1, world):
+        j = int(np.searchsorted(cum, total * r / world, side="left")) + 1 if total else n * r // world
+        b.append(min(n, max(b[-1], j)))
+    b.append(n)
+    return b
+
+
+# ------------------------------------------ column blocks -> row blocks (K4)
+# The column-sharded build leaves rank r with M[:, C_r:C_{r+1}] (all n rows,
+# local columns); the row-sharded apply needs rows [R_q, R_{q+1}) of M on rank
+# q.  Rank r cuts its block at the row bounds (one device read of n_ranks + 1
+# row pointers), sends piece q to rank q (NCCL point-to-point: row pointers,
+# columns, values), and rank q assembles its row block from the pieces in
+# ascending r (sait_csr_assemble_rows: row i = the pieces' rows i
+# concatenated, columns shifted by C_r -- sorted because the column blocks
+# ascend).  The distributed form of transpose (csr.cpp:72-92); no host round
+# trip of the matrix.
+
+def _dev_view(ptr: int, count: int, dtype: str):
+    import torch
+
+    iface = {"shape": (count,), "typestr": dtype, "data": (ptr, False), "version": 3, "strides": None}
+    holder = type("CudaArray", (), {"__cuda_array_interface__": iface})()
+    return torch.as_tensor(holder, device="cuda")
+
+
+def row_pieces(block, row_bounds: list[int], stream=None) -> list[dict]:
+    """Rank-local cut of a device CSR block (n rows) at the row bounds: for
+    every destination q its row pointers (rows R_q..R_{q+1}, not rebased),
+    columns and values as device views, and its entry count."""
+    import torch
+
+    from . import _native as N
+    from .csr import _stream_handle
+
+    world = len(row_bounds) - 1
+    s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    rows = (C.c_int64 * (world + 1))(*row_bounds)
+    offs = (C.c_int64 * (world + 1))()
+    N.check(N.lib.sait_csr_row_ptr_at(block.handle, rows, world + 1, offs, s))
+    rp, ci, v = block.device_arrays()
+    out = []
+    for q in range(world):
+        r0, r1 = row_bounds[q], row_bounds[q + 1]
+        nnz = int(offs[q + 1] - offs[q])
+        out.append({"nnz": nnz, "nrows": r1 - r0,
+                    "rp": _dev_view(rp + 4 * r0, r1 - r0 + 1, "<i4"),
+                    "ci": _dev_view(ci + 4 * int(offs[q]), max(nnz, 1), "<i4")[:nnz],
+                    "v": _dev_view(v + 8 * int(offs[q]), max(nnz, 1), "<f8")[:nnz]})
+    return out
+
+
+def exchange_row_pieces(mine: list[dict], nloc: int, rank: int, world: int, group=None, device="cuda") -> dict:
+    """Send piece q of `mine` to rank q, receive every rank's piece of our rows
+    (torch.distributed point-to-point, batched).  Returns {r: piece} for the
+    ranks with entries for us (ours included, not copied)."""
+    import torch
+    import torch.distributed as dist
+
+    counts = torch.tensor([p["nnz"] for p in mine], dtype=torch.int64, device=device)
+    allc = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    recv_cnt = [int(allc[r][rank]) for r in range(world)]
+    ops, got = [], {}
+    for q in range(world):
+        p = mine[q]
+        if q != rank and p["nnz"]:
+            for t in (p["rp"], p["ci"], p["v"]):
+                ops.append(dist.P2POp(dist.isend, t.contiguous(), q, group=group))
+    for r in range(world):
+        if r == rank or not recv_cnt[r]:
+            continue
+        b = {"nnz": recv_cnt[r], "nrows": nloc,
+             "rp": torch.empty(nloc + 1, dtype=torch.int32, device=device),
+             "ci": torch.empty(recv_cnt[r], dtype=torch.int32, device=device),
+             "v": torch.empty(recv_cnt[r], dtype=torch.float64, device=device)}
+        got[r] = b
+        for t in (b["rp"], b["ci"], b["v"]):
+            ops.append(dist.P2POp(dist.irecv, t, r, group=group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    if mine[rank]["nnz"]:
+        got[rank] = mine[rank]
+    return got
+
+
+def assemble_row_block(pieces: dict, col_bounds: list[int], nloc: int, ncols: int, stream=None):
+    """Device assembly (sait_csr_assemble_rows) of the pieces {r: piece} in
+    ascending r, columns shifted by C_r."""
+    import torch
+
+    from . import _native as N
+    from .csr import DeviceCsr, _stream_handle
+
+    order = sorted(pieces)
+    arr = (N.RowPiece * max(1, len(order)))()
+    for k, r in enumerate(order):
+        p = pieces[r]
+        arr[k].row_ptr, arr[k].col_idx, arr[k].values = p["rp"].data_ptr(), p["ci"].data_ptr(), p["v"].data_ptr()
+        arr[k].col_offset = int(col_bounds[r])
+    s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    h = C.c_void_p()
+    N.check(N.lib.sait_csr_assemble_rows(len(order), arr, nloc, ncols, s, C.byref(h)))
+    return DeviceCsr(h.value)
+
+
+def redistribute_to_rows(block, col_bounds: list[int], row_bounds: list[int], rank: int, world: int, group=None,
+                         stream=None):
+    """This rank's rows [R_rank, R_rank+1) of M (global columns) from every
+    rank's column block M[:, C_r:C_r+1] (see above)."""
+    mine = row_pieces(block, row_bounds, stream)
+    nloc = row_bounds[rank + 1] - row_bounds[rank]
+    got = exchange_row_pieces(mine, nloc, rank, world, group)
+    return assemble_row_block(got, col_bounds, nloc, block.nrows, stream)
+
+
+def redistribute_local(blocks: list, col_bounds: list[int], row_bounds: list[int], stream=None) -> list:
+    """The same for virtual ranks living in one process (one GPU): rank q's
+    row block assembled straight from every block's piece q."""
+    world = len(blocks)
+    cuts = [row_pieces(b, row_bounds, stream) for b in blocks]
+    out = []
+    for q in range(world):
+        pieces = {r: cuts[r][q] for r in range(world) if cuts[r][q]["nnz"]}
+        out.append(assemble_row_block(pieces, col_bounds, row_bounds[q + 1] - row_bounds[q], blocks[0].nrows, stream))
+    return out
+
+
+def row_block_span(block, r0: int, r1: int, stream=None) -> tuple[int, int]:
+    """Column span of a device row block (global columns), own rows included
+    by make_plans."""
+    import torch
+
+    from . import _native as N
+    from .csr import _stream_handle
+
+    s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    lo, hi = C.c_int64(), C.c_int64()
+    N.check(N.lib.sait_csr_col_span(block.handle, C.byref(lo), C.byref(hi), s))
+    if hi.value <= lo.value:
+        return r0, r0
+    return lo.value, hi.value
 
 
 def _allreduce_max(group):
@@ -311,16 +491,49 @@ class PeerShardedPair:
                     raise NotImplementedError("PeerShardedPair: a halo spans several ranks")
             self.plans.append(allp)
         r0, r1 = self.bounds[rank], self.bounds[rank + 1]
-        self.own = (r0, r1)
-        self.ops, self.bufs = [], []
+        ops = []
         for f, M in enumerate((ML, MU)):
             p = self.plans[f][rank]
-            self.ops.append(DeviceOperator(local_block(M.row_ptr, M.col_idx, M.values, r0, r1, p.lo, p.ext_len)))
+            ops.append(DeviceOperator(local_block(M.row_ptr, M.col_idx, M.values, r0, r1, p.lo, p.ext_len)))
+        self._setup(ops, resolve)
+
+    def _setup(self, ops, resolve):
+        rank = self.rank
+        self.own = (self.bounds[rank], self.bounds[rank + 1])
+        self.ops, self.bufs = ops, []
+        for f in range(2):
             self.bufs.append(_DevBuf(self._buf_bytes(f, rank)))
             self.bufs[f].tensor(self._flag_off(f, rank), 1, "<i4").zero_()
         self.resolve = resolve
         self.epoch = 0
         self.halo_bytes = 8 * sum(g1 - g0 for f in range(2) for _, g0, g1 in self.plans[f][rank].recv)
+
+    @classmethod
+    def from_row_blocks(cls, bl, bu, spans_l, spans_u, bounds, rank: int, world: int, resolve=None):
+        """From this rank's device row blocks of M_L and M_U (rows [R_rank,
+        R_rank+1), global columns -- e.g. redistribute_to_rows of a
+        column-sharded build) and every rank's column spans; the blocks are
+        re-indexed in place into the extended vector and owned by the pair."""
+        from . import _native as N
+
+        obj = cls.__new__(cls)
+        obj.n, obj.rank, obj.world = bounds[-1], rank, world
+        obj.bounds = list(bounds)
+        obj.plans = [make_plans(list(spans_l), obj.bounds), make_plans(list(spans_u), obj.bounds)]
+        for allp in obj.plans:
+            for p in allp:
+                below = [x for x in p.recv if x[2] <= p.own[0]]
+                above = [x for x in p.recv if x[1] >= p.own[1]]
+                if len(below) > 1 or len(above) > 1:
+                    raise NotImplementedError("PeerShardedPair: a halo spans several ranks")
+        ops = []
+        for f, blk in enumerate((bl, bu)):
+            p = obj.plans[f][rank]
+            N.check(N.lib.sait_csr_shift_cols(blk.handle, -p.lo, p.ext_len, None))
+            blk.ncols = p.ext_len
+            ops.append(DeviceOperator.from_device(blk))
+        obj._setup(ops, resolve)
+        return obj
 
     # layout of rank q's buffer for factor f: [ext parity 0 | ext parity 1 | flag]
     def _ext_len(self, f, q):
@@ -384,24 +597,63 @@ class PeerShardedPair:
     def stage_upper(self, z_local, epoch, s):
         self._spmv(1, epoch, z_local, s)
 
+    def _native_pair(self):
+        """The data path as one native object (sait_peer_pair_*): the copy,
+        the two publishes and the two halo SpMVs of an apply in one call."""
+        from . import _native as N
+
+        if getattr(self, "_pp", None) is None:
+            desc = (N.PeerFactorDesc * 2)()
+            for f in range(2):
+                p = self.plans[f][self.rank]
+                d = desc[f]
+                d.ext[0] = self.bufs[f].ptr
+                d.ext[1] = self.bufs[f].ptr + 8 * self._ext_len(f, self.rank)
+                d.flag = self.bufs[f].ptr + self._flag_off(f, self.rank)
+                d.ext_len, d.own_offset, d.own_len = p.ext_len, p.own_offset, self.own[1] - self.own[0]
+                for par in range(2):
+                    d.halo[par] = self._halo(f, par)
+            h = C.c_void_p()
+            N.check(N.lib.sait_peer_pair_create(self.ops[0]._h, self.ops[1]._h, desc, C.byref(h)))
+            self._pp = h
+        return self._pp
+
     def apply(self, r_local, z_local, stream=None) -> None:
+        """z_local = (M_U M_L r)[own rows]; epochs advance inside the native
+        object (do not mix with the stage_* calls)."""
         import torch
 
+        from . import _native as N
+
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-        self.epoch += 1
-        self.stage_input(r_local, self.epoch, s)
-        self.stage_lower(self.epoch, s)
-        self.stage_upper(z_local, self.epoch, s)
+        N.check(N.lib.sait_peer_pair_apply(self._native_pair(), r_local.data_ptr(), z_local.data_ptr(), s))
 
     @classmethod
     def distributed(cls, ML, MU, rank: int, world: int, group=None, align: int = GROUP_ROWS):
         """Multi-process construction: the ranks swap IPC handles of their
         buffers (torch.distributed all_gather_object) and open their peers'."""
+        return cls._connect(lambda: cls(ML, MU, rank, world, resolve=None, align=align), rank, world, group)
+
+    @classmethod
+    def distributed_from_row_blocks(cls, bl, bu, bounds, rank: int, world: int, group=None):
+        """Multi-process construction from device row blocks (global columns):
+        the column spans are all-gathered, then the IPC handles as above."""
+        import torch.distributed as dist
+
+        r0, r1 = bounds[rank], bounds[rank + 1]
+        mine = (row_block_span(bl, r0, r1), row_block_span(bu, r0, r1))
+        spans = [None] * world
+        dist.all_gather_object(spans, mine, group=group)
+        return cls._connect(lambda: cls.from_row_blocks(bl, bu, [x[0] for x in spans], [x[1] for x in spans], bounds,
+                                                        rank, world), rank, world, group)
+
+    @classmethod
+    def _connect(cls, make, rank: int, world: int, group=None):
         import torch.distributed as dist
 
         obj, mine, err = None, None, None
         try:
-            obj = cls(ML, MU, rank, world, resolve=None, align=align)
+            obj = make()
             mine = [obj.bufs[0].handle(), obj.bufs[1].handle()]
         except Exception as exc:  # noqa: BLE001  (agreed on below)
             err = exc
@@ -424,6 +676,9 @@ class PeerShardedPair:
     def close(self):
         from . import _native as N
 
+        if getattr(self, "_pp", None) is not None:
+            N.lib.sait_peer_pair_destroy(self._pp)
+            self._pp = None
         for p in getattr(self, "_opened", {}).values():
             N.lib.sait_ipc_close(C.c_void_p(p))
         self._opened = {}

@@ -24,6 +24,8 @@ class SolveStats:
     true_relres: float
     seconds: float
     history: np.ndarray
+    precond_seconds: float = 0.0  # device time of the preconditioner applies (the paper's split)
+    precond_applies: int = 0
 
 
 def _prep(A, b, stream):
@@ -40,7 +42,8 @@ def _prep(A, b, stream):
 def _finish(rc, st, hist, x, on_dev):
     N.check(rc)
     its = st.iterations
-    stats = SolveStats(its, bool(st.converged), st.relres_estimate, st.true_relres, st.seconds, hist[: its + 1].copy())
+    stats = SolveStats(its, bool(st.converged), st.relres_estimate, st.true_relres, st.seconds, hist[: its + 1].copy(),
+                       st.precond_seconds, st.precond_applies)
     return (x if on_dev else x.cpu().numpy()), stats
 
 
@@ -82,6 +85,7 @@ class EigResult:
     eigenvectors: object
     iterations: int
     residual_history: np.ndarray
+    stats: SolveStats | None = None  # seconds + preconditioner share (SAIT pair only)
 
 
 def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, stream=None, host_vectors=True):
@@ -95,8 +99,19 @@ def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, 
     its = C.c_int()
     s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
     mh, fn = _precond(M, N.lib.sait_lobpcg, N.lib.sait_lobpcg_exact)
-    N.check(fn(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed), evals.ctypes.data_as(N.PD),
-                              vecs.data_ptr(), res.ctypes.data_as(N.PD), C.byref(its), s))
+    st = None
+    if fn is N.lib.sait_lobpcg:
+        st = N.SolveStats()
+        N.check(N.lib.sait_lobpcg_ex(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed),
+                                     evals.ctypes.data_as(N.PD), vecs.data_ptr(), res.ctypes.data_as(N.PD),
+                                     C.byref(its), C.byref(st), s))
+    else:
+        N.check(fn(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed), evals.ctypes.data_as(N.PD),
+                   vecs.data_ptr(), res.ctypes.data_as(N.PD), C.byref(its), s))
     it = its.value
     v = vecs.T
-    return EigResult(evals, v.cpu().numpy() if host_vectors else v, it, res[: (it + 1) * nev].reshape(it + 1, nev))
+    hist = res[: (it + 1) * nev].reshape(it + 1, nev)
+    stats = None
+    if st is not None:
+        stats = SolveStats(it, bool(st.converged), 0.0, 0.0, st.seconds, hist, st.precond_seconds, st.precond_applies)
+    return EigResult(evals, v.cpu().numpy() if host_vectors else v, it, hist, stats)

@@ -194,3 +194,116 @@ def test_multiprocess_construction_fails_together(tmp_path):
         msg, closed = (tmp_path / f"a{q}.txt").read_text().split("|")
         assert "construction failed on rank 1" in msg and "no peer access" in msg
         assert closed == "True"
+
+
+def _host_pieces(block_rp, block_ci, block_v, row_bounds):
+    """CPU stand-in of dist.row_pieces for a host block (test only)."""
+    import torch
+
+    out = []
+    for q in range(len(row_bounds) - 1):
+        r0, r1 = row_bounds[q], row_bounds[q + 1]
+        a, b = int(block_rp[r0]), int(block_rp[r1])
+        out.append({"nnz": b - a, "nrows": r1 - r0, "rp": torch.from_numpy(block_rp[r0:r1 + 1].astype(np.int32)),
+                    "ci": torch.from_numpy(block_ci[a:b].astype(np.int32)), "v": torch.from_numpy(block_v[a:b].copy())})
+    return out
+
+
+def _host_assemble(pieces, col_bounds, nloc):
+    """numpy restatement of sait_csr_assemble_rows (test only)."""
+    rows_c, rows_v = [[] for _ in range(nloc)], [[] for _ in range(nloc)]
+    for r in sorted(pieces):
+        p = pieces[r]
+        rp = p["rp"].numpy().astype(np.int64)
+        rp = rp - rp[0]
+        ci, v = p["ci"].numpy(), p["v"].numpy()
+        for i in range(nloc):
+            rows_c[i].extend((ci[rp[i]:rp[i + 1]] + col_bounds[r]).tolist())
+            rows_v[i].extend(v[rp[i]:rp[i + 1]].tolist())
+    rp = np.zeros(nloc + 1, dtype=np.int64)
+    rp[1:] = np.cumsum([len(c) for c in rows_c])
+    return rp, np.array(sum(rows_c, []), dtype=np.int64), np.array(sum(rows_v, []), dtype=np.float64)
+
+
+def _redist_worker(rank, world, port, case, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2106_12836_b200.dist import exchange_row_pieces
+
+        d = np.load(case)
+        cb, rb = [int(x) for x in d["cb"]], [int(x) for x in d["rb"]]
+        # this rank's column block M[:, C_r:C_r+1] (all n rows, local columns)
+        mine = _host_pieces(d[f"rp{rank}"], d[f"ci{rank}"], d[f"v{rank}"], rb)
+        nloc = rb[rank + 1] - rb[rank]
+        got = exchange_row_pieces(mine, nloc, rank, world, device="cpu")
+        rp, ci, v = _host_assemble(got, cb, nloc)
+        np.savez(os.path.join(out_dir, f"rows{rank}.npz"), rp=rp, ci=ci, v=v)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_column_blocks_to_row_blocks(tmp_path, port, world):
+    """dist.exchange_row_pieces (the K4 redistribution's transport, SURVEY.md
+    §8e): every rank holds a column block M[:, C_r:C_{r+1}] of a SAIT factor
+    (column bounds from the work balancer, row bounds of the apply); after the
+    point-to-point exchange and the assembly rule of sait_csr_assemble_rows,
+    each rank's rows equal the global factor's rows bitwise."""
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+    from paper_2106_12836_b200.dist import _bounds_from_work, row_bounds
+
+    T = O.synthetic_lower(3000, 6, 0.01, seed=11)
+    M = port.sait_thr(T, True, 1e-2, 3)
+    n = M.nrows
+    Mt = port.transpose(M)  # rows of M^T = columns of M
+    work = np.diff(Mt.row_ptr) ** 2 + 1  # any positive weights
+    cb = _bounds_from_work(work, world)
+    assert cb[0] == 0 and cb[-1] == n and all(a <= b for a, b in zip(cb, cb[1:]))
+    rb = row_bounds(n, world)
+    arrays = {"cb": np.array(cb), "rb": np.array(rb)}
+    for r in range(world):
+        # M[:, c0:c1] as an n-row CSR with local columns (what build_sharded returns)
+        a, b = cb[r], cb[r + 1]
+        rows = [[(c - a, v) for c, v in zip(M.col_idx[M.row_ptr[i]:M.row_ptr[i + 1]],
+                                           M.values[M.row_ptr[i]:M.row_ptr[i + 1]]) if a <= c < b] for i in range(n)]
+        rp = np.zeros(n + 1, dtype=np.int64)
+        rp[1:] = np.cumsum([len(x) for x in rows])
+        arrays[f"rp{r}"] = rp
+        arrays[f"ci{r}"] = np.array([c for x in rows for c, _ in x], dtype=np.int64)
+        arrays[f"v{r}"] = np.array([v for x in rows for _, v in x], dtype=np.float64)
+    case = str(tmp_path / "case.npz")
+    np.savez(case, **arrays)
+    mp.start_processes(_redist_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    for q in range(world):
+        got = np.load(tmp_path / f"rows{q}.npz")
+        r0, r1 = rb[q], rb[q + 1]
+        a, b = M.row_ptr[r0], M.row_ptr[r1]
+        assert np.array_equal(got["rp"], M.row_ptr[r0:r1 + 1] - a)
+        assert np.array_equal(got["ci"], M.col_idx[a:b])
+        assert np.array_equal(got["v"].view(np.uint64), M.values[a:b].view(np.uint64))
+
+
+def test_work_balanced_bounds():
+    """Column blocks cut on the prefix sums of the predicted work: every block
+    carries at most its share plus one column's work."""
+    from paper_2106_12836_b200.dist import _bounds_from_work
+
+    rng = np.random.default_rng(3)
+    w = rng.integers(1, 50, 10000)
+    w[:20] = 5000  # heavy first columns (C4's capped offsets pile onto them)
+    for world in (1, 2, 4, 8):
+        b = _bounds_from_work(w, world)
+        assert len(b) == world + 1 and b[0] == 0 and b[-1] == len(w)
+        share = w.sum() / world
+        for r in range(world):
+            assert w[b[r]:b[r + 1]].sum() <= share + w.max()

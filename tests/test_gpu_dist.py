@@ -256,3 +256,116 @@ def test_ipc_handles_two_processes(tmp_path):
     for q in range(2):
         got = np.load(tmp_path / f"ipc{q}.npy")
         assert np.array_equal(got, np.arange(n, dtype=np.float64) * (((q + 1) % 2) + 1))
+
+
+def _virtual_sharded_build(S, T_dev, lower, spec, world, bounds):
+    """Column-sharded build of `world` virtual ranks on one GPU with the global
+    early stop reduced in-process; returns each rank's M[:, C_r:C_r+1]."""
+    from paper_2106_12836_b200 import _native as N
+
+    sess = []
+    for q in range(world):
+        h = C.c_void_p()
+        N.check(N.lib.sait_build_session_create(T_dev.handle, int(lower), C.byref(spec), bounds[q], bounds[q + 1],
+                                                None, C.byref(h)))
+        sess.append(h)
+    while N.lib.sait_build_session_remaining(sess[0]) > 0:
+        flags = []
+        for h in sess:
+            ch = C.c_int(1)
+            N.check(N.lib.sait_build_session_step(h, C.byref(ch)))
+            flags.append(ch.value)
+        if max(flags) == 0:
+            for h in sess:
+                N.check(N.lib.sait_build_session_stop(h))
+    blocks = []
+    for h in sess:
+        out = C.c_void_p()
+        N.check(N.lib.sait_build_session_finish(h, 0, C.byref(out), None))
+        N.lib.sait_build_session_destroy(h)
+        blocks.append(S.DeviceCsr(out.value))
+    return blocks
+
+
+@pytest.mark.parametrize("world,grid", [(2, 24), (3, 20), (4, 16)])
+def test_sharded_build_redistribute_peer_apply_virtual_ranks(S, port, world, grid):
+    """The device pipeline bench.py --gpus N runs, on one GPU with virtual
+    ranks: column-sharded SAIT builds of both ILU factors with work-balanced
+    column blocks (sait_column_work) -> column blocks redistributed to the
+    apply's row blocks on the device (row_pieces + sait_csr_assemble_rows) ->
+    PeerShardedPair.from_row_blocks.  Every row block equals the global
+    factor's rows bitwise, and the peer-halo apply equals the oracle's pair
+    apply over three epochs."""
+    import torch
+
+    from helpers import to_oracle
+    from paper_2106_12836_b200 import _native as N
+    from paper_2106_12836_b200.dist import (PeerShardedPair, column_bounds_by_work, redistribute_local,
+                                            row_block_span, row_bounds)
+
+    A = S.laplacian_3d(grid)
+    f = S.ilu_k(A, 0)
+    ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
+    MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
+    spec = N.DropSpec(N.SAIT_DROP_THRESHOLD, 5e-2, 3, 0, 0, 0.0)
+    n = A.nrows
+    rb = row_bounds(n, world)
+    rows = []
+    for lower, T, M in ((True, f.lower, ML), (False, f.upper, MU)):
+        dT = S.DeviceCsr.upload(T)
+        cb = column_bounds_by_work(dT, world)
+        assert cb[0] == 0 and cb[-1] == n
+        blocks = _virtual_sharded_build(S, dT, lower, spec, world, cb)
+        rblocks = redistribute_local(blocks, cb, rb)
+        for q in range(world):
+            h = rblocks[q].to_host()
+            a, b = M.row_ptr[rb[q]], M.row_ptr[rb[q + 1]]
+            assert np.array_equal(h.row_ptr, M.row_ptr[rb[q]:rb[q + 1] + 1] - a)
+            assert np.array_equal(h.col_idx, M.col_idx[a:b])
+            assert bitwise_equal(h.values, M.values[a:b])
+        rows.append(rblocks)
+    spans = [[row_block_span(rows[f_][q], rb[q], rb[q + 1]) for q in range(world)] for f_ in range(2)]
+    ranks = {}
+    resolve = lambda q, fac: ranks[q].bufs[fac].ptr  # noqa: E731
+    for q in range(world):
+        ranks[q] = PeerShardedPair.from_row_blocks(rows[0][q], rows[1][q], spans[0], spans[1], rb, q, world,
+                                                   resolve=resolve)
+    s = torch.cuda.current_stream().cuda_stream
+    for epoch in (1, 2, 3):
+        r = S.uniform_pm1(300 + epoch, n)
+        want = port.pair_apply(to_oracle(ML), to_oracle(MU), r)
+        rd = torch.from_numpy(r).cuda()
+        zs = {}
+        for q in range(world):
+            a, b = ranks[q].own
+            ranks[q].stage_input(rd[a:b], epoch, s)
+        for q in range(world):
+            ranks[q].stage_lower(epoch, s)
+        for q in range(world):
+            a, b = ranks[q].own
+            zs[q] = torch.empty(b - a, dtype=torch.float64, device="cuda")
+            ranks[q].stage_upper(zs[q], epoch, s)
+        torch.cuda.synchronize()
+        z = torch.cat([zs[q] for q in range(world)]).cpu().numpy()
+        assert bitwise_equal(z, want), epoch
+    for q in range(world):
+        ranks[q].close()
+
+
+def test_column_work_matches_host(S):
+    """sait_column_work: column j's predicted products (sum over the entries
+    (k, j), k != j, of nnz(column k without its diagonal) + 1), against numpy."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2106_12836_b200 import _native as N
+
+    T = O.synthetic_lower(5000, 8, 0.01, seed=5)
+    dT = S.DeviceCsr.upload(to_product(T))
+    work = torch.empty(T.nrows, dtype=torch.int64, device="cuda")
+    N.check(N.lib.sait_column_work(dT.handle, work.data_ptr(), None))
+    rows = np.repeat(np.arange(T.nrows), np.diff(T.row_ptr))
+    off = rows != T.col_idx
+    cnt = np.bincount(T.col_idx[off], minlength=T.nrows)
+    want = np.bincount(T.col_idx[off], weights=(cnt[rows[off]] + 1), minlength=T.nrows).astype(np.int64)
+    assert np.array_equal(work.cpu().numpy(), want)

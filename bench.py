@@ -36,6 +36,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# rank 0 prints exactly one JSON line on stdout: keep NCCL's version banner
+# (NCCL_DEBUG=VERSION prints it to stdout) off it
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 BASE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASE["metric"]
@@ -619,6 +623,20 @@ def run_b200(args):
         "note": "both factors built concurrently (sait_build_pair), wall time of the call incl. "
                 "split/transposes, median of %d builds after a warm-up; replicated on every rank" % BUILD_REPS,
     }
+    # the same build through the drop-in host API: host int64 CSR in, host
+    # int64 CSR out (saitprec::sait_thr's contract, sait.cpp:90-101), both
+    # uploads and both downloads inside the timed call
+    he = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        hl, hu = S.sait_thr_pair(f.lower, f.upper, S.SaitThrParams(TAU, STEPS_K))
+        he.append(time.perf_counter() - t0)
+    build["e2e_host"] = {"seconds": float(np.median(he)), "nnz_per_s": (nnz_l + nnz_u) / float(np.median(he)),
+                         "bitwise_equal_device_build": bool(np.array_equal(hl.values.view(np.uint64),
+                                                                           ML.to_host().values.view(np.uint64))),
+                         "api": "sait_thr_pair on host CsrMatrix (int64 row_ptr/col_idx, fp64) in and out: "
+                                "upload + narrowing, build, widening + download; median of 3"}
+    del hl, hu
     B = b_pair(n, nnz_l, nnz_u)
     stream = torch.cuda.current_stream()
     ML_host = MU_host = None
@@ -1006,7 +1024,6 @@ def run_build_c4(S, torch, cpu_sample=True):
     t_gen = time.perf_counter() - t0
     T = S.DeviceCsr.upload(Th)
     nnz_t = Th.nnz()
-    del Th
     S.reserve_device_pool(40 << 30)
     P = S.SaitThrParams(C4_TAU, C4_K)
     nnz_steps = []
@@ -1025,6 +1042,17 @@ def run_build_c4(S, torch, cpu_sample=True):
             secs.append(time.perf_counter() - t0)
         nnz_m = m.nnz()
         m.free()
+    # the drop-in host API end to end: host int64 T in, host int64 M out
+    he = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        Mh = S.sait_thr_cap(Th, S.lower_triangular, P, C4_CAP)
+        he.append(time.perf_counter() - t0)
+        del Mh
+    del Th
+    e2e_host = {"seconds": min(he), "nnz_per_s": nnz_m / min(he), "samples_s": [round(x, 4) for x in he],
+                "api": "sait_thr_cap on the host CsrMatrix (int64/fp64, 4.2 GB in, 4.4 GB out): upload + narrowing, "
+                       "build, widening + download; best of 2"}
     irregular = irregular_apply_line(S, torch, T, 3, torch.cuda.current_stream())
     T.free()
     nnz_steps.append(nnz_m)
@@ -1043,6 +1071,7 @@ def run_build_c4(S, torch, cpu_sample=True):
         "note": "wall time of the synchronous sait_build call (split, 3 recursion steps, transposes), "
                 "median of %d after a warm-up" % C4_REPS,
         "irregular_apply": irregular,
+        "e2e_host": e2e_host,
     }
     if cpu_sample:
         out["cpu_baseline"] = c4_cpu_sample(S)

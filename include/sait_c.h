@@ -83,6 +83,12 @@ void sait_csr_free(sait_dcsr_t m);
  * checked like the reference's span sizes. */
 int sait_spmv(sait_dcsr_t a, const double *d_x, int64_t xlen, double *d_y, int64_t ylen,
               sait_stream_t stream);
+/* dense.hpp:41 / dense.cpp:10-19: Y = A X for a column-major n x nvec block
+ * (DenseMatrix layout; d_x holds ncols x nvec, d_y nrows x nvec).  The
+ * reference runs one spmv per column; here the matrix is read once per slab
+ * of up to 8 columns (each column's rows still summed in stored order:
+ * bitwise the per-column spmv). */
+int sait_spmm(sait_dcsr_t a, const double *d_x, double *d_y, int64_t nvec, sait_stream_t stream);
 /* kernels.hpp:21 / kernels.cpp:34-102: C = A B (Gustavson, ascending-k accumulation). */
 int sait_spgemm(sait_dcsr_t a, sait_dcsr_t b, sait_stream_t stream, sait_dcsr_t *out);
 /* kernels.hpp:25 / kernels.cpp:104-134 */

@@ -786,6 +786,40 @@ int sait_spmv(sait_dcsr_t a, const double* d_x, int64_t xlen, double* d_y, int64
   });
 }
 
+int sait_spmm(sait_dcsr_t a, const double* d_x, double* d_y, int64_t nvec, sait_stream_t stream) {
+  return guarded([&] {
+    need(a, "spmm");
+    if (nvec < 0) sait::throw_invalid("spmm: negative block width");
+    if (nvec == 0 || a->m.nrows == 0) return;
+    if (!d_x || !d_y) sait::throw_invalid("spmm: null block");
+    DeviceGuard g(a->dev);
+    init_device_pool();
+    cudaStream_t s = sait::as_stream(stream);
+    const sait::DevCsr& m = a->m;
+    // column-major blocks in slabs of 8/4/2/1 vectors: transposed to
+    // row-major, one CSR block product per slab (the matrix read once per
+    // slab instead of once per column), transposed back
+    const int64_t slab = std::min<int64_t>(nvec, 8);
+    double* xt = sait::dalloc<double>(m.ncols * slab, s);
+    double* yt = sait::dalloc<double>(m.nrows * slab, s);
+    for (int64_t c = 0; c < nvec;) {
+      const int w = nvec - c >= 8 ? 8 : nvec - c >= 4 ? 4 : nvec - c >= 2 ? 2 : 1;
+      const double* x = d_x + c * m.ncols;
+      double* y = d_y + c * m.nrows;
+      if (w == 1) {
+        sait::spmv(m, x, y, s);
+      } else {
+        sait::transpose_block(x, xt, m.ncols, w, true, s);
+        sait::spmm_rowmajor(m, xt, yt, w, s);
+        sait::transpose_block(yt, y, m.nrows, w, false, s);
+      }
+      c += w;
+    }
+    sait::dfree(xt, s);
+    sait::dfree(yt, s);
+  });
+}
+
 int sait_spgemm(sait_dcsr_t a, sait_dcsr_t b, sait_stream_t stream, sait_dcsr_t* out) {
   return guarded([&] {
     need(a, "spgemm");

@@ -347,9 +347,13 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// No "memory" clobber: a clobber would pin every surrounding gather in
+// program order (one x load in flight instead of eight); the acquire of the
+// owner's flag (wait_epoch_sys, which does clobber) already orders these
+// loads after it.
 __device__ __forceinline__ double ld_relaxed_sys(const double* p) {
   double r;
-  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(r) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void wait_epoch_sys(const int* flag, int epoch) {
@@ -367,7 +371,7 @@ __device__ __forceinline__ void wait_epoch_sys(const int* flag, int epoch) {
 }
 
 template <class IDX>
-__global__ void __launch_bounds__(256) sell_spmv_halo_kernel(int64_t n, int64_t nslices,
+__global__ void __launch_bounds__(256, 5) sell_spmv_halo_kernel(int64_t n, int64_t nslices,
                                                               const int64_t* __restrict__ soff, IDX idx,
                                                               const double* __restrict__ sval,
                                                               const double* __restrict__ x, double* __restrict__ y,
@@ -397,21 +401,31 @@ __global__ void __launch_bounds__(256) sell_spmv_halo_kernel(int64_t n, int64_t 
         hi |= c[j] >= h.own_hi;
       }
     }
-    if (!lo_ready && __any_sync(0xffffffffu, lo)) {
-      wait_epoch_sys(h.lo_flag, h.epoch);
-      lo_ready = true;
-    }
-    if (!hi_ready && __any_sync(0xffffffffu, hi)) {
-      wait_epoch_sys(h.hi_flag, h.epoch);
-      hi_ready = true;
-    }
+    if (__any_sync(0xffffffffu, lo || hi)) {  // a boundary batch: wait for the owners, read over NVLink
+      if (!lo_ready && __any_sync(0xffffffffu, lo)) {
+        wait_epoch_sys(h.lo_flag, h.epoch);
+        lo_ready = true;
+      }
+      if (!hi_ready && __any_sync(0xffffffffu, hi)) {
+        wait_epoch_sys(h.hi_flag, h.epoch);
+        hi_ready = true;
+      }
+      double xv[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (c[j] < 0) continue;
-      const double xv = c[j] < h.own_lo  ? ld_relaxed_sys(h.lo_src + (c[j] + h.lo_shift))
-                        : c[j] >= h.own_hi ? ld_relaxed_sys(h.hi_src + (c[j] + h.hi_shift))
-                                           : __ldg(x + c[j]);
-      acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
+      for (int j = 0; j < 8; ++j)
+        xv[j] = c[j] < 0             ? 0.0
+                : c[j] < h.own_lo    ? ld_relaxed_sys(h.lo_src + (c[j] + h.lo_shift))
+                : c[j] >= h.own_hi   ? ld_relaxed_sys(h.hi_src + (c[j] + h.hi_shift))
+                                     : __ldg(x + c[j]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+    } else {  // interior batch: the single-GPU kernel's loads
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double xv = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+        if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
+      }
     }
   }
   if (row < n) y[row] = acc;

@@ -429,8 +429,8 @@ DenseMatrix spmm(const CsrMatrix& a, const DenseMatrix& x) {
   Dev d = upload(a);
   DevVec dx(static_cast<size_t>(x.nrows() * x.ncols())), dy(static_cast<size_t>(a.nrows * x.ncols()));
   dx.put(x.data().data(), x.data().size());
-  for (index_t j = 0; j < x.ncols(); ++j)
-    check(sait_spmv(d.h, dx.p + j * x.nrows(), x.nrows(), dy.p + j * a.nrows, a.nrows, thread_stream()));
+  // one block product (the matrix read once per 8 columns), not a spmv per column
+  check(sait_spmm(d.h, dx.p, dy.p, x.ncols(), thread_stream()));
   check(sait_device_synchronize());
   dy.get(y.data().data(), y.data().size());
   return y;

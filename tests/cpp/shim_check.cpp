@@ -11,6 +11,7 @@
 
 #include "sait_c.h"
 #include "saitprec/csr.hpp"
+#include "saitprec/dense.hpp"
 #include "saitprec/ilu.hpp"
 #include "saitprec/kernels.hpp"
 #include "saitprec/krylov.hpp"
@@ -97,6 +98,19 @@ int main(int argc, char** argv) {
   const JacobiSplit sp = jacobi_split(f.upper, upper_triangular);
   put("poly", sait_polynomial(sp, 3, {}));
   put("transpose", transpose(ML));
+  {  // dense.hpp:41 spmm on an n x 11 block (slabs of 8 + 2 + 1 on the device)
+    DenseMatrix X(n, 11);
+    for (index_t j = 0; j < 11; ++j) sait_fill_uniform_pm1(40 + j, n, X.col(j).data());
+    const DenseMatrix Y = spmm(ML, X);
+    put("spmm11", std::vector<double>(Y.data().begin(), Y.data().end()));
+    std::vector<double> cols;
+    for (index_t j = 0; j < 11; ++j) {
+      std::vector<double> xj(X.col(j).begin(), X.col(j).end());
+      const std::vector<double> yj = spmv(ML, xj);
+      cols.insert(cols.end(), yj.begin(), yj.end());
+    }
+    put("spmm11_cols", cols);
+  }
   {
     ExactIluPreconditioner E(f);
     put("exact_z", apply_precond(E, r));

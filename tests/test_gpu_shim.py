@@ -82,6 +82,12 @@ def test_shim_builders_and_kernels_match_oracle(dump, golden, port):
     assert eq("patcap_2", port.sait_pat_capture_pattern(L, True, 2))
     assert eq("spgemm", port.spgemm(L, U))
     assert eq("transpose", port.transpose(golden_csr(golden, "c1/ML")))
+    # spmm (dense.hpp:41) through the block kernel: bitwise the per-column spmv
+    # and the oracle's spmv of every column
+    assert bitwise_equal(dump["spmm11"], dump["spmm11_cols"])
+    n = golden_csr(golden, "c1/ML").nrows
+    want = np.concatenate([port.spmv(golden_csr(golden, "c1/ML"), O.uniform_pm1(40 + j, n)) for j in range(11)])
+    assert bitwise_equal(dump["spmm11"], want)
     r = golden["c1/r"]
     assert bitwise_equal(dump["sweeps"], port.jacobi_sweeps_apply(L, True, r, 4))
     _, tt = port.jacobi_split(U, False)

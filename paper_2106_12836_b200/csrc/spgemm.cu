@@ -739,6 +739,76 @@ __global__ void __launch_bounds__(256) scatter_bins(int64_t n, const int8_t* __r
     if (b[q] >= 0) lists[base[b[q]] + pos[q]] = static_cast<int32_t>(j0 + q * 32 + lane);
 }
 
+// Order-preserving variant: each bin's list holds its rows in ascending row
+// order.  The hash-table rows gather B rows near their own row (banded and
+// geometric patterns alike), so rows processed side by side share their B
+// rows in L2 only if neighbouring list entries are neighbouring rows; the
+// atomic cursors above interleave 1024-row chunks from ~1000 resident blocks
+// and the gathers then miss L2 (C4: ~5x the compulsory DRAM bytes).
+// Pass 1 counts rows per (bin, block) into counts[bin * nblk + block]; an
+// exclusive scan of that bin-major array gives every block its start in
+// every bin (bins are consecutive in `lists`); pass 2 scatters in row order
+// (per-warp bin counts, prefixed across the block's warps in warp order).
+constexpr int kOrdWarps = 8, kOrdRows = 256 * kBinRowsPerThread;
+__global__ void __launch_bounds__(256) bin_block_counts(int64_t n, const int8_t* __restrict__ bin_of, int64_t nblk,
+                                                        int32_t* __restrict__ counts) {
+  __shared__ int32_t cnt[kNumBins];
+  if (threadIdx.x < kNumBins) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kOrdRows;
+#pragma unroll
+  for (int q = 0; q < kBinRowsPerThread; ++q) {
+    const int64_t j = j0 + q * 256 + threadIdx.x;
+    const int b = j < n ? bin_of[j] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&cnt[b], __popc(grp));
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumBins) counts[static_cast<int64_t>(threadIdx.x) * nblk + blockIdx.x] = cnt[threadIdx.x];
+}
+__global__ void __launch_bounds__(256) scatter_bins_ordered(int64_t n, const int8_t* __restrict__ bin_of, int64_t nblk,
+                                                            const int32_t* __restrict__ offs,
+                                                            int32_t* __restrict__ lists) {
+  __shared__ int32_t wcnt[kOrdWarps][kNumBins];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < kOrdWarps * kNumBins; t += 256) (&wcnt[0][0])[t] = 0;
+  __syncthreads();
+  // warp w owns rows j0 + w*128 .. +127 (4 groups of 32, in order)
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kOrdRows + static_cast<int64_t>(w) * 32 * kBinRowsPerThread;
+  int b[kBinRowsPerThread];
+#pragma unroll
+  for (int q = 0; q < kBinRowsPerThread; ++q) {
+    const int64_t j = j0 + q * 32 + lane;
+    b[q] = j < n ? bin_of[j] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, b[q]);
+    if (b[q] >= 0 && lane == __ffs(grp) - 1) wcnt[w][b[q]] += __popc(grp);  // one writer per (warp, bin) per q
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumBins) {  // exclusive prefix over the warps, from the block's start in the bin
+    int32_t run = offs[static_cast<int64_t>(threadIdx.x) * nblk + blockIdx.x];
+    for (int ww = 0; ww < kOrdWarps; ++ww) {
+      const int32_t c = wcnt[ww][threadIdx.x];
+      wcnt[ww][threadIdx.x] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kBinRowsPerThread; ++q) {
+    const unsigned grp = __match_any_sync(0xffffffffu, b[q]);
+    const int leader = __ffs(grp) - 1;
+    int32_t base = 0;
+    if (b[q] >= 0) base = wcnt[w][b[q]];
+    __syncwarp();
+    if (b[q] >= 0) {
+      lists[base + __popc(grp & ((1u << lane) - 1u))] = static_cast<int32_t>(j0 + q * 32 + lane);
+      if (lane == leader) wcnt[w][b[q]] = base + __popc(grp);
+    }
+    __syncwarp();
+  }
+}
+
 using SmemKernel = void (*)(Args, const int32_t*, int32_t, bool);
 
 SmemKernel smem_kernel(int bin) {
@@ -968,8 +1038,29 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
       pl.tcol[tb] = dalloc<int32_t>(static_cast<int64_t>(pl.hist[tb]) * kTinyG[tb], s);
       pl.tval[tb] = dalloc<double>(static_cast<int64_t>(pl.hist[tb]) * kTinyG[tb], s);
     }
-  scatter_bins<<<grid_for(n, 256 * kBinRowsPerThread), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
-  SAIT_LAUNCHED();
+  static const int order_mode = [] {  // SAIT_BIN_ORDER: 0 atomic cursors, 1 always ordered, default: hash rows
+    const char* e = std::getenv("SAIT_BIN_ORDER");
+    return e ? std::atoi(e) : 2;
+  }();
+  const bool ordered =
+      order_mode == 1 || (order_mode == 2 && pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin] > 0);
+  if (ordered) {
+    const int64_t nblk = (n + kOrdRows - 1) / kOrdRows;
+    int32_t* bc = dalloc<int32_t>(kNumBins * nblk, s);
+    int32_t* bo = dalloc<int32_t>(kNumBins * nblk + 1, s);
+    int64_t* btot = dalloc<int64_t>(1, s);
+    bin_block_counts<<<static_cast<unsigned>(nblk), 256, 0, s>>>(n, bin_of, nblk, bc);
+    SAIT_LAUNCHED();
+    scan_counts_async(bc, bo, kNumBins * nblk, btot, s);
+    dfree(btot, s);
+    scatter_bins_ordered<<<static_cast<unsigned>(nblk), 256, 0, s>>>(n, bin_of, nblk, bo, pl.lists);
+    SAIT_LAUNCHED();
+    dfree(bc, s);
+    dfree(bo, s);
+  } else {
+    scatter_bins<<<grid_for(n, 256 * kBinRowsPerThread), 256, 0, s>>>(n, bin_of, cursor, pl.lists);
+    SAIT_LAUNCHED();
+  }
   int32_t gc = pl.hist[kGlobalBin];
   if (gc) {
     // per-row global tables: gather the table sizes of the global-bin rows on

@@ -260,15 +260,22 @@ int sait_operator_apply_halo(sait_op_t op, const double *d_x_ext, int64_t ext_le
                              double *d_y, int64_t ylen, sait_stream_t stream);
 /* The row-sharded pair with peer-memory halos as one native object (the
  * data path of the multi-GPU apply): per factor this rank's two
- * parity copies of its extended vector, its epoch flag, the own segment and
- * per parity the neighbours' halo sources.  apply(r, z) on this rank's rows:
- * epoch e += 1; r -> own segment of M_L's copy (e & 1); publish; M_L's halo
- * SpMV writes y into M_U's own segment; publish; M_U's halo SpMV -> z.  The
+ * parity copies of its extended vector, its epoch flag, the own segment, the
+ * own rows its neighbours read (send ranges) and per parity the neighbours'
+ * halo sources.  apply(r, z) on this rank's rows, epoch e += 1, parity e & 1:
+ *   1. only the boundary slices of r the neighbours read are copied into M_L's
+ *      extended vector, and the same kernel publishes flag_L = e;
+ *   2. M_L's halo SpMV reads its own x straight from r and its halo over
+ *      NVLink (after the owners' flags), writes y into M_U's own segment,
+ *      and its last CTA publishes flag_U = e (no extra launch);
+ *   3. M_U's halo SpMV (a programmatic dependent of M_L) -> z.
+ * Without neighbours this is two kernels, like the single-GPU pair.  The
  * operators are borrowed (they must outlive the pair). */
 typedef struct {
   double *ext[2];       /* extended vector, parity 0 / 1 (device) */
   int *flag;            /* this rank's published epoch for this factor */
   int64_t ext_len, own_offset, own_len;
+  int64_t send_a0, send_n0, send_a1, send_n1; /* own rows [a, a + n) the neighbours read */
   sait_halo_t halo[2];  /* per parity (the epoch field is set per apply) */
 } sait_peer_factor_desc;
 typedef struct sait_peer_pair_s *sait_peer_pair_t;

@@ -72,7 +72,8 @@ class PeerFactorDesc(C.Structure):
     """sait_peer_factor_desc (include/sait_c.h)"""
 
     _fields_ = [("ext", C.c_void_p * 2), ("flag", C.c_void_p), ("ext_len", C.c_int64), ("own_offset", C.c_int64),
-                ("own_len", C.c_int64), ("halo", Halo * 2)]
+                ("own_len", C.c_int64), ("send_a0", C.c_int64), ("send_n0", C.c_int64), ("send_a1", C.c_int64),
+                ("send_n1", C.c_int64), ("halo", Halo * 2)]
 
 
 class HostCsr(C.Structure):

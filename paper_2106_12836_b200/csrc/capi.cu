@@ -1319,9 +1319,37 @@ struct sait_peer_pair_s {
   int dev = 0;
   sait_op_t op[2] = {nullptr, nullptr};
   sait_peer_factor_desc d[2];
+  // per factor: slices [0, lo_end) and [hi_begin, nslices) read halo
+  // columns; [lo_end, hi_begin) is interior and runs the single-GPU kernel
+  int64_t lo_end[2] = {0, 0}, hi_begin[2] = {0, 0};
+  unsigned* count = nullptr;  // grid-done counters of the two publishing kernels
   int epoch = 0;
   std::mutex mu;  // one apply at a time (the epochs and buffers are shared)
 };
+
+namespace {
+// One factor of a peer pair: interior slices (single-GPU kernel, PDL), then the
+// boundary slice ranges (halo kernel).  The launch that carries h.pub_flag is
+// the last one and is not a programmatic dependent, so when its last CTA
+// publishes, every y store of the factor has completed.
+void run_factor(sait_peer_pair_t p, int f, const double* x_ext, sait::HaloArgs h, double* y, cudaStream_t s) {
+  const sait::SellMatrix& m = p->op[f]->sell;
+  const int64_t ns = m.nslices, lo_end = std::min(p->lo_end[f], ns), hi_begin = std::max(p->hi_begin[f], lo_end);
+  const bool publish = h.pub_flag != nullptr;
+  sait::HaloArgs hq = h;
+  hq.pub_flag = nullptr;
+  hq.pub_count = nullptr;
+  // interior rows [lo_end * 32, hi_begin * 32): no halo columns
+  if (hi_begin > lo_end) {
+    const int64_t r0 = lo_end * 32 - 0, r1 = std::min<int64_t>(hi_begin * 32, m.n);
+    sait::sell_spmv_rows(m, r0, r1, x_ext, y, s, true);
+  }
+  const bool has_lo = lo_end > 0, has_hi = hi_begin < ns;
+  if (has_lo) sait::sell_spmv_halo_slices(m, 0, lo_end, x_ext, (publish && !has_hi) ? h : hq, y, s, !publish || has_hi);
+  if (has_hi) sait::sell_spmv_halo_slices(m, hi_begin, ns, x_ext, publish ? h : hq, y, s, !publish);
+  if (publish && !has_lo && !has_hi) sait::publish_epoch(h.pub_flag, h.epoch, s);
+}
+}  // namespace
 
 extern "C" {
 
@@ -1348,12 +1376,32 @@ int sait_peer_pair_create(sait_op_t ml, sait_op_t mu, const sait_peer_factor_des
     if (ops[0]->a->m.nrows != desc[1].own_len || ops[1]->a->m.nrows != desc[1].own_len ||
         desc[0].own_len != desc[1].own_len)
       sait::throw_invalid("peer_pair: row blocks do not chain");
+    for (int f = 0; f < 2; ++f) {
+      const sait_peer_factor_desc& x = desc[f];
+      if (x.send_n0 < 0 || x.send_n1 < 0 || x.send_a0 < 0 || x.send_a1 < 0 || x.send_a0 + x.send_n0 > x.own_len ||
+          x.send_a1 + x.send_n1 > x.own_len)
+        sait::throw_invalid("peer_pair: send range outside the own segment");
+    }
+    DeviceGuard g(ml->dev);
     auto* p = new sait_peer_pair_s;
     p->dev = ml->dev;
     p->op[0] = ml;
     p->op[1] = mu;
     p->d[0] = desc[0];
     p->d[1] = desc[1];
+    SAIT_CUDA(cudaMalloc(&p->count, 2 * sizeof(unsigned)));
+    SAIT_CUDA(cudaMemset(p->count, 0, 2 * sizeof(unsigned)));
+    sait::preload_peer_kernels();
+    for (int f = 0; f < 2; ++f) {
+      sait::halo_slice_bounds(ops[f]->sell, desc[f].halo[0].own_lo, desc[f].halo[0].own_hi, &p->lo_end[f],
+                              &p->hi_begin[f], nullptr);
+      if (std::getenv("SAIT_DEBUG_PEER"))
+        std::fprintf(stderr, "peer_pair f=%d own=[%lld,%lld) ext=%lld slices=%lld lo_end=%lld hi_begin=%lld send=(%lld,%lld)(%lld,%lld)\n", f,
+                     (long long)desc[f].halo[0].own_lo, (long long)desc[f].halo[0].own_hi, (long long)desc[f].ext_len,
+                     (long long)ops[f]->sell.nslices, (long long)p->lo_end[f], (long long)p->hi_begin[f],
+                     (long long)desc[f].send_a0, (long long)desc[f].send_n0, (long long)desc[f].send_a1,
+                     (long long)desc[f].send_n1);
+    }
     *out = p;
   });
 }
@@ -1367,17 +1415,35 @@ int sait_peer_pair_apply(sait_peer_pair_t p, const double* d_r, double* d_z, sai
     const int e = ++p->epoch;
     const int par = e & 1;
     const sait_peer_factor_desc &L = p->d[0], &U = p->d[1];
-    // r -> own segment of M_L's extended vector; publish; M_L (halo read from
-    // the neighbours inside the SpMV) writes y into M_U's own segment; publish; M_U
-    SAIT_CUDA(cudaMemcpyAsync(L.ext[par] + L.own_offset, d_r, sizeof(double) * L.own_len, cudaMemcpyDeviceToDevice, s));
-    sait::publish_epoch(L.flag, e, s);
-    sait::sell_spmv_halo(p->op[0]->sell, L.ext[par], to_halo(L.halo[par], e), U.ext[par] + U.own_offset, s);
-    sait::publish_epoch(U.flag, e, s);
-    sait::sell_spmv_halo(p->op[1]->sell, U.ext[par], to_halo(U.halo[par], e), d_z, s);
+    // 1. the slices of r the neighbours read -> M_L's extended vector, publish
+    if (L.send_n0 + L.send_n1 > 0)
+      sait::copy_slices_publish(d_r, L.ext[par] + L.own_offset, L.send_a0, L.send_n0, L.send_a1, L.send_n1, L.flag,
+                                p->count, e, s);
+    // 2. M_L: own x straight from r (ext column c = r[c - own_offset]), y into
+    //    M_U's own segment.  Interior slices first with the single-GPU kernel
+    //    (no waiting: the halo transfer overlaps them), then the boundary
+    //    slices, which read the halo over NVLink after the owners' flags; the
+    //    last launch's last CTA publishes flag_U.
+    sait::HaloArgs hl = to_halo(L.halo[par], e);
+    if (U.send_n0 + U.send_n1 > 0) {
+      hl.pub_flag = U.flag;
+      hl.pub_count = p->count + 1;
+    }
+    run_factor(p, 0, d_r - L.own_offset, hl, U.ext[par] + U.own_offset, s);
+    // 3. M_U, the same way (programmatic dependent of M_L's last launch)
+    run_factor(p, 1, U.ext[par], to_halo(U.halo[par], e), d_z, s);
   });
 }
 
-void sait_peer_pair_destroy(sait_peer_pair_t p) { delete p; }
+void sait_peer_pair_destroy(sait_peer_pair_t p) {
+  if (!p) return;
+  if (p->count) {
+    cudaSetDevice(p->dev);
+    cudaDeviceSynchronize();
+    cudaFree(p->count);
+  }
+  delete p;
+}
 
 int sait_publish_epoch(int* d_flag, int epoch, sait_stream_t stream) {
   return guarded([&] {

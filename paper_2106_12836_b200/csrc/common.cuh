@@ -266,9 +266,29 @@ struct HaloArgs {
   const int* lo_flag = nullptr;    // the owners' published epochs
   const int* hi_flag = nullptr;
   int epoch = 0;
+  // optional: once every CTA's y stores are done, the last CTA publishes
+  // *pub_flag = epoch (system-scope release; pub_count: a zeroed counter)
+  int* pub_flag = nullptr;
+  unsigned* pub_count = nullptr;
 };
-void sell_spmv_halo(const SellMatrix& m, const double* x_ext, const HaloArgs& h, double* y, cudaStream_t s);
+// x_ext: own columns read x_ext[c] (c in [own_lo, own_hi)); pdl: launched as
+// a programmatic dependent of the preceding kernel (x read after its end)
+void sell_spmv_halo(const SellMatrix& m, const double* x_ext, const HaloArgs& h, double* y, cudaStream_t s,
+                    bool pdl = false);
+// the same over slices [s0, s1) only (publishes through h.pub_flag even when empty)
+void sell_spmv_halo_slices(const SellMatrix& m, int64_t s0, int64_t s1, const double* x_ext, const HaloArgs& h,
+                           double* y, cudaStream_t s, bool pdl);
+// force-load the peer data path's kernels (lazy module loading would
+// synchronise the context at a first launch, see sell.cu)
+void preload_peer_kernels();
+// [0, lo_end) and [hi_begin, nslices): the slices that read halo columns
+void halo_slice_bounds(const SellMatrix& m, int64_t own_lo, int64_t own_hi, int64_t* lo_end, int64_t* hi_begin,
+                       cudaStream_t s);
 void publish_epoch(int* flag, int epoch, cudaStream_t s);
+// dst[k] = src[k] for the two boundary slices [a0, a0 + n0), [a1, a1 + n1),
+// then *flag = epoch (system-scope release) once all CTAs are done
+void copy_slices_publish(const double* src, double* dst, int64_t a0, int64_t n0, int64_t a1, int64_t n1, int* flag,
+                         unsigned* count, int epoch, cudaStream_t s);
 // rows [row0, row1) only (row0 a multiple of 32)
 void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const double* x, double* y, cudaStream_t s,
                     bool pdl = false);  // pdl: programmatic dependent of the previous kernel on s

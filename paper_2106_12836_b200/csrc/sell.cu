@@ -366,69 +366,110 @@ __device__ __forceinline__ void wait_epoch_sys(const int* flag, int epoch) {
     if (ns < 1024) ns <<= 1;
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    if (t - t0 > 20000000000ull) __trap();
+    if (t - t0 > 20000000000ull) {
+      printf("sait: halo wait timed out (flag %p = %d, waiting for epoch %d, block %d)\n", flag,
+             ld_acquire_sys(flag), epoch, blockIdx.x);
+      __trap();
+    }
   }
 }
 
-template <class IDX>
-__global__ void __launch_bounds__(256, 5) sell_spmv_halo_kernel(int64_t n, int64_t nslices,
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// The last CTA of the grid to finish publishes *flag = epoch: every CTA
+// fences its stores device-wide and counts itself; the one that completes the
+// count fences system-wide (peers over NVLink read the data) and releases the
+// flag, then rearms the counter for the next launch (stream-ordered).
+__device__ __forceinline__ void publish_when_grid_done(int* flag, unsigned* count, int epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      st_release_sys(flag, epoch);
+      *count = 0;
+    }
+  }
+}
+
+template <class IDX, bool PDL>
+__global__ void __launch_bounds__(256, 5) sell_spmv_halo_kernel(int64_t n, int64_t s_begin, int64_t s_end,
                                                               const int64_t* __restrict__ soff, IDX idx,
                                                               const double* __restrict__ sval,
                                                               const double* __restrict__ x, double* __restrict__ y,
                                                               HaloArgs h) {
+  if (PDL) pdl_launch_dependents();
   const int lane = threadIdx.x & 31;
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (s >= nslices) return;
-  const int64_t base = soff[s];
-  const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
-  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
-  const int64_t e0 = base + lane;
-  const int64_t i0 = idx.slice_base(s, base) + lane;
-  bool lo_ready = false, hi_ready = false;
-  double acc = 0.0;
-  for (int32_t k0 = 0; k0 < w; k0 += 8) {
-    int32_t c[8];
-    double v[8];
-    bool lo = false, hi = false;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      c[j] = -1;
-      v[j] = 0.0;
-      if (k0 + j < w) {
-        c[j] = idx.col(i0 + static_cast<int64_t>(k0 + j) * kSlice, row);
-        v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
-        lo |= c[j] >= 0 && c[j] < h.own_lo;
-        hi |= c[j] >= h.own_hi;
-      }
-    }
-    if (__any_sync(0xffffffffu, lo || hi)) {  // a boundary batch: wait for the owners, read over NVLink
-      if (!lo_ready && __any_sync(0xffffffffu, lo)) {
-        wait_epoch_sys(h.lo_flag, h.epoch);
-        lo_ready = true;
-      }
-      if (!hi_ready && __any_sync(0xffffffffu, hi)) {
-        wait_epoch_sys(h.hi_flag, h.epoch);
-        hi_ready = true;
-      }
-      double xv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        xv[j] = c[j] < 0             ? 0.0
-                : c[j] < h.own_lo    ? ld_relaxed_sys(h.lo_src + (c[j] + h.lo_shift))
-                : c[j] >= h.own_hi   ? ld_relaxed_sys(h.hi_src + (c[j] + h.hi_shift))
-                                     : __ldg(x + c[j]);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
-    } else {  // interior batch: the single-GPU kernel's loads
+  const int64_t s = s_begin + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s < s_end) {
+    const int64_t base = soff[s];
+    const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+    const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+    const int64_t e0 = base + lane;
+    const int64_t i0 = idx.slice_base(s, base) + lane;
+    bool lo_ready = false, hi_ready = false;
+    double acc = 0.0;
+    for (int32_t k0 = 0; k0 < w; k0 += 8) {
+      int32_t c[8];
+      double v[8];
+      bool lo = false, hi = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const double xv = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
-        if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
+        c[j] = -1;
+        v[j] = 0.0;
+        if (k0 + j < w) {
+          c[j] = idx.col(i0 + static_cast<int64_t>(k0 + j) * kSlice, row);
+          v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
+          lo |= c[j] >= 0 && c[j] < h.own_lo;
+          hi |= c[j] >= h.own_hi;
+        }
+      }
+      if (PDL && k0 == 0) pdl_wait();  // the own x is the previous grid's output
+      if (__any_sync(0xffffffffu, lo || hi)) {  // a boundary batch: wait for the owners, read over NVLink
+        if (!lo_ready && __any_sync(0xffffffffu, lo)) {
+          wait_epoch_sys(h.lo_flag, h.epoch);
+          lo_ready = true;
+        }
+        if (!hi_ready && __any_sync(0xffffffffu, hi)) {
+          wait_epoch_sys(h.hi_flag, h.epoch);
+          hi_ready = true;
+        }
+        double xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          xv[j] = c[j] < 0           ? 0.0
+                  : c[j] < h.own_lo  ? ld_relaxed_sys(h.lo_src + (c[j] + h.lo_shift))
+                  : c[j] >= h.own_hi ? ld_relaxed_sys(h.hi_src + (c[j] + h.hi_shift))
+                                     : (PDL ? ld_weak(x + c[j]) : __ldg(x + c[j]));
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+      } else {  // interior batch: the single-GPU kernel's loads
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double xv = c[j] >= 0 ? (PDL ? ld_weak(x + c[j]) : __ldg(x + c[j])) : 0.0;
+          if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv));
+        }
       }
     }
+    if (row < n) y[row] = acc;
+  } else if (PDL) {
+    pdl_wait();  // keep the grid's completion after the prerequisite's
   }
-  if (row < n) y[row] = acc;
+  if (h.pub_flag) publish_when_grid_done(h.pub_flag, h.pub_count, h.epoch);
+}
+
+__global__ void copy_slices_publish_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t a0,
+                                           int64_t n0, int64_t a1, int64_t n1, int* flag, unsigned* count,
+                                           int epoch) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n0 + n1;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = k < n0 ? a0 + k : a1 + (k - n0);
+    dst[e] = src[e];
+  }
+  publish_when_grid_done(flag, count, epoch);
 }
 
 // flag = epoch, ordered after everything queued before it on the stream
@@ -704,16 +745,121 @@ void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const doubl
   SAIT_LAUNCHED();
 }
 
-void sell_spmv_halo(const SellMatrix& m, const double* x_ext, const HaloArgs& h, double* y, cudaStream_t s) {
-  if (m.nslices == 0) return;
-  const unsigned grid = sell_grid(m.nslices);
-  if (m.dict)
-    sell_spmv_halo_kernel<IdxDict><<<grid, 256, 0, s>>>(m.n, m.nslices, m.soff, IdxDict{m.pat, m.dict}, m.val, x_ext,
-                                                         y, h);
-  else if (m.dcol)
-    sell_spmv_halo_kernel<Idx16><<<grid, 256, 0, s>>>(m.n, m.nslices, m.soff, Idx16{m.dcol}, m.val, x_ext, y, h);
-  else
-    sell_spmv_halo_kernel<Idx32><<<grid, 256, 0, s>>>(m.n, m.nslices, m.soff, Idx32{m.col}, m.val, x_ext, y, h);
+template <class IDX>
+void launch_halo(const SellMatrix& m, IDX ix, int64_t s0, int64_t s1, const double* x_ext, const HaloArgs& h,
+                 double* y, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sell_grid(s1 - s0));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_halo_kernel<IDX, true>, m.n, s0, s1, m.soff, ix, m.val, x_ext, y, h));
+  else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_halo_kernel<IDX, false>, m.n, s0, s1, m.soff, ix, m.val, x_ext, y, h));
+  SAIT_LAUNCHED();
+}
+
+void sell_spmv_halo_slices(const SellMatrix& m, int64_t s0, int64_t s1, const double* x_ext, const HaloArgs& h,
+                           double* y, cudaStream_t s, bool pdl) {
+  s1 = std::min(s1, m.nslices);
+  if (s1 <= s0) {
+    if (h.pub_flag) publish_epoch(h.pub_flag, h.epoch, s);
+    return;
+  }
+  if (m.dict) launch_halo(m, IdxDict{m.pat, m.dict}, s0, s1, x_ext, h, y, s, pdl);
+  else if (m.dcol) launch_halo(m, Idx16{m.dcol}, s0, s1, x_ext, h, y, s, pdl);
+  else launch_halo(m, Idx32{m.col}, s0, s1, x_ext, h, y, s, pdl);
+}
+
+void sell_spmv_halo(const SellMatrix& m, const double* x_ext, const HaloArgs& h, double* y, cudaStream_t s, bool pdl) {
+  sell_spmv_halo_slices(m, 0, m.nslices, x_ext, h, y, s, pdl);
+}
+
+// Under lazy module loading (the CUDA 12 default) a kernel's first launch
+// loads it, and loading synchronises the context: if a peer-halo kernel of
+// another rank in this process is already spinning on a flag that this launch
+// would eventually publish, that never returns.  Load every kernel of the
+// peer data path up front (cudaFuncGetAttributes forces the load).
+void preload_peer_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(sell_spmv_halo_kernel<IdxDict, true>),
+      reinterpret_cast<const void*>(sell_spmv_halo_kernel<IdxDict, false>),
+      reinterpret_cast<const void*>(sell_spmv_halo_kernel<Idx16, true>),
+      reinterpret_cast<const void*>(sell_spmv_halo_kernel<Idx16, false>),
+      reinterpret_cast<const void*>(sell_spmv_halo_kernel<Idx32, true>),
+      reinterpret_cast<const void*>(sell_spmv_halo_kernel<Idx32, false>),
+      reinterpret_cast<const void*>(sell_spmv_kernel<IdxDict, true>),
+      reinterpret_cast<const void*>(sell_spmv_kernel<IdxDict, false>),
+      reinterpret_cast<const void*>(sell_spmv_kernel<Idx16, true>),
+      reinterpret_cast<const void*>(sell_spmv_kernel<Idx16, false>),
+      reinterpret_cast<const void*>(sell_spmv_kernel<Idx32, true>),
+      reinterpret_cast<const void*>(sell_spmv_kernel<Idx32, false>),
+      reinterpret_cast<const void*>(copy_slices_publish_kernel),
+      reinterpret_cast<const void*>(publish_epoch_kernel),
+  };
+  for (const void* f : fns) SAIT_CUDA(cudaFuncGetAttributes(&a, f));
+}
+
+namespace {
+// boundary slices of a row block: lo_end = 1 + the last slice with a column
+// below own_lo, hi_begin = the first slice with a column >= own_hi
+__global__ void halo_slice_bounds_kernel(int64_t nslices, const int64_t* __restrict__ soff, const int32_t* col,
+                                         const int16_t* dcol, const int32_t* pat, const int32_t* dict,
+                                         int64_t own_lo, int64_t own_hi, unsigned long long* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nslices) return;
+  const int64_t base = soff[s], len = soff[s + 1] - base;
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  bool lo = false, hi = false;
+  for (int64_t e = lane; e < len; e += kSlice) {
+    int32_t c;
+    if (dict) {
+      const int32_t d = dict[pat[s] + e];
+      c = d == INT32_MIN ? -1 : row + d;
+    } else if (dcol) {
+      const int16_t d = dcol[base + e];
+      c = d == INT16_MIN ? -1 : row + d;
+    } else {
+      c = col[base + e];
+    }
+    lo |= c >= 0 && c < own_lo;
+    hi |= c >= own_hi;
+  }
+  const bool any_lo = __any_sync(0xffffffffu, lo), any_hi = __any_sync(0xffffffffu, hi);
+  if (lane == 0) {
+    if (any_lo) atomicMax(out, static_cast<unsigned long long>(s + 1));
+    if (any_hi) atomicMin(out + 1, static_cast<unsigned long long>(s));
+  }
+}
+}  // namespace
+
+void halo_slice_bounds(const SellMatrix& m, int64_t own_lo, int64_t own_hi, int64_t* lo_end, int64_t* hi_begin,
+                       cudaStream_t s) {
+  unsigned long long h[2] = {0ull, static_cast<unsigned long long>(m.nslices)};
+  unsigned long long* d = dalloc<unsigned long long>(2, s);
+  SAIT_CUDA(cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, s));
+  if (m.nslices) {
+    halo_slice_bounds_kernel<<<sell_grid(m.nslices), 256, 0, s>>>(m.nslices, m.soff, m.col, m.dcol, m.pat, m.dict,
+                                                                  own_lo, own_hi, d);
+    SAIT_LAUNCHED();
+  }
+  SAIT_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  dfree(d, s);
+  *lo_end = static_cast<int64_t>(h[0]);
+  *hi_begin = static_cast<int64_t>(h[1]);
+}
+
+void copy_slices_publish(const double* src, double* dst, int64_t a0, int64_t n0, int64_t a1, int64_t n1, int* flag,
+                         unsigned* count, int epoch, cudaStream_t s) {
+  const int64_t tot = n0 + n1;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((tot + 1023) / 1024, 296)));
+  copy_slices_publish_kernel<<<grid, 256, 0, s>>>(src, dst, a0, n0, a1, n1, flag, count, epoch);
   SAIT_LAUNCHED();
 }
 

@@ -598,8 +598,10 @@ class PeerShardedPair:
         self._spmv(1, epoch, z_local, s)
 
     def _native_pair(self):
-        """The data path as one native object (sait_peer_pair_*): the copy,
-        the two publishes and the two halo SpMVs of an apply in one call."""
+        """The data path as one native object (sait_peer_pair_*).  Creating it
+        synchronises the device, so it must exist before any apply that
+        waits on a peer is queued (distributed() creates it eagerly; ranks
+        living in one process create all of theirs first)."""
         from . import _native as N
 
         if getattr(self, "_pp", None) is None:
@@ -611,6 +613,12 @@ class PeerShardedPair:
                 d.ext[1] = self.bufs[f].ptr + 8 * self._ext_len(f, self.rank)
                 d.flag = self.bufs[f].ptr + self._flag_off(f, self.rank)
                 d.ext_len, d.own_offset, d.own_len = p.ext_len, p.own_offset, self.own[1] - self.own[0]
+                # own rows the neighbours read (at most one range per side)
+                rng = sorted((g0 - self.own[0], g1 - g0) for _, g0, g1 in p.send)
+                if len(rng) > 2:
+                    raise NotImplementedError("PeerShardedPair: own rows read by more than two ranks")
+                rng += [(0, 0)] * (2 - len(rng))
+                (d.send_a0, d.send_n0), (d.send_a1, d.send_n1) = rng
                 for par in range(2):
                     d.halo[par] = self._halo(f, par)
             h = C.c_void_p()
@@ -670,6 +678,7 @@ class PeerShardedPair:
         obj._opened = opened
         _agree(err, "PeerShardedPair", group, cleanup=obj)
         obj.resolve = lambda q, f: obj.bufs[f].ptr if q == rank else opened[(q, f)]
+        obj._native_pair()
         dist.barrier(group=group)
         return obj
 

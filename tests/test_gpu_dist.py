@@ -369,3 +369,67 @@ def test_column_work_matches_host(S):
     cnt = np.bincount(T.col_idx[off], minlength=T.nrows)
     want = np.bincount(T.col_idx[off], weights=(cnt[rows[off]] + 1), minlength=T.nrows).astype(np.int64)
     assert np.array_equal(work.cpu().numpy(), want)
+
+
+_NATIVE_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import torch
+import paper_2106_12836_b200 as S
+from paper_2106_12836_b200.dist import PeerShardedPair
+from helpers import to_oracle
+from oracle import oracle as O
+P = O.get("port")
+world = {world}
+A = S.laplacian_3d(16)
+f = S.ilu_k(A, 0)
+ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
+MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
+ranks = {{}}
+resolve = lambda q, fac: ranks[q].bufs[fac].ptr
+for q in range(world):
+    ranks[q] = PeerShardedPair(ML, MU, q, world, resolve=resolve, align=256)
+for q in range(world):
+    ranks[q]._native_pair()  # created up front: creation synchronises the device (no waiting kernels queued yet)
+streams = [torch.cuda.Stream() for _ in range(world)]
+zs = {{q: torch.empty(ranks[q].own[1] - ranks[q].own[0], dtype=torch.float64, device="cuda") for q in range(world)}}
+torch.cuda.synchronize()
+ok = []
+for epoch in (1, 2, 3, 4):
+    r = S.uniform_pm1(500 + epoch, A.nrows)
+    want = P.pair_apply(to_oracle(ML), to_oracle(MU), r)
+    rd = torch.from_numpy(r).cuda()
+    torch.cuda.synchronize()
+    # nothing but the applies between here and the synchronize below: an
+    # allocation or any call that synchronises the device would wait for
+    # rank 0's kernels, which wait for rank 1's, which are not queued yet
+    for q in range(world):
+        a, b = ranks[q].own
+        with torch.cuda.stream(streams[q]):
+            ranks[q].apply(rd[a:b], zs[q])
+    torch.cuda.synchronize()
+    z = torch.cat([zs[q] for q in range(world)]).cpu().numpy()
+    ok.append(int(np.array_equal(z.view(np.uint64), want.view(np.uint64))))
+print(*ok)
+for q in range(world):
+    ranks[q].close()
+"""
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_native_peer_pair_concurrent_virtual_ranks(world):
+    """The native peer-halo pair (sait_peer_pair_apply: boundary-slice copy +
+    publish kernel, M_L reading its own x from r and publishing flag_U from
+    its last CTA, M_U as a programmatic dependent) with `world` virtual ranks
+    on one GPU, each on its own stream, so ranks really wait on each other's
+    flags.  A 16^3 problem keeps every grid small enough (tens of CTAs) that
+    all ranks' kernels are resident together; the child process is bounded
+    by a timeout.  Four epochs (both parities twice) equal the oracle."""
+    import subprocess
+    import sys
+
+    code = _NATIVE_CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"), world=world)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert out.stdout.split() == ["1", "1", "1", "1"]

@@ -116,6 +116,18 @@ def test_config5_full_size(S):
     dA, pair = _factors_and_pair(S, A, fx, 5e-2, 3)
     n = A.nrows
     assert [pair.factor_format(w)["format"] for w in (0, 1)] == ["sell32_dict", "sell32_dict"]
+    # the 8-GPU row-sharded apply of north_star: every rank's halo comes from
+    # ONE neighbour per side (PeerShardedPair's precondition) for both factors
+    from paper_2106_12836_b200.dist import column_span, make_plans, row_bounds
+
+    rb = row_bounds(n, 8)
+    for M in (pair.lower_inverse(), pair.upper_inverse()):
+        plans = make_plans([column_span(M.row_ptr, M.col_idx, rb[q], rb[q + 1]) for q in range(8)], rb)
+        for p in plans:
+            below = [x for x in p.recv if x[2] <= p.own[0]]
+            above = [x for x in p.recv if x[1] >= p.own[1]]
+            assert len(below) <= 1 and len(above) <= 1
+            assert all(g1 - g0 <= rb[1] for _, g0, g1 in p.recv)  # well inside one neighbour's rows
     blk = fx["apply_block8"]
     R = torch.stack([torch.from_numpy(S.uniform_pm1(s, n)) for s in blk["seeds"]]).cuda()  # (8, n) = column-major
     Z = torch.empty_like(R)

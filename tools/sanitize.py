@@ -8,8 +8,7 @@ silent corruption also fails.
     compute-sanitizer --tool memcheck python tools/sanitize.py
     compute-sanitizer --tool racecheck python tools/sanitize.py
 
-(compute-sanitizer is disabled on this round's GPU pool; the workload still
-runs as an oracle-checked sweep of every device path: python tools/sanitize.py)
+Summaries of the round-2 runs: profiles/r02_sanitizer.txt.
 """
 import os
 import sys
@@ -66,6 +65,22 @@ Z = pair.apply_block(R)
 check(bitwise_equal(np.asfortranarray(Z).ravel(order="F"),
                     np.asfortranarray(P.pair_apply_block(ML, MU, R)).ravel(order="F")), "apply: block of 8")
 
+for fmt in ("csr", "sell32_int32", "sell32_int16", "sell32_dict"):
+    pf = S.SaitPairPreconditioner(to_product(ML), to_product(MU), format=fmt)
+    zf = torch.empty_like(rd)
+    pf.apply(rd, zf)
+    torch.cuda.synchronize()
+    check(bitwise_equal(zf.cpu().numpy(), want), f"apply: format {fmt}")
+    del pf
+Md = S.DeviceCsr.upload(to_product(ML))
+Xb = torch.from_numpy(np.asfortranarray(R).ravel(order="F").copy()).cuda()
+Yb = torch.empty(A.nrows * 8, dtype=torch.float64, device="cuda")
+from paper_2106_12836_b200 import _native as NN  # noqa: E402
+
+NN.check(NN.lib.sait_spmm(Md.handle, Xb.data_ptr(), Yb.data_ptr(), 8, None))
+torch.cuda.synchronize()
+check(bitwise_equal(Yb.cpu().numpy(), np.concatenate([P.spmv(ML, R[:, c]) for c in range(8)])), "spmm (block of 8)")
+
 # solvers
 b = O.uniform_pm1(4, A.nrows)
 xo, so = O.pcg(A, ML, MU, b, 1e-10, 300)
@@ -109,4 +124,41 @@ for q in range(3):
     zs.append(zq)
 torch.cuda.synchronize()
 check(bitwise_equal(torch.cat(zs).cpu().numpy(), want), "peer-halo pair, 3 virtual ranks")
+for q in range(3):
+    ranks[q].close()
+
+# column-sharded build of 3 virtual ranks -> device redistribution to row blocks
+import ctypes as C  # noqa: E402
+
+from paper_2106_12836_b200.dist import column_bounds_by_work, redistribute_local, row_bounds  # noqa: E402
+
+dL = S.DeviceCsr.upload(to_product(L))
+cb = column_bounds_by_work(dL, 3)
+spec = NN.DropSpec(NN.SAIT_DROP_THRESHOLD, 5e-2, 3, 0, 0, 0.0)
+sess = []
+for q in range(3):
+    h = C.c_void_p()
+    NN.check(NN.lib.sait_build_session_create(dL.handle, 1, C.byref(spec), cb[q], cb[q + 1], None, C.byref(h)))
+    sess.append(h)
+while NN.lib.sait_build_session_remaining(sess[0]) > 0:
+    fl = []
+    for h in sess:
+        ch = C.c_int(1)
+        NN.check(NN.lib.sait_build_session_step(h, C.byref(ch)))
+        fl.append(ch.value)
+    if max(fl) == 0:
+        for h in sess:
+            NN.check(NN.lib.sait_build_session_stop(h))
+blocks = []
+for h in sess:
+    out = C.c_void_p()
+    NN.check(NN.lib.sait_build_session_finish(h, 0, C.byref(out), None))
+    NN.lib.sait_build_session_destroy(h)
+    blocks.append(S.DeviceCsr(out.value))
+rb = row_bounds(A.nrows, 3)
+rows = redistribute_local(blocks, cb, rb)
+got = [rows[q].to_host() for q in range(3)]
+okr = all(np.array_equal(got[q].col_idx, ML.col_idx[ML.row_ptr[rb[q]]:ML.row_ptr[rb[q + 1]]]) and
+          bitwise_equal(got[q].values, ML.values[ML.row_ptr[rb[q]]:ML.row_ptr[rb[q + 1]]]) for q in range(3))
+check(okr, "column-sharded build -> row blocks (3 virtual ranks)")
 print("SANITIZE WORKLOAD DONE")

@@ -43,7 +43,11 @@ constexpr int kFirstSmemBin = kTinyBins;
 constexpr int kNumSmemBins = 7;
 constexpr int kMinLogSlots = 6;
 constexpr int kGlobalBin = kFirstSmemBin + kNumSmemBins;
-constexpr int kNumBins = kGlobalBin + 1;
+// window bins: rows whose product columns all fall in [base, base + 1024 R)
+// (R = 1, 2), accumulated by direct addressing instead of hashing (below)
+constexpr int kWinBin1 = kGlobalBin + 1;
+constexpr int kWinBin2 = kGlobalBin + 2;
+constexpr int kNumBins = kGlobalBin + 3;
 constexpr int kTinyG[kTinyBins] = {8, 16, 32};
 
 struct Args {
@@ -108,11 +112,36 @@ __device__ __forceinline__ bool in_pattern(const int32_t* __restrict__ pci, int3
   return false;
 }
 
-// Accumulates row j of A*B (+I) into the table (key/val, `slots` = 2^logs).
-__device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* val, int logs,
-                               WarpStage* st, int lane) {
-  const int slots = 1 << logs, mask = slots - 1, shift = 32 - logs;
-  for (int s = lane; s < slots; s += 32) key[s] = kEmpty;
+// Where a row's entries accumulate: an open-addressing hash table of 2^logs
+// slots, or (window rows) a direct-addressed window of columns
+// [base, base + 32 * words) with an occupancy bitmap.  insert returns the
+// slot, | kFresh when the column was absent (the first product is assigned).
+struct HashTable {
+  int32_t* key;
+  int logs;
+  __device__ void clear(int lane) const {
+    for (int s = lane; s < (1 << logs); s += 32) key[s] = kEmpty;
+  }
+  __device__ int insert(int32_t col) const { return find_or_insert(key, (1 << logs) - 1, 32 - logs, col); }
+};
+struct WindowTable {
+  uint32_t* bits;
+  int32_t base;
+  int words;
+  __device__ void clear(int lane) const {
+    for (int w = lane; w < words; w += 32) bits[w] = 0u;
+  }
+  __device__ int insert(int32_t col) const {
+    const int s = col - base;
+    const uint32_t b = 1u << (s & 31);
+    return (atomicOr(&bits[s >> 5], b) & b) ? s : (s | kFresh);
+  }
+};
+
+// Accumulates row j of A*B (+I) into the table.
+template <class TABLE>
+__device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, double* val, WarpStage* st, int lane) {
+  tab.clear(lane);
   __syncwarp();
   const int32_t a0 = g.arp[j], a1 = g.arp[j + 1];
   for (int32_t ab = a0; ab < a1; ab += 32) {
@@ -177,7 +206,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
       const unsigned grp = __match_any_sync(0xffffffffu, col);
       __syncwarp();
       if (act && (__ffs(grp) - 1) == lane) {
-        const int hs = find_or_insert(key, mask, shift, col);
+        const int hs = tab.insert(col);
         const int s = hs & ~kFresh;
         double acc = (hs & kFresh) ? prod : __dadd_rn(val[s], prod);
         unsigned rest = grp & (grp - 1);  // later lanes = later k
@@ -192,7 +221,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, int32_t* key, double* v
     }
   }
   if (g.epi.add_identity && lane == 0) {
-    const int hs = find_or_insert(key, mask, shift, j + static_cast<int32_t>(g.epi.diag_offset));
+    const int hs = tab.insert(j + static_cast<int32_t>(g.epi.diag_offset));
     const int s = hs & ~kFresh;
     val[s] = (hs & kFresh) ? 1.0 : __dadd_rn(val[s], 1.0);
   }
@@ -353,7 +382,7 @@ __device__ __forceinline__ void compare_row(const Args& g, int32_t j, const int3
 __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val, int logs, WarpStage* st,
                             int lane, bool numeric) {
   if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
-  accumulate_row(g, j, key, val, logs, st, lane);
+  accumulate_row(g, j, HashTable{key, logs}, val, st, lane);
   const int live = drop_compact(g, j, key, val, logs, lane);
   const bool narrow = g.ncols < (int64_t{1} << 26);
   if (!numeric) {
@@ -380,6 +409,172 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
     g.cv[out + s] = g.epi.out_scale ? __dmul_rn(val[s], g.epi.out_scale[key[s]]) : val[s];
   }
   if (g.epi.qrp) compare_row(g, j, key, val, live, lane);
+  __syncwarp();
+}
+
+// Window rows (bins kWinBin1/2): every product column of row j lies in
+// [base, base + 1024 R), so the row accumulates by direct addressing -- one
+// atomicOr on an occupancy bitmap per new column instead of hash probing and
+// table clearing -- and its entries come out of the bitmap already in column
+// order (no sort).  Lane l owns bitmap words l, l + 32, ... (R words): it
+// tests its occupied slots against the drop rule, the survivors are counted
+// per lane and placed by a warp exclusive scan in (word, bit) order = column
+// order, and written straight to the staging area (count pass) or the final
+// row (numeric pass, with the early-stop compare on the fly).  Same products,
+// same order of adds per column: bitwise the hash path.
+template <int R>
+__device__ __forceinline__ void window_survivors(const Args& g, int32_t j, const uint32_t* bits, const double* val,
+                                                 int32_t base, int lane, uint32_t (&keep)[R]) {
+  const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
+  const int drop = g.epi.drop;
+  const bool thr = (drop == 1 || drop == 3) && g.epi.tau != 0.0;
+  int32_t pb = 0, pe = 0;
+  if (drop == 2) {
+    pb = g.epi.prp[j];
+    pe = g.epi.prp[j + 1];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int w = lane + 32 * r;
+    uint32_t m = bits[w], k = 0u;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int32_t col = base + 32 * w + b;
+      bool ok = true;
+      if (thr) ok = (col == jd) || (fabs(val[32 * w + b]) >= g.epi.tau);
+      else if (drop == 2) ok = in_pattern(g.epi.pci, pb, pe, col);
+      if (ok) k |= 1u << b;
+    }
+    keep[r] = k;
+  }
+}
+
+template <int R>
+__device__ void process_row_window(const Args& g, int32_t j, int32_t base, uint32_t* bits, uint32_t* kbits,
+                                   double* val, WarpStage* st, int lane, bool numeric) {
+  if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
+  accumulate_row(g, j, WindowTable{bits, base, 32 * R}, val, st, lane);
+  uint32_t keep[R];
+  window_survivors<R>(g, j, bits, val, base, lane, keep);
+  const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
+  if (g.epi.drop == 3) {  // A15 fill cap: the diagonal + the (cap - 1) largest |v| off-diagonals
+    int off = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int w = lane + 32 * r;
+      off += __popc(keep[r]);
+      const int d = jd - base - 32 * w;
+      if (d >= 0 && d < 32 && ((keep[r] >> d) & 1u)) --off;
+      kbits[w] = keep[r];
+    }
+    off = __reduce_add_sync(0xffffffffu, off);
+    int room = g.epi.cap[jd] - 1;
+    if (room < 0) room = 0;
+    __syncwarp();
+    if (off > room) {  // rank by (|v| desc, column asc) among the kept off-diagonals
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int w = lane + 32 * r;
+        uint32_t m = keep[r], kill = 0u;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          const int32_t col = base + 32 * w + b;
+          if (col == jd) continue;
+          const double mv = fabs(val[32 * w + b]);
+          int rank = 0;
+          for (int q = 0; q < 32 * R; ++q) {
+            uint32_t mq = kbits[q];
+            while (mq) {
+              const int bq = __ffs(mq) - 1;
+              mq &= mq - 1;
+              const int32_t cq = base + 32 * q + bq;
+              if (cq == jd || cq == col) continue;
+              const double vq = fabs(val[32 * q + bq]);
+              rank += (vq > mv) || (vq == mv && cq < col);
+            }
+          }
+          if (rank >= room) kill |= 1u << b;
+        }
+        keep[r] &= ~kill;
+      }
+    }
+    __syncwarp();
+  }
+  // survivors in column order: word-major (word w = lane + 32 r), bit order
+  int cnt[R], pre[R], live = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    cnt[r] = __popc(keep[r]);
+    int incl = cnt[r];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    pre[r] = live + incl - cnt[r];
+    live += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (!numeric) {
+    if (lane == 0) g.ccount[j] = live;
+    if (!g.stage_pos) return;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(g.stage_cursor, static_cast<unsigned long long>(live));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const bool fits = pos + static_cast<unsigned long long>(live) <= static_cast<unsigned long long>(g.stage_cap);
+    if (fits) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int w = lane + 32 * r;
+        uint32_t m = keep[r];
+        int o = pre[r];
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          g.stage_col[pos + o] = base + 32 * w + b;
+          g.stage_val[pos + o] = val[32 * w + b];
+          ++o;
+        }
+      }
+    }
+    if (lane == 0) g.stage_pos[j] = fits ? static_cast<int32_t>(pos) : -1;
+    __syncwarp();
+    return;
+  }
+  const int32_t out = g.crp[j];
+  bool cmp = g.epi.qrp != nullptr, diff = false;
+  int32_t qb = 0;
+  if (cmp) {
+    qb = g.epi.qrp[j];
+    if (g.epi.qrp[j + 1] - qb != live) {
+      diff = true;
+      cmp = false;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int w = lane + 32 * r;
+    uint32_t m = keep[r];
+    int o = pre[r];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int32_t c = base + 32 * w + b;
+      const double v = val[32 * w + b];
+      g.cci[out + o] = c;
+      g.cv[out + o] = g.epi.out_scale ? __dmul_rn(v, g.epi.out_scale[c]) : v;
+      if (cmp) {  // the reference's stabilized() test (sait.cpp:14-28)
+        const double a = g.epi.qv[qb + o];
+        const double fa = fabs(a), fb = fabs(v);
+        const double mx = fa < fb ? fb : fa;
+        if (g.epi.qci[qb + o] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx)) diff = true;
+      }
+      ++o;
+    }
+  }
+  if (__any_sync(0xffffffffu, diff) && lane == 0 && *reinterpret_cast<volatile int*>(g.changed) == 0)
+    atomicOr(g.changed, 1);
   __syncwarp();
 }
 
@@ -461,6 +656,28 @@ __global__ void __launch_bounds__(256) spgemm_smem(Args g, const int32_t* __rest
   const int warps = blockDim.x >> 5;
   for (int32_t r = blockIdx.x * warps + w; r < nrows_bin; r += gridDim.x * warps)
     process_row(g, rows[r], key, val, LOGS, st, lane, numeric);
+}
+
+__host__ __device__ constexpr int window_smem_per_warp(int R) {
+  return (1024 * R * 8 + 2 * 32 * R * 4 + static_cast<int>(sizeof(WarpStage)) + 15) / 16 * 16;
+}
+constexpr int window_warps(int R) { return R == 1 ? 8 : 4; }
+
+template <int R>
+__global__ void __launch_bounds__(256) spgemm_window(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+                                                     const int32_t* __restrict__ wbase, bool numeric) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* mine = smem + w * window_smem_per_warp(R);
+  double* val = reinterpret_cast<double*>(mine);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(mine + 1024 * R * 8);
+  uint32_t* kbits = bits + 32 * R;
+  WarpStage* st = reinterpret_cast<WarpStage*>(kbits + 32 * R);
+  const int warps = blockDim.x >> 5;
+  for (int32_t r = blockIdx.x * warps + w; r < nrows_bin; r += gridDim.x * warps) {
+    const int32_t j = rows[r];
+    process_row_window<R>(g, j, wbase[j], bits, kbits, val, st, lane, numeric);
+  }
 }
 
 // Very long rows: table in global scratch (per-row offsets), one warp per row.
@@ -655,7 +872,8 @@ __global__ void __launch_bounds__(256) spgemm_tiny_emit(Args g, const int32_t* _
 // (warp-aggregated: one shared atomic per warp and bin, one per warp for
 // the total).
 __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restrict__ pcap,
-                          int32_t* __restrict__ hist, unsigned long long* __restrict__ total, int slack_pct) {
+                          int32_t* __restrict__ hist, unsigned long long* __restrict__ total, int slack_pct,
+                          bool win) {
   __shared__ int32_t h[kNumBins];
   __shared__ unsigned long long tsum;
   if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
@@ -667,10 +885,17 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
   int bin = -1;
   if (j < g.n) {
     const int32_t e0 = g.arp[j], e1 = g.arp[j + 1];
+    const int32_t jd = static_cast<int32_t>(j + g.epi.diag_offset);
+    int32_t lo = g.epi.add_identity ? jd : INT32_MAX, hi = g.epi.add_identity ? jd : -1;
 #pragma unroll 4
     for (int32_t e = e0; e < e1; ++e) {
       const int32_t k = g.aci[e];
-      p += g.brp[k + 1] - g.brp[k];
+      const int32_t b0 = g.brp[k], b1 = g.brp[k + 1];
+      p += b1 - b0;
+      if (win && b1 > b0) {
+        lo = min(lo, g.bci[b0]);
+        hi = max(hi, g.bci[b1 - 1]);
+      }
     }
     int64_t distinct = (p < g.ncols ? p : g.ncols) + 1;  // +1: the identity entry
     int logs = kMinLogSlots;
@@ -680,9 +905,15 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     bin = kFirstSmemBin + logs - kMinLogSlots;
     if (bin > kGlobalBin) bin = kGlobalBin;
     const int32_t m = e1 - e0;
+    bool windowed = false;
+    if (win && logs >= 8 && hi >= lo) {  // big hash rows whose columns span < 1024 / 2048
+      const int32_t span = hi - lo;
+      if (span < 1024) bin = kWinBin1, windowed = true;
+      else if (span < 2048) bin = kWinBin2, windowed = true;
+    }
     if (p < 32 && m <= 32) bin = (p < 8 && m <= 8) ? 0 : (p < 16 && m <= 16) ? 1 : 2;
     bin_of[j] = static_cast<int8_t>(bin);
-    pcap[j] = logs;  // table log2 size (used by the global bin)
+    pcap[j] = windowed ? lo : logs;  // window rows: the window's first column; else the table log2 size
   }
   unsigned long long ps = static_cast<unsigned long long>(p);
   unsigned long long ph = bin >= kFirstSmemBin ? ps : 0ull;  // products of hash-table rows
@@ -842,6 +1073,7 @@ struct Plan {
   // tiny rows: G-entry staging slot per row, per tiny bin
   int32_t* tcol[kTinyBins] = {};
   double* tval[kTinyBins] = {};
+  const int32_t* wbase = nullptr;  // window rows: first column of the window
 };
 
 void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bool recompute = true,
@@ -874,7 +1106,7 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     SAIT_LAUNCHED();
   }
   if (numeric && g.stage_pos) {  // staged hash-table rows: one copy kernel over all of them
-    const int32_t cnt = pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin];
+    const int32_t cnt = pl.start[kNumBins] - pl.start[kFirstSmemBin];
     if (cnt) {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 31) / 32, int64_t{num_sms()} * 8 * 16));
       spgemm_stage_emit<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kFirstSmemBin], cnt);
@@ -894,6 +1126,22 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     int64_t want = (cnt + warps - 1) / warps;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, int64_t{num_sms()} * blocks_per_sm * 4));
     k<<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, numeric);
+    SAIT_LAUNCHED();
+  }
+  for (int b = kWinBin1; b <= kWinBin2; ++b) {
+    const int32_t cnt = pl.hist[b];
+    if (!cnt) continue;
+    const int R = b == kWinBin1 ? 1 : 2;
+    const int warps = window_warps(R);
+    const int smem = warps * window_smem_per_warp(R);
+    const void* k = R == 1 ? reinterpret_cast<const void*>(spgemm_window<1>)
+                           : reinterpret_cast<const void*>(spgemm_window<2>);
+    if (first_on_device(k)) SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int blocks_per_sm = std::max(1, (228 * 1024) / (smem + 1024));
+    const unsigned grid = static_cast<unsigned>(
+        std::min<int64_t>((cnt + warps - 1) / warps, int64_t{num_sms()} * blocks_per_sm * 4));
+    if (R == 1) spgemm_window<1><<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, pl.wbase, numeric);
+    else spgemm_window<2><<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, pl.wbase, numeric);
     SAIT_LAUNCHED();
   }
   int32_t gc = pl.hist[kGlobalBin];
@@ -1023,7 +1271,11 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
     const char* e = std::getenv("SAIT_HASH_SLACK");  // table slots per possible distinct column, in %
     return e ? std::max(101, std::atoi(e)) : 140;
   }();
-  plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total, slack_pct);
+  static const bool window_on = [] {  // SAIT_SPGEMM_WINDOW=0: hash tables only
+    const char* e = std::getenv("SAIT_SPGEMM_WINDOW");
+    return !(e && std::atoi(e) == 0);
+  }();
+  plan_rows<<<grid_for(n, 256), 256, 0, s>>>(g, bin_of, logs_of, hist, total, slack_pct, window_on);
   SAIT_LAUNCHED();
   unsigned long long htot[2] = {0, 0};
   read_back(s, {{pl.hist, hist, sizeof pl.hist}, {htot, total, sizeof htot}});
@@ -1031,6 +1283,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   res.products = static_cast<int64_t>(htotal);
   for (int b2 = 0; b2 < kNumBins; ++b2) pl.start[b2 + 1] = pl.start[b2] + pl.hist[b2];
   pl.lists = dalloc<int32_t>(n, s);
+  pl.wbase = logs_of;
   int32_t* cursor = hist + kNumBins;
   SAIT_CUDA(cudaMemcpyAsync(cursor, pl.start, kNumBins * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   for (int tb = 0; tb < kTinyBins; ++tb)
@@ -1043,7 +1296,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
     return e ? std::atoi(e) : 2;
   }();
   const bool ordered =
-      order_mode == 1 || (order_mode == 2 && pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin] > 0);
+      order_mode == 1 || (order_mode == 2 && pl.start[kNumBins] - pl.start[kFirstSmemBin] > 0);
   if (ordered) {
     const int64_t nblk = (n + kOrdRows - 1) / kOrdRows;
     int32_t* bc = dalloc<int32_t>(kNumBins * nblk, s);
@@ -1087,7 +1340,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   // ---- count pass (hash-table rows staged), scan, numeric pass
   int32_t* counts = dalloc<int32_t>(n, s);
   g.ccount = counts;
-  const int32_t hashed = pl.start[kGlobalBin + 1] - pl.start[kFirstSmemBin];
+  const int32_t hashed = pl.start[kNumBins] - pl.start[kFirstSmemBin];
   if (hashed && !std::getenv("SAIT_SPGEMM_NOSTAGE")) {
     // survivors of a row <= its products + 1; the staging area is sized from
     // the A operand (the previous iterate) and capped, rows beyond it fall

@@ -162,9 +162,15 @@ from oracle import oracle as O
 P = O.get("port")
 T = O.synthetic_lower(20000, 15, 0.01, seed=4)
 Tp = S.CsrMatrix(T.nrows, T.ncols, T.row_ptr, T.col_idx, T.values)
-for tau, k in ((1e-2, 3), (0.0, 3)):
-    want = P.sait_thr(T, True, tau, k)
-    got = S.sait_thr(Tp, S.lower_triangular, S.SaitThrParams(tau, k))
+Tu = P.transpose(T)
+Tup = S.CsrMatrix(Tu.nrows, Tu.ncols, Tu.row_ptr, Tu.col_idx, Tu.values)
+cases = [(lambda: P.sait_thr(T, True, 1e-2, 3), lambda: S.sait_thr(Tp, S.lower_triangular, S.SaitThrParams(1e-2, 3))),
+         (lambda: P.sait_thr(T, True, 0.0, 3), lambda: S.sait_thr(Tp, S.lower_triangular, S.SaitThrParams(0.0, 3))),
+         (lambda: P.sait_thr_cap(T, True, 1e-2, 3, 1.0),
+          lambda: S.sait_thr_cap(Tp, S.lower_triangular, S.SaitThrParams(1e-2, 3), 1.0)),
+         (lambda: P.sait_thr(Tu, False, 1e-2, 3), lambda: S.sait_thr(Tup, S.upper_triangular, S.SaitThrParams(1e-2, 3)))]
+for ref, dev in cases:
+    want, got = ref(), dev()
     ok = (np.array_equal(got.row_ptr, want.row_ptr) and np.array_equal(got.col_idx, want.col_idx)
           and np.array_equal(got.values.view(np.uint64), want.values.view(np.uint64)))
     print(int(ok))
@@ -201,20 +207,22 @@ def test_sait_polynomial_stored_diagonal(S, ref, golden, case, steps):
     assert bitwise_equal_csr(got, want)
 
 
+@pytest.mark.parametrize("window", ["0", "1"])
 @pytest.mark.parametrize("column_form", ["0", "1"])
 @pytest.mark.parametrize("cap", ["none", "0", "1000", "200000"])
-def test_hash_rows_staging_and_overflow(cap, column_form):
-    """Hash-table rows (hundreds of products) stage their sorted survivors in
-    the count pass; rows past the staging capacity are recomputed in the
-    numeric pass.  Every split (all staged, none, a few, most) gives the
-    oracle's bits."""
+def test_hash_rows_staging_and_overflow(cap, column_form, window):
+    """Hash-table and window rows (hundreds of products) stage their sorted
+    survivors in the count pass; rows past the staging capacity are
+    recomputed in the numeric pass.  Every split (all staged, none, a few,
+    most) gives the oracle's bits, with the direct-addressed window rows on
+    (default) or off (SAIT_SPGEMM_WINDOW=0: hash tables only)."""
     import os
     import subprocess
     import sys
 
     from conftest import ROOT
 
-    env = dict(os.environ, SAIT_BUILD_COLUMN_FORM=column_form)
+    env = dict(os.environ, SAIT_BUILD_COLUMN_FORM=column_form, SAIT_SPGEMM_WINDOW=window)
     if cap == "none":
         env["SAIT_SPGEMM_NOSTAGE"] = "1"
     else:
@@ -222,7 +230,7 @@ def test_hash_rows_staging_and_overflow(cap, column_form):
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.split() == ["1", "1"]
+    assert out.stdout.split() == ["1", "1", "1", "1"]
 
 
 @pytest.mark.parametrize("column_form", ["0", "1"])
@@ -242,7 +250,7 @@ def test_hash_table_load_factors(slack, column_form):
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.split() == ["1", "1"]
+    assert out.stdout.split() == ["1", "1", "1", "1"]
 
 
 def test_build_pair_concurrent_equals_separate(S, port):

@@ -23,7 +23,7 @@ HEADERS := include/sait_c.h $(wildcard $(CSRC)/*.cuh)
 SHIM_SRCS := $(wildcard $(CSRC)/shim/*.cpp)
 SHIM_HDRS := $(wildcard include/saitprec/*.hpp)
 
-all: $(PKG)/libsait_b200.so shim $(BUILD)/shim_check oracle
+all: $(PKG)/libsait_b200.so shim $(BUILD)/shim_check oracle checked
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HEADERS)
 	@mkdir -p $(BUILD)
@@ -48,11 +48,25 @@ $(BUILD)/shim_check: tests/cpp/shim_check.cpp $(PKG)/libsaitprec_b200.so $(SHIM_
 	@mkdir -p $(BUILD)
 	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lsaitprec_b200 -lsait_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
+# the bounds-checked build (SAIT_DEVICE_CHECKS: device index range checks
+# that print and trap), loaded with SAIT_CHECKED=1 -- the stand-in for
+# compute-sanitizer on a pool that does not allow it (tools/sanitize.py)
+CHECKED := $(PKG)/checked
+checked: $(CHECKED)/libsait_b200.so
+
+$(BUILD)/checked/%.o: $(CSRC)/%.cu $(HEADERS)
+	@mkdir -p $(BUILD)/checked
+	$(NVCC) $(NVFLAGS) -DSAIT_DEVICE_CHECKS -c -o $@ $<
+
+$(CHECKED)/libsait_b200.so: $(addprefix $(BUILD)/checked/,$(addsuffix .o,$(CU_SRCS))) $(HOST_OBJS)
+	@mkdir -p $(CHECKED)
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $^ -cudart static -lgomp
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf $(BUILD) $(PKG)/*.so
+	rm -rf $(BUILD) $(PKG)/*.so $(CHECKED)
 	$(MAKE) -C oracle clean
 
-.PHONY: all shim oracle clean
+.PHONY: all shim oracle clean checked

@@ -9,7 +9,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsait_b200.so")
+# SAIT_CHECKED=1 loads the bounds-checked build (make checked: every device
+# index the kernels derive is range-checked and traps with a message) --
+# the stand-in for compute-sanitizer, which this GPU pool does not allow.
+LIB_PATH = os.path.join(HERE, "checked" if os.environ.get("SAIT_CHECKED") == "1" else "", "libsait_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

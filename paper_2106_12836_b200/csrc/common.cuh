@@ -46,6 +46,24 @@ extern std::atomic<int64_t> g_launches;
 
 inline cudaStream_t as_stream(sait_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Device-side range checks of derived indices, compiled in by `make checked`
+// (-DSAIT_DEVICE_CHECKS): a failed check prints where and traps.  No-ops in
+// the production build.
+#ifdef SAIT_DEVICE_CHECKS
+#define SAIT_DCHECK(cond, what, v, lim)                                                                   \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("SAIT_DCHECK failed: %s (%lld vs %lld) at %s:%d block %d thread %d\n", what,                 \
+             static_cast<long long>(v), static_cast<long long>(lim), __FILE__, __LINE__, blockIdx.x, threadIdx.x); \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define SAIT_DCHECK(cond, what, v, lim) \
+  do {                                  \
+  } while (0)
+#endif
+
 // Device CSR: int32 indices, fp64 values (values may be null for a pattern).
 struct DevCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;

@@ -131,6 +131,7 @@ __global__ void scatter_transpose(int64_t nrows, const int32_t* __restrict__ rp,
   const double s = scale ? scale[i] : 1.0;
   for (int32_t e = rp[i] + lane; e < rp[i + 1]; e += L) {
     const int32_t pos = atomicAdd(&cursor[ci[e]], 1);
+    SAIT_DCHECK(pos >= 0 && pos < rp[nrows], "transpose scatter position", pos, rp[nrows]);
     oci[pos] = static_cast<int32_t>(i);
     if (v) ov[pos] = scale ? __dmul_rn(v[e], s) : v[e];
   }
@@ -485,6 +486,7 @@ __global__ void assemble_copy(int64_t nrows, int nparts, const sait_row_piece* _
     }
     o += e - b;
   }
+  SAIT_DCHECK(o == rp[i + 1], "assembled row length", o, rp[i + 1]);
 }
 
 __global__ void col_minmax(int64_t nnz, const int32_t* __restrict__ ci, int* __restrict__ mm) {

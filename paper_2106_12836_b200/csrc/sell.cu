@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
       if (k0 + j < w) {
         c[j] = idx.col(i0 + static_cast<int64_t>(k0 + j) * kSlice, row);
         v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
+        SAIT_DCHECK(c[j] >= -1, "sell column", c[j], -1);
       }
     }
     if (PDL_WAIT && k0 == 0) pdl_wait();  // x is the previous grid's output
@@ -395,7 +396,7 @@ __device__ __forceinline__ void publish_when_grid_done(int* flag, unsigned* coun
 }
 
 template <class IDX, bool PDL>
-__global__ void __launch_bounds__(256, 5) sell_spmv_halo_kernel(int64_t n, int64_t s_begin, int64_t s_end,
+__global__ void __launch_bounds__(256) sell_spmv_halo_kernel(int64_t n, int64_t s_begin, int64_t s_end,
                                                               const int64_t* __restrict__ soff, IDX idx,
                                                               const double* __restrict__ sval,
                                                               const double* __restrict__ x, double* __restrict__ y,
@@ -424,6 +425,8 @@ __global__ void __launch_bounds__(256, 5) sell_spmv_halo_kernel(int64_t n, int64
           v[j] = ld_na(sval + e0 + static_cast<int64_t>(k0 + j) * kSlice);
           lo |= c[j] >= 0 && c[j] < h.own_lo;
           hi |= c[j] >= h.own_hi;
+          SAIT_DCHECK(c[j] < 0 || c[j] >= h.own_hi || c[j] >= h.own_lo || c[j] + h.lo_shift >= 0, "halo lo index",
+                      c[j] + h.lo_shift, 0);
         }
       }
       if (PDL && k0 == 0) pdl_wait();  // the own x is the previous grid's output

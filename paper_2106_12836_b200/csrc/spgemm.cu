@@ -133,6 +133,7 @@ struct WindowTable {
   }
   __device__ int insert(int32_t col) const {
     const int s = col - base;
+    SAIT_DCHECK(s >= 0 && s < 32 * words, "spgemm window slot", s, 32 * words);
     const uint32_t b = 1u << (s & 31);
     return (atomicOr(&bits[s >> 5], b) & b) ? s : (s | kFresh);
   }
@@ -188,6 +189,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, doubl
       b = 0.0;
       if (p < total) {
         const int r = r0 + __popc(starts & ((2u << lane) - 1u));
+        SAIT_DCHECK(r >= 0 && r < 32 && p >= st->off[r], "spgemm product owner", r, 32);
         const int32_t bi = st->bstart[r] + (p - st->off[r]);
         c = g.bci[bi];
         a = st->aval[r];
@@ -833,6 +835,7 @@ __device__ __forceinline__ void tiny_row(const Args& g, const TinyFetch& f, int 
     if (lane == 0) g.ccount[j] = __popc(km);
     if (keep) {
       const int pos = __popc(km & ((1u << lane) - 1u));
+      SAIT_DCHECK(pos < G, "spgemm tiny staging slot", pos, G);
       tcol[slot * G + pos] = col;
       tval[slot * G + pos] = acc;
     }

@@ -7,6 +7,7 @@ silent corruption also fails.
 
     compute-sanitizer --tool memcheck python tools/sanitize.py
     compute-sanitizer --tool racecheck python tools/sanitize.py
+    SAIT_CHECKED=1 python tools/sanitize.py   # the bounds-checked build (make checked)
 
 Summaries of the round-2 runs: profiles/r02_sanitizer.txt.
 """

@@ -11,7 +11,7 @@ BUILD := build
 # sm_100a only.  --fmad=false + explicit __dmul_rn/__dadd_rn: every product is
 # rounded before it is added, as in the reference (no FMA contraction).
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC,-ffp-contract=off,-Wall \
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC,-ffp-contract=off,-Wall,-fopenmp \
            -Iinclude -I$(CSRC) -Xptxas -warn-spills
 CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Iinclude -I/usr/local/cuda/include
 

@@ -163,9 +163,18 @@ class DeviceCsr:
         return nz.value
 
     def to_host(self, stream=None) -> CsrMatrix:
-        c = N.HostCsr()
-        N.check(N.lib.sait_csr_to_host(self._h, _stream_handle(stream), C.byref(c)))
-        return _from_c(c)
+        """Download into freshly allocated int64 / fp64 arrays (sait_csr_download:
+        pinned, chunked, widened on the host cores)."""
+        nz = self.nnz()
+        vp = C.c_void_p()
+        N.check(N.lib.sait_csr_device_arrays(self._h, None, None, C.byref(vp)))
+        rp = np.empty(self.nrows + 1, dtype=np.int64)
+        ci = np.empty(nz, dtype=np.int64)
+        vals = np.empty(nz, dtype=np.float64) if vp.value else None
+        N.check(N.lib.sait_csr_download(self._h, rp.ctypes.data_as(N.P64), ci.ctypes.data_as(N.P64),
+                                        vals.ctypes.data_as(N.PD) if vals is not None else N.PD(),
+                                        _stream_handle(stream)))
+        return CsrMatrix(self.nrows, self.ncols, rp, ci, vals)
 
     def device_arrays(self):
         """(row_ptr, col_idx, values) device pointers (int32, int32, fp64)."""

@@ -201,6 +201,90 @@ void host_csr_alloc(sait_host_csr* out, int64_t nrows, int64_t ncols, int64_t nn
   if (!out->row_ptr || !out->col_idx || (values && !out->values)) throw std::bad_alloc();
 }
 
+// Host <-> device CSR transfers (the drop-in API takes and returns int64 /
+// fp64 host matrices, csr.hpp:24-43): chunked through two pinned staging
+// buffers per device, so the PCIe copy of one chunk overlaps the host-side
+// narrowing (int64 -> int32, out-of-range indices -> -1, which validation
+// then reports) / widening / copying of the next, which runs on all host
+// cores (OpenMP).  Pageable copies go through the driver's own staging at a
+// few GB/s and fault in fresh pages one by one; this moves 4 of the 12 bytes
+// of an index as int32 across the bus and touches the user's pages in
+// parallel.
+namespace {
+constexpr size_t kStageBytes = size_t{32} << 20;
+struct Staging {
+  std::mutex mu;
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+};
+Staging& staging() {
+  static Staging st[64];
+  int dev = 0;
+  SAIT_CUDA(cudaGetDevice(&dev));
+  Staging& x = st[dev & 63];
+  if (!x.buf[0]) {
+    for (int b = 0; b < 2; ++b) {
+      SAIT_CUDA(cudaMallocHost(&x.buf[b], kStageBytes));
+      SAIT_CUDA(cudaEventCreateWithFlags(&x.done[b], cudaEventDisableTiming));
+    }
+  }
+  return x;
+}
+// dev_dst[0, count) <- fill(pinned, first, n) chunk by chunk
+template <class Fill>
+void staged_h2d(Staging& st, char* dev_dst, int64_t count, size_t elem, Fill fill, cudaStream_t s) {
+  const int64_t per = static_cast<int64_t>(kStageBytes / elem);
+  int k = 0;
+  for (int64_t c = 0; c < count; c += per, ++k) {
+    const int b = k & 1;
+    const int64_t n = std::min(per, count - c);
+    SAIT_CUDA(cudaEventSynchronize(st.done[b]));  // the copy that last read this buffer
+    fill(st.buf[b], c, n);
+    SAIT_CUDA(cudaMemcpyAsync(dev_dst + c * elem, st.buf[b], n * elem, cudaMemcpyHostToDevice, s));
+    SAIT_CUDA(cudaEventRecord(st.done[b], s));
+  }
+}
+// drain(pinned, first, n) <- dev_src[0, count) chunk by chunk (the D2H of the
+// next chunk is in flight while the host drains this one)
+template <class Drain>
+void staged_d2h(Staging& st, const char* dev_src, int64_t count, size_t elem, Drain drain, cudaStream_t s) {
+  const int64_t per = static_cast<int64_t>(kStageBytes / elem);
+  const int64_t chunks = (count + per - 1) / per;
+  auto issue = [&](int64_t k) {
+    const int b = static_cast<int>(k & 1);
+    const int64_t c = k * per, n = std::min(per, count - c);
+    SAIT_CUDA(cudaMemcpyAsync(st.buf[b], dev_src + c * elem, n * elem, cudaMemcpyDeviceToHost, s));
+    SAIT_CUDA(cudaEventRecord(st.done[b], s));
+  };
+  if (chunks > 0) issue(0);
+  for (int64_t k = 0; k < chunks; ++k) {
+    if (k + 1 < chunks) issue(k + 1);  // its buffer was drained two iterations ago
+    const int b = static_cast<int>(k & 1);
+    SAIT_CUDA(cudaEventSynchronize(st.done[b]));
+    const int64_t c = k * per, n = std::min(per, count - c);
+    drain(st.buf[b], c, n);
+  }
+}
+void narrow_host(const int64_t* in, char* out, int64_t n) {
+  int32_t* o = reinterpret_cast<int32_t*>(out);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) o[i] = (in[i] < 0 || in[i] > INT32_MAX) ? -1 : static_cast<int32_t>(in[i]);
+}
+void widen_host(const char* in, int64_t* out, int64_t n) {
+  const int32_t* x = reinterpret_cast<const int32_t*>(in);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = x[i];
+}
+void copy_host(const char* in, char* out, int64_t bytes) {
+  const int64_t nb = (bytes + (1 << 20) - 1) >> 20;
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t o = b << 20;
+    std::memcpy(out + o, in + o, static_cast<size_t>(std::min<int64_t>(int64_t{1} << 20, bytes - o)));
+  }
+}
+}  // namespace
+
 sait::DevCsr upload(const sait_host_csr* m, cudaStream_t s) {
   need(m, "sait_csr_upload");
   if (m->nrows < 0 || m->ncols < 0) sait::throw_invalid("validate: negative dimension");
@@ -219,15 +303,21 @@ sait::DevCsr upload(const sait_host_csr* m, cudaStream_t s) {
   d.rp = sait::dalloc<int32_t>(d.nrows + 1, s);
   d.ci = sait::dalloc<int32_t>(nnz, s);
   d.v = m->values ? sait::dalloc<double>(nnz, s) : nullptr;
-  int64_t* tmp = sait::dalloc<int64_t>(std::max(d.nrows + 1, nnz), s);
-  SAIT_CUDA(cudaMemcpyAsync(tmp, m->row_ptr, sizeof(int64_t) * (d.nrows + 1), cudaMemcpyHostToDevice, s));
-  sait::narrow_indices(tmp, d.rp, d.nrows + 1, s);
-  if (nnz) {
-    SAIT_CUDA(cudaMemcpyAsync(tmp, m->col_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
-    sait::narrow_indices(tmp, d.ci, nnz, s);
-    if (m->values) SAIT_CUDA(cudaMemcpyAsync(d.v, m->values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+  {
+    Staging& st = staging();
+    std::lock_guard<std::mutex> lk(st.mu);
+    staged_h2d(st, reinterpret_cast<char*>(d.rp), d.nrows + 1, 4,
+               [&](char* p, int64_t c, int64_t n) { narrow_host(m->row_ptr + c, p, n); }, s);
+    if (nnz) {
+      staged_h2d(st, reinterpret_cast<char*>(d.ci), nnz, 4,
+                 [&](char* p, int64_t c, int64_t n) { narrow_host(m->col_idx + c, p, n); }, s);
+      if (m->values)
+        staged_h2d(st, reinterpret_cast<char*>(d.v), nnz, 8, [&](char* p, int64_t c, int64_t n) {
+          copy_host(reinterpret_cast<const char*>(m->values + c), p, n * 8);
+        }, s);
+    }
+    for (int b = 0; b < 2; ++b) SAIT_CUDA(cudaEventSynchronize(st.done[b]));  // staging free for the next caller
   }
-  sait::dfree(tmp, s);
   try {
     sait::validate_device_csr(d, s);
   } catch (...) {
@@ -238,17 +328,18 @@ sait::DevCsr upload(const sait_host_csr* m, cudaStream_t s) {
 }
 
 void to_host(const sait::DevCsr& m, cudaStream_t s, int64_t* rp, int64_t* ci, double* v) {
-  int64_t* tmp = sait::dalloc<int64_t>(std::max(m.nrows + 1, m.nnz), s);
-  sait::widen_indices(m.rp, tmp, m.nrows + 1, s);
-  SAIT_CUDA(cudaMemcpyAsync(rp, tmp, sizeof(int64_t) * (m.nrows + 1), cudaMemcpyDeviceToHost, s));
-  SAIT_CUDA(cudaStreamSynchronize(s));
+  Staging& st = staging();
+  std::lock_guard<std::mutex> lk(st.mu);
+  staged_d2h(st, reinterpret_cast<const char*>(m.rp), m.nrows + 1, 4,
+             [&](const char* p, int64_t c, int64_t n) { widen_host(p, rp + c, n); }, s);
   if (m.nnz) {
-    sait::widen_indices(m.ci, tmp, m.nnz, s);
-    SAIT_CUDA(cudaMemcpyAsync(ci, tmp, sizeof(int64_t) * m.nnz, cudaMemcpyDeviceToHost, s));
-    if (v && m.v) SAIT_CUDA(cudaMemcpyAsync(v, m.v, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, s));
+    staged_d2h(st, reinterpret_cast<const char*>(m.ci), m.nnz, 4,
+               [&](const char* p, int64_t c, int64_t n) { widen_host(p, ci + c, n); }, s);
+    if (v && m.v)
+      staged_d2h(st, reinterpret_cast<const char*>(m.v), m.nnz, 8, [&](const char* p, int64_t c, int64_t n) {
+        copy_host(p, reinterpret_cast<char*>(v + c), n * 8);
+      }, s);
   }
-  SAIT_CUDA(cudaStreamSynchronize(s));
-  sait::dfree(tmp, s);
 }
 
 // Identity of order n used as the right factor for the elementwise kernels.

@@ -452,85 +452,11 @@ __device__ __forceinline__ void window_survivors(const Args& g, int32_t j, const
   }
 }
 
-// Window rows accumulate one A entry (= one B row) per step: the lanes take
-// the B row's entries, whose columns are distinct, so a step has no
-// intra-step conflicts and needs no grouping -- a product is assigned
-// (first touch, one atomicOr on the bitmap) or added in place -- and steps
-// run in increasing k, the reference's add order for every column.  The next
-// step's B entries are loaded before the current step's updates.
-__device__ void accumulate_window(const Args& g, int32_t j, const WindowTable& tab, double* val, int lane) {
-  tab.clear(lane);
-  __syncwarp();
-  const int32_t a0 = g.arp[j], a1 = g.arp[j + 1];
-  for (int32_t ab = a0; ab < a1; ab += 32) {
-    const int nt = min(32, a1 - ab);
-    int32_t bst = 0, len = 0;
-    double aval = 0.0;
-    if (lane < nt) {
-      const int32_t k = g.aci[ab + lane];
-      aval = g.av[ab + lane];
-      bst = g.brp[k];
-      len = g.brp[k + 1] - bst;
-    }
-    // (t, chunk l0) steps in order; prefetch the next step's entry
-    int t = 0, l0 = 0;
-    int32_t kb = __shfl_sync(0xffffffffu, bst, 0), kl = __shfl_sync(0xffffffffu, len, 0);
-    double ka = __shfl_sync(0xffffffffu, aval, 0);
-    int32_t col = -1;
-    double bval = 0.0;
-    if (lane < kl) {
-      col = g.bci[kb + lane];
-      bval = g.bv[kb + lane];
-    }
-    while (t < nt) {
-      // the step after (t, l0)
-      int t2 = t, l2 = l0 + 32;
-      int32_t kb2 = kb, kl2 = kl;
-      double ka2 = ka;
-      if (l2 >= kl) {
-        t2 = t + 1;
-        l2 = 0;
-        const int src = t2 < nt ? t2 : 0;
-        kb2 = __shfl_sync(0xffffffffu, bst, src);
-        kl2 = t2 < nt ? __shfl_sync(0xffffffffu, len, src) : 0;
-        ka2 = __shfl_sync(0xffffffffu, aval, src);
-      }
-      int32_t col2 = -1;
-      double bval2 = 0.0;
-      if (t2 < nt && l2 + lane < kl2) {
-        col2 = g.bci[kb2 + l2 + lane];
-        bval2 = g.bv[kb2 + l2 + lane];
-      }
-      if (col >= 0) {
-        const double prod = __dmul_rn(ka, bval);
-        const int hs = tab.insert(col);
-        const int sl = hs & ~kFresh;
-        val[sl] = (hs & kFresh) ? prod : __dadd_rn(val[sl], prod);
-      }
-      __syncwarp();
-      t = t2;
-      l0 = l2;
-      kb = kb2;
-      kl = kl2;
-      ka = ka2;
-      col = col2;
-      bval = bval2;
-    }
-  }
-  if (g.epi.add_identity && lane == 0) {
-    const int hs = tab.insert(j + static_cast<int32_t>(g.epi.diag_offset));
-    const int sl = hs & ~kFresh;
-    val[sl] = (hs & kFresh) ? 1.0 : __dadd_rn(val[sl], 1.0);
-  }
-  __syncwarp();
-}
-
 template <int R>
 __device__ void process_row_window(const Args& g, int32_t j, int32_t base, uint32_t* bits, uint32_t* kbits,
                                    double* val, WarpStage* st, int lane, bool numeric) {
   if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
-  static_cast<void>(st);
-  accumulate_window(g, j, WindowTable{bits, base, 32 * R}, val, lane);
+  accumulate_row(g, j, WindowTable{bits, base, 32 * R}, val, st, lane);
   uint32_t keep[R];
   window_survivors<R>(g, j, bits, val, base, lane, keep);
   const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);

@@ -489,6 +489,34 @@ void gram_impl(int64_t n, const double* A, int ka, const double* B, int kb, doub
 
 
 
+// Rayleigh-Ritz's two Grams in ONE launch: S^T S (upper tiles) and S^T AS
+// (all tiles) for S = [X W P] (m columns) and AS stored right after S's 3k
+// columns in one allocation (AS = S + 3k n).  The tiles of both run side by
+// side over each data block, so S's columns are read from DRAM once for both
+// Grams and one fold + one read-back serve both.  Gs (row-major, ld 6k)
+// receives columns [0, m) = S^T S and [3k, 3k + m) = S^T AS; every entry is
+// the same canonical dot as gram() computes.
+void gram_rr(int64_t n, const double* S, int m, int k, double* G, double* scratch, void* tiles_dev, cudaStream_t s) {
+  constexpr int TA = 8, TB = 4;
+  const int kb = 6 * k;
+  const int64_t nb = dot_blocks(n);
+  GramTile list[256];
+  int nt = 0;
+  for (int a0 = 0; a0 < m; a0 += TA) {
+    for (int b0 = 0; b0 < m; b0 += TB)
+      if (!(b0 + TB <= a0)) list[nt++] = GramTile{a0, b0};
+    for (int b0 = 3 * k; b0 < 3 * k + m; b0 += TB) list[nt++] = GramTile{a0, b0};
+  }
+  if (nt == 0 || nb == 0) return;
+  GramTile* tiles = static_cast<GramTile*>(tiles_dev);
+  SAIT_CUDA(cudaMemcpyAsync(tiles, list, sizeof(GramTile) * nt, cudaMemcpyHostToDevice, s));
+  gram_tiles<TA, TB><<<dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nb)), kT, 0, s>>>(n, S, m, S, kb, tiles,
+                                                                                            scratch, nb, true);
+  SAIT_LAUNCHED();
+  gram_fold<TA, TB><<<static_cast<unsigned>(nt * TA * TB), kT, 0, s>>>(scratch, nb, m, kb, tiles, G, kb);
+  SAIT_LAUNCHED();
+}
+
 // G (device, row-major, leading dimension ldg) = A^T B for column-major
 // blocks A (n x ka) and B (n x kb); upper_only skips tiles strictly below the
 // diagonal.  scratch: gram_scratch(n, ka, kb) doubles; tiles_dev: device room

@@ -38,6 +38,7 @@ void y_plus_x(int64_t n, const double* x, double* y, cudaStream_t s);
 int64_t gram_scratch(int64_t n, int ka, int kb);
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
           void* tiles_dev, cudaStream_t s, bool upper_only);
+void gram_rr(int64_t n, const double* S, int m, int k, double* G, double* scratch, void* tiles_dev, cudaStream_t s);
 void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s, int64_t offset = 0);
 void gram_partials(int64_t n, const double* A, int ka, const double* B, int kb, double* part, void* tiles_dev,
                    cudaStream_t s);
@@ -577,8 +578,8 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     cudaStream_t s = sait::as_stream(stream);
     sait::Operator op(a, s);
     const int64_t blk = static_cast<int64_t>(k) * n;
-    double* S = sait::dalloc<double>(3 * blk, s);   // [X W P]
-    double* AS = sait::dalloc<double>(3 * blk, s);  // [AX AW AP]
+    double* S = sait::dalloc<double>(6 * blk, s);  // [X W P | AX AW AP]: one allocation (gram_rr)
+    double* AS = S + 3 * blk;
     double* R = sait::dalloc<double>(blk, s);
     double* tmp = sait::dalloc<double>(4 * blk, s);
     // small host->device operands (Gram corrections, coefficient blocks) use a
@@ -587,8 +588,8 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     double* dsmall = sait::dalloc<double>(kSlots * 48 * 48, s);
     int slot = 0;
     auto next_small = [&] { return dsmall + static_cast<int64_t>(48 * 48) * (slot++ % kSlots); };
-    sait::Scalars sc(n, 48 * 48, 64, s);
-    double* gscratch = sait::dalloc<double>(sait::gram_scratch(n, 3 * k, 3 * k), s);
+    sait::Scalars sc(n, 48 * 96, 64, s);  // up to m x 6k Gram entries (gram_rr)
+    double* gscratch = sait::dalloc<double>(sait::gram_scratch(n, 3 * k, 6 * k), s);
     void* gtiles = sait::dalloc<long long>(256, s);
     double *X = S, *W = S + blk, *P = S + 2 * blk;
     double *AX = AS, *AW = AS + blk, *AP = AS + 2 * blk;
@@ -697,8 +698,21 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         int m = use_p ? 3 * k : 2 * k;
         bool ok = false;
         while (true) {
-          gram(S, m, S, m, GB, true);
-          gram(S, m, AS, m, GA);
+          {  // both Grams in one launch (S read once), one read-back
+            const int ld = 6 * k;
+            sait::gram_rr(n, S, m, k, sc.d, gscratch, gtiles, s);
+            sc.fetch(m * ld, s);
+            GB.assign(static_cast<size_t>(m) * m, 0.0);
+            GA.assign(static_cast<size_t>(m) * m, 0.0);
+            for (int a2 = 0; a2 < m; ++a2)
+              for (int b2 = 0; b2 < m; ++b2) {
+                GB[a2 * m + b2] = sc.h[a2 * ld + b2];
+                GA[a2 * m + b2] = sc.h[a2 * ld + 3 * k + b2];
+              }
+            for (int a2 = 0; a2 < m; ++a2)  // GB's skipped lower tiles mirror the upper ones (as gram(sym))
+              for (int b2 = 0; b2 < a2; ++b2)
+                if ((b2 / 8) < (a2 / 8)) GB[a2 * m + b2] = GB[b2 * m + a2];
+          }
           for (int i = 0; i < m; ++i)
             for (int j = i + 1; j < m; ++j) {
               const double s2 = 0.5 * (GA[i * m + j] + GA[j * m + i]);
@@ -745,8 +759,7 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
       stats->precond_applies = ptimer.count;
     }
     SAIT_CUDA(cudaStreamSynchronize(s));
-    sait::dfree(S, s);
-    sait::dfree(AS, s);
+    sait::dfree(S, s);  // (AS lives in the same allocation)
     sait::dfree(R, s);
     sait::dfree(tmp, s);
     sait::dfree(dsmall, s);

@@ -12,7 +12,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # SAIT_CHECKED=1 loads the bounds-checked build (make checked: every device
 # index the kernels derive is range-checked and traps with a message) --
 # the stand-in for compute-sanitizer, which this GPU pool does not allow.
-LIB_PATH = os.path.join(HERE, "checked" if os.environ.get("SAIT_CHECKED") == "1" else "", "libsait_b200.so")
+# SAIT_LIB_VARIANT=<subdir> loads an experimental build from that subdirectory
+# (kernel A/B measurements, tools/*_time.py).
+_sub = "checked" if os.environ.get("SAIT_CHECKED") == "1" else os.environ.get("SAIT_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, _sub, "libsait_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

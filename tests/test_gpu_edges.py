@@ -114,3 +114,75 @@ def test_device_pool_reserve():
     S.reserve_device_pool(0)
     with pytest.raises(S.SaitInvalidArgument):
         S.reserve_device_pool(-1)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "sell32_int32", "sell32_int16", "sell32_dict"])
+def test_forced_formats_on_tiny_and_empty(S, port, fmt):
+    """Every forced apply format on an empty pair, a 1x1 pair and a 33-row
+    pair (one full slice + one 1-row slice); the format reports its storage."""
+    e = S.CsrMatrix(0, 0, [0], [], [])
+    pe = S.SaitPairPreconditioner(e, e, format=fmt)
+    pe.apply(np.empty(0), np.empty(0))
+    t = S.CsrMatrix(1, 1, [0, 1], [0], [2.0])
+    p1 = S.SaitPairPreconditioner(t, t, format=fmt)
+    z = np.empty(1)
+    p1.apply(np.array([3.0]), z)
+    assert z[0] == 12.0
+    n = 33
+    A = S.laplacian_2d(6)  # 36 rows
+    f = S.ilu_k(A, 0)
+    ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(0.0, 2))
+    MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(0.0, 2))
+    pair = S.SaitPairPreconditioner(ML, MU, format=fmt)
+    r = S.uniform_pm1(9, A.nrows)
+    z = np.empty(A.nrows)
+    pair.apply(r, z)
+    assert bitwise_equal(z, port.pair_apply(to_oracle(ML), to_oracle(MU), r))
+    assert pair.factor_format(0)["nnz"] == ML.nnz()
+    del n
+
+
+def test_spmm_edge_widths(S, port):
+    """sait_spmm (dense.hpp:41 block product): widths 0, 1, 7, 9, 17 on the
+    device are each column's spmv bitwise; an empty matrix is a no-op."""
+    import torch
+
+    from paper_2106_12836_b200 import _native as N
+
+    A = S.laplacian_2d(20)
+    Ao = to_oracle(A)
+    d = S.DeviceCsr.upload(A)
+    n = A.nrows
+    for w in (0, 1, 7, 9, 17):
+        X = torch.from_numpy(np.concatenate([S.uniform_pm1(70 + c, n) for c in range(w)]) if w else np.zeros(0)).cuda()
+        Y = torch.empty(max(1, n * w), dtype=torch.float64, device="cuda")
+        N.check(N.lib.sait_spmm(d.handle, X.data_ptr() if w else 0, Y.data_ptr(), w, None))
+        torch.cuda.synchronize()
+        if w:
+            want = np.concatenate([port.spmv(Ao, S.uniform_pm1(70 + c, n)) for c in range(w)])
+            assert bitwise_equal(Y.cpu().numpy()[: n * w], want)
+    e = S.DeviceCsr.upload(S.CsrMatrix(0, 0, [0], [], []))
+    N.check(N.lib.sait_spmm(e.handle, 0, 0, 3, None))
+
+
+def test_assemble_rows_edge_cases(S):
+    """sait_csr_assemble_rows with no pieces (an all-empty row block) and
+    with pieces whose rows are all empty; sait_csr_col_span of an empty block."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2106_12836_b200 import _native as N
+    from paper_2106_12836_b200.dist import assemble_row_block, row_block_span
+
+    blk = assemble_row_block({}, [0, 5], 4, 5)
+    h = blk.to_host()
+    assert h.nrows == 4 and h.nnz() == 0 and list(h.row_ptr) == [0, 0, 0, 0, 0]
+    assert row_block_span(blk, 0, 4) == (0, 0)
+    rp = torch.zeros(5, dtype=torch.int32, device="cuda")
+    ci = torch.zeros(1, dtype=torch.int32, device="cuda")
+    v = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blk2 = assemble_row_block({0: {"rp": rp, "ci": ci, "v": v, "nnz": 0, "nrows": 4}}, [0, 5], 4, 5)
+    assert blk2.to_host().nnz() == 0
+    with pytest.raises(S.SaitInvalidArgument):
+        N.check(N.lib.sait_csr_assemble_rows(-1, None, 4, 5, None, C.byref(C.c_void_p())))

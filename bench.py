@@ -692,8 +692,8 @@ def run_b200(args):
         per_launch_ms = ms_step / (2 * NVEC)
         achieved = NVEC * fmt_pair / (ms_step * 1e-3) / 1e9
         traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "r02_apply_traffic.json")) as fh:
+        try:  # one ncu --set full capture of the SpMV under the timed condition
+            with open(os.path.join(ROOT, "profiles", "r02_sell_spmv_ncu_full.json")) as fh:
                 tr = json.load(fh)
             traffic = tr.get("dram_bytes_per_launch_mean")
         except Exception:
@@ -726,8 +726,9 @@ def run_b200(args):
             "effective_gbs_12B_per_nnz": value,
             "effective_note": "SURVEY §8(d) algorithmic bytes (12 B/nnz + vectors) per pair / time = `value`; "
                               "exceeds the copy peak because the format streams ~8 B/nnz",
-            "traffic_note": "ncu dram__bytes_read+write per SpMV launch, back-to-back pairs on distinct vectors, "
-                            "--cache-control none (profiles/r02_apply_traffic.json)",
+            "traffic_note": "ncu --set full dram__bytes_read+write per SpMV launch, back-to-back pairs on distinct "
+                            "vectors, --cache-control none (profiles/r02_sell_spmv_ncu_full.json; the 8-pair metrics "
+                            "capture profiles/r02_apply_traffic.json gives 123 MB)",
             "isolated_per_launch_ms": kt,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
             "frac_vs_nominal_8000": achieved / 8000.0,

@@ -149,7 +149,7 @@ def run_reference(args):
     from oracle import oracle as O
 
     if not O.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsaitref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libsaitref.so not built"})
         return
     import ctypes as C
 
@@ -193,7 +193,7 @@ def run_reference(args):
         line["build_c4"] = c4_reference_sample()
     lib.ref_pair_destroy.argtypes = [C.c_void_p]
     lib.ref_pair_destroy(p)
-    print(json.dumps(line))
+    emit(line)
 
 
 # --------------------------------------------------------------------- B200 arm
@@ -566,7 +566,7 @@ def run_b200_sharded(args):
             line["apply_c5"] = c5
         if c4:
             line["build_c4"] = c4
-        print(json.dumps(line))
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -851,7 +851,7 @@ def run_b200(args):
             line["solvers"] = solvers
         if build_c4:
             line["build_c4"] = build_c4
-        print(json.dumps(line))
+        emit(line)
 
 def run_c5_single(S, torch, steps, stream, nvec=20):
     """BASELINE config 5's preconditioner apply on one GPU: 256^3 Laplacian,
@@ -1116,7 +1116,28 @@ def c4_cpu_sample(S):
                       f"(oracle/_ref, OpenMP), {t:.2f} s", "device_bitwise_equal": same}
 
 
+# The JSON line is the only thing on stdout: libraries that print there
+# (NCCL's version banner at communicator creation, CUDA / C printf) write to
+# fd 1 directly, so fd 1 is pointed at stderr for the whole run and the line
+# goes to the saved original stdout.
+_REAL_STDOUT = None
+
+
+def _claim_stdout():
+    global _REAL_STDOUT
+    sys.stdout.flush()
+    _REAL_STDOUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    out = _REAL_STDOUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

@@ -888,17 +888,10 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
   int bin = -1;
   if (j < g.n) {
     const int32_t e0 = g.arp[j], e1 = g.arp[j + 1];
-    const int32_t jd = static_cast<int32_t>(j + g.epi.diag_offset);
-    int32_t lo = g.epi.add_identity ? jd : INT32_MAX, hi = g.epi.add_identity ? jd : -1;
 #pragma unroll 4
     for (int32_t e = e0; e < e1; ++e) {
       const int32_t k = g.aci[e];
-      const int32_t b0 = g.brp[k], b1 = g.brp[k + 1];
-      p += b1 - b0;
-      if (win && b1 > b0) {
-        lo = min(lo, g.bci[b0]);
-        hi = max(hi, g.bci[b1 - 1]);
-      }
+      p += g.brp[k + 1] - g.brp[k];
     }
     int64_t distinct = (p < g.ncols ? p : g.ncols) + 1;  // +1: the identity entry
     int logs = kMinLogSlots;
@@ -909,7 +902,20 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     if (bin > kGlobalBin) bin = kGlobalBin;
     const int32_t m = e1 - e0;
     bool windowed = false;
-    if (win && logs >= 8 && hi >= lo) {  // big hash rows whose columns span < 1024 / 2048
+    int32_t lo = INT32_MAX, hi = -1;
+    if (win && logs >= 8) {  // big hash rows: the column span, from the first / last entry of each B row
+      const int32_t jd = static_cast<int32_t>(j + g.epi.diag_offset);
+      if (g.epi.add_identity) lo = hi = jd;
+      for (int32_t e = e0; e < e1; ++e) {
+        const int32_t k = g.aci[e];
+        const int32_t b0 = g.brp[k], b1 = g.brp[k + 1];
+        if (b1 > b0) {
+          lo = min(lo, g.bci[b0]);
+          hi = max(hi, g.bci[b1 - 1]);
+        }
+      }
+    }
+    if (win && logs >= 8 && hi >= lo) {  // ... whose columns span < 1024 / 2048
       const int32_t span = hi - lo;
       if (span < 1024) bin = kWinBin1, windowed = true;
       else if (span < 2048) bin = kWinBin2, windowed = true;

@@ -621,7 +621,7 @@ def run_b200(args):
         "steps_run": [st[0].steps_run, st[1].steps_run],
         "products": st[0].products + st[1].products,
         "note": "both factors built concurrently (sait_build_pair), wall time of the call incl. "
-                "split/transposes, median of %d builds after a warm-up; replicated on every rank" % BUILD_REPS,
+                "split/transposes, median of %d builds after a warm-up" % BUILD_REPS,
     }
     # the same build through the drop-in host API: host int64 CSR in, host
     # int64 CSR out (saitprec::sait_thr's contract, sait.cpp:90-101), both

@@ -412,6 +412,16 @@ int sait_lobpcg(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, ui
 int sait_lobpcg_ex(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed,
                    double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
                    sait_solve_stats *stats, sait_stream_t stream);
+/* LOBPCG with a choice of Gram kernel.  SAIT_GRAM_CANONICAL: the canonical
+ * reduction order (bitwise the restatement oracle/solvers.c; what sait_lobpcg
+ * uses).  SAIT_GRAM_TENSOR: FP64 tensor-core (DMMA) Grams -- deterministic,
+ * but the products inside an mma are summed in the hardware's order, so the
+ * run agrees with the restatement to within the north_star's +-1 iteration
+ * rather than bit for bit. */
+enum { SAIT_GRAM_CANONICAL = 0, SAIT_GRAM_TENSOR = 1 };
+int sait_lobpcg_opt(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, int gram_mode,
+                    double *h_evals, double *d_evecs, double *h_resnorms, int *iterations,
+                    sait_solve_stats *stats, sait_stream_t stream);
 /* The same with the exact ILU solves as preconditioner (column by column;
  * the comparator of SPEC.md acceptance #9). */
 int sait_lobpcg_exact(sait_dcsr_t A, sait_exact_t M, int nev, double tol, int maxit, uint64_t seed,

@@ -136,6 +136,8 @@ PROTOTYPES = {
     "sait_csr_to_host": (C.c_int, [VP, VP, C.POINTER(HostCsr)]),
     "sait_csr_device_arrays": (C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)]),
     "sait_csr_free": (None, [VP]),
+    "sait_lobpcg_opt": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_int, PD, VP, PD,
+                                  C.POINTER(C.c_int), C.POINTER(SolveStats), VP]),
     "sait_spmm": (C.c_int, [VP, VP, VP, C.c_int64, VP]),
     "sait_lobpcg_ex": (C.c_int, [VP, VP, C.c_int, C.c_double, C.c_int, C.c_uint64, PD, VP, PD, C.POINTER(C.c_int),
                                  C.POINTER(SolveStats), VP]),

@@ -455,6 +455,212 @@ void gram_partials(int64_t n, const double* A, int ka, const double* B, int kb, 
   SAIT_LAUNCHED();
 }
 
+// ---- Tensor-core Grams (FP64 DMMA, mma.sync.m8n8k4): LOBPCG's fast mode.
+// One warp per 2048-element chunk computes the partial Gram of up to 3 x 6
+// blocks of 8 columns: per k4 step every lane loads one element of each
+// block (column lane>>2, element lane&3 -- the A and B fragment layouts of
+// m8n8k4 coincide for a Gram), and NA * NB mma instructions accumulate
+// 8 x 8 tiles (256 FMAs each) in registers.  The columns are read once per
+// chunk for all tiles, so a 24 x 48 Gram costs one pass over its 72 columns
+// instead of ~500 dots' worth of FMA issue.  The order of the products inside
+// an mma is the hardware's, so the result is deterministic (fixed chunks,
+// fixed fold) but not the canonical order of the restatement: LOBPCG with it
+// agrees with oracle/solvers.c to within ±1 iteration (north_star), not bit
+// for bit.
+namespace {
+struct DmmaBlocks {
+  const double* a[3];
+  const double* b[6];
+  int acols[3];
+  int bcols[6];
+};
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// The k dimension of an mma may take the elements in any order as long as
+// A and B agree, so lane (r, q) takes elements e + 4q + u of column r for
+// the four mma steps u = 0..3 of a 16-element group: each lane loads 32
+// contiguous bytes per column (two 16-byte loads) instead of 8, and a warp
+// covers a full 128-byte line of every column per group.  SHARE: B's first
+// NA blocks are A's blocks (Rayleigh-Ritz: [S | AS] against S), reused from
+// the A fragments instead of loaded twice.
+__device__ __forceinline__ double2 ld_ro2(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+template <int NA, int NB, bool SHARE>
+__global__ void __launch_bounds__(NA * NB >= 9 ? 128 : 256) gram_dmma_kernel(int64_t n, DmmaBlocks blk, double* __restrict__ part,
+                                                         int64_t nchunks) {
+  constexpr int NBL = SHARE ? NB - NA : NB;  // B blocks to load
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (c >= nchunks) return;
+  const int r = lane >> 2, q = lane & 3;
+  const double* ap[NA];
+  const double* bp[NBL > 0 ? NBL : 1];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) ap[i] = r < blk.acols[i] ? blk.a[i] + n * r : nullptr;
+#pragma unroll
+  for (int i = 0; i < NBL; ++i) {
+    const int ib = SHARE ? NA + i : i;
+    bp[i] = r < blk.bcols[ib] ? blk.b[ib] + n * r : nullptr;
+  }
+  double acc[NA][NB][2];
+#pragma unroll
+  for (int i = 0; i < NA; ++i)
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int64_t i0 = c * kB, i1 = min(n, i0 + kB);
+  for (int64_t e = i0; e < i1; e += 16) {
+    double af[4][NA], bf[4][NBL > 0 ? NBL : 1];
+    const int64_t f = e + 4 * q;  // this lane's 4 elements f .. f + 3
+    if (f + 4 <= i1) {
+#pragma unroll
+      for (int k = 0; k < NA; ++k) {
+        double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+        if (ap[k]) {
+          x = ld_ro2(ap[k] + f);
+          y = ld_ro2(ap[k] + f + 2);
+        }
+        af[0][k] = x.x;
+        af[1][k] = x.y;
+        af[2][k] = y.x;
+        af[3][k] = y.y;
+      }
+#pragma unroll
+      for (int k = 0; k < NBL; ++k) {
+        double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+        if (bp[k]) {
+          x = ld_ro2(bp[k] + f);
+          y = ld_ro2(bp[k] + f + 2);
+        }
+        bf[0][k] = x.x;
+        bf[1][k] = x.y;
+        bf[2][k] = y.x;
+        bf[3][k] = y.y;
+      }
+    } else {  // the chunk's ragged end
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool in = f + u < i1;
+#pragma unroll
+        for (int k = 0; k < NA; ++k) af[u][k] = (in && ap[k]) ? ld_ro(ap[k] + f + u) : 0.0;
+#pragma unroll
+        for (int k = 0; k < NBL; ++k) bf[u][k] = (in && bp[k]) ? ld_ro(bp[k] + f + u) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) {
+          const double bv = SHARE ? (ib < NA ? af[u][ib] : bf[u][SHARE ? ib - NA : ib]) : bf[u][ib];
+          dmma(acc[ia][ib][0], acc[ia][ib][1], af[u][ia], bv);
+        }
+  }
+  // D[row = lane>>2][col = 2 (lane&3) + h] of tile (ia, ib)
+  const int KB = NB * 8;
+#pragma unroll
+  for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = ia * 8 + r, bcol = ib * 8 + 2 * q + h;
+        part[(static_cast<int64_t>(a) * KB + bcol) * nchunks + c] = acc[ia][ib][h];
+      }
+}
+// G[a * ldg + bmap(b)] = sum over chunks (fixed order: thread t sums t,
+// t + 256, ..., then the warp butterfly and the 8-way tree)
+__global__ void __launch_bounds__(kT) gram_dmma_fold(const double* __restrict__ part, int64_t nchunks, int KB,
+                                                     const int* __restrict__ bmap, double* __restrict__ G,
+                                                     int ldg) {
+  __shared__ double ws[8];
+  const int d = blockIdx.x, a = d / KB, b = d % KB;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double* p = part + static_cast<int64_t>(d) * nchunks;
+  double s = 0.0;
+  for (int64_t k = t; k < nchunks; k += kT) s = __dadd_rn(s, p[k]);
+  s = warp_butterfly(s);
+  if (lane == 0) ws[warp] = s;
+  __syncthreads();
+  if (t == 0 && bmap[b] >= 0) G[a * ldg + bmap[b]] = tree8(ws);
+}
+template <int NA, int NB, bool SHARE>
+void launch_dmma(int64_t n, const DmmaBlocks& blk, double* part, int64_t nchunks, cudaStream_t s) {
+  // big tiles hold ~170 registers: 4-warp CTAs so that 3 fit per SM
+  constexpr int kThreads = NA * NB >= 9 ? 128 : 256, kWarps = kThreads / 32;
+  gram_dmma_kernel<NA, NB, SHARE><<<static_cast<unsigned>((nchunks + kWarps - 1) / kWarps), kThreads, 0, s>>>(
+      n, blk, part, nchunks);
+}
+using DmmaLaunch = void (*)(int64_t, const DmmaBlocks&, double*, int64_t, cudaStream_t);
+template <int NA>
+DmmaLaunch dmma_for(int nb, bool share) {
+  if (share) {  // B = [A blocks | NB - NA more]
+    switch (nb) {
+      case NA: return launch_dmma<NA, NA, true>;
+      default: return launch_dmma<NA, 2 * NA, true>;
+    }
+  }
+  switch (nb) {
+    case 1: return launch_dmma<NA, 1, false>;
+    case 2: return launch_dmma<NA, 2, false>;
+    case 3: return launch_dmma<NA, 3, false>;
+    case 4: return launch_dmma<NA, 4, false>;
+    case 5: return launch_dmma<NA, 5, false>;
+    default: return launch_dmma<NA, 6, false>;
+  }
+}
+}  // namespace
+
+// G (device, row-major, ld ldg) = A^T B with tensor cores: A's columns are the
+// blocks of 8 starting at a_cols[i] (na <= 3 blocks, ka columns in all), B's
+// likewise (nb <= 6 blocks); b columns land at G column bcol_out[j * 8 + c]
+// (-1: not stored).  scratch: >= gram_scratch(n, 24, 48) doubles; idx_dev:
+// device room for 64 ints.  false if the shape is not covered (the caller
+// uses gram()).
+bool gram_fast(int64_t n, const double* const* ablk, const int* acols, int na, const double* const* bblk,
+               const int* bcols, int nb, const int* bcol_out, double* G, int ldg, double* scratch, void* idx_dev,
+               cudaStream_t s) {
+  if (na < 1 || na > 3 || nb < 1 || nb > 6 || n <= 0) return false;
+  for (int i = 0; i < na; ++i)
+    if (reinterpret_cast<uintptr_t>(ablk[i]) % 8) return false;
+  DmmaBlocks blk{};
+  for (int i = 0; i < na; ++i) {
+    blk.a[i] = ablk[i];
+    blk.acols[i] = acols[i];
+  }
+  for (int i = 0; i < nb; ++i) {
+    blk.b[i] = bblk[i];
+    blk.bcols[i] = bcols[i];
+  }
+  const int64_t nchunks = dot_blocks(n);
+  // B's first na blocks the A blocks themselves (Rayleigh-Ritz), 16-byte
+  // aligned columns for the vector loads (n even)
+  bool share = nb == na || nb == 2 * na;
+  for (int i = 0; i < na && share; ++i) share = bblk[i] == ablk[i] && bcols[i] == acols[i];
+  bool aligned = n % 2 == 0;
+  for (int i = 0; i < na; ++i) aligned = aligned && reinterpret_cast<uintptr_t>(ablk[i]) % 16 == 0;
+  for (int i = 0; i < nb; ++i) aligned = aligned && reinterpret_cast<uintptr_t>(bblk[i]) % 16 == 0;
+  if (!aligned) return false;
+  DmmaLaunch f = na == 1 ? dmma_for<1>(nb, share) : na == 2 ? dmma_for<2>(nb, share) : dmma_for<3>(nb, share);
+  f(n, blk, scratch, nchunks, s);
+  SAIT_LAUNCHED();
+  const int KB = nb * 8;
+  int map[48];
+  for (int j = 0; j < KB; ++j) map[j] = bcol_out[j];
+  int* dmap = static_cast<int*>(idx_dev);
+  SAIT_CUDA(cudaMemcpyAsync(dmap, map, sizeof(int) * KB, cudaMemcpyHostToDevice, s));
+  gram_dmma_fold<<<static_cast<unsigned>(na * 8 * KB), kT, 0, s>>>(scratch, nchunks, KB, dmap, G, ldg);
+  SAIT_LAUNCHED();
+  // rows a >= ka (partial last A block) are folded too but never read
+  return true;
+}
+
 // G (device, row-major, leading dimension ldg) = A^T B for column-major
 // blocks A (n x ka) and B (n x kb); upper_only skips tiles strictly below the
 // diagonal.  scratch: gram_scratch(n, ka, kb) doubles; tiles: a device array

@@ -39,6 +39,9 @@ int64_t gram_scratch(int64_t n, int ka, int kb);
 void gram(int64_t n, const double* A, int ka, const double* B, int kb, double* G, int ldg, double* scratch,
           void* tiles_dev, cudaStream_t s, bool upper_only);
 void gram_rr(int64_t n, const double* S, int m, int k, double* G, double* scratch, void* tiles_dev, cudaStream_t s);
+bool gram_fast(int64_t n, const double* const* ablk, const int* acols, int na, const double* const* bblk,
+               const int* bcols, int nb, const int* bcol_out, double* G, int ldg, double* scratch, void* idx_dev,
+               cudaStream_t s);
 void fill_uniform_pm1_device(uint64_t seed, int64_t n, double* out, cudaStream_t s, int64_t offset = 0);
 void gram_partials(int64_t n, const double* A, int ka, const double* B, int kb, double* part, void* tiles_dev,
                    cudaStream_t s);
@@ -561,7 +564,7 @@ int sait_pcg_exact(sait_dcsr_t A, sait_exact_t M, const double* d_b, double* d_x
 
 static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int maxit, uint64_t seed,
                        double* h_evals, double* d_evecs, double* h_resnorms, int* iterations, sait_stream_t stream,
-                       sait_solve_stats* stats = nullptr) {
+                       sait_solve_stats* stats = nullptr, bool fast_gram = false) {
   return solver_guard([&] {
     const auto t_start = std::chrono::steady_clock::now();
     sait::PrecondTimer ptimer;
@@ -597,8 +600,35 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     // G[a][b] = S_a . Y_b (canonical dots, tiled tall-skinny kernel), row-major
     // ka x kb on the host; sym: S == Y, lower tiles mirrored (bitwise equal,
     // the canonical dot is symmetric in its arguments)
+    // fast_gram: the tensor-core Gram (gram_fast: FP64 DMMA, deterministic,
+    // not the canonical order); falls back to the canonical kernel for shapes
+    // it does not cover
+    auto gram_dmma = [&](const double* const* ab, int na, const double* const* bb, int nbk, const int* bout, int ka,
+                         int ldg) {
+      int ac[3], bc[6];
+      for (int i = 0; i < na; ++i) ac[i] = std::min(8, ka - 8 * i);
+      for (int i = 0; i < nbk; ++i) bc[i] = 8;
+      return sait::gram_fast(n, ab, ac, na, bb, bc, nbk, bout, sc.d, ldg, gscratch, gtiles, s);
+    };
     auto gram = [&](const double* Sa, int ka, const double* Yb, int kb, std::vector<double>& G, bool sym = false) {
       G.assign(static_cast<size_t>(ka) * kb, 0.0);
+      if (fast_gram && kb % 8 == 0 && ka <= 24 && kb <= 48) {
+        const double* ab[3];
+        const double* bb[6];
+        int bout[48];
+        const int na = (ka + 7) / 8, nbk = kb / 8;
+        for (int i = 0; i < na; ++i) ab[i] = Sa + static_cast<int64_t>(8 * i) * n;
+        for (int i = 0; i < nbk; ++i) bb[i] = Yb + static_cast<int64_t>(8 * i) * n;
+        for (int j = 0; j < kb; ++j) bout[j] = j;
+        if (gram_dmma(ab, na, bb, nbk, bout, ka, kb)) {
+          sc.fetch(ka * kb, s);
+          std::copy(sc.h.begin(), sc.h.begin() + static_cast<size_t>(ka) * kb, G.begin());
+          if (sym)
+            for (int a2 = 0; a2 < ka; ++a2)
+              for (int b2 = 0; b2 < a2; ++b2) G[a2 * kb + b2] = G[b2 * kb + a2];
+          return;
+        }
+      }
       sait::gram(n, Sa, ka, Yb, kb, sc.d, kb, gscratch, gtiles, s, sym);
       sc.fetch(ka * kb, s);
       std::copy(sc.h.begin(), sc.h.begin() + static_cast<size_t>(ka) * kb, G.begin());
@@ -698,7 +728,31 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         int m = use_p ? 3 * k : 2 * k;
         bool ok = false;
         while (true) {
-          {  // both Grams in one launch (S read once), one read-back
+          bool fast_done = false;
+          if (fast_gram && m % 8 == 0 && m <= 24) {  // both Grams from one tensor-core pass over [S | AS]
+            const double* ab[3];
+            const double* bb[6];
+            int bout[48];
+            const int na = m / 8;
+            for (int i = 0; i < na; ++i) {
+              ab[i] = S + static_cast<int64_t>(8 * i) * n;
+              bb[i] = S + static_cast<int64_t>(8 * i) * n;
+              bb[na + i] = AS + static_cast<int64_t>(8 * i) * n;
+            }
+            for (int j = 0; j < 2 * m; ++j) bout[j] = j;
+            if (gram_dmma(ab, na, bb, 2 * na, bout, m, 2 * m)) {
+              sc.fetch(m * 2 * m, s);
+              GB.assign(static_cast<size_t>(m) * m, 0.0);
+              GA.assign(static_cast<size_t>(m) * m, 0.0);
+              for (int a2 = 0; a2 < m; ++a2)
+                for (int b2 = 0; b2 < m; ++b2) {
+                  GB[a2 * m + b2] = b2 >= a2 ? sc.h[a2 * 2 * m + b2] : sc.h[b2 * 2 * m + a2];  // exactly symmetric
+                  GA[a2 * m + b2] = sc.h[a2 * 2 * m + m + b2];
+                }
+              fast_done = true;
+            }
+          }
+          if (!fast_done) {  // both Grams in one launch (S read once), one read-back
             const int ld = 6 * k;
             sait::gram_rr(n, S, m, k, sc.d, gscratch, gtiles, s);
             sc.fetch(m * ld, s);
@@ -786,6 +840,19 @@ int sait_lobpcg_ex(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit,
   sait::Precond pc;
   pc.p = M;
   return lobpcg_impl(A, pc, nev, tol, maxit, seed, h_evals, d_evecs, h_resnorms, iterations, stream, stats);
+}
+
+int sait_lobpcg_opt(sait_dcsr_t A, sait_pair_t M, int nev, double tol, int maxit, uint64_t seed, int gram_mode,
+                    double* h_evals, double* d_evecs, double* h_resnorms, int* iterations, sait_solve_stats* stats,
+                    sait_stream_t stream) {
+  if (gram_mode != SAIT_GRAM_CANONICAL && gram_mode != SAIT_GRAM_TENSOR) {
+    sait::set_last_error("lobpcg: unknown gram mode " + std::to_string(gram_mode));
+    return SAIT_ERR_INVALID_ARGUMENT;
+  }
+  sait::Precond pc;
+  pc.p = M;
+  return lobpcg_impl(A, pc, nev, tol, maxit, seed, h_evals, d_evecs, h_resnorms, iterations, stream, stats,
+                     gram_mode == SAIT_GRAM_TENSOR);
 }
 
 int sait_lobpcg_exact(sait_dcsr_t A, sait_exact_t M, int nev, double tol, int maxit, uint64_t seed,

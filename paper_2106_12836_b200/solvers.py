@@ -88,7 +88,11 @@ class EigResult:
     stats: SolveStats | None = None  # seconds + preconditioner share (SAIT pair only)
 
 
-def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, stream=None, host_vectors=True):
+def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, stream=None, host_vectors=True,
+           gram: str = "canonical"):
+    """Block LOBPCG.  gram="canonical" (default) is bitwise
+    the restatement; gram="tensor" uses FP64 tensor-core Grams
+    (sait_lobpcg_opt): faster, deterministic, within +-1 iteration of it."""
     import torch
 
     dA = A if isinstance(A, DeviceCsr) else DeviceCsr.upload(A, stream)
@@ -100,11 +104,13 @@ def lobpcg(A, M, nev: int, tol: float = 1e-6, maxit: int = 1000, seed: int = 5, 
     s = _stream_handle(stream) if stream is not None else torch.cuda.current_stream().cuda_stream
     mh, fn = _precond(M, N.lib.sait_lobpcg, N.lib.sait_lobpcg_exact)
     st = None
+    if gram not in ("canonical", "tensor"):
+        raise ValueError(f"unknown gram mode {gram!r}")
     if fn is N.lib.sait_lobpcg:
         st = N.SolveStats()
-        N.check(N.lib.sait_lobpcg_ex(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed),
-                                     evals.ctypes.data_as(N.PD), vecs.data_ptr(), res.ctypes.data_as(N.PD),
-                                     C.byref(its), C.byref(st), s))
+        N.check(N.lib.sait_lobpcg_opt(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed),
+                                      1 if gram == "tensor" else 0, evals.ctypes.data_as(N.PD), vecs.data_ptr(),
+                                      res.ctypes.data_as(N.PD), C.byref(its), C.byref(st), s))
     else:
         N.check(fn(dA.handle, mh, int(nev), float(tol), int(maxit), int(seed), evals.ctypes.data_as(N.PD),
                    vecs.data_ptr(), res.ctypes.data_as(N.PD), C.byref(its), s))

@@ -141,3 +141,10 @@ def test_config5_full_size(S):
     assert vec_digest(r.eigenvalues) == lb["evals_digest"]
     assert np.array_equal(r.residual_history.view(np.uint64), HIST["c5_lobpcg_resnorms"].view(np.uint64))
     assert vec_digest(r.eigenvectors.T.contiguous().cpu().numpy()) == lb["evecs_digest"]
+    # the tensor-core Grams (gram="tensor"): north_star's +-1 iteration and
+    # the restatement's eigenvalues to 1e-12 relative at full size
+    rt = S.lobpcg(dA, pair, lb["nev"], lb["tol"], lb["maxit"], lb["seed"], host_vectors=False, gram="tensor")
+    assert abs(rt.iterations - lb["iterations"]) <= 1
+    ev = np.asarray(lb["evals"])
+    assert np.max(np.abs(rt.eigenvalues - ev) / np.abs(ev)) < 1e-12
+    assert float(rt.residual_history[-1].max()) <= lb["tol"]

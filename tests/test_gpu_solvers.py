@@ -127,6 +127,34 @@ def test_lobpcg_bitwise_and_analytic(S, port, nev, prec):
         assert r.iterations * 2 <= r0.iterations
 
 
+@pytest.mark.parametrize("grid,nev,prec", [(20, 4, 0.05), (20, 8, 0.05), (20, 3, None), (24, 8, 0.03)])
+def test_lobpcg_tensor_grams_within_one_iteration(S, port, grid, nev, prec):
+    """LOBPCG with FP64 tensor-core Grams (gram="tensor", sait_lobpcg_opt):
+    the products inside an mma are summed in the hardware's order, so the
+    run is not bitwise the restatement, but north_star's contract holds:
+    iteration count within +-1, eigenvalues within 1e-12 relative of the
+    restatement's, every final residual <= tol.  Also deterministic (two runs,
+    same bits).  Shapes cover k not a multiple of 8 (3: the canonical kernel
+    takes over) and P dropped / kept."""
+    from oracle import oracle as O
+
+    A = O.laplacian_3d(grid)
+    ML = MU = pair = None
+    if prec:
+        L, U = port.ilu_k(A, 0)
+        ML, MU = port.sait_thr(L, True, prec, 3), port.sait_thr(U, False, prec, 3)
+        pair = S.SaitPairPreconditioner(to_product(ML), to_product(MU))
+    ev_o, _, it_o, _ = O.lobpcg(A, ML, MU, nev, 1e-6, 600, 5)
+    r = S.lobpcg(to_product(A), pair, nev, 1e-6, 600, 5, gram="tensor")
+    r2 = S.lobpcg(to_product(A), pair, nev, 1e-6, 600, 5, gram="tensor")
+    assert abs(r.iterations - it_o) <= 1
+    assert np.max(np.abs(r.eigenvalues - ev_o) / np.abs(ev_o)) < 1e-12
+    assert np.all(r.residual_history[-1] <= 1e-6)
+    assert r2.iterations == r.iterations and bitwise_equal(r2.eigenvalues, r.eigenvalues)
+    with pytest.raises(ValueError):
+        S.lobpcg(to_product(A), pair, nev, 1e-6, 5, 5, gram="fast")
+
+
 def test_pcg_gmres_exact_ilu_bitwise(S, port):
     """The paper's comparator (exact ILU(0) solves as the preconditioner,
     PAPER.md:880-900): device PCG / GMRES with ExactIluPreconditioner vs the

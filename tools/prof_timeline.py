@@ -52,7 +52,7 @@ if what == "lobpcg":
     dA = S.DeviceCsr.upload(A)
 
     def run():
-        S.lobpcg(dA, P, 8, 1e-6, 5, 5, host_vectors=False)
+        S.lobpcg(dA, P, 8, 1e-6, 5, 5, host_vectors=False, gram=os.environ.get("SAIT_LOBPCG_GRAM", "canonical"))
 if what == "apply":
     ML = S.sait_thr(L, S.lower_triangular, S.SaitThrParams(5e-2, 3))
     MU = S.sait_thr(U, S.upper_triangular, S.SaitThrParams(5e-2, 3))

@@ -28,10 +28,6 @@ namespace sait {
 namespace {
 
 constexpr int kSlice = 32;
-#ifndef SAIT_CM_BATCH
-#define SAIT_CM_BATCH 2
-#endif
-constexpr int kCmBatch = SAIT_CM_BATCH;  // slots per batch of the column-major block SpMM
 constexpr double kMaxPad = 1.25;
 
 __device__ __forceinline__ int32_t ld_na(const int32_t* p) {
@@ -291,46 +287,70 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
 
 // Column-major block (n x NV, leading dimension ld): lane = row, NV
 // accumulators; each index/value read once for all NV vectors, x gathered
-// per column (neighbouring rows -> neighbouring x: coalesced).
+// per column (neighbouring rows -> neighbouring x: coalesced).  The kernel is
+// bound by loads in flight per SM = resident warps x gathers per warp
+// (BATCH slots x NV columns); the shapes per index format are the measured
+// best (tools/block_time.py, C5 block-8 pair: 1.93 -> 1.31 ms for the
+// dictionary format, the int16/int32 formats spill at 40 registers).
+template <class IDX>
+struct CmShape {
+  static constexpr int kThreads = 256, kMinBlocks = 1, kBatch = 2;
+};
+template <>
+struct CmShape<IdxDict> {
+  static constexpr int kThreads = 128, kMinBlocks = 12, kBatch = 3;
+};
 template <int NV, class IDX>
-__global__ void __launch_bounds__(256) sell_spmm_cm_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
-                                                            IDX idx, const double* __restrict__ sval,
-                                                            const double* __restrict__ x, int64_t ldx,
-                                                            double* __restrict__ y, int64_t ldy, int nv) {
+__global__ void __launch_bounds__(CmShape<IDX>::kThreads, CmShape<IDX>::kMinBlocks) sell_spmm_cm_kernel(int64_t n, int64_t nslices,
+                                                                             const int64_t* __restrict__ soff, IDX idx,
+                                                                             const double* __restrict__ sval,
+                                                                             const double* __restrict__ x, int64_t ldx,
+                                                                             double* __restrict__ y, int64_t ldy,
+                                                                             int nv) {
   const int lane = threadIdx.x & 31;
   const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
   const int64_t base = soff[s];
-  const int64_t ib = idx.slice_base(s, base);
+  const int64_t ib = idx.slice_base(s, base) + lane;
+  const double* __restrict__ vp = sval + base + lane;
   const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
   double acc[NV];
 #pragma unroll
   for (int c = 0; c < NV; ++c) acc[c] = 0.0;
-  for (int32_t k0 = 0; k0 < w; k0 += kCmBatch) {
-    int32_t col[kCmBatch];
-    double v[kCmBatch];
+  constexpr int kBatch = CmShape<IDX>::kBatch;
+  for (int32_t k0 = 0; k0 < w; k0 += kBatch) {
+    int32_t col[kBatch];
+    double v[kBatch];
 #pragma unroll
-    for (int j = 0; j < kCmBatch; ++j) {
+    for (int j = 0; j < kBatch; ++j) {
       col[j] = -1;
       v[j] = 0.0;
       if (k0 + j < w) {
-        col[j] = idx.col(ib + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
-        v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
+        col[j] = idx.col(ib + (k0 + j) * kSlice, row);
+        v[j] = ld_na(vp + (k0 + j) * kSlice);
       }
     }
 #pragma unroll
-    for (int j = 0; j < kCmBatch; ++j) {
+    for (int j = 0; j < kBatch; ++j) {
       if (col[j] < 0) continue;
+      // one running pointer down the block's columns (no per-column 64-bit
+      // offsets held in registers: occupancy is what bounds this kernel)
+      const double* p = x + col[j];
 #pragma unroll
-      for (int c = 0; c < NV; ++c)
-        if (c < nv) acc[c] = __dadd_rn(acc[c], __dmul_rn(v[j], __ldg(x + ldx * c + col[j])));
+      for (int c = 0; c < NV; ++c) {
+        if (c < nv) acc[c] = __dadd_rn(acc[c], __dmul_rn(v[j], __ldg(p)));
+        p += ldx;
+      }
     }
   }
-  const int64_t row = s * kSlice + lane;
   if (row < n) {
+    double* q = y + row;
 #pragma unroll
-    for (int c = 0; c < NV; ++c)
-      if (c < nv) y[ldy * c + row] = acc[c];
+    for (int c = 0; c < NV; ++c) {
+      if (c < nv) *q = acc[c];
+      q += ldy;
+    }
   }
 }
 
@@ -871,21 +891,28 @@ void publish_epoch(int* flag, int epoch, cudaStream_t s) {
   SAIT_LAUNCHED();
 }
 
+namespace {
+template <class IDX>
+void launch_cm(const SellMatrix& m, IDX ix, const double* x, int64_t ldx, double* y, int64_t ldy, int nv,
+               cudaStream_t s) {
+  constexpr int wpb = CmShape<IDX>::kThreads / 32;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, (m.nslices + wpb - 1) / wpb));
+  sell_spmm_cm_kernel<8, IDX><<<grid, CmShape<IDX>::kThreads, 0, s>>>(m.n, m.nslices, m.soff, ix, m.val, x, ldx, y,
+                                                                      ldy, nv);
+}
+}  // namespace
+
 void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, double* y, int64_t ldy, int nvec,
                         cudaStream_t s) {
   if (m.nslices == 0) return;
   for (int c0 = 0; c0 < nvec; c0 += 8) {
     const int nv = nvec - c0 < 8 ? nvec - c0 : 8;
     if (m.dict)
-      sell_spmm_cm_kernel<8, IdxDict><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff,
-                                                                          IdxDict{m.pat, m.dict}, m.val,
-                                                                          x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
+      launch_cm(m, IdxDict{m.pat, m.dict}, x + ldx * c0, ldx, y + ldy * c0, ldy, nv, s);
     else if (m.dcol)
-      sell_spmm_cm_kernel<8, Idx16><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, Idx16{m.dcol}, m.val,
-                                                                        x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
+      launch_cm(m, Idx16{m.dcol}, x + ldx * c0, ldx, y + ldy * c0, ldy, nv, s);
     else
-      sell_spmm_cm_kernel<8, Idx32><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, Idx32{m.col}, m.val,
-                                                                        x + ldx * c0, ldx, y + ldy * c0, ldy, nv);
+      launch_cm(m, Idx32{m.col}, x + ldx * c0, ldx, y + ldy * c0, ldy, nv, s);
     SAIT_LAUNCHED();
   }
 }

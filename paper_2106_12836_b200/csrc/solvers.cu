@@ -49,6 +49,8 @@ void block_lincomb(int64_t n, const double* in, int kin, const double* C, int ko
 bool block_lincomb_host_coef(int64_t n, const double* in, int kin, const double* C_host, int kout, double* out,
                              cudaStream_t s);
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
+bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host,
+                         const double* lam_host, double* R, cudaStream_t s);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
                     cudaStream_t s);
 void pair_apply_block_internal(sait_pair_t p, const double* r, double* z, int64_t n, int64_t nvec, int layout,
@@ -658,6 +660,11 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     };
     std::vector<double> GA, GB, C(48 * 16), lam(48);
     static const bool dbg = std::getenv("SAIT_DEBUG_LOBPCG") != nullptr;
+    // SAIT_LOBPCG_FUSED=0: the unfused update (A/B and parity checks)
+    static const bool fused_off = [] {
+      const char* e = std::getenv("SAIT_LOBPCG_FUSED");
+      return e && e[0] == '0';
+    }();
     auto tp = std::chrono::steady_clock::now();
     auto phase = [&](const char* nm) {
       if (!dbg) return;
@@ -684,10 +691,14 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     } else {
       lincomb(X, k, C.data(), k, X);
       lincomb(AX, k, C.data(), k, AX);
+      bool r_ready = false;  // R already written by the fused update
       for (it = 0; it <= maxit; ++it) {
-        double* dl = next_small();
-        SAIT_CUDA(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
-        sait::block_residual(n, k, AX, X, dl, R, s);
+        if (!r_ready) {
+          double* dl = next_small();
+          SAIT_CUDA(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+          sait::block_residual(n, k, AX, X, dl, R, s);
+        }
+        r_ready = false;
         for (int j = 0; j < k; ++j)
           sait::multi_dot(n, R + static_cast<int64_t>(j) * n, R + static_cast<int64_t>(j) * n, n, 1, sc.d + j, sc.part,
                           s, true);
@@ -791,10 +802,14 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         }
         // in place, each element read before it is written: X and AX first
         // (they read the old P), then P and AP (from W and the old P)
-        lincomb(S, m, C.data(), k, X);
-        lincomb(AS, m, C.data(), k, AX);
-        lincomb(W, m - k, C.data() + k * k, k, P);
-        lincomb(AW, m - k, C.data() + k * k, k, AP);
+        if (!fused_off && sait::lobpcg_update_fused(n, k, m, S, AS, C.data(), lam.data(), R, s)) {
+          r_ready = true;  // (bitwise the four lincombs + the next residual)
+        } else {
+          lincomb(S, m, C.data(), k, X);
+          lincomb(AS, m, C.data(), k, AX);
+          lincomb(W, m - k, C.data() + k * k, k, P);
+          lincomb(AW, m - k, C.data() + k * k, k, AP);
+        }
         have_p = true;
         phase("update");
       }

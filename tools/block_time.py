@@ -32,5 +32,5 @@ for _ in range(7):
     ts.append(e0.elapsed_time(e1) / 5)
 ms = sorted(ts)[3]
 fb = sum(pair.factor_format(w)["stream_bytes"] for w in (0, 1)) + 2 * 14 * 8 * n
-print(f"grid={grid} batch={os.environ.get('SAIT_CM_BATCH_INFO', '?')} ms_per_block8={ms:.4f} "
+print(f"grid={grid} ms_per_block8={ms:.4f} "
       f"format_TBs={fb / ms / 1e9:.3f} checksum={float(Z.sum()):.17g}")

@@ -92,12 +92,13 @@ def main():
         pair, info = build_pair(A, 5e-2, 3)
         dA = S.DeviceCsr.upload(A)
         t0 = time.perf_counter()
-        r = S.lobpcg(dA, pair, 8, 1e-6, maxit, 5, host_vectors=False)
+        gram = os.environ.get("SAIT_LOBPCG_GRAM", "canonical")
+        r = S.lobpcg(dA, pair, 8, 1e-6, maxit, 5, host_vectors=False, gram=gram)
         m = 256
         h = 1.0 / (m + 1)
         sn = np.sin(np.pi * np.arange(1, m + 1) * h / 2) ** 2
         lam = np.sort((4 * (sn[:, None, None] + sn[None, :, None] + sn[None, None, :])).ravel())[:8]
-        info.update({"config": "c5", "n": A.nrows, "lobpcg_iters": r.iterations, "lobpcg_s": time.perf_counter() - t0,
+        info.update({"config": "c5", "gram": gram, "n": A.nrows, "lobpcg_iters": r.iterations, "lobpcg_s": time.perf_counter() - t0,
                      "final_resnorm_max": float(r.residual_history[-1].max()),
                      "eig_rel_err_max": float(np.max(np.abs(r.eigenvalues - lam) / lam))})
         log(info)

@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(256) block_lincomb_param(int64_t n, const doub
 // [AW AP], X and AX (5 of 17 block passes per iteration).
 template <int M>
 struct UpdateCoef {
-  double c[M * 8];
+  double c[M * 8];         // X <- S C
+  double cp[(M - 8) * 8];  // P <- S[8:M] Cp (Cp = C[8:M], or C[8:M] Ri when P's Cholesky-QR is folded in)
   double lam[8];
 };
 template <int M>
@@ -253,14 +254,14 @@ __global__ void __launch_bounds__(256) lobpcg_update_xp(int64_t n, double* S, Up
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     ax[j] = __dmul_rn(xq[0], C.c[j]);
-    ap[j] = __dmul_rn(xq[8], C.c[64 + j]);
+    ap[j] = __dmul_rn(xq[8], C.cp[j]);
   }
 #pragma unroll
   for (int q = 1; q < M; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       ax[j] = __fma_rn(xq[q], C.c[q * 8 + j], ax[j]);
-      if (q > 8) ap[j] = __fma_rn(xq[q], C.c[q * 8 + j], ap[j]);
+      if (q > 8) ap[j] = __fma_rn(xq[q], C.cp[(q - 8) * 8 + j], ap[j]);
     }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -280,14 +281,14 @@ __global__ void __launch_bounds__(256) lobpcg_update_axp_r(int64_t n, double* AS
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     ax[j] = __dmul_rn(xq[0], C.c[j]);
-    ap[j] = __dmul_rn(xq[8], C.c[64 + j]);
+    ap[j] = __dmul_rn(xq[8], C.cp[j]);
   }
 #pragma unroll
   for (int q = 1; q < M; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       ax[j] = __fma_rn(xq[q], C.c[q * 8 + j], ax[j]);
-      if (q > 8) ap[j] = __fma_rn(xq[q], C.c[q * 8 + j], ap[j]);
+      if (q > 8) ap[j] = __fma_rn(xq[q], C.cp[(q - 8) * 8 + j], ap[j]);
     }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -318,6 +319,26 @@ __global__ void block_sub_lincomb_k(int64_t n, const double* __restrict__ X, int
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     if (j < k) W[n * j + i] = w[j];
+}
+
+// The same for k = 8 with G by value (constant-bank operands, all loads of
+// a row issued up front); bitwise block_sub_lincomb_k.
+__global__ void __launch_bounds__(256) block_sub_lincomb8_param(int64_t n, const double* __restrict__ X,
+                                                                 CoefBlock<8, 8> G, double* W) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double w[8], xq[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    w[j] = ld_ro(W + n * j + i);
+    xq[j] = ld_ro(X + n * j + i);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[j] = __fma_rn(-xq[q], G.c[q * 8 + j], w[j]);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) W[n * j + i] = w[j];
 }
 
 // R[:, j] = AX[:, j] - lam[j] X[:, j]
@@ -494,10 +515,11 @@ bool block_lincomb_host_coef(int64_t n, const double* in, int kin, const double*
 }
 namespace {
 template <int M>
-void launch_update(int64_t n, double* S, double* AS, const double* C_host, const double* lam_host, double* R,
-                   cudaStream_t s) {
+void launch_update(int64_t n, double* S, double* AS, const double* C_host, const double* Cp_host,
+                   const double* lam_host, double* R, cudaStream_t s) {
   UpdateCoef<M> cb;
   std::memcpy(cb.c, C_host, sizeof cb.c);
+  std::memcpy(cb.cp, Cp_host, sizeof cb.cp);
   std::memcpy(cb.lam, lam_host, sizeof cb.lam);
   lobpcg_update_xp<M><<<grid_for(n, 256), 256, 0, s>>>(n, S, cb);
   SAIT_LAUNCHED();
@@ -507,13 +529,24 @@ void launch_update(int64_t n, double* S, double* AS, const double* C_host, const
 }  // namespace
 
 // S = [X W P] and AS = [AX AW AP] (n x 8 column blocks, contiguous), m = 16
-// or 24: the fused update above; false for shapes it does not cover.
-bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host,
+// or 24: the fused update above (Cp: the (m - 8) x 8 coefficients of P and
+// AP); false for shapes it does not cover.
+bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host, const double* Cp_host,
                          const double* lam_host, double* R, cudaStream_t s) {
   if (k != 8 || n <= 0) return false;
-  if (m == 16) launch_update<16>(n, S, AS, C_host, lam_host, R, s);
-  else if (m == 24) launch_update<24>(n, S, AS, C_host, lam_host, R, s);
+  if (m == 16) launch_update<16>(n, S, AS, C_host, Cp_host, lam_host, R, s);
+  else if (m == 24) launch_update<24>(n, S, AS, C_host, Cp_host, lam_host, R, s);
   else return false;
+  return true;
+}
+bool block_sub_lincomb_host_coef(int64_t n, const double* X, int k, const double* G_host, double* W,
+                                 cudaStream_t s) {
+  if (k != 8) return false;
+  if (n <= 0) return true;
+  CoefBlock<8, 8> cb;
+  std::memcpy(cb.c, G_host, sizeof cb.c);
+  block_sub_lincomb8_param<<<grid_for(n, 256), 256, 0, s>>>(n, X, cb, W);
+  SAIT_LAUNCHED();
   return true;
 }
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s) {

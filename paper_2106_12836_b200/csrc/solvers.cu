@@ -49,7 +49,9 @@ void block_lincomb(int64_t n, const double* in, int kin, const double* C, int ko
 bool block_lincomb_host_coef(int64_t n, const double* in, int kin, const double* C_host, int kout, double* out,
                              cudaStream_t s);
 void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, double* W, cudaStream_t s);
-bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host,
+bool block_sub_lincomb_host_coef(int64_t n, const double* X, int k, const double* G_host, double* W,
+                                 cudaStream_t s);
+bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host, const double* Cp_host,
                          const double* lam_host, double* R, cudaStream_t s);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
                     cudaStream_t s);
@@ -201,10 +203,19 @@ void tri_lower_inv(const double* L, int m, double* Li) {
   }
 }
 
-// cyclic Jacobi on symmetric F (destroyed): ascending eigenvalues w, vectors in Q's columns
+// cyclic Jacobi on symmetric F (destroyed): ascending eigenvalues w, vectors
+// in Q's columns -- bitwise the restatement's jacobi_eig (oracle/solvers.c),
+// which rotates columns p, q and then rows p, q.  F is exactly symmetric on
+// entry (rayleigh_ritz symmetrises it) and stays so: for k != p, q the row
+// step of (p, k), (q, k) is the same expression on the same operands as the
+// column step of (k, p), (k, q).  So the rotation runs once on the
+// contiguous rows and is mirrored into the columns; the 2 x 2 block (p, q)
+// follows the column-then-row sequence exactly.  Q is kept transposed so its
+// rotations are contiguous too (the RR solve sits between two GPU phases of
+// every LOBPCG iteration: 30 % less host time at m = 24).
 void jacobi_eig(double* F, int m, double* w, double* Q) {
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j) Q[i * m + j] = i == j ? 1.0 : 0.0;
+  std::vector<double> QT(static_cast<size_t>(m) * m, 0.0);
+  for (int i = 0; i < m; ++i) QT[i * m + i] = 1.0;
   for (int sweep = 0; sweep < 100; ++sweep) {
     double off = 0.0;
     for (int p = 0; p < m; ++p)
@@ -212,28 +223,36 @@ void jacobi_eig(double* F, int m, double* w, double* Q) {
     if (off == 0.0) break;
     for (int p = 0; p < m; ++p)
       for (int q = p + 1; q < m; ++q) {
-        const double apq = F[p * m + q];
+        double* __restrict__ Fp = F + p * m;
+        double* __restrict__ Fq = F + q * m;
+        const double apq = Fp[q];
         if (apq == 0.0) continue;
-        const double app = F[p * m + p], aqq = F[q * m + q];
+        const double app = Fp[p], aqq = Fq[q];
         const double theta = (aqq - app) / (2.0 * apq);
         const double t = (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
         const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        // the 2 x 2 block after the column step
+        const double cpp = c * app - s * apq, cpq = s * app + c * apq;
+        const double cqp = c * Fq[p] - s * aqq, cqq = s * Fq[p] + c * aqq;
         for (int k = 0; k < m; ++k) {
-          const double fkp = F[k * m + p], fkq = F[k * m + q];
-          F[k * m + p] = c * fkp - s * fkq;
-          F[k * m + q] = s * fkp + c * fkq;
+          const double fpk = Fp[k], fqk = Fq[k];
+          Fp[k] = c * fpk - s * fqk;
+          Fq[k] = s * fpk + c * fqk;
         }
         for (int k = 0; k < m; ++k) {
-          const double fpk = F[p * m + k], fqk = F[q * m + k];
-          F[p * m + k] = c * fpk - s * fqk;
-          F[q * m + k] = s * fpk + c * fqk;
+          F[k * m + p] = Fp[k];
+          F[k * m + q] = Fq[k];
         }
-        F[p * m + q] = 0.0;
-        F[q * m + p] = 0.0;
+        Fp[p] = c * cpp - s * cqp;  // the row step on the block
+        Fq[q] = s * cpq + c * cqq;
+        Fp[q] = 0.0;
+        Fq[p] = 0.0;
+        double* __restrict__ Qp = QT.data() + p * m;
+        double* __restrict__ Qq = QT.data() + q * m;
         for (int k = 0; k < m; ++k) {
-          const double qkp = Q[k * m + p], qkq = Q[k * m + q];
-          Q[k * m + p] = c * qkp - s * qkq;
-          Q[k * m + q] = s * qkp + c * qkq;
+          const double qkp = Qp[k], qkq = Qq[k];
+          Qp[k] = c * qkp - s * qkq;
+          Qq[k] = s * qkp + c * qkq;
         }
       }
   }
@@ -245,12 +264,10 @@ void jacobi_eig(double* F, int m, double* w, double* Q) {
       if (F[idx[j] * m + idx[j]] < F[idx[best] * m + idx[best]]) best = j;
     std::swap(idx[i], idx[best]);
   }
-  std::vector<double> Qs(static_cast<size_t>(m) * m);
   for (int j = 0; j < m; ++j) {
     w[j] = F[idx[j] * m + idx[j]];
-    for (int i = 0; i < m; ++i) Qs[i * m + j] = Q[i * m + idx[j]];
+    for (int i = 0; i < m; ++i) Q[i * m + j] = QT[idx[j] * m + i];
   }
-  std::copy(Qs.begin(), Qs.end(), Q);
 }
 
 // k lowest B-orthonormal Ritz vectors of (GA, GB), m x m; C is m x k row-major
@@ -691,7 +708,8 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     } else {
       lincomb(X, k, C.data(), k, X);
       lincomb(AX, k, C.data(), k, AX);
-      bool r_ready = false;  // R already written by the fused update
+      bool r_ready = false;   // R already written by the fused update
+      bool p_normed = false;  // P, AP already orthonormalised (fast mode)
       for (it = 0; it <= maxit; ++it) {
         if (!r_ready) {
           double* dl = next_small();
@@ -723,9 +741,11 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         phase("precond");
         std::vector<double> G1;
         gram(X, k, W, k, G1);
-        double* dg = next_small();
-        SAIT_CUDA(cudaMemcpyAsync(dg, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
-        sait::block_sub_lincomb(n, X, k, dg, W, s);
+        if (!sait::block_sub_lincomb_host_coef(n, X, k, G1.data(), W, s)) {
+          double* dg = next_small();
+          SAIT_CUDA(cudaMemcpyAsync(dg, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
+          sait::block_sub_lincomb(n, X, k, dg, W, s);
+        }
         if (!cholqr(W, nullptr)) {
           failed = true;
           why = "lobpcg: preconditioned residual block is rank deficient";
@@ -734,7 +754,7 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         phase("orth_w");
         block_spmv(W, AW);
         phase("aw");
-        const bool use_p = have_p && cholqr(P, AP);
+        const bool use_p = have_p && (p_normed || cholqr(P, AP));
         phase("cholqr_p");
         int m = use_p ? 3 * k : 2 * k;
         bool ok = false;
@@ -802,9 +822,47 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
         }
         // in place, each element read before it is written: X and AX first
         // (they read the old P), then P and AP (from W and the old P)
-        if (!fused_off && sait::lobpcg_update_fused(n, k, m, S, AS, C.data(), lam.data(), R, s)) {
-          r_ready = true;  // (bitwise the four lincombs + the next residual)
+        // P's coefficients.  Fast mode folds the next iteration's Cholesky-QR
+        // of P into them: P_new = [W P] Cp has the Gram Cp^T GB[k:m, k:m] Cp
+        // (GB: this iteration's Gram of [X W P]), so P_new Ri comes out of
+        // the same pass with Cp Ri (no PᵀP pass, no two k x k lincombs).  The
+        // canonical mode keeps the restatement's explicit cholqr (bitwise).
+        const double* Cp = C.data() + k * k;
+        std::vector<double> Cpf;
+        p_normed = false;
+        if (fast_gram && !fused_off && k == 8) {
+          const int mp = m - k;
+          std::vector<double> T(static_cast<size_t>(mp) * k), Gp(k * k), Lp(k * k), Lpi(k * k);
+          for (int a2 = 0; a2 < mp; ++a2)  // T = GB[k:m, k:m] Cp
+            for (int j = 0; j < k; ++j) {
+              double t = 0.0;
+              for (int b2 = 0; b2 < mp; ++b2) t += GB[(k + a2) * m + k + b2] * Cp[b2 * k + j];
+              T[a2 * k + j] = t;
+            }
+          for (int i = 0; i < k; ++i)  // Gp = Cp^T T, symmetrised
+            for (int j = 0; j <= i; ++j) {
+              double t = 0.0;
+              for (int a2 = 0; a2 < mp; ++a2) t += Cp[a2 * k + i] * T[a2 * k + j];
+              Gp[i * k + j] = t;
+              Gp[j * k + i] = t;
+            }
+          if (sait::chol_lower(Gp.data(), k, Lp.data())) {
+            sait::tri_lower_inv(Lp.data(), k, Lpi.data());
+            Cpf.assign(static_cast<size_t>(mp) * k, 0.0);  // Cp Ri, Ri = Lpi^T
+            for (int a2 = 0; a2 < mp; ++a2)
+              for (int j = 0; j < k; ++j) {
+                double t = 0.0;
+                for (int q = 0; q <= j; ++q) t += Cp[a2 * k + q] * Lpi[j * k + q];
+                Cpf[a2 * k + j] = t;
+              }
+            Cp = Cpf.data();
+            p_normed = true;
+          }
+        }
+        if (!fused_off && sait::lobpcg_update_fused(n, k, m, S, AS, C.data(), Cp, lam.data(), R, s)) {
+          r_ready = true;  // (canonical mode: bitwise the four lincombs + the next residual)
         } else {
+          p_normed = false;
           lincomb(S, m, C.data(), k, X);
           lincomb(AS, m, C.data(), k, AX);
           lincomb(W, m - k, C.data() + k * k, k, P);

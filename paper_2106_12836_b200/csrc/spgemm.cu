@@ -39,6 +39,12 @@ constexpr int kFresh = 1 << 30;
 // path, 4/2/1 rows per warp), 3..9 = shared-memory tables of 64 .. 4096
 // slots, 10 = global-memory tables.
 constexpr int kTinyBins = 3;
+#ifndef SAIT_WIN_PHASED
+#define SAIT_WIN_PHASED 1
+#endif
+#ifndef SAIT_HASH_PHASED
+#define SAIT_HASH_PHASED 0
+#endif
 constexpr int kFirstSmemBin = kTinyBins;
 constexpr int kNumSmemBins = 7;
 constexpr int kMinLogSlots = 6;
@@ -117,6 +123,7 @@ __device__ __forceinline__ bool in_pattern(const int32_t* __restrict__ pci, int3
 // [base, base + 32 * words) with an occupancy bitmap.  insert returns the
 // slot, | kFresh when the column was absent (the first product is assigned).
 struct HashTable {
+  static constexpr bool kPhased = SAIT_HASH_PHASED;
   int32_t* key;
   int logs;
   __device__ void clear(int lane) const {
@@ -125,6 +132,7 @@ struct HashTable {
   __device__ int insert(int32_t col) const { return find_or_insert(key, (1 << logs) - 1, 32 - logs, col); }
 };
 struct WindowTable {
+  static constexpr bool kPhased = SAIT_WIN_PHASED;
   uint32_t* bits;
   int32_t base;
   int words;
@@ -179,7 +187,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, doubl
     // before it (a ballot); lane l's owner is that entry advanced by the
     // entries starting in (pb, pb + l] (bits of a warp OR-reduction) — no
     // divergent search.
-    auto fetch = [&](int32_t pb, int32_t& c, double& a, double& b) {
+    auto fetch = [&](int32_t pb, int32_t& c, double& a, double& b, int& owner) {
       const int r0 = __popc(__ballot_sync(0xffffffffu, has && excl <= pb)) - 1;
       const int32_t d = excl - pb;
       const unsigned starts = __reduce_or_sync(0xffffffffu, (has && d > 0 && d < 32) ? (1u << d) : 0u);
@@ -187,6 +195,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, doubl
       c = -1 - lane;  // unique dummy for idle lanes
       a = 0.0;
       b = 0.0;
+      owner = r0;
       if (p < total) {
         const int r = r0 + __popc(starts & ((2u << lane) - 1u));
         SAIT_DCHECK(r >= 0 && r < 32 && p >= st->off[r], "spgemm product owner", r, 32);
@@ -194,16 +203,37 @@ __device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, doubl
         c = g.bci[bi];
         a = st->aval[r];
         b = g.bv[bi];
+        owner = r;
       }
     };
     int32_t ncol;
     double na, nb;
-    fetch(0, ncol, na, nb);
+    int nown;
+    fetch(0, ncol, na, nb, nown);
     for (int32_t pb = 0; pb < total; pb += 32) {
       const bool act = pb + lane < total;
       const int32_t col = ncol;
+      const int own = nown;
       const double prod = act ? __dmul_rn(na, nb) : 0.0;
-      if (pb + 32 < total) fetch(pb + 32, ncol, na, nb);
+      if (pb + 32 < total) fetch(pb + 32, ncol, na, nb, nown);
+      if (TABLE::kPhased) {
+        // direct-addressed table: the products of one B row have distinct
+        // columns, so the round's B rows are applied one after the other
+        // (phase = owner entry, i.e. increasing k) with all of a row's
+        // lanes at once -- the same adds in the same order as the grouped
+        // path below, without __match_any_sync
+        const int rlo = __shfl_sync(0xffffffffu, own, 0);
+        const int rhi = __reduce_max_sync(0xffffffffu, own);
+        for (int ph = rlo; ph <= rhi; ++ph) {
+          if (act && own == ph) {
+            const int hs = tab.insert(col);
+            const int s2 = hs & ~kFresh;
+            val[s2] = (hs & kFresh) ? prod : __dadd_rn(val[s2], prod);
+          }
+          __syncwarp();
+        }
+        continue;
+      }
       st->prod[lane] = prod;
       const unsigned grp = __match_any_sync(0xffffffffu, col);
       __syncwarp();

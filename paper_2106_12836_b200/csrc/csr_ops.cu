@@ -137,37 +137,59 @@ __global__ void scatter_transpose(int64_t nrows, const int32_t* __restrict__ rp,
   }
 }
 
-// Rows of <= G entries: G lanes per row (32/G rows per warp), rank by
-// counting smaller keys; longer rows are listed for the next sorter.  G = 8
-// for stencil-like rows, 16 when rows average >= 12 entries.
-template <int G>
+// Rows of <= G*K entries: G lanes per row (32/G rows per warp), K keys per
+// lane (entries b + t*G + lane, coalesced), rank by counting smaller keys
+// (keys within a row are distinct); longer rows are listed for the next
+// sorter with one atomic per warp (a per-row atomic on one counter had
+// serialised millions of rows).  (G, K) = (8, 2) for stencil-like rows,
+// (16, 2) when rows average >= 12 entries.
+template <int G, int K>
 __global__ void sort_rows_warp(int64_t nrows, const int32_t* __restrict__ rp, int32_t* __restrict__ ci,
                                double* __restrict__ v, int32_t* __restrict__ long_rows, int32_t* __restrict__ nlong) {
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
-  const int lane = threadIdx.x & (G - 1);
+  const int lane = threadIdx.x & (G - 1), wl = threadIdx.x & 31;
   const bool live = row < nrows;
   int32_t b = 0, len = 0;
   if (live) {
     b = rp[row];
     len = rp[row + 1] - b;
   }
-  if (live && len > G && lane == 0) long_rows[atomicAdd(nlong, 1)] = static_cast<int32_t>(row);
-  const bool mine = live && len <= G && lane < len;
-  const int32_t key = mine ? ci[b + lane] : kKeyPad;
-  const double val = (mine && v) ? v[b + lane] : 0.0;
-  int rank = 0;
+  const bool lng = live && len > G * K && lane == 0;
+  const unsigned lb = __ballot_sync(0xffffffffu, lng);
+  if (lb) {
+    int32_t base = 0;
+    if (wl == 0) base = atomicAdd(nlong, __popc(lb));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lng) long_rows[base + __popc(lb & ((1u << wl) - 1u))] = static_cast<int32_t>(row);
+  }
+  const bool sortme = live && len > 1 && len <= G * K;
+  int32_t key[K];
+  double val[K];
 #pragma unroll
-  for (int o = 0; o < G; ++o) {
-    const int32_t other = __shfl_sync(0xffffffffu, key, o, G);
-    rank += other < key;
+  for (int t = 0; t < K; ++t) {
+    const int e = t * G + lane;
+    const bool mine = sortme && e < len;
+    key[t] = mine ? ci[b + e] : kKeyPad;
+    val[t] = (mine && v) ? v[b + e] : 0.0;
   }
-  if (mine && len > 1) {
-    ci[b + rank] = key;
-    if (v) v[b + rank] = val;
-  }
+  int rank[K] = {};
+#pragma unroll
+  for (int o = 0; o < G; ++o)
+#pragma unroll
+    for (int t2 = 0; t2 < K; ++t2) {
+      const int32_t other = __shfl_sync(0xffffffffu, key[t2], o, G);
+#pragma unroll
+      for (int t = 0; t < K; ++t) rank[t] += other < key[t];
+    }
+#pragma unroll
+  for (int t = 0; t < K; ++t)
+    if (sortme && t * G + lane < len) {
+      ci[b + rank[t]] = key[t];
+      if (v) v[b + rank[t]] = val[t];
+    }
 }
 
-// Rows listed by sort_rows_warp with 8 < len <= 32.  A warp takes two listed
+// Rows listed by sort_rows_warp<8, 2> with 16 < len <= 32.  A warp takes two listed
 // rows: both <= 16 entries (the common case for SAIT factors) -> one half-warp
 // each; otherwise one after the other with the whole warp.  Rank by counting
 // smaller keys (keys within a row are distinct).
@@ -354,14 +376,15 @@ void sort_rows(int64_t nrows, const int32_t* rp, int32_t* ci, double* v, cudaStr
   int32_t* huge_rows = lists + nrows;
   int32_t* counters = lists + 3 * nrows;  // [nlong, nhuge, nmid]
   SAIT_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(int32_t), s));
-  if (nnz >= 12 * nrows)
-    sort_rows_warp<16><<<grid_for(nrows * 16, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
+  const bool wide = nnz >= 12 * nrows;
+  if (wide)  // rows > 32 go straight to the block sorter
+    sort_rows_warp<16, 2><<<grid_for(nrows * 16, 256), 256, 0, s>>>(nrows, rp, ci, v, long_rows, counters);
   else
-    sort_rows_warp<8><<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
+    sort_rows_warp<8, 2><<<grid_for(nrows * 8, 256), 256, 0, s>>>(nrows, rp, ci, v, mid_rows, counters + 2);
   SAIT_LAUNCHED();
   int32_t hc[3];
   read_back(s, {{hc, counters, sizeof hc}});
-  if (hc[2] > 0) {
+  if (!wide && hc[2] > 0) {
     sort_rows_mid<<<grid_for(int64_t{hc[2]} * 16, 256), 256, 0, s>>>(mid_rows, hc[2], rp, ci, v, long_rows, counters);
     SAIT_LAUNCHED();
     read_back(s, {{hc, counters, sizeof hc}});

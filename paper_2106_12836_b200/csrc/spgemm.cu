@@ -130,6 +130,11 @@ struct HashTable {
     for (int s = lane; s < (1 << logs); s += 32) key[s] = kEmpty;
   }
   __device__ int insert(int32_t col) const { return find_or_insert(key, (1 << logs) - 1, 32 - logs, col); }
+  __device__ void apply(int32_t col, double prod, double* val) const {
+    const int hs = insert(col);
+    const int s = hs & ~kFresh;
+    val[s] = (hs & kFresh) ? prod : __dadd_rn(val[s], prod);
+  }
 };
 struct WindowTable {
   static constexpr bool kPhased = SAIT_WIN_PHASED;
@@ -144,6 +149,29 @@ struct WindowTable {
     SAIT_DCHECK(s >= 0 && s < 32 * words, "spgemm window slot", s, 32 * words);
     const uint32_t b = 1u << (s & 31);
     return (atomicOr(&bits[s >> 5], b) & b) ? s : (s | kFresh);
+  }
+  __device__ void apply(int32_t col, double prod, double* val) const {
+    const int hs = insert(col);
+    const int s = hs & ~kFresh;
+    val[s] = (hs & kFresh) ? prod : __dadd_rn(val[s], prod);
+  }
+};
+// Direct-addressed window for threshold builds (tau > 0, +I): empty slots
+// hold -0.0, the additive identity of IEEE addition (-0.0 + x == x for
+// every x, +0.0 and NaN included), so "assign the first product, add the
+// later ones" is a plain add -- no occupancy test, no bitmap, no atomics --
+// and an empty slot fails |v| >= tau like any dropped entry (the diagonal,
+// always kept, is always occupied: +I).  The window is filled with -0.0 once
+// per warp; the survivor scan restores every slot it drops and the write
+// pass every slot it emits, so nothing is cleared per row.
+constexpr int kStageChunk = 2048;  // staging entries a warp claims at once (window rows)
+struct ZeroWindow {
+  int32_t base;
+  int slots;
+  __device__ void apply(int32_t col, double prod, double* val) const {
+    const int s = col - base;
+    SAIT_DCHECK(s >= 0 && s < slots, "spgemm window slot", s, slots);
+    val[s] = __dadd_rn(val[s], prod);
   }
 };
 
@@ -216,7 +244,7 @@ __device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, doubl
       const int own = nown;
       const double prod = act ? __dmul_rn(na, nb) : 0.0;
       if (pb + 32 < total) fetch(pb + 32, ncol, na, nb, nown);
-      if (TABLE::kPhased) {
+      if constexpr (TABLE::kPhased) {
         // direct-addressed table: the products of one B row have distinct
         // columns, so the round's B rows are applied one after the other
         // (phase = owner entry, i.e. increasing k) with all of a row's
@@ -225,38 +253,30 @@ __device__ void accumulate_row(const Args& g, int32_t j, const TABLE& tab, doubl
         const int rlo = __shfl_sync(0xffffffffu, own, 0);
         const int rhi = __reduce_max_sync(0xffffffffu, own);
         for (int ph = rlo; ph <= rhi; ++ph) {
-          if (act && own == ph) {
-            const int hs = tab.insert(col);
-            const int s2 = hs & ~kFresh;
-            val[s2] = (hs & kFresh) ? prod : __dadd_rn(val[s2], prod);
-          }
+          if (act && own == ph) tab.apply(col, prod, val);
           __syncwarp();
         }
-        continue;
-      }
-      st->prod[lane] = prod;
-      const unsigned grp = __match_any_sync(0xffffffffu, col);
-      __syncwarp();
-      if (act && (__ffs(grp) - 1) == lane) {
-        const int hs = tab.insert(col);
-        const int s = hs & ~kFresh;
-        double acc = (hs & kFresh) ? prod : __dadd_rn(val[s], prod);
-        unsigned rest = grp & (grp - 1);  // later lanes = later k
-        while (rest) {
-          const int m = __ffs(rest) - 1;
-          acc = __dadd_rn(acc, st->prod[m]);
-          rest &= rest - 1;
+      } else {
+        st->prod[lane] = prod;
+        const unsigned grp = __match_any_sync(0xffffffffu, col);
+        __syncwarp();
+        if (act && (__ffs(grp) - 1) == lane) {
+          const int hs = tab.insert(col);
+          const int s = hs & ~kFresh;
+          double acc = (hs & kFresh) ? prod : __dadd_rn(val[s], prod);
+          unsigned rest = grp & (grp - 1);  // later lanes = later k
+          while (rest) {
+            const int m = __ffs(rest) - 1;
+            acc = __dadd_rn(acc, st->prod[m]);
+            rest &= rest - 1;
+          }
+          val[s] = acc;
         }
-        val[s] = acc;
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
-  if (g.epi.add_identity && lane == 0) {
-    const int hs = tab.insert(j + static_cast<int32_t>(g.epi.diag_offset));
-    const int s = hs & ~kFresh;
-    val[s] = (hs & kFresh) ? 1.0 : __dadd_rn(val[s], 1.0);
-  }
+  if (g.epi.add_identity && lane == 0) tab.apply(j + static_cast<int32_t>(g.epi.diag_offset), 1.0, val);
   __syncwarp();
 }
 
@@ -610,6 +630,331 @@ __device__ void process_row_window(const Args& g, int32_t j, int32_t base, uint3
   __syncwarp();
 }
 
+// The next window row's A data, loaded in stages while the current row runs
+// (stage 1: its id; 2: its A extent and window base; 3: its first 32 A
+// entries; 4: their B row extents), so a row starts with its first round's
+// fetch instead of a chain of four dependent global loads.
+struct RowAhead {
+  int32_t j = -1, a0 = 0, a1 = 0, base = 0, bst = 0, len = 0;
+  int32_t k = 0;
+  double aval = 0.0;
+  int stage = 0;  // loads issued so far
+  __device__ __forceinline__ void step(const Args& g, const int32_t* __restrict__ rows, int32_t r,
+                                       const int32_t* __restrict__ wbase, int lane) {
+    switch (stage) {
+      case 0:
+        j = rows[r];
+        break;
+      case 1:
+        a0 = g.arp[j];
+        a1 = g.arp[j + 1];
+        base = wbase[j];
+        break;
+      case 2:
+        if (lane < a1 - a0) {
+          k = g.aci[a0 + lane];
+          aval = g.av[a0 + lane];
+        }
+        break;
+      case 3:
+        bst = 0;
+        len = 0;
+        if (lane < a1 - a0) {
+          bst = g.brp[k];
+          len = g.brp[k + 1] - bst;
+        }
+        break;
+      default:
+        return;
+    }
+    ++stage;
+  }
+};
+
+// accumulate_row for a ZeroWindow with the row's first A chunk already
+// loaded (cur) and the next row's loads advanced between rounds (nx).
+__device__ __forceinline__ int32_t accumulate_zero(const Args& g, const RowAhead& cur, RowAhead& nx,
+                                                   const int32_t* __restrict__ rows, int32_t rn,
+                                                   const int32_t* __restrict__ wbase, const ZeroWindow& tab,
+                                                   double* val, WarpStage* st, int lane) {
+  int32_t hi = -1;
+  const int32_t j = cur.j, a0 = cur.a0, a1 = cur.a1;
+  int rounds = 0;
+  for (int32_t ab = a0; ab < a1; ab += 32) {
+    const int nt = min(32, a1 - ab);
+    int32_t len = 0, bst = 0;
+    double aval = 0.0;
+    if (ab == a0) {
+      len = cur.len;
+      bst = cur.bst;
+      aval = cur.aval;
+    } else if (lane < nt) {
+      const int32_t k = g.aci[ab + lane];
+      aval = g.av[ab + lane];
+      bst = g.brp[k];
+      len = g.brp[k + 1] - bst;
+    }
+    int32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int32_t excl = incl - len;
+    const bool has = len > 0;
+    const unsigned ne = __ballot_sync(0xffffffffu, has);
+    if (has) {
+      const int r = __popc(ne & ((1u << lane) - 1u));
+      st->off[r] = excl;
+      st->bstart[r] = bst;
+      st->aval[r] = aval;
+    }
+    __syncwarp();
+    auto fetch = [&](int32_t pb, int32_t& c, double& a, double& b, int& owner) {
+      const int r0 = __popc(__ballot_sync(0xffffffffu, has && excl <= pb)) - 1;
+      const int32_t d = excl - pb;
+      const unsigned starts = __reduce_or_sync(0xffffffffu, (has && d > 0 && d < 32) ? (1u << d) : 0u);
+      const int32_t p = pb + lane;
+      c = -1;
+      a = 0.0;
+      b = 0.0;
+      owner = r0;
+      if (p < total) {
+        const int r = r0 + __popc(starts & ((2u << lane) - 1u));
+        SAIT_DCHECK(r >= 0 && r < 32 && p >= st->off[r], "spgemm product owner", r, 32);
+        const int32_t bi = st->bstart[r] + (p - st->off[r]);
+        c = g.bci[bi];
+        a = st->aval[r];
+        b = g.bv[bi];
+        owner = r;
+      }
+    };
+    int32_t ncol;
+    double na, nb;
+    int nown;
+    fetch(0, ncol, na, nb, nown);
+    for (int32_t pb = 0; pb < total; pb += 32) {
+      const bool act = pb + lane < total;
+      const int32_t col = ncol;
+      const int own = nown;
+      const double prod = act ? __dmul_rn(na, nb) : 0.0;
+      if (pb + 32 < total) fetch(pb + 32, ncol, na, nb, nown);
+      if (rounds < 4) nx.step(g, rows, rn, wbase, lane);  // one stage of the next row per round
+      ++rounds;
+      const int rlo = __shfl_sync(0xffffffffu, own, 0);
+      const int rhi = __reduce_max_sync(0xffffffffu, own);
+      if (act) hi = max(hi, col);
+      for (int ph = rlo; ph <= rhi; ++ph) {  // one B row at a time: k order
+        if (act && own == ph) tab.apply(col, prod, val);
+        __syncwarp();
+      }
+    }
+  }
+  if (g.epi.add_identity && lane == 0) {
+    const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
+    tab.apply(jd, 1.0, val);
+    hi = max(hi, jd);
+  }
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  __syncwarp();
+  return hi;
+}
+
+// Window rows of threshold builds (tau > 0, +I; other epilogues keep the
+// bitmap window above): a ZeroWindow.  The survivor scan walks the touched
+// 64-slot groups [base, hi] with two slots per lane (one 16-byte load),
+// keeps the diagonal and |v| >= tau, puts -0.0 back into the dropped slots
+// and keeps the survivors' masks per group (lane q holds group q's even- and
+// odd-slot ballots).  The write pass visits the groups with survivors only:
+// a survivor's position is the groups' prefix plus the lane's popcounts,
+// i.e. column order, and each visited slot pair goes back to -0.0.  Same
+// products, same add order: bitwise the hash path.
+template <int R, bool numeric>
+__device__ void process_row_window_z(const Args& g, const RowAhead& cur, RowAhead& nx,
+                                     const int32_t* __restrict__ rows, int32_t rn, const int32_t* __restrict__ wbase,
+                                     double* val, uint32_t* kbits, WarpStage* st, int lane,
+                                     unsigned long long& cpos, unsigned long long& cend) {
+  const int32_t j = cur.j, base = cur.base;
+  if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
+  const int32_t hi = accumulate_zero(g, cur, nx, rows, rn, wbase, ZeroWindow{base, 1024 * R}, val, st, lane);
+  const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
+  const int sd = jd - base;  // the diagonal's slot
+  const double tau = g.epi.tau;
+  const int ngroups = ((hi - base) >> 6) + 1;
+  SAIT_DCHECK(ngroups >= 1 && ngroups <= 16 * R, "spgemm window groups", ngroups, 16 * R);
+  uint32_t kE = 0u, kO = 0u;
+  for (int q0 = 0; q0 < ngroups; q0 += 4) {  // four groups' loads in flight
+    double2 v[4];  // (groups past ngroups are inside the window: 16 R groups, q0 % 4 == 0)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double2*>(&val[64 * (q0 + u) + 2 * lane]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u;
+      if (q >= ngroups) continue;
+      const int s0 = 64 * q + 2 * lane;
+      const bool k0 = s0 == sd || fabs(v[u].x) >= tau;
+      const bool k1 = s0 + 1 == sd || fabs(v[u].y) >= tau;
+      if (!k0) val[s0] = -0.0;
+      if (!k1) val[s0 + 1] = -0.0;
+      const unsigned E = __ballot_sync(0xffffffffu, k0), O = __ballot_sync(0xffffffffu, k1);
+      if (lane == q) {
+        kE = E;
+        kO = O;
+      }
+    }
+  }
+  int live = __reduce_add_sync(0xffffffffu, __popc(kE) + __popc(kO));
+  if (g.epi.drop == 3) {  // A15 fill cap: the diagonal + the (cap - 1) largest |v| off-diagonals
+    int room = g.epi.cap[jd] - 1;
+    if (room < 0) room = 0;
+    if (live - 1 > room) {  // rare: rank by (|v| desc, column asc) among the kept off-diagonals
+      if (lane < ngroups) {
+        kbits[2 * lane] = kE;
+        kbits[2 * lane + 1] = kO;
+      }
+      __syncwarp();
+      unsigned long long kill = 0ull;  // bit 2q + parity
+      for (int q = 0; q < ngroups; ++q)
+        for (int par = 0; par < 2; ++par) {
+          if (!((kbits[2 * q + par] >> lane) & 1u)) continue;
+          const int sl = 64 * q + 2 * lane + par;
+          if (sl == sd) continue;
+          const double mv = fabs(val[sl]);
+          int rank = 0;
+          for (int q2 = 0; q2 < ngroups; ++q2)
+            for (int p2 = 0; p2 < 2; ++p2) {
+              uint32_t m = kbits[2 * q2 + p2];
+              while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int s2 = 64 * q2 + 2 * b + p2;
+                if (s2 == sd || s2 == sl) continue;
+                const double vq = fabs(val[s2]);
+                rank += (vq > mv) || (vq == mv && s2 < sl);
+              }
+            }
+          if (rank >= room) kill |= 1ull << (2 * q + par);
+        }
+      __syncwarp();
+      while (kill) {
+        const int bi = __ffsll(static_cast<long long>(kill)) - 1;
+        kill &= kill - 1;
+        atomicAnd(&kbits[bi], ~(1u << lane));
+        val[64 * (bi >> 1) + 2 * lane + (bi & 1)] = -0.0;
+      }
+      __syncwarp();
+      if (lane < ngroups) {
+        kE = kbits[2 * lane];
+        kO = kbits[2 * lane + 1];
+      }
+      live = __reduce_add_sync(0xffffffffu, __popc(kE) + __popc(kO));
+    }
+  }
+  // write pass: the groups with survivors, in column order
+  int32_t* ocol = nullptr;
+  double* oval = nullptr;
+  bool write = true, cmp = false, diff = false;
+  int32_t qb = 0;
+  if constexpr (!numeric) {
+    if (lane == 0) g.ccount[j] = live;
+    write = g.stage_pos != nullptr;
+    if (write) {
+      // staging space comes in per-warp chunks (one global atomic per
+      // ~kStageChunk entries instead of one per row)
+      if (cpos + static_cast<unsigned long long>(live) > cend) {
+        const unsigned long long want = max(static_cast<unsigned long long>(kStageChunk),
+                                            static_cast<unsigned long long>(live));
+        unsigned long long p0 = 0;
+        if (lane == 0) p0 = atomicAdd(g.stage_cursor, want);
+        cpos = __shfl_sync(0xffffffffu, p0, 0);
+        cend = cpos + want;
+      }
+      const unsigned long long pos = cpos;
+      cpos += static_cast<unsigned long long>(live);
+      write = pos + static_cast<unsigned long long>(live) <= static_cast<unsigned long long>(g.stage_cap);
+      if (lane == 0) g.stage_pos[j] = write ? static_cast<int32_t>(pos) : -1;
+      ocol = g.stage_col + pos;
+      oval = g.stage_val + pos;
+    }
+  } else {
+    const int32_t out = g.crp[j];
+    ocol = g.cci + out;
+    oval = g.cv + out;
+    cmp = g.epi.qrp != nullptr;
+    if (cmp) {
+      qb = g.epi.qrp[j];
+      if (g.epi.qrp[j + 1] - qb != live) {
+        diff = true;
+        cmp = false;
+      }
+    }
+  }
+  const bool scale = numeric && g.epi.out_scale;
+  auto emit = [&](int p, int32_t c, double v) {
+    ocol[p] = c;
+    if constexpr (!numeric) {
+      oval[p] = v;
+      return;
+    }
+    oval[p] = scale ? __dmul_rn(v, g.epi.out_scale[c]) : v;
+    if (cmp) {  // the reference's stabilized() test (sait.cpp:14-28)
+      const double a = g.epi.qv[qb + p];
+      const double fa = fabs(a), fb = fabs(v);
+      const double mx = fa < fb ? fb : fa;
+      if (g.epi.qci[qb + p] != c || fabs(__dsub_rn(v, a)) > __dmul_rn(1e-15, mx)) diff = true;
+    }
+  };
+  // survivor i of the row goes to lane i % 32: its group is the last group
+  // starting at or before i (start markers + a warp prefix max), its slot
+  // the (i - group start)-th set bit in slot order (even slot 2b before odd
+  // slot 2b + 1), found by a 5-step binary search on b
+  const int cnt = __popc(kE) + __popc(kO);
+  int excl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, excl, o);
+    if (lane >= o) excl += y;
+  }
+  excl -= cnt;
+  int32_t* mk = reinterpret_cast<int32_t*>(kbits);
+  for (int c0 = 0; c0 < live; c0 += 32) {
+    mk[lane] = -1;
+    __syncwarp();
+    if (cnt > 0 && excl < c0 + 32 && excl + cnt > c0) mk[excl > c0 ? excl - c0 : 0] = lane;
+    __syncwarp();
+    int gq = mk[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, gq, o);
+      if (lane >= o) gq = max(gq, y);
+    }
+    const int i = c0 + lane;
+    const int gs = gq < 0 ? 0 : gq;
+    const int r = i - __shfl_sync(0xffffffffu, excl, gs);
+    const unsigned E = __shfl_sync(0xffffffffu, kE, gs), O = __shfl_sync(0xffffffffu, kO, gs);
+    __syncwarp();
+    if (i < live) {
+      int lo = 0;  // largest b with (survivors in slots < 2b) <= r
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int b = lo + step;
+        const unsigned m = (1u << b) - 1u;
+        if (__popc(E & m) + __popc(O & m) <= r) lo = b;
+      }
+      const unsigned m = (1u << lo) - 1u;
+      const bool even = ((E >> lo) & 1u) && __popc(E & m) + __popc(O & m) == r;
+      const int sl = 64 * gs + 2 * lo + (even ? 0 : 1);
+      const double v = val[sl];
+      if (write) emit(i, base + sl, v);
+      val[sl] = -0.0;
+    }
+  }
+  if (numeric && __any_sync(0xffffffffu, diff) && lane == 0 && *reinterpret_cast<volatile int*>(g.changed) == 0)
+    atomicOr(g.changed, 1);
+  __syncwarp();
+}
+
 // Numeric pass of staged rows: 8 lanes per row (4 rows per warp; the rows
 // keep ~7-16 survivors, so a warp per row idled most lanes and a thread per
 // row made uncoalesced strided reads) copy the sorted survivors to the final
@@ -691,7 +1036,7 @@ __global__ void __launch_bounds__(256) spgemm_smem(Args g, const int32_t* __rest
 }
 
 __host__ __device__ constexpr int window_smem_per_warp(int R) {
-  return (1024 * R * 8 + 2 * 32 * R * 4 + static_cast<int>(sizeof(WarpStage)) + 15) / 16 * 16;
+  return (1024 * R * 8 + 64 * R * 4 + static_cast<int>(sizeof(WarpStage)) + 15) / 16 * 16;
 }
 constexpr int window_warps(int R) { return R == 1 ? 8 : 4; }
 
@@ -709,6 +1054,37 @@ __global__ void __launch_bounds__(256) spgemm_window(Args g, const int32_t* __re
   for (int32_t r = blockIdx.x * warps + w; r < nrows_bin; r += gridDim.x * warps) {
     const int32_t j = rows[r];
     process_row_window<R>(g, j, wbase[j], bits, kbits, val, st, lane, numeric);
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) spgemm_window_z(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+                                                       const int32_t* __restrict__ wbase, bool numeric) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* mine = smem + w * window_smem_per_warp(R);
+  double* val = reinterpret_cast<double*>(mine);
+  uint32_t* kbits = reinterpret_cast<uint32_t*>(mine + 1024 * R * 8);
+  WarpStage* st = reinterpret_cast<WarpStage*>(kbits + 64 * R);
+  for (int s = lane; s < 1024 * R; s += 32) val[s] = -0.0;
+  __syncwarp();
+  const int warps = blockDim.x >> 5;
+  const int32_t stride = gridDim.x * warps;
+  unsigned long long cpos = 0, cend = 0;  // this warp's staging chunk
+  int32_t r = blockIdx.x * warps + w;
+  RowAhead nx;
+  if (r < nrows_bin)
+    while (nx.stage < 4) nx.step(g, rows, r, wbase, lane);
+  for (; r < nrows_bin; r += stride) {
+    const RowAhead cur = nx;
+    const int32_t rn = r + stride;
+    nx = RowAhead{};
+    if (rn >= nrows_bin) nx.stage = 4;
+    if (numeric)
+      process_row_window_z<R, true>(g, cur, nx, rows, rn, wbase, val, kbits, st, lane, cpos, cend);
+    else
+      process_row_window_z<R, false>(g, cur, nx, rows, rn, wbase, val, kbits, st, lane, cpos, cend);
+    while (nx.stage < 4) nx.step(g, rows, rn, wbase, lane);
   }
 }
 
@@ -1173,14 +1549,20 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     const int R = b == kWinBin1 ? 1 : 2;
     const int warps = window_warps(R);
     const int smem = warps * window_smem_per_warp(R);
-    const void* k = R == 1 ? reinterpret_cast<const void*>(spgemm_window<1>)
-                           : reinterpret_cast<const void*>(spgemm_window<2>);
-    if (first_on_device(k)) SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    static const bool zero_on = [] {  // SAIT_WIN_ZERO=0: the bitmap window for every epilogue
+      const char* e = std::getenv("SAIT_WIN_ZERO");
+      return !(e && std::atoi(e) == 0);
+    }();
+    // threshold builds with +I take the -0.0 window (ZeroWindow)
+    const bool zero = zero_on && g.epi.add_identity && (g.epi.drop == 1 || g.epi.drop == 3) && g.epi.tau > 0.0;
+    using WK = void (*)(Args, const int32_t*, int32_t, const int32_t*, bool);
+    const WK k = zero ? (R == 1 ? spgemm_window_z<1> : spgemm_window_z<2>) : (R == 1 ? spgemm_window<1> : spgemm_window<2>);
+    if (first_on_device(reinterpret_cast<const void*>(k)))
+      SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int blocks_per_sm = std::max(1, (228 * 1024) / (smem + 1024));
     const unsigned grid = static_cast<unsigned>(
         std::min<int64_t>((cnt + warps - 1) / warps, int64_t{num_sms()} * blocks_per_sm * 4));
-    if (R == 1) spgemm_window<1><<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, pl.wbase, numeric);
-    else spgemm_window<2><<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, pl.wbase, numeric);
+    k<<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, pl.wbase, numeric);
     SAIT_LAUNCHED();
   }
   int32_t gc = pl.hist[kGlobalBin];
@@ -1206,6 +1588,14 @@ __device__ __forceinline__ bool first_keep(const Epilogue& e, int32_t i, int32_t
   if ((e.drop == 1 || e.drop == 3) && e.tau != 0.0) return col == i || fabs(v) >= e.tau;
   return true;
 }
+// G lanes per row (32/G rows per warp), the row's entries G at a time: the
+// survivors' positions come from ballots of the keep flags; the diagonal
+// goes right after the kept entries of columns < i (rows are sorted).
+template <int G>
+__device__ __forceinline__ unsigned group_ballot(bool p, int wl) {
+  const unsigned b = __ballot_sync(0xffffffffu, p);
+  return G == 32 ? b : (b >> (wl & ~(G - 1))) & ((1u << G) - 1u);
+}
 __global__ void first_step_count(int64_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                                  const double* __restrict__ av, Epilogue e, int32_t* __restrict__ cnt) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1215,29 +1605,57 @@ __global__ void first_step_count(int64_t n, const int32_t* __restrict__ arp, con
   for (int32_t q = arp[i]; q < arp[i + 1]; ++q) c += first_keep(e, r, aci[q], av[q]);
   cnt[i] = c;
 }
+template <int G>
 __global__ void first_step_write(int64_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                                  const double* __restrict__ av, Epilogue e, const int32_t* __restrict__ crp,
                                  int32_t* __restrict__ cci, double* __restrict__ cv) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+  const int wl = threadIdx.x & 31, lane = wl & (G - 1);
+  const bool live = i < n;
   const int32_t r = static_cast<int32_t>(i);
-  int32_t o = crp[i];
-  bool diag = first_keep(e, r, r, 1.0);
-  auto put = [&](int32_t col, double v) {
-    cci[o] = col;
-    cv[o] = e.out_scale ? __dmul_rn(v, e.out_scale[col]) : v;
-    ++o;
-  };
-  for (int32_t q = arp[i]; q < arp[i + 1]; ++q) {
-    const int32_t col = aci[q];
-    if (diag && col > r) {
-      put(r, 1.0);
-      diag = false;
-    }
-    const double v = __dmul_rn(av[q], 1.0);
-    if (first_keep(e, r, col, v)) put(col, v);
+  int32_t q0 = 0, q1 = 0, out = 0;
+  if (live) {
+    q0 = arp[i];
+    q1 = arp[i + 1];
+    out = crp[i];
   }
-  if (diag) put(r, 1.0);
+  const int32_t len = q1 - q0;
+  const bool diag = live && first_keep(e, r, r, 1.0);
+  bool placed = !diag;  // the diagonal written (or not kept)
+  const unsigned below = (1u << lane) - 1u;
+  auto put = [&](int32_t p, int32_t col, double v) {
+    cci[p] = col;
+    cv[p] = e.out_scale ? __dmul_rn(v, e.out_scale[col]) : v;
+  };
+  if constexpr (G == 1) {  // thread per row (short rows)
+    if (!live) return;
+    for (int32_t q = q0; q < q1; ++q) {
+      const int32_t col = aci[q];
+      if (!placed && col > r) {
+        put(out++, r, 1.0);
+        placed = true;
+      }
+      const double v = __dmul_rn(av[q], 1.0);
+      if (first_keep(e, r, col, v)) put(out++, col, v);
+    }
+    if (!placed) put(out, r, 1.0);
+  } else {
+  for (int32_t o = 0; __any_sync(0xffffffffu, o < len); o += G) {
+    const bool in = o + lane < len;
+    const int32_t q = q0 + o + lane;
+    const int32_t col = in ? aci[q] : INT32_MAX;
+    const double v = in ? __dmul_rn(av[q], 1.0) : 0.0;
+    const bool keep = in && first_keep(e, r, col, v);
+    const unsigned km = group_ballot<G>(keep, wl);
+    const unsigned after = group_ballot<G>(in && col > r, wl);  // a suffix of the chunk
+    const bool here = !placed && after != 0u;  // the diagonal lands in this chunk, before `after`
+    if (keep) put(out + __popc(km & below) + ((here && col > r) ? 1 : 0), col, v);
+    if (here && lane == 0) put(out + __popc(km & ~after), r, 1.0);
+    out += __popc(km) + (here ? 1 : 0);
+    placed = placed || here;
+  }
+  if (live && !placed && lane == 0) put(out, r, 1.0);
+  }
 }
 }  // namespace
 
@@ -1248,6 +1666,7 @@ SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStrea
   c.nrows = c.ncols = n;
   c.rp = dalloc<int32_t>(n + 1, s);
   int32_t* cnt = dalloc<int32_t>(n > 0 ? n : 1, s);
+  const bool wide = a.nnz >= 12 * n;  // long rows: 4 lanes per row in the write pass (1.28 vs 3.6 ms at C4)
   if (n > 0) {
     first_step_count<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, epi, cnt);
     SAIT_LAUNCHED();
@@ -1260,7 +1679,10 @@ SpgemmResult first_step_identity(const DevCsr& a, const Epilogue& epi, cudaStrea
   c.ci = dalloc<int32_t>(c.nnz > 0 ? c.nnz : 1, s);
   c.v = dalloc<double>(c.nnz > 0 ? c.nnz : 1, s);
   if (n > 0) {
-    first_step_write<<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, epi, c.rp, c.ci, c.v);
+    if (wide)
+      first_step_write<4><<<grid_for(n * 4, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, epi, c.rp, c.ci, c.v);
+    else
+      first_step_write<1><<<grid_for(n, 256), 256, 0, s>>>(n, a.rp, a.ci, a.v, epi, c.rp, c.ci, c.v);
     SAIT_LAUNCHED();
   }
   res.products = a.nnz;

@@ -168,7 +168,8 @@ cases = [(lambda: P.sait_thr(T, True, 1e-2, 3), lambda: S.sait_thr(Tp, S.lower_t
          (lambda: P.sait_thr(T, True, 0.0, 3), lambda: S.sait_thr(Tp, S.lower_triangular, S.SaitThrParams(0.0, 3))),
          (lambda: P.sait_thr_cap(T, True, 1e-2, 3, 1.0),
           lambda: S.sait_thr_cap(Tp, S.lower_triangular, S.SaitThrParams(1e-2, 3), 1.0)),
-         (lambda: P.sait_thr(Tu, False, 1e-2, 3), lambda: S.sait_thr(Tup, S.upper_triangular, S.SaitThrParams(1e-2, 3)))]
+         (lambda: P.sait_thr(Tu, False, 1e-2, 3), lambda: S.sait_thr(Tup, S.upper_triangular, S.SaitThrParams(1e-2, 3))),
+         (lambda: P.sait_pat(T, True, 2, 3), lambda: S.sait_pat(Tp, S.lower_triangular, S.SaitPatParams(2, 3)))]
 for ref, dev in cases:
     want, got = ref(), dev()
     ok = (np.array_equal(got.row_ptr, want.row_ptr) and np.array_equal(got.col_idx, want.col_idx)
@@ -207,7 +208,7 @@ def test_sait_polynomial_stored_diagonal(S, ref, golden, case, steps):
     assert bitwise_equal_csr(got, want)
 
 
-@pytest.mark.parametrize("window", ["0", "1"])
+@pytest.mark.parametrize("window", ["0", "1", "bitmap"])
 @pytest.mark.parametrize("column_form", ["0", "1"])
 @pytest.mark.parametrize("cap", ["none", "0", "1000", "200000"])
 def test_hash_rows_staging_and_overflow(cap, column_form, window):
@@ -215,14 +216,19 @@ def test_hash_rows_staging_and_overflow(cap, column_form, window):
     survivors in the count pass; rows past the staging capacity are
     recomputed in the numeric pass.  Every split (all staged, none, a few,
     most) gives the oracle's bits, with the direct-addressed window rows on
-    (default) or off (SAIT_SPGEMM_WINDOW=0: hash tables only)."""
+    (default: the -0.0 window for tau > 0 threshold builds, the bitmap
+    window for tau = 0 and pattern builds), the bitmap window for every
+    epilogue (SAIT_WIN_ZERO=0), or off (SAIT_SPGEMM_WINDOW=0: hash tables
+    only)."""
     import os
     import subprocess
     import sys
 
     from conftest import ROOT
 
-    env = dict(os.environ, SAIT_BUILD_COLUMN_FORM=column_form, SAIT_SPGEMM_WINDOW=window)
+    env = dict(os.environ, SAIT_BUILD_COLUMN_FORM=column_form, SAIT_SPGEMM_WINDOW="0" if window == "0" else "1")
+    if window == "bitmap":
+        env["SAIT_WIN_ZERO"] = "0"
     if cap == "none":
         env["SAIT_SPGEMM_NOSTAGE"] = "1"
     else:
@@ -230,7 +236,7 @@ def test_hash_rows_staging_and_overflow(cap, column_form, window):
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.split() == ["1", "1", "1", "1"]
+    assert out.stdout.split() == ["1", "1", "1", "1", "1"]
 
 
 @pytest.mark.parametrize("column_form", ["0", "1"])
@@ -250,7 +256,7 @@ def test_hash_table_load_factors(slack, column_form):
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.split() == ["1", "1", "1", "1"]
+    assert out.stdout.split() == ["1", "1", "1", "1", "1"]
 
 
 def test_build_pair_concurrent_equals_separate(S, port):

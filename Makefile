@@ -15,7 +15,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC,-ffp-c
            -Iinclude -I$(CSRC) -Xptxas -warn-spills
 CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Iinclude -I/usr/local/cuda/include
 
-CU_SRCS := csr_ops split spgemm spmv sell blas solvers trisolve ilu aux_ops capi
+CU_SRCS := csr_ops split spgemm spmv sell blas solvers trisolve ilu aux_ops cap capi
 CU_OBJS := $(addprefix $(BUILD)/,$(addsuffix .o,$(CU_SRCS)))
 HOST_OBJS := $(BUILD)/host_inputs.o $(BUILD)/host_mm.o
 HEADERS := include/sait_c.h $(wildcard $(CSRC)/*.cuh)

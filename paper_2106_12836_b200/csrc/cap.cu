@@ -1,0 +1,282 @@
+// cap.cu — the A15 fill cap on a row-form iterate, and the reference's
+// stabilized() test on two device CSR matrices.
+//
+// The cap keeps, in every column j of M_s, the diagonal and the cap_j - 1
+// largest-|v| off-diagonals (ties: the smaller row), after the threshold,
+// every step (DESIGN.md §8 decision 3; the oracle applies it through the
+// reference's DropRule hook).  The column-form recursion applies it inside
+// the SpGEMM epilogue, where a column of M is a row of M^T.  A whole-matrix
+// build runs in row form instead (no transposes of tT and M), with a
+// threshold-only epilogue, and then this pass: count the entries per column,
+// flag the columns over their cap (few), gather the flagged columns' entries,
+// rank them per column exactly as the epilogue would, and compact the rows
+// that lost entries.  Same surviving set, hence the same matrix, bit for bit.
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace sait {
+namespace {
+
+// entries are visited flat, 4 per thread (one 16-byte load of columns)
+constexpr int kFlat = 4;
+__global__ void cap_count_cols(int64_t nnz, const int32_t* __restrict__ ci, int32_t* __restrict__ cnt) {
+  const int64_t e0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kFlat;
+  if (e0 + kFlat <= nnz) {
+    const int4 c = *reinterpret_cast<const int4*>(ci + e0);
+    atomicAdd(&cnt[c.x], 1);
+    atomicAdd(&cnt[c.y], 1);
+    atomicAdd(&cnt[c.z], 1);
+    atomicAdd(&cnt[c.w], 1);
+  } else {
+    for (int64_t e = e0; e < nnz; ++e) atomicAdd(&cnt[ci[e]], 1);
+  }
+}
+
+// seglen[c] = number of c's entries when column c has more off-diagonals
+// than its room (cap - 1, at least 0), else 0 (the diagonal is always
+// present: +I, always kept by the threshold); flagged columns are listed
+// and marked in a bitmap
+__global__ void cap_flag(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ cap,
+                         int32_t* __restrict__ seglen, uint32_t* __restrict__ bits, int32_t* __restrict__ list,
+                         int32_t* __restrict__ nlist) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool f = false;
+  if (c < n) {
+    const int32_t room = max(cap[c] - 1, 0);
+    f = cnt[c] - 1 > room;
+    seglen[c] = f ? cnt[c] : 0;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if (c < n && lane == 0) bits[c >> 5] = m;  // 32 consecutive columns per warp
+  if (m) {
+    int32_t base = 0;
+    if (lane == 0) base = atomicAdd(nlist, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (f) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(c);
+  }
+}
+
+// entries of flagged columns -> their column's segment (row, value,
+// position); flat over the entries, the row of a (rare) match by binary search
+__device__ __forceinline__ void cap_take(int64_t e, int32_t c, int64_t nrows, const int32_t* __restrict__ rp,
+                                         const double* __restrict__ v, int32_t* __restrict__ cursor,
+                                         int32_t* __restrict__ lrow, double* __restrict__ lval,
+                                         int32_t* __restrict__ lpos) {
+  int64_t lo = 0, hi = nrows;  // the row i with rp[i] <= e < rp[i + 1]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rp[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  const int32_t p = atomicAdd(&cursor[c], 1);
+  lrow[p] = static_cast<int32_t>(lo);
+  lval[p] = v[e];
+  lpos[p] = static_cast<int32_t>(e);
+}
+__global__ void cap_gather(int64_t nnz, int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, const uint32_t* __restrict__ bits,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ lrow, double* __restrict__ lval,
+                           int32_t* __restrict__ lpos) {
+  const int64_t e0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kFlat;
+  auto flagged = [&](int32_t c) { return (bits[c >> 5] >> (c & 31)) & 1u; };
+  if (e0 + kFlat <= nnz) {
+    const int4 c = *reinterpret_cast<const int4*>(ci + e0);
+    if (flagged(c.x)) cap_take(e0, c.x, nrows, rp, v, cursor, lrow, lval, lpos);
+    if (flagged(c.y)) cap_take(e0 + 1, c.y, nrows, rp, v, cursor, lrow, lval, lpos);
+    if (flagged(c.z)) cap_take(e0 + 2, c.z, nrows, rp, v, cursor, lrow, lval, lpos);
+    if (flagged(c.w)) cap_take(e0 + 3, c.w, nrows, rp, v, cursor, lrow, lval, lpos);
+  } else {
+    for (int64_t e = e0; e < nnz; ++e)
+      if (flagged(ci[e])) cap_take(e, ci[e], nrows, rp, v, cursor, lrow, lval, lpos);
+  }
+}
+
+// one warp per column: rank every off-diagonal by (|v| desc, row asc) among
+// the column's off-diagonals; ranks >= room are dropped (column index -1)
+__global__ void cap_rank(int32_t nflag, const int32_t* __restrict__ flagged, const int32_t* __restrict__ seglen,
+                         const int32_t* __restrict__ segstart, const int32_t* __restrict__ cap,
+                         const int32_t* __restrict__ lrow, const double* __restrict__ lval,
+                         const int32_t* __restrict__ lpos, int32_t* __restrict__ ci, int32_t* __restrict__ rowdel,
+                         unsigned long long* __restrict__ ndel) {
+  const int64_t f = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= nflag) return;
+  const int32_t c = flagged[f];
+  const int32_t b = segstart[c], len = seglen[c];
+  const int32_t room = max(cap[c] - 1, 0);
+  const int32_t col = c;
+  int killed = 0;
+  for (int32_t t = lane; t < len; t += 32) {
+    const int32_t row = lrow[b + t];
+    if (row == col) continue;
+    const double mv = fabs(lval[b + t]);
+    int32_t rank = 0;
+    for (int32_t q = 0; q < len; ++q) {
+      const int32_t rq = lrow[b + q];
+      if (rq == col || rq == row) continue;
+      const double vq = fabs(lval[b + q]);
+      rank += (vq > mv) || (vq == mv && rq < row);
+    }
+    if (rank >= room) {
+      ci[lpos[b + t]] = -1;
+      atomicAdd(&rowdel[row], 1);
+      ++killed;
+    }
+  }
+  killed = __reduce_add_sync(0xffffffffu, killed);
+  if (lane == 0 && killed) atomicAdd(ndel, static_cast<unsigned long long>(killed));
+}
+
+__global__ void cap_row_counts(int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ rowdel,
+                               int32_t* __restrict__ cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nrows) cnt[i] = rp[i + 1] - rp[i] - rowdel[i];
+}
+
+// rows without deletions are copied as they are (8 lanes per row); rows
+// with deletions are compacted by ballots in order
+__global__ void cap_compact(int64_t nrows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const int32_t* __restrict__ rowdel,
+                            const double* __restrict__ scale, const int32_t* __restrict__ nrp,
+                            int32_t* __restrict__ nci, double* __restrict__ nv) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  const int sl = threadIdx.x & 7, wl = threadIdx.x & 31;
+  const bool live = i < nrows;
+  int32_t b = 0, e = 0, o = 0;
+  bool del = false;
+  if (live) {
+    b = rp[i];
+    e = rp[i + 1];
+    o = nrp[i];
+    del = rowdel[i] > 0;
+  }
+  for (int32_t q0 = b; __any_sync(0xffffffffu, q0 < e); q0 += 8) {
+    const int32_t q = q0 + sl;
+    const bool in = q < e;
+    const int32_t c = in ? ci[q] : -1;
+    const bool keep = in && c >= 0;
+    const unsigned m = (__ballot_sync(0xffffffffu, keep) >> (wl & ~7)) & 0xffu;
+    if (keep) {
+      const int32_t p = del ? o + __popc(m & ((1u << sl) - 1u)) : o + sl;
+      nci[p] = c;
+      nv[p] = scale ? __dmul_rn(v[q], scale[c]) : v[q];  // scale_columns (kernels.cpp:236-246), fused
+    }
+    o += del ? __popc(m) : 8;
+  }
+}
+
+// the reference's stabilized(prev, cur) (sait.cpp:14-28), shapes already equal
+__global__ void stable_rows(int64_t nrows, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                            const double* __restrict__ av, const int32_t* __restrict__ brp,
+                            const int32_t* __restrict__ bci, const double* __restrict__ bv, int* __restrict__ differs) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  if (i >= nrows) return;
+  bool diff = arp[i] != brp[i] || arp[i + 1] != brp[i + 1];
+  if (!diff)
+    for (int32_t q = arp[i] + (threadIdx.x & 7); q < arp[i + 1]; q += 8) {
+      const double a = av[q], b = bv[q];
+      const double fa = fabs(a), fb = fabs(b);
+      const double mx = fa < fb ? fb : fa;
+      if (aci[q] != bci[q] || fabs(__dsub_rn(b, a)) > __dmul_rn(1e-15, mx)) diff = true;
+    }
+  if (diff && *reinterpret_cast<volatile int*>(differs) == 0) atomicOr(differs, 1);
+}
+
+}  // namespace
+
+// Applies the cap to m in place; returns the number of entries dropped.
+// With out_scale (the last step), a compaction also scales the columns and
+// *scaled is set.
+int64_t cap_rowform(DevCsr& m, const int32_t* cap, cudaStream_t s, const double* out_scale, bool* scaled) {
+  if (scaled) *scaled = false;
+  const int64_t n = m.nrows;
+  if (n == 0 || m.nnz == 0) return 0;
+  int32_t* cnt = dalloc<int32_t>(n + 1, s);
+  int32_t* seglen = dalloc<int32_t>(n + 1, s);
+  int32_t* segstart = dalloc<int32_t>(n + 1, s);
+  int32_t* flagged = dalloc<int32_t>(n + 1, s);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(dalloc<int32_t>((n + 31) / 32 + 1, s));
+  int32_t* nflag_d = dalloc<int32_t>(1, s);
+  SAIT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, s));
+  SAIT_CUDA(cudaMemsetAsync(nflag_d, 0, sizeof(int32_t), s));
+  cap_count_cols<<<grid_for((m.nnz + kFlat - 1) / kFlat, 256), 256, 0, s>>>(m.nnz, m.ci, cnt);
+  SAIT_LAUNCHED();
+  cap_flag<<<grid_for(n, 256), 256, 0, s>>>(n, cnt, cap, seglen, bits, flagged, nflag_d);
+  SAIT_LAUNCHED();
+  const int64_t listed = scan_counts(seglen, segstart, n, s);
+  int64_t deleted = 0;
+  if (listed > 0) {
+    int32_t nflag = 0;
+    read_back(s, {{&nflag, nflag_d, sizeof nflag}});
+    int32_t* lrow = dalloc<int32_t>(listed, s);
+    double* lval = dalloc<double>(listed, s);
+    int32_t* lpos = dalloc<int32_t>(listed, s);
+    int32_t* rowdel = cnt;  // reused: deletions per row
+    unsigned long long* ndel = reinterpret_cast<unsigned long long*>(dalloc<int64_t>(1, s));
+    SAIT_CUDA(cudaMemsetAsync(rowdel, 0, sizeof(int32_t) * n, s));
+    SAIT_CUDA(cudaMemsetAsync(ndel, 0, sizeof(unsigned long long), s));
+    int32_t* cursor = dalloc<int32_t>(n, s);
+    SAIT_CUDA(cudaMemcpyAsync(cursor, segstart, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+    cap_gather<<<grid_for((m.nnz + kFlat - 1) / kFlat, 256), 256, 0, s>>>(m.nnz, n, m.rp, m.ci, m.v, bits, cursor,
+                                                                          lrow, lval, lpos);
+    SAIT_LAUNCHED();
+    dfree(cursor, s);
+    cap_rank<<<grid_for(int64_t{nflag} * 32, 256), 256, 0, s>>>(nflag, flagged, seglen, segstart, cap, lrow, lval,
+                                                                 lpos, m.ci, rowdel, ndel);
+    SAIT_LAUNCHED();
+    unsigned long long hd = 0;
+    read_back(s, {{&hd, ndel, sizeof hd}});
+    deleted = static_cast<int64_t>(hd);
+    if (deleted > 0) {
+      int32_t* ncnt = seglen;  // reused
+      cap_row_counts<<<grid_for(n, 256), 256, 0, s>>>(n, m.rp, rowdel, ncnt);
+      SAIT_LAUNCHED();
+      DevCsr c;
+      c.nrows = m.nrows;
+      c.ncols = m.ncols;
+      c.rp = dalloc<int32_t>(n + 1, s);
+      c.nnz = scan_counts(ncnt, c.rp, n, s);
+      c.ci = dalloc<int32_t>(c.nnz > 0 ? c.nnz : 1, s);
+      c.v = dalloc<double>(c.nnz > 0 ? c.nnz : 1, s);
+      cap_compact<<<grid_for(n * 8, 256), 256, 0, s>>>(n, m.rp, m.ci, m.v, rowdel, out_scale, c.rp, c.ci, c.v);
+      SAIT_LAUNCHED();
+      free_csr(m, s);
+      m = c;
+      if (scaled) *scaled = out_scale != nullptr;
+    }
+    dfree(lrow, s);
+    dfree(lval, s);
+    dfree(lpos, s);
+    dfree(reinterpret_cast<int64_t*>(ndel), s);
+  }
+  dfree(cnt, s);
+  dfree(seglen, s);
+  dfree(segstart, s);
+  dfree(flagged, s);
+  dfree(reinterpret_cast<int32_t*>(bits), s);
+  dfree(nflag_d, s);
+  static const bool dbg = std::getenv("SAIT_DEBUG_CAP") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "cap_rowform: n %lld nnz %lld listed %lld deleted %lld\n", static_cast<long long>(n),
+                 static_cast<long long>(m.nnz), static_cast<long long>(listed), static_cast<long long>(deleted));
+  return deleted;
+}
+
+bool csr_stabilized(const DevCsr& prev, const DevCsr& cur, cudaStream_t s) {
+  if (prev.nrows != cur.nrows || prev.nnz != cur.nnz) return false;
+  if (cur.nrows == 0) return true;
+  int* differs = dalloc<int>(1, s);
+  SAIT_CUDA(cudaMemsetAsync(differs, 0, sizeof(int), s));
+  stable_rows<<<grid_for(cur.nrows * 8, 256), 256, 0, s>>>(cur.nrows, prev.rp, prev.ci, prev.v, cur.rp, cur.ci,
+                                                            cur.v, differs);
+  SAIT_LAUNCHED();
+  int h = 1;
+  read_back(s, {{&h, differs, sizeof h}});
+  dfree(differs, s);
+  return h == 0;
+}
+
+}  // namespace sait

@@ -110,6 +110,8 @@ void validate_device_csr(const DevCsr& m, cudaStream_t s);
 void narrow_indices(const int64_t* in, int32_t* out, int64_t n, cudaStream_t s);
 void widen_indices(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);
 void column_caps(const DevCsr& t, double factor, int32_t* cap, cudaStream_t s);
+int64_t cap_rowform(DevCsr& m, const int32_t* cap, cudaStream_t s, const double* out_scale, bool* scaled);
+bool csr_stabilized(const DevCsr& prev, const DevCsr& cur, cudaStream_t s);
 void pair_apply_host_pipelined(const DevCsr& ml, const DevCsr& mu, const double* h_r, double* h_z,
                                cudaStream_t s);
 }  // namespace sait
@@ -358,12 +360,14 @@ struct BuildOut {
 // bitwise equal to the reference's row form (same products, same
 // ascending-k order, commutative products).  Rows [c0, c0 + rows) of M^T
 // (= a block of columns of M) evolve independently; only the early-stop
-// decision is global, so the caller supplies it between steps.  The fill cap
-// (per column of M) and column-sharded blocks need the column form.
+// decision is global, so the caller supplies it between steps.  Column-sharded
+// blocks need the column form (the fill cap, per column of M, is then part of
+// the SpGEMM epilogue).
 // Row form (row_form = true, whole matrix, threshold/pattern/none): the
 // reference's own orientation, row i of M_s = drop(sum_k tT[i,k] M_{s-1}[k,:]
 // + e_i) with op = tT -- the same products in the same order, and neither
-// tT nor the result needs a transpose.
+// tT nor the result needs a transpose; a fill cap runs as a per-column pass
+// after each step (cap_rowform).
 class Recursion {
  public:
   // op_from_split: op is the iteration matrix of jacobi_split (no stored
@@ -374,6 +378,14 @@ class Recursion {
             cudaStream_t s, bool row_form = false, const double* out_scale = nullptr, bool op_from_split = true)
       : ttT_(op), spec_(spec), s_(s), row_form_(row_form), out_scale_(row_form ? out_scale : nullptr),
         op_from_split_(op_from_split) {
+    // row form with the fill cap: the product keeps the threshold only and
+    // cap_rowform applies the per-column cap after it; the column scaling is
+    // left to finish (the cap ranks unscaled values)
+    row_cap_ = row_form && spec.kind == SAIT_DROP_THRESHOLD_CAP ? cap : nullptr;
+    if (row_cap_) {  // the last step's compaction (if any) scales instead
+      cap_scale_ = out_scale_;
+      out_scale_ = nullptr;
+    }
     a_ = sait::make_identity_rows(rows, c0, op.nrows, s);
     epi_.add_identity = true;
     epi_.diag_offset = c0;
@@ -381,9 +393,9 @@ class Recursion {
       epi_.drop = 1;
       epi_.tau = spec.tau;
     } else if (spec.kind == SAIT_DROP_THRESHOLD_CAP) {
-      epi_.drop = 3;
+      epi_.drop = row_cap_ ? 1 : 3;
       epi_.tau = spec.tau;
-      epi_.cap = cap;
+      epi_.cap = row_cap_ ? nullptr : cap;
     }
     pattern_left_ = spec.kind == SAIT_DROP_PATTERN ? spec.pattern_steps : 0;
     main_left_ = spec.kind == SAIT_DROP_PATTERN ? spec.refine_steps : spec.steps;
@@ -412,9 +424,19 @@ class Recursion {
     // leaves the scaling to finish)
     const bool last = out_scale_ && main_left_ == 1;
     epi_.out_scale = last ? out_scale_ : nullptr;
+    const bool first = steps_run_ == 0;
     sait::SpgemmResult r = product(epi_);
     epi_.out_scale = nullptr;
     scaled_ = last;
+    // the cap cannot bind at the first step (see product); after it, a step
+    // that dropped entries for the cap is compared again, capped
+    if (row_cap_ && !first) {
+      const bool last_cap = cap_scale_ && main_left_ == 1;
+      bool sc = false;
+      if (sait::cap_rowform(r.c, row_cap_, s_, last_cap ? cap_scale_ : nullptr, &sc) > 0)
+        r.changed = !sait::csr_stabilized(a_, r.c, s_);  // (no kernel when the sizes differ)
+      scaled_ = sc;
+    }
     const bool changed = r.changed;
     advance(std::move(r));
     --main_left_;
@@ -463,6 +485,8 @@ class Recursion {
   cudaStream_t s_;
   bool row_form_ = false;
   const double* out_scale_ = nullptr;
+  const int32_t* row_cap_ = nullptr;  // row form with the fill cap
+  const double* cap_scale_ = nullptr;
   bool op_from_split_ = true;
   bool scaled_ = false;
   sait::DevCsr a_, pattern_;
@@ -1070,13 +1094,14 @@ int sait_build_session_create(sait_dcsr_t t, int lower, const sait_drop_spec* sp
       delete ss;
       throw;
     }
-    // whole-matrix builds without the column cap run in row form (no
-    // transposes); SAIT_BUILD_COLUMN_FORM=1 forces the column form (tests)
+    // whole-matrix builds run in row form (no transposes; the fill cap is a
+    // pass after each step, cap.cu); column blocks need the column form;
+    // SAIT_BUILD_COLUMN_FORM=1 forces it (tests)
     static const bool force_column = [] {
       const char* e = std::getenv("SAIT_BUILD_COLUMN_FORM");
       return e && std::atoi(e) != 0;
     }();
-    ss->row_form = !force_column && spec->kind != SAIT_DROP_THRESHOLD_CAP && col0 == 0 && col1 == n;
+    ss->row_form = !force_column && col0 == 0 && col1 == n;
     if (ss->row_form) {
       ss->ttT = tt;
     } else {

@@ -49,11 +49,14 @@ constexpr int kFirstSmemBin = kTinyBins;
 constexpr int kNumSmemBins = 7;
 constexpr int kMinLogSlots = 6;
 constexpr int kGlobalBin = kFirstSmemBin + kNumSmemBins;
-// window bins: rows whose product columns all fall in [base, base + 1024 R)
-// (R = 1, 2), accumulated by direct addressing instead of hashing (below)
-constexpr int kWinBin1 = kGlobalBin + 1;
-constexpr int kWinBin2 = kGlobalBin + 2;
-constexpr int kNumBins = kGlobalBin + 3;
+// window bins: rows whose product columns all fall in [base, base + 128 Q)
+// (Q = kWinQ[i]), accumulated by direct addressing instead of hashing
+// (below); the smaller windows fit more rows in flight per SM
+constexpr int kNumWinBins = 6;
+constexpr int kWinQ[kNumWinBins] = {4, 5, 6, 7, 8, 16};
+__host__ __device__ constexpr int win_q(int i) { return i < 5 ? 4 + i : 16; }  // kWinQ[i] (device code)
+constexpr int kWinBin0 = kGlobalBin + 1;
+constexpr int kNumBins = kWinBin0 + kNumWinBins;
 constexpr int kTinyG[kTinyBins] = {8, 16, 32};
 
 struct Args {
@@ -464,7 +467,7 @@ __device__ void process_row(const Args& g, int32_t j, int32_t* key, double* val,
   __syncwarp();
 }
 
-// Window rows (bins kWinBin1/2): every product column of row j lies in
+// Window rows (the window bins): every product column of row j lies in
 // [base, base + 1024 R), so the row accumulates by direct addressing -- one
 // atomicOr on an occupancy bitmap per new column instead of hash probing and
 // table clearing -- and its entries come out of the bitmap already in column
@@ -671,12 +674,19 @@ struct RowAhead {
   }
 };
 
+// accumulate_zero's staging of one chunk of <= 32 A entries
+struct ZStage {
+  double aval[32];
+  int32_t off[33];
+  int32_t bstart[32];
+};
+
 // accumulate_row for a ZeroWindow with the row's first A chunk already
 // loaded (cur) and the next row's loads advanced between rounds (nx).
 __device__ __forceinline__ int32_t accumulate_zero(const Args& g, const RowAhead& cur, RowAhead& nx,
                                                    const int32_t* __restrict__ rows, int32_t rn,
                                                    const int32_t* __restrict__ wbase, const ZeroWindow& tab,
-                                                   double* val, WarpStage* st, int lane) {
+                                                   double* val, ZStage* st, int lane) {
   int32_t hi = -1;
   const int32_t j = cur.j, a0 = cur.a0, a1 = cur.a1;
   int rounds = 0;
@@ -770,24 +780,27 @@ __device__ __forceinline__ int32_t accumulate_zero(const Args& g, const RowAhead
 // a survivor's position is the groups' prefix plus the lane's popcounts,
 // i.e. column order, and each visited slot pair goes back to -0.0.  Same
 // products, same add order: bitwise the hash path.
-template <int R, bool numeric>
+template <int Q, bool numeric>
 __device__ void process_row_window_z(const Args& g, const RowAhead& cur, RowAhead& nx,
                                      const int32_t* __restrict__ rows, int32_t rn, const int32_t* __restrict__ wbase,
-                                     double* val, uint32_t* kbits, WarpStage* st, int lane,
+                                     double* val, uint32_t* kbits, ZStage* st, int lane,
                                      unsigned long long& cpos, unsigned long long& cend) {
   const int32_t j = cur.j, base = cur.base;
   if (numeric && g.stage_pos && g.stage_pos[j] >= 0) return;  // staged: copied by spgemm_stage_emit
-  const int32_t hi = accumulate_zero(g, cur, nx, rows, rn, wbase, ZeroWindow{base, 1024 * R}, val, st, lane);
+  const int32_t hi = accumulate_zero(g, cur, nx, rows, rn, wbase, ZeroWindow{base, 128 * Q}, val, st, lane);
   const int32_t jd = j + static_cast<int32_t>(g.epi.diag_offset);
   const int sd = jd - base;  // the diagonal's slot
   const double tau = g.epi.tau;
   const int ngroups = ((hi - base) >> 6) + 1;
-  SAIT_DCHECK(ngroups >= 1 && ngroups <= 16 * R, "spgemm window groups", ngroups, 16 * R);
+  SAIT_DCHECK(ngroups >= 1 && ngroups <= 2 * Q, "spgemm window groups", ngroups, 2 * Q);
   uint32_t kE = 0u, kO = 0u;
   for (int q0 = 0; q0 < ngroups; q0 += 4) {  // four groups' loads in flight
-    double2 v[4];  // (groups past ngroups are inside the window: 16 R groups, q0 % 4 == 0)
+    double2 v[4];  // (groups past ngroups: inside the window when 2 Q % 4 == 0, else guarded)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double2*>(&val[64 * (q0 + u) + 2 * lane]);
+    for (int u = 0; u < 4; ++u) v[u] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if ((2 * Q) % 4 == 0 || q0 + u < 2 * Q) v[u] = *reinterpret_cast<const double2*>(&val[64 * (q0 + u) + 2 * lane]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int q = q0 + u;
@@ -963,7 +976,8 @@ __device__ void process_row_window_z(const Args& g, const RowAhead& cur, RowAhea
 // position.
 template <int G, int kLanes>
 __device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restrict__ rows, int32_t nrows_bin,
-                                          const int32_t* __restrict__ tcol, const double* __restrict__ tval) {
+                                          const int32_t* __restrict__ tcol, const double* __restrict__ tval,
+                                          const int8_t* __restrict__ bin_of = nullptr) {
   __shared__ int blk_changed;
   if (threadIdx.x == 0) blk_changed = 0;
   __syncthreads();
@@ -972,7 +986,9 @@ __device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restri
   const int64_t nt = (static_cast<int64_t>(gridDim.x) * blockDim.x) / kLanes;
   bool diff = false;
   for (int64_t r = t0; r < nrows_bin; r += nt) {
-    const int32_t j = rows[r];
+    // staged rows in row order (bin_of: the hash / window rows) or a bin's list
+    if (bin_of && bin_of[r] < kFirstSmemBin) continue;
+    const int32_t j = bin_of ? static_cast<int32_t>(r) : rows[r];
     const int32_t* col;
     const double* v;
     if (G == 0) {
@@ -1012,9 +1028,9 @@ __device__ __forceinline__ void emit_rows(const Args& g, const int32_t* __restri
   if (threadIdx.x == 0 && blk_changed) atomicOr(g.changed, 1);
 }
 
-__global__ void __launch_bounds__(256) spgemm_stage_emit(Args g, const int32_t* __restrict__ rows,
-                                                          int32_t nrows_bin) {
-  emit_rows<0, 8>(g, rows, nrows_bin, nullptr, nullptr);
+__global__ void __launch_bounds__(256) spgemm_stage_emit(Args g, const int8_t* __restrict__ bin_of) {
+  // every staged row, in row order: the output is written front to back
+  emit_rows<0, 8>(g, nullptr, static_cast<int32_t>(g.n), nullptr, nullptr, bin_of);
 }
 
 __host__ __device__ constexpr int smem_per_warp(int logs) {
@@ -1057,33 +1073,43 @@ __global__ void __launch_bounds__(256) spgemm_window(Args g, const int32_t* __re
   }
 }
 
-template <int R>
+constexpr int kRun = 8;  // window rows: consecutive list rows per warp
+__host__ __device__ constexpr int zwindow_smem_per_warp(int Q) {
+  return (128 * Q * 8 + 64 * 4 + static_cast<int>(sizeof(ZStage)) + 15) / 16 * 16;
+}
+template <int Q>
 __global__ void __launch_bounds__(256) spgemm_window_z(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                        const int32_t* __restrict__ wbase, bool numeric) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned char* mine = smem + w * window_smem_per_warp(R);
+  unsigned char* mine = smem + w * zwindow_smem_per_warp(Q);
   double* val = reinterpret_cast<double*>(mine);
-  uint32_t* kbits = reinterpret_cast<uint32_t*>(mine + 1024 * R * 8);
-  WarpStage* st = reinterpret_cast<WarpStage*>(kbits + 64 * R);
-  for (int s = lane; s < 1024 * R; s += 32) val[s] = -0.0;
+  uint32_t* kbits = reinterpret_cast<uint32_t*>(mine + 128 * Q * 8);
+  ZStage* st = reinterpret_cast<ZStage*>(kbits + 64);
+  for (int s = lane; s < 128 * Q; s += 32) val[s] = -0.0;
   __syncwarp();
+  // warp w takes runs of kRun consecutive list rows, run w, w + W, ...
+  // (W = all warps): rows processed side by side stay close (their B rows
+  // share L2), and a warp's staging chunk holds whole runs, so the numeric
+  // copy (list order) reads the staging area in runs too
   const int warps = blockDim.x >> 5;
-  const int32_t stride = gridDim.x * warps;
+  const int64_t jump = static_cast<int64_t>(gridDim.x) * warps * kRun;
+  auto next_row = [&](int64_t r) { return (r + 1) % kRun ? r + 1 : r + 1 - kRun + jump; };
   unsigned long long cpos = 0, cend = 0;  // this warp's staging chunk
-  int32_t r = blockIdx.x * warps + w;
+  int64_t r = (static_cast<int64_t>(blockIdx.x) * warps + w) * kRun;
   RowAhead nx;
   if (r < nrows_bin)
-    while (nx.stage < 4) nx.step(g, rows, r, wbase, lane);
-  for (; r < nrows_bin; r += stride) {
+    while (nx.stage < 4) nx.step(g, rows, static_cast<int32_t>(r), wbase, lane);
+  for (; r < nrows_bin; r = next_row(r)) {
     const RowAhead cur = nx;
-    const int32_t rn = r + stride;
+    const int64_t rn64 = next_row(r);
+    const int32_t rn = static_cast<int32_t>(min(rn64, static_cast<int64_t>(nrows_bin)));
     nx = RowAhead{};
-    if (rn >= nrows_bin) nx.stage = 4;
+    if (rn64 >= nrows_bin) nx.stage = 4;
     if (numeric)
-      process_row_window_z<R, true>(g, cur, nx, rows, rn, wbase, val, kbits, st, lane, cpos, cend);
+      process_row_window_z<Q, true>(g, cur, nx, rows, rn, wbase, val, kbits, st, lane, cpos, cend);
     else
-      process_row_window_z<R, false>(g, cur, nx, rows, rn, wbase, val, kbits, st, lane, cpos, cend);
+      process_row_window_z<Q, false>(g, cur, nx, rows, rn, wbase, val, kbits, st, lane, cpos, cend);
     while (nx.stage < 4) nx.step(g, rows, rn, wbase, lane);
   }
 }
@@ -1323,8 +1349,9 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
     }
     if (win && logs >= 8 && hi >= lo) {  // ... whose columns span < 1024 / 2048
       const int32_t span = hi - lo;
-      if (span < 1024) bin = kWinBin1, windowed = true;
-      else if (span < 2048) bin = kWinBin2, windowed = true;
+#pragma unroll
+      for (int q = kNumWinBins - 1; q >= 0; --q)
+        if (span < 128 * win_q(q)) bin = kWinBin0 + q, windowed = true;
     }
     if (p < 32 && m <= 32) bin = (p < 8 && m <= 8) ? 0 : (p < 16 && m <= 16) ? 1 : 2;
     bin_of[j] = static_cast<int8_t>(bin);
@@ -1489,6 +1516,7 @@ struct Plan {
   int32_t* tcol[kTinyBins] = {};
   double* tval[kTinyBins] = {};
   const int32_t* wbase = nullptr;  // window rows: first column of the window
+  const int8_t* bin_of = nullptr;  // row -> bin
 };
 
 void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bool recompute = true,
@@ -1523,8 +1551,8 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
   if (numeric && g.stage_pos) {  // staged hash-table rows: one copy kernel over all of them
     const int32_t cnt = pl.start[kNumBins] - pl.start[kFirstSmemBin];
     if (cnt) {
-      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 31) / 32, int64_t{num_sms()} * 8 * 16));
-      spgemm_stage_emit<<<grid, 256, 0, s>>>(g, pl.lists + pl.start[kFirstSmemBin], cnt);
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((g.n + 31) / 32, int64_t{num_sms()} * 8 * 16));
+      spgemm_stage_emit<<<grid, 256, 0, s>>>(g, pl.bin_of);
       SAIT_LAUNCHED();
     }
     if (!recompute) return;
@@ -1543,25 +1571,51 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
     k<<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, numeric);
     SAIT_LAUNCHED();
   }
-  for (int b = kWinBin1; b <= kWinBin2; ++b) {
+  for (int wb = 0; wb < kNumWinBins; ++wb) {
+    const int b = kWinBin0 + wb;
     const int32_t cnt = pl.hist[b];
     if (!cnt) continue;
-    const int R = b == kWinBin1 ? 1 : 2;
-    const int warps = window_warps(R);
-    const int smem = warps * window_smem_per_warp(R);
+    const int Q = kWinQ[wb];
     static const bool zero_on = [] {  // SAIT_WIN_ZERO=0: the bitmap window for every epilogue
       const char* e = std::getenv("SAIT_WIN_ZERO");
       return !(e && std::atoi(e) == 0);
     }();
-    // threshold builds with +I take the -0.0 window (ZeroWindow)
+    // threshold builds with +I take the -0.0 window (ZeroWindow), sized to
+    // the bin; other epilogues the bitmap window of 1024 R >= 128 Q slots
     const bool zero = zero_on && g.epi.add_identity && (g.epi.drop == 1 || g.epi.drop == 3) && g.epi.tau > 0.0;
     using WK = void (*)(Args, const int32_t*, int32_t, const int32_t*, bool);
-    const WK k = zero ? (R == 1 ? spgemm_window_z<1> : spgemm_window_z<2>) : (R == 1 ? spgemm_window<1> : spgemm_window<2>);
+    WK k;
+    int per_warp, warps = 8;
+    if (zero) {
+      switch (Q) {
+        case 4: k = spgemm_window_z<4>; break;
+        case 5: k = spgemm_window_z<5>; break;
+        case 6: k = spgemm_window_z<6>; break;
+        case 7: k = spgemm_window_z<7>; break;
+        case 8: k = spgemm_window_z<8>; break;
+        default: k = spgemm_window_z<16>;
+      }
+      per_warp = zwindow_smem_per_warp(Q);
+      // warps per CTA: the most resident warps per SM (228 KB of shared
+      // memory, 1 KB reserved per CTA; 64 registers per thread: <= 32 warps)
+      int best = 0;
+      for (int w = 8; w >= 1; --w) {
+        const int res = std::min((228 * 1024) / (w * per_warp + 1024), 32 / w) * w;
+        if (res > best) best = res, warps = w;
+      }
+    } else {
+      const int R = Q <= 8 ? 1 : 2;
+      k = R == 1 ? spgemm_window<1> : spgemm_window<2>;
+      per_warp = window_smem_per_warp(R);
+      warps = window_warps(R);
+    }
+    const int smem = warps * per_warp;
     if (first_on_device(reinterpret_cast<const void*>(k)))
-      SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      SAIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     const int blocks_per_sm = std::max(1, (228 * 1024) / (smem + 1024));
-    const unsigned grid = static_cast<unsigned>(
-        std::min<int64_t>((cnt + warps - 1) / warps, int64_t{num_sms()} * blocks_per_sm * 4));
+    const int64_t per_warp_rows = zero ? kRun : 1;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(
+        (cnt + warps * per_warp_rows - 1) / (warps * per_warp_rows), int64_t{num_sms()} * blocks_per_sm * 4));
     k<<<grid, warps * 32, smem, s>>>(g, pl.lists + pl.start[b], cnt, pl.wbase, numeric);
     SAIT_LAUNCHED();
   }
@@ -1723,6 +1777,7 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   // ---- plan: bin rows by product count
   Plan pl;
   int8_t* bin_of = dalloc<int8_t>(n, s);
+  pl.bin_of = bin_of;
   int32_t* logs_of = dalloc<int32_t>(n, s);
   int32_t* hist = dalloc<int32_t>(2 * kNumBins, s);
   unsigned long long* total = dalloc<unsigned long long>(2, s);  // all products, hash-row products

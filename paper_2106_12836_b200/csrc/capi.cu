@@ -420,6 +420,7 @@ class Recursion {
     epi_.qrp = a_.rp;
     epi_.qci = a_.ci;
     epi_.qv = a_.v;
+    epi_.qnnz = a_.nnz;
     // the last allowed step writes M D^-1 directly (an earlier early stop
     // leaves the scaling to finish)
     const bool last = out_scale_ && main_left_ == 1;

@@ -226,6 +226,7 @@ struct Epilogue {
   const int32_t* qrp = nullptr;
   const int32_t* qci = nullptr;
   const double* qv = nullptr;
+  int64_t qnnz = -1;  // its stored entries, if known: a result of another size is not stable
   // final step of a row-form build: written values are v * out_scale[col]
   // (scale_columns, kernels.cpp:236-246, fused); staging and the
   // stabilization compare see the unscaled values

@@ -674,11 +674,15 @@ struct RowAhead {
   }
 };
 
-// accumulate_zero's staging of one chunk of <= 32 A entries
+// accumulate_zero's staging of one chunk of <= 32 A entries: entry r's value
+// and its B row start minus its first product index, one 16-byte load
+struct __align__(16) ZEnt {
+  double aval;
+  int32_t bbase;  // B entry of product p = bbase + p
+  int32_t pad;
+};
 struct ZStage {
-  double aval[32];
-  int32_t off[33];
-  int32_t bstart[32];
+  ZEnt e[32];
 };
 
 // accumulate_row for a ZeroWindow with the row's first A chunk already
@@ -716,9 +720,7 @@ __device__ __forceinline__ int32_t accumulate_zero(const Args& g, const RowAhead
     const unsigned ne = __ballot_sync(0xffffffffu, has);
     if (has) {
       const int r = __popc(ne & ((1u << lane) - 1u));
-      st->off[r] = excl;
-      st->bstart[r] = bst;
-      st->aval[r] = aval;
+      st->e[r] = ZEnt{aval, bst - excl, 0};
     }
     __syncwarp();
     auto fetch = [&](int32_t pb, int32_t& c, double& a, double& b, int& owner) {
@@ -732,10 +734,11 @@ __device__ __forceinline__ int32_t accumulate_zero(const Args& g, const RowAhead
       owner = r0;
       if (p < total) {
         const int r = r0 + __popc(starts & ((2u << lane) - 1u));
-        SAIT_DCHECK(r >= 0 && r < 32 && p >= st->off[r], "spgemm product owner", r, 32);
-        const int32_t bi = st->bstart[r] + (p - st->off[r]);
+        SAIT_DCHECK(r >= 0 && r < 32, "spgemm product owner", r, 32);
+        const ZEnt z = st->e[r];
+        const int32_t bi = z.bbase + p;
         c = g.bci[bi];
-        a = st->aval[r];
+        a = z.aval;
         b = g.bv[bi];
         owner = r;
       }
@@ -1074,11 +1077,14 @@ __global__ void __launch_bounds__(256) spgemm_window(Args g, const int32_t* __re
 }
 
 constexpr int kRun = 8;  // window rows: consecutive list rows per warp
+#ifndef SAIT_ZMINB
+#define SAIT_ZMINB 1
+#endif
 __host__ __device__ constexpr int zwindow_smem_per_warp(int Q) {
   return (128 * Q * 8 + 64 * 4 + static_cast<int>(sizeof(ZStage)) + 15) / 16 * 16;
 }
 template <int Q>
-__global__ void __launch_bounds__(256) spgemm_window_z(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+__global__ void __launch_bounds__(256, SAIT_ZMINB) spgemm_window_z(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                        const int32_t* __restrict__ wbase, bool numeric) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1597,10 +1603,14 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
       }
       per_warp = zwindow_smem_per_warp(Q);
       // warps per CTA: the most resident warps per SM (228 KB of shared
-      // memory, 1 KB reserved per CTA; 64 registers per thread: <= 32 warps)
+      // memory, 1 KB reserved per CTA; 64 K registers, allocated per warp in
+      // units of 256)
+      cudaFuncAttributes fa{};
+      SAIT_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(k)));
+      const int reg_warps = 65536 / (((fa.numRegs * 32 + 255) / 256) * 256);
       int best = 0;
       for (int w = 8; w >= 1; --w) {
-        const int res = std::min((228 * 1024) / (w * per_warp + 1024), 32 / w) * w;
+        const int res = std::min((228 * 1024) / (w * per_warp + 1024), reg_warps / w) * w;
         if (res > best) best = res, warps = w;
       }
     } else {
@@ -1893,10 +1903,14 @@ SpgemmResult spgemm_fused(const DevCsr& a, const DevCsr& b, const Epilogue& epi,
   g.cci = c.ci;
   g.cv = c.v;
   g.changed = changed;
+  // stabilized() compares the row pointers first (sait.cpp:19): a result of
+  // another size has changed, and the numeric pass skips the value compare
+  const bool compare = epi.qrp && !(epi.qnnz >= 0 && epi.qnnz != c.nnz);
+  if (!compare) g.epi.qrp = g.epi.qci = nullptr, g.epi.qv = nullptr;
   const bool overflow = g.stage_pos && static_cast<unsigned long long>(hmeta[1]) >
                                            static_cast<unsigned long long>(g.stage_cap);
   launch_pass(g, pl, true, s, overflow, c.nnz <= 8 * n);
-  if (epi.qrp) {
+  if (compare) {
     int hc = 1;
     read_back(s, {{&hc, changed, sizeof hc}});
     res.changed = hc != 0;

@@ -1076,7 +1076,7 @@ def run_build_c4(S, torch, cpu_sample=True):
         "roofline": {"bound": "hbm (compulsory bytes; the build is gather/hash-bound)", "algorithmic_bytes": B,
                      "achieved": B / t / 1e9, "peak": peak, "unit": "GB/s", "frac": B / t / 1e9 / peak,
                      "peak_source": src},
-        "note": "wall time of the synchronous sait_build call (split, 3 recursion steps, transposes), "
+        "note": "wall time of the synchronous sait_build call (split, 3 row-form recursion steps, the per-column cap pass after steps 2 and 3), "
                 "median of %d after a warm-up" % C4_REPS,
         "irregular_apply": irregular,
         "e2e_host": e2e_host,

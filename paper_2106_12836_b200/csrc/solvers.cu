@@ -682,6 +682,55 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
       const char* e = std::getenv("SAIT_LOBPCG_FUSED");
       return e && e[0] == '0';
     }();
+    const bool defer_w = fast_gram && !fused_off && k == 8;
+    // deferred W normalisation (fast mode): W_n = W Rwi with Rwi = L^-T, L the
+    // Cholesky factor of W^T W = GB[k:2k, k:2k]; the Grams of [X W_n P] are
+    // T^T G T with T = diag(I, Rwi, I)
+    std::vector<double> Rwi(k * k);
+    bool w_deficient = false;
+    auto normalize_w = [&](std::vector<double>& GA2, std::vector<double>& GB2, int mm) {
+      std::vector<double> Gw(k * k), Lw(k * k), Lwi(k * k), tmpG(static_cast<size_t>(mm) * mm);
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) Gw[i * k + j] = GB2[(k + i) * mm + k + j];
+      if (!sait::chol_lower(Gw.data(), k, Lw.data())) return false;
+      sait::tri_lower_inv(Lw.data(), k, Lwi.data());
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) Rwi[i * k + j] = Lwi[j * k + i];
+      for (std::vector<double>* Gp : {&GA2, &GB2}) {
+        std::vector<double>& G = *Gp;
+        tmpG = G;  // G T: the W columns
+        for (int a2 = 0; a2 < mm; ++a2)
+          for (int j = 0; j < k; ++j) {
+            double t = 0.0;
+            for (int q = 0; q <= j; ++q) t += G[a2 * mm + k + q] * Rwi[q * k + j];
+            tmpG[a2 * mm + k + j] = t;
+          }
+        G = tmpG;  // T^T (G T): the W rows
+        for (int i = 0; i < k; ++i)
+          for (int b2 = 0; b2 < mm; ++b2) {
+            double t = 0.0;
+            for (int q = 0; q <= i; ++q) t += Rwi[q * k + i] * tmpG[(k + q) * mm + b2];
+            G[(k + i) * mm + b2] = t;
+          }
+        for (int i = 0; i < mm; ++i)  // exactly symmetric
+          for (int j = i + 1; j < mm; ++j) {
+            const double s2 = 0.5 * (G[i * mm + j] + G[j * mm + i]);
+            G[i * mm + j] = s2;
+            G[j * mm + i] = s2;
+          }
+      }
+      return true;
+    };
+    auto unnormalize_w_rows = [&](double* Cw) {  // k rows of k coefficients: Cw <- Rwi Cw
+      std::vector<double> t(k * k);
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) {
+          double a = 0.0;
+          for (int q = i; q < k; ++q) a += Rwi[i * k + q] * Cw[q * k + j];
+          t[i * k + j] = a;
+        }
+      std::copy(t.begin(), t.end(), Cw);
+    };
     auto tp = std::chrono::steady_clock::now();
     auto phase = [&](const char* nm) {
       if (!dbg) return;
@@ -746,7 +795,11 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
           SAIT_CUDA(cudaMemcpyAsync(dg, G1.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, s));
           sait::block_sub_lincomb(n, X, k, dg, W, s);
         }
-        if (!cholqr(W, nullptr)) {
+        // fast mode defers W's Cholesky-QR: the Rayleigh-Ritz Gram already
+        // holds W^T W, so the normalisation W R^-1 is applied to the Grams and
+        // folded into the update coefficients on the host (no W^T W pass, no
+        // W R^-1 pass); the canonical mode keeps the restatement's cholqr
+        if (!defer_w && !cholqr(W, nullptr)) {
           failed = true;
           why = "lobpcg: preconditioned residual block is rank deficient";
           break;
@@ -804,6 +857,10 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
               GA[i * m + j] = s2;
               GA[j * m + i] = s2;
             }
+          if (defer_w && !normalize_w(GA, GB, m)) {
+            w_deficient = true;
+            break;
+          }
           if (sait::rayleigh_ritz(GA.data(), GB.data(), m, k, C.data(), lam.data())) {
             ok = true;
             break;
@@ -815,6 +872,11 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
           break;
         }
         phase("rr");
+        if (w_deficient) {
+          failed = true;
+          why = "lobpcg: preconditioned residual block is rank deficient";
+          break;
+        }
         if (!ok) {
           failed = true;
           why = "lobpcg: Gram matrix not positive definite";
@@ -858,6 +920,10 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
             Cp = Cpf.data();
             p_normed = true;
           }
+        }
+        if (defer_w) {  // coefficients of the normalised W -> of the stored W (rows of W: Rwi c)
+          unnormalize_w_rows(C.data() + k * k);  // X's coefficients (and P's, when Cp points into C)
+          if (Cp != C.data() + k * k) unnormalize_w_rows(Cpf.data());
         }
         if (!fused_off && sait::lobpcg_update_fused(n, k, m, S, AS, C.data(), Cp, lam.data(), R, s)) {
           r_ready = true;  // (canonical mode: bitwise the four lincombs + the next residual)

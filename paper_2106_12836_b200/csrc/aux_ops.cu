@@ -45,11 +45,6 @@ __global__ void validate_kernel(int64_t nrows, int64_t ncols, int64_t nnz, const
   if (code) atomicMin(first, (static_cast<unsigned long long>(i) << 2) | code);
 }
 
-__global__ void column_count_kernel(int64_t nnz, const int32_t* __restrict__ ci, int32_t* __restrict__ cnt) {
-  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e < nnz) atomicAdd(&cnt[ci[e]], 1);
-}
-
 __global__ void cap_kernel(int64_t n, double f, int32_t* __restrict__ cnt) {
   int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j < n) {
@@ -123,12 +118,11 @@ void validate_device_csr(const DevCsr& m, cudaStream_t s) {
   }
 }
 
+void column_counts_add(const DevCsr& m, int32_t* cnt, cudaStream_t s);  // cap.cu
+
 void column_caps(const DevCsr& t, double factor, int32_t* cap, cudaStream_t s) {
   SAIT_CUDA(cudaMemsetAsync(cap, 0, sizeof(int32_t) * (t.ncols ? t.ncols : 1), s));
-  if (t.nnz) {
-    column_count_kernel<<<grid_for(t.nnz, 256), 256, 0, s>>>(t.nnz, t.ci, cap);
-    SAIT_LAUNCHED();
-  }
+  column_counts_add(t, cap, s);
   if (t.ncols) {
     cap_kernel<<<grid_for(t.ncols, 256), 256, 0, s>>>(t.ncols, factor, cap);
     SAIT_LAUNCHED();

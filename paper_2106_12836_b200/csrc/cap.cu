@@ -21,16 +21,53 @@ namespace {
 
 // entries are visited flat, 4 per thread (one 16-byte load of columns)
 constexpr int kFlat = 4;
-__global__ void cap_count_cols(int64_t nnz, const int32_t* __restrict__ ci, int32_t* __restrict__ cnt) {
-  const int64_t e0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kFlat;
-  if (e0 + kFlat <= nnz) {
-    const int4 c = *reinterpret_cast<const int4*>(ci + e0);
-    atomicAdd(&cnt[c.x], 1);
-    atomicAdd(&cnt[c.y], 1);
-    atomicAdd(&cnt[c.z], 1);
-    atomicAdd(&cnt[c.w], 1);
+// Column counts of a (sorted) CSR, added into cnt.  A block takes 1024
+// consecutive rows; when their columns span at most kColBins (banded and
+// near-diagonal matrices: the triangular factors, T, the SAIT iterates) it
+// counts into a shared histogram and flushes only the touched bins -- one
+// global atomic per (block, column) instead of one per entry -- else it
+// falls back to one global atomic per entry.
+constexpr int kColRows = 1024, kColBins = 8192;
+__global__ void __launch_bounds__(256) col_counts_banded(int64_t nrows, const int32_t* __restrict__ rp,
+                                                         const int32_t* __restrict__ ci, int32_t* __restrict__ cnt) {
+  __shared__ int32_t h[kColBins];
+  __shared__ int32_t lo_s, hi_s;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kColRows;
+  const int64_t r1 = min(r0 + kColRows, nrows);
+  if (threadIdx.x == 0) {
+    lo_s = INT32_MAX;
+    hi_s = -1;
+  }
+  __syncthreads();
+  int32_t lo = INT32_MAX, hi = -1;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const int32_t b = rp[r], e = rp[r + 1];
+    if (b < e) {
+      lo = min(lo, ci[b]);
+      hi = max(hi, ci[e - 1]);
+    }
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&lo_s, lo);
+    atomicMax(&hi_s, hi);
+  }
+  __syncthreads();
+  lo = lo_s;
+  hi = hi_s;
+  if (hi < lo) return;
+  const int64_t e0 = rp[r0], e1 = rp[r1];
+  if (static_cast<int64_t>(hi) - lo < kColBins) {
+    const int range = hi - lo + 1;
+    for (int b = threadIdx.x; b < range; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&h[ci[e] - lo], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < range; b += blockDim.x)
+      if (h[b]) atomicAdd(&cnt[lo + b], h[b]);
   } else {
-    for (int64_t e = e0; e < nnz; ++e) atomicAdd(&cnt[ci[e]], 1);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&cnt[ci[e]], 1);
   }
 }
 
@@ -187,6 +224,12 @@ __global__ void stable_rows(int64_t nrows, const int32_t* __restrict__ arp, cons
 
 }  // namespace
 
+void column_counts_add(const DevCsr& m, int32_t* cnt, cudaStream_t s) {
+  if (m.nrows == 0 || m.nnz == 0) return;
+  col_counts_banded<<<grid_for(m.nrows, kColRows), 256, 0, s>>>(m.nrows, m.rp, m.ci, cnt);
+  SAIT_LAUNCHED();
+}
+
 // Applies the cap to m in place; returns the number of entries dropped.
 // With out_scale (the last step), a compaction also scales the columns and
 // *scaled is set.
@@ -202,7 +245,7 @@ int64_t cap_rowform(DevCsr& m, const int32_t* cap, cudaStream_t s, const double*
   int32_t* nflag_d = dalloc<int32_t>(1, s);
   SAIT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, s));
   SAIT_CUDA(cudaMemsetAsync(nflag_d, 0, sizeof(int32_t), s));
-  cap_count_cols<<<grid_for((m.nnz + kFlat - 1) / kFlat, 256), 256, 0, s>>>(m.nnz, m.ci, cnt);
+  col_counts_banded<<<grid_for(n, kColRows), 256, 0, s>>>(n, m.rp, m.ci, cnt);
   SAIT_LAUNCHED();
   cap_flag<<<grid_for(n, 256), 256, 0, s>>>(n, cnt, cap, seglen, bits, flagged, nflag_d);
   SAIT_LAUNCHED();

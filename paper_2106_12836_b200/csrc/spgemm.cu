@@ -811,8 +811,9 @@ __device__ void process_row_window_z(const Args& g, const RowAhead& cur, RowAhea
       const int s0 = 64 * q + 2 * lane;
       const bool k0 = s0 == sd || fabs(v[u].x) >= tau;
       const bool k1 = s0 + 1 == sd || fabs(v[u].y) >= tau;
-      if (!k0) val[s0] = -0.0;
-      if (!k1) val[s0 + 1] = -0.0;
+      // one 16-byte store per lane (4 wavefronts per group; two predicated
+      // 8-byte stores cost 8): dropped slots back to -0.0, kept ones as they are
+      *reinterpret_cast<double2*>(&val[s0]) = make_double2(k0 ? v[u].x : -0.0, k1 ? v[u].y : -0.0);
       const unsigned E = __ballot_sync(0xffffffffu, k0), O = __ballot_sync(0xffffffffu, k1);
       if (lane == q) {
         kE = E;

@@ -150,6 +150,26 @@ void reserve_pool(cudaMemPool_t pool, size_t bytes) {
   cudaGetLastError();
 }
 
+// Grows the pool to `bytes` in one bulk mapping when it holds less: a fresh
+// process's first build otherwise maps its working set allocation by
+// allocation (~6.5 GB/s; the first config-4 build took 0.27 s against
+// 0.14 s warm, one bulk 12 GiB mapping 0.07 s).  Capped at 80 % of the free
+// device memory; the pool keeps what it maps (release threshold unlimited),
+// as it would after the incremental growth.
+void ensure_pool(size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t have = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have);
+  if (have >= bytes) return;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
+  const size_t want = std::min(bytes, have + free_b / 10 * 8);
+  if (want > have) reserve_pool(pool, want);
+}
+
 void init_device_pool() {
   static std::once_flag once[64];
   int dev = 0;
@@ -1114,6 +1134,10 @@ int sait_build_session_create(sait_dcsr_t t, int lower, const sait_drop_spec* sp
       sait::column_caps(t->m, spec->cap_factor, ss->cap, s);
     }
     ss->rec = new Recursion(ss->ttT, *spec, ss->cap, col0, col1 - col0, s, ss->row_form, ss->inv);
+    // the build's working set (two iterates, the staging area, tT, the
+    // plan): ~64 B per entry of T plus ~40 B per row, mapped up front
+    if (!std::getenv("SAIT_NO_POOL_ESTIMATE"))
+      ensure_pool(static_cast<size_t>(64 * t->m.nnz * (col1 - col0) / std::max<int64_t>(n, 1) + 40 * n));
     *out = ss;
   });
 }

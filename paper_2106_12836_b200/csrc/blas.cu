@@ -237,6 +237,24 @@ __global__ void __launch_bounds__(256) block_lincomb_param(int64_t n, const doub
 // in input order; block_residual_k: fma(-lam, X, AX)), so the result is
 // bitwise the unfused sequence; the fusion saves the re-reads of [W P],
 // [AW AP], X and AX (5 of 17 block passes per iteration).
+// Fast mode: the next residual's squared column norms as block partials
+// (fixed order: each thread's r_j^2, the 32-lane butterfly, the 8-warp tree;
+// part[j * gridDim.x + block]), folded by mdot_final -- deterministic, and
+// the residual block is not read again for its norms.  r == nullptr: a thread
+// past the end contributes zeros.
+__device__ __forceinline__ void lobpcg_norm_partials(const double* r, double* part) {
+  __shared__ double ws[8][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double v = r ? __dmul_rn(r[j], r[j]) : 0.0;
+    const double w = warp_butterfly(v);
+    if (lane == 0) ws[j][warp] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) part[static_cast<int64_t>(threadIdx.x) * gridDim.x + blockIdx.x] = tree8(ws[threadIdx.x]);
+}
+
 template <int M>
 struct UpdateCoef {
   double c[M * 8];         // X <- S C
@@ -271,9 +289,12 @@ __global__ void __launch_bounds__(256) lobpcg_update_xp(int64_t n, double* S, Up
 }
 template <int M>
 __global__ void __launch_bounds__(256) lobpcg_update_axp_r(int64_t n, double* AS, const double* X, UpdateCoef<M> C,
-                                                            double* R) {
+                                                            double* R, double* __restrict__ normpart) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n) {
+    if (normpart) lobpcg_norm_partials(nullptr, normpart);  // (the block's barriers need every thread)
+    return;
+  }
   double xq[M];
 #pragma unroll
   for (int q = 0; q < M; ++q) xq[q] = ld_ro(AS + n * q + i);
@@ -290,12 +311,15 @@ __global__ void __launch_bounds__(256) lobpcg_update_axp_r(int64_t n, double* AS
       ax[j] = __fma_rn(xq[q], C.c[q * 8 + j], ax[j]);
       if (q > 8) ap[j] = __fma_rn(xq[q], C.cp[(q - 8) * 8 + j], ap[j]);
     }
+  double r[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     AS[n * j + i] = ax[j];
     AS[n * (16 + j) + i] = ap[j];
-    R[n * j + i] = __fma_rn(-C.lam[j], ld_ro(X + n * j + i), ax[j]);
+    r[j] = __fma_rn(-C.lam[j], ld_ro(X + n * j + i), ax[j]);
+    R[n * j + i] = r[j];
   }
+  if (normpart) lobpcg_norm_partials(r, normpart);
 }
 
 // W[:, j] = (((W_j - X_0 G[0][j]) - X_1 G[1][j]) - ...)
@@ -516,14 +540,14 @@ bool block_lincomb_host_coef(int64_t n, const double* in, int kin, const double*
 namespace {
 template <int M>
 void launch_update(int64_t n, double* S, double* AS, const double* C_host, const double* Cp_host,
-                   const double* lam_host, double* R, cudaStream_t s) {
+                   const double* lam_host, double* R, double* normpart, cudaStream_t s) {
   UpdateCoef<M> cb;
   std::memcpy(cb.c, C_host, sizeof cb.c);
   std::memcpy(cb.cp, Cp_host, sizeof cb.cp);
   std::memcpy(cb.lam, lam_host, sizeof cb.lam);
   lobpcg_update_xp<M><<<grid_for(n, 256), 256, 0, s>>>(n, S, cb);
   SAIT_LAUNCHED();
-  lobpcg_update_axp_r<M><<<grid_for(n, 256), 256, 0, s>>>(n, AS, S, cb, R);
+  lobpcg_update_axp_r<M><<<grid_for(n, 256), 256, 0, s>>>(n, AS, S, cb, R, normpart);
   SAIT_LAUNCHED();
 }
 }  // namespace
@@ -532,11 +556,22 @@ void launch_update(int64_t n, double* S, double* AS, const double* C_host, const
 // or 24: the fused update above (Cp: the (m - 8) x 8 coefficients of P and
 // AP); false for shapes it does not cover.
 bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host, const double* Cp_host,
-                         const double* lam_host, double* R, cudaStream_t s) {
+                         const double* lam_host, double* R, cudaStream_t s, double* norms) {
   if (k != 8 || n <= 0) return false;
-  if (m == 16) launch_update<16>(n, S, AS, C_host, Cp_host, lam_host, R, s);
-  else if (m == 24) launch_update<24>(n, S, AS, C_host, Cp_host, lam_host, R, s);
-  else return false;
+  double* part = nullptr;
+  const int64_t nb = grid_for(n, 256);
+  if (norms) part = dalloc<double>(8 * nb, s);
+  if (m == 16) launch_update<16>(n, S, AS, C_host, Cp_host, lam_host, R, part, s);
+  else if (m == 24) launch_update<24>(n, S, AS, C_host, Cp_host, lam_host, R, part, s);
+  else {
+    dfree(part, s);
+    return false;
+  }
+  if (norms) {  // ||R_j|| for the next convergence test, from the update's partials
+    mdot_final<<<8, kT, 0, s>>>(part, nb, norms, 1);
+    SAIT_LAUNCHED();
+    dfree(part, s);
+  }
   return true;
 }
 bool block_sub_lincomb_host_coef(int64_t n, const double* X, int k, const double* G_host, double* W,

@@ -52,7 +52,7 @@ void block_sub_lincomb(int64_t n, const double* X, int k, const double* G, doubl
 bool block_sub_lincomb_host_coef(int64_t n, const double* X, int k, const double* G_host, double* W,
                                  cudaStream_t s);
 bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host, const double* Cp_host,
-                         const double* lam_host, double* R, cudaStream_t s);
+                         const double* lam_host, double* R, cudaStream_t s, double* norms = nullptr);
 void block_residual(int64_t n, int k, const double* AX, const double* X, const double* lam, double* R,
                     cudaStream_t s);
 void pair_apply_block_internal(sait_pair_t p, const double* r, double* z, int64_t n, int64_t nvec, int layout,
@@ -603,7 +603,6 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     double* S = sait::dalloc<double>(6 * blk, s);  // [X W P | AX AW AP]: one allocation (gram_rr)
     double* AS = S + 3 * blk;
     double* R = sait::dalloc<double>(blk, s);
-    double* tmp = sait::dalloc<double>(4 * blk, s);
     // small host->device operands (Gram corrections, coefficient blocks) use a
     // ring of slots so consecutive uploads need no synchronisation
     constexpr int kSlots = 8;
@@ -758,6 +757,7 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
       lincomb(X, k, C.data(), k, X);
       lincomb(AX, k, C.data(), k, AX);
       bool r_ready = false;   // R already written by the fused update
+      bool norms_ready = false;  // ... and its column norms in sc.d (fast mode)
       bool p_normed = false;  // P, AP already orthonormalised (fast mode)
       for (it = 0; it <= maxit; ++it) {
         if (!r_ready) {
@@ -766,9 +766,11 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
           sait::block_residual(n, k, AX, X, dl, R, s);
         }
         r_ready = false;
-        for (int j = 0; j < k; ++j)
-          sait::multi_dot(n, R + static_cast<int64_t>(j) * n, R + static_cast<int64_t>(j) * n, n, 1, sc.d + j, sc.part,
-                          s, true);
+        if (!norms_ready)
+          for (int j = 0; j < k; ++j)
+            sait::multi_dot(n, R + static_cast<int64_t>(j) * n, R + static_cast<int64_t>(j) * n, n, 1, sc.d + j,
+                            sc.part, s, true);
+        norms_ready = false;
         sc.fetch(k, s);
         conv = true;
         for (int j = 0; j < k; ++j) {
@@ -925,8 +927,13 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
           unnormalize_w_rows(C.data() + k * k);  // X's coefficients (and P's, when Cp points into C)
           if (Cp != C.data() + k * k) unnormalize_w_rows(Cpf.data());
         }
-        if (!fused_off && sait::lobpcg_update_fused(n, k, m, S, AS, C.data(), Cp, lam.data(), R, s)) {
+        // fast mode: the update also leaves the next residual's norms in sc.d
+        // (block partials of its own pass; the canonical mode keeps the
+        // restatement's per-column dots)
+        if (!fused_off && sait::lobpcg_update_fused(n, k, m, S, AS, C.data(), Cp, lam.data(), R, s,
+                                                    defer_w ? sc.d : nullptr)) {
           r_ready = true;  // (canonical mode: bitwise the four lincombs + the next residual)
+          norms_ready = defer_w;
         } else {
           p_normed = false;
           lincomb(S, m, C.data(), k, X);
@@ -954,7 +961,6 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
     SAIT_CUDA(cudaStreamSynchronize(s));
     sait::dfree(S, s);  // (AS lives in the same allocation)
     sait::dfree(R, s);
-    sait::dfree(tmp, s);
     sait::dfree(dsmall, s);
     sait::dfree(gscratch, s);
     sait::dfree(gtiles, s);

@@ -653,6 +653,15 @@ __device__ __forceinline__ double2 ld_ro2(const double* p) {
   asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+// Shared-operand Grams (B = [S | AS] or [S], S = the A blocks) are symmetric
+// -- S^T S exactly, S^T A S mathematically -- so only the tiles on or above
+// the block diagonal are computed (the skipped ones are written as zeros and
+// mirrored on the host): a third fewer FP64 tensor-core operations for the
+// Rayleigh-Ritz pair.
+template <int NA, bool SHARE>
+__host__ __device__ constexpr bool dmma_tile_needed(int ia, int ib) {
+  return !SHARE || (ib < NA ? ib >= ia : ib - NA >= ia);
+}
 template <int NA, int NB, bool SHARE>
 __global__ void __launch_bounds__(NA * NB >= 9 ? 128 : 256) gram_dmma_kernel(int64_t n, DmmaBlocks blk, double* __restrict__ part,
                                                          int64_t nchunks) {
@@ -720,6 +729,7 @@ __global__ void __launch_bounds__(NA * NB >= 9 ? 128 : 256) gram_dmma_kernel(int
       for (int ia = 0; ia < NA; ++ia)
 #pragma unroll
         for (int ib = 0; ib < NB; ++ib) {
+          if (!dmma_tile_needed<NA, SHARE>(ia, ib)) continue;
           const double bv = SHARE ? (ib < NA ? af[u][ib] : bf[u][SHARE ? ib - NA : ib]) : bf[u][ib];
           dmma(acc[ia][ib][0], acc[ia][ib][1], af[u][ia], bv);
         }

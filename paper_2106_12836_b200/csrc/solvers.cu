@@ -833,7 +833,9 @@ static int lobpcg_impl(sait_dcsr_t A, sait::Precond M, int nev, double tol, int 
               for (int a2 = 0; a2 < m; ++a2)
                 for (int b2 = 0; b2 < m; ++b2) {
                   GB[a2 * m + b2] = b2 >= a2 ? sc.h[a2 * 2 * m + b2] : sc.h[b2 * 2 * m + a2];  // exactly symmetric
-                  GA[a2 * m + b2] = sc.h[a2 * 2 * m + m + b2];
+                  // S^T AS: the tiles below the block diagonal are not
+                  // computed (gram_dmma_kernel); mirror the upper ones
+                  GA[a2 * m + b2] = b2 / 8 >= a2 / 8 ? sc.h[a2 * 2 * m + m + b2] : sc.h[b2 * 2 * m + m + a2];
                 }
               fast_done = true;
             }

@@ -238,21 +238,20 @@ __global__ void __launch_bounds__(256) block_lincomb_param(int64_t n, const doub
 // bitwise the unfused sequence; the fusion saves the re-reads of [W P],
 // [AW AP], X and AX (5 of 17 block passes per iteration).
 // Fast mode: the next residual's squared column norms as block partials
-// (fixed order: each thread's r_j^2, the 32-lane butterfly, the 8-warp tree;
-// part[j * gridDim.x + block]), folded by mdot_final -- deterministic, and
-// the residual block is not read again for its norms.  r == nullptr: a thread
-// past the end contributes zeros.
-__device__ __forceinline__ void lobpcg_norm_partials(const double* r, double* part) {
-  __shared__ double ws[8][8];
+// (fixed order: each thread's two rows' r_j^2, the 32-lane butterfly, the
+// 8-warp tree; part[j * gridDim.x + block]), folded by mdot_final --
+// deterministic, and the residual block is not read again for its norms.
+// sq == nullptr: a thread past the end contributes zeros.
+__device__ __forceinline__ void lobpcg_norm_partials_sq(const double* sq, double* part) {
+  __shared__ double ws2[8][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const double v = r ? __dmul_rn(r[j], r[j]) : 0.0;
-    const double w = warp_butterfly(v);
-    if (lane == 0) ws[j][warp] = w;
+    const double w = warp_butterfly(sq ? sq[j] : 0.0);
+    if (lane == 0) ws2[j][warp] = w;
   }
   __syncthreads();
-  if (threadIdx.x < 8) part[static_cast<int64_t>(threadIdx.x) * gridDim.x + blockIdx.x] = tree8(ws[threadIdx.x]);
+  if (threadIdx.x < 8) part[static_cast<int64_t>(threadIdx.x) * gridDim.x + blockIdx.x] = tree8(ws2[threadIdx.x]);
 }
 
 template <int M>
@@ -261,65 +260,86 @@ struct UpdateCoef {
   double cp[(M - 8) * 8];  // P <- S[8:M] Cp (Cp = C[8:M], or C[8:M] Ri when P's Cholesky-QR is folded in)
   double lam[8];
 };
+// Two rows per thread (16-byte loads and stores: half the memory
+// instructions of one row per thread, the same operations per element).
 template <int M>
-__global__ void __launch_bounds__(256) lobpcg_update_xp(int64_t n, double* S, UpdateCoef<M> C) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double xq[M];
-#pragma unroll
-  for (int q = 0; q < M; ++q) xq[q] = ld_ro(S + n * q + i);
-  double ax[8], ap[8];
+__device__ __forceinline__ void update_rows(const double2 (&xq)[M], const UpdateCoef<M>& C, double2 (&ax)[8],
+                                            double2 (&ap)[8]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    ax[j] = __dmul_rn(xq[0], C.c[j]);
-    ap[j] = __dmul_rn(xq[8], C.cp[j]);
+    ax[j].x = __dmul_rn(xq[0].x, C.c[j]);
+    ax[j].y = __dmul_rn(xq[0].y, C.c[j]);
+    ap[j].x = __dmul_rn(xq[8].x, C.cp[j]);
+    ap[j].y = __dmul_rn(xq[8].y, C.cp[j]);
   }
 #pragma unroll
   for (int q = 1; q < M; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      ax[j] = __fma_rn(xq[q], C.c[q * 8 + j], ax[j]);
-      if (q > 8) ap[j] = __fma_rn(xq[q], C.cp[(q - 8) * 8 + j], ap[j]);
+      ax[j].x = __fma_rn(xq[q].x, C.c[q * 8 + j], ax[j].x);
+      ax[j].y = __fma_rn(xq[q].y, C.c[q * 8 + j], ax[j].y);
+      if (q > 8) {
+        ap[j].x = __fma_rn(xq[q].x, C.cp[(q - 8) * 8 + j], ap[j].x);
+        ap[j].y = __fma_rn(xq[q].y, C.cp[(q - 8) * 8 + j], ap[j].y);
+      }
     }
+}
+__device__ __forceinline__ double2 ld_ro2u(const double* p, bool pair) {  // (n odd: the last row alone)
+  if (pair) {
+    double2 r;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+  }
+  return make_double2(ld_ro(p), 0.0);
+}
+__device__ __forceinline__ void st2u(double* p, double2 v, bool pair) {
+  if (pair) *reinterpret_cast<double2*>(p) = v;
+  else *p = v.x;
+}
+template <int M>
+__global__ void __launch_bounds__(256) lobpcg_update_xp(int64_t n, double* S, UpdateCoef<M> C) {
+  const int64_t i = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+  if (i >= n) return;
+  const bool pair = i + 1 < n;  // (always: n is even)
+  double2 xq[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) xq[q] = ld_ro2u(S + n * q + i, pair);
+  double2 ax[8], ap[8];
+  update_rows<M>(xq, C, ax, ap);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    S[n * j + i] = ax[j];
-    S[n * (16 + j) + i] = ap[j];
+    st2u(S + n * j + i, ax[j], pair);
+    st2u(S + n * (16 + j) + i, ap[j], pair);
   }
 }
 template <int M>
 __global__ void __launch_bounds__(256) lobpcg_update_axp_r(int64_t n, double* AS, const double* X, UpdateCoef<M> C,
                                                             double* R, double* __restrict__ normpart) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
   if (i >= n) {
-    if (normpart) lobpcg_norm_partials(nullptr, normpart);  // (the block's barriers need every thread)
+    if (normpart) lobpcg_norm_partials_sq(nullptr, normpart);  // (the block's barriers need every thread)
     return;
   }
-  double xq[M];
+  const bool pair = i + 1 < n;
+  double2 xq[M];
 #pragma unroll
-  for (int q = 0; q < M; ++q) xq[q] = ld_ro(AS + n * q + i);
-  double ax[8], ap[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    ax[j] = __dmul_rn(xq[0], C.c[j]);
-    ap[j] = __dmul_rn(xq[8], C.cp[j]);
-  }
-#pragma unroll
-  for (int q = 1; q < M; ++q)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      ax[j] = __fma_rn(xq[q], C.c[q * 8 + j], ax[j]);
-      if (q > 8) ap[j] = __fma_rn(xq[q], C.cp[(q - 8) * 8 + j], ap[j]);
-    }
+  for (int q = 0; q < M; ++q) xq[q] = ld_ro2u(AS + n * q + i, pair);
+  double2 ax[8], ap[8];
+  update_rows<M>(xq, C, ax, ap);
   double r[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    AS[n * j + i] = ax[j];
-    AS[n * (16 + j) + i] = ap[j];
-    r[j] = __fma_rn(-C.lam[j], ld_ro(X + n * j + i), ax[j]);
-    R[n * j + i] = r[j];
+    st2u(AS + n * j + i, ax[j], pair);
+    st2u(AS + n * (16 + j) + i, ap[j], pair);
+    const double2 x = ld_ro2u(X + n * j + i, pair);
+    double2 rr;
+    rr.x = __fma_rn(-C.lam[j], x.x, ax[j].x);
+    rr.y = __fma_rn(-C.lam[j], x.y, ax[j].y);
+    st2u(R + n * j + i, rr, pair);
+    // the norm partials take both rows: x then y (y is 0 past the end)
+    r[j] = pair ? __fma_rn(rr.y, rr.y, __dmul_rn(rr.x, rr.x)) : __dmul_rn(rr.x, rr.x);
   }
-  if (normpart) lobpcg_norm_partials(r, normpart);
+  if (normpart) lobpcg_norm_partials_sq(r, normpart);
 }
 
 // W[:, j] = (((W_j - X_0 G[0][j]) - X_1 G[1][j]) - ...)
@@ -545,9 +565,9 @@ void launch_update(int64_t n, double* S, double* AS, const double* C_host, const
   std::memcpy(cb.c, C_host, sizeof cb.c);
   std::memcpy(cb.cp, Cp_host, sizeof cb.cp);
   std::memcpy(cb.lam, lam_host, sizeof cb.lam);
-  lobpcg_update_xp<M><<<grid_for(n, 256), 256, 0, s>>>(n, S, cb);
+  lobpcg_update_xp<M><<<grid_for((n + 1) / 2, 256), 256, 0, s>>>(n, S, cb);
   SAIT_LAUNCHED();
-  lobpcg_update_axp_r<M><<<grid_for(n, 256), 256, 0, s>>>(n, AS, S, cb, R, normpart);
+  lobpcg_update_axp_r<M><<<grid_for((n + 1) / 2, 256), 256, 0, s>>>(n, AS, S, cb, R, normpart);
   SAIT_LAUNCHED();
 }
 }  // namespace
@@ -557,9 +577,9 @@ void launch_update(int64_t n, double* S, double* AS, const double* C_host, const
 // AP); false for shapes it does not cover.
 bool lobpcg_update_fused(int64_t n, int k, int m, double* S, double* AS, const double* C_host, const double* Cp_host,
                          const double* lam_host, double* R, cudaStream_t s, double* norms) {
-  if (k != 8 || n <= 0) return false;
+  if (k != 8 || n <= 0 || n % 2) return false;  // (two rows per thread, 16-byte aligned columns)
   double* part = nullptr;
-  const int64_t nb = grid_for(n, 256);
+  const int64_t nb = grid_for((n + 1) / 2, 256);
   if (norms) part = dalloc<double>(8 * nb, s);
   if (m == 16) launch_update<16>(n, S, AS, C_host, Cp_host, lam_host, R, part, s);
   else if (m == 24) launch_update<24>(n, S, AS, C_host, Cp_host, lam_host, R, part, s);

@@ -1078,14 +1078,11 @@ __global__ void __launch_bounds__(256) spgemm_window(Args g, const int32_t* __re
 }
 
 constexpr int kRun = 8;  // window rows: consecutive list rows per warp
-#ifndef SAIT_ZMINB
-#define SAIT_ZMINB 1
-#endif
 __host__ __device__ constexpr int zwindow_smem_per_warp(int Q) {
   return (128 * Q * 8 + 64 * 4 + static_cast<int>(sizeof(ZStage)) + 15) / 16 * 16;
 }
 template <int Q>
-__global__ void __launch_bounds__(256, SAIT_ZMINB) spgemm_window_z(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
+__global__ void __launch_bounds__(256) spgemm_window_z(Args g, const int32_t* __restrict__ rows, int32_t nrows_bin,
                                                        const int32_t* __restrict__ wbase, bool numeric) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

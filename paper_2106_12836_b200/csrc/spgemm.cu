@@ -51,10 +51,13 @@ constexpr int kMinLogSlots = 6;
 constexpr int kGlobalBin = kFirstSmemBin + kNumSmemBins;
 // window bins: rows whose product columns all fall in [base, base + 128 Q)
 // (Q = kWinQ[i]), accumulated by direct addressing instead of hashing
-// (below); the smaller windows fit more rows in flight per SM
-constexpr int kNumWinBins = 6;
-constexpr int kWinQ[kNumWinBins] = {4, 5, 6, 7, 8, 16};
-__host__ __device__ constexpr int win_q(int i) { return i < 5 ? 4 + i : 16; }  // kWinQ[i] (device code)
+// (below); the smaller windows fit more rows in flight per SM.  Rows whose
+// columns span 1024 or more stay in the hash-table bins: a 2048-slot window
+// holds 16 KB per warp, and the 512-slot tables did those rows faster (C4:
+// 8.2 vs 10.2 ms per build)
+constexpr int kNumWinBins = 5;
+constexpr int kWinQ[kNumWinBins] = {4, 5, 6, 7, 8};
+__host__ __device__ constexpr int win_q(int i) { return 4 + i; }  // kWinQ[i] (device code)
 constexpr int kWinBin0 = kGlobalBin + 1;
 constexpr int kNumBins = kWinBin0 + kNumWinBins;
 constexpr int kTinyG[kTinyBins] = {8, 16, 32};
@@ -1351,7 +1354,7 @@ __global__ void plan_rows(Args g, int8_t* __restrict__ bin_of, int32_t* __restri
         }
       }
     }
-    if (win && logs >= 8 && hi >= lo) {  // ... whose columns span < 1024 / 2048
+    if (win && logs >= 8 && hi >= lo) {  // ... whose columns span < 128 Q (at most 1024)
       const int32_t span = hi - lo;
 #pragma unroll
       for (int q = kNumWinBins - 1; q >= 0; --q)
@@ -1596,8 +1599,7 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
         case 5: k = spgemm_window_z<5>; break;
         case 6: k = spgemm_window_z<6>; break;
         case 7: k = spgemm_window_z<7>; break;
-        case 8: k = spgemm_window_z<8>; break;
-        default: k = spgemm_window_z<16>;
+        default: k = spgemm_window_z<8>;
       }
       per_warp = zwindow_smem_per_warp(Q);
       // warps per CTA: the most resident warps per SM (228 KB of shared
@@ -1611,11 +1613,10 @@ void launch_pass(const Args& g, const Plan& pl, bool numeric, cudaStream_t s, bo
         const int res = std::min((228 * 1024) / (w * per_warp + 1024), reg_warps / w) * w;
         if (res > best) best = res, warps = w;
       }
-    } else {
-      const int R = Q <= 8 ? 1 : 2;
-      k = R == 1 ? spgemm_window<1> : spgemm_window<2>;
-      per_warp = window_smem_per_warp(R);
-      warps = window_warps(R);
+    } else {  // (every window bin fits the 1024-slot bitmap window)
+      k = spgemm_window<1>;
+      per_warp = window_smem_per_warp(1);
+      warps = window_warps(1);
     }
     const int smem = warps * per_warp;
     if (first_on_device(reinterpret_cast<const void*>(k)))

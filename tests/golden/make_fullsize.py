@@ -9,7 +9,8 @@ For BASELINE configs 3, 4 and 5 at their full sizes, the CPU side runs once:
   * two seeded pair applies (preconditioner.cpp:42-45) and, for C5, the
     block-8 apply (preconditioner.cpp:47-49);
   * the solvers of oracle/solvers.c: C3 GMRES(30) to 1e-8 from the seed-3
-    rhs, C5 block LOBPCG (8 pairs, tol 1e-6, seed 5).
+    rhs; C5 block LOBPCG (8 pairs, tol 1e-6, seed 5) for its first
+    C5_PREFIX iterations (the whole 570-iteration run would take ~9 h here).
 Only digests (SHA-256 of int64 row_ptr / col_idx and the fp64 value bits),
 sizes, step/iteration counts and the (short) residual histories are stored:
 tests/golden/fullsize.json and tests/golden/fullsize_hist.npz.  The -m gpu
@@ -33,6 +34,7 @@ sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
 
 OUT_JSON = os.path.join(HERE, "fullsize.json")
+C5_PREFIX = 12  # LOBPCG iterations pinned at config-5 size (see c5)
 OUT_NPZ = os.path.join(HERE, "fullsize_hist.npz")
 
 
@@ -152,14 +154,19 @@ def c5(rec, hist, cross):
     # digest of the column-major (n, 8) block = the 8 columns one after the other
     d["apply_block8"] = {"seeds": [5100 + j for j in range(8)], "digest": vec_digest(np.asfortranarray(Zb).T)}
     del Rb, Zb
+    # the restatement's LOBPCG costs ~1 min per iteration at this size on
+    # this host (570 iterations: ~9 h), so the fixture pins a prefix: the
+    # first C5_PREFIX iterations' residual-norm history, Ritz values and
+    # block, bitwise (the device's canonical mode is the same arithmetic)
+    prefix = C5_PREFIX
     t0 = time.perf_counter()
-    ev, X, its, res = O.lobpcg(A, ML, MU, 8, tol=1e-6, maxit=2000, seed=5)
+    ev, X, its, res = O.lobpcg(A, ML, MU, 8, tol=1e-6, maxit=prefix, seed=5)
     t = time.perf_counter() - t0
-    log(f"  oracle LOBPCG: {its} its, evals {ev}, final max res {res[-1].max():.3e}, {t:.0f} s")
-    d["lobpcg"] = {"nev": 8, "tol": 1e-6, "maxit": 2000, "seed": 5, "iterations": int(its),
-                   "evals": [float(v) for v in ev], "evals_digest": vec_digest(ev), "evecs_digest": vec_digest(X.T),
-                   "cpu_seconds": t, "cpu_threads": os.cpu_count()}
-    hist["c5_lobpcg_resnorms"] = res
+    log(f"  oracle LOBPCG prefix: {its} its, evals {ev}, max res {res[-1].max():.3e}, {t:.0f} s")
+    d["lobpcg_prefix"] = {"nev": 8, "tol": 1e-6, "maxit": prefix, "seed": 5, "iterations": int(its),
+                          "evals": [float(v) for v in ev], "evals_digest": vec_digest(ev),
+                          "evecs_digest": vec_digest(X.T), "cpu_seconds": t, "cpu_threads": os.cpu_count()}
+    hist["c5_lobpcg_prefix_resnorms"] = res
     rec["c5"] = d
     save(rec, hist)
 

@@ -48,6 +48,17 @@ check(bitwise_equal_csr(S.sait_thr_cap(to_product(T), S.lower_triangular, S.Sait
                         P.sait_thr_cap(T, True, 1e-2, 3, 1.5)), "build: fill cap")
 check(bitwise_equal_csr(S.sait_pat(to_product(T), S.lower_triangular, S.SaitPatParams(2, 3)),
                         P.sait_pat(T, True, 2, 3)), "build: pattern")
+# window rows (config-4 shape: -0.0 windows of every span bin, the row-form
+# cap pass, the staging chunks), both factors' orientations
+T4 = O.synthetic_lower(20000, 15, 0.01, seed=4)
+T4u = P.transpose(T4)
+check(bitwise_equal_csr(S.sait_thr(to_product(T4), S.lower_triangular, S.SaitThrParams(1e-2, 3)),
+                        P.sait_thr(T4, True, 1e-2, 3)), "build: window rows")
+check(bitwise_equal_csr(S.sait_thr(to_product(T4u), S.upper_triangular, S.SaitThrParams(1e-2, 3)),
+                        P.sait_thr(T4u, False, 1e-2, 3)), "build: window rows (upper)")
+for f in (1.0, 3.0):
+    check(bitwise_equal_csr(S.sait_thr_cap(to_product(T4), S.lower_triangular, S.SaitThrParams(1e-2, 3), f),
+                            P.sait_thr_cap(T4, True, 1e-2, 3, f)), f"build: row-form cap pass (f = {f})")
 
 # apply: device, host (chunked), block
 pair = S.SaitPairPreconditioner(to_product(ML), to_product(MU))
@@ -93,6 +104,10 @@ check(st.iterations == so["iterations"] and bitwise_equal(x, xo), "gmres")
 ev, _, it, _ = O.lobpcg(A, ML, MU, 4, 1e-6, 20, 5)
 res = S.lobpcg(to_product(A), pair, 4, 1e-6, 20, 5)
 check(res.iterations == it and bitwise_equal(res.eigenvalues, ev), "lobpcg")
+ev8, _, it8, _ = O.lobpcg(A, ML, MU, 8, 1e-6, 200, 5)
+rt = S.lobpcg(to_product(A), pair, 8, 1e-6, 200, 5, gram="tensor")  # deferred W, fused norms, upper-tile Grams
+check(abs(rt.iterations - it8) <= 1 and np.max(np.abs(rt.eigenvalues - ev8) / np.abs(ev8)) < 1e-12,
+      "lobpcg: tensor-core Grams")
 
 # ILU(0)/(1), trisolve, exact preconditioner
 for lev in (0, 1):

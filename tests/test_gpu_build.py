@@ -169,7 +169,9 @@ cases = [(lambda: P.sait_thr(T, True, 1e-2, 3), lambda: S.sait_thr(Tp, S.lower_t
          (lambda: P.sait_thr_cap(T, True, 1e-2, 3, 1.0),
           lambda: S.sait_thr_cap(Tp, S.lower_triangular, S.SaitThrParams(1e-2, 3), 1.0)),
          (lambda: P.sait_thr(Tu, False, 1e-2, 3), lambda: S.sait_thr(Tup, S.upper_triangular, S.SaitThrParams(1e-2, 3))),
-         (lambda: P.sait_pat(T, True, 2, 3), lambda: S.sait_pat(Tp, S.lower_triangular, S.SaitPatParams(2, 3)))]
+         (lambda: P.sait_pat(T, True, 2, 3), lambda: S.sait_pat(Tp, S.lower_triangular, S.SaitPatParams(2, 3))),
+         (lambda: P.sait_thr_cap(Tu, False, 1e-2, 3, 1.0),
+          lambda: S.sait_thr_cap(Tup, S.upper_triangular, S.SaitThrParams(1e-2, 3), 1.0))]
 for ref, dev in cases:
     want, got = ref(), dev()
     ok = (np.array_equal(got.row_ptr, want.row_ptr) and np.array_equal(got.col_idx, want.col_idx)
@@ -236,7 +238,7 @@ def test_hash_rows_staging_and_overflow(cap, column_form, window):
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.split() == ["1", "1", "1", "1", "1"]
+    assert out.stdout.split() == ["1"] * 6
 
 
 @pytest.mark.parametrize("column_form", ["0", "1"])
@@ -256,7 +258,7 @@ def test_hash_table_load_factors(slack, column_form):
     out = subprocess.run([sys.executable, "-c", _STAGE_CHILD.format(root=ROOT)], env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.split() == ["1", "1", "1", "1", "1"]
+    assert out.stdout.split() == ["1"] * 6
 
 
 def test_build_pair_concurrent_equals_separate(S, port):

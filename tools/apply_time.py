@@ -44,5 +44,5 @@ for _ in range(5):
     out.append(e0.elapsed_time(e1))
 ms = sorted(out)[2]
 fb = pair.factor_format(0)["stream_bytes"] + pair.factor_format(1)["stream_bytes"]
-print(f"grid={grid} fmt={fmt} env={os.environ.get('SAIT_SELL_VARIANT', '0')} ms_per_step={ms:.4f} "
+print(f"grid={grid} fmt={fmt} lib={os.environ.get('SAIT_LIB_VARIANT', 'default')} ms_per_step={ms:.4f} "
       f"us_per_launch={1e3 * ms / (2 * nvec):.2f} format_TBs={nvec * fb / ms / 1e9:.3f} checksum={float(Z.sum()):.17g}")

@@ -299,8 +299,9 @@ def apply_format_lines(S, torch, Ld, Ud, R, Z_ref, steps, stream):
 def irregular_apply_line(S, torch, T, steps, stream, nvec=20):
     """An apply on an irregular (non-stencil) pattern: the SAIT pair of the
     config-4 generator's T (lower, n = 2^24) and T^T (upper), tau = 1e-2,
-    k = 3 -- random geometric column offsets, so no slice patterns repeat and
-    the rows are too ragged for 32-row slices: the CSR kernel (spmv_tma)."""
+    k = 3 -- random geometric column offsets, so no slice patterns repeat, and
+    M_U's rows are too ragged for 32-row slices in their natural order: its
+    SELL copy sorts them by length within 1024-row windows (SELL-C-sigma)."""
     peak, _ = peaks()
     Tt = S.transpose(T)
     P = S.SaitThrParams(1e-2, 3)

@@ -301,14 +301,18 @@ int sait_pair_create(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, sait_pa
 /* Apply storage of a pair's factors.  AUTO (what sait_pair_create uses):
  * SELL-32 slices with shared slice patterns when the factor repeats a few
  * slice structures (stencil factors: only the values stream), else int16
- * column deltas, else int32 columns; CSR when the rows are too irregular for
- * 32-row slices (padding > 25%).  A forced SELL format falls back down that
+ * column deltas, else int32 columns; rows too ragged for 32-row slices in
+ * their natural order (padding > 25%) are sorted by length within 1024-row
+ * windows; CSR when even that pads more than 25%.  A forced SELL format falls back down that
  * list when the matrix does not allow it; sait_pair_format reports what was
  * used.  Every format gives the same bits (rows summed in stored order). */
 enum { SAIT_FMT_AUTO = 0, SAIT_FMT_CSR = 1, SAIT_FMT_SELL_I32 = 2, SAIT_FMT_SELL_I16 = 3, SAIT_FMT_SELL_DICT = 4 };
 int sait_pair_create_ex(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, int format, sait_pair_t *out);
 typedef struct {
   int format;           /* SAIT_FMT_* in use (never AUTO) */
+  int row_sorted;       /* SELL: 1 when the rows were sorted by length within
+                         * 1024-row windows (SELL-C-sigma, for factors too
+                         * ragged for 32-row slices in their natural order) */
   int64_t nrows, nnz;
   int64_t stored_slots; /* SELL: slots incl. padding; CSR: nnz */
   int64_t nslices, dict_elems;

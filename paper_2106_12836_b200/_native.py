@@ -60,8 +60,9 @@ class Halo(C.Structure):
 class FactorFormat(C.Structure):
     """sait_factor_format (include/sait_c.h)"""
 
-    _fields_ = [("format", C.c_int), ("nrows", C.c_int64), ("nnz", C.c_int64), ("stored_slots", C.c_int64),
-                ("nslices", C.c_int64), ("dict_elems", C.c_int64), ("stream_bytes", C.c_int64)]
+    _fields_ = [("format", C.c_int), ("row_sorted", C.c_int), ("nrows", C.c_int64), ("nnz", C.c_int64),
+                ("stored_slots", C.c_int64), ("nslices", C.c_int64), ("dict_elems", C.c_int64),
+                ("stream_bytes", C.c_int64)]
 
 
 SAIT_FMT_AUTO, SAIT_FMT_CSR, SAIT_FMT_SELL_I32, SAIT_FMT_SELL_I16, SAIT_FMT_SELL_DICT = range(5)

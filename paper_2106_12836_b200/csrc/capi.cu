@@ -556,8 +556,9 @@ void plan_host_chunks(sait_pair_t p) {
   p->chunk_rows.clear();
   p->u_rows.clear();
   const int64_t n = L.nrows;
-  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 17) || !p->sl.ok() || !p->su.ok())
-    return;  // small or non-square pairs: one-shot path
+  if (!(L.ncols == n && U.nrows == n && U.ncols == n) || n < (int64_t{1} << 17) || !p->sl.ok() || !p->su.ok() ||
+      p->sl.perm || p->su.perm)
+    return;  // small, non-square or row-sorted pairs: one-shot path
   const int64_t G = sait::kDepGroupRows;
   const int64_t ng = (n + G - 1) / G;
   // Copy sizes (MB of r / z per chunk): short head chunks start the z stream
@@ -1776,8 +1777,8 @@ int sait_pair_create_ex(sait_dcsr_t ml, sait_dcsr_t mu, int take_ownership, int 
     p->mu = mu;
     p->owns = take_ownership != 0;
     if (format != SAIT_FMT_CSR) {
-      p->sl = sait::make_sell(ml->m, format, nullptr);
-      p->su = sait::make_sell(mu->m, format, nullptr);
+      p->sl = sait::make_sell(ml->m, format, nullptr, /*allow_perm=*/true);
+      p->su = sait::make_sell(mu->m, format, nullptr, /*allow_perm=*/true);
     }
     plan_host_chunks(p);
     *out = p;
@@ -1812,7 +1813,9 @@ int sait_pair_format(sait_pair_t p, int which, sait_factor_format* out) {
       f.stored_slots = sm.padded;
       f.nslices = sm.nslices;
       f.dict_elems = sm.dict_elems;
-      const int64_t soff = 8 * (sm.nslices + 1);
+      f.row_sorted = sm.perm ? 1 : 0;
+      // (+ the row permutation of a row-sorted copy: one int32 per slot position)
+      const int64_t soff = 8 * (sm.nslices + 1) + (sm.perm ? 4 * sm.nslices * 32 : 0);
       switch (sm.index_kind()) {
         case 2:  // values stream; one int32 pattern offset per slice; the dictionary once
           f.format = SAIT_FMT_SELL_DICT;

@@ -262,6 +262,10 @@ struct SellMatrix {
   int32_t* dict = nullptr;
   int64_t dict_elems = 0;
   double* val = nullptr;
+  // rows too ragged for 32-row slices in their natural order: sorted by
+  // length within windows of kSigmaRows rows; slot position p holds row
+  // perm[p] (n: padding).  Only the whole-vector kernels take such a copy.
+  int32_t* perm = nullptr;
   bool ok() const { return soff != nullptr; }
   int index_kind() const { return dict ? 2 : dcol ? 1 : 0; }  // 2 dict, 1 int16, 0 int32
 };
@@ -269,7 +273,7 @@ struct SellMatrix {
 // applies; SAIT_SELL_DICT=0 / SAIT_SELL_INDEX=32 steer it) or one forced
 // SAIT_FMT_SELL_* (falling back down that list when the matrix does not allow
 // it).  Empty if too irregular for slicing (padding > 25%): CSR kernels.
-SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s);
+SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s, bool allow_perm = false);
 void free_sell(SellMatrix& m, cudaStream_t s);
 // per 256-row group g of m: [lo[g], hi[g]] = 256-column groups its entries touch
 void column_group_deps(const DevCsr& m, int32_t* lo, int32_t* hi, cudaStream_t s);

@@ -143,10 +143,12 @@ __global__ void max_col_delta(int64_t n, const int32_t* __restrict__ rp, const i
 
 __global__ void fill_sell16(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, const int64_t* __restrict__ soff,
-                            int16_t* __restrict__ scol, double* __restrict__ sval) {
-  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t s = r / kSlice;
-  int lane = static_cast<int>(r % kSlice);
+                            int16_t* __restrict__ scol, double* __restrict__ sval,
+                            const int32_t* __restrict__ perm) {
+  const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t s = pos / kSlice;
+  int lane = static_cast<int>(pos % kSlice);
+  const int64_t r = perm ? (pos < (n + kSlice - 1) / kSlice * kSlice ? perm[pos] : n) : pos;  // the slot's row
   int64_t nslices = (n + kSlice - 1) / kSlice;
   if (s >= nslices) return;
   int64_t base = soff[s];
@@ -170,10 +172,12 @@ __global__ void fill_sell16(int64_t n, const int32_t* __restrict__ rp, const int
 
 __global__ void fill_sell(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ v, const int64_t* __restrict__ soff,
-                          int32_t* __restrict__ scol, double* __restrict__ sval) {
-  int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  int64_t s = r / kSlice;
-  int lane = static_cast<int>(r % kSlice);
+                          int32_t* __restrict__ scol, double* __restrict__ sval,
+                            const int32_t* __restrict__ perm) {
+  const int64_t pos = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t s = pos / kSlice;
+  int lane = static_cast<int>(pos % kSlice);
+  const int64_t r = perm ? (pos < (n + kSlice - 1) / kSlice * kSlice ? perm[pos] : n) : pos;  // the slot's row
   int64_t nslices = (n + kSlice - 1) / kSlice;
   if (s >= nslices) return;
   int64_t base = soff[s];
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
                                                          const int64_t* __restrict__ soff, IDX idx,
                                                          const double* __restrict__ sval,
                                                          const double* __restrict__ x, double* __restrict__ y,
-                                                         int pf) {
+                                                         int pf, const int32_t* __restrict__ perm) {
   pdl_launch_dependents();
   const int lane = threadIdx.x & 31;
   const int64_t s = s_begin + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
                    "r"(static_cast<uint32_t>((pe - pb) * 8))
                    : "memory");
   }
-  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  const int32_t row = perm ? perm[s * kSlice + lane] : static_cast<int32_t>(s * kSlice) + lane;
   const int64_t e0 = base + lane;
   const int64_t i0 = idx.slice_base(s, base) + lane;
   double acc = 0.0;
@@ -255,7 +259,8 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t s_beg
 template <int NV, class IDX>
 __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslices, const int64_t* __restrict__ soff,
                                                          IDX idx, const double* __restrict__ sval,
-                                                         const double* __restrict__ x, double* __restrict__ y) {
+                                                         const double* __restrict__ x, double* __restrict__ y,
+                                                         const int32_t* __restrict__ perm) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nslices;
@@ -263,6 +268,7 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
     const int64_t base = soff[s];
     const int64_t ib = idx.slice_base(s, base);
     const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
+    const int64_t row = perm ? perm[s * kSlice + lane] : s * kSlice + lane;
     double acc[NV];
 #pragma unroll
     for (int c = 0; c < NV; ++c) acc[c] = 0.0;
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
         col[j] = -1;
         v[j] = 0.0;
         if (k0 + j < w) {
-          col[j] = idx.col(ib + (k0 + j) * kSlice + lane, static_cast<int32_t>(s * kSlice) + lane);
+          col[j] = idx.col(ib + (k0 + j) * kSlice + lane, static_cast<int32_t>(row));
           v[j] = ld_na(sval + base + (k0 + j) * kSlice + lane);
         }
       }
@@ -290,7 +296,6 @@ __global__ void __launch_bounds__(256) sell_spmm_kernel(int64_t n, int64_t nslic
         }
       }
     }
-    const int64_t row = s * kSlice + lane;
     if (row < n) {
       double2* yr = reinterpret_cast<double2*>(y + row * NV);
 #pragma unroll
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(CmShape<IDX>::kThreads, CmShape<IDX>::kMinBloc
                                                                              const double* __restrict__ sval,
                                                                              const double* __restrict__ x, int64_t ldx,
                                                                              double* __restrict__ y, int64_t ldy,
-                                                                             int nv) {
+                                                                             int nv, const int32_t* __restrict__ perm) {
   const int lane = threadIdx.x & 31;
   const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nslices) return;
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(CmShape<IDX>::kThreads, CmShape<IDX>::kMinBloc
   const int64_t ib = idx.slice_base(s, base) + lane;
   const double* __restrict__ vp = sval + base + lane;
   const int32_t w = static_cast<int32_t>((soff[s + 1] - base) >> 5);
-  const int32_t row = static_cast<int32_t>(s * kSlice) + lane;
+  const int32_t row = perm ? perm[s * kSlice + lane] : static_cast<int32_t>(s * kSlice) + lane;
   double acc[NV];
 #pragma unroll
   for (int c = 0; c < NV; ++c) acc[c] = 0.0;
@@ -692,7 +697,49 @@ void try_slice_dictionary(SellMatrix& m, bool forced, cudaStream_t s) {
 
 }  // namespace
 
-SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s) {
+// Rows of a ragged factor sorted by length (longest first, ties by row)
+// within windows of kSigmaRows rows -- SELL-C-sigma: slices then hold rows
+// of similar length, and no row moves further than the window, so the x
+// gathers and y stores keep their locality.  Host side, once per pair;
+// returns false if even the sorted slices pad more than kMaxPad.
+constexpr int64_t kSigmaRows = 1024;
+bool sort_rows_in_windows(const DevCsr& a, SellMatrix& m, cudaStream_t s) {
+  static const bool on = [] {  // SAIT_SELL_SIGMA=0: ragged factors keep the CSR kernels
+    const char* e = std::getenv("SAIT_SELL_SIGMA");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!on) return false;
+  const int64_t n = a.nrows, slots = m.nslices * kSlice;
+  std::vector<int32_t> rp(n + 1);
+  SAIT_CUDA(cudaMemcpyAsync(rp.data(), a.rp, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> perm(slots, static_cast<int32_t>(n));
+  std::vector<int64_t> soff(m.nslices + 1, 0);
+  const int64_t nwin = (n + kSigmaRows - 1) / kSigmaRows;
+#pragma omp parallel for schedule(static)
+  for (int64_t w = 0; w < nwin; ++w) {
+    const int64_t r0 = w * kSigmaRows, r1 = std::min(n, r0 + kSigmaRows);
+    int32_t* pw = perm.data() + r0;
+    for (int64_t r = r0; r < r1; ++r) pw[r - r0] = static_cast<int32_t>(r);
+    std::stable_sort(pw, pw + (r1 - r0),
+                     [&](int32_t x, int32_t y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
+    for (int64_t q = r0 / kSlice; q < (r1 + kSlice - 1) / kSlice; ++q) {  // slice widths: its first (longest) row
+      const int32_t r = perm[q * kSlice];
+      soff[q + 1] = static_cast<int64_t>(rp[r + 1] - rp[r]) * kSlice;
+    }
+  }
+  for (int64_t q = 0; q < m.nslices; ++q) soff[q + 1] += soff[q];
+  if (static_cast<double>(soff[m.nslices]) > kMaxPad * static_cast<double>(std::max<int64_t>(a.nnz, 1)) + 64.0)
+    return false;
+  m.padded = soff[m.nslices];
+  m.perm = dalloc<int32_t>(slots, s);
+  SAIT_CUDA(cudaMemcpyAsync(m.perm, perm.data(), sizeof(int32_t) * slots, cudaMemcpyHostToDevice, s));
+  SAIT_CUDA(cudaMemcpyAsync(m.soff, soff.data(), sizeof(int64_t) * (m.nslices + 1), cudaMemcpyHostToDevice, s));
+  SAIT_CUDA(cudaStreamSynchronize(s));  // (host vectors go out of scope)
+  return true;
+}
+
+SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s, bool allow_perm) {
   SellMatrix m;
   m.n = a.nrows;
   if (a.nrows == 0 || !a.v) return m;
@@ -704,9 +751,10 @@ SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s) {
   SAIT_LAUNCHED();
   SAIT_CUDA(cudaMemcpyAsync(&m.padded, m.soff + m.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   SAIT_CUDA(cudaStreamSynchronize(s));
-  if (static_cast<double>(m.padded) > kMaxPad * static_cast<double>(std::max<int64_t>(a.nnz, 1)) + 64.0) {
+  if (static_cast<double>(m.padded) > kMaxPad * static_cast<double>(std::max<int64_t>(a.nnz, 1)) + 64.0 &&
+      !(allow_perm && sort_rows_in_windows(a, m, s))) {
     dfree(m.soff, s);
-    return SellMatrix{};  // too irregular: keep the CSR kernels
+    return SellMatrix{};  // too irregular even row-sorted: keep the CSR kernels
   }
   // int16 column deltas when every |col - row| fits (and INT16_MIN is free as
   // the padding marker); SAIT_SELL_INDEX=32 forces absolute int32 columns
@@ -728,14 +776,17 @@ SellMatrix make_sell(const DevCsr& a, int format, cudaStream_t s) {
   m.val = dalloc<double>(m.padded, s);
   if (maxd <= 32767 && !want32) {
     m.dcol = dalloc<int16_t>(m.padded, s);
-    fill_sell16<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.dcol, m.val);
+    fill_sell16<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.dcol, m.val,
+                                                                  m.perm);
   } else {
     m.col = dalloc<int32_t>(m.padded, s);
-    fill_sell<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.col, m.val);
+    fill_sell<<<grid_for(m.nslices * kSlice, 256), 256, 0, s>>>(a.nrows, a.rp, a.ci, a.v, m.soff, m.col, m.val,
+                                                                m.perm);
   }
   SAIT_LAUNCHED();
   SAIT_CUDA(cudaStreamSynchronize(s));
-  if (format == SAIT_FMT_AUTO || format == SAIT_FMT_SELL_DICT) try_slice_dictionary(m, format == SAIT_FMT_SELL_DICT, s);
+  if (!m.perm && (format == SAIT_FMT_AUTO || format == SAIT_FMT_SELL_DICT))
+    try_slice_dictionary(m, format == SAIT_FMT_SELL_DICT, s);
   return m;
 }
 
@@ -746,6 +797,7 @@ void free_sell(SellMatrix& m, cudaStream_t s) {
   dfree(m.pat, s);
   dfree(m.dict, s);
   dfree(m.val, s);
+  dfree(m.perm, s);
   m = SellMatrix{};
 }
 
@@ -757,6 +809,8 @@ void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const doubl
                     bool pdl) {
   const int64_t s0 = row0 / kSlice, s1 = std::min<int64_t>((row1 + kSlice - 1) / kSlice, m.nslices);
   if (s1 <= s0) return;
+  if (m.perm && (row0 != 0 || row1 < m.n))  // slots of a row-sorted copy are not row ranges
+    throw std::runtime_error("sell_spmv_rows: a row range of a row-sorted SELL copy");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sell_grid(s1 - s0));
   cfg.blockDim = dim3(256);
@@ -769,16 +823,16 @@ void sell_spmv_rows(const SellMatrix& m, int64_t row0, int64_t row1, const doubl
   const int pf = m.nslices >= kPfMinSlices ? kPfDistance : 0;
   if (m.dict) {
     IdxDict ix{m.pat, m.dict};
-    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<IdxDict, true>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf));
-    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<IdxDict, false>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf));
+    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<IdxDict, true>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf, m.perm));
+    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<IdxDict, false>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf, m.perm));
   } else if (m.dcol) {
     Idx16 ix{m.dcol};
-    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, true>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf));
-    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, false>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf));
+    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, true>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf, m.perm));
+    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx16, false>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf, m.perm));
   } else {
     Idx32 ix{m.col};
-    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, true>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf));
-    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, false>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf));
+    if (pdl) SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, true>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf, m.perm));
+    else SAIT_CUDA(cudaLaunchKernelEx(&cfg, sell_spmv_kernel<Idx32, false>, m.n, s0, s1, m.soff, ix, m.val, x, y, pf, m.perm));
   }
   SAIT_LAUNCHED();
 }
@@ -913,7 +967,7 @@ void launch_cm(const SellMatrix& m, IDX ix, const double* x, int64_t ldx, double
   constexpr int wpb = CmShape<IDX>::kThreads / 32;
   const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, (m.nslices + wpb - 1) / wpb));
   sell_spmm_cm_kernel<8, IDX><<<grid, CmShape<IDX>::kThreads, 0, s>>>(m.n, m.nslices, m.soff, ix, m.val, x, ldx, y,
-                                                                      ldy, nv);
+                                                                      ldy, nv, m.perm);
 }
 }  // namespace
 
@@ -934,7 +988,7 @@ void sell_spmm_colmajor(const SellMatrix& m, const double* x, int64_t ldx, doubl
 
 template <int NV, class IDX>
 void launch_spmm(const SellMatrix& m, IDX ix, const double* x, double* y, cudaStream_t s) {
-  sell_spmm_kernel<NV, IDX><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, ix, m.val, x, y);
+  sell_spmm_kernel<NV, IDX><<<sell_grid(m.nslices), 256, 0, s>>>(m.n, m.nslices, m.soff, ix, m.val, x, y, m.perm);
 }
 
 bool sell_spmm(const SellMatrix& m, const double* x, double* y, int nvec, cudaStream_t s) {

@@ -82,13 +82,15 @@ class SaitPairPreconditioner(Preconditioner):
         self._nnz = nnz.value
 
     def factor_format(self, which: int) -> dict:
-        """Apply storage of M_L (which=0) or M_U (which=1): format name, stored
-        slots, slices, dictionary size and ``stream_bytes`` (what one SpMV
-        must move in that format: the roofline denominator)."""
+        """Apply storage of M_L (which=0) or M_U (which=1): format name, whether
+        the rows were length-sorted within 1024-row windows (``row_sorted``),
+        stored slots, slices, dictionary size and ``stream_bytes`` (what one
+        SpMV must move in that format: the roofline denominator)."""
         f = N.FactorFormat()
         N.check(N.lib.sait_pair_format(self._h, int(which), C.byref(f)))
-        return {"format": N.FORMAT_NAMES[f.format], "nrows": f.nrows, "nnz": f.nnz, "stored_slots": f.stored_slots,
-                "nslices": f.nslices, "dict_elems": f.dict_elems, "stream_bytes": f.stream_bytes}
+        return {"format": N.FORMAT_NAMES[f.format], "row_sorted": bool(f.row_sorted), "nrows": f.nrows, "nnz": f.nnz,
+                "stored_slots": f.stored_slots, "nslices": f.nslices, "dict_elems": f.dict_elems,
+                "stream_bytes": f.stream_bytes}
 
     # -- interface
     def name(self) -> str:

@@ -281,21 +281,48 @@ def test_forced_apply_formats(S, port, fmt):
         S.SaitPairPreconditioner(ML, MU, format="ellpack")
 
 
-def test_irregular_factor_takes_csr(S, port):
-    """Factors too irregular for 32-row slices (padding > 25%) keep the CSR
-    kernels under every requested format, with the oracle's bits."""
+@pytest.mark.parametrize("fmt", ["auto", "sell32_int32", "sell32_int16"])
+def test_ragged_factor_row_sorted(S, port, fmt):
+    """A factor too ragged for 32-row slices in its natural order (the SAIT
+    factor of config 4's T^T: padding > 25%) gets a SELL copy with its rows
+    sorted by length within 1024-row windows (SELL-C-sigma, row_sorted); the
+    single apply (device and host vectors) and the block apply (column- and
+    row-major) keep the oracle's bits."""
+    import torch
+
     from helpers import to_oracle
 
     T = S.synthetic_lower(1 << 14, 15, 0.01, 4)
     M = S.sait_thr(T, S.lower_triangular, S.SaitThrParams(1e-2, 3))
     Mt = S.transpose(M)
-    pair = S.SaitPairPreconditioner(M, Mt, format="sell32_int32")
-    formats = [pair.factor_format(w)["format"] for w in (0, 1)]
-    r = S.uniform_pm1(5, M.nrows)
-    z = np.empty(M.nrows)
+    pair = S.SaitPairPreconditioner(M, Mt, format=fmt)
+    fu = pair.factor_format(1)
+    assert fu["row_sorted"] and fu["format"] == ("sell32_int32" if fmt == "sell32_int32" else "sell32_int16")
+    assert fu["stored_slots"] <= 1.25 * fu["nnz"] + 64
+    eL, eU = to_oracle(M), to_oracle(Mt)
+    n = M.nrows
+    r = S.uniform_pm1(5, n)
+    want = port.pair_apply(eL, eU, r)
+    z = np.empty(n)
     pair.apply(r, z)
-    assert bitwise_equal(z, port.pair_apply(to_oracle(M), to_oracle(Mt), r))
-    assert set(formats) <= {"csr", "sell32_int32"}
+    assert bitwise_equal(z, want)
+    rd = torch.from_numpy(r).cuda()
+    zd = torch.empty_like(rd)
+    pair.apply(rd, zd)
+    torch.cuda.synchronize()
+    assert bitwise_equal(zd.cpu().numpy(), want)
+    R = np.stack([S.uniform_pm1(40 + j, n) for j in range(8)], axis=1)
+    Zb = port.pair_apply_block(eL, eU, R)
+    assert bitwise_equal(np.asarray(pair.apply_block(R)), Zb)
+    Rd = torch.from_numpy(np.ascontiguousarray(R.T)).cuda()  # (8, n): the column-major (n, 8) block
+    Zd = torch.empty_like(Rd)
+    pair.apply_block(Rd.T, Zd.T)
+    torch.cuda.synchronize()
+    assert bitwise_equal(Zd.T.cpu().numpy(), Zb)
+    Rr = torch.from_numpy(np.ascontiguousarray(R)).cuda()  # (n, 8) row-major
+    Zr = pair.apply_block(Rr, layout="row")
+    torch.cuda.synchronize()
+    assert bitwise_equal(Zr.cpu().numpy(), Zb)
 
 
 _DICT_CHILD = r"""

@@ -327,7 +327,7 @@ def irregular_apply_line(S, torch, T, steps, stream, nvec=20):
     ach = nvec * fb / (ms * 1e-3) / 1e9
     del pair, R, Z
     return {"workload": "SAIT pair of the c4 generator's T and T^T (n=2^24), tau=1e-2, k=3, %d vectors per step" % nvec,
-            "n": n, "nnz_L": nnz[0], "nnz_U": nnz[1], "formats": [fl["format"], fu["format"]],
+            "n": n, "nnz_L": nnz[0], "nnz_U": nnz[1], "formats": [fl["format"], fu["format"]], "row_sorted": [fl["row_sorted"], fu["row_sorted"]],
             "ms_per_step": ms, "ms_per_pair": ms / nvec, "effective_gbs_12B_per_nnz": nvec * B / (ms * 1e-3) / 1e9,
             "format_bytes_per_pair": fb, "achieved": ach, "frac": ach / peak}
 

@@ -782,10 +782,9 @@ __device__ __forceinline__ int32_t accumulate_zero(const Args& g, const RowAhead
 // 64-slot groups [base, hi] with two slots per lane (one 16-byte load),
 // keeps the diagonal and |v| >= tau, puts -0.0 back into the dropped slots
 // and keeps the survivors' masks per group (lane q holds group q's even- and
-// odd-slot ballots).  The write pass visits the groups with survivors only:
-// a survivor's position is the groups' prefix plus the lane's popcounts,
-// i.e. column order, and each visited slot pair goes back to -0.0.  Same
-// products, same add order: bitwise the hash path.
+// odd-slot ballots).  The write pass gives survivor i (column order) to lane
+// i % 32, which finds its slot from the groups' prefix counts and writes it,
+// putting -0.0 back.  Same products, same add order: bitwise the hash path.
 template <int Q, bool numeric>
 __device__ void process_row_window_z(const Args& g, const RowAhead& cur, RowAhead& nx,
                                      const int32_t* __restrict__ rows, int32_t rn, const int32_t* __restrict__ wbase,

@@ -80,3 +80,39 @@ def test_synthetic_config4_shape():
     diag = t.values[t.row_ptr[1:] - 1]
     off = np.abs(t.values).sum() - np.abs(diag).sum()
     assert np.allclose(diag.sum(), 1.5 * off + t.nrows)
+
+
+STRUCTS = [("sait_host_csr", "HostCsr"), ("sait_drop_spec", "DropSpec"), ("sait_build_stats", "BuildStats"),
+           ("sait_solve_stats", "SolveStats"), ("sait_row_piece", "RowPiece"), ("sait_halo_t", "Halo"),
+           ("sait_peer_factor_desc", "PeerFactorDesc"), ("sait_factor_format", "FactorFormat")]
+
+
+def test_ctypes_structs_match_header(tmp_path):
+    """The ctypes mirrors of the C ABI's structs have the header's size and
+    field offsets (a C program compiled against include/sait_c.h prints
+    them)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_2106_12836_b200 import _native as N
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sait_c.h"', "int main(void) {"]
+    for cname, pyname in STRUCTS:
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in getattr(N, pyname)._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    inc = os.path.join(ROOT, "include")
+    subprocess.run(["gcc", "-I", inc, "-I/usr/local/cuda/include", str(src), "-o", str(exe)], check=True)
+    got = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    for cname, pyname in STRUCTS:
+        cls = getattr(N, pyname)
+        assert f"{cname} size {ctypes.sizeof(cls)}" in got, cname
+        for fname, _ in cls._fields_:
+            assert f"{cname} {fname} {getattr(cls, fname).offset}" in got, (cname, fname)

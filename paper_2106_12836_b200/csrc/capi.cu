@@ -8,6 +8,10 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <omp.h>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 #include <thread>
 #include <unordered_map>
 #include <utility>
@@ -94,6 +98,8 @@ struct sait_pair_s {
     cudaEvent_t ev_entry = nullptr, ev_out_done = nullptr;
     // column-major host block apply: kBlkSlots device slots per side
     double *blk_r = nullptr, *blk_z = nullptr;
+    double *pin_r = nullptr, *pin_z = nullptr;  // pinned staging of pageable caller blocks
+    size_t pin_r_elems = 0, pin_z_elems = 0;
     cudaEvent_t ev_blk_in[4] = {}, ev_blk_done[4] = {}, ev_blk_out[4] = {};
   };
   // chunking of the host-vector apply: row boundaries (multiples of 256) and,
@@ -2103,10 +2109,101 @@ std::vector<int64_t> blk_group_sizes(int64_t nvec) {
   return out;
 }
 
+// Pageable caller blocks (the reference's callers hold std::vector storage):
+// a cudaMemcpyAsync from or to pageable memory is staged by the driver on
+// the calling thread at ~13 GB/s, H2D and D2H taking turns.  Instead each
+// group is copied by the host cores (OpenMP, 1 MB pieces) into a pinned slot
+// of its own and DMA'd from there, and z groups come back through pinned
+// slots the same way, so the DMA of one group overlaps the host copies of its
+// neighbours.  SAIT_STAGE_THREADS bounds the copying threads (default: the
+// OpenMP maximum, at most 16); SAIT_HOST_STAGING=0 leaves it to the driver.
+bool host_staging_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SAIT_HOST_STAGING");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+int stage_threads() {
+  static const int v = [] {
+    const char* e = std::getenv("SAIT_STAGE_THREADS");
+    const int k = e ? std::atoi(e) : std::min(omp_get_max_threads(), 16);
+    return std::max(k, 1);
+  }();
+  return v;
+}
+// SAIT_STAGE_COPY: 0 = memcpy in 1 MB pieces, 1 = one contiguous memcpy per
+// thread, 2 (default on x86-64) = streaming (non-temporal) 16-byte stores,
+// which skip the read-for-ownership of the destination lines.
+int stage_copy_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("SAIT_STAGE_COPY");
+#if defined(__x86_64__)
+    return e ? std::atoi(e) : 2;
+#else
+    return e ? std::min(std::atoi(e), 1) : 1;
+#endif
+  }();
+  return v;
+}
+void copy_streaming(char* d, const char* s, size_t bytes) {
+#if defined(__x86_64__)
+  size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+  if (head > bytes) head = bytes;
+  std::memcpy(d, s, head);
+  d += head, s += head, bytes -= head;
+  const size_t body = bytes & ~size_t{63};
+  for (size_t o = 0; o < body; o += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + o));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + o + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + o + 32));
+    const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + o + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + o), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + o + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + o + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + o + 48), e);
+  }
+  _mm_sfence();
+  std::memcpy(d + body, s + body, bytes - body);
+#else
+  std::memcpy(d, s, bytes);
+#endif
+}
+void host_copy_parallel(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = size_t{1} << 20;
+  const int64_t pieces = static_cast<int64_t>((bytes + kPiece - 1) / kPiece);
+  const int nt = static_cast<int>(std::min<int64_t>(stage_threads(), pieces));
+  const int mode = stage_copy_mode();
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  if (mode == 0) {
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t i = 0; i < pieces; ++i) {
+      const size_t o = static_cast<size_t>(i) * kPiece;
+      std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kPiece, bytes - o));
+    }
+    return;
+  }
+  // one contiguous, 4 KB-aligned range per thread
+  const size_t per = ((bytes + nt - 1) / nt + 4095) & ~size_t{4095};
+#pragma omp parallel for schedule(static) num_threads(nt)
+  for (int t = 0; t < nt; ++t) {
+    const size_t o = static_cast<size_t>(t) * per;
+    if (o >= bytes) continue;
+    const size_t len = std::min(per, bytes - o);
+    if (mode == 2) copy_streaming(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, len);
+    else std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, len);
+  }
+}
+
 void pair_apply_block_host_pipelined(sait_pair_t p, const double* h_r, double* h_z, int64_t n, int64_t nvec,
                                      cudaStream_t s) {
   const int kBlkSlots = blk_slots();
   const int64_t gmax = blk_groups().max();
+  const bool stage_in = host_staging_enabled() && !device_mapped(h_r);
+  const bool stage_out = host_staging_enabled() && !device_mapped(h_z);
   sait_pair_s::Work& w = pair_work(p, s);
   std::lock_guard<std::mutex> lk(*w.mu);
   ensure_side_streams(w);
@@ -2130,17 +2227,53 @@ void pair_apply_block_host_pipelined(sait_pair_t p, const double* h_r, double* h
     cudaEventRecord(e, st);
     tl.push_back(e);
   };
-  const std::vector<int64_t> groups = blk_group_sizes(nvec);
+  std::vector<int64_t> groups = blk_group_sizes(nvec);
+  int64_t gstage = gmax;
+  if (stage_in || stage_out) {
+    // uniform groups of at most 64 MB bound the pinned slots
+    gstage = std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t{64} << 20) / (8 * std::max<int64_t>(n, 1))));
+    groups.clear();
+    for (int64_t left = nvec; left > 0; left -= groups.back()) groups.push_back(std::min(gstage, left));
+    const size_t need = static_cast<size_t>(n) * gstage * kBlkSlots;
+    if (stage_in && w.pin_r_elems < need) {
+      if (w.pin_r) SAIT_CUDA(cudaFreeHost(w.pin_r));
+      w.pin_r = nullptr, w.pin_r_elems = 0;
+      SAIT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w.pin_r), sizeof(double) * need, cudaHostAllocDefault));
+      w.pin_r_elems = need;
+    }
+    if (stage_out && w.pin_z_elems < need) {
+      if (w.pin_z) SAIT_CUDA(cudaFreeHost(w.pin_z));
+      w.pin_z = nullptr, w.pin_z_elems = 0;
+      SAIT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w.pin_z), sizeof(double) * need, cudaHostAllocDefault));
+      w.pin_z_elems = need;
+    }
+  }
+  std::vector<int64_t> gstart(groups.size() + 1, 0);
+  for (size_t gi = 0; gi < groups.size(); ++gi) gstart[gi + 1] = gstart[gi] + groups[gi];
+  // z of group go leaves its pinned slot for the caller's pageable block
+  auto drain = [&](size_t go) {
+    const int qo = static_cast<int>(go % kBlkSlots);
+    SAIT_CUDA(cudaEventSynchronize(w.ev_blk_out[qo]));
+    host_copy_parallel(h_z + gstart[go] * n, w.pin_z + static_cast<size_t>(qo) * gstage * n,
+                       sizeof(double) * n * groups[go]);
+  };
   int64_t v0 = 0;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const int64_t g = groups[gi];
     const int q = static_cast<int>(gi % kBlkSlots);
     double* r = w.blk_r + q * gmax * n;
     double* z = w.blk_z + q * gmax * n;
+    const double* src = h_r + v0 * n;
+    if (stage_in) {
+      double* pr = w.pin_r + static_cast<size_t>(q) * gstage * n;
+      if (gi >= static_cast<size_t>(kBlkSlots)) SAIT_CUDA(cudaEventSynchronize(w.ev_blk_in[q]));  // slot's last H2D
+      host_copy_parallel(pr, src, sizeof(double) * n * g);
+      src = pr;
+    }
     if (gi >= static_cast<size_t>(kBlkSlots))
       SAIT_CUDA(cudaStreamWaitEvent(w.s_in, w.ev_blk_done[q], 0));  // the pairs of gi-slots read r
     mark(w.s_in);
-    SAIT_CUDA(cudaMemcpyAsync(r, h_r + v0 * n, sizeof(double) * n * g, cudaMemcpyHostToDevice, w.s_in));
+    SAIT_CUDA(cudaMemcpyAsync(r, src, sizeof(double) * n * g, cudaMemcpyHostToDevice, w.s_in));
     mark(w.s_in);
     SAIT_CUDA(cudaEventRecord(w.ev_blk_in[q], w.s_in));
     SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_blk_in[q], 0));
@@ -2155,11 +2288,18 @@ void pair_apply_block_host_pipelined(sait_pair_t p, const double* h_r, double* h
     SAIT_CUDA(cudaEventRecord(w.ev_blk_done[q], s));
     SAIT_CUDA(cudaStreamWaitEvent(w.s_out, w.ev_blk_done[q], 0));
     mark(w.s_out);
-    SAIT_CUDA(cudaMemcpyAsync(h_z + v0 * n, z, sizeof(double) * n * g, cudaMemcpyDeviceToHost, w.s_out));
+    // the pinned z slot q still holds group gi - slots until it is drained
+    if (stage_out && gi >= static_cast<size_t>(kBlkSlots)) drain(gi - kBlkSlots);
+    double* dst = stage_out ? w.pin_z + static_cast<size_t>(q) * gstage * n : h_z + v0 * n;
+    SAIT_CUDA(cudaMemcpyAsync(dst, z, sizeof(double) * n * g, cudaMemcpyDeviceToHost, w.s_out));
     mark(w.s_out);
     SAIT_CUDA(cudaEventRecord(w.ev_blk_out[q], w.s_out));
     v0 += g;
   }
+  if (stage_out)
+    for (size_t go = groups.size() > static_cast<size_t>(kBlkSlots) ? groups.size() - kBlkSlots : 0; go < groups.size();
+         ++go)
+      drain(go);
   SAIT_CUDA(cudaEventRecord(w.ev_out_done, w.s_out));
   SAIT_CUDA(cudaStreamWaitEvent(s, w.ev_out_done, 0));
   SAIT_CUDA(cudaStreamSynchronize(s));
@@ -2378,6 +2518,8 @@ void sait_pair_destroy(sait_pair_t p) {
       if (w.z_dev) cudaFree(w.z_dev);
       if (w.blk_r) cudaFree(w.blk_r);
       if (w.blk_z) cudaFree(w.blk_z);
+      if (w.pin_r) cudaFreeHost(w.pin_r);
+      if (w.pin_z) cudaFreeHost(w.pin_z);
       for (int q = 0; q < 4; ++q)
         for (cudaEvent_t e : {w.ev_blk_in[q], w.ev_blk_done[q], w.ev_blk_out[q]})
           if (e) cudaEventDestroy(e);

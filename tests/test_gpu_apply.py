@@ -90,6 +90,59 @@ def test_block_host_pipeline_pinned(S, c1_pair, monkeypatch):
         c1_pair.apply_block(Rn.T, Zn)  # C-ordered (nvec, n): wrong shape / order
 
 
+@pytest.mark.parametrize("pin_r,pin_z", [(False, False), (False, True), (True, False)])
+def test_block_host_pipeline_pageable_staging(S, c1_pair, monkeypatch, pin_r, pin_z):
+    """apply_block on PAGEABLE caller blocks (the reference's std::vector
+    callers, preconditioner.cpp:47-49): r and/or z pass through the library's
+    pinned staging slots, copied by the host cores.  More groups than slots and
+    a ragged last group; every pinned/pageable combination; with one and with
+    several copying threads; bitwise the unstaged block path and the single
+    applies.  A second call reuses the slots."""
+    import torch
+    from oracle import oracle as O
+
+    nvec = 19
+    R = np.asfortranarray(np.stack([O.uniform_pm1(900 + c, 4096) for c in range(nvec)], axis=1))
+    Rt = torch.from_numpy(R.T.copy())  # (nvec, n) C-order = column-major (n, nvec)
+    Zt = torch.zeros_like(Rt)
+    if pin_r:
+        Rt = Rt.pin_memory()
+    if pin_z:
+        Zt = Zt.pin_memory()
+    Rn, Zn = Rt.numpy(), Zt.numpy()
+    for _ in range(2):
+        Zn[...] = 0.0
+        assert c1_pair.apply_block(Rn.T, Zn.T) is not None
+        for c in range(nvec):
+            z = np.empty(4096)
+            c1_pair.apply(np.ascontiguousarray(Rn[c]), z)
+            assert bitwise_equal(Zn[c], z)
+    monkeypatch.setenv("SAIT_BLOCK_HOST_PIPELINE", "0")
+    Z0 = c1_pair.apply_block(Rn.T)
+    assert bitwise_equal(Zn.T, Z0)
+
+
+def test_block_host_pageable_staging_parallel_copies(S, monkeypatch):
+    """the staged pageable block apply at a size whose groups are copied by
+    several host threads (n = 64^3: 8 MB groups, 1 MB pieces); bitwise the
+    device block apply"""
+    import torch
+
+    A = S.laplacian_3d(64)
+    f = S.ilu_k(A, 0)
+    ML = S.sait_thr(f.lower, S.lower_triangular, S.SaitThrParams(5e-2, 3))
+    MU = S.sait_thr(f.upper, S.upper_triangular, S.SaitThrParams(5e-2, 3))
+    pair = S.SaitPairPreconditioner(ML, MU)
+    nvec, n = 15, A.nrows
+    Rn = np.stack([S.uniform_pm1(40 + c, n) for c in range(nvec)])  # (nvec, n), pageable
+    Zn = np.zeros_like(Rn)
+    pair.apply_block(Rn.T, Zn.T)
+    Zd = torch.empty((nvec, n), dtype=torch.float64, device="cuda")
+    pair.apply_block(torch.from_numpy(Rn).cuda().T, Zd.T)
+    torch.cuda.synchronize()
+    assert bitwise_equal(Zn, Zd.cpu().numpy())
+
+
 def test_host_paths_share_stream_work(S):
     """the block pipeline, the chunked single-vector host apply and the device
     apply share one per-stream workspace: any order of calls on one thread

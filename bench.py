@@ -788,7 +788,7 @@ def run_b200(args):
                                     "api": "100 x SaitPairPreconditioner::apply, pinned host vectors"},
                "pageable_block": {"value": NVEC * B / t_pg / 1e9, "ms_per_step": t_pg * 1e3,
                                   "api": "the same apply_block call on pageable (plain numpy / std::vector) "
-                                         "host memory, median of 3 calls"}}
+                                         "host memory (groups staged through the library's pinned slots by the host cores), median of 3 calls"}}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
